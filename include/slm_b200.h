@@ -1,0 +1,174 @@
+/*
+ * slm_b200.h — C ABI of the B200-native LM/PCG hot path (libslm_b200.so).
+ *
+ * The entry points are what a binding of the reference's C++ API would call:
+ * each one names the reference function/method it replaces (paths relative
+ * to /root/reference/proj).  Conventions:
+ *   - every function returns 0 on success, else an error code
+ *     (SLM_E_INVALID <- std::invalid_argument, SLM_E_DOMAIN <- std::domain_error,
+ *      SLM_E_RUNTIME <- std::runtime_error, SLM_E_CUDA on a CUDA/NCCL failure);
+ *     slm_last_error() returns the thread's last message.  No exceptions cross
+ *     the ABI.
+ *   - host buffers are caller-owned; ParamVectors are the reference's AoS
+ *     14-stride layout (types.hpp:11-20) in f64; residual vectors are ordered
+ *     (view, sample, channel) (jacobian.hpp:13-15).
+ *   - "_dev" variants take device pointers to f32 SoA [14][Gp] vectors
+ *     (slm_scene_count returns Gp) and never synchronise the host.
+ *   - a context owns one CUDA stream; calls on one context are not
+ *     thread-safe (reference: SPEC.md:370).
+ * There is no CPU fallback: without a CUDA device every compute call fails
+ * with SLM_E_CUDA.
+ */
+#ifndef SLM_B200_H
+#define SLM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "slm_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SLM_OK = 0, SLM_E_INVALID = 1, SLM_E_DOMAIN = 2, SLM_E_RUNTIME = 3, SLM_E_CUDA = 4 };
+
+typedef struct slm_context slm_context;   /* device + stream + optional NCCL comm */
+typedef struct slm_scene slm_scene;       /* device-resident GaussianSet (types.hpp:31-57) */
+typedef struct slm_jacobian slm_jacobian; /* autodiff::SampledJacobian (jacobian.hpp:25-76) */
+typedef struct slm_train slm_train;       /* solver::TrainData (lm.hpp:53-60) */
+typedef struct slm_rng slm_rng;           /* std::mt19937_64 shared by init/batch/sampler */
+typedef struct slm_plan_h slm_plan_h;     /* sampling::SamplePlan owned by the library */
+
+const char* slm_last_error(void);
+int slm_version(void);
+int slm_device_count(int* out);
+
+/* ---- context (no reference counterpart: the reference is one process, host threads only) */
+int slm_context_create(int device, slm_context** out);
+int slm_context_destroy(slm_context* ctx);
+int slm_context_synchronize(slm_context* ctx);
+/* Multi-GPU view sharding: rank 0 creates the id, every rank calls init_comm. */
+int slm_nccl_unique_id(uint8_t out[128]);
+int slm_context_init_comm(slm_context* ctx, const uint8_t id[128], int rank, int world);
+int slm_context_rank(slm_context* ctx, int* rank, int* world);
+/* Per-stage CUDA-event timings of the last lm_step / gn_apply (ms). */
+int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n);
+
+/* ---- RNG: std::mt19937_64 (io/run.cpp:126-127) */
+int slm_rng_create(uint64_t seed, slm_rng** out);
+void slm_rng_destroy(slm_rng* rng);
+uint64_t slm_rng_next(slm_rng* rng);
+
+/* ---- scene (GaussianSet) */
+int slm_scene_create(slm_context* ctx, const slm_gaussians* host, slm_scene** out);
+void slm_scene_destroy(slm_scene* s);
+int slm_scene_upload(slm_scene* s, const slm_gaussians* host);
+int slm_scene_download(slm_scene* s, slm_gaussians* host);
+int slm_scene_count(slm_scene* s, int* count, int* padded);
+/* GaussianSet::apply_update (types.cpp:48-60): beta += eta*delta, re-normalise. */
+int slm_scene_apply_update(slm_scene* s, const double* delta_aos, double eta);
+
+/* ---- render (render/rasterizer.hpp) */
+/* render::bin_and_sort (rasterizer.hpp:154-156): CSR tile lists, offsets[tiles+1]. */
+int slm_bin_and_sort(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam,
+                     int32_t* offsets, int32_t* indices, int64_t capacity, int64_t* n_entries);
+/* render::prepare_camera value parts (rasterizer.cpp:10-19), f32 records -> f64. */
+int slm_prepare(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, double* mean2d,
+                double* conic, double* opacity, double* color, double* depth, double* radius,
+                int32_t* valid);
+/* render::render_full (rasterizer.cpp:93-95); any output may be NULL. */
+int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, double* image,
+                    double* transmittance, int32_t* contrib);
+int slm_scene_render(slm_scene* s, const slm_camera* cam, float* image, float* transmittance,
+                     int32_t* contrib);
+
+/* ---- sampling (sampling/ headers), host side with the reference's libstdc++ RNG */
+/* build_sample_plan (sample_plan.cpp:62-171); aux_* are per-camera rendered
+ * image (H*W*3), contrib counts (H*W) and ground truth (H*W*3), only read for
+ * the weighted distributions. */
+int slm_build_sample_plan(const slm_camera* cams, int n_cams, int samples_per_tile, int dist,
+                          int lane_width, slm_rng* rng, const double* const* aux_image,
+                          const int32_t* const* aux_contrib, const double* const* aux_gt,
+                          slm_plan_h** out);
+int slm_exhaustive_plan(const slm_camera* cams, int n_cams, slm_plan_h** out); /* :173-197 */
+void slm_plan_destroy(slm_plan_h* p);
+int slm_plan_size(slm_plan_h* p, int* n_views, int64_t* total);
+int slm_plan_export(slm_plan_h* p, int32_t* view_camera, int64_t* view_offset, int32_t* px,
+                    int32_t* py, int32_t* tile, double* weight);
+/* estimate_loss (sample_plan.cpp:199-222) on host residual fields. */
+int slm_estimate_loss(const slm_camera* cams, const slm_plan* plan,
+                      const double* const* residual_fields, double* out);
+/* camera_features / kmeans_cameras / sample_view_batch (view_sampler.cpp:10-184). */
+int slm_camera_features(const slm_camera* cams, int n_cams, double* feats);
+int slm_kmeans_cameras(const slm_camera* cams, int n_cams, int k, uint64_t seed, int32_t* assign);
+int slm_sample_view_batch(const int32_t* assign, int n_cams, int k, slm_rng* rng, int32_t* batch);
+
+/* ---- SampledJacobian (autodiff/jacobian.hpp:25-76) */
+int slm_jacobian_create(slm_context* ctx, const slm_gaussians* g, const slm_camera* cams, int n_cams,
+                        const slm_plan* plan, slm_jacobian** out);
+int slm_jacobian_create_scene(slm_scene* s, const slm_camera* cams, int n_cams,
+                              const slm_plan* plan, slm_jacobian** out);
+void slm_jacobian_destroy(slm_jacobian* j);
+int slm_jacobian_dims(slm_jacobian* j, int64_t* residual_dim, int64_t* param_dim);
+int slm_jacobian_jvp(slm_jacobian* j, const double* v, double* out);          /* :191-211 */
+int slm_jacobian_vjp(slm_jacobian* j, const double* u, double* out);          /* :219-264 */
+int slm_jacobian_jtj_diag(slm_jacobian* j, double* out);                      /* :272-337 */
+int slm_jacobian_gn_apply(slm_jacobian* j, double lambda, const double* p, double* out); /* :339-344 */
+int slm_jacobian_weights(slm_jacobian* j, double* out);                       /* jacobian.hpp:43 */
+int slm_jacobian_set_weights(slm_jacobian* j, const double* w);              /* :121-125 */
+/* Device-resident products on f32 SoA vectors (the hot path lm_step uses). */
+int slm_jacobian_gn_apply_dev(slm_jacobian* j, float lambda, const float* d_p, float* d_out);
+/* pcg_solve (pcg.cpp:10-53) on (J^T W J + lambda I) x = b, entirely on device. */
+int slm_jacobian_pcg(slm_jacobian* j, double lambda, const double* b, const double* minv,
+                     int max_iters, double* x, slm_pcg_result* res);
+
+/* ---- PCG on a caller-supplied operator (pcg.hpp:16-23): vector algebra on
+ * the device, the operator callback receives/returns host f64 vectors. */
+typedef void (*slm_apply_fn)(void* user, const double* p, double* out);
+int slm_pcg_solve(slm_context* ctx, slm_apply_fn apply, void* user, const double* b,
+                  const double* minv, int64_t n, int max_iters, double* x, slm_pcg_result* res);
+
+/* ---- solver (solver/lm.hpp) */
+int slm_learning_rate(slm_context* ctx, const double* delta, int64_t n, int iteration,
+                      const slm_lm_config* cfg, double* eta);                 /* lm.cpp:26-37 */
+void slm_default_lm_config(slm_lm_config* cfg);
+/* TrainData with the f32 dataset images (H*W*3 per camera) resident in HBM. */
+int slm_train_create(slm_context* ctx, const slm_camera* cams, int n_cams, const float* images,
+                     slm_train** out);
+void slm_train_destroy(slm_train* t);
+int slm_train_rebuild_clusters(slm_train* t, int k, uint64_t seed);       /* lm.cpp:21-24 */
+int slm_train_set_clusters(slm_train* t, const int32_t* assign, int k);
+int slm_train_clusters(slm_train* t, int32_t* assign, int* k);
+/* lm_step (lm.cpp:56-157) on a device-resident scene. */
+int slm_lm_step(slm_scene* s, slm_train* t, const slm_lm_config* cfg, int iteration, slm_rng* rng,
+                slm_step_report* report);
+/* Drop-in host form: state is the caller's GaussianSet, updated in place. */
+int slm_lm_step_host(slm_context* ctx, slm_gaussians* state, slm_train* t,
+                     const slm_lm_config* cfg, int iteration, slm_rng* rng,
+                     slm_step_report* report);
+/* batch_loss (lm.cpp:39-54), MSE; cameras index the TrainData. */
+int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cams, int n, double* out);
+
+/* ---- io helpers the harness uses (io/dataset.cpp:138-166, io/scene_gen.cpp) */
+int slm_random_init(int count, const double* cube_min, const double* cube_max, slm_rng* rng,
+                    slm_gaussians* out);
+int slm_ring_camera(double angle, double radius, double height, int width, int height_px,
+                    slm_camera* out);
+
+/* ---- instrumentation (no reference counterpart) */
+/* Run the context's work on a caller stream (e.g. torch.cuda.Stream().cuda_stream),
+ * so the caller's CUDA events bracket the library's kernels. */
+int slm_context_set_stream(slm_context* ctx, void* stream);
+int slm_context_set_timing(slm_context* ctx, int on);
+long long slm_launch_count(void); /* kernels launched by this library so far */
+int slm_scene_beta_ptrs(slm_scene* s, double** beta, float** beta32);
+int slm_jacobian_device_ptrs(slm_jacobian* j, void* stream_out[1]);
+/* [views, 0, tile-list entries, samples, warp groups, tiles] */
+int slm_jacobian_stats(slm_jacobian* j, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SLM_B200_H */

@@ -1,0 +1,397 @@
+// chain.cu — per-Gaussian FP64 linearisation kernels.
+//
+// The reference builds a 5x10 ProjChain per (view, Gaussian) from 10 dual
+// probes (jacobian.cpp:127-165) and re-runs the full dual preparation for
+// every Jv (dual_splats :167-189).  Here the same derivatives are taken
+// analytically and factored through the view-independent 3D covariance:
+//
+//   (mean, log_scale, quat) --view-independent--> (mu, Sigma)
+//   (mu, Sigma) --per view--> t = W mu + t_cam, T = J(t) W, cov2d = T Sigma T^T + 0.3 I,
+//                             conic = cov2d^{-1}, mean2d = proj(t)
+//
+// so one thread per Gaussian computes dSigma (forward) or accumulates
+// dL/dSigma over the views (reverse) once, and each view only touches the
+// cheap projection part.  Mathematically identical to the reference's dual
+// evaluation (same function, exact chain rule); differs only in rounding.
+//
+//  * k_tangents       Jv probe: per (view, Gaussian) tangent record of
+//                     (mean2d, conic, opacity, colour) along p            [K8]
+//  * k_chain          J^T: 9-float intermediates -> 14 parameter grads, + lambda p,
+//                     zeroes the intermediates for the next product         [K11]
+//  * k_diag_finalize  diag(J^T W J) from the per-entry quadratic forms     [K13]
+#include <cstdint>
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace slm { extern std::atomic<long long> g_launches; }
+
+namespace slm {
+
+struct Geom {  // view-independent part, FP64
+    double mu[3];
+    double qn[4];   // normalised quaternion
+    double qinv;    // 1/|q|
+    double R[9], s[3], M[9], Sig[9];
+    double o;       // sigmoid(logit)
+    double dcol[3]; // C0 if the colour gate is open else 0 (rasterizer.hpp:83-86)
+};
+
+__device__ __forceinline__ void load_geom(const double* __restrict__ beta, int Gp, int g, Geom& G) {
+    for (int k = 0; k < 3; ++k) G.mu[k] = beta[k * Gp + g];
+    const double q[4] = {beta[6 * Gp + g], beta[7 * Gp + g], beta[8 * Gp + g], beta[9 * Gp + g]};
+    const double nsq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    G.qinv = nsq > 0.0 ? 1.0 / sqrt(nsq) : 0.0;
+    for (int k = 0; k < 4; ++k) G.qn[k] = q[k] * G.qinv;
+    const double w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
+    G.R[0] = 1.0 - 2.0 * (y * y + z * z);
+    G.R[1] = 2.0 * (x * y - w * z);
+    G.R[2] = 2.0 * (x * z + w * y);
+    G.R[3] = 2.0 * (x * y + w * z);
+    G.R[4] = 1.0 - 2.0 * (x * x + z * z);
+    G.R[5] = 2.0 * (y * z - w * x);
+    G.R[6] = 2.0 * (x * z - w * y);
+    G.R[7] = 2.0 * (y * z + w * x);
+    G.R[8] = 1.0 - 2.0 * (x * x + y * y);
+    for (int k = 0; k < 3; ++k) G.s[k] = exp(beta[(3 + k) * Gp + g]);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) G.M[3 * i + j] = G.R[3 * i + j] * G.s[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            G.Sig[3 * i + j] = G.M[3 * i] * G.M[3 * j] + G.M[3 * i + 1] * G.M[3 * j + 1] +
+                               G.M[3 * i + 2] * G.M[3 * j + 2];
+    G.o = 1.0 / (1.0 + exp(-beta[10 * Gp + g]));
+    for (int k = 0; k < 3; ++k) {
+        const double raw = 0.5 + kColorC0 * beta[(11 + k) * Gp + g];
+        G.dcol[k] = raw > 0.0 ? kColorC0 : 0.0;
+    }
+}
+
+struct View {  // per-view projection part, FP64
+    double tx, ty, tz, iz;
+    double j00, j02, j11, j12;
+    double r0[3], r1[3], Sr0[3], Sr1[3];
+    double a, b, c, det, ca, cb, cc;
+};
+
+__device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, View& V) {
+    const double* W = cam.R;
+    V.tx = W[0] * G.mu[0] + W[1] * G.mu[1] + W[2] * G.mu[2] + cam.t[0];
+    V.ty = W[3] * G.mu[0] + W[4] * G.mu[1] + W[5] * G.mu[2] + cam.t[1];
+    V.tz = W[6] * G.mu[0] + W[7] * G.mu[1] + W[8] * G.mu[2] + cam.t[2];
+    V.iz = 1.0 / V.tz;
+    const double iz2 = V.iz * V.iz;
+    V.j00 = cam.fx * V.iz;
+    V.j02 = -cam.fx * V.tx * iz2;
+    V.j11 = cam.fy * V.iz;
+    V.j12 = -cam.fy * V.ty * iz2;
+    for (int k = 0; k < 3; ++k) {
+        V.r0[k] = V.j00 * W[k] + V.j02 * W[6 + k];
+        V.r1[k] = V.j11 * W[3 + k] + V.j12 * W[6 + k];
+    }
+    for (int i = 0; i < 3; ++i) {
+        V.Sr0[i] = G.Sig[3 * i] * V.r0[0] + G.Sig[3 * i + 1] * V.r0[1] + G.Sig[3 * i + 2] * V.r0[2];
+        V.Sr1[i] = G.Sig[3 * i] * V.r1[0] + G.Sig[3 * i + 1] * V.r1[1] + G.Sig[3 * i + 2] * V.r1[2];
+    }
+    V.a = V.r0[0] * V.Sr0[0] + V.r0[1] * V.Sr0[1] + V.r0[2] * V.Sr0[2] + 0.3;
+    V.b = V.r0[0] * V.Sr1[0] + V.r0[1] * V.Sr1[1] + V.r0[2] * V.Sr1[2];
+    V.c = V.r1[0] * V.Sr1[0] + V.r1[1] * V.Sr1[1] + V.r1[2] * V.Sr1[2] + 0.3;
+    V.det = V.a * V.c - V.b * V.b;
+    const double inv = 1.0 / V.det;
+    V.ca = V.c * inv;
+    V.cb = -V.b * inv;
+    V.cc = V.a * inv;
+}
+
+// dSigma (full 3x3) along (dlog_scale, dquat) — forward mode of covariance_3d.
+__device__ __forceinline__ void dsigma(const Geom& G, const double dls[3], const double dq[4],
+                                       double dS[9]) {
+    // normalisation: dqn = (dq - qn (qn . dq)) / |q|
+    const double proj = G.qn[0] * dq[0] + G.qn[1] * dq[1] + G.qn[2] * dq[2] + G.qn[3] * dq[3];
+    double dn[4];
+    for (int k = 0; k < 4; ++k) dn[k] = (dq[k] - G.qn[k] * proj) * G.qinv;
+    const double w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
+    const double dw = dn[0], dx = dn[1], dy = dn[2], dz = dn[3];
+    double dR[9];
+    dR[0] = -4.0 * (y * dy + z * dz);
+    dR[1] = 2.0 * (dx * y + x * dy - dw * z - w * dz);
+    dR[2] = 2.0 * (dx * z + x * dz + dw * y + w * dy);
+    dR[3] = 2.0 * (dx * y + x * dy + dw * z + w * dz);
+    dR[4] = -4.0 * (x * dx + z * dz);
+    dR[5] = 2.0 * (dy * z + y * dz - dw * x - w * dx);
+    dR[6] = 2.0 * (dx * z + x * dz - dw * y - w * dy);
+    dR[7] = 2.0 * (dy * z + y * dz + dw * x + w * dx);
+    dR[8] = -4.0 * (x * dx + y * dy);
+    double dM[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            dM[3 * i + j] = dR[3 * i + j] * G.s[j] + G.R[3 * i + j] * G.s[j] * dls[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += dM[3 * i + k] * G.M[3 * j + k] + G.M[3 * i + k] * dM[3 * j + k];
+            dS[3 * i + j] = acc;
+        }
+}
+
+// Tangent of (mean2d, conic) for one view given (dmu, dSigma).
+__device__ __forceinline__ void view_tangent(const Geom& G, const View& V, const DevCam& cam,
+                                             const double dmu[3], const double dS[9], double out[5]) {
+    const double* W = cam.R;
+    const double dtx = W[0] * dmu[0] + W[1] * dmu[1] + W[2] * dmu[2];
+    const double dty = W[3] * dmu[0] + W[4] * dmu[1] + W[5] * dmu[2];
+    const double dtz = W[6] * dmu[0] + W[7] * dmu[1] + W[8] * dmu[2];
+    const double diz = -dtz * V.iz * V.iz;
+    out[0] = cam.fx * (dtx * V.iz + V.tx * diz);
+    out[1] = cam.fy * (dty * V.iz + V.ty * diz);
+    const double iz2 = V.iz * V.iz, diz2 = 2.0 * V.iz * diz;
+    const double dj00 = cam.fx * diz, dj02 = -cam.fx * (dtx * iz2 + V.tx * diz2);
+    const double dj11 = cam.fy * diz, dj12 = -cam.fy * (dty * iz2 + V.ty * diz2);
+    double dr0[3], dr1[3];
+    for (int k = 0; k < 3; ++k) {
+        dr0[k] = dj00 * W[k] + dj02 * W[6 + k];
+        dr1[k] = dj11 * W[3 + k] + dj12 * W[6 + k];
+    }
+    // d(r0^T S r0) = 2 dr0 . S r0 + r0^T dS r0, etc.
+    double dSr0[3], dSr1[3];
+    for (int i = 0; i < 3; ++i) {
+        dSr0[i] = dS[3 * i] * V.r0[0] + dS[3 * i + 1] * V.r0[1] + dS[3 * i + 2] * V.r0[2];
+        dSr1[i] = dS[3 * i] * V.r1[0] + dS[3 * i + 1] * V.r1[1] + dS[3 * i + 2] * V.r1[2];
+    }
+    const double da = 2.0 * (dr0[0] * V.Sr0[0] + dr0[1] * V.Sr0[1] + dr0[2] * V.Sr0[2]) +
+                      (V.r0[0] * dSr0[0] + V.r0[1] * dSr0[1] + V.r0[2] * dSr0[2]);
+    const double db = (dr0[0] * V.Sr1[0] + dr0[1] * V.Sr1[1] + dr0[2] * V.Sr1[2]) +
+                      (dr1[0] * V.Sr0[0] + dr1[1] * V.Sr0[1] + dr1[2] * V.Sr0[2]) +
+                      (V.r0[0] * dSr1[0] + V.r0[1] * dSr1[1] + V.r0[2] * dSr1[2]);
+    const double dc = 2.0 * (dr1[0] * V.Sr1[0] + dr1[1] * V.Sr1[1] + dr1[2] * V.Sr1[2]) +
+                      (V.r1[0] * dSr1[0] + V.r1[1] * dSr1[1] + V.r1[2] * dSr1[2]);
+    // conic = cov2d^-1: d conic = -conic d cov2d conic
+    const double ca = V.ca, cb = V.cb, cc = V.cc;
+    out[2] = -(ca * ca * da + 2.0 * ca * cb * db + cb * cb * dc);
+    out[3] = -(ca * cb * da + (ca * cc + cb * cb) * db + cb * cc * dc);
+    out[4] = -(cb * cb * da + 2.0 * cb * cc * db + cc * cc * dc);
+}
+
+__device__ __forceinline__ bool rec_valid(const float4* rec, size_t vg) {
+    return rec[3 * vg + 2].y != 0.0f;  // validity marker written by k_prepare
+}
+
+// ------------------------------------------------------------------ K8
+// One thread per Gaussian; loops over the batch's views.  p is the f32 SoA
+// probe; writes tan[(v*Gp+g)] for valid (view, Gaussian) pairs.
+__global__ void k_tangents(const double* __restrict__ beta, const float* __restrict__ p, int G,
+                           int Gp, const DevCam* __restrict__ cams, int V,
+                           const float4* __restrict__ rec, float4* __restrict__ tan,
+                           const int* __restrict__ done_flag) {
+    if (done_flag && *done_flag) return;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    Geom Gm;
+    load_geom(beta, Gp, g, Gm);
+    double pv[kP];
+    for (int k = 0; k < kP; ++k) pv[k] = (double)p[k * Gp + g];
+    double dS[9];
+    dsigma(Gm, pv + 3, pv + 6, dS);
+    const float dop = (float)(Gm.o * (1.0 - Gm.o) * pv[10]);
+    const float dr = (float)(Gm.dcol[0] * pv[11]), dg = (float)(Gm.dcol[1] * pv[12]),
+                db = (float)(Gm.dcol[2] * pv[13]);
+    for (int v = 0; v < V; ++v) {
+        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        if (!rec_valid(rec, vg)) continue;
+        const DevCam& cam = cams[v];
+        View Vw;
+        load_view(Gm, cam, Vw);
+        double o5[5];
+        view_tangent(Gm, Vw, cam, pv, dS, o5);
+        float4* t = tan + 3 * vg;
+        t[0] = make_float4((float)o5[0], (float)o5[1], (float)o5[2], (float)o5[3]);
+        t[1] = make_float4((float)o5[4], dop, dr, dg);
+        t[2] = make_float4(db, 0.f, 0.f, 0.f);
+    }
+}
+
+// ------------------------------------------------------------------ K11
+// out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
+// exact reverse mode of the projection; inter is zeroed after reading.
+__global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
+                        const DevCam* __restrict__ cams, int V, const float4* __restrict__ rec,
+                        float* __restrict__ inter, const float* __restrict__ p, float lambda,
+                        float* __restrict__ out, const int* __restrict__ done_flag) {
+    if (done_flag && *done_flag) return;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    Geom Gm;
+    load_geom(beta, Gp, g, Gm);
+    double gS[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double gmu[3] = {0, 0, 0};
+    double go = 0.0, gcol[3] = {0, 0, 0};
+    for (int v = 0; v < V; ++v) {
+        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        if (!rec_valid(rec, vg)) continue;
+        float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
+        const float4 i0 = ip[0], i1 = ip[1], i2 = ip[2];
+        ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ip[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const double gmx = i0.x, gmy = i0.y, gca = i0.z, gcb = i0.w, gcc = i1.x;
+        go += i1.y;
+        gcol[0] += i1.z;
+        gcol[1] += i1.w;
+        gcol[2] += i2.x;
+        const DevCam& cam = cams[v];
+        View Vw;
+        load_view(Gm, cam, Vw);
+        const double ca = Vw.ca, cb = Vw.cb, cc = Vw.cc;
+        // conic -> cov2d (a, b, c): adjoint of d conic = -C dA C
+        const double ga = -(gca * ca * ca + gcb * ca * cb + gcc * cb * cb);
+        const double gb = -(2.0 * gca * ca * cb + gcb * (ca * cc + cb * cb) + 2.0 * gcc * cc * cb);
+        const double gc = -(gca * cb * cb + gcb * cb * cc + gcc * cc * cc);
+        // cov2d -> r0, r1, Sigma
+        double gr0[3], gr1[3];
+        for (int k = 0; k < 3; ++k) {
+            gr0[k] = 2.0 * ga * Vw.Sr0[k] + gb * Vw.Sr1[k];
+            gr1[k] = gb * Vw.Sr0[k] + 2.0 * gc * Vw.Sr1[k];
+        }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                gS[3 * i + j] += ga * Vw.r0[i] * Vw.r0[j] + gb * Vw.r0[i] * Vw.r1[j] +
+                                 gc * Vw.r1[i] * Vw.r1[j];
+        const double* W = cam.R;
+        const double gj00 = gr0[0] * W[0] + gr0[1] * W[1] + gr0[2] * W[2];
+        const double gj02 = gr0[0] * W[6] + gr0[1] * W[7] + gr0[2] * W[8];
+        const double gj11 = gr1[0] * W[3] + gr1[1] * W[4] + gr1[2] * W[5];
+        const double gj12 = gr1[0] * W[6] + gr1[1] * W[7] + gr1[2] * W[8];
+        const double iz = Vw.iz, iz2 = iz * iz;
+        const double gtx = gmx * cam.fx * iz - gj02 * cam.fx * iz2;
+        const double gty = gmy * cam.fy * iz - gj12 * cam.fy * iz2;
+        const double giz = gmx * cam.fx * Vw.tx + gmy * cam.fy * Vw.ty + gj00 * cam.fx + gj11 * cam.fy -
+                           2.0 * gj02 * cam.fx * Vw.tx * iz - 2.0 * gj12 * cam.fy * Vw.ty * iz;
+        const double gtz = -giz * iz2;
+        for (int k = 0; k < 3; ++k) gmu[k] += W[k] * gtx + W[3 + k] * gty + W[6 + k] * gtz;
+    }
+    // Sigma = M M^T: gM = (gS + gS^T) M ; M = R diag(s)
+    double gM[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += (gS[3 * i + k] + gS[3 * k + i]) * Gm.M[3 * k + j];
+            gM[3 * i + j] = acc;
+        }
+    double gR[9], gls[3];
+    for (int j = 0; j < 3; ++j) {
+        double gs = 0.0;
+        for (int i = 0; i < 3; ++i) {
+            gR[3 * i + j] = gM[3 * i + j] * Gm.s[j];
+            gs += gM[3 * i + j] * Gm.R[3 * i + j];
+        }
+        gls[j] = gs * Gm.s[j];
+    }
+    const double w = Gm.qn[0], x = Gm.qn[1], y = Gm.qn[2], z = Gm.qn[3];
+    double gn[4];
+    gn[0] = 2.0 * (-z * gR[1] + y * gR[2] + z * gR[3] - x * gR[5] - y * gR[6] + x * gR[7]);
+    gn[1] = 2.0 * (y * gR[1] + z * gR[2] + y * gR[3] - 2.0 * x * gR[4] - w * gR[5] + z * gR[6] +
+                   w * gR[7] - 2.0 * x * gR[8]);
+    gn[2] = 2.0 * (-2.0 * y * gR[0] + x * gR[1] + w * gR[2] + x * gR[3] + z * gR[5] - w * gR[6] +
+                   z * gR[7] - 2.0 * y * gR[8]);
+    gn[3] = 2.0 * (-2.0 * z * gR[0] - w * gR[1] + x * gR[2] + w * gR[3] - 2.0 * z * gR[4] +
+                   y * gR[5] + x * gR[6] + y * gR[7]);
+    const double proj = Gm.qn[0] * gn[0] + Gm.qn[1] * gn[1] + Gm.qn[2] * gn[2] + Gm.qn[3] * gn[3];
+    double res[kP];
+    for (int k = 0; k < 3; ++k) res[k] = gmu[k];
+    for (int k = 0; k < 3; ++k) res[3 + k] = gls[k];
+    for (int k = 0; k < 4; ++k) res[6 + k] = (gn[k] - Gm.qn[k] * proj) * Gm.qinv;
+    res[10] = go * Gm.o * (1.0 - Gm.o);
+    for (int k = 0; k < 3; ++k) res[11 + k] = gcol[k] * Gm.dcol[k];
+    for (int k = 0; k < kP; ++k) {
+        float val = (float)res[k];
+        if (p) val += lambda * p[k * Gp + g];
+        out[k * Gp + g] = val;
+    }
+}
+
+// ------------------------------------------------------------------ K13 finalize
+// diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
+// ProjChain columns P_j are the view_tangent of the unit probes e_j.
+__global__ void k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
+                                const DevCam* __restrict__ cams, int V,
+                                const float4* __restrict__ rec, float* __restrict__ diagacc,
+                                float* __restrict__ out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    Geom Gm;
+    load_geom(beta, Gp, g, Gm);
+    double dSj[7][9];  // dSigma for the 3 log-scale + 4 quaternion unit probes
+    for (int j = 0; j < 7; ++j) {
+        double dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0};
+        if (j < 3) dls[j] = 1.0; else dq[j - 3] = 1.0;
+        dsigma(Gm, dls, dq, dSj[j]);
+    }
+    double d[kP];
+    for (int k = 0; k < kP; ++k) d[k] = 0.0;
+    const double zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const double zero3[3] = {0, 0, 0};
+    for (int v = 0; v < V; ++v) {
+        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        if (!rec_valid(rec, vg)) continue;
+        float* acc = diagacc + vg * kDiagRec;
+        double M[5][5];
+        int q = 0;
+        for (int i = 0; i < 5; ++i)
+            for (int jj = i; jj < 5; ++jj) {
+                M[i][jj] = acc[q];
+                M[jj][i] = acc[q];
+                ++q;
+            }
+        const double aop = acc[15], ac0 = acc[16], ac1 = acc[17], ac2 = acc[18];
+        for (int i = 0; i < kDiagRec; ++i) acc[i] = 0.0f;
+        const DevCam& cam = cams[v];
+        View Vw;
+        load_view(Gm, cam, Vw);
+        for (int j = 0; j < 10; ++j) {
+            double col[5];
+            if (j < 3) {
+                double dmu[3] = {0, 0, 0};
+                dmu[j] = 1.0;
+                view_tangent(Gm, Vw, cam, dmu, zero9, col);
+            } else {
+                view_tangent(Gm, Vw, cam, zero3, dSj[j - 3], col);
+            }
+            double qf = 0.0;
+            for (int a = 0; a < 5; ++a) {
+                double r = 0.0;
+                for (int b = 0; b < 5; ++b) r += M[a][b] * col[b];
+                qf += col[a] * r;
+            }
+            d[j] += qf;
+        }
+        const double ds = Gm.o * (1.0 - Gm.o);
+        d[10] += aop * ds * ds;
+        d[11] += ac0 * Gm.dcol[0] * Gm.dcol[0];
+        d[12] += ac1 * Gm.dcol[1] * Gm.dcol[1];
+        d[13] += ac2 * Gm.dcol[2] * Gm.dcol[2];
+    }
+    for (int k = 0; k < kP; ++k) out[k * Gp + g] = (float)d[k];
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
+                     const float4* rec, float4* tan, const int* done, cudaStream_t st) {
+    if (G == 0) return;
+    k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
+}
+
+void launch_chain(const double* beta, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                  float* inter, const float* p, float lambda, float* out, const int* done,
+                  cudaStream_t st) {
+    if (G == 0) return;
+    k_chain<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
+}
+
+void launch_diag_finalize(const double* beta, int G, int Gp, const DevCam* cams, int V,
+                          const float4* rec, float* diagacc, float* out, cudaStream_t st) {
+    if (G == 0) return;
+    k_diag_finalize<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
+}
+
+}  // namespace slm

@@ -1,0 +1,90 @@
+// layout.hpp — POD types and constants shared by host (runtime.cpp, g++) and
+// device (*.cu, nvcc) code.  See common.cuh for the HBM layout notes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "slm_types.h"
+
+namespace slm {
+
+constexpr int kTile = 16;               // rasterizer.hpp:14
+constexpr int kP = 14;                  // types.hpp:20
+constexpr int kRec = 12;                // floats per splat / tangent / inter record
+constexpr int kDiagRec = 20;            // floats per diag accumulator record (19 used)
+constexpr double kAlphaClampD = 0.99;   // rasterizer.hpp:15
+constexpr double kAlphaSkipD = 1.0 / 255.0;
+constexpr double kTFloorD = 1e-4;       // rasterizer.hpp:17
+constexpr double kColorC0 = 0.28209479177387814;  // types.hpp:24
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr double kLn2 = 0.69314718055994530942;
+
+// Device-side camera (slm_camera minus nothing): passed by value in kernel
+// params or staged in __constant__/smem.
+struct DevCam {
+    double R[9];
+    double t[3];
+    double fx, fy, cx, cy, near_clip;
+    int width, height;
+    int tiles_x, tiles_y;
+    int tile_base;   // first tile of this view in the batch-concatenated tile arrays
+    int pad0;
+    long long pix_base;  // first pixel of this view in the concatenated pixel arrays
+};
+
+// A unit of sampled-raster work: up to 32 samples of one tile of one view.
+struct Group {
+    int view;
+    int tile;       // tile index within the view
+    int begin;      // first sample (group order) of this group
+    int count;      // 1..32
+};
+
+struct SampleArgs {
+    const Group* groups;
+    int n_groups;
+    const DevCam* cams;
+    const int* tile_offsets;
+    const int* entries;
+    const float4* rec;
+    const float4* tan;
+    int Gp;
+    const int* spix;   // px | py << 16, group order
+    const int* sorig;  // original sample index (plan order)
+    const float* sw;   // per-sample per-channel weights, group order [3*s+c]
+    const float* image;
+    const int* last_img;
+    const float* gt;
+    const float* in_res;  // VJP: u in plan order [3*orig+c]
+    float* out_res;       // JVP: Jv in plan order
+    float* inter;         // J^T accumulators [(v*Gp+g)*12 + i]
+    const int* done_flag; // optional: skip all work when *done_flag != 0 (PCG converged)
+};
+
+struct DiagArgs {
+    const Group* groups;
+    int n_groups;
+    const DevCam* cams;
+    const int* tile_offsets;
+    const int* entries;
+    const float4* rec;
+    int Gp;
+    const int* spix;
+    const float* sw;
+    const float* image;
+    const int* last_img;
+    float* diagacc;
+};
+
+struct CgState {
+    double rz, pu, alpha, beta, rr, bnorm;
+    int iterations, breakdown, done, pad;
+};
+
+enum Mode { kJvp = 0, kVjp = 1, kGn = 2, kRhs = 3 };
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+
+}  // namespace slm

@@ -1,0 +1,1650 @@
+// runtime.cpp — host C++ runtime and C ABI of libslm_b200.so.
+//
+// Mirrors the reference's C++ solver API (proj/include/splatlm/**) on top of
+// the sm_100a kernels: device-resident GaussianSet (Scene), the batch's
+// prepared views and tile lists (Batch), the sample plan laid out as warp
+// groups (Samples), SampledJacobian (Jacobian), the device PCG and lm_step.
+// The samplers (build_sample_plan, k-means view batching, random_init) stay on
+// the host with libstdc++'s <random>, which is what makes the sampled pixel
+// sets bit-identical to the reference (SURVEY §7 hard part 2).
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdlib>
+#include <cmath>
+#include <limits>
+#include <memory>
+#include <numeric>
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "slm_b200.h"
+
+namespace slm {
+
+std::atomic<long long> g_launches{0};
+
+namespace {
+thread_local std::string g_err;
+
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// NCCL is resolved at first use with dlopen, never at load time: the library
+// must coexist with whichever libnccl.so.2 the host process (e.g. PyTorch's
+// bundled 2.28) already mapped, and single-GPU use needs no NCCL at all.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (loaded) return api;
+    void* h = nullptr;
+    if (const char* env = std::getenv("SLM_NCCL_LIB")) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw NcclError("NCCL library not found (set SLM_NCCL_LIB)");
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString)
+        throw NcclError("NCCL library lacks required symbols");
+    loaded = true;
+    return api;
+}
+
+#define SLM_NCCL_CHECK(x)                                                                  \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess) throw NcclError(std::string("NCCL error: ") + nccl().GetErrorString(r_)); \
+    } while (0)
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+}  // namespace
+
+// =========================================================================== Context
+struct StepBuffers;
+void destroy_step(StepBuffers*);
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    DevBuf<double> partial;
+    DevBuf<CgState> cg;
+    DevBuf<double> dscalar;
+    DevBuf<float> fscalar;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    std::vector<double> last_timings;
+    bool timing = false;
+    StepBuffers* step = nullptr;  // persistent lm_step workspace
+
+    explicit Context(int dev) : device(dev) {
+        SLM_CUDA_CHECK(cudaSetDevice(dev));
+        SLM_CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        partial.ensure(2 * kRedBlocks);
+        cg.ensure(1);
+        dscalar.ensure(16);
+        fscalar.ensure(16);
+    }
+    ~Context() {
+        destroy_step(step);
+        for (auto& m : marks) cudaEventDestroy(m.second);
+        if (comm) nccl().CommDestroy(comm);
+        if (stream && own_stream) cudaStreamDestroy(stream);
+    }
+    void activate() const { SLM_CUDA_CHECK(cudaSetDevice(device)); }
+    void sync() const { SLM_CUDA_CHECK(cudaStreamSynchronize(stream)); }
+    void check_launch() const { SLM_CUDA_CHECK(cudaGetLastError()); }
+
+    void mark(const char* name) {
+        if (!timing) return;
+        cudaEvent_t e;
+        SLM_CUDA_CHECK(cudaEventCreate(&e));
+        SLM_CUDA_CHECK(cudaEventRecord(e, stream));
+        marks.emplace_back(name, e);
+    }
+    void finish_marks() {
+        if (!timing || marks.empty()) return;
+        sync();
+        last_timings.clear();
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+            last_timings.push_back(ms);
+        }
+        for (auto& m : marks) cudaEventDestroy(m.second);
+        marks.clear();
+    }
+
+    void allreduce(float* p, size_t n) {
+        if (world <= 1 || n == 0) return;
+        SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, ncclFloat32, ncclSum, comm, stream));
+    }
+    void allreduce(double* p, size_t n) {
+        if (world <= 1 || n == 0) return;
+        SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, ncclFloat64, ncclSum, comm, stream));
+    }
+};
+
+// =========================================================================== Scene
+struct Scene {
+    Context* ctx;
+    int G = 0, Gp = 0;
+    DevBuf<double> beta;    // f64 SoA [14][Gp]
+    DevBuf<float> beta32;   // f32 mirror
+    DevBuf<double> stage;   // host-layout staging (5 arrays)
+
+    Scene(Context* c, const slm_gaussians& h) : ctx(c) { upload(h); }
+
+    void upload(const slm_gaussians& h) {
+        if (h.count < 0) throw std::invalid_argument("negative Gaussian count");
+        ctx->activate();
+        G = h.count;
+        Gp = round_up(std::max(G, 1), 256);
+        const size_t P = static_cast<size_t>(kP) * Gp;
+        beta.ensure(P);
+        beta32.ensure(P);
+        SLM_CUDA_CHECK(cudaMemsetAsync(beta.p, 0, P * sizeof(double), ctx->stream));
+        SLM_CUDA_CHECK(cudaMemsetAsync(beta32.p, 0, P * sizeof(float), ctx->stream));
+        if (G == 0) return;
+        stage.ensure(static_cast<size_t>(14) * G);
+        double* s = stage.p;
+        cudaStream_t st = ctx->stream;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(s, h.means, sizeof(double) * 3 * G, cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(s + 3 * G, h.log_scales, sizeof(double) * 3 * G, cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(s + 6 * G, h.rotations, sizeof(double) * 4 * G, cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(s + 10 * G, h.opacity_logits, sizeof(double) * G, cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(s + 11 * G, h.colors, sizeof(double) * 3 * G, cudaMemcpyHostToDevice, st));
+        launch_set_to_beta(s, s + 3 * G, s + 6 * G, s + 10 * G, s + 11 * G, G, Gp, beta.p, beta32.p, st);
+        ctx->check_launch();
+    }
+
+    void download(slm_gaussians& h) {
+        if (h.count != G) throw std::invalid_argument("download: Gaussian count mismatch");
+        if (G == 0) return;
+        ctx->activate();
+        stage.ensure(static_cast<size_t>(14) * G);
+        double* s = stage.p;
+        cudaStream_t st = ctx->stream;
+        launch_beta_to_set(beta.p, G, Gp, s, s + 3 * G, s + 6 * G, s + 10 * G, s + 11 * G, st);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.means, s, sizeof(double) * 3 * G, cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.log_scales, s + 3 * G, sizeof(double) * 3 * G, cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.rotations, s + 6 * G, sizeof(double) * 4 * G, cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.opacity_logits, s + 10 * G, sizeof(double) * G, cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.colors, s + 11 * G, sizeof(double) * 3 * G, cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+    }
+
+    size_t P() const { return static_cast<size_t>(kP) * Gp; }
+};
+
+// =========================================================================== Batch
+// The prepared views of one scene state: splat records, tile lists (K1, K3,
+// K4) and, after render(), the per-pixel forward state (K6).
+struct Batch {
+    Context* ctx;
+    int V = 0, n_tiles = 0, Gp = 0, G = 0;
+    long long n_pix = 0, n_entries = 0;
+    std::vector<DevCam> hcams;
+    std::vector<int> htile_view;
+    DevBuf<DevCam> cams;
+    DevBuf<int> tile_view, tile_count, tile_offsets, cursor, entries, overflow, overflow_count, err;
+    DevBuf<long long> total;
+    DevBuf<float4> rec;
+    DevBuf<unsigned long long> keys;
+    DevBuf<short4> rect;
+    DevBuf<float> image, trans, gt;
+    DevBuf<int> contrib, last;
+    DevBuf<double> sse_tile, sse_view;
+    bool rendered = false, has_gt = false;
+
+    explicit Batch(Context* c) : ctx(c) {}
+
+    void prepare(const Scene& s, const std::vector<slm_camera>& cv) {
+        ctx->activate();
+        cudaStream_t st = ctx->stream;
+        V = static_cast<int>(cv.size());
+        G = s.G;
+        Gp = s.Gp;
+        hcams.assign(V, DevCam{});
+        htile_view.clear();
+        n_tiles = 0;
+        n_pix = 0;
+        for (int v = 0; v < V; ++v) {
+            const slm_camera& c = cv[v];
+            if (c.width <= 0 || c.height <= 0) throw std::invalid_argument("camera size must be positive");
+            if (c.width > 32767 * kTile || c.height > 32767 * kTile) throw std::invalid_argument("camera too large");
+            DevCam& d = hcams[v];
+            std::memcpy(d.R, c.world_to_cam, sizeof d.R);
+            std::memcpy(d.t, c.translation, sizeof d.t);
+            d.fx = c.fx;
+            d.fy = c.fy;
+            d.cx = c.cx;
+            d.cy = c.cy;
+            d.near_clip = c.near_clip;
+            d.width = c.width;
+            d.height = c.height;
+            d.tiles_x = (c.width + kTile - 1) / kTile;
+            d.tiles_y = (c.height + kTile - 1) / kTile;
+            d.tile_base = n_tiles;
+            d.pix_base = n_pix;
+            n_tiles += d.tiles_x * d.tiles_y;
+            n_pix += static_cast<long long>(c.width) * c.height;
+            htile_view.insert(htile_view.end(), d.tiles_x * d.tiles_y, v);
+        }
+        cams.ensure(std::max(V, 1));
+        tile_view.ensure(std::max(n_tiles, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(cams.p, hcams.data(), sizeof(DevCam) * V, cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(tile_view.p, htile_view.data(), sizeof(int) * n_tiles, cudaMemcpyHostToDevice, st));
+        const size_t VG = static_cast<size_t>(V) * Gp;
+        rec.ensure(3 * VG);
+        keys.ensure(VG);
+        rect.ensure(VG);
+        tile_count.ensure(n_tiles + 1);
+        tile_offsets.ensure(n_tiles + 1);
+        cursor.ensure(n_tiles + 1);
+        total.ensure(1);
+        err.ensure(2);
+        overflow.ensure(n_tiles + 1);
+        overflow_count.ensure(1);
+        SLM_CUDA_CHECK(cudaMemsetAsync(tile_count.p, 0, sizeof(int) * (n_tiles + 1), st));
+        SLM_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int) * 2, st));
+        SLM_CUDA_CHECK(cudaMemsetAsync(overflow_count.p, 0, sizeof(int), st));
+        launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p, tile_count.p, err.p, st);
+        launch_scan_tiles(tile_count.p, n_tiles, tile_offsets.p, cursor.p, total.p, st);
+        ctx->check_launch();
+        long long hdr[2];
+        int herr = 0;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+        if (herr) throw std::domain_error("zero-norm quaternion");
+        n_entries = hdr[0];
+        if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
+        entries.ensure(std::max<long long>(n_entries, 1));
+        launch_bin_scatter(G, Gp, V, cams.p, rect.p, cursor.p, entries.p, st);
+        launch_tile_sort(tile_offsets.p, entries.p, keys.p, tile_view.p, n_tiles, Gp, overflow.p,
+                         overflow_count.p, st);
+        ctx->check_launch();
+        rendered = false;
+        has_gt = false;
+    }
+
+    // Forward render of every pixel of every view (K6); gt (concatenated f32
+    // H*W*3 per view, device) enables the per-view SSE.
+    void render(bool with_gt) {
+        cudaStream_t st = ctx->stream;
+        image.ensure(3 * std::max<long long>(n_pix, 1));
+        trans.ensure(std::max<long long>(n_pix, 1));
+        contrib.ensure(std::max<long long>(n_pix, 1));
+        last.ensure(std::max<long long>(n_pix, 1));
+        sse_tile.ensure(std::max(n_tiles, 1));
+        sse_view.ensure(std::max(V, 1));
+        launch_render(cams.p, tile_view.p, n_tiles, tile_offsets.p, entries.p, rec.p, Gp,
+                      with_gt ? gt.p : nullptr, image.p, trans.p, contrib.p, last.p,
+                      with_gt ? sse_tile.p : nullptr, st);
+        if (with_gt) launch_sse_views(cams.p, V, n_tiles, sse_tile.p, sse_view.p, st);
+        ctx->check_launch();
+        rendered = true;
+        has_gt = with_gt;
+    }
+
+    std::vector<double> view_sse() {
+        std::vector<double> h(V);
+        if (V == 0) return h;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.data(), sse_view.p, sizeof(double) * V, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        return h;
+    }
+};
+
+// =========================================================================== Samples
+// A plan laid out for the warp-per-group raster: per view, samples grouped
+// by tile in chunks of <= 32 (the reference emits them tile-major already,
+// sample_plan.cpp:96-168, so this is a no-op permutation for its plans).
+struct Samples {
+    std::vector<Group> hgroups;
+    DevBuf<Group> groups;
+    DevBuf<int> spix, sorig;
+    DevBuf<float> sw;
+    std::vector<int> order;  // group order -> plan sample index
+    long long total = 0;
+
+    void build(Context* ctx, const slm_plan& plan, int view_lo, int view_hi,
+               const std::vector<DevCam>& cams, const std::vector<double>& weights3) {
+        hgroups.clear();
+        order.clear();
+        for (int v = view_lo; v < view_hi; ++v) {
+            const DevCam& c = cams[v - view_lo];
+            const long long a = plan.view_offset[v], b = plan.view_offset[v + 1];
+            std::vector<int> idx(b - a);
+            std::iota(idx.begin(), idx.end(), static_cast<int>(a));
+            for (int s : idx) {
+                if (plan.px[s] < 0 || plan.px[s] >= c.width || plan.py[s] < 0 || plan.py[s] >= c.height)
+                    throw std::invalid_argument("sample pixel outside the camera");
+                if (plan.tile[s] < 0 || plan.tile[s] >= c.tiles_x * c.tiles_y)
+                    throw std::invalid_argument("sample tile outside the camera");
+            }
+            std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return plan.tile[x] < plan.tile[y]; });
+            size_t i = 0;
+            while (i < idx.size()) {
+                const int t = plan.tile[idx[i]];
+                size_t j = i;
+                while (j < idx.size() && plan.tile[idx[j]] == t && j - i < 32) ++j;
+                hgroups.push_back(Group{v - view_lo, t, static_cast<int>(order.size()), static_cast<int>(j - i)});
+                for (size_t k = i; k < j; ++k) order.push_back(idx[k]);
+                i = j;
+            }
+        }
+        total = static_cast<long long>(order.size());
+        std::vector<int> hpix(order.size()), horig(order.size());
+        std::vector<float> hw(3 * order.size());
+        for (size_t k = 0; k < order.size(); ++k) {
+            const int s = order[k];
+            hpix[k] = plan.px[s] | (plan.py[s] << 16);
+            horig[k] = s - static_cast<int>(plan.view_offset[view_lo]);
+            for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(s) + c]);
+        }
+        cudaStream_t st = ctx->stream;
+        groups.ensure(std::max<size_t>(hgroups.size(), 1));
+        spix.ensure(std::max<size_t>(order.size(), 1));
+        sorig.ensure(std::max<size_t>(order.size(), 1));
+        sw.ensure(std::max<size_t>(3 * order.size(), 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(groups.p, hgroups.data(), sizeof(Group) * hgroups.size(), cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(spix.p, hpix.data(), sizeof(int) * hpix.size(), cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(sorig.p, horig.data(), sizeof(int) * horig.size(), cudaMemcpyHostToDevice, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, st));
+        ctx->sync();  // host staging vectors go out of scope
+    }
+
+    void upload_weights(Context* ctx, const std::vector<double>& weights3, long long plan_base) {
+        std::vector<float> hw(3 * order.size());
+        for (size_t k = 0; k < order.size(); ++k)
+            for (int c = 0; c < 3; ++c)
+                hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(order[k] - plan_base) + c]);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->sync();
+    }
+};
+
+// =========================================================================== Jacobian
+struct Jacobian {
+    Context* ctx;
+    Scene* scene;                    // parameters (owned or borrowed)
+    std::unique_ptr<Scene> own_scene;
+    Batch* batch;
+    std::unique_ptr<Batch> own_batch;
+    Samples samples;
+    std::vector<double> weights;     // (1/q)/N_total per residual, (view, sample, channel)
+    long long rdim = 0, plan_base = 0;
+    DevBuf<float4> tan;
+    DevBuf<float> inter, diagacc, vin, vout, res_in, res_out;
+    DevBuf<double> host_stage;
+    DevBuf<float> r, z, p, u;
+
+    Jacobian(Context* c, Scene* s, Batch* b) : ctx(c), scene(s), batch(b) {}
+
+    // plan views [lo, hi) are this rank's; the weights use the global N_total.
+    void init(const slm_plan& plan, int lo, int hi, double inv_total) {
+        rdim = 0;
+        plan_base = plan.view_offset[lo];
+        for (int v = lo; v < hi; ++v) rdim += 3 * (plan.view_offset[v + 1] - plan.view_offset[v]);
+        weights.resize(rdim);
+        for (long long s = plan.view_offset[lo], k = 0; s < plan.view_offset[hi]; ++s, ++k)
+            for (int c = 0; c < 3; ++c) weights[3 * k + c] = plan.weight[s] * inv_total;
+        std::vector<double> w_by_plan(3 * static_cast<size_t>(plan.view_offset[hi]), 0.0);
+        std::copy(weights.begin(), weights.end(), w_by_plan.begin() + 3 * plan_base);
+        samples.build(ctx, plan, lo, hi, batch->hcams, w_by_plan);
+        const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
+        tan.ensure(3 * VG);
+        inter.ensure(VG * kRec);
+        diagacc.ensure(VG * kDiagRec);
+        SLM_CUDA_CHECK(cudaMemsetAsync(inter.p, 0, VG * kRec * sizeof(float), ctx->stream));
+        SLM_CUDA_CHECK(cudaMemsetAsync(diagacc.p, 0, VG * kDiagRec * sizeof(float), ctx->stream));
+        SLM_CUDA_CHECK(cudaMemsetAsync(tan.p, 0, 3 * VG * sizeof(float4), ctx->stream));
+    }
+
+    SampleArgs args() const {
+        SampleArgs a{};
+        a.groups = samples.groups.p;
+        a.n_groups = static_cast<int>(samples.hgroups.size());
+        a.cams = batch->cams.p;
+        a.tile_offsets = batch->tile_offsets.p;
+        a.entries = batch->entries.p;
+        a.rec = batch->rec.p;
+        a.tan = tan.p;
+        a.Gp = scene->Gp;
+        a.spix = samples.spix.p;
+        a.sorig = samples.sorig.p;
+        a.sw = samples.sw.p;
+        a.image = batch->image.p;
+        a.last_img = batch->last.p;
+        a.gt = batch->gt.p;
+        a.inter = inter.p;
+        return a;
+    }
+
+    size_t P() const { return scene->P(); }
+
+    // out = J^T W J p + lambda p, device f32 SoA; allreduced across ranks.
+    void gn_apply_dev(float lambda, const float* dp, float* dout, const int* done = nullptr) {
+        cudaStream_t st = ctx->stream;
+        launch_tangents(scene->beta.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                        tan.p, done, st);
+        SampleArgs a = args();
+        a.done_flag = done;
+        launch_sample_raster(kGn, a, st);
+        if (ctx->world > 1) {
+            launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                         inter.p, nullptr, 0.f, dout, done, st);
+            ctx->allreduce(dout, P());
+            launch_axpy(dout, dp, static_cast<long long>(P()), lambda, st);
+        } else {
+            launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                         inter.p, dp, lambda, dout, done, st);
+        }
+        ctx->check_launch();
+    }
+
+    // b = J^T(-W r), r = render - truth at the samples (lm.cpp:99-121)
+    void rhs_dev(float* dout) {
+        launch_sample_raster(kRhs, args(), ctx->stream);
+        launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                     inter.p, nullptr, 0.f, dout, nullptr, ctx->stream);
+        ctx->check_launch();
+    }
+
+    void diag_dev(float* dout) {
+        DiagArgs d{};
+        d.groups = samples.groups.p;
+        d.n_groups = static_cast<int>(samples.hgroups.size());
+        d.cams = batch->cams.p;
+        d.tile_offsets = batch->tile_offsets.p;
+        d.entries = batch->entries.p;
+        d.rec = batch->rec.p;
+        d.Gp = scene->Gp;
+        d.spix = samples.spix.p;
+        d.sw = samples.sw.p;
+        d.image = batch->image.p;
+        d.last_img = batch->last.p;
+        d.diagacc = diagacc.p;
+        launch_diag_raster(d, ctx->stream);
+        launch_diag_finalize(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V,
+                             batch->rec.p, diagacc.p, dout, ctx->stream);
+        ctx->check_launch();
+    }
+
+    // ---- host-vector API (drop-in SampledJacobian methods)
+    void upload_param(const double* h, float* d) {
+        const int G = scene->G;
+        host_stage.ensure(std::max<size_t>(static_cast<size_t>(kP) * G, 1));
+        SLM_CUDA_CHECK(cudaMemsetAsync(d, 0, P() * sizeof(float), ctx->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(host_stage.p, h, sizeof(double) * kP * G, cudaMemcpyHostToDevice, ctx->stream));
+        launch_aos64_to_soa32(host_stage.p, G, scene->Gp, d, ctx->stream);
+    }
+    void download_param(const float* d, double* h) {
+        const int G = scene->G;
+        host_stage.ensure(std::max<size_t>(static_cast<size_t>(kP) * G, 1));
+        launch_soa32_to_aos64(d, G, scene->Gp, host_stage.p, ctx->stream);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h, host_stage.p, sizeof(double) * kP * G, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+    }
+
+    void jvp(const double* v, double* out) {
+        vin.ensure(P());
+        res_out.ensure(std::max<long long>(rdim, 1));
+        upload_param(v, vin.p);
+        launch_tangents(scene->beta.p, vin.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                        tan.p, nullptr, ctx->stream);
+        SampleArgs a = args();
+        a.out_res = res_out.p;
+        launch_sample_raster(kJvp, a, ctx->stream);
+        ctx->check_launch();
+        std::vector<float> h(rdim);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h.data(), res_out.p, sizeof(float) * rdim, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        for (long long i = 0; i < rdim; ++i) out[i] = h[i];
+    }
+
+    void vjp(const double* uvec, double* out) {
+        std::vector<float> h(rdim);
+        for (long long i = 0; i < rdim; ++i) h[i] = static_cast<float>(uvec[i]);
+        res_in.ensure(std::max<long long>(rdim, 1));
+        vout.ensure(P());
+        SLM_CUDA_CHECK(cudaMemcpyAsync(res_in.p, h.data(), sizeof(float) * rdim, cudaMemcpyHostToDevice, ctx->stream));
+        SampleArgs a = args();
+        a.in_res = res_in.p;
+        launch_sample_raster(kVjp, a, ctx->stream);
+        launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+                     nullptr, 0.f, vout.p, nullptr, ctx->stream);
+        ctx->check_launch();
+        download_param(vout.p, out);
+    }
+
+    void jtj_diag(double* out) {
+        vout.ensure(P());
+        diag_dev(vout.p);
+        download_param(vout.p, out);
+    }
+
+    void gn_apply(double lambda, const double* pvec, double* out) {
+        vin.ensure(P());
+        vout.ensure(P());
+        upload_param(pvec, vin.p);
+        gn_apply_dev(static_cast<float>(lambda), vin.p, vout.p);
+        download_param(vout.p, out);
+    }
+
+    // pcg_solve (pcg.cpp:10-53) on device; returns the final CgState.
+    CgState pcg_dev(float lambda, const float* b, const float* minv, int iters, float* x) {
+        const size_t n = P();
+        r.ensure(n);
+        z.ensure(n);
+        p.ensure(n);
+        u.ensure(n);
+        SLM_CUDA_CHECK(cudaMemsetAsync(u.p, 0, n * sizeof(float), ctx->stream));
+        CgState* cg = ctx->cg.p;
+        launch_cg_init(b, minv, static_cast<long long>(n), x, r.p, z.p, p.p, ctx->partial.p, cg, ctx->stream);
+        for (int it = 0; it < iters; ++it) {
+            gn_apply_dev(lambda, p.p, u.p, &cg->done);
+            launch_cg_pu(p.p, u.p, static_cast<long long>(n), ctx->partial.p, cg, ctx->stream);
+            launch_cg_update(x, r.p, z.p, p.p, u.p, minv, static_cast<long long>(n), ctx->partial.p, cg, ctx->stream);
+        }
+        ctx->check_launch();
+        CgState h;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(&h, cg, sizeof(CgState), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        return h;
+    }
+};
+
+// =========================================================================== host samplers
+// build_sample_plan (sample_plan.cpp:62-171) with libstdc++'s distributions.
+struct PlanH {
+    std::vector<int> view_camera;
+    std::vector<int64_t> view_offset{0};
+    std::vector<int> px, py, tile;
+    std::vector<double> weight;
+    int samples_per_tile = 0, dist = SLM_DIST_UNIFORM;
+    slm_plan view() const {
+        return slm_plan{static_cast<int32_t>(view_camera.size()), samples_per_tile, dist,
+                        view_camera.data(), view_offset.data(), px.data(), py.data(), tile.data(),
+                        weight.data()};
+    }
+};
+
+static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int spt, int dist, int lane,
+                                         std::mt19937_64& rng, const double* const* aux_image,
+                                         const int32_t* const* aux_contrib, const double* const* aux_gt) {
+    if (spt < 1) throw std::invalid_argument("samples_per_tile must be positive");
+    if (spt > kTile * kTile) throw std::invalid_argument("samples_per_tile exceeds the pixels in a tile");
+    if (lane < 1 || spt % lane != 0)
+        throw std::invalid_argument("samples_per_tile must be a multiple of the lane width");
+    if (dist != SLM_DIST_UNIFORM) {
+        if (!aux_image || !aux_contrib) throw std::invalid_argument("weighted distributions need per-camera aux data");
+        if (dist == SLM_DIST_RESIDUAL && !aux_gt)
+            throw std::invalid_argument("residual distribution needs ground-truth images");
+    }
+    auto plan = std::make_unique<PlanH>();
+    plan->samples_per_tile = spt;
+    plan->dist = dist;
+    size_t total = 0;
+    for (int ci = 0; ci < n_cams; ++ci) {
+        const int txn = (cams[ci].width + kTile - 1) / kTile, tyn = (cams[ci].height + kTile - 1) / kTile;
+        for (int ty = 0; ty < tyn; ++ty)
+            for (int tx = 0; tx < txn; ++tx) {
+                const int w = std::min(cams[ci].width - tx * kTile, kTile);
+                const int h = std::min(cams[ci].height - ty * kTile, kTile);
+                total += std::min(spt, w * h);
+            }
+    }
+    const double n_total = static_cast<double>(total);
+    plan->px.reserve(total);
+    plan->py.reserve(total);
+    plan->tile.reserve(total);
+    plan->weight.reserve(total);
+    std::vector<int> pool;
+    std::vector<double> density, cdf;
+    for (int ci = 0; ci < n_cams; ++ci) {
+        const slm_camera& cam = cams[ci];
+        const int txn = (cam.width + kTile - 1) / kTile, tyn = (cam.height + kTile - 1) / kTile;
+        plan->view_camera.push_back(ci);
+        for (int ty = 0; ty < tyn; ++ty)
+            for (int tx = 0; tx < txn; ++tx) {
+                const int x0 = tx * kTile, y0 = ty * kTile;
+                const int rw = std::min(cam.width - x0, kTile), rh = std::min(cam.height - y0, kTile);
+                const int m = rw * rh, n = std::min(spt, m), tile = ty * txn + tx;
+                auto emit = [&](int local, double q_tile) {
+                    plan->px.push_back(x0 + local % rw);
+                    plan->py.push_back(y0 + local / rw);
+                    plan->tile.push_back(tile);
+                    const double q = (n / n_total) * q_tile;
+                    plan->weight.push_back(1.0 / std::max(q, 1e-12));
+                };
+                if (dist == SLM_DIST_UNIFORM) {
+                    pool.resize(m);
+                    std::iota(pool.begin(), pool.end(), 0);
+                    for (int i = 0; i < n; ++i) {
+                        std::uniform_int_distribution<int> d(i, m - 1);
+                        std::swap(pool[i], pool[d(rng)]);
+                    }
+                    for (int i = 0; i < n; ++i) emit(pool[i], 1.0 / m);
+                    continue;
+                }
+                density.assign(m, 0.0);
+                if (dist == SLM_DIST_RESIDUAL) {
+                    double vmax = -1.0;
+                    for (int l = 0; l < m; ++l) {
+                        const size_t pix = static_cast<size_t>(y0 + l / rw) * cam.width + x0 + l % rw;
+                        double v = 0.0;
+                        for (int c = 0; c < 3; ++c) v += std::abs(aux_image[ci][3 * pix + c] - aux_gt[ci][3 * pix + c]);
+                        density[l] = v / 3.0;
+                        vmax = std::max(vmax, density[l]);
+                    }
+                    double sum = 0.0;
+                    for (double& v : density) sum += (v = std::exp(v - vmax));
+                    for (double& v : density) v /= sum;
+                } else {
+                    double sum = 0.0;
+                    for (int l = 0; l < m; ++l) {
+                        const size_t pix = static_cast<size_t>(y0 + l / rw) * cam.width + x0 + l % rw;
+                        sum += (density[l] = 1.0 + aux_contrib[ci][pix]);
+                    }
+                    for (double& v : density) v /= sum;
+                }
+                cdf.resize(m);
+                std::partial_sum(density.begin(), density.end(), cdf.begin());
+                for (int k = 0; k < n; ++k) {
+                    std::uniform_real_distribution<double> uni(0.0, 1.0);
+                    const double uu = uni(rng) * cdf.back();
+                    const auto it = std::upper_bound(cdf.begin(), cdf.end(), uu);
+                    const int local = std::min<int>(static_cast<int>(it - cdf.begin()), m - 1);
+                    emit(local, density[local]);
+                }
+            }
+        plan->view_offset.push_back(static_cast<int64_t>(plan->px.size()));
+    }
+    return plan;
+}
+
+static std::unique_ptr<PlanH> exhaustive(const slm_camera* cams, int n_cams) {  // :173-197
+    auto plan = std::make_unique<PlanH>();
+    plan->samples_per_tile = kTile * kTile;
+    double n_total = 0;
+    for (int i = 0; i < n_cams; ++i) n_total += static_cast<double>(cams[i].width) * cams[i].height;
+    for (int ci = 0; ci < n_cams; ++ci) {
+        const int txn = (cams[ci].width + kTile - 1) / kTile;
+        plan->view_camera.push_back(ci);
+        for (int y = 0; y < cams[ci].height; ++y)
+            for (int x = 0; x < cams[ci].width; ++x) {
+                plan->px.push_back(x);
+                plan->py.push_back(y);
+                plan->tile.push_back((y / kTile) * txn + x / kTile);
+                plan->weight.push_back(n_total);
+            }
+        plan->view_offset.push_back(static_cast<int64_t>(plan->px.size()));
+    }
+    return plan;
+}
+
+// camera_features / kmeans_cameras / sample_view_batch (view_sampler.cpp:10-184)
+static std::vector<std::array<double, 6>> features(const slm_camera* cams, int n) {
+    std::vector<std::array<double, 6>> f(n);
+    if (n == 0) return f;
+    double lo[3], hi[3];
+    for (int i = 0; i < 3; ++i) {
+        lo[i] = std::numeric_limits<double>::max();
+        hi[i] = std::numeric_limits<double>::lowest();
+    }
+    std::vector<std::array<double, 3>> pos(n);
+    for (int c = 0; c < n; ++c) {
+        const double* r = cams[c].world_to_cam;
+        const double* t = cams[c].translation;
+        pos[c] = {-(r[0] * t[0] + r[3] * t[1] + r[6] * t[2]), -(r[1] * t[0] + r[4] * t[1] + r[7] * t[2]),
+                  -(r[2] * t[0] + r[5] * t[1] + r[8] * t[2])};
+        for (int i = 0; i < 3; ++i) {
+            lo[i] = std::min(lo[i], pos[c][i]);
+            hi[i] = std::max(hi[i], pos[c][i]);
+        }
+    }
+    for (int c = 0; c < n; ++c) {
+        for (int i = 0; i < 3; ++i) {
+            const double ext = hi[i] - lo[i];
+            f[c][i] = ext > 1e-12 ? (pos[c][i] - lo[i]) / ext : 0.5;
+        }
+        for (int i = 0; i < 3; ++i) f[c][3 + i] = cams[c].world_to_cam[6 + i];
+    }
+    return f;
+}
+
+static double dist6(const std::array<double, 6>& a, const std::array<double, 6>& b) {
+    double acc = 0.0;
+    for (int i = 0; i < 6; ++i) {
+        const double d = a[i] - b[i];
+        acc += d * d;
+    }
+    return acc;
+}
+
+static std::vector<int> kmeans(const std::vector<std::array<double, 6>>& f, int k, uint64_t seed) {
+    const int n = static_cast<int>(f.size());
+    if (k < 1) throw std::invalid_argument("cluster count must be at least 1");
+    if (k > n) throw std::invalid_argument("cluster count exceeds camera count");
+    std::mt19937_64 rng(seed);
+    std::vector<std::array<double, 6>> cen;
+    std::vector<bool> chosen(n, false);
+    std::uniform_int_distribution<int> first(0, n - 1);
+    const int idx = first(rng);
+    cen.push_back(f[idx]);
+    chosen[idx] = true;
+    std::vector<double> d2(n);
+    while (static_cast<int>(cen.size()) < k) {  // k-means++ seeding (:55-97)
+        double total = 0.0;
+        for (int i = 0; i < n; ++i) {
+            d2[i] = std::numeric_limits<double>::max();
+            for (const auto& c : cen) d2[i] = std::min(d2[i], dist6(f[i], c));
+            if (chosen[i]) d2[i] = 0.0;
+            total += d2[i];
+        }
+        int pick = -1;
+        if (total > 0.0) {
+            std::uniform_real_distribution<double> uni(0.0, total);
+            double uu = uni(rng);
+            for (int i = 0; i < n; ++i) {
+                uu -= d2[i];
+                if (uu <= 0.0) {
+                    pick = i;
+                    break;
+                }
+            }
+            if (pick < 0) pick = n - 1;
+        }
+        if (pick < 0 || chosen[pick])
+            pick = static_cast<int>(std::find(chosen.begin(), chosen.end(), false) - chosen.begin());
+        cen.push_back(f[pick]);
+        chosen[pick] = true;
+    }
+    std::vector<int> assign(n, -1);
+    for (int iter = 0; iter < 100; ++iter) {  // Lloyd (:101-171)
+        bool changed = false;
+        for (int i = 0; i < n; ++i) {
+            int best = 0;
+            double bd = dist6(f[i], cen[0]);
+            for (int c = 1; c < k; ++c) {
+                const double d = dist6(f[i], cen[c]);
+                if (d < bd) {
+                    bd = d;
+                    best = c;
+                }
+            }
+            if (assign[i] != best) {
+                assign[i] = best;
+                changed = true;
+            }
+        }
+        std::vector<int> sizes(k, 0);
+        for (int a : assign) ++sizes[a];
+        for (int c = 0; c < k; ++c) {
+            if (sizes[c] > 0) continue;
+            int far = -1;
+            double far_d = -1.0;
+            for (int i = 0; i < n; ++i) {
+                if (sizes[assign[i]] <= 1) continue;
+                const double d = dist6(f[i], cen[assign[i]]);
+                if (d > far_d) {
+                    far_d = d;
+                    far = i;
+                }
+            }
+            if (far < 0) continue;
+            --sizes[assign[far]];
+            assign[far] = c;
+            ++sizes[c];
+            cen[c] = f[far];
+            changed = true;
+        }
+        for (int c = 0; c < k; ++c) {
+            std::array<double, 6> mean{};
+            int count = 0;
+            for (int i = 0; i < n; ++i) {
+                if (assign[i] != c) continue;
+                for (int d = 0; d < 6; ++d) mean[d] += f[i][d];
+                ++count;
+            }
+            if (count > 0)
+                for (int d = 0; d < 6; ++d) cen[c][d] = mean[d] / count;
+        }
+        if (!changed) break;
+    }
+    return assign;
+}
+
+static std::vector<int> view_batch(const std::vector<int>& assign, int k, std::mt19937_64& rng) {
+    if (k < 1) throw std::invalid_argument("no clusters to sample from");
+    std::vector<std::vector<int>> cl(k);
+    for (size_t i = 0; i < assign.size(); ++i) {
+        if (assign[i] < 0 || assign[i] >= k) throw std::invalid_argument("cluster index out of range");
+        cl[assign[i]].push_back(static_cast<int>(i));
+    }
+    std::vector<int> batch;
+    for (const auto& c : cl) {
+        if (c.empty()) throw std::invalid_argument("empty cluster in batch sampler");
+        std::uniform_int_distribution<size_t> d(0, c.size() - 1);
+        batch.push_back(c[d(rng)]);
+    }
+    return batch;
+}
+
+// =========================================================================== TrainData + lm_step
+struct Train {
+    Context* ctx;
+    std::vector<slm_camera> cams;
+    std::vector<size_t> img_off;
+    DevBuf<float> images;
+    std::vector<int> assign;
+    int k = 0;
+};
+
+static double learning_rate_from(double m, int iteration, const slm_lm_config& cfg) {  // lm.cpp:26-37
+    if (iteration < cfg.warmup_iterations) return cfg.warmup_lr;
+    if (m > 1.0) return std::min(cfg.lr_cap, 1.0 / m);
+    return std::min(cfg.lr_cap, 1.0);
+}
+
+static void copy_gt(Train& t, Batch& b, const std::vector<int>& cam_ids) {
+    b.gt.ensure(3 * std::max<long long>(b.n_pix, 1));
+    for (size_t v = 0; v < cam_ids.size(); ++v) {
+        const slm_camera& c = t.cams[cam_ids[v]];
+        SLM_CUDA_CHECK(cudaMemcpyAsync(b.gt.p + 3 * b.hcams[v].pix_base, t.images.p + t.img_off[cam_ids[v]],
+                                       sizeof(float) * 3 * c.width * c.height, cudaMemcpyDeviceToDevice,
+                                       b.ctx->stream));
+    }
+}
+
+struct StepBuffers {  // per-context persistent lm_step workspace (no per-step cudaMalloc)
+    Batch batch;
+    Jacobian jac;
+    DevBuf<float> b, x, maxabs;
+    explicit StepBuffers(Context* c) : batch(c), jac(c, nullptr, &batch) {}
+};
+
+void destroy_step(StepBuffers* s) { delete s; }
+
+static StepBuffers& step_buffers(Context* ctx) {
+    if (!ctx->step) ctx->step = new StepBuffers(ctx);
+    return *ctx->step;
+}
+
+static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration, std::mt19937_64& rng,
+                    slm_step_report& rep) {
+    Context* ctx = s.ctx;
+    ctx->activate();
+    if (t.k < 1) throw std::invalid_argument("lm_step: no view clusters");
+    if (cfg.loss != SLM_LOSS_MSE)
+        throw std::invalid_argument("lm_step: only the mse loss is on the B200 path (mse+ssim is out of scope)");
+    ctx->mark("start");
+    rep.iteration = iteration;
+    // 1. view batch (lm.cpp:63)
+    const std::vector<int> batch = view_batch(t.assign, t.k, rng);
+    const int VB = static_cast<int>(batch.size());
+    const int lo = static_cast<int>(static_cast<long long>(VB) * ctx->rank / ctx->world);
+    const int hi = static_cast<int>(static_cast<long long>(VB) * (ctx->rank + 1) / ctx->world);
+    std::vector<slm_camera> all_cams, my_cams;
+    std::vector<int> my_ids;
+    for (int i = 0; i < VB; ++i) all_cams.push_back(t.cams[batch[i]]);
+    for (int i = lo; i < hi; ++i) {
+        my_cams.push_back(t.cams[batch[i]]);
+        my_ids.push_back(batch[i]);
+    }
+    // 2./3. forward render + residual fields of this rank's views (lm.cpp:75-78)
+    StepBuffers& sb = step_buffers(ctx);
+    Batch& B = sb.batch;
+    B.prepare(s, my_cams);
+    copy_gt(t, B, my_ids);
+    B.render(true);
+    ctx->mark("prepare+render");
+    // 4. plan for the whole batch; every rank replays the same RNG stream
+    std::vector<std::vector<double>> aux_img;
+    std::vector<std::vector<int32_t>> aux_cn;
+    std::vector<std::vector<double>> aux_gt;
+    std::vector<const double*> pi, pg;
+    std::vector<const int32_t*> pc;
+    if (cfg.dist != SLM_DIST_UNIFORM) {
+        if (ctx->world > 1)
+            throw std::invalid_argument("weighted residual distributions are single-rank only on the B200 path");
+        for (int v = 0; v < VB; ++v) {
+            const size_t np = static_cast<size_t>(all_cams[v].width) * all_cams[v].height;
+            std::vector<float> fi(3 * np), fg(3 * np);
+            aux_cn.emplace_back(np);
+            SLM_CUDA_CHECK(cudaMemcpyAsync(fi.data(), B.image.p + 3 * B.hcams[v].pix_base, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, ctx->stream));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(fg.data(), B.gt.p + 3 * B.hcams[v].pix_base, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, ctx->stream));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(aux_cn.back().data(), B.contrib.p + B.hcams[v].pix_base, sizeof(int) * np, cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->sync();
+            aux_img.emplace_back(fi.begin(), fi.end());
+            aux_gt.emplace_back(fg.begin(), fg.end());
+        }
+        for (int v = 0; v < VB; ++v) {
+            pi.push_back(aux_img[v].data());
+            pc.push_back(aux_cn[v].data());
+            pg.push_back(aux_gt[v].data());
+        }
+    }
+    const auto plan = build_plan(all_cams.data(), VB, cfg.samples_per_tile, cfg.dist, cfg.sample_lane_width, rng,
+                                 pi.empty() ? nullptr : pi.data(), pc.empty() ? nullptr : pc.data(),
+                                 pg.empty() ? nullptr : pg.data());
+    const slm_plan pv = plan->view();
+    const long long total = plan->view_offset.back();
+    const double inv_total = total > 0 ? 1.0 / static_cast<double>(total) : 0.0;
+    // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
+    double before = 0.0;
+    {
+        const auto sse = B.view_sse();
+        for (int v = 0; v < B.V; ++v)
+            before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
+    }
+    Jacobian& J = sb.jac;
+    J.scene = &s;
+    J.init(pv, lo, hi, inv_total);
+    ctx->mark("plan");
+    const size_t P = s.P();
+    sb.b.ensure(2 * P);  // [b | diag] contiguous for one fused allreduce
+    sb.x.ensure(P);
+    sb.maxabs.ensure(1);
+    float* db = sb.b.p;
+    float* dd = sb.b.p + P;
+    SLM_CUDA_CHECK(cudaMemsetAsync(sb.b.p, 0, 2 * P * sizeof(float), ctx->stream));
+    // 5. b = J^T(-W r) and diag(J^T W J) (lm.cpp:121-125)
+    J.rhs_dev(db);
+    ctx->mark("rhs");
+    J.diag_dev(dd);
+    ctx->allreduce(sb.b.p, 2 * P);
+    launch_minv(dd, static_cast<long long>(P), static_cast<float>(cfg.damping), ctx->stream);
+    ctx->mark("diag");
+    // 7. PCG (lm.cpp:128-132)
+    const int iters = iteration >= cfg.pcg_switch_iteration ? cfg.pcg_iters_late : cfg.pcg_iters_initial;
+    const CgState cs = J.pcg_dev(static_cast<float>(cfg.damping), db, dd, iters, sb.x.p);
+    rep.pcg_iterations = cs.iterations;
+    rep.breakdown = cs.breakdown;
+    ctx->mark("pcg");
+    // 8./9./10. learning rate and update (lm.cpp:135-137)
+    launch_color_maxabs(sb.x.p, s.G, s.Gp, sb.maxabs.p, ctx->stream);
+    float m = 0.f;
+    SLM_CUDA_CHECK(cudaMemcpyAsync(&m, sb.maxabs.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+    rep.eta = learning_rate_from(static_cast<double>(m), iteration, cfg);
+    if (cs.breakdown) rep.eta *= 0.5;
+    launch_apply_update(s.beta.p, sb.x.p, s.G, s.Gp, rep.eta, s.beta32.p, ctx->stream);
+    ctx->check_launch();
+    ctx->mark("update");
+    // loss_after = batch_loss of the updated state (lm.cpp:149-153)
+    B.prepare(s, my_cams);
+    B.render(true);
+    double after = 0.0;
+    {
+        const auto sse = B.view_sse();
+        for (int v = 0; v < B.V; ++v) after += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
+    }
+    if (ctx->world > 1) {
+        double h[2] = {before, after};
+        ctx->dscalar.ensure(2);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(ctx->dscalar.p, h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+        ctx->allreduce(ctx->dscalar.p, 2);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(h, ctx->dscalar.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        before = h[0];
+        after = h[1];
+    }
+    ctx->mark("loss_after");
+    ctx->finish_marks();
+    rep.loss_before = before / VB;
+    rep.loss_after = after / VB;
+    rep.batch_size = VB;
+    for (int i = 0; i < VB && i < rep.batch_capacity; ++i) rep.batch[i] = batch[i];
+    if (!std::isfinite(rep.loss_after)) throw std::runtime_error("lm_step: non-finite loss after update");
+}
+
+}  // namespace slm
+
+// =========================================================================== C ABI
+using namespace slm;
+
+struct slm_context { Context impl; explicit slm_context(int d) : impl(d) {} };
+struct slm_scene { Scene impl; slm_scene(Context* c, const slm_gaussians& h) : impl(c, h) {} };
+struct slm_rng { std::mt19937_64 eng; explicit slm_rng(uint64_t s) : eng(s) {} };
+struct slm_plan_h { std::unique_ptr<PlanH> impl; };
+struct slm_train { Train impl; };
+struct slm_jacobian {
+    std::unique_ptr<Scene> scene;
+    std::unique_ptr<Batch> batch;
+    std::unique_ptr<Jacobian> jac;
+};
+
+namespace {
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SLM_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SLM_E_INVALID;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return SLM_E_DOMAIN;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return SLM_E_CUDA;
+    } catch (const NcclError& e) {
+        g_err = e.what();
+        return SLM_E_CUDA;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return SLM_E_RUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SLM_E_RUNTIME;
+    }
+}
+
+Jacobian* make_jacobian(Context* ctx, Scene* scene, const slm_camera* cams, int n_cams, const slm_plan& plan,
+                        slm_jacobian* holder) {
+    std::vector<slm_camera> vc;
+    for (int v = 0; v < plan.n_views; ++v) {
+        if (plan.view_camera[v] < 0 || plan.view_camera[v] >= n_cams)
+            throw std::invalid_argument("sample plan references a camera outside the batch");
+        vc.push_back(cams[plan.view_camera[v]]);
+    }
+    holder->batch = std::make_unique<Batch>(ctx);
+    holder->batch->prepare(*scene, vc);
+    holder->batch->render(false);
+    holder->jac = std::make_unique<Jacobian>(ctx, scene, holder->batch.get());
+    const long long total = plan.view_offset[plan.n_views];
+    holder->jac->init(plan, 0, plan.n_views, total > 0 ? 1.0 / static_cast<double>(total) : 0.0);
+    ctx->sync();
+    return holder->jac.get();
+}
+}  // namespace
+
+extern "C" {
+
+const char* slm_last_error(void) { return g_err.c_str(); }
+int slm_version(void) { return 1; }
+int slm_device_count(int* out) {
+    return guarded([&] { SLM_CUDA_CHECK(cudaGetDeviceCount(out)); });
+}
+
+int slm_context_create(int device, slm_context** out) {
+    *out = nullptr;
+    return guarded([&] { *out = new slm_context(device); });
+}
+int slm_context_destroy(slm_context* ctx) {
+    return guarded([&] { delete ctx; });
+}
+int slm_context_synchronize(slm_context* ctx) {
+    return guarded([&] { ctx->impl.sync(); });
+}
+int slm_context_set_stream(slm_context* ctx, void* stream) {
+    return guarded([&] {
+        Context& c = ctx->impl;
+        if (c.stream && c.own_stream) cudaStreamDestroy(c.stream);
+        c.stream = static_cast<cudaStream_t>(stream);
+        c.own_stream = false;
+    });
+}
+int slm_context_set_timing(slm_context* ctx, int on) {
+    return guarded([&] { ctx->impl.timing = on != 0; });
+}
+int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n) {
+    return guarded([&] {
+        const auto& t = ctx->impl.last_timings;
+        *n = static_cast<int>(t.size());
+        for (int i = 0; i < *n && i < capacity; ++i) out[i] = t[i];
+    });
+}
+long long slm_launch_count(void) { return g_launches.load(); }
+
+int slm_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        ncclUniqueId id;
+        SLM_NCCL_CHECK(nccl().GetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(out, &id, 128);
+    });
+}
+int slm_context_init_comm(slm_context* ctx, const uint8_t id[128], int rank, int world) {
+    return guarded([&] {
+        Context& c = ctx->impl;
+        c.activate();
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
+        if (world > 1) {
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, 128);
+            SLM_NCCL_CHECK(nccl().CommInitRank(&c.comm, world, uid, rank));
+        }
+        c.rank = rank;
+        c.world = world;
+    });
+}
+int slm_context_rank(slm_context* ctx, int* rank, int* world) {
+    *rank = ctx->impl.rank;
+    *world = ctx->impl.world;
+    return SLM_OK;
+}
+
+int slm_rng_create(uint64_t seed, slm_rng** out) {
+    return guarded([&] { *out = new slm_rng(seed); });
+}
+void slm_rng_destroy(slm_rng* rng) { delete rng; }
+uint64_t slm_rng_next(slm_rng* rng) { return rng->eng(); }
+
+int slm_scene_create(slm_context* ctx, const slm_gaussians* host, slm_scene** out) {
+    return guarded([&] {
+        ctx->impl.activate();
+        *out = new slm_scene(&ctx->impl, *host);
+        ctx->impl.sync();
+    });
+}
+void slm_scene_destroy(slm_scene* s) { delete s; }
+int slm_scene_upload(slm_scene* s, const slm_gaussians* host) {
+    return guarded([&] {
+        s->impl.upload(*host);
+        s->impl.ctx->sync();
+    });
+}
+int slm_scene_download(slm_scene* s, slm_gaussians* host) {
+    return guarded([&] { s->impl.download(*host); });
+}
+int slm_scene_count(slm_scene* s, int* count, int* padded) {
+    *count = s->impl.G;
+    *padded = s->impl.Gp;
+    return SLM_OK;
+}
+int slm_scene_apply_update(slm_scene* s, const double* delta_aos, double eta) {
+    return guarded([&] {
+        Scene& sc = s->impl;
+        Context* c = sc.ctx;
+        c->activate();
+        DevBuf<double> d;
+        d.ensure(std::max<size_t>(static_cast<size_t>(kP) * sc.G, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(d.p, delta_aos, sizeof(double) * kP * sc.G, cudaMemcpyHostToDevice, c->stream));
+        launch_apply_update_f64(sc.beta.p, d.p, sc.G, sc.Gp, eta, sc.beta32.p, c->stream);
+        c->check_launch();
+        c->sync();
+    });
+}
+int slm_scene_beta_ptrs(slm_scene* s, double** beta, float** beta32) {
+    *beta = s->impl.beta.p;
+    *beta32 = s->impl.beta32.p;
+    return SLM_OK;
+}
+
+int slm_bin_and_sort(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, int32_t* offsets,
+                     int32_t* indices, int64_t capacity, int64_t* n_entries) {
+    return guarded([&] {
+        Context* c = &ctx->impl;
+        c->activate();
+        Scene s(c, *g);
+        Batch b(c);
+        b.prepare(s, {*cam});
+        *n_entries = b.n_entries;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(offsets, b.tile_offsets.p, sizeof(int) * (b.n_tiles + 1), cudaMemcpyDeviceToHost, c->stream));
+        if (b.n_entries <= capacity)
+            SLM_CUDA_CHECK(cudaMemcpyAsync(indices, b.entries.p, sizeof(int) * b.n_entries, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+    });
+}
+
+int slm_prepare(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, double* mean2d, double* conic,
+                double* opacity, double* color, double* depth, double* radius, int32_t* valid) {
+    return guarded([&] {
+        Context* c = &ctx->impl;
+        c->activate();
+        Scene s(c, *g);
+        Batch b(c);
+        b.prepare(s, {*cam});
+        const int G = s.G;
+        std::vector<float4> rec(3 * static_cast<size_t>(s.Gp));
+        std::vector<unsigned long long> keys(s.Gp);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(rec.data(), b.rec.p, sizeof(float4) * rec.size(), cudaMemcpyDeviceToHost, c->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(keys.data(), b.keys.p, sizeof(unsigned long long) * keys.size(), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        const double ln2 = 0.69314718055994530942;
+        for (int i = 0; i < G; ++i) {
+            const float4 r0 = rec[3 * i], r1 = rec[3 * i + 1], r2 = rec[3 * i + 2];
+            valid[i] = r2.y != 0.f;
+            mean2d[2 * i] = r0.x;
+            mean2d[2 * i + 1] = r0.y;
+            conic[3 * i] = -2.0 * ln2 * r0.z;
+            conic[3 * i + 1] = -ln2 * r0.w;
+            conic[3 * i + 2] = -2.0 * ln2 * r1.x;
+            opacity[i] = r1.y;
+            color[3 * i] = r1.z;
+            color[3 * i + 1] = r1.w;
+            color[3 * i + 2] = r2.x;
+            unsigned long long k = keys[i];
+            k = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+            double d;
+            std::memcpy(&d, &k, sizeof d);
+            depth[i] = d;
+            radius[i] = 0.0;
+        }
+    });
+}
+
+int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, double* image,
+                    double* transmittance, int32_t* contrib) {
+    return guarded([&] {
+        Context* c = &ctx->impl;
+        c->activate();
+        Scene s(c, *g);
+        Batch b(c);
+        b.prepare(s, {*cam});
+        b.render(false);
+        const size_t np = static_cast<size_t>(cam->width) * cam->height;
+        std::vector<float> img(3 * np), tr(np);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(img.data(), b.image.p, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, c->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(tr.data(), b.trans.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
+        if (contrib) SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, b.contrib.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (image) for (size_t i = 0; i < 3 * np; ++i) image[i] = img[i];
+        if (transmittance) for (size_t i = 0; i < np; ++i) transmittance[i] = tr[i];
+    });
+}
+
+int slm_scene_render(slm_scene* s, const slm_camera* cam, float* image, float* transmittance, int32_t* contrib) {
+    return guarded([&] {
+        Context* c = s->impl.ctx;
+        c->activate();
+        Batch b(c);
+        b.prepare(s->impl, {*cam});
+        b.render(false);
+        const size_t np = static_cast<size_t>(cam->width) * cam->height;
+        if (image) SLM_CUDA_CHECK(cudaMemcpyAsync(image, b.image.p, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, c->stream));
+        if (transmittance) SLM_CUDA_CHECK(cudaMemcpyAsync(transmittance, b.trans.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
+        if (contrib) SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, b.contrib.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+    });
+}
+
+int slm_build_sample_plan(const slm_camera* cams, int n_cams, int samples_per_tile, int dist, int lane_width,
+                          slm_rng* rng, const double* const* aux_image, const int32_t* const* aux_contrib,
+                          const double* const* aux_gt, slm_plan_h** out) {
+    return guarded([&] {
+        auto p = build_plan(cams, n_cams, samples_per_tile, dist, lane_width, rng->eng, aux_image, aux_contrib, aux_gt);
+        *out = new slm_plan_h{std::move(p)};
+    });
+}
+int slm_exhaustive_plan(const slm_camera* cams, int n_cams, slm_plan_h** out) {
+    return guarded([&] { *out = new slm_plan_h{exhaustive(cams, n_cams)}; });
+}
+void slm_plan_destroy(slm_plan_h* p) { delete p; }
+int slm_plan_size(slm_plan_h* p, int* n_views, int64_t* total) {
+    *n_views = static_cast<int>(p->impl->view_camera.size());
+    *total = p->impl->view_offset.back();
+    return SLM_OK;
+}
+int slm_plan_export(slm_plan_h* p, int32_t* view_camera, int64_t* view_offset, int32_t* px, int32_t* py,
+                    int32_t* tile, double* weight) {
+    const PlanH& h = *p->impl;
+    std::copy(h.view_camera.begin(), h.view_camera.end(), view_camera);
+    std::copy(h.view_offset.begin(), h.view_offset.end(), view_offset);
+    std::copy(h.px.begin(), h.px.end(), px);
+    std::copy(h.py.begin(), h.py.end(), py);
+    std::copy(h.tile.begin(), h.tile.end(), tile);
+    std::copy(h.weight.begin(), h.weight.end(), weight);
+    return SLM_OK;
+}
+int slm_estimate_loss(const slm_camera* cams, const slm_plan* plan, const double* const* fields, double* out) {
+    return guarded([&] {  // sample_plan.cpp:199-222 (host: O(samples) gather, not on the hot path)
+        const long long n_total = plan->view_offset[plan->n_views];
+        if (n_total == 0) {
+            *out = 0.0;
+            return;
+        }
+        double pixels = 0.0;
+        for (int v = 0; v < plan->n_views; ++v)
+            pixels += static_cast<double>(cams[plan->view_camera[v]].width) * cams[plan->view_camera[v]].height;
+        double acc = 0.0;
+        for (int v = 0; v < plan->n_views; ++v) {
+            const int w = cams[plan->view_camera[v]].width;
+            for (long long s = plan->view_offset[v]; s < plan->view_offset[v + 1]; ++s) {
+                double sq = 0.0;
+                for (int c = 0; c < 3; ++c) {
+                    const double r = fields[v][(static_cast<size_t>(plan->py[s]) * w + plan->px[s]) * 3 + c];
+                    sq += r * r;
+                }
+                acc += plan->weight[s] * sq;
+            }
+        }
+        *out = acc / (static_cast<double>(n_total) * pixels * 3.0);
+    });
+}
+int slm_camera_features(const slm_camera* cams, int n_cams, double* feats) {
+    return guarded([&] {
+        const auto f = features(cams, n_cams);
+        for (int i = 0; i < n_cams; ++i)
+            for (int d = 0; d < 6; ++d) feats[6 * i + d] = f[i][d];
+    });
+}
+int slm_kmeans_cameras(const slm_camera* cams, int n_cams, int k, uint64_t seed, int32_t* assign) {
+    return guarded([&] {
+        const auto a = kmeans(features(cams, n_cams), k, seed);
+        std::copy(a.begin(), a.end(), assign);
+    });
+}
+int slm_sample_view_batch(const int32_t* assign, int n_cams, int k, slm_rng* rng, int32_t* batch) {
+    return guarded([&] {
+        const auto b = view_batch(std::vector<int>(assign, assign + n_cams), k, rng->eng);
+        std::copy(b.begin(), b.end(), batch);
+    });
+}
+
+int slm_jacobian_create(slm_context* ctx, const slm_gaussians* g, const slm_camera* cams, int n_cams,
+                        const slm_plan* plan, slm_jacobian** out) {
+    *out = nullptr;
+    return guarded([&] {
+        Context* c = &ctx->impl;
+        c->activate();
+        auto h = std::make_unique<slm_jacobian>();
+        h->scene = std::make_unique<Scene>(c, *g);  // SampledJacobian copies the set (jacobian.cpp:100)
+        make_jacobian(c, h->scene.get(), cams, n_cams, *plan, h.get());
+        *out = h.release();
+    });
+}
+int slm_jacobian_create_scene(slm_scene* s, const slm_camera* cams, int n_cams, const slm_plan* plan,
+                              slm_jacobian** out) {
+    *out = nullptr;
+    return guarded([&] {
+        auto h = std::make_unique<slm_jacobian>();
+        make_jacobian(s->impl.ctx, &s->impl, cams, n_cams, *plan, h.get());
+        *out = h.release();
+    });
+}
+void slm_jacobian_destroy(slm_jacobian* j) { delete j; }
+int slm_jacobian_dims(slm_jacobian* j, int64_t* rdim, int64_t* pdim) {
+    *rdim = j->jac->rdim;
+    *pdim = static_cast<int64_t>(kP) * j->jac->scene->G;
+    return SLM_OK;
+}
+int slm_jacobian_jvp(slm_jacobian* j, const double* v, double* out) {
+    return guarded([&] { j->jac->ctx->activate(); j->jac->jvp(v, out); });
+}
+int slm_jacobian_vjp(slm_jacobian* j, const double* u, double* out) {
+    return guarded([&] { j->jac->ctx->activate(); j->jac->vjp(u, out); });
+}
+int slm_jacobian_jtj_diag(slm_jacobian* j, double* out) {
+    return guarded([&] { j->jac->ctx->activate(); j->jac->jtj_diag(out); });
+}
+int slm_jacobian_gn_apply(slm_jacobian* j, double lambda, const double* p, double* out) {
+    return guarded([&] { j->jac->ctx->activate(); j->jac->gn_apply(lambda, p, out); });
+}
+int slm_jacobian_weights(slm_jacobian* j, double* out) {
+    std::copy(j->jac->weights.begin(), j->jac->weights.end(), out);
+    return SLM_OK;
+}
+int slm_jacobian_set_weights(slm_jacobian* j, const double* w) {
+    return guarded([&] {
+        Jacobian& J = *j->jac;
+        J.weights.assign(w, w + J.rdim);
+        J.samples.upload_weights(J.ctx, J.weights, J.plan_base);
+    });
+}
+int slm_jacobian_gn_apply_dev(slm_jacobian* j, float lambda, const float* d_p, float* d_out) {
+    return guarded([&] { j->jac->gn_apply_dev(lambda, d_p, d_out); });
+}
+int slm_jacobian_device_ptrs(slm_jacobian* j, void* stream_out[1]) {
+    stream_out[0] = j->jac->ctx->stream;
+    return SLM_OK;
+}
+int slm_jacobian_stats(slm_jacobian* j, int64_t* out) {
+    // [views, G_valid_sum (unknown: 0), entries, samples, groups, tiles]
+    Batch& b = *j->jac->batch;
+    out[0] = b.V;
+    out[1] = 0;
+    out[2] = b.n_entries;
+    out[3] = j->jac->samples.total;
+    out[4] = static_cast<int64_t>(j->jac->samples.hgroups.size());
+    out[5] = b.n_tiles;
+    return SLM_OK;
+}
+int slm_jacobian_pcg(slm_jacobian* j, double lambda, const double* b, const double* minv, int max_iters,
+                     double* x, slm_pcg_result* res) {
+    return guarded([&] {
+        Jacobian& J = *j->jac;
+        J.ctx->activate();
+        DevBuf<float> db, dm, dx;
+        db.ensure(J.P());
+        dm.ensure(J.P());
+        dx.ensure(J.P());
+        J.upload_param(b, db.p);
+        J.upload_param(minv, dm.p);
+        const CgState cs = J.pcg_dev(static_cast<float>(lambda), db.p, dm.p, max_iters, dx.p);
+        J.download_param(dx.p, x);
+        res->iterations = cs.iterations;
+        res->breakdown = cs.breakdown;
+        res->rel_residual = cs.bnorm == 0.0 ? 0.0 : std::sqrt(cs.rr) / cs.bnorm;
+    });
+}
+
+int slm_pcg_solve(slm_context* ctx, slm_apply_fn apply, void* user, const double* b, const double* minv,
+                  int64_t n, int max_iters, double* x, slm_pcg_result* res) {
+    return guarded([&] {
+        // Vector algebra on the device (f32 storage, f64 reductions); the
+        // caller's operator runs on host vectors between the device steps.
+        Context& c = ctx->impl;
+        c.activate();
+        const long long np = (n + 3) / 4 * 4;
+        DevBuf<float> db, dm, dx, dr, dz, dp, du;
+        for (auto* buf : {&db, &dm, &dx, &dr, &dz, &dp, &du}) {
+            buf->ensure(np);
+            SLM_CUDA_CHECK(cudaMemsetAsync(buf->p, 0, np * sizeof(float), c.stream));
+        }
+        std::vector<float> hf(n);
+        std::vector<double> hp(n), hu(n);
+        auto up = [&](const double* src, float* dst) {
+            for (int64_t i = 0; i < n; ++i) hf[i] = static_cast<float>(src[i]);
+            SLM_CUDA_CHECK(cudaMemcpyAsync(dst, hf.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c.stream));
+            c.sync();
+        };
+        auto down = [&](const float* src, double* dst) {
+            SLM_CUDA_CHECK(cudaMemcpyAsync(hf.data(), src, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int64_t i = 0; i < n; ++i) dst[i] = hf[i];
+        };
+        up(b, db.p);
+        up(minv, dm.p);
+        CgState* cg = c.cg.p;
+        launch_cg_init(db.p, dm.p, np, dx.p, dr.p, dz.p, dp.p, c.partial.p, cg, c.stream);
+        CgState h;
+        for (int it = 0; it < max_iters; ++it) {
+            SLM_CUDA_CHECK(cudaMemcpyAsync(&h, cg, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            if (h.done) break;
+            down(dp.p, hp.data());
+            apply(user, hp.data(), hu.data());
+            up(hu.data(), du.p);
+            launch_cg_pu(dp.p, du.p, np, c.partial.p, cg, c.stream);
+            launch_cg_update(dx.p, dr.p, dz.p, dp.p, du.p, dm.p, np, c.partial.p, cg, c.stream);
+        }
+        c.check_launch();
+        SLM_CUDA_CHECK(cudaMemcpyAsync(&h, cg, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        down(dx.p, x);
+        res->iterations = h.iterations;
+        res->breakdown = h.breakdown;
+        res->rel_residual = h.bnorm == 0.0 ? 0.0 : std::sqrt(h.rr) / h.bnorm;
+    });
+}
+
+void slm_default_lm_config(slm_lm_config* c) {
+    *c = slm_lm_config{0.1, 3, 8, 50, 8, 8, 50, 32, 32, 0.2, 0.05, 10, SLM_DIST_UNIFORM, SLM_LOSS_MSE, 0.2};
+}
+
+int slm_learning_rate(slm_context* ctx, const double* delta, int64_t n, int iteration, const slm_lm_config* cfg,
+                      double* eta) {
+    return guarded([&] {
+        if (n % kP != 0) throw std::invalid_argument("learning_rate: bad update length");
+        Context& c = ctx->impl;
+        c.activate();
+        const int G = static_cast<int>(n / kP);
+        const int Gp = round_up(std::max(G, 1), 256);
+        DevBuf<double> a;
+        DevBuf<float> s, m;
+        a.ensure(std::max<int64_t>(n, 1));
+        s.ensure(static_cast<size_t>(kP) * Gp);
+        m.ensure(1);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(a.p, delta, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+        launch_aos64_to_soa32(a.p, G, Gp, s.p, c.stream);
+        launch_color_maxabs(s.p, G, Gp, m.p, c.stream);
+        float hm = 0.f;
+        SLM_CUDA_CHECK(cudaMemcpyAsync(&hm, m.p, sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        *eta = learning_rate_from(hm, iteration, *cfg);
+    });
+}
+
+int slm_train_create(slm_context* ctx, const slm_camera* cams, int n_cams, const float* images, slm_train** out) {
+    return guarded([&] {
+        Context* c = &ctx->impl;
+        c->activate();
+        auto t = std::make_unique<slm_train>();
+        t->impl.ctx = c;
+        t->impl.cams.assign(cams, cams + n_cams);
+        size_t off = 0;
+        for (int i = 0; i < n_cams; ++i) {
+            t->impl.img_off.push_back(off);
+            off += 3 * static_cast<size_t>(cams[i].width) * cams[i].height;
+        }
+        t->impl.images.ensure(std::max<size_t>(off, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(t->impl.images.p, images, sizeof(float) * off, cudaMemcpyHostToDevice, c->stream));
+        c->sync();
+        *out = t.release();
+    });
+}
+void slm_train_destroy(slm_train* t) { delete t; }
+int slm_train_rebuild_clusters(slm_train* t, int k, uint64_t seed) {
+    return guarded([&] {
+        auto& T = t->impl;
+        T.assign = kmeans(features(T.cams.data(), static_cast<int>(T.cams.size())), k, seed);
+        T.k = k;
+    });
+}
+int slm_train_set_clusters(slm_train* t, const int32_t* assign, int k) {
+    return guarded([&] {
+        t->impl.assign.assign(assign, assign + t->impl.cams.size());
+        t->impl.k = k;
+    });
+}
+int slm_train_clusters(slm_train* t, int32_t* assign, int* k) {
+    std::copy(t->impl.assign.begin(), t->impl.assign.end(), assign);
+    *k = t->impl.k;
+    return SLM_OK;
+}
+
+int slm_lm_step(slm_scene* s, slm_train* t, const slm_lm_config* cfg, int iteration, slm_rng* rng,
+                slm_step_report* report) {
+    return guarded([&] { lm_step(s->impl, t->impl, *cfg, iteration, rng->eng, *report); });
+}
+
+int slm_lm_step_host(slm_context* ctx, slm_gaussians* state, slm_train* t, const slm_lm_config* cfg,
+                     int iteration, slm_rng* rng, slm_step_report* report) {
+    return guarded([&] {
+        Scene s(&ctx->impl, *state);
+        lm_step(s, t->impl, *cfg, iteration, rng->eng, *report);
+        s.download(*state);
+    });
+}
+
+int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, double* out) {
+    return guarded([&] {
+        Context* c = s->impl.ctx;
+        c->activate();
+        std::vector<slm_camera> cv;
+        std::vector<int> ids(cam_ids, cam_ids + n);
+        for (int i : ids) {
+            if (i < 0 || i >= static_cast<int>(t->impl.cams.size())) throw std::invalid_argument("camera index");
+            cv.push_back(t->impl.cams[i]);
+        }
+        Batch b(c);
+        b.prepare(s->impl, cv);
+        copy_gt(t->impl, b, ids);
+        b.render(true);
+        const auto sse = b.view_sse();
+        double acc = 0.0;
+        for (int v = 0; v < n; ++v) acc += sse[v] / (3.0 * cv[v].width * cv[v].height);
+        *out = n == 0 ? 0.0 : acc / n;
+    });
+}
+
+int slm_random_init(int count, const double* lo, const double* hi, slm_rng* rng, slm_gaussians* out) {
+    return guarded([&] {  // io::random_init (dataset.cpp:138-166)
+        if (count < 1) throw std::invalid_argument("random_init: count must be at least 1");
+        std::uniform_real_distribution<double> ux(lo[0], hi[0]), uy(lo[1], hi[1]), uz(lo[2], hi[2]);
+        const double coeff_max = 0.5 / 0.28209479177387814;
+        std::uniform_real_distribution<double> ucolor(-coeff_max, coeff_max);
+        const double edge = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+        const double scale = std::log(0.5 * edge * std::pow(static_cast<double>(count), -1.0 / 3.0));
+        const double logit = std::log(0.1 / 0.9);
+        for (int i = 0; i < count; ++i) {
+            out->means[3 * i] = ux(rng->eng);
+            out->means[3 * i + 1] = uy(rng->eng);
+            out->means[3 * i + 2] = uz(rng->eng);
+            for (int c = 0; c < 3; ++c) {
+                out->log_scales[3 * i + c] = scale;
+                out->colors[3 * i + c] = ucolor(rng->eng);
+            }
+            out->rotations[4 * i] = 1.0;
+            out->rotations[4 * i + 1] = out->rotations[4 * i + 2] = out->rotations[4 * i + 3] = 0.0;
+            out->opacity_logits[i] = logit;
+        }
+    });
+}
+
+int slm_ring_camera(double angle, double radius, double height, int width, int height_px, slm_camera* out) {
+    return guarded([&] {  // io::ring_camera (scene_gen.cpp:11-36), W x H allowed
+        const double pos[3] = {radius * std::cos(angle), height, radius * std::sin(angle)};
+        double fwd[3] = {0.0 - pos[0], 0.0 - pos[1], 0.0 - pos[2]};
+        const double fn = std::sqrt(fwd[0] * fwd[0] + fwd[1] * fwd[1] + fwd[2] * fwd[2]);
+        for (double& v : fwd) v /= fn;
+        double right[3] = {fwd[1] * 0.0 - fwd[2] * 1.0, fwd[2] * 0.0 - fwd[0] * 0.0, fwd[0] * 1.0 - fwd[1] * 0.0};
+        const double rn = std::sqrt(right[0] * right[0] + right[1] * right[1] + right[2] * right[2]);
+        for (double& v : right) v /= rn;
+        const double down[3] = {fwd[1] * right[2] - fwd[2] * right[1], fwd[2] * right[0] - fwd[0] * right[2],
+                                fwd[0] * right[1] - fwd[1] * right[0]};
+        std::memset(out, 0, sizeof *out);
+        for (int k = 0; k < 3; ++k) {
+            out->world_to_cam[k] = right[k];
+            out->world_to_cam[3 + k] = down[k];
+            out->world_to_cam[6 + k] = fwd[k];
+        }
+        for (int r = 0; r < 3; ++r) {
+            const double* row = out->world_to_cam + 3 * r;
+            out->translation[r] = -(row[0] * pos[0] + row[1] * pos[1] + row[2] * pos[2]);
+        }
+        out->width = width;
+        out->height = height_px > 0 ? height_px : width;
+        const double fov_x = 50.0 * 3.14159265358979323846 / 180.0;
+        out->fx = out->fy = 0.5 * width / std::tan(0.5 * fov_x);
+        out->cx = 0.5 * width;
+        out->cy = 0.5 * out->height;
+        out->near_clip = 0.2;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// runtime.hpp — host-side C++ runtime of libslm_b200 (compiled with g++;
+// the kernels it drives live in the *.cu files).
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "layout.hpp"
+
+namespace slm {
+
+struct CudaError : std::runtime_error {
+    cudaError_t code;
+    CudaError(cudaError_t c, const char* what, const char* file, int line)
+        : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(c) + " at " + file + ":" +
+                             std::to_string(line) + " (" + what + ")"),
+          code(c) {}
+};
+
+#define SLM_CUDA_CHECK(x)                                                          \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess) throw ::slm::CudaError(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+extern std::atomic<long long> g_launches;  // kernels launched by this library
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    // Grow-only allocation; contents are undefined after a reallocation.
+    T* ensure(size_t count) {
+        if (count <= n && p) return p;
+        release();
+        const size_t bytes = (count > 0 ? count : 1) * sizeof(T);
+        SLM_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
+        n = count;
+        return p;
+    }
+    T* ensure_zero(size_t count, cudaStream_t st) {
+        const bool fresh = count > n || !p;
+        ensure(count);
+        if (fresh) SLM_CUDA_CHECK(cudaMemsetAsync(p, 0, (count > 0 ? count : 1) * sizeof(T), st));
+        return p;
+    }
+};
+
+// ---- launchers (defined in the .cu files)
+void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
+                    unsigned long long* keys, short4* rect, int* tile_count, int* err, cudaStream_t st);
+void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total, cudaStream_t st);
+void launch_bin_scatter(int G, int Gp, int V, const DevCam* cams, const short4* rect, int* cursor,
+                        int* entries, cudaStream_t st);
+void launch_tile_sort(const int* offsets, int* entries, const unsigned long long* keys,
+                      const int* tile_view, int n_tiles, int Gp, int* overflow, int* overflow_count,
+                      cudaStream_t st);
+void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta, float* beta32,
+                         cudaStream_t st);
+void launch_apply_update_f64(double* beta, const double* delta_aos, int G, int Gp, double eta,
+                             float* beta32, cudaStream_t st);
+void launch_beta_mirror(const double* beta, float* beta32, int n, cudaStream_t st);
+void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
+                   const int* entries, const float4* rec, int Gp, const float* gt, float* image,
+                   float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st);
+void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile, double* sse_view,
+                      cudaStream_t st);
+void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);
+void launch_diag_raster(const DiagArgs& a, cudaStream_t st);
+void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
+                     const float4* rec, float4* tan, const int* done, cudaStream_t st);
+void launch_chain(const double* beta, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                  float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st);
+void launch_diag_finalize(const double* beta, int G, int Gp, const DevCam* cams, int V,
+                          const float4* rec, float* diagacc, float* out, cudaStream_t st);
+void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
+void launch_soa32_to_aos64(const float* soa, int G, int Gp, double* aos, cudaStream_t st);
+void launch_set_to_beta(const double* m, const double* ls, const double* rot, const double* logit,
+                        const double* col, int G, int Gp, double* beta, float* beta32, cudaStream_t st);
+void launch_beta_to_set(const double* beta, int G, int Gp, double* m, double* ls, double* rot,
+                        double* logit, double* col, cudaStream_t st);
+void launch_dot(const float* a, const float* b, long long n, double* partial, double* out, cudaStream_t st);
+void launch_color_maxabs(const float* x, int G, int Gp, float* out, cudaStream_t st);
+void launch_cg_init(const float* b, const float* minv, long long n, float* x, float* r, float* z,
+                    float* p, double* partial, CgState* s, cudaStream_t st);
+void launch_cg_pu(const float* p, const float* u, long long n, double* partial, CgState* s, cudaStream_t st);
+void launch_cg_update(float* x, float* r, float* z, float* p, const float* u, const float* minv,
+                      long long n, double* partial, CgState* s, cudaStream_t st);
+void launch_minv(float* d, long long n, float lambda, cudaStream_t st);
+void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
+
+}  // namespace slm

@@ -1,0 +1,302 @@
+"""GPU parity: the sm_100a path through the C ABI vs the reference.
+
+Anchors: the golden fixtures made by the unmodified reference
+(tests/golden/*.npz) and the C restatement (oracle/liboracle.so, pinned to the
+reference bit for bit by tests/test_oracle.py) on fresh seeded inputs.
+
+Bars (BASELINE.json north_star):
+* bit-exact: tile/Gaussian lists, per-tile sort order, sampled pixel sets,
+  view batches;
+* norm-relative 1e-4: Jv, J^T u, diag(J^T W J), J^T W J p, the CG solution,
+  per-iteration loss.  The raster runs in FP32 (the reference in FP64), so a
+  pixel whose alpha sits within FP32 rounding of a gate (1/255 skip, 0.99
+  clamp, 1e-4 termination) may take the other branch; the tolerance absorbs
+  that and the tests report the worst case they see.
+"""
+import numpy as np
+import pytest
+
+from paper_2504_12905_b200.types import LmConfig, SamplePlan
+from support import (MT64, g_cams, g_plan, g_set, golden, norm_rel, random_scene, rel_error)
+from support import test_camera as tcam
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    from paper_2504_12905_b200 import splatlm
+    return splatlm.lib()
+
+
+# ----------------------------------------------------------------- K1/K3/K4
+@pytest.mark.parametrize("t", range(20))
+def test_tile_lists_bit_exact_random_scenes(gpu, t):
+    d = golden("render")
+    g = g_set(d, f"r{t}")
+    cam = g_cams(d[f"r{t}_cam"])[0]
+    off, idx = gpu.bin_and_sort(g, cam)
+    assert np.array_equal(off, d[f"r{t}_offsets"])
+    assert np.array_equal(idx, d[f"r{t}_indices"])
+
+
+@pytest.mark.parametrize("i", range(3))
+def test_tile_lists_bit_exact_ring_views(gpu, i):
+    d = golden("render")
+    g = g_set(d, "ring")
+    cam = g_cams(d["ring_cams"])[i]
+    off, idx = gpu.bin_and_sort(g, cam)
+    assert np.array_equal(off, d[f"ring{i}_offsets"])
+    assert np.array_equal(idx, d[f"ring{i}_indices"])
+    p = gpu.prepare(g, cam)
+    assert np.array_equal(p["valid"], d[f"ring{i}_prep_valid"])
+    assert np.array_equal(p["depth"][p["valid"] == 1], d[f"ring{i}_prep_depth"][p["valid"] == 1])
+    v = p["valid"] == 1
+    assert np.allclose(p["mean2d"].reshape(-1, 2)[v], d[f"ring{i}_prep_mean2d"].reshape(-1, 2)[v], rtol=1e-6)
+
+
+def test_bin_and_sort_known_answers(gpu):
+    """test_render.cpp:89-120: empty scene, single-tile locality, depth order."""
+    from paper_2504_12905_b200.types import GaussianSet
+    cam = tcam(64, 3.0)
+    off, idx = gpu.bin_and_sort(GaussianSet.zeros(0), cam)
+    assert idx.size == 0 and np.all(off == 0)
+    one = GaussianSet.zeros(1)
+    one.means[:] = [-0.30, -0.30, 0.0]
+    one.log_scales[:] = np.log(0.01)
+    one.opacity_logits[:] = 0.5
+    off, idx = gpu.bin_and_sort(one, cam)
+    assert np.count_nonzero(np.diff(off)) == 1
+    two = GaussianSet.zeros(2)
+    two.means[:] = [0, 0, 1.0, 0, 0, 0.0]
+    two.log_scales[:] = np.log(0.2)
+    two.opacity_logits[:] = 0.5
+    off, idx = gpu.bin_and_sort(two, cam)
+    shared = [idx[off[t]:off[t + 1]] for t in range(off.size - 1) if off[t + 1] - off[t] == 2]
+    assert shared and all(list(s) == [1, 0] for s in shared)
+
+
+def test_permuted_storage_order(gpu):
+    """test_render.cpp:137: the per-tile sort removes storage-order dependence."""
+    rng = MT64(33)
+    g = random_scene(12, rng)
+    perm = np.random.default_rng(1).permutation(12)
+    h = g.copy()
+    h.means = g.means.reshape(-1, 3)[perm].reshape(-1).copy()
+    h.log_scales = g.log_scales.reshape(-1, 3)[perm].reshape(-1).copy()
+    h.colors = g.colors.reshape(-1, 3)[perm].reshape(-1).copy()
+    h.rotations = g.rotations.reshape(-1, 4)[perm].reshape(-1).copy()
+    h.opacity_logits = g.opacity_logits[perm].copy()
+    a = gpu.render_full(g, tcam(32, 3.0))[0]
+    b = gpu.render_full(h, tcam(32, 3.0))[0]
+    assert np.max(np.abs(a - b)) < 1e-6
+
+
+# ----------------------------------------------------------------- K6
+@pytest.mark.parametrize("t", range(0, 20, 3))
+def test_render_random_scenes(gpu, t):
+    d = golden("render")
+    g = g_set(d, f"r{t}")
+    cam = g_cams(d[f"r{t}_cam"])[0]
+    img, tr, cn = gpu.render_full(g, cam)
+    assert norm_rel(img, d[f"r{t}_image"]) < TOL
+    assert np.max(np.abs(img - d[f"r{t}_image"])) < 1e-3
+    assert np.mean(cn != d[f"r{t}_contrib"]) < 0.01
+
+
+@pytest.mark.parametrize("i", range(3))
+def test_render_ring_views(gpu, i):
+    d = golden("render")
+    g = g_set(d, "ring")
+    cam = g_cams(d["ring_cams"])[i]
+    img, tr, cn = gpu.render_full(g, cam)
+    assert norm_rel(img, d[f"ring{i}_image"]) < TOL
+    assert norm_rel(tr, d[f"ring{i}_trans"]) < TOL
+    assert np.mean(cn != d[f"ring{i}_contrib"]) < 0.01
+
+
+def test_render_known_answers(gpu):
+    """test_render.cpp:170-182: empty scene is background, T = 1."""
+    from paper_2504_12905_b200.types import GaussianSet
+    img, tr, cn = gpu.render_full(GaussianSet.zeros(0), tcam(32, 3.0))
+    assert np.all(img == 0) and np.all(tr == 1) and np.all(cn == 0)
+
+
+# ----------------------------------------------------------------- Jacobian products
+@pytest.mark.parametrize("name", ["jx", "js", "jr"])
+def test_jacobian_products_vs_reference(gpu, name):
+    d = golden("jacobian")
+    g = g_set(d, name)
+    cams = g_cams(d[f"{name}_cams"])
+    jac = gpu.jacobian(g, cams, g_plan(d, name))
+    assert jac.residual_dim() == d[f"{name}_jvp"].size and jac.param_dim() == d[f"{name}_vjp"].size
+    assert np.array_equal(jac.residual_weights(), d[f"{name}_weights"])
+    errs = {
+        "jvp": norm_rel(jac.jvp(d[f"{name}_v"]), d[f"{name}_jvp"]),
+        "vjp": norm_rel(jac.vjp(d[f"{name}_u"]), d[f"{name}_vjp"]),
+        "diag": norm_rel(jac.jtj_diag(), d[f"{name}_diag"]),
+        "gn": norm_rel(jac.gn_apply(0.1, d[f"{name}_p"]), d[f"{name}_gn"]),
+    }
+    print(name, errs)
+    assert all(e < TOL for e in errs.values()), errs
+    minv = 1.0 / (d[f"{name}_diag"] + 0.1)
+    res = jac.pcg(0.1, d[f"{name}_vjp"], minv, 8)
+    meta = d[f"{name}_pcg_meta"]
+    assert res.iterations == int(meta[0]) and res.breakdown == bool(meta[1])
+    assert norm_rel(res.x, d[f"{name}_pcg_x"]) < TOL
+
+
+def test_adjoint_identity(gpu):
+    """test_autodiff.cpp:131: <Jv, u> == <v, J^T u> (FP32 raster: 1e-4)."""
+    g = random_scene(5, MT64(48))
+    cams = [tcam(32, 3.0)]
+    host = gpu
+    plan = host.exhaustive_plan(cams)
+    jac = gpu.jacobian(g, cams, plan)
+    r = np.random.default_rng(49)
+    for _ in range(10):
+        v = r.uniform(-1, 1, jac.param_dim())
+        u = r.uniform(-1, 1, jac.residual_dim())
+        lhs = float(np.dot(jac.jvp(v), u))
+        rhs = float(np.dot(v, jac.vjp(u)))
+        assert rel_error(lhs, rhs) < TOL
+
+
+def test_gn_apply_symmetric_pd_and_linear(gpu):
+    """test_autodiff.cpp:106,264: linearity, symmetry, positive definiteness."""
+    rng = MT64(56)
+    g = random_scene(5, rng)
+    cams = [tcam(32, 3.0)]
+    plan = gpu.build_sample_plan(cams, 8, 0, gpu.rng(57), lane_width=1)
+    jac = gpu.jacobian(g, cams, plan)
+    r = np.random.default_rng(57)
+    assert np.all(jac.gn_apply(0.05, np.zeros(jac.param_dim())) == 0)
+    for _ in range(5):
+        p1, p2 = r.uniform(-1, 1, (2, jac.param_dim()))
+        a1, a2 = jac.gn_apply(0.05, p1), jac.gn_apply(0.05, p2)
+        assert rel_error(float(p1 @ a2), float(p2 @ a1)) < TOL
+        assert float(p1 @ a1) >= 0.05 * float(p1 @ p1) * (1 - TOL)
+        a12 = jac.gn_apply(0.05, 1.7 * p1 - 0.6 * p2)
+        assert norm_rel(a12, 1.7 * a1 - 0.6 * a2) < TOL
+    assert np.all(jac.jtj_diag() >= 0)
+
+
+@pytest.mark.parametrize("seed,n,size,spt", [(140, 12, 48, 32), (77, 30, 64, 13), (5, 40, 80, 64)])
+def test_products_vs_oracle_fresh_cases(gpu, port, seed, n, size, spt):
+    rng = MT64(seed)
+    g = random_scene(n, rng)
+    cams = [tcam(size, 3.0), tcam(size // 2 + 8, 3.2)]
+    plan = port.build_sample_plan(cams, spt, 0, port.rng(seed), lane_width=1)
+    ja, jb = gpu.jacobian(g, cams, plan), port.jacobian(g, cams, plan)
+    r = np.random.default_rng(seed)
+    v, u, p = r.uniform(-1, 1, ja.param_dim()), r.uniform(-1, 1, ja.residual_dim()), r.uniform(-1, 1, ja.param_dim())
+    assert norm_rel(ja.jvp(v), jb.jvp(v)) < TOL
+    assert norm_rel(ja.vjp(u), jb.vjp(u)) < TOL
+    assert norm_rel(ja.jtj_diag(), jb.jtj_diag()) < TOL
+    assert norm_rel(ja.gn_apply(0.1, p), jb.gn_apply(0.1, p)) < TOL
+
+
+def test_empty_plan_views(gpu):
+    """test_autodiff.cpp:226: an empty plan gives zero products."""
+    g = random_scene(6, MT64(52))
+    cams = [tcam(32, 3.0)]
+    plan = SamplePlan(np.array([0], np.int32), np.array([0, 0], np.int64), np.zeros(0, np.int32),
+                      np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    jac = gpu.jacobian(g, cams, plan)
+    assert np.all(jac.jtj_diag() == 0)
+    assert np.all(jac.gn_apply(0.1, np.zeros(jac.param_dim())) == 0)
+
+
+def test_jacobian_errors(gpu):
+    g = random_scene(3, MT64(47))
+    cams = [tcam(32, 3.0)]
+    plan = gpu.build_sample_plan(cams, 16, 0, gpu.rng(1), lane_width=1)
+    jac = gpu.jacobian(g, cams, plan)
+    with pytest.raises(ValueError):
+        jac.vjp(np.ones(3))
+    bad = SamplePlan(np.array([3], np.int32), plan.view_offset, plan.px, plan.py, plan.tile, plan.weight)
+    with pytest.raises(ValueError):
+        gpu.jacobian(g, cams, bad)
+
+
+# ----------------------------------------------------------------- PCG / solver
+def test_pcg_dense_operator(gpu):
+    """test_solver.cpp:44-107 through the host-operator PCG."""
+    b = np.arange(1.0, 8.0)
+    res = gpu.pcg_dense(np.eye(7), b, np.ones(7), 5)
+    assert res.iterations == 1 and not res.breakdown and np.allclose(res.x, b, rtol=1e-6)
+    res = gpu.pcg_dense(np.eye(5), np.zeros(5), np.ones(5), 5)
+    assert res.iterations == 0 and np.all(res.x == 0)
+    r = np.random.default_rng(91)
+    for _ in range(10):
+        n = int(r.integers(2, 21))
+        a = r.uniform(-1, 1, (n, n))
+        m = a.T @ a + 0.1 * np.eye(n)
+        bb = r.uniform(-1, 1, n)
+        res = gpu.pcg_dense(m, bb, 1.0 / np.diag(m), n + 3)
+        assert np.linalg.norm(m @ res.x - bb) / np.linalg.norm(bb) < 1e-3
+    m = np.eye(4)
+    m[2, 2] = -2.0
+    assert gpu.pcg_dense(m, np.array([0, 0, 1.0, 0]), np.ones(4), 10).breakdown
+
+
+def test_learning_rate(gpu):
+    cfg = LmConfig()
+    delta = np.zeros(28)
+    delta[11] = 123.0
+    assert gpu.learning_rate(delta, 5, cfg) == 0.05
+    delta[11] = 10.0
+    assert gpu.learning_rate(delta, 50, cfg) == pytest.approx(0.1)
+    delta[:] = 0
+    delta[0] = 99.0
+    assert gpu.learning_rate(delta, 50, cfg) == pytest.approx(0.2)
+    delta[14 + 13] = -10.0
+    assert gpu.learning_rate(delta, 50, cfg) == pytest.approx(0.1)
+
+
+def test_apply_update(gpu, port):
+    g = random_scene(20, MT64(3))
+    h = g.copy()
+    delta = np.random.default_rng(0).uniform(-1, 1, 14 * 20)
+    gpu.apply_update(g, delta, 0.2)
+    port.apply_update(h, delta, 0.2)
+    assert np.max(np.abs(g.pack() - h.pack())) < 1e-12
+
+
+# ----------------------------------------------------------------- lm_step
+def test_lm_trajectory_vs_reference(gpu):
+    """12 free-running LM steps on the toy scene vs the reference's own run:
+    identical view batches (RNG replay), losses within 1e-4 relative."""
+    d = golden("lm")
+    tc = g_cams(d["toy_train_cams"])
+    rng = gpu.rng(1)
+    st = gpu.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    assert st == g_set(d, "lm_init")
+    td = gpu.train_data(tc, list(d["toy_train_imgs"]))
+    td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8)
+    worst = 0.0
+    for it, row in enumerate(d["lm_reports"]):
+        r = gpu.lm_step(st, td, cfg, it, rng)
+        assert r.batch == [int(b) for b in row[6:]]
+        assert r.pcg_iterations == int(row[4]) and r.breakdown == bool(row[5])
+        assert r.eta == pytest.approx(row[3], rel=1e-6)
+        worst = max(worst, rel_error(r.loss_before, row[1]), rel_error(r.loss_after, row[2]))
+    print("worst per-iteration loss rel err", worst)
+    assert worst < TOL
+    assert rng() == int(d["lm_rng_next"][0])  # same RNG position: samplers replayed exactly
+    assert norm_rel(st.pack(), g_set(d, "lm_final").pack()) < 1e-3
+
+
+def test_lm_step_fixed_point(gpu, port):
+    """test_solver.cpp:132: at zero residual the step does not move the state."""
+    gt, tc, ti, sc, si = port.toy_scene(8, 4, 1, 32, 93)
+    imgs = [gpu.render_full(gt, c)[0].astype(np.float32) for c in tc]
+    td = gpu.train_data(tc, imgs)
+    td.rebuild_clusters(4, 1)
+    st = gt.copy()
+    r = gpu.lm_step(st, td, LmConfig(batch_size_initial=4), 0, gpu.rng(94))
+    assert r.loss_before < 1e-10
+    assert np.max(np.abs(st.pack() - gt.pack())) < 1e-5
