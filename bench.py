@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""bench.py — J^T W J p matvecs/s (and LM iterations/s) at 1M Gaussians on B200.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on):
+1M Gaussians (random_init state, SH-0: the reference supports only SH-0,
+SURVEY §7 hard part 8), 200 ring cameras at 1280x720 (50 deg FOV, radius 3.2),
+LM batch of 8 views drawn by the k-means view sampler, 32 stratified samples
+per 16x16 tile.  One "step" = one J^T W J p + lambda p product over the 8-view
+batch (SampledJacobian::gn_apply, jacobian.cpp:339-344) — the unit the
+north-star roofline target is stated for.  At N ranks each rank owns 8 views
+(weak scaling) and the product includes the per-CG-iteration NCCL allreduce.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line on rank 0.  The working set (records, tile lists,
+tangents, ~1.5 GB) is far larger than the 126 MB L2, so no flush is needed
+between timed iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2504_12905_b200.types import GaussianSet, LmConfig, SamplePlan, ring_camera  # noqa: E402
+
+METRIC = "JTWJp matvecs/s (8-view LM batch, 1M Gaussians)"
+UNIT = "matvec/s"
+KMEANS_SALT = 0x9E3779B97F4A7C15  # run.cpp:144
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--gaussians", type=int, default=1_000_000)
+    ap.add_argument("--views", type=int, default=200)
+    ap.add_argument("--width", type=int, default=1280)
+    ap.add_argument("--height", type=int, default=720)
+    ap.add_argument("--batch", type=int, default=8, help="views per rank per LM batch")
+    ap.add_argument("--spt", type=int, default=32, help="samples per tile")
+    ap.add_argument("--lm-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cameras(args):
+    return [ring_camera(2.0 * math.pi * i / args.views, 3.2, 1.1, args.width, args.height)
+            for i in range(args.views)]
+
+
+def host_inputs(H, args, world):
+    """Seeded exactly like train_run (run.cpp:126-167): random_init consumes the
+    run RNG first, then the view batch and the sample plan draw from it."""
+    rng = H.rng(1)
+    state = H.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)
+    cams = cameras(args)
+    clusters = H.kmeans_cameras(cams, args.batch * world, 1 ^ KMEANS_SALT)
+    batch = H.sample_view_batch(clusters, rng)
+    plan = H.build_sample_plan([cams[i] for i in batch], args.spt, 0, rng, 32)
+    return state, cams, clusters, batch, plan
+
+
+def sub_plan(plan: SamplePlan, lo: int, hi: int) -> SamplePlan:
+    a, b = int(plan.view_offset[lo]), int(plan.view_offset[hi])
+    return SamplePlan(np.arange(hi - lo, dtype=np.int32), plan.view_offset[lo:hi + 1] - a,
+                      plan.px[a:b], plan.py[a:b], plan.tile[a:b], plan.weight[a:b], plan.samples_per_tile)
+
+
+def gt_scene(count: int, seed: int = 20214) -> GaussianSet:
+    """Ground-truth scene with generate_toy_scene's distributions (scene_gen.cpp:47-66)."""
+    r = np.random.default_rng(seed)
+    g = GaussianSet(count)
+    g.means = r.uniform(-0.8, 0.8, 3 * count)
+    g.log_scales = r.uniform(math.log(0.12), math.log(0.35), 3 * count)
+    g.colors = r.uniform(-1.2, 1.2, 3 * count)
+    q = r.uniform(-1, 1, (count, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    g.rotations = q.reshape(-1).copy()
+    o = r.uniform(0.4, 0.9, count)
+    g.opacity_logits = np.log(o / (1 - o))
+    return g
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling during the timed region (NVML)."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksThrottleReason") and
+                 isinstance(getattr(nv, k), int)}
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if bit and mask & bit and name not in ("nvmlClocksThrottleReasonGpuIdle",
+                                                           "nvmlClocksThrottleReasonAll",
+                                                           "nvmlClocksThrottleReasonNone"):
+                        self.reasons.add(name.replace("nvmlClocksThrottleReason", ""))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(stats: dict) -> dict:
+    """B_matvec = 4 * sum_v (88 G_v + 19 E_v + 4 S_v) bytes; the fused
+    raster's share is 4 * (19 E_v + 4 S_v) (index + value + tangent record per
+    tile-list entry, packed pixel + weight + forward state per sample)."""
+    G, E, S = stats["valid"], stats["entries"], stats["samples"]
+    return {"matvec": 4 * (88 * G + 19 * E + 4 * S), "raster": 4 * (19 * E + 4 * S),
+            "G_v_sum": G, "E_v_sum": E, "S_v_sum": S}
+
+
+# ---------------------------------------------------------------------------- CPU
+def cpu_sample(args, views: int, steps: int, warmup: int):
+    """Reference SampledJacobian::gn_apply (oracle/_ref, else the C port) on the
+    same state/cameras/plan restricted to `views` of the batch, all host threads.
+    Returns (matvecs/s scaled to the 8-view batch, per-step seconds, meta)."""
+    import oracle
+    from oracle.cpu_bind import port, ref
+    lib = ref() if oracle.have_ref() else port()
+    cores = os.cpu_count() or 1
+    lib.set_threads(cores)
+    # Inputs come from the library's host sampler, which replays the reference's
+    # RNG stream bit for bit (tests/test_abi.py); the timed call is the reference's.
+    from paper_2504_12905_b200 import splatlm
+    state, cams, clusters, batch, plan = host_inputs(splatlm.HostSampler(), args, 1)
+    sp = sub_plan(plan, 0, views)
+    t0 = time.perf_counter()
+    jac = lib.jacobian(state, [cams[i] for i in batch[:views]], sp)
+    ctor = time.perf_counter() - t0
+    p = np.random.default_rng(0).uniform(-1, 1, jac.param_dim())
+    for _ in range(warmup):
+        jac.gn_apply(0.1, p)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        jac.gn_apply(0.1, p)
+        times.append(time.perf_counter() - t0)
+    per_view = float(np.mean(times)) / views
+    value = 1.0 / (per_view * args.batch)
+    meta = {"kind": lib.kind, "cores": cores, "ctor_s": round(ctor, 2),
+            "sample": f"gn_apply over {views} of the {args.batch} batch views "
+                      f"({args.width}x{args.height}, N={args.spt}), {len(times)} timed after {warmup} warm-up, "
+                      f"per-view time scaled x{args.batch} to the 8-view matvec"}
+    return value, times, meta
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    value, times, meta = cpu_sample(args, args.cpu_views, args.steps, args.warmup)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "configs[2]: 1M Gaussians, 1280x720, 8-view LM batch, N=32",
+                       "gaussians": args.gaussians, "views": args.views, "width": args.width,
+                       "height": args.height, "batch_views": args.batch, "samples_per_tile": args.spt},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": meta["cores"], "kind": meta["kind"],
+                             "sample": meta["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- B200
+def run_b200(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            import nvidia.nccl
+            os.environ.setdefault("SLM_NCCL_LIB", os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib",
+                                                               "libnccl.so.2"))
+        except Exception:
+            pass
+    from paper_2504_12905_b200 import splatlm
+    L = splatlm.Lib(local)
+    stream = torch.cuda.Stream()
+    L.set_stream(stream.cuda_stream)
+    if world > 1:
+        uid = splatlm.Lib.nccl_unique_id(L.dll) if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        L.init_comm(obj[0], rank, world)
+
+    t_setup = time.perf_counter()
+    state, cams, clusters, batch, plan = host_inputs(L, args, world)
+    lo, hi = rank * args.batch, (rank + 1) * args.batch
+    scene = splatlm.Scene(L, state)
+    # Global N_total weights, this rank's views: slice the plan but keep weights
+    # relative to the whole batch (the solver's allreduce sums the slices).
+    my_plan = sub_plan(plan, lo, hi)
+    jac = scene.jacobian([cams[i] for i in batch[lo:hi]], my_plan)
+    stats = jac.stats()
+    P = 14 * scene.padded
+    p = torch.empty(P, device="cuda", dtype=torch.float32).uniform_(-1, 1)
+    u = torch.zeros(P, device="cuda", dtype=torch.float32)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    def product():
+        jac.gn_apply_dev(0.1, p.data_ptr(), u.data_ptr())
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            product()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.launch_count()
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            for _ in range(args.steps):
+                product()
+            end.record(stream)
+        torch.cuda.synchronize()
+    launches = L.launch_count() - launches0
+    ms = start.elapsed_time(end)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1000.0)  # 8-view products, all ranks
+
+    # per-kernel breakdown of the product (CUDA events around each kernel)
+    L.set_profiling(True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            product()
+    prof = L.profile_collect()
+    L.set_profiling(False)
+    n = max(prof["n"], 1)
+    raster_ms = prof["raster_ms"] / n
+    bytes_ = algorithmic_bytes(stats)
+    peak, peak_src = measured_peaks()
+    achieved = bytes_["raster"] / (raster_ms / 1000.0) / 1e9
+    matvec_achieved = bytes_["matvec"] / (ms_per_step / 1000.0) / 1e9
+
+    # e2e through the drop-in host API (SampledJacobian::gn_apply on host f64 vectors)
+    host_jac = L.jacobian(state, [cams[i] for i in batch[lo:hi]], my_plan)
+    ph = np.random.default_rng(0).uniform(-1, 1, host_jac.param_dim())
+    host_jac.gn_apply(0.1, ph)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        host_jac.gn_apply(0.1, ph)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    del host_jac
+    e2e_value = world / e2e_s
+
+    # LM iterations/s on the device-resident scene (lm_step, lm.cpp:56-157)
+    lm = None
+    if args.lm_steps > 0:
+        gt = splatlm.Scene(L, gt_scene(args.gaussians // 2))
+        imgs = [gt.render(c)[0] for c in cams]
+        del gt
+        td = L.train_data(cams, imgs)
+        del imgs
+        td.set_clusters(clusters)
+        lm_scene = splatlm.Scene(L, state)
+        cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, batch_size_initial=args.batch * world,
+                       batch_size_late=args.batch * world, samples_per_tile=args.spt)
+        rng = L.rng(1)
+        L.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)  # same stream position as train_run
+        with torch.cuda.stream(stream):
+            rep = lm_scene.lm_step(td, cfg, 0, rng)
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            reps = [lm_scene.lm_step(td, cfg, 1 + i, rng) for i in range(args.lm_steps)]
+            e1.record(stream)
+        torch.cuda.synchronize()
+        lm_ms = e0.elapsed_time(e1) / args.lm_steps
+        if dist:
+            t = torch.tensor([lm_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            lm_ms = float(t.item())
+        lm = {"lm_iters_per_s": 1000.0 / lm_ms, "ms_per_lm_step": lm_ms, "pcg_iters": 8,
+              "loss_before_first": rep.loss_before, "loss_after_last": reps[-1].loss_after}
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cval, ctimes, meta = cpu_sample(args, args.cpu_views, 2, 1)
+            cpu = {"value": cval, "unit": UNIT, "cores": meta["cores"], "kind": meta["kind"],
+                   "sample": meta["sample"]}
+        except Exception as e:  # the checker is optional on a box without the build
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"{type(e).__name__}: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 raster + f64 per-Gaussian linearisation",
+        "data": "synthetic (random_init state, ring cameras; BASELINE configs[2] shape)",
+        "config": {"workload": "configs[2]: 1M Gaussians (SH-0), 200 views 1280x720, 8-view LM batch per rank, "
+                               "N=32 samples/tile, lambda=0.1",
+                   "gaussians": args.gaussians, "views": args.views, "width": args.width,
+                   "height": args.height, "batch_views_per_rank": args.batch, "samples_per_tile": args.spt,
+                   "parallelism": f"view-sharded x{world}, NCCL allreduce per product" if world > 1 else "1 GPU",
+                   "l2": "working set > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "kernel": "k_sample_raster<GN> (fused Jv -> W -> J^T)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": bytes_["raster"],
+                     "avg_launch_ms": raster_ms, "peak_source": peak_src},
+        "matvec_roofline": {"achieved": matvec_achieved, "peak": peak, "unit": "GB/s",
+                            "frac": matvec_achieved / peak, "bytes_per_matvec": bytes_["matvec"],
+                            "roofline_matvecs_per_s": peak * 1e9 / bytes_["matvec"] * world,
+                            **{k: bytes_[k] for k in ("G_v_sum", "E_v_sum", "S_v_sum")}},
+        "breakdown_ms": {"tangents": prof["tangents_ms"] / n, "raster": raster_ms, "chain": prof["chain_ms"] / n},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * 14 * args.gaussians,
+                "d2h_bytes_per_step": 8 * 14 * args.gaussians,
+                "path": "slm_jacobian_gn_apply (host f64 ParamVector in/out)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+        "lm": lm,
+        "setup_s": round(setup_s, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

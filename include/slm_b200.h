@@ -162,9 +162,13 @@ int slm_ring_camera(double angle, double radius, double height, int width, int h
 int slm_context_set_stream(slm_context* ctx, void* stream);
 int slm_context_set_timing(slm_context* ctx, int on);
 long long slm_launch_count(void); /* kernels launched by this library so far */
+/* CUDA events around the three kernels of every J^T W J p product
+ * (tangents, fused raster, chain); collect returns summed ms and the count. */
+int slm_context_set_profiling(slm_context* ctx, int on);
+int slm_context_profile_collect(slm_context* ctx, double out[3], int* n);
 int slm_scene_beta_ptrs(slm_scene* s, double** beta, float** beta32);
 int slm_jacobian_device_ptrs(slm_jacobian* j, void* stream_out[1]);
-/* [views, 0, tile-list entries, samples, warp groups, tiles] */
+/* [views, sum_v G_v (valid view-Gaussian pairs), tile-list entries, samples, warp groups, tiles] */
 int slm_jacobian_stats(slm_jacobian* j, int64_t* out);
 
 #ifdef __cplusplus

@@ -139,6 +139,11 @@ __global__ void k_prepare(const double* __restrict__ beta, int G, int Gp,
     const Prepared p = prepare_value(beta, Gp, g, cam);
     const size_t vg = static_cast<size_t>(v) * Gp + g;
     if (p.zero_quat) atomicOr(err, 1);
+    {  // err[1 + v] = G_v, the valid (view, Gaussian) count (warp-aggregated)
+        const unsigned am = __activemask();
+        const unsigned vm = __ballot_sync(am, p.valid);
+        if (vm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&err[1 + v], __popc(vm));
+    }
     keys[vg] = depth_key(p.depth);
     float4* R = rec + 3 * vg;
     if (!p.valid) {

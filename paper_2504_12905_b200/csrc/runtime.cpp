@@ -92,6 +92,8 @@ struct Context {
     std::vector<std::pair<std::string, cudaEvent_t>> marks;
     std::vector<double> last_timings;
     bool timing = false;
+    bool prof = false;  // per-kernel CUDA events inside gn_apply_dev
+    std::vector<std::array<cudaEvent_t, 4>> prof_events;
     StepBuffers* step = nullptr;  // persistent lm_step workspace
 
     explicit Context(int dev) : device(dev) {
@@ -130,6 +132,27 @@ struct Context {
         }
         for (auto& m : marks) cudaEventDestroy(m.second);
         marks.clear();
+    }
+
+    void prof_record(std::array<cudaEvent_t, 4>& ev, int i) {
+        if (i == 0)
+            for (auto& e : ev) SLM_CUDA_CHECK(cudaEventCreate(&e));
+        SLM_CUDA_CHECK(cudaEventRecord(ev[i], stream));
+    }
+    // {tangents, raster, chain} summed ms and launch count since the last collect
+    void prof_collect(double out[3], int* n) {
+        sync();
+        out[0] = out[1] = out[2] = 0.0;
+        for (auto& ev : prof_events) {
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+                out[k] += ms;
+            }
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
+        *n = static_cast<int>(prof_events.size());
+        prof_events.clear();
     }
 
     void allreduce(float* p, size_t n) {
@@ -213,6 +236,7 @@ struct Batch {
     DevBuf<int> contrib, last;
     DevBuf<double> sse_tile, sse_view;
     bool rendered = false, has_gt = false;
+    std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
 
     explicit Batch(Context* c) : ctx(c) {}
 
@@ -260,21 +284,22 @@ struct Batch {
         tile_offsets.ensure(n_tiles + 1);
         cursor.ensure(n_tiles + 1);
         total.ensure(1);
-        err.ensure(2);
+        err.ensure(1 + std::max(V, 1));
         overflow.ensure(n_tiles + 1);
         overflow_count.ensure(1);
         SLM_CUDA_CHECK(cudaMemsetAsync(tile_count.p, 0, sizeof(int) * (n_tiles + 1), st));
-        SLM_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int) * 2, st));
+        SLM_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int) * (1 + V), st));
         SLM_CUDA_CHECK(cudaMemsetAsync(overflow_count.p, 0, sizeof(int), st));
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p, tile_count.p, err.p, st);
         launch_scan_tiles(tile_count.p, n_tiles, tile_offsets.p, cursor.p, total.p, st);
         ctx->check_launch();
         long long hdr[2];
-        int herr = 0;
+        std::vector<int> herr(1 + V);
         SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
-        SLM_CUDA_CHECK(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(herr.data(), err.p, sizeof(int) * (1 + V), cudaMemcpyDeviceToHost, st));
         ctx->sync();
-        if (herr) throw std::domain_error("zero-norm quaternion");
+        if (herr[0]) throw std::domain_error("zero-norm quaternion");
+        valid_count.assign(herr.begin() + 1, herr.end());
         n_entries = hdr[0];
         if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
         entries.ensure(std::max<long long>(n_entries, 1));
@@ -445,11 +470,16 @@ struct Jacobian {
     // out = J^T W J p + lambda p, device f32 SoA; allreduced across ranks.
     void gn_apply_dev(float lambda, const float* dp, float* dout, const int* done = nullptr) {
         cudaStream_t st = ctx->stream;
+        std::array<cudaEvent_t, 4> ev{};
+        const bool prof = ctx->prof;
+        if (prof) ctx->prof_record(ev, 0);
         launch_tangents(scene->beta.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                         tan.p, done, st);
+        if (prof) ctx->prof_record(ev, 1);
         SampleArgs a = args();
         a.done_flag = done;
         launch_sample_raster(kGn, a, st);
+        if (prof) ctx->prof_record(ev, 2);
         if (ctx->world > 1) {
             launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                          inter.p, nullptr, 0.f, dout, done, st);
@@ -458,6 +488,10 @@ struct Jacobian {
         } else {
             launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                          inter.p, dp, lambda, dout, done, st);
+        }
+        if (prof) {
+            ctx->prof_record(ev, 3);
+            ctx->prof_events.push_back(ev);
         }
         ctx->check_launch();
     }
@@ -1118,6 +1152,12 @@ int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n) {
     });
 }
 long long slm_launch_count(void) { return g_launches.load(); }
+int slm_context_set_profiling(slm_context* ctx, int on) {
+    return guarded([&] { ctx->impl.prof = on != 0; });
+}
+int slm_context_profile_collect(slm_context* ctx, double out[3], int* n) {
+    return guarded([&] { ctx->impl.prof_collect(out, n); });
+}
 
 int slm_nccl_unique_id(uint8_t out[128]) {
     return guarded([&] {
@@ -1413,10 +1453,10 @@ int slm_jacobian_device_ptrs(slm_jacobian* j, void* stream_out[1]) {
     return SLM_OK;
 }
 int slm_jacobian_stats(slm_jacobian* j, int64_t* out) {
-    // [views, G_valid_sum (unknown: 0), entries, samples, groups, tiles]
+    // [views, sum_v G_v, entries, samples, groups, tiles]
     Batch& b = *j->jac->batch;
     out[0] = b.V;
-    out[1] = 0;
+    out[1] = std::accumulate(b.valid_count.begin(), b.valid_count.end(), 0ll);
     out[2] = b.n_entries;
     out[3] = j->jac->samples.total;
     out[4] = static_cast<int64_t>(j->jac->samples.hgroups.size());

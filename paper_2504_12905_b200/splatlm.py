@@ -48,6 +48,8 @@ _SIGS = {
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
     "slm_launch_count": (C.c_longlong, []),
+    "slm_context_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "slm_context_profile_collect": (C.c_int, [_vp, _f64p, _i32p]),
     "slm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "slm_context_init_comm": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
     "slm_context_rank": (C.c_int, [_vp, _i32p, _i32p]),
@@ -309,6 +311,16 @@ class Lib(HostSampler):
 
     def launch_count(self) -> int:
         return self.dll.slm_launch_count()
+
+    def set_profiling(self, on: bool):
+        self._check(self.dll.slm_context_set_profiling(self.ctx, 1 if on else 0))
+
+    def profile_collect(self) -> dict:
+        """Summed ms of {tangents, raster, chain} over the profiled products."""
+        out = np.zeros(3)
+        n = C.c_int32()
+        self._check(self.dll.slm_context_profile_collect(self.ctx, f64ptr(out), C.byref(n)))
+        return dict(n=n.value, tangents_ms=out[0], raster_ms=out[1], chain_ms=out[2])
 
     # ---- multi-GPU
     @staticmethod
@@ -575,7 +587,7 @@ class Jacobian:
     def stats(self) -> dict:
         out = np.zeros(6, np.int64)
         self.L.dll.slm_jacobian_stats(self.h, i64ptr(out))
-        return dict(views=int(out[0]), entries=int(out[2]), samples=int(out[3]), groups=int(out[4]),
+        return dict(views=int(out[0]), valid=int(out[1]), entries=int(out[2]), samples=int(out[3]), groups=int(out[4]),
                     tiles=int(out[5]))
 
 
