@@ -57,6 +57,13 @@ def parse():
     return ap.parse_args()
 
 
+T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    print(f"[bench {time.perf_counter() - T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -85,11 +92,15 @@ def sub_plan(plan: SamplePlan, lo: int, hi: int) -> SamplePlan:
 
 
 def gt_scene(count: int, seed: int = 20214) -> GaussianSet:
-    """Ground-truth scene with generate_toy_scene's distributions (scene_gen.cpp:47-66)."""
+    """Ground-truth scene with generate_toy_scene's distributions (scene_gen.cpp:47-66),
+    scales shrunk by (20/count)^(1/3) so the scene keeps the toy scene's density
+    (20 Gaussians): the toy scales at 500k Gaussians would cover every pixel with
+    ~10^4 splats, which is not a scene anyone fits."""
     r = np.random.default_rng(seed)
     g = GaussianSet(count)
+    s = (20.0 / count) ** (1.0 / 3.0)
     g.means = r.uniform(-0.8, 0.8, 3 * count)
-    g.log_scales = r.uniform(math.log(0.12), math.log(0.35), 3 * count)
+    g.log_scales = r.uniform(math.log(0.12 * s), math.log(0.35 * s), 3 * count)
     g.colors = r.uniform(-1.2, 1.2, 3 * count)
     q = r.uniform(-1, 1, (count, 4))
     q /= np.linalg.norm(q, axis=1, keepdims=True)
@@ -247,6 +258,7 @@ def run_b200(args):
 
     t_setup = time.perf_counter()
     state, cams, clusters, batch, plan = host_inputs(L, args, world)
+    log(f"host inputs: G={args.gaussians}, batch={batch}, samples={plan.total_samples()}")
     lo, hi = rank * args.batch, (rank + 1) * args.batch
     scene = splatlm.Scene(L, state)
     # Global N_total weights, this rank's views: slice the plan but keep weights
@@ -254,6 +266,7 @@ def run_b200(args):
     my_plan = sub_plan(plan, lo, hi)
     jac = scene.jacobian([cams[i] for i in batch[lo:hi]], my_plan)
     stats = jac.stats()
+    log(f"jacobian ready: {stats}")
     P = 14 * scene.padded
     p = torch.empty(P, device="cuda", dtype=torch.float32).uniform_(-1, 1)
     u = torch.zeros(P, device="cuda", dtype=torch.float32)
@@ -280,6 +293,7 @@ def run_b200(args):
         torch.cuda.synchronize()
     launches = L.launch_count() - launches0
     ms = start.elapsed_time(end)
+    log(f"timed {args.steps} products: {ms / args.steps:.3f} ms each")
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -295,6 +309,7 @@ def run_b200(args):
             product()
     prof = L.profile_collect()
     L.set_profiling(False)
+    log(f"profile: {prof}")
     n = max(prof["n"], 1)
     raster_ms = prof["raster_ms"] / n
     bytes_ = algorithmic_bytes(stats)
@@ -319,6 +334,7 @@ def run_b200(args):
         e2e_s = float(t.item())
     del host_jac
     e2e_value = world / e2e_s
+    log(f"e2e host gn_apply: {e2e_s * 1000:.1f} ms")
 
     # LM iterations/s on the device-resident scene (lm_step, lm.cpp:56-157)
     lm = None
@@ -326,6 +342,7 @@ def run_b200(args):
         gt = splatlm.Scene(L, gt_scene(args.gaussians // 2))
         imgs = [gt.render(c)[0] for c in cams]
         del gt
+        log("ground truth rendered")
         td = L.train_data(cams, imgs)
         del imgs
         td.set_clusters(clusters)
@@ -334,6 +351,7 @@ def run_b200(args):
                        batch_size_late=args.batch * world, samples_per_tile=args.spt)
         rng = L.rng(1)
         L.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)  # same stream position as train_run
+        L.set_timing(True)
         with torch.cuda.stream(stream):
             rep = lm_scene.lm_step(td, cfg, 0, rng)
             torch.cuda.synchronize()
@@ -349,6 +367,7 @@ def run_b200(args):
             t = torch.tensor([lm_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             lm_ms = float(t.item())
+        log(f"lm_step: {lm_ms:.1f} ms/step, stages {L.timings()}")
         lm = {"lm_iters_per_s": 1000.0 / lm_ms, "ms_per_lm_step": lm_ms, "pcg_iters": 8,
               "loss_before_first": rep.loss_before, "loss_after_last": reps[-1].loss_after}
 
@@ -357,7 +376,9 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
+            log("cpu baseline")
             cval, ctimes, meta = cpu_sample(args, args.cpu_views, 2, 1)
+            log(f"cpu baseline: {cval:.4f} matvec/s ({meta['kind']}, {meta['cores']} cores)")
             cpu = {"value": cval, "unit": UNIT, "cores": meta["cores"], "kind": meta["kind"],
                    "sample": meta["sample"]}
         except Exception as e:  # the checker is optional on a box without the build

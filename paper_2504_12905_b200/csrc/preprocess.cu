@@ -177,10 +177,18 @@ __global__ void k_scan_tiles(const int* __restrict__ count, int n, int* __restri
                              int* __restrict__ cursor, long long* __restrict__ total_out) {
     __shared__ long long part[1024];
     const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ int smax;
     const int per = (n + nt - 1) / nt;
     const int lo = tid * per, hi = min(n, lo + per);
     long long s = 0;
-    for (int i = lo; i < hi; ++i) s += count[i];
+    int mx = 0;
+    if (tid == 0) smax = 0;
+    __syncthreads();
+    for (int i = lo; i < hi; ++i) {
+        s += count[i];
+        mx = max(mx, count[i]);
+    }
+    atomicMax(&smax, mx);
     part[tid] = s;
     __syncthreads();
     for (int off = 1; off < nt; off <<= 1) {  // Hillis-Steele inclusive scan of partials
@@ -197,7 +205,8 @@ __global__ void k_scan_tiles(const int* __restrict__ count, int n, int* __restri
     }
     if (tid == nt - 1) {
         offsets[n] = (int)part[nt - 1];
-        *total_out = part[nt - 1];
+        total_out[0] = part[nt - 1];
+        total_out[1] = smax;  // longest tile list: sizes the big-tile sort scratch
     }
 }
 
@@ -287,54 +296,114 @@ __global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ offse
     for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = sval[i];
 }
 
-// Overflow tiles (n > 2048): persistent CTAs with up to 16384 entries in
-// dynamic shared memory; anything larger falls back to an in-place
-// odd-even transposition sort in global memory (correct, slow, rare).
+// Overflow tiles (n > 2048): persistent CTAs with up to 16384 entries sorted
+// in dynamic shared memory.  Longer lists are sorted in 16384-entry chunks in
+// smem and then merged pairwise in global scratch with a merge-path split
+// per thread (log2(n/16384) passes), so any list length is handled.
 constexpr int kBigCap = 16384;
+
+__device__ __forceinline__ void load_pad(const int* __restrict__ src, int n, int np2,
+                                         const unsigned long long* __restrict__ keys, size_t vbase,
+                                         unsigned long long* skey, int* sval) {
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+        if (i < n) {
+            const int g = src[i];
+            skey[i] = keys[vbase + g];
+            sval[i] = g;
+        } else {
+            skey[i] = ~0ull;
+            sval[i] = 0x7fffffff;
+        }
+    }
+    __syncthreads();
+}
+
+// Merge sorted runs A=[a0,a1) and B=[a1,b1) of (ka,va) into (kd,vd), whole CTA.
+__device__ void merge_runs(const unsigned long long* __restrict__ ka, const int* __restrict__ va,
+                           unsigned long long* __restrict__ kd, int* __restrict__ vd, int a0, int a1,
+                           int b1) {
+    const int la = a1 - a0, lb = b1 - a1, m = la + lb;
+    const int T = blockDim.x;
+    const int d0 = static_cast<int>(static_cast<long long>(m) * threadIdx.x / T);
+    const int d1 = static_cast<int>(static_cast<long long>(m) * (threadIdx.x + 1) / T);
+    auto split = [&](int d) {  // number of A elements among the first d merged outputs
+        int lo = max(0, d - lb), hi = min(d, la);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int j = d - 1 - mid;
+            if (!pair_gt(ka[a0 + mid], va[a0 + mid], ka[a1 + j], va[a1 + j])) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    int i = split(d0), j = d0 - i;
+    for (int d = d0; d < d1; ++d) {
+        bool take_a;
+        if (i >= la) take_a = false;
+        else if (j >= lb) take_a = true;
+        else take_a = !pair_gt(ka[a0 + i], va[a0 + i], ka[a1 + j], va[a1 + j]);
+        if (take_a) {
+            kd[a0 + d] = ka[a0 + i];
+            vd[a0 + d] = va[a0 + i];
+            ++i;
+        } else {
+            kd[a0 + d] = ka[a1 + j];
+            vd[a0 + d] = va[a1 + j];
+            ++j;
+        }
+    }
+}
 
 __global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ offsets,
                                                         int* __restrict__ entries,
                                                         const unsigned long long* __restrict__ keys,
                                                         const int* __restrict__ tile_view, int Gp,
                                                         const int* __restrict__ overflow,
-                                                        const int* __restrict__ overflow_count) {
+                                                        const int* __restrict__ overflow_count,
+                                                        unsigned long long* __restrict__ scratch_k,
+                                                        int* __restrict__ scratch_v, long long max_n) {
     extern __shared__ unsigned char smem_raw[];
     unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem_raw);
     int* sval = reinterpret_cast<int*>(smem_raw + sizeof(unsigned long long) * kBigCap);
     const int cnt = *overflow_count;
+    unsigned long long* kA = scratch_k ? scratch_k + 2 * max_n * blockIdx.x : nullptr;
+    unsigned long long* kB = kA ? kA + max_n : nullptr;
+    int* vA = scratch_v ? scratch_v + 2 * max_n * blockIdx.x : nullptr;
+    int* vB = vA ? vA + max_n : nullptr;
     for (int w = blockIdx.x; w < cnt; w += gridDim.x) {
         const int tile = overflow[w];
         const int b = offsets[tile], n = offsets[tile + 1] - b;
         const size_t vbase = static_cast<size_t>(tile_view[tile]) * Gp;
         if (n <= kBigCap) {
-            const int np2 = next_pow2(n);
-            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-                if (i < n) {
-                    const int g = entries[b + i];
-                    skey[i] = keys[vbase + g];
-                    sval[i] = g;
-                } else {
-                    skey[i] = ~0ull;
-                    sval[i] = 0x7fffffff;
-                }
-            }
-            __syncthreads();
-            bitonic_smem(skey, sval, np2);
+            load_pad(entries + b, n, next_pow2(n), keys, vbase, skey, sval);
+            bitonic_smem(skey, sval, next_pow2(n));
             for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = sval[i];
             __syncthreads();
-        } else {
-            int* e = entries + b;
-            for (int phase = 0; phase < n; ++phase) {
-                for (int i = 2 * threadIdx.x + (phase & 1); i + 1 < n; i += 2 * blockDim.x) {
-                    const int ga = e[i], gb = e[i + 1];
-                    if (pair_gt(keys[vbase + ga], ga, keys[vbase + gb], gb)) {
-                        e[i] = gb;
-                        e[i + 1] = ga;
-                    }
-                }
-                __syncthreads();
-            }
+            continue;
         }
+        for (int c0 = 0; c0 < n; c0 += kBigCap) {  // sorted chunks -> scratch A
+            const int cn = min(kBigCap, n - c0);
+            load_pad(entries + b + c0, cn, next_pow2(cn), keys, vbase, skey, sval);
+            bitonic_smem(skey, sval, next_pow2(cn));
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+                kA[c0 + i] = skey[i];
+                vA[c0 + i] = sval[i];
+            }
+            __syncthreads();
+        }
+        unsigned long long *ks = kA, *kd = kB;
+        int *vs = vA, *vd = vB;
+        for (int width = kBigCap; width < n; width <<= 1) {
+            for (int a0 = 0; a0 < n; a0 += 2 * width) {
+                const int a1 = min(a0 + width, n), b1 = min(a0 + 2 * width, n);
+                merge_runs(ks, vs, kd, vd, a0, a1, b1);
+            }
+            __syncthreads();
+            unsigned long long* tk = ks; ks = kd; kd = tk;
+            int* tv = vs; vs = vd; vd = tv;
+        }
+        for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = vs[i];
+        __syncthreads();
     }
 }
 
@@ -409,6 +478,7 @@ void launch_bin_scatter(int G, int Gp, int V, const DevCam* cams, const short4* 
 
 void launch_tile_sort(const int* offsets, int* entries, const unsigned long long* keys,
                       const int* tile_view, int n_tiles, int Gp, int* overflow, int* overflow_count,
+                      unsigned long long* scratch_k, int* scratch_v, long long max_n, int big_blocks,
                       cudaStream_t st) {
     if (n_tiles == 0) return;
     k_tile_sort<2048><<<n_tiles, 256, 0, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
@@ -419,8 +489,8 @@ void launch_tile_sort(const int* offsets, int* entries, const unsigned long long
         cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_tile_sort_big<<<148, 1024, smem, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
-                                             overflow_count); ++g_launches;
+    k_tile_sort_big<<<big_blocks, 1024, smem, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
+                                                    overflow_count, scratch_k, scratch_v, max_n); ++g_launches;
 }
 
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta,

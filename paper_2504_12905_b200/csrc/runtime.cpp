@@ -237,6 +237,9 @@ struct Batch {
     DevBuf<double> sse_tile, sse_view;
     bool rendered = false, has_gt = false;
     std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
+    long long max_list = 0;        // longest tile list of the batch
+    DevBuf<unsigned long long> scratch_k;
+    DevBuf<int> scratch_v;
 
     explicit Batch(Context* c) : ctx(c) {}
 
@@ -283,7 +286,7 @@ struct Batch {
         tile_count.ensure(n_tiles + 1);
         tile_offsets.ensure(n_tiles + 1);
         cursor.ensure(n_tiles + 1);
-        total.ensure(1);
+        total.ensure(2);
         err.ensure(1 + std::max(V, 1));
         overflow.ensure(n_tiles + 1);
         overflow_count.ensure(1);
@@ -295,7 +298,7 @@ struct Batch {
         ctx->check_launch();
         long long hdr[2];
         std::vector<int> herr(1 + V);
-        SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(herr.data(), err.p, sizeof(int) * (1 + V), cudaMemcpyDeviceToHost, st));
         ctx->sync();
         if (herr[0]) throw std::domain_error("zero-norm quaternion");
@@ -304,8 +307,16 @@ struct Batch {
         if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
         entries.ensure(std::max<long long>(n_entries, 1));
         launch_bin_scatter(G, Gp, V, cams.p, rect.p, cursor.p, entries.p, st);
+        max_list = hdr[1];
+        // lists longer than the 16384-entry smem sort need chunk+merge scratch
+        const int big_blocks = 148;
+        if (max_list > 16384) {
+            scratch_k.ensure(static_cast<size_t>(2) * big_blocks * max_list);
+            scratch_v.ensure(static_cast<size_t>(2) * big_blocks * max_list);
+        }
         launch_tile_sort(tile_offsets.p, entries.p, keys.p, tile_view.p, n_tiles, Gp, overflow.p,
-                         overflow_count.p, st);
+                         overflow_count.p, max_list > 16384 ? scratch_k.p : nullptr,
+                         max_list > 16384 ? scratch_v.p : nullptr, max_list, big_blocks, st);
         ctx->check_launch();
         rendered = false;
         has_gt = false;

@@ -70,6 +70,7 @@ void launch_bin_scatter(int G, int Gp, int V, const DevCam* cams, const short4* 
                         int* entries, cudaStream_t st);
 void launch_tile_sort(const int* offsets, int* entries, const unsigned long long* keys,
                       const int* tile_view, int n_tiles, int Gp, int* overflow, int* overflow_count,
+                      unsigned long long* scratch_k, int* scratch_v, long long max_n, int big_blocks,
                       cudaStream_t st);
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta, float* beta32,
                          cudaStream_t st);

@@ -300,3 +300,23 @@ def test_lm_step_fixed_point(gpu, port):
     r = gpu.lm_step(st, td, LmConfig(batch_size_initial=4), 0, gpu.rng(94))
     assert r.loss_before < 1e-10
     assert np.max(np.abs(st.pack() - gt.pack())) < 1e-5
+
+
+@pytest.mark.parametrize("count", [3000, 20000])
+def test_long_tile_lists_sorted_exactly(gpu, port, count):
+    """Lists beyond the 2048-entry CTA sort (smem 16384 path) and beyond 16384
+    (chunk + merge-path path) still match the reference order bit for bit."""
+    from paper_2504_12905_b200.types import GaussianSet
+    r = np.random.default_rng(count)
+    g = GaussianSet(count)
+    g.means = r.uniform(-0.3, 0.3, 3 * count)
+    g.log_scales = np.full(3 * count, np.log(0.6))  # every splat covers the whole image
+    g.rotations = r.uniform(-1, 1, 4 * count)
+    g.renormalize_rotations()
+    g.opacity_logits = r.uniform(-1, 2, count)
+    g.colors = r.uniform(-1, 1, 3 * count)
+    cam = tcam(48, 3.0)
+    oo, io = port.bin_and_sort(g, cam)
+    og, ig = gpu.bin_and_sort(g, cam)
+    assert int(np.max(np.diff(oo))) > (2048 if count < 10000 else 16384)
+    assert np.array_equal(oo, og) and np.array_equal(io, ig)
