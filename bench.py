@@ -57,6 +57,16 @@ def parse():
     return ap.parse_args()
 
 
+def parse_args_for(gaussians: int):
+    """Default bench arguments (for tools/ drivers)."""
+    saved = sys.argv
+    sys.argv = [saved[0], "--gaussians", str(gaussians)]
+    try:
+        return parse()
+    finally:
+        sys.argv = saved
+
+
 T0 = time.perf_counter()
 
 
