@@ -60,6 +60,9 @@ struct SampleArgs {
     float* out_res;       // JVP: Jv in plan order
     float* inter;         // J^T accumulators [(v*Gp+g)*12 + i]
     const int* done_flag; // optional: skip all work when *done_flag != 0 (PCG converged)
+    const unsigned* masks;      // blend bitmasks [group][window][lane] (k_masks)
+    const long long* mask_off;  // per-group offset into masks, in words
+    unsigned* masks_out;        // k_masks output (same buffer as masks)
 };
 
 struct DiagArgs {
@@ -75,6 +78,8 @@ struct DiagArgs {
     const float* image;
     const int* last_img;
     float* diagacc;
+    const unsigned* masks;
+    const long long* mask_off;
 };
 
 struct CgState {

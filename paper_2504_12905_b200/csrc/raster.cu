@@ -4,20 +4,33 @@
 //                      one CTA per 16x16 tile, splat records staged in smem; writes
 //                      RGB, final T, contrib count and `last` (the list position
 //                      where blend_pixel stopped) and per-tile SSE vs ground truth.
-//  * k_sample_raster   the sampled-pixel passes, one warp per group of <=32 samples
-//                      of one tile (lanes = samples, all lanes walk the same entry):
+//  * k_masks           once per LM step: for every sampled pixel, one bit per tile-list
+//                      entry saying whether blend_pixel blends it (alpha gates passed
+//                      and before `last`).  The gates depend only on the state, not on
+//                      the probe p, so the per-product passes never re-evaluate the
+//                      ~85% of (pixel, entry) pairs that are skipped.
+//  * k_sample_raster   the sampled-pixel products, one warp per group of <=32 samples
+//                      of one tile.  The list is walked in windows of 32 entries; in a
+//                      window every lane iterates only over ITS OWN blended entries
+//                      (its mask word), so lanes do useful work instead of idling
+//                      through a shared entry loop:
 //        JVP   Jv      dual blend (jvp, jacobian.cpp:191-211)
 //        VJP   J^T u   reverse blend into the 9-float intermediate (vjp :219-247)
 //        GN    J^T W J p fused: Jv, *W, J^T in one kernel (gn_apply :339-344)
 //        RHS   J^T(-W r) with r read from the forward render (lm.cpp:99-121)
-//  * k_diag_raster     diag(J^T W J) accumulators (jtj_diag :272-337), factored as
-//                      a per-(tile,Gaussian) 5x5 quadratic form.
+//                      J^T contributions are added into a per-window smem tile
+//                      [32 entries][12] (lanes are mostly at different entries, so
+//                      the shared atomics rarely conflict) and flushed with one
+//                      vector red.global.add per 4 floats per entry.
+//  * k_diag_raster     diag(J^T W J) accumulators (jtj_diag :272-337), factored as a
+//                      per-(tile, Gaussian) 5x5 quadratic form, same
+//                      windowed walk with a [32][20] smem tile.
 //
 // The J^T passes sweep front-to-back: the reference's reverse sweep needs
 // suffix_c = sum_{j>k} w_j c_j (backward_pixel_vjp :67-94); with the pixel's
 // final colour C from the forward render, suffix = C - prefix_incl(k), and
 // prefix is accumulated with the very same FP32 operations as the forward
-// render, so the gate decisions and sums replay exactly.
+// render, so gate decisions and sums replay exactly.
 #include <cstdint>
 
 #include <atomic>
@@ -121,57 +134,102 @@ __global__ void k_sse_views(const DevCam* __restrict__ cams, int V, int n_tiles_
     if (threadIdx.x == 0) sse_view[v] = s;
 }
 
-// ------------------------------------------------------------------ sampled passes
-// Reduce one 9-float intermediate over the warp and add it to global memory.
-__device__ __forceinline__ void warp_accumulate9(const float (&gv)[9], unsigned mask, float* dst,
-                                                 int lane) {
-    if (__popc(mask) == 1) {
-        if ((mask >> lane) & 1u) {
-#pragma unroll
-            for (int i = 0; i < 9; ++i) atomicAdd(dst + i, gv[i]);
-        }
+// ------------------------------------------------------------------ group setup
+struct GroupCtx {
+    bool active;
+    int s, orig, px, py, mylast, maxlast;
+    size_t pix, vbase;
+    const int* list;
+    float pxc, pyc;
+    const unsigned* masks;  // this group's mask words: [window][lane]
+};
+
+__device__ __forceinline__ bool setup_group(const Group* groups, int n_groups, const DevCam* cams,
+                                            const int* tile_offsets, const int* entries,
+                                            const int* spix, const int* sorig, const int* last_img,
+                                            const unsigned* masks, const long long* mask_off, int Gp,
+                                            int gi, int lane, GroupCtx& c) {
+    if (gi >= n_groups) return false;
+    const Group grp = groups[gi];
+    const DevCam& cam = cams[grp.view];
+    c.active = lane < grp.count;
+    c.s = grp.begin + (c.active ? lane : 0);
+    const int packed = spix[c.s];
+    c.px = packed & 0xffff;
+    c.py = packed >> 16;
+    c.orig = sorig ? sorig[c.s] : 0;
+    c.pix = cam.pix_base + static_cast<size_t>(c.py) * cam.width + c.px;
+    c.mylast = c.active ? last_img[c.pix] : 0;
+    c.maxlast = __reduce_max_sync(0xffffffffu, c.mylast);
+    c.list = entries + tile_offsets[cam.tile_base + grp.tile];
+    c.vbase = static_cast<size_t>(grp.view) * Gp;
+    c.pxc = (float)c.px + 0.5f;
+    c.pyc = (float)c.py + 0.5f;
+    c.masks = masks ? masks + mask_off[gi] : nullptr;
+    return true;
+}
+
+// ------------------------------------------------------------------ masks
+// One warp per group: bit k of word [w][lane] = entry 32w+k is blended at the
+// lane's pixel (same eval_alpha as k_render, and k < last).
+__global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
+    __shared__ float4 s_rec[4][32][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    GroupCtx c;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, nullptr,
+                     A.last_img, nullptr, nullptr, A.Gp, blockIdx.x * 4 + warp, lane, c))
         return;
+    unsigned* out = A.masks_out + A.mask_off[blockIdx.x * 4 + warp];
+    for (int base = 0, w = 0; base < c.maxlast; base += 32, ++w) {
+        const int j = base + lane;
+        if (j < c.maxlast) {
+            const float4* r = A.rec + 3 * (c.vbase + c.list[j]);
+            s_rec[warp][lane][0] = r[0];
+            s_rec[warp][lane][1] = r[1];
+        }
+        __syncwarp();
+        const int m = min(32, c.mylast - base);
+        unsigned bits = 0u;
+        for (int k = 0; k < m; ++k) {
+            Alpha a;
+            if (eval_alpha(s_rec[warp][k][0], s_rec[warp][k][1], c.pxc, c.pyc, a)) bits |= 1u << k;
+        }
+        out[w * 32 + lane] = bits;
+        __syncwarp();
     }
-    float mine = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-        const float s = warp_sum(gv[i]);
-        if (lane == i) mine = s;
-    }
-    if (lane < 9) atomicAdd(dst + lane, mine);
+}
+
+// ------------------------------------------------------------------ products
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     __shared__ float4 s_rec[4][32][3];
     __shared__ float4 s_tan[4][32][3];
+    __shared__ __align__(16) float s_acc[4][32][12];
     __shared__ int s_g[4][32];
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gi = blockIdx.x * 4 + warp;
-    if (gi >= A.n_groups) return;
-    const Group grp = A.groups[gi];
-    const DevCam& cam = A.cams[grp.view];
-    const bool active = lane < grp.count;
-    const int s = grp.begin + (active ? lane : 0);
-    const int packed = A.spix[s];
-    const int px = packed & 0xffff, py = packed >> 16;
-    const int orig = A.sorig[s];
-    const size_t pix = cam.pix_base + static_cast<size_t>(py) * cam.width + px;
-    const int mylast = active ? A.last_img[pix] : 0;
-    const int maxlast = __reduce_max_sync(0xffffffffu, mylast);
-    const int* list = A.entries + A.tile_offsets[cam.tile_base + grp.tile];
-    const size_t vbase = static_cast<size_t>(grp.view) * A.Gp;
-    const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;
+    GroupCtx c;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, A.sorig,
+                     A.last_img, A.masks, A.mask_off, A.Gp, blockIdx.x * 4 + warp, lane, c))
+        return;
     constexpr float kLn2f = 0.69314718055994530942f;
+    const int nwin = (c.maxlast + 31) >> 5;
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     if (MODE == kJvp || MODE == kGn) {
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
-        for (int base = 0; base < maxlast; base += 32) {
-            const int j = base + lane;
-            if (j < maxlast) {
-                const size_t rg = vbase + list[j];
+        for (int w = 0; w < nwin; ++w) {
+            unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
+            const unsigned un = __reduce_or_sync(0xffffffffu, m);
+            if (!un) continue;
+            if ((un >> lane) & 1u) {
+                const size_t rg = c.vbase + c.list[w * 32 + lane];
                 const float4* r = A.rec + 3 * rg;
                 const float4* t = A.tan + 3 * rg;
                 s_rec[warp][lane][0] = r[0];
@@ -182,119 +240,124 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
                 s_tan[warp][lane][2] = t[2];
             }
             __syncwarp();
-            const int m = min(32, maxlast - base);
-            for (int k = 0; k < m; ++k) {
-                if (base + k >= mylast) continue;
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
                 const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
                 Alpha a;
-                if (!eval_alpha(r0, r1, pxc, pyc, a)) continue;
+                eval_alpha(r0, r1, c.pxc, c.pyc, a);  // blended: the mask already decided
                 const float4 t0 = s_tan[warp][k][0], t1 = s_tan[warp][k][1];
-                const float4 t2 = s_tan[warp][k][2];
+                const float db = s_tan[warp][k][2].x;
                 const float alpha = a.alpha, dx = a.dx, dy = a.dy;
-                // natural conic from the log2-scaled record
-                const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
                 float dalpha = 0.0f;
                 if (!a.clamped) {
+                    const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
                     const float dpow = -(ca * dx + cb * dy) * t0.x - (cb * dx + cc * dy) * t0.y -
                                        0.5f * dx * dx * t0.z - dx * dy * t0.w - 0.5f * dy * dy * t1.x;
                     dalpha = alpha * dpow + (alpha / r1.y) * t1.y;
                 }
-                const float w = alpha * T;
+                const float wgt = alpha * T;
                 const float dw = dalpha * T + alpha * dT;
-                dC0 += dw * r1.z + w * t1.z;
-                dC1 += dw * r1.w + w * t1.w;
-                dC2 += dw * s_rec[warp][k][2].x + w * t2.x;
-                const float om = 1.0f - alpha;
-                dT = dT * om - T * dalpha;
+                dC0 += dw * r1.z + wgt * t1.z;
+                dC1 += dw * r1.w + wgt * t1.w;
+                dC2 += dw * s_rec[warp][k][2].x + wgt * db;
+                dT = dT * (1.0f - alpha) - T * dalpha;
                 T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
             }
             __syncwarp();
         }
         if (MODE == kJvp) {
-            if (active) {
-                A.out_res[3 * orig] = dC0;
-                A.out_res[3 * orig + 1] = dC1;
-                A.out_res[3 * orig + 2] = dC2;
+            if (c.active) {
+                A.out_res[3 * c.orig] = dC0;
+                A.out_res[3 * c.orig + 1] = dC1;
+                A.out_res[3 * c.orig + 2] = dC2;
             }
             return;
         }
-        if (active) {
-            u0 = A.sw[3 * s] * dC0;
-            u1 = A.sw[3 * s + 1] * dC1;
-            u2 = A.sw[3 * s + 2] * dC2;
+        if (c.active) {
+            u0 = A.sw[3 * c.s] * dC0;
+            u1 = A.sw[3 * c.s + 1] * dC1;
+            u2 = A.sw[3 * c.s + 2] * dC2;
         }
     } else if (MODE == kVjp) {
-        if (active) {
-            u0 = A.in_res[3 * orig];
-            u1 = A.in_res[3 * orig + 1];
-            u2 = A.in_res[3 * orig + 2];
+        if (c.active) {
+            u0 = A.in_res[3 * c.orig];
+            u1 = A.in_res[3 * c.orig + 1];
+            u2 = A.in_res[3 * c.orig + 2];
         }
     } else {  // kRhs: u = -w (rendered - truth)
-        if (active) {
-            const float* gp = A.gt + 3 * pix;
-            u0 = -A.sw[3 * s] * (A.image[3 * pix] - gp[0]);
-            u1 = -A.sw[3 * s + 1] * (A.image[3 * pix + 1] - gp[1]);
-            u2 = -A.sw[3 * s + 2] * (A.image[3 * pix + 2] - gp[2]);
+        if (c.active) {
+            const float* gp = A.gt + 3 * c.pix;
+            u0 = -A.sw[3 * c.s] * (A.image[3 * c.pix] - gp[0]);
+            u1 = -A.sw[3 * c.s + 1] * (A.image[3 * c.pix + 1] - gp[1]);
+            u2 = -A.sw[3 * c.s + 2] * (A.image[3 * c.pix + 2] - gp[2]);
         }
     }
 
-    // ---- J^T pass, front to back with suffix = C - inclusive prefix
-    const float Cf0 = active ? A.image[3 * pix] : 0.f;
-    const float Cf1 = active ? A.image[3 * pix + 1] : 0.f;
-    const float Cf2 = active ? A.image[3 * pix + 2] : 0.f;
+    // ---- J^T pass: front to back, suffix = C - inclusive prefix
+    const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
+    const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
+    const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
+    float* acc = &s_acc[warp][0][0];
+    for (int i = lane; i < 32 * 12; i += 32) acc[i] = 0.f;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-    for (int base = 0; base < maxlast; base += 32) {
-        const int j = base + lane;
-        if (j < maxlast) {
-            const int g = list[j];
-            const float4* r = A.rec + 3 * (vbase + g);
+    for (int w = 0; w < nwin; ++w) {
+        unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned un = __reduce_or_sync(0xffffffffu, m);
+        if (!un) continue;
+        if ((un >> lane) & 1u) {
+            const int g = c.list[w * 32 + lane];
+            const float4* r = A.rec + 3 * (c.vbase + g);
             s_rec[warp][lane][0] = r[0];
             s_rec[warp][lane][1] = r[1];
             s_rec[warp][lane][2] = r[2];
             s_g[warp][lane] = g;
         }
         __syncwarp();
-        const int m = min(32, maxlast - base);
-        for (int k = 0; k < m; ++k) {
-            float gv[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            bool blended = false;
-            if (base + k < mylast) {
-                const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
-                Alpha a;
-                if (eval_alpha(r0, r1, pxc, pyc, a)) {
-                    blended = true;
-                    const float alpha = a.alpha, dx = a.dx, dy = a.dy;
-                    const float c2 = s_rec[warp][k][2].x;
-                    const float w = __fmul_rn(alpha, T);
-                    const float n0 = __fmaf_rn(w, r1.z, S0), n1 = __fmaf_rn(w, r1.w, S1),
-                                n2 = __fmaf_rn(w, c2, S2);
-                    const float inv1m = 1.0f / (1.0f - alpha);
-                    const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) +
-                                         u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
-                                         u2 * (T * c2 - (Cf2 - n2) * inv1m);
-                    gv[6] = u0 * w;
-                    gv[7] = u1 * w;
-                    gv[8] = u2 * w;
-                    if (!a.clamped) {
-                        const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w,
-                                    cc = -2.0f * kLn2f * r1.x;
-                        const float dpow = dalpha * alpha;
-                        gv[0] = dpow * -(ca * dx + cb * dy);
-                        gv[1] = dpow * -(cb * dx + cc * dy);
-                        gv[2] = dpow * (-0.5f * dx * dx);
-                        gv[3] = dpow * (-dx * dy);
-                        gv[4] = dpow * (-0.5f * dy * dy);
-                        gv[5] = dalpha * (alpha / r1.y);
-                    }
-                    S0 = n0;
-                    S1 = n1;
-                    S2 = n2;
-                    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                }
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
+            Alpha a;
+            eval_alpha(r0, r1, c.pxc, c.pyc, a);
+            const float alpha = a.alpha, dx = a.dx, dy = a.dy;
+            const float c2 = s_rec[warp][k][2].x;
+            const float wgt = __fmul_rn(alpha, T);
+            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
+                        n2 = __fmaf_rn(wgt, c2, S2);
+            const float inv1m = 1.0f / (1.0f - alpha);
+            const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) + u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
+                                 u2 * (T * c2 - (Cf2 - n2) * inv1m);
+            float* row = acc + k * 12;
+            atomicAdd(row + 6, u0 * wgt);
+            atomicAdd(row + 7, u1 * wgt);
+            atomicAdd(row + 8, u2 * wgt);
+            if (!a.clamped) {
+                const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
+                const float dpow = dalpha * alpha;
+                atomicAdd(row + 0, dpow * -(ca * dx + cb * dy));
+                atomicAdd(row + 1, dpow * -(cb * dx + cc * dy));
+                atomicAdd(row + 2, dpow * (-0.5f * dx * dx));
+                atomicAdd(row + 3, dpow * (-dx * dy));
+                atomicAdd(row + 4, dpow * (-0.5f * dy * dy));
+                atomicAdd(row + 5, dalpha * (alpha / r1.y));
             }
-            const unsigned mask = __ballot_sync(0xffffffffu, blended);
-            if (mask)
-                warp_accumulate9(gv, mask, A.inter + (vbase + s_g[warp][k]) * kRec, lane);
+            S0 = n0;
+            S1 = n1;
+            S2 = n2;
+            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+        }
+        __syncwarp();
+        if ((un >> lane) & 1u) {  // flush entry `lane` of the window
+            float4* src = reinterpret_cast<float4*>(acc + lane * 12);
+            const float4 a0 = src[0], a1 = src[1], a2 = src[2];
+            src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            src[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            float* dst = A.inter + (c.vbase + s_g[warp][lane]) * kRec;
+            red_add_v4(dst, a0.x, a0.y, a0.z, a0.w);
+            red_add_v4(dst + 4, a1.x, a1.y, a1.z, a1.w);
+            atomicAdd(dst + 8, a2.x);
         }
         __syncwarp();
     }
@@ -311,101 +374,84 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
 // dsig and dcol (chain.cu).  Layout per (view, Gaussian): 20 floats.
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     __shared__ float4 s_rec[4][32][3];
+    __shared__ __align__(16) float s_acc[4][32][kDiagRec];
     __shared__ int s_g[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gi = blockIdx.x * 4 + warp;
-    if (gi >= A.n_groups) return;
-    const Group grp = A.groups[gi];
-    const DevCam& cam = A.cams[grp.view];
-    const bool active = lane < grp.count;
-    const int s = grp.begin + (active ? lane : 0);
-    const int packed = A.spix[s];
-    const int px = packed & 0xffff, py = packed >> 16;
-    const size_t pix = cam.pix_base + static_cast<size_t>(py) * cam.width + px;
-    const int mylast = active ? A.last_img[pix] : 0;
-    const int maxlast = __reduce_max_sync(0xffffffffu, mylast);
-    const int* list = A.entries + A.tile_offsets[cam.tile_base + grp.tile];
-    const size_t vbase = static_cast<size_t>(grp.view) * A.Gp;
-    const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;
-    const float W0 = active ? A.sw[3 * s] : 0.f, W1 = active ? A.sw[3 * s + 1] : 0.f,
-                W2 = active ? A.sw[3 * s + 2] : 0.f;
-    const float Cf0 = active ? A.image[3 * pix] : 0.f;
-    const float Cf1 = active ? A.image[3 * pix + 1] : 0.f;
-    const float Cf2 = active ? A.image[3 * pix + 2] : 0.f;
+    GroupCtx c;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, nullptr,
+                     A.last_img, A.masks, A.mask_off, A.Gp, blockIdx.x * 4 + warp, lane, c))
+        return;
     constexpr float kLn2f = 0.69314718055994530942f;
+    const int nwin = (c.maxlast + 31) >> 5;
+    const float W0 = c.active ? A.sw[3 * c.s] : 0.f, W1 = c.active ? A.sw[3 * c.s + 1] : 0.f,
+                W2 = c.active ? A.sw[3 * c.s + 2] : 0.f;
+    const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
+    const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
+    const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
+    float* acc = &s_acc[warp][0][0];
+    for (int i = lane; i < 32 * kDiagRec; i += 32) acc[i] = 0.f;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-    for (int base = 0; base < maxlast; base += 32) {
-        const int j = base + lane;
-        if (j < maxlast) {
-            const int g = list[j];
-            const float4* r = A.rec + 3 * (vbase + g);
+    for (int w = 0; w < nwin; ++w) {
+        unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned un = __reduce_or_sync(0xffffffffu, m);
+        if (!un) continue;
+        if ((un >> lane) & 1u) {
+            const int g = c.list[w * 32 + lane];
+            const float4* r = A.rec + 3 * (c.vbase + g);
             s_rec[warp][lane][0] = r[0];
             s_rec[warp][lane][1] = r[1];
             s_rec[warp][lane][2] = r[2];
             s_g[warp][lane] = g;
         }
         __syncwarp();
-        const int m = min(32, maxlast - base);
-        for (int k = 0; k < m; ++k) {
-            float acc[19];
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
+            Alpha a;
+            eval_alpha(r0, r1, c.pxc, c.pyc, a);
+            const float alpha = a.alpha, dx = a.dx, dy = a.dy;
+            const float c2 = s_rec[warp][k][2].x;
+            const float wgt = __fmul_rn(alpha, T);
+            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
+                        n2 = __fmaf_rn(wgt, c2, S2);
+            const float inv1m = 1.0f / (1.0f - alpha);
+            const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
+            const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
+            const float da2 = T * c2 - (Cf2 - n2) * inv1m;
+            float* row = acc + k * kDiagRec;
+            const float w2 = wgt * wgt;
+            atomicAdd(row + 16, W0 * w2);
+            atomicAdd(row + 17, W1 * w2);
+            atomicAdd(row + 18, W2 * w2);
+            if (!a.clamped) {
+                const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
+                const float gp[5] = {-(ca * dx + cb * dy), -(cb * dx + cc * dy), -0.5f * dx * dx, -dx * dy,
+                                     -0.5f * dy * dy};
+                const float sw2 = W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2;
+                const float sdp = alpha * alpha * sw2;
+                int q = 0;
 #pragma unroll
-            for (int i = 0; i < 19; ++i) acc[i] = 0.f;
-            bool blended = false;
-            if (base + k < mylast) {
-                const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
-                Alpha a;
-                if (eval_alpha(r0, r1, pxc, pyc, a)) {
-                    blended = true;
-                    const float alpha = a.alpha, dx = a.dx, dy = a.dy;
-                    const float c2 = s_rec[warp][k][2].x;
-                    const float w = __fmul_rn(alpha, T);
-                    const float n0 = __fmaf_rn(w, r1.z, S0), n1 = __fmaf_rn(w, r1.w, S1),
-                                n2 = __fmaf_rn(w, c2, S2);
-                    const float inv1m = 1.0f / (1.0f - alpha);
-                    const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
-                    const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
-                    const float da2 = T * c2 - (Cf2 - n2) * inv1m;
-                    acc[16] = W0 * w * w;
-                    acc[17] = W1 * w * w;
-                    acc[18] = W2 * w * w;
-                    if (!a.clamped) {
-                        const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w,
-                                    cc = -2.0f * kLn2f * r1.x;
-                        const float gp[5] = {-(ca * dx + cb * dy), -(cb * dx + cc * dy),
-                                             -0.5f * dx * dx, -dx * dy, -0.5f * dy * dy};
-                        const float a2 = alpha * alpha;
-                        const float sdp = a2 * (W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2);
-                        int q = 0;
+                for (int i = 0; i < 5; ++i)
 #pragma unroll
-                        for (int i = 0; i < 5; ++i)
-#pragma unroll
-                            for (int jj = i; jj < 5; ++jj) acc[q++] = sdp * gp[i] * gp[jj];
-                        const float ao = alpha / r1.y;
-                        acc[15] = ao * ao * (W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2);
-                    }
-                    S0 = n0;
-                    S1 = n1;
-                    S2 = n2;
-                    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                }
+                    for (int jj = i; jj < 5; ++jj) atomicAdd(row + q++, sdp * gp[i] * gp[jj]);
+                const float ao = alpha / r1.y;
+                atomicAdd(row + 15, ao * ao * sw2);
             }
-            const unsigned mask = __ballot_sync(0xffffffffu, blended);
-            if (mask) {
-                float* dst = A.diagacc + (vbase + s_g[warp][k]) * kDiagRec;
-                if (__popc(mask) == 1) {
-                    if ((mask >> lane) & 1u) {
+            S0 = n0;
+            S1 = n1;
+            S2 = n2;
+            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+        }
+        __syncwarp();
+        if ((un >> lane) & 1u) {
+            float4* src = reinterpret_cast<float4*>(acc + lane * kDiagRec);
+            float* dst = A.diagacc + (c.vbase + s_g[warp][lane]) * kDiagRec;
 #pragma unroll
-                        for (int i = 0; i < 19; ++i) atomicAdd(dst + i, acc[i]);
-                    }
-                } else {
-                    float mine = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 19; ++i) {
-                        const float sum = warp_sum(acc[i]);
-                        if (lane == i) mine = sum;
-                    }
-                    if (lane < 19) atomicAdd(dst + lane, mine);
-                }
+            for (int q4 = 0; q4 < 5; ++q4) {
+                const float4 v = src[q4];
+                src[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+                red_add_v4(dst + 4 * q4, v.x, v.y, v.z, v.w);
             }
         }
         __syncwarp();
@@ -425,6 +471,11 @@ void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_
                       double* sse_view, cudaStream_t st) {
     if (V == 0) return;
     k_sse_views<<<V, 32, 0, st>>>(cams, V, n_tiles, sse_tile, sse_view); ++g_launches;
+}
+
+void launch_masks(const SampleArgs& a, cudaStream_t st) {
+    if (a.n_groups == 0) return;
+    k_masks<<<(a.n_groups + 3) / 4, 128, 0, st>>>(a); ++g_launches;
 }
 
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st) {

@@ -226,6 +226,7 @@ struct Batch {
     long long n_pix = 0, n_entries = 0;
     std::vector<DevCam> hcams;
     std::vector<int> htile_view;
+    std::vector<int> htile_offsets;  // CSR offsets of the tile lists (host copy)
     DevBuf<DevCam> cams;
     DevBuf<int> tile_view, tile_count, tile_offsets, cursor, entries, overflow, overflow_count, err;
     DevBuf<long long> total;
@@ -300,6 +301,9 @@ struct Batch {
         std::vector<int> herr(1 + V);
         SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(herr.data(), err.p, sizeof(int) * (1 + V), cudaMemcpyDeviceToHost, st));
+        htile_offsets.resize(n_tiles + 1);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(htile_offsets.data(), tile_offsets.p, sizeof(int) * (n_tiles + 1),
+                                       cudaMemcpyDeviceToHost, st));
         ctx->sync();
         if (herr[0]) throw std::domain_error("zero-norm quaternion");
         valid_count.assign(herr.begin() + 1, herr.end());
@@ -359,11 +363,14 @@ struct Samples {
     DevBuf<Group> groups;
     DevBuf<int> spix, sorig;
     DevBuf<float> sw;
+    DevBuf<long long> mask_off;
+    DevBuf<unsigned> masks;
     std::vector<int> order;  // group order -> plan sample index
-    long long total = 0;
+    long long total = 0, mask_words = 0;
 
     void build(Context* ctx, const slm_plan& plan, int view_lo, int view_hi,
-               const std::vector<DevCam>& cams, const std::vector<double>& weights3) {
+               const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets,
+               const std::vector<double>& weights3) {
         hgroups.clear();
         order.clear();
         for (int v = view_lo; v < view_hi; ++v) {
@@ -397,7 +404,19 @@ struct Samples {
             horig[k] = s - static_cast<int>(plan.view_offset[view_lo]);
             for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(s) + c]);
         }
+        // blend bitmasks: 32 words (one per lane) per 32-entry window of the tile list
+        std::vector<long long> hoff(hgroups.size());
+        mask_words = 0;
+        for (size_t g = 0; g < hgroups.size(); ++g) {
+            const int t = cams[hgroups[g].view].tile_base + hgroups[g].tile;
+            const long long n = tile_offsets[t + 1] - tile_offsets[t];
+            hoff[g] = mask_words;
+            mask_words += 32 * ((n + 31) / 32);
+        }
         cudaStream_t st = ctx->stream;
+        mask_off.ensure(std::max<size_t>(hoff.size(), 1));
+        masks.ensure(std::max<long long>(mask_words, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(mask_off.p, hoff.data(), sizeof(long long) * hoff.size(), cudaMemcpyHostToDevice, st));
         groups.ensure(std::max<size_t>(hgroups.size(), 1));
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
@@ -446,7 +465,7 @@ struct Jacobian {
             for (int c = 0; c < 3; ++c) weights[3 * k + c] = plan.weight[s] * inv_total;
         std::vector<double> w_by_plan(3 * static_cast<size_t>(plan.view_offset[hi]), 0.0);
         std::copy(weights.begin(), weights.end(), w_by_plan.begin() + 3 * plan_base);
-        samples.build(ctx, plan, lo, hi, batch->hcams, w_by_plan);
+        samples.build(ctx, plan, lo, hi, batch->hcams, batch->htile_offsets, w_by_plan);
         const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
         tan.ensure(3 * VG);
         inter.ensure(VG * kRec);
@@ -454,6 +473,11 @@ struct Jacobian {
         SLM_CUDA_CHECK(cudaMemsetAsync(inter.p, 0, VG * kRec * sizeof(float), ctx->stream));
         SLM_CUDA_CHECK(cudaMemsetAsync(diagacc.p, 0, VG * kDiagRec * sizeof(float), ctx->stream));
         SLM_CUDA_CHECK(cudaMemsetAsync(tan.p, 0, 3 * VG * sizeof(float4), ctx->stream));
+        // the blend masks depend on the state only: computed once per (state, plan)
+        SampleArgs a = args();
+        a.masks_out = samples.masks.p;
+        launch_masks(a, ctx->stream);
+        ctx->check_launch();
     }
 
     SampleArgs args() const {
@@ -473,6 +497,8 @@ struct Jacobian {
         a.last_img = batch->last.p;
         a.gt = batch->gt.p;
         a.inter = inter.p;
+        a.masks = samples.masks.p;
+        a.mask_off = samples.mask_off.p;
         return a;
     }
 
@@ -529,6 +555,8 @@ struct Jacobian {
         d.image = batch->image.p;
         d.last_img = batch->last.p;
         d.diagacc = diagacc.p;
+        d.masks = samples.masks.p;
+        d.mask_off = samples.mask_off.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V,
                              batch->rec.p, diagacc.p, dout, ctx->stream);

@@ -83,6 +83,7 @@ void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const 
 void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile, double* sse_view,
                       cudaStream_t st);
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);
+void launch_masks(const SampleArgs& a, cudaStream_t st);
 void launch_diag_raster(const DiagArgs& a, cudaStream_t st);
 void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st);
