@@ -210,8 +210,9 @@ template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     __shared__ float4 s_rec[4][32][3];
     __shared__ float4 s_tan[4][32][3];
-    __shared__ __align__(16) float s_acc[4][32][12];
-    __shared__ int s_g[4][32];
+    __shared__ float2 s_pair[4][32][33];  // [pixel lane][entry] (dL/dalpha, alpha*T), padded
+    __shared__ float4 s_pix[4][32];       // per pixel lane: (px+.5, py+.5, u0, u1)
+    __shared__ float s_pu2[4][32];
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     GroupCtx c;
@@ -294,33 +295,44 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         }
     }
 
-    // ---- J^T pass: front to back, suffix = C - inclusive prefix
+    // ---- J^T pass: front to back, suffix = C - inclusive prefix.
+    // Per 32-entry window: phase A (lane = pixel) walks the lane's own blended
+    // entries, keeping T and the colour prefix, and stores per pair
+    // (dL/dalpha, alpha*T) in a [pixel][entry] smem tile; phase B (lane =
+    // entry) gathers its column of pixels (ballot-transposed masks), rebuilds
+    // the 9-float intermediate in registers and adds it to HBM with vector reds.
+    // No shared atomics (they are CAS loops on sm_100a), no 32-lane shuffles.
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
-    float* acc = &s_acc[warp][0][0];
-    for (int i = lane; i < 32 * 12; i += 32) acc[i] = 0.f;
+    s_pix[warp][lane] = make_float4(c.pxc, c.pyc, u0, u1);
+    s_pu2[warp][lane] = u2;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     for (int w = 0; w < nwin; ++w) {
-        unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
-        const unsigned un = __reduce_or_sync(0xffffffffu, m);
+        const unsigned m0 = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned un = __reduce_or_sync(0xffffffffu, m0);
         if (!un) continue;
-        if ((un >> lane) & 1u) {
-            const int g = c.list[w * 32 + lane];
-            const float4* r = A.rec + 3 * (c.vbase + g);
-            s_rec[warp][lane][0] = r[0];
-            s_rec[warp][lane][1] = r[1];
-            s_rec[warp][lane][2] = r[2];
-            s_g[warp][lane] = g;
+        const bool mine = (un >> lane) & 1u;
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0;
+        int gq = 0;
+        if (mine) {
+            gq = c.list[w * 32 + lane];
+            const float4* r = A.rec + 3 * (c.vbase + gq);
+            q0 = r[0];
+            q1 = r[1];
+            q2 = r[2];
+            s_rec[warp][lane][0] = q0;
+            s_rec[warp][lane][1] = q1;
+            s_rec[warp][lane][2] = q2;
         }
         __syncwarp();
-        while (m) {
+        // phase A
+        for (unsigned m = m0; m; m &= m - 1) {
             const int k = __ffs(m) - 1;
-            m &= m - 1;
             const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
             Alpha a;
             eval_alpha(r0, r1, c.pxc, c.pyc, a);
-            const float alpha = a.alpha, dx = a.dx, dy = a.dy;
+            const float alpha = a.alpha;
             const float c2 = s_rec[warp][k][2].x;
             const float wgt = __fmul_rn(alpha, T);
             const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
@@ -328,36 +340,49 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             const float inv1m = 1.0f / (1.0f - alpha);
             const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) + u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
                                  u2 * (T * c2 - (Cf2 - n2) * inv1m);
-            float* row = acc + k * 12;
-            atomicAdd(row + 6, u0 * wgt);
-            atomicAdd(row + 7, u1 * wgt);
-            atomicAdd(row + 8, u2 * wgt);
-            if (!a.clamped) {
-                const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
-                const float dpow = dalpha * alpha;
-                atomicAdd(row + 0, dpow * -(ca * dx + cb * dy));
-                atomicAdd(row + 1, dpow * -(cb * dx + cc * dy));
-                atomicAdd(row + 2, dpow * (-0.5f * dx * dx));
-                atomicAdd(row + 3, dpow * (-dx * dy));
-                atomicAdd(row + 4, dpow * (-0.5f * dy * dy));
-                atomicAdd(row + 5, dalpha * (alpha / r1.y));
-            }
+            s_pair[warp][lane][k] = make_float2(dalpha, wgt);
             S0 = n0;
             S1 = n1;
             S2 = n2;
             T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
         }
+        // transpose the masks: col = pixels that blend entry `lane`
+        unsigned col = 0u;
+        for (unsigned uu = un; uu; uu &= uu - 1) {
+            const int k = __ffs(uu) - 1;
+            const unsigned b = __ballot_sync(0xffffffffu, (m0 >> k) & 1u);
+            if (lane == k) col = b;
+        }
         __syncwarp();
-        if ((un >> lane) & 1u) {  // flush entry `lane` of the window
-            float4* src = reinterpret_cast<float4*>(acc + lane * 12);
-            const float4 a0 = src[0], a1 = src[1], a2 = src[2];
-            src[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-            src[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            src[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-            float* dst = A.inter + (c.vbase + s_g[warp][lane]) * kRec;
-            red_add_v4(dst, a0.x, a0.y, a0.z, a0.w);
-            red_add_v4(dst + 4, a1.x, a1.y, a1.z, a1.w);
-            atomicAdd(dst + 8, a2.x);
+        // phase B
+        if (mine) {
+            const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
+            float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
+            for (; col; col &= col - 1) {
+                const int p = __ffs(col) - 1;
+                const float4 pi = s_pix[warp][p];
+                const float pu2 = s_pu2[warp][p];
+                const float2 pr = s_pair[warp][p][lane];
+                Alpha a;
+                eval_alpha(q0, q1, pi.x, pi.y, a);
+                g6 += pi.z * pr.y;
+                g7 += pi.w * pr.y;
+                g8 += pu2 * pr.y;
+                if (!a.clamped) {
+                    const float dx = a.dx, dy = a.dy;
+                    const float dpow = pr.x * a.alpha;
+                    g0 += dpow * -(ca * dx + cb * dy);
+                    g1 += dpow * -(cb * dx + cc * dy);
+                    g2 += dpow * (-0.5f * dx * dx);
+                    g3 += dpow * (-dx * dy);
+                    g4 += dpow * (-0.5f * dy * dy);
+                    g5 += pr.x * (a.alpha / q1.y);
+                }
+            }
+            float* dst = A.inter + (c.vbase + gq) * kRec;
+            red_add_v4(dst, g0, g1, g2, g3);
+            red_add_v4(dst + 4, g4, g5, g6, g7);
+            atomicAdd(dst + 8, g8);
         }
         __syncwarp();
     }
@@ -372,10 +397,13 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
 // M = sum_pixels s gpow gpow^T (15 floats), sum W_c dalpha_c^2 (alpha/o)^2 (1),
 // and sum W_c (alpha T)^2 per channel (3); k_diag_finalize applies P_j,
 // dsig and dcol (chain.cu).  Layout per (view, Gaussian): 20 floats.
+// Same two-phase window walk as the J^T pass; the pair scalars are
+// (sum_c W_c dalpha_c^2, alpha*T).
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     __shared__ float4 s_rec[4][32][3];
-    __shared__ __align__(16) float s_acc[4][32][kDiagRec];
-    __shared__ int s_g[4][32];
+    __shared__ float2 s_pair[4][32][33];
+    __shared__ float4 s_pix[4][32];
+    __shared__ float s_pw2[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     GroupCtx c;
     if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, nullptr,
@@ -388,29 +416,33 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
-    float* acc = &s_acc[warp][0][0];
-    for (int i = lane; i < 32 * kDiagRec; i += 32) acc[i] = 0.f;
+    s_pix[warp][lane] = make_float4(c.pxc, c.pyc, W0, W1);
+    s_pw2[warp][lane] = W2;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     for (int w = 0; w < nwin; ++w) {
-        unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
-        const unsigned un = __reduce_or_sync(0xffffffffu, m);
+        const unsigned m0 = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned un = __reduce_or_sync(0xffffffffu, m0);
         if (!un) continue;
-        if ((un >> lane) & 1u) {
-            const int g = c.list[w * 32 + lane];
-            const float4* r = A.rec + 3 * (c.vbase + g);
-            s_rec[warp][lane][0] = r[0];
-            s_rec[warp][lane][1] = r[1];
-            s_rec[warp][lane][2] = r[2];
-            s_g[warp][lane] = g;
+        const bool mine = (un >> lane) & 1u;
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0;
+        int gq = 0;
+        if (mine) {
+            gq = c.list[w * 32 + lane];
+            const float4* r = A.rec + 3 * (c.vbase + gq);
+            q0 = r[0];
+            q1 = r[1];
+            q2 = r[2];
+            s_rec[warp][lane][0] = q0;
+            s_rec[warp][lane][1] = q1;
+            s_rec[warp][lane][2] = q2;
         }
         __syncwarp();
-        while (m) {
+        for (unsigned m = m0; m; m &= m - 1) {
             const int k = __ffs(m) - 1;
-            m &= m - 1;
             const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
             Alpha a;
             eval_alpha(r0, r1, c.pxc, c.pyc, a);
-            const float alpha = a.alpha, dx = a.dx, dy = a.dy;
+            const float alpha = a.alpha;
             const float c2 = s_rec[warp][k][2].x;
             const float wgt = __fmul_rn(alpha, T);
             const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
@@ -419,40 +451,55 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
             const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
             const float da2 = T * c2 - (Cf2 - n2) * inv1m;
-            float* row = acc + k * kDiagRec;
-            const float w2 = wgt * wgt;
-            atomicAdd(row + 16, W0 * w2);
-            atomicAdd(row + 17, W1 * w2);
-            atomicAdd(row + 18, W2 * w2);
-            if (!a.clamped) {
-                const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
-                const float gp[5] = {-(ca * dx + cb * dy), -(cb * dx + cc * dy), -0.5f * dx * dx, -dx * dy,
-                                     -0.5f * dy * dy};
-                const float sw2 = W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2;
-                const float sdp = alpha * alpha * sw2;
-                int q = 0;
-#pragma unroll
-                for (int i = 0; i < 5; ++i)
-#pragma unroll
-                    for (int jj = i; jj < 5; ++jj) atomicAdd(row + q++, sdp * gp[i] * gp[jj]);
-                const float ao = alpha / r1.y;
-                atomicAdd(row + 15, ao * ao * sw2);
-            }
+            s_pair[warp][lane][k] = make_float2(W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2, wgt);
             S0 = n0;
             S1 = n1;
             S2 = n2;
             T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
         }
+        unsigned col = 0u;
+        for (unsigned uu = un; uu; uu &= uu - 1) {
+            const int k = __ffs(uu) - 1;
+            const unsigned b = __ballot_sync(0xffffffffu, (m0 >> k) & 1u);
+            if (lane == k) col = b;
+        }
         __syncwarp();
-        if ((un >> lane) & 1u) {
-            float4* src = reinterpret_cast<float4*>(acc + lane * kDiagRec);
-            float* dst = A.diagacc + (c.vbase + s_g[warp][lane]) * kDiagRec;
+        if (mine) {
+            const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
+            float acc[19];
 #pragma unroll
-            for (int q4 = 0; q4 < 5; ++q4) {
-                const float4 v = src[q4];
-                src[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-                red_add_v4(dst + 4 * q4, v.x, v.y, v.z, v.w);
+            for (int i = 0; i < 19; ++i) acc[i] = 0.f;
+            for (; col; col &= col - 1) {
+                const int p = __ffs(col) - 1;
+                const float4 pi = s_pix[warp][p];
+                const float pw2 = s_pw2[warp][p];
+                const float2 pr = s_pair[warp][p][lane];
+                Alpha a;
+                eval_alpha(q0, q1, pi.x, pi.y, a);
+                const float w2 = pr.y * pr.y;
+                acc[16] += pi.z * w2;
+                acc[17] += pi.w * w2;
+                acc[18] += pw2 * w2;
+                if (!a.clamped) {
+                    const float dx = a.dx, dy = a.dy;
+                    const float gp[5] = {-(ca * dx + cb * dy), -(cb * dx + cc * dy), -0.5f * dx * dx, -dx * dy,
+                                         -0.5f * dy * dy};
+                    const float sdp = a.alpha * a.alpha * pr.x;
+                    int q = 0;
+#pragma unroll
+                    for (int i = 0; i < 5; ++i)
+#pragma unroll
+                        for (int jj = i; jj < 5; ++jj) acc[q++] += sdp * gp[i] * gp[jj];
+                    const float ao = a.alpha / q1.y;
+                    acc[15] += ao * ao * pr.x;
+                }
             }
+            float* dst = A.diagacc + (c.vbase + gq) * kDiagRec;
+            red_add_v4(dst, acc[0], acc[1], acc[2], acc[3]);
+            red_add_v4(dst + 4, acc[4], acc[5], acc[6], acc[7]);
+            red_add_v4(dst + 8, acc[8], acc[9], acc[10], acc[11]);
+            red_add_v4(dst + 12, acc[12], acc[13], acc[14], acc[15]);
+            red_add_v4(dst + 16, acc[16], acc[17], acc[18], 0.f);
         }
         __syncwarp();
     }
