@@ -177,16 +177,30 @@ __device__ __forceinline__ bool rec_valid(const float4* rec, size_t vg) {
     return rec[3 * vg + 2].y != 0.0f;  // validity marker written by k_prepare
 }
 
+// Parallel layout of the three kernels: a group of kLanes = 8 consecutive
+// threads per Gaussian, lane `sub` owns views sub, sub+8, ...; the
+// view-independent Geom is recomputed by each lane (cheaper than a broadcast)
+// and per-view partial sums are combined with 3 xor-shuffle levels.
+constexpr int kLanes = 8;
+
+__device__ __forceinline__ double grp_sum(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
+
 // ------------------------------------------------------------------ K8
-// One thread per Gaussian; loops over the batch's views.  p is the f32 SoA
-// probe; writes tan[(v*Gp+g)] for valid (view, Gaussian) pairs.
-__global__ void k_tangents(const double* __restrict__ beta, const float* __restrict__ p, int G,
-                           int Gp, const DevCam* __restrict__ cams, int V,
-                           const float4* __restrict__ rec, float4* __restrict__ tan,
-                           const int* __restrict__ done_flag) {
+// Jv probe: tangent record of (mean2d, conic, opacity, colour) along p for
+// every valid (view, Gaussian); p is the f32 SoA probe.
+__global__ void __launch_bounds__(256) k_tangents(const double* __restrict__ beta, const float* __restrict__ p,
+                                                  int G, int Gp, const DevCam* __restrict__ cams, int V,
+                                                  const float4* __restrict__ rec, float4* __restrict__ tan,
+                                                  const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = tid / kLanes, sub = tid % kLanes;
+    if (g >= G || sub >= V) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     double pv[kP];
@@ -196,7 +210,7 @@ __global__ void k_tangents(const double* __restrict__ beta, const float* __restr
     const float dop = (float)(Gm.o * (1.0 - Gm.o) * pv[10]);
     const float dr = (float)(Gm.dcol[0] * pv[11]), dg = (float)(Gm.dcol[1] * pv[12]),
                 db = (float)(Gm.dcol[2] * pv[13]);
-    for (int v = 0; v < V; ++v) {
+    for (int v = sub; v < V; v += kLanes) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         if (!rec_valid(rec, vg)) continue;
         const DevCam& cam = cams[v];
@@ -214,19 +228,21 @@ __global__ void k_tangents(const double* __restrict__ beta, const float* __restr
 // ------------------------------------------------------------------ K11
 // out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
 // exact reverse mode of the projection; inter is zeroed after reading.
-__global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
-                        const DevCam* __restrict__ cams, int V, const float4* __restrict__ rec,
-                        float* __restrict__ inter, const float* __restrict__ p, float lambda,
-                        float* __restrict__ out, const int* __restrict__ done_flag) {
+__global__ void __launch_bounds__(256) k_chain(const double* __restrict__ beta, int G, int Gp,
+                                               const DevCam* __restrict__ cams, int V,
+                                               const float4* __restrict__ rec, float* __restrict__ inter,
+                                               const float* __restrict__ p, float lambda,
+                                               float* __restrict__ out, const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = tid / kLanes, sub = tid % kLanes;
+    const bool ok = g < G;  // every lane stays for the group shuffles
     Geom Gm;
-    load_geom(beta, Gp, g, Gm);
-    double gS[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    double gmu[3] = {0, 0, 0};
-    double go = 0.0, gcol[3] = {0, 0, 0};
-    for (int v = 0; v < V; ++v) {
+    if (ok) load_geom(beta, Gp, g, Gm);
+    // symmetrised dL/dSigma (gS + gS^T, 6 unique), dL/dmu, opacity, colour
+    double gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;
+    double gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
+    for (int v = sub; ok && v < V; v += kLanes) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         if (!rec_valid(rec, vg)) continue;
         float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
@@ -236,9 +252,9 @@ __global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
         ip[2] = make_float4(0.f, 0.f, 0.f, 0.f);
         const double gmx = i0.x, gmy = i0.y, gca = i0.z, gcb = i0.w, gcc = i1.x;
         go += i1.y;
-        gcol[0] += i1.z;
-        gcol[1] += i1.w;
-        gcol[2] += i2.x;
+        gc0 += i1.z;
+        gc1 += i1.w;
+        gc2 += i2.x;
         const DevCam& cam = cams[v];
         View Vw;
         load_view(Gm, cam, Vw);
@@ -253,10 +269,14 @@ __global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
             gr0[k] = 2.0 * ga * Vw.Sr0[k] + gb * Vw.Sr1[k];
             gr1[k] = gb * Vw.Sr0[k] + 2.0 * gc * Vw.Sr1[k];
         }
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j)
-                gS[3 * i + j] += ga * Vw.r0[i] * Vw.r0[j] + gb * Vw.r0[i] * Vw.r1[j] +
-                                 gc * Vw.r1[i] * Vw.r1[j];
+        const double* r0 = Vw.r0;
+        const double* r1 = Vw.r1;
+        gs00 += 2.0 * (ga * r0[0] * r0[0] + gb * r0[0] * r1[0] + gc * r1[0] * r1[0]);
+        gs11 += 2.0 * (ga * r0[1] * r0[1] + gb * r0[1] * r1[1] + gc * r1[1] * r1[1]);
+        gs22 += 2.0 * (ga * r0[2] * r0[2] + gb * r0[2] * r1[2] + gc * r1[2] * r1[2]);
+        gs01 += 2.0 * ga * r0[0] * r0[1] + gb * (r0[0] * r1[1] + r1[0] * r0[1]) + 2.0 * gc * r1[0] * r1[1];
+        gs02 += 2.0 * ga * r0[0] * r0[2] + gb * (r0[0] * r1[2] + r1[0] * r0[2]) + 2.0 * gc * r1[0] * r1[2];
+        gs12 += 2.0 * ga * r0[1] * r0[2] + gb * (r0[1] * r1[2] + r1[1] * r0[2]) + 2.0 * gc * r1[1] * r1[2];
         const double* W = cam.R;
         const double gj00 = gr0[0] * W[0] + gr0[1] * W[1] + gr0[2] * W[2];
         const double gj02 = gr0[0] * W[6] + gr0[1] * W[7] + gr0[2] * W[8];
@@ -268,24 +288,29 @@ __global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
         const double giz = gmx * cam.fx * Vw.tx + gmy * cam.fy * Vw.ty + gj00 * cam.fx + gj11 * cam.fy -
                            2.0 * gj02 * cam.fx * Vw.tx * iz - 2.0 * gj12 * cam.fy * Vw.ty * iz;
         const double gtz = -giz * iz2;
-        for (int k = 0; k < 3; ++k) gmu[k] += W[k] * gtx + W[3 + k] * gty + W[6 + k] * gtz;
+        gmu0 += W[0] * gtx + W[3] * gty + W[6] * gtz;
+        gmu1 += W[1] * gtx + W[4] * gty + W[7] * gtz;
+        gmu2 += W[2] * gtx + W[5] * gty + W[8] * gtz;
     }
+    gs00 = grp_sum(gs00); gs01 = grp_sum(gs01); gs02 = grp_sum(gs02);
+    gs11 = grp_sum(gs11); gs12 = grp_sum(gs12); gs22 = grp_sum(gs22);
+    gmu0 = grp_sum(gmu0); gmu1 = grp_sum(gmu1); gmu2 = grp_sum(gmu2);
+    go = grp_sum(go); gc0 = grp_sum(gc0); gc1 = grp_sum(gc1); gc2 = grp_sum(gc2);
+    if (!ok || sub != 0) return;
     // Sigma = M M^T: gM = (gS + gS^T) M ; M = R diag(s)
+    const double gSs[9] = {gs00, gs01, gs02, gs01, gs11, gs12, gs02, gs12, gs22};
     double gM[9];
     for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) {
-            double acc = 0.0;
-            for (int k = 0; k < 3; ++k) acc += (gS[3 * i + k] + gS[3 * k + i]) * Gm.M[3 * k + j];
-            gM[3 * i + j] = acc;
-        }
+        for (int j = 0; j < 3; ++j)
+            gM[3 * i + j] = gSs[3 * i] * Gm.M[j] + gSs[3 * i + 1] * Gm.M[3 + j] + gSs[3 * i + 2] * Gm.M[6 + j];
     double gR[9], gls[3];
     for (int j = 0; j < 3; ++j) {
-        double gs = 0.0;
+        double gsj = 0.0;
         for (int i = 0; i < 3; ++i) {
             gR[3 * i + j] = gM[3 * i + j] * Gm.s[j];
-            gs += gM[3 * i + j] * Gm.R[3 * i + j];
+            gsj += gM[3 * i + j] * Gm.R[3 * i + j];
         }
-        gls[j] = gs * Gm.s[j];
+        gls[j] = gsj * Gm.s[j];
     }
     const double w = Gm.qn[0], x = Gm.qn[1], y = Gm.qn[2], z = Gm.qn[3];
     double gn[4];
@@ -298,11 +323,15 @@ __global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
                    y * gR[5] + x * gR[6] + y * gR[7]);
     const double proj = Gm.qn[0] * gn[0] + Gm.qn[1] * gn[1] + Gm.qn[2] * gn[2] + Gm.qn[3] * gn[3];
     double res[kP];
-    for (int k = 0; k < 3; ++k) res[k] = gmu[k];
+    res[0] = gmu0;
+    res[1] = gmu1;
+    res[2] = gmu2;
     for (int k = 0; k < 3; ++k) res[3 + k] = gls[k];
     for (int k = 0; k < 4; ++k) res[6 + k] = (gn[k] - Gm.qn[k] * proj) * Gm.qinv;
     res[10] = go * Gm.o * (1.0 - Gm.o);
-    for (int k = 0; k < 3; ++k) res[11 + k] = gcol[k] * Gm.dcol[k];
+    res[11] = gc0 * Gm.dcol[0];
+    res[12] = gc1 * Gm.dcol[1];
+    res[13] = gc2 * Gm.dcol[2];
     for (int k = 0; k < kP; ++k) {
         float val = (float)res[k];
         if (p) val += lambda * p[k * Gp + g];
@@ -313,25 +342,20 @@ __global__ void k_chain(const double* __restrict__ beta, int G, int Gp,
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
-__global__ void k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
-                                const DevCam* __restrict__ cams, int V,
-                                const float4* __restrict__ rec, float* __restrict__ diagacc,
-                                float* __restrict__ out) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+__global__ void __launch_bounds__(256) k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
+                                                       const DevCam* __restrict__ cams, int V,
+                                                       const float4* __restrict__ rec,
+                                                       float* __restrict__ diagacc, float* __restrict__ out) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = tid / kLanes, sub = tid % kLanes;
+    const bool ok = g < G;
     Geom Gm;
-    load_geom(beta, Gp, g, Gm);
-    double dSj[7][9];  // dSigma for the 3 log-scale + 4 quaternion unit probes
-    for (int j = 0; j < 7; ++j) {
-        double dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0};
-        if (j < 3) dls[j] = 1.0; else dq[j - 3] = 1.0;
-        dsigma(Gm, dls, dq, dSj[j]);
-    }
+    if (ok) load_geom(beta, Gp, g, Gm);
     double d[kP];
     for (int k = 0; k < kP; ++k) d[k] = 0.0;
     const double zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const double zero3[3] = {0, 0, 0};
-    for (int v = 0; v < V; ++v) {
+    for (int v = sub; ok && v < V; v += kLanes) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         if (!rec_valid(rec, vg)) continue;
         float* acc = diagacc + vg * kDiagRec;
@@ -355,7 +379,10 @@ __global__ void k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
                 dmu[j] = 1.0;
                 view_tangent(Gm, Vw, cam, dmu, zero9, col);
             } else {
-                view_tangent(Gm, Vw, cam, zero3, dSj[j - 3], col);
+                double dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0}, dS[9];
+                if (j < 6) dls[j - 3] = 1.0; else dq[j - 6] = 1.0;
+                dsigma(Gm, dls, dq, dS);
+                view_tangent(Gm, Vw, cam, zero3, dS, col);
             }
             double qf = 0.0;
             for (int a = 0; a < 5; ++a) {
@@ -371,6 +398,8 @@ __global__ void k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
         d[12] += ac1 * Gm.dcol[1] * Gm.dcol[1];
         d[13] += ac2 * Gm.dcol[2] * Gm.dcol[2];
     }
+    for (int k = 0; k < kP; ++k) d[k] = grp_sum(d[k]);
+    if (!ok || sub != 0) return;
     for (int k = 0; k < kP; ++k) out[k * Gp + g] = (float)d[k];
 }
 
@@ -378,20 +407,20 @@ __global__ void k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
 void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st) {
     if (G == 0) return;
-    k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
+    k_tangents<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
 }
 
 void launch_chain(const double* beta, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                   float* inter, const float* p, float lambda, float* out, const int* done,
                   cudaStream_t st) {
     if (G == 0) return;
-    k_chain<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
+    k_chain<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
 }
 
 void launch_diag_finalize(const double* beta, int G, int Gp, const DevCam* cams, int V,
                           const float4* rec, float* diagacc, float* out, cudaStream_t st) {
     if (G == 0) return;
-    k_diag_finalize<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
+    k_diag_finalize<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
 }
 
 }  // namespace slm
