@@ -1,4 +1,4 @@
-// chain.cu — per-Gaussian FP64 linearisation kernels.
+// chain.cu — per-Gaussian linearisation kernels.
 //
 // The reference builds a 5x10 ProjChain per (view, Gaussian) from 10 dual
 // probes (jacobian.cpp:127-165) and re-runs the full dual preparation for
@@ -13,6 +13,12 @@
 // dL/dSigma over the views (reverse) once, and each view only touches the
 // cheap projection part.  Mathematically identical to the reference's dual
 // evaluation (same function, exact chain rule); differs only in rounding.
+//
+// FP32 throughout: the conic derivative is taken in matrix form
+// (d conic = -conic d cov2d conic) rather than through the determinant, so
+// there is no cancellation to protect, and the conic itself comes from the
+// FP64 preparation's record; the parameters come from the f32 mirror of the
+// f64 state.  These kernels are HBM-bound (records, probe, intermediates).
 //
 //  * k_tangents       Jv probe: per (view, Gaussian) tangent record of
 //                     (mean2d, conic, opacity, colour) along p            [K8]
@@ -29,198 +35,172 @@ namespace slm { extern std::atomic<long long> g_launches; }
 
 namespace slm {
 
-struct Geom {  // view-independent part, FP64
-    double mu[3];
-    double qn[4];   // normalised quaternion
-    double qinv;    // 1/|q|
-    double R[9], s[3], M[9], Sig[9];
-    double o;       // sigmoid(logit)
-    double dcol[3]; // C0 if the colour gate is open else 0 (rasterizer.hpp:83-86)
+struct Geom {  // view-independent part
+    float mu[3];
+    float qn[4];   // normalised quaternion
+    float qinv;    // 1/|q|
+    float R[9], s[3], M[9], Sig[9];
+    float o;       // sigmoid(logit)
+    float dcol[3]; // C0 if the colour gate is open else 0 (rasterizer.hpp:83-86)
 };
 
-__device__ __forceinline__ void load_geom(const double* __restrict__ beta, int Gp, int g, Geom& G) {
+__device__ __forceinline__ void load_geom(const float* __restrict__ beta, int Gp, int g, Geom& G) {
     for (int k = 0; k < 3; ++k) G.mu[k] = beta[k * Gp + g];
-    const double q[4] = {beta[6 * Gp + g], beta[7 * Gp + g], beta[8 * Gp + g], beta[9 * Gp + g]};
-    const double nsq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
-    G.qinv = nsq > 0.0 ? 1.0 / sqrt(nsq) : 0.0;
+    const float q[4] = {beta[6 * Gp + g], beta[7 * Gp + g], beta[8 * Gp + g], beta[9 * Gp + g]};
+    const float nsq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    G.qinv = nsq > 0.0f ? rsqrtf(nsq) : 0.0f;
     for (int k = 0; k < 4; ++k) G.qn[k] = q[k] * G.qinv;
-    const double w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
-    G.R[0] = 1.0 - 2.0 * (y * y + z * z);
-    G.R[1] = 2.0 * (x * y - w * z);
-    G.R[2] = 2.0 * (x * z + w * y);
-    G.R[3] = 2.0 * (x * y + w * z);
-    G.R[4] = 1.0 - 2.0 * (x * x + z * z);
-    G.R[5] = 2.0 * (y * z - w * x);
-    G.R[6] = 2.0 * (x * z - w * y);
-    G.R[7] = 2.0 * (y * z + w * x);
-    G.R[8] = 1.0 - 2.0 * (x * x + y * y);
-    for (int k = 0; k < 3; ++k) G.s[k] = exp(beta[(3 + k) * Gp + g]);
+    const float w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
+    G.R[0] = 1.0f - 2.0f * (y * y + z * z);
+    G.R[1] = 2.0f * (x * y - w * z);
+    G.R[2] = 2.0f * (x * z + w * y);
+    G.R[3] = 2.0f * (x * y + w * z);
+    G.R[4] = 1.0f - 2.0f * (x * x + z * z);
+    G.R[5] = 2.0f * (y * z - w * x);
+    G.R[6] = 2.0f * (x * z - w * y);
+    G.R[7] = 2.0f * (y * z + w * x);
+    G.R[8] = 1.0f - 2.0f * (x * x + y * y);
+    for (int k = 0; k < 3; ++k) G.s[k] = expf(beta[(3 + k) * Gp + g]);
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) G.M[3 * i + j] = G.R[3 * i + j] * G.s[j];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
             G.Sig[3 * i + j] = G.M[3 * i] * G.M[3 * j] + G.M[3 * i + 1] * G.M[3 * j + 1] +
                                G.M[3 * i + 2] * G.M[3 * j + 2];
-    G.o = 1.0 / (1.0 + exp(-beta[10 * Gp + g]));
+    G.o = 1.0f / (1.0f + expf(-beta[10 * Gp + g]));
     for (int k = 0; k < 3; ++k) {
-        const double raw = 0.5 + kColorC0 * beta[(11 + k) * Gp + g];
-        G.dcol[k] = raw > 0.0 ? kColorC0 : 0.0;
+        const float raw = 0.5f + (float)kColorC0 * beta[(11 + k) * Gp + g];
+        G.dcol[k] = raw > 0.0f ? (float)kColorC0 : 0.0f;
     }
 }
 
-struct View {  // per-view projection part, FP64
-    double tx, ty, tz, iz;
-    double j00, j02, j11, j12;
-    double r0[3], r1[3], Sr0[3], Sr1[3];
-    double a, b, c, det, ca, cb, cc;
+struct View {  // per-view projection part
+    float tx, ty, iz;
+    float r0[3], r1[3], Sr0[3], Sr1[3];
+    float ca, cb, cc;
 };
 
-__device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, View& V) {
-    const double* W = cam.R;
-    V.tx = W[0] * G.mu[0] + W[1] * G.mu[1] + W[2] * G.mu[2] + cam.t[0];
-    V.ty = W[3] * G.mu[0] + W[4] * G.mu[1] + W[5] * G.mu[2] + cam.t[1];
-    V.tz = W[6] * G.mu[0] + W[7] * G.mu[1] + W[8] * G.mu[2] + cam.t[2];
-    V.iz = 1.0 / V.tz;
-    const double iz2 = V.iz * V.iz;
-    V.j00 = cam.fx * V.iz;
-    V.j02 = -cam.fx * V.tx * iz2;
-    V.j11 = cam.fy * V.iz;
-    V.j12 = -cam.fy * V.ty * iz2;
+// The conic comes from the FP64 preparation (k_prepare's record, scaled by
+// log2(e)), so only t, J, r0, r1 and Sigma r are recomputed here.
+__device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, const float4 r0rec,
+                                          const float4 r1rec, View& V) {
+    const float W[9] = {(float)cam.R[0], (float)cam.R[1], (float)cam.R[2], (float)cam.R[3], (float)cam.R[4],
+                        (float)cam.R[5], (float)cam.R[6], (float)cam.R[7], (float)cam.R[8]};
+    const float fx = (float)cam.fx, fy = (float)cam.fy;
+    V.tx = W[0] * G.mu[0] + W[1] * G.mu[1] + W[2] * G.mu[2] + (float)cam.t[0];
+    V.ty = W[3] * G.mu[0] + W[4] * G.mu[1] + W[5] * G.mu[2] + (float)cam.t[1];
+    const float tz = W[6] * G.mu[0] + W[7] * G.mu[1] + W[8] * G.mu[2] + (float)cam.t[2];
+    V.iz = 1.0f / tz;
+    const float iz2 = V.iz * V.iz;
+    const float j00 = fx * V.iz, j02 = -fx * V.tx * iz2;
+    const float j11 = fy * V.iz, j12 = -fy * V.ty * iz2;
     for (int k = 0; k < 3; ++k) {
-        V.r0[k] = V.j00 * W[k] + V.j02 * W[6 + k];
-        V.r1[k] = V.j11 * W[3 + k] + V.j12 * W[6 + k];
+        V.r0[k] = j00 * W[k] + j02 * W[6 + k];
+        V.r1[k] = j11 * W[3 + k] + j12 * W[6 + k];
     }
     for (int i = 0; i < 3; ++i) {
         V.Sr0[i] = G.Sig[3 * i] * V.r0[0] + G.Sig[3 * i + 1] * V.r0[1] + G.Sig[3 * i + 2] * V.r0[2];
         V.Sr1[i] = G.Sig[3 * i] * V.r1[0] + G.Sig[3 * i + 1] * V.r1[1] + G.Sig[3 * i + 2] * V.r1[2];
     }
-    V.a = V.r0[0] * V.Sr0[0] + V.r0[1] * V.Sr0[1] + V.r0[2] * V.Sr0[2] + 0.3;
-    V.b = V.r0[0] * V.Sr1[0] + V.r0[1] * V.Sr1[1] + V.r0[2] * V.Sr1[2];
-    V.c = V.r1[0] * V.Sr1[0] + V.r1[1] * V.Sr1[1] + V.r1[2] * V.Sr1[2] + 0.3;
-    V.det = V.a * V.c - V.b * V.b;
-    const double inv = 1.0 / V.det;
-    V.ca = V.c * inv;
-    V.cb = -V.b * inv;
-    V.cc = V.a * inv;
+    constexpr float kLn2f = 0.69314718055994530942f;
+    V.ca = -2.0f * kLn2f * r0rec.z;
+    V.cb = -kLn2f * r0rec.w;
+    V.cc = -2.0f * kLn2f * r1rec.x;
 }
 
 // dSigma (full 3x3) along (dlog_scale, dquat) — forward mode of covariance_3d.
-__device__ __forceinline__ void dsigma(const Geom& G, const double dls[3], const double dq[4],
-                                       double dS[9]) {
-    // normalisation: dqn = (dq - qn (qn . dq)) / |q|
-    const double proj = G.qn[0] * dq[0] + G.qn[1] * dq[1] + G.qn[2] * dq[2] + G.qn[3] * dq[3];
-    double dn[4];
+__device__ __forceinline__ void dsigma(const Geom& G, const float dls[3], const float dq[4], float dS[9]) {
+    const float proj = G.qn[0] * dq[0] + G.qn[1] * dq[1] + G.qn[2] * dq[2] + G.qn[3] * dq[3];
+    float dn[4];
     for (int k = 0; k < 4; ++k) dn[k] = (dq[k] - G.qn[k] * proj) * G.qinv;
-    const double w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
-    const double dw = dn[0], dx = dn[1], dy = dn[2], dz = dn[3];
-    double dR[9];
-    dR[0] = -4.0 * (y * dy + z * dz);
-    dR[1] = 2.0 * (dx * y + x * dy - dw * z - w * dz);
-    dR[2] = 2.0 * (dx * z + x * dz + dw * y + w * dy);
-    dR[3] = 2.0 * (dx * y + x * dy + dw * z + w * dz);
-    dR[4] = -4.0 * (x * dx + z * dz);
-    dR[5] = 2.0 * (dy * z + y * dz - dw * x - w * dx);
-    dR[6] = 2.0 * (dx * z + x * dz - dw * y - w * dy);
-    dR[7] = 2.0 * (dy * z + y * dz + dw * x + w * dx);
-    dR[8] = -4.0 * (x * dx + y * dy);
-    double dM[9];
+    const float w = G.qn[0], x = G.qn[1], y = G.qn[2], z = G.qn[3];
+    const float dw = dn[0], dx = dn[1], dy = dn[2], dz = dn[3];
+    float dR[9];
+    dR[0] = -4.0f * (y * dy + z * dz);
+    dR[1] = 2.0f * (dx * y + x * dy - dw * z - w * dz);
+    dR[2] = 2.0f * (dx * z + x * dz + dw * y + w * dy);
+    dR[3] = 2.0f * (dx * y + x * dy + dw * z + w * dz);
+    dR[4] = -4.0f * (x * dx + z * dz);
+    dR[5] = 2.0f * (dy * z + y * dz - dw * x - w * dx);
+    dR[6] = 2.0f * (dx * z + x * dz - dw * y - w * dy);
+    dR[7] = 2.0f * (dy * z + y * dz + dw * x + w * dx);
+    dR[8] = -4.0f * (x * dx + y * dy);
+    float dM[9];
     for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            dM[3 * i + j] = dR[3 * i + j] * G.s[j] + G.R[3 * i + j] * G.s[j] * dls[j];
+        for (int j = 0; j < 3; ++j) dM[3 * i + j] = dR[3 * i + j] * G.s[j] + G.R[3 * i + j] * G.s[j] * dls[j];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) {
-            double acc = 0.0;
+            float acc = 0.0f;
             for (int k = 0; k < 3; ++k) acc += dM[3 * i + k] * G.M[3 * j + k] + G.M[3 * i + k] * dM[3 * j + k];
             dS[3 * i + j] = acc;
         }
 }
 
 // Tangent of (mean2d, conic) for one view given (dmu, dSigma).
-__device__ __forceinline__ void view_tangent(const Geom& G, const View& V, const DevCam& cam,
-                                             const double dmu[3], const double dS[9], double out[5]) {
-    const double* W = cam.R;
-    const double dtx = W[0] * dmu[0] + W[1] * dmu[1] + W[2] * dmu[2];
-    const double dty = W[3] * dmu[0] + W[4] * dmu[1] + W[5] * dmu[2];
-    const double dtz = W[6] * dmu[0] + W[7] * dmu[1] + W[8] * dmu[2];
-    const double diz = -dtz * V.iz * V.iz;
-    out[0] = cam.fx * (dtx * V.iz + V.tx * diz);
-    out[1] = cam.fy * (dty * V.iz + V.ty * diz);
-    const double iz2 = V.iz * V.iz, diz2 = 2.0 * V.iz * diz;
-    const double dj00 = cam.fx * diz, dj02 = -cam.fx * (dtx * iz2 + V.tx * diz2);
-    const double dj11 = cam.fy * diz, dj12 = -cam.fy * (dty * iz2 + V.ty * diz2);
-    double dr0[3], dr1[3];
+__device__ __forceinline__ void view_tangent(const View& V, const DevCam& cam, const float dmu[3],
+                                             const float dS[9], float out[5]) {
+    const float W[9] = {(float)cam.R[0], (float)cam.R[1], (float)cam.R[2], (float)cam.R[3], (float)cam.R[4],
+                        (float)cam.R[5], (float)cam.R[6], (float)cam.R[7], (float)cam.R[8]};
+    const float fx = (float)cam.fx, fy = (float)cam.fy;
+    const float dtx = W[0] * dmu[0] + W[1] * dmu[1] + W[2] * dmu[2];
+    const float dty = W[3] * dmu[0] + W[4] * dmu[1] + W[5] * dmu[2];
+    const float dtz = W[6] * dmu[0] + W[7] * dmu[1] + W[8] * dmu[2];
+    const float diz = -dtz * V.iz * V.iz;
+    out[0] = fx * (dtx * V.iz + V.tx * diz);
+    out[1] = fy * (dty * V.iz + V.ty * diz);
+    const float iz2 = V.iz * V.iz, diz2 = 2.0f * V.iz * diz;
+    const float dj00 = fx * diz, dj02 = -fx * (dtx * iz2 + V.tx * diz2);
+    const float dj11 = fy * diz, dj12 = -fy * (dty * iz2 + V.ty * diz2);
+    float dr0[3], dr1[3];
     for (int k = 0; k < 3; ++k) {
         dr0[k] = dj00 * W[k] + dj02 * W[6 + k];
         dr1[k] = dj11 * W[3 + k] + dj12 * W[6 + k];
     }
-    // d(r0^T S r0) = 2 dr0 . S r0 + r0^T dS r0, etc.
-    double dSr0[3], dSr1[3];
+    float dSr0[3], dSr1[3];
     for (int i = 0; i < 3; ++i) {
         dSr0[i] = dS[3 * i] * V.r0[0] + dS[3 * i + 1] * V.r0[1] + dS[3 * i + 2] * V.r0[2];
         dSr1[i] = dS[3 * i] * V.r1[0] + dS[3 * i + 1] * V.r1[1] + dS[3 * i + 2] * V.r1[2];
     }
-    const double da = 2.0 * (dr0[0] * V.Sr0[0] + dr0[1] * V.Sr0[1] + dr0[2] * V.Sr0[2]) +
-                      (V.r0[0] * dSr0[0] + V.r0[1] * dSr0[1] + V.r0[2] * dSr0[2]);
-    const double db = (dr0[0] * V.Sr1[0] + dr0[1] * V.Sr1[1] + dr0[2] * V.Sr1[2]) +
-                      (dr1[0] * V.Sr0[0] + dr1[1] * V.Sr0[1] + dr1[2] * V.Sr0[2]) +
-                      (V.r0[0] * dSr1[0] + V.r0[1] * dSr1[1] + V.r0[2] * dSr1[2]);
-    const double dc = 2.0 * (dr1[0] * V.Sr1[0] + dr1[1] * V.Sr1[1] + dr1[2] * V.Sr1[2]) +
-                      (V.r1[0] * dSr1[0] + V.r1[1] * dSr1[1] + V.r1[2] * dSr1[2]);
-    // conic = cov2d^-1: d conic = -conic d cov2d conic
-    const double ca = V.ca, cb = V.cb, cc = V.cc;
-    out[2] = -(ca * ca * da + 2.0 * ca * cb * db + cb * cb * dc);
+    const float da = 2.0f * (dr0[0] * V.Sr0[0] + dr0[1] * V.Sr0[1] + dr0[2] * V.Sr0[2]) +
+                     (V.r0[0] * dSr0[0] + V.r0[1] * dSr0[1] + V.r0[2] * dSr0[2]);
+    const float db = (dr0[0] * V.Sr1[0] + dr0[1] * V.Sr1[1] + dr0[2] * V.Sr1[2]) +
+                     (dr1[0] * V.Sr0[0] + dr1[1] * V.Sr0[1] + dr1[2] * V.Sr0[2]) +
+                     (V.r0[0] * dSr1[0] + V.r0[1] * dSr1[1] + V.r0[2] * dSr1[2]);
+    const float dc = 2.0f * (dr1[0] * V.Sr1[0] + dr1[1] * V.Sr1[1] + dr1[2] * V.Sr1[2]) +
+                     (V.r1[0] * dSr1[0] + V.r1[1] * dSr1[1] + V.r1[2] * dSr1[2]);
+    const float ca = V.ca, cb = V.cb, cc = V.cc;
+    out[2] = -(ca * ca * da + 2.0f * ca * cb * db + cb * cb * dc);
     out[3] = -(ca * cb * da + (ca * cc + cb * cb) * db + cb * cc * dc);
-    out[4] = -(cb * cb * da + 2.0 * cb * cc * db + cc * cc * dc);
-}
-
-__device__ __forceinline__ bool rec_valid(const float4* rec, size_t vg) {
-    return rec[3 * vg + 2].y != 0.0f;  // validity marker written by k_prepare
-}
-
-// Parallel layout of the three kernels: a group of kLanes = 8 consecutive
-// threads per Gaussian, lane `sub` owns views sub, sub+8, ...; the
-// view-independent Geom is recomputed by each lane (cheaper than a broadcast)
-// and per-view partial sums are combined with 3 xor-shuffle levels.
-constexpr int kLanes = 8;
-
-__device__ __forceinline__ double grp_sum(double v) {
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    return v;
+    out[4] = -(cb * cb * da + 2.0f * cb * cc * db + cc * cc * dc);
 }
 
 // ------------------------------------------------------------------ K8
-// Jv probe: tangent record of (mean2d, conic, opacity, colour) along p for
-// every valid (view, Gaussian); p is the f32 SoA probe.
-__global__ void __launch_bounds__(256) k_tangents(const double* __restrict__ beta, const float* __restrict__ p,
+__global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta, const float* __restrict__ p,
                                                   int G, int Gp, const DevCam* __restrict__ cams, int V,
                                                   const float4* __restrict__ rec, float4* __restrict__ tan,
                                                   const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = tid / kLanes, sub = tid % kLanes;
-    if (g >= G || sub >= V) return;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
-    double pv[kP];
-    for (int k = 0; k < kP; ++k) pv[k] = (double)p[k * Gp + g];
-    double dS[9];
+    float pv[kP];
+    for (int k = 0; k < kP; ++k) pv[k] = p[k * Gp + g];
+    float dS[9];
     dsigma(Gm, pv + 3, pv + 6, dS);
-    const float dop = (float)(Gm.o * (1.0 - Gm.o) * pv[10]);
-    const float dr = (float)(Gm.dcol[0] * pv[11]), dg = (float)(Gm.dcol[1] * pv[12]),
-                db = (float)(Gm.dcol[2] * pv[13]);
-    for (int v = sub; v < V; v += kLanes) {
+    const float dop = Gm.o * (1.0f - Gm.o) * pv[10];
+    const float dr = Gm.dcol[0] * pv[11], dg = Gm.dcol[1] * pv[12], db = Gm.dcol[2] * pv[13];
+    for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        if (!rec_valid(rec, vg)) continue;
+        if (rec[3 * vg + 2].y == 0.0f) continue;  // invalid (view, Gaussian)
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, Vw);
-        double o5[5];
-        view_tangent(Gm, Vw, cam, pv, dS, o5);
+        load_view(Gm, cam, rec[3 * vg], rec[3 * vg + 1], Vw);
+        float o5[5];
+        view_tangent(Vw, cam, pv, dS, o5);
         float4* t = tan + 3 * vg;
-        t[0] = make_float4((float)o5[0], (float)o5[1], (float)o5[2], (float)o5[3]);
-        t[1] = make_float4((float)o5[4], dop, dr, dg);
+        t[0] = make_float4(o5[0], o5[1], o5[2], o5[3]);
+        t[1] = make_float4(o5[4], dop, dr, dg);
         t[2] = make_float4(db, 0.f, 0.f, 0.f);
     }
 }
@@ -228,112 +208,106 @@ __global__ void __launch_bounds__(256) k_tangents(const double* __restrict__ bet
 // ------------------------------------------------------------------ K11
 // out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
 // exact reverse mode of the projection; inter is zeroed after reading.
-__global__ void __launch_bounds__(256) k_chain(const double* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ rec, float* __restrict__ inter,
                                                const float* __restrict__ p, float lambda,
                                                float* __restrict__ out, const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = tid / kLanes, sub = tid % kLanes;
-    const bool ok = g < G;  // every lane stays for the group shuffles
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     Geom Gm;
-    if (ok) load_geom(beta, Gp, g, Gm);
-    // symmetrised dL/dSigma (gS + gS^T, 6 unique), dL/dmu, opacity, colour
-    double gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;
-    double gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
-    for (int v = sub; ok && v < V; v += kLanes) {
+    load_geom(beta, Gp, g, Gm);
+    float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
+    float gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
+    for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        if (!rec_valid(rec, vg)) continue;
+        if (rec[3 * vg + 2].y == 0.0f) continue;
         float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
         const float4 i0 = ip[0], i1 = ip[1], i2 = ip[2];
         ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
         ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
         ip[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const double gmx = i0.x, gmy = i0.y, gca = i0.z, gcb = i0.w, gcc = i1.x;
+        const float gmx = i0.x, gmy = i0.y, gca = i0.z, gcb = i0.w, gcc = i1.x;
         go += i1.y;
         gc0 += i1.z;
         gc1 += i1.w;
         gc2 += i2.x;
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, Vw);
-        const double ca = Vw.ca, cb = Vw.cb, cc = Vw.cc;
+        load_view(Gm, cam, rec[3 * vg], rec[3 * vg + 1], Vw);
+        const float ca = Vw.ca, cb = Vw.cb, cc = Vw.cc;
         // conic -> cov2d (a, b, c): adjoint of d conic = -C dA C
-        const double ga = -(gca * ca * ca + gcb * ca * cb + gcc * cb * cb);
-        const double gb = -(2.0 * gca * ca * cb + gcb * (ca * cc + cb * cb) + 2.0 * gcc * cc * cb);
-        const double gc = -(gca * cb * cb + gcb * cb * cc + gcc * cc * cc);
-        // cov2d -> r0, r1, Sigma
-        double gr0[3], gr1[3];
+        const float ga = -(gca * ca * ca + gcb * ca * cb + gcc * cb * cb);
+        const float gb = -(2.0f * gca * ca * cb + gcb * (ca * cc + cb * cb) + 2.0f * gcc * cc * cb);
+        const float gc = -(gca * cb * cb + gcb * cb * cc + gcc * cc * cc);
+        float gr0[3], gr1[3];
         for (int k = 0; k < 3; ++k) {
-            gr0[k] = 2.0 * ga * Vw.Sr0[k] + gb * Vw.Sr1[k];
-            gr1[k] = gb * Vw.Sr0[k] + 2.0 * gc * Vw.Sr1[k];
+            gr0[k] = 2.0f * ga * Vw.Sr0[k] + gb * Vw.Sr1[k];
+            gr1[k] = gb * Vw.Sr0[k] + 2.0f * gc * Vw.Sr1[k];
         }
-        const double* r0 = Vw.r0;
-        const double* r1 = Vw.r1;
-        gs00 += 2.0 * (ga * r0[0] * r0[0] + gb * r0[0] * r1[0] + gc * r1[0] * r1[0]);
-        gs11 += 2.0 * (ga * r0[1] * r0[1] + gb * r0[1] * r1[1] + gc * r1[1] * r1[1]);
-        gs22 += 2.0 * (ga * r0[2] * r0[2] + gb * r0[2] * r1[2] + gc * r1[2] * r1[2]);
-        gs01 += 2.0 * ga * r0[0] * r0[1] + gb * (r0[0] * r1[1] + r1[0] * r0[1]) + 2.0 * gc * r1[0] * r1[1];
-        gs02 += 2.0 * ga * r0[0] * r0[2] + gb * (r0[0] * r1[2] + r1[0] * r0[2]) + 2.0 * gc * r1[0] * r1[2];
-        gs12 += 2.0 * ga * r0[1] * r0[2] + gb * (r0[1] * r1[2] + r1[1] * r0[2]) + 2.0 * gc * r1[1] * r1[2];
-        const double* W = cam.R;
-        const double gj00 = gr0[0] * W[0] + gr0[1] * W[1] + gr0[2] * W[2];
-        const double gj02 = gr0[0] * W[6] + gr0[1] * W[7] + gr0[2] * W[8];
-        const double gj11 = gr1[0] * W[3] + gr1[1] * W[4] + gr1[2] * W[5];
-        const double gj12 = gr1[0] * W[6] + gr1[1] * W[7] + gr1[2] * W[8];
-        const double iz = Vw.iz, iz2 = iz * iz;
-        const double gtx = gmx * cam.fx * iz - gj02 * cam.fx * iz2;
-        const double gty = gmy * cam.fy * iz - gj12 * cam.fy * iz2;
-        const double giz = gmx * cam.fx * Vw.tx + gmy * cam.fy * Vw.ty + gj00 * cam.fx + gj11 * cam.fy -
-                           2.0 * gj02 * cam.fx * Vw.tx * iz - 2.0 * gj12 * cam.fy * Vw.ty * iz;
-        const double gtz = -giz * iz2;
+        const float* r0 = Vw.r0;
+        const float* r1 = Vw.r1;
+        gs00 += 2.0f * (ga * r0[0] * r0[0] + gb * r0[0] * r1[0] + gc * r1[0] * r1[0]);
+        gs11 += 2.0f * (ga * r0[1] * r0[1] + gb * r0[1] * r1[1] + gc * r1[1] * r1[1]);
+        gs22 += 2.0f * (ga * r0[2] * r0[2] + gb * r0[2] * r1[2] + gc * r1[2] * r1[2]);
+        gs01 += 2.0f * ga * r0[0] * r0[1] + gb * (r0[0] * r1[1] + r1[0] * r0[1]) + 2.0f * gc * r1[0] * r1[1];
+        gs02 += 2.0f * ga * r0[0] * r0[2] + gb * (r0[0] * r1[2] + r1[0] * r0[2]) + 2.0f * gc * r1[0] * r1[2];
+        gs12 += 2.0f * ga * r0[1] * r0[2] + gb * (r0[1] * r1[2] + r1[1] * r0[2]) + 2.0f * gc * r1[1] * r1[2];
+        const float W[9] = {(float)cam.R[0], (float)cam.R[1], (float)cam.R[2], (float)cam.R[3], (float)cam.R[4],
+                            (float)cam.R[5], (float)cam.R[6], (float)cam.R[7], (float)cam.R[8]};
+        const float fx = (float)cam.fx, fy = (float)cam.fy;
+        const float gj00 = gr0[0] * W[0] + gr0[1] * W[1] + gr0[2] * W[2];
+        const float gj02 = gr0[0] * W[6] + gr0[1] * W[7] + gr0[2] * W[8];
+        const float gj11 = gr1[0] * W[3] + gr1[1] * W[4] + gr1[2] * W[5];
+        const float gj12 = gr1[0] * W[6] + gr1[1] * W[7] + gr1[2] * W[8];
+        const float iz = Vw.iz, iz2 = iz * iz;
+        const float gtx = gmx * fx * iz - gj02 * fx * iz2;
+        const float gty = gmy * fy * iz - gj12 * fy * iz2;
+        const float giz = gmx * fx * Vw.tx + gmy * fy * Vw.ty + gj00 * fx + gj11 * fy -
+                          2.0f * gj02 * fx * Vw.tx * iz - 2.0f * gj12 * fy * Vw.ty * iz;
+        const float gtz = -giz * iz2;
         gmu0 += W[0] * gtx + W[3] * gty + W[6] * gtz;
         gmu1 += W[1] * gtx + W[4] * gty + W[7] * gtz;
         gmu2 += W[2] * gtx + W[5] * gty + W[8] * gtz;
     }
-    gs00 = grp_sum(gs00); gs01 = grp_sum(gs01); gs02 = grp_sum(gs02);
-    gs11 = grp_sum(gs11); gs12 = grp_sum(gs12); gs22 = grp_sum(gs22);
-    gmu0 = grp_sum(gmu0); gmu1 = grp_sum(gmu1); gmu2 = grp_sum(gmu2);
-    go = grp_sum(go); gc0 = grp_sum(gc0); gc1 = grp_sum(gc1); gc2 = grp_sum(gc2);
-    if (!ok || sub != 0) return;
     // Sigma = M M^T: gM = (gS + gS^T) M ; M = R diag(s)
-    const double gSs[9] = {gs00, gs01, gs02, gs01, gs11, gs12, gs02, gs12, gs22};
-    double gM[9];
+    const float gSs[9] = {gs00, gs01, gs02, gs01, gs11, gs12, gs02, gs12, gs22};
+    float gM[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
             gM[3 * i + j] = gSs[3 * i] * Gm.M[j] + gSs[3 * i + 1] * Gm.M[3 + j] + gSs[3 * i + 2] * Gm.M[6 + j];
-    double gR[9], gls[3];
+    float gR[9], gls[3];
     for (int j = 0; j < 3; ++j) {
-        double gsj = 0.0;
+        float gsj = 0.0f;
         for (int i = 0; i < 3; ++i) {
             gR[3 * i + j] = gM[3 * i + j] * Gm.s[j];
             gsj += gM[3 * i + j] * Gm.R[3 * i + j];
         }
         gls[j] = gsj * Gm.s[j];
     }
-    const double w = Gm.qn[0], x = Gm.qn[1], y = Gm.qn[2], z = Gm.qn[3];
-    double gn[4];
-    gn[0] = 2.0 * (-z * gR[1] + y * gR[2] + z * gR[3] - x * gR[5] - y * gR[6] + x * gR[7]);
-    gn[1] = 2.0 * (y * gR[1] + z * gR[2] + y * gR[3] - 2.0 * x * gR[4] - w * gR[5] + z * gR[6] +
-                   w * gR[7] - 2.0 * x * gR[8]);
-    gn[2] = 2.0 * (-2.0 * y * gR[0] + x * gR[1] + w * gR[2] + x * gR[3] + z * gR[5] - w * gR[6] +
-                   z * gR[7] - 2.0 * y * gR[8]);
-    gn[3] = 2.0 * (-2.0 * z * gR[0] - w * gR[1] + x * gR[2] + w * gR[3] - 2.0 * z * gR[4] +
-                   y * gR[5] + x * gR[6] + y * gR[7]);
-    const double proj = Gm.qn[0] * gn[0] + Gm.qn[1] * gn[1] + Gm.qn[2] * gn[2] + Gm.qn[3] * gn[3];
-    double res[kP];
+    const float w = Gm.qn[0], x = Gm.qn[1], y = Gm.qn[2], z = Gm.qn[3];
+    float gn[4];
+    gn[0] = 2.0f * (-z * gR[1] + y * gR[2] + z * gR[3] - x * gR[5] - y * gR[6] + x * gR[7]);
+    gn[1] = 2.0f * (y * gR[1] + z * gR[2] + y * gR[3] - 2.0f * x * gR[4] - w * gR[5] + z * gR[6] +
+                    w * gR[7] - 2.0f * x * gR[8]);
+    gn[2] = 2.0f * (-2.0f * y * gR[0] + x * gR[1] + w * gR[2] + x * gR[3] + z * gR[5] - w * gR[6] +
+                    z * gR[7] - 2.0f * y * gR[8]);
+    gn[3] = 2.0f * (-2.0f * z * gR[0] - w * gR[1] + x * gR[2] + w * gR[3] - 2.0f * z * gR[4] +
+                    y * gR[5] + x * gR[6] + y * gR[7]);
+    const float proj = Gm.qn[0] * gn[0] + Gm.qn[1] * gn[1] + Gm.qn[2] * gn[2] + Gm.qn[3] * gn[3];
+    float res[kP];
     res[0] = gmu0;
     res[1] = gmu1;
     res[2] = gmu2;
     for (int k = 0; k < 3; ++k) res[3 + k] = gls[k];
     for (int k = 0; k < 4; ++k) res[6 + k] = (gn[k] - Gm.qn[k] * proj) * Gm.qinv;
-    res[10] = go * Gm.o * (1.0 - Gm.o);
+    res[10] = go * Gm.o * (1.0f - Gm.o);
     res[11] = gc0 * Gm.dcol[0];
     res[12] = gc1 * Gm.dcol[1];
     res[13] = gc2 * Gm.dcol[2];
     for (int k = 0; k < kP; ++k) {
-        float val = (float)res[k];
+        float val = res[k];
         if (p) val += lambda * p[k * Gp + g];
         out[k * Gp + g] = val;
     }
@@ -342,24 +316,38 @@ __global__ void __launch_bounds__(256) k_chain(const double* __restrict__ beta, 
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
-__global__ void __launch_bounds__(256) k_diag_finalize(const double* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
                                                        const float4* __restrict__ rec,
                                                        float* __restrict__ diagacc, float* __restrict__ out) {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = tid / kLanes, sub = tid % kLanes;
-    const bool ok = g < G;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     Geom Gm;
-    if (ok) load_geom(beta, Gp, g, Gm);
-    double d[kP];
-    for (int k = 0; k < kP; ++k) d[k] = 0.0;
-    const double zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const double zero3[3] = {0, 0, 0};
-    for (int v = sub; ok && v < V; v += kLanes) {
+    load_geom(beta, Gp, g, Gm);
+    float dSj[7][9];  // dSigma for the 3 log-scale + 4 quaternion unit probes
+    for (int j = 0; j < 7; ++j) {
+        float dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0};
+        if (j < 3) dls[j] = 1.0f; else dq[j - 3] = 1.0f;
+        dsigma(Gm, dls, dq, dSj[j]);
+    }
+    float d[kP];
+    for (int k = 0; k < kP; ++k) d[k] = 0.0f;
+    const float zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const float zero3[3] = {0, 0, 0};
+    for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        if (!rec_valid(rec, vg)) continue;
-        float* acc = diagacc + vg * kDiagRec;
-        double M[5][5];
+        if (rec[3 * vg + 2].y == 0.0f) continue;
+        float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
+        float acc[20];
+        for (int q4 = 0; q4 < 5; ++q4) {
+            const float4 a = acc4[q4];
+            acc[4 * q4] = a.x;
+            acc[4 * q4 + 1] = a.y;
+            acc[4 * q4 + 2] = a.z;
+            acc[4 * q4 + 3] = a.w;
+            acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float M[5][5];
         int q = 0;
         for (int i = 0; i < 5; ++i)
             for (int jj = i; jj < 5; ++jj) {
@@ -367,60 +355,52 @@ __global__ void __launch_bounds__(256) k_diag_finalize(const double* __restrict_
                 M[jj][i] = acc[q];
                 ++q;
             }
-        const double aop = acc[15], ac0 = acc[16], ac1 = acc[17], ac2 = acc[18];
-        for (int i = 0; i < kDiagRec; ++i) acc[i] = 0.0f;
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, Vw);
+        load_view(Gm, cam, rec[3 * vg], rec[3 * vg + 1], Vw);
         for (int j = 0; j < 10; ++j) {
-            double col[5];
+            float col[5];
             if (j < 3) {
-                double dmu[3] = {0, 0, 0};
-                dmu[j] = 1.0;
-                view_tangent(Gm, Vw, cam, dmu, zero9, col);
+                float dmu[3] = {0, 0, 0};
+                dmu[j] = 1.0f;
+                view_tangent(Vw, cam, dmu, zero9, col);
             } else {
-                double dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0}, dS[9];
-                if (j < 6) dls[j - 3] = 1.0; else dq[j - 6] = 1.0;
-                dsigma(Gm, dls, dq, dS);
-                view_tangent(Gm, Vw, cam, zero3, dS, col);
+                view_tangent(Vw, cam, zero3, dSj[j - 3], col);
             }
-            double qf = 0.0;
+            float qf = 0.0f;
             for (int a = 0; a < 5; ++a) {
-                double r = 0.0;
+                float r = 0.0f;
                 for (int b = 0; b < 5; ++b) r += M[a][b] * col[b];
                 qf += col[a] * r;
             }
             d[j] += qf;
         }
-        const double ds = Gm.o * (1.0 - Gm.o);
-        d[10] += aop * ds * ds;
-        d[11] += ac0 * Gm.dcol[0] * Gm.dcol[0];
-        d[12] += ac1 * Gm.dcol[1] * Gm.dcol[1];
-        d[13] += ac2 * Gm.dcol[2] * Gm.dcol[2];
+        const float ds = Gm.o * (1.0f - Gm.o);
+        d[10] += acc[15] * ds * ds;
+        d[11] += acc[16] * Gm.dcol[0] * Gm.dcol[0];
+        d[12] += acc[17] * Gm.dcol[1] * Gm.dcol[1];
+        d[13] += acc[18] * Gm.dcol[2] * Gm.dcol[2];
     }
-    for (int k = 0; k < kP; ++k) d[k] = grp_sum(d[k]);
-    if (!ok || sub != 0) return;
-    for (int k = 0; k < kP; ++k) out[k * Gp + g] = (float)d[k];
+    for (int k = 0; k < kP; ++k) out[k * Gp + g] = d[k];
 }
 
 // ------------------------------------------------------------------ launchers
-void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
+void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st) {
     if (G == 0) return;
-    k_tangents<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
+    k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
 }
 
-void launch_chain(const double* beta, int G, int Gp, const DevCam* cams, int V, const float4* rec,
-                  float* inter, const float* p, float lambda, float* out, const int* done,
-                  cudaStream_t st) {
+void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                  float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st) {
     if (G == 0) return;
-    k_chain<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
+    k_chain<<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
 }
 
-void launch_diag_finalize(const double* beta, int G, int Gp, const DevCam* cams, int V,
-                          const float4* rec, float* diagacc, float* out, cudaStream_t st) {
+void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                          float* diagacc, float* out, cudaStream_t st) {
     if (G == 0) return;
-    k_diag_finalize<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
+    k_diag_finalize<<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
 }
 
 }  // namespace slm

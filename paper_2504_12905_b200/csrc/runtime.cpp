@@ -510,7 +510,7 @@ struct Jacobian {
         std::array<cudaEvent_t, 4> ev{};
         const bool prof = ctx->prof;
         if (prof) ctx->prof_record(ev, 0);
-        launch_tangents(scene->beta.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+        launch_tangents(scene->beta32.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                         tan.p, done, st);
         if (prof) ctx->prof_record(ev, 1);
         SampleArgs a = args();
@@ -518,12 +518,12 @@ struct Jacobian {
         launch_sample_raster(kGn, a, st);
         if (prof) ctx->prof_record(ev, 2);
         if (ctx->world > 1) {
-            launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+            launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                          inter.p, nullptr, 0.f, dout, done, st);
             ctx->allreduce(dout, P());
             launch_axpy(dout, dp, static_cast<long long>(P()), lambda, st);
         } else {
-            launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+            launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                          inter.p, dp, lambda, dout, done, st);
         }
         if (prof) {
@@ -536,7 +536,7 @@ struct Jacobian {
     // b = J^T(-W r), r = render - truth at the samples (lm.cpp:99-121)
     void rhs_dev(float* dout) {
         launch_sample_raster(kRhs, args(), ctx->stream);
-        launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                      inter.p, nullptr, 0.f, dout, nullptr, ctx->stream);
         ctx->check_launch();
     }
@@ -558,7 +558,7 @@ struct Jacobian {
         d.masks = samples.masks.p;
         d.mask_off = samples.mask_off.p;
         launch_diag_raster(d, ctx->stream);
-        launch_diag_finalize(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V,
+        launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
                              batch->rec.p, diagacc.p, dout, ctx->stream);
         ctx->check_launch();
     }
@@ -583,7 +583,7 @@ struct Jacobian {
         vin.ensure(P());
         res_out.ensure(std::max<long long>(rdim, 1));
         upload_param(v, vin.p);
-        launch_tangents(scene->beta.p, vin.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+        launch_tangents(scene->beta32.p, vin.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
                         tan.p, nullptr, ctx->stream);
         SampleArgs a = args();
         a.out_res = res_out.p;
@@ -604,7 +604,7 @@ struct Jacobian {
         SampleArgs a = args();
         a.in_res = res_in.p;
         launch_sample_raster(kVjp, a, ctx->stream);
-        launch_chain(scene->beta.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
                      nullptr, 0.f, vout.p, nullptr, ctx->stream);
         ctx->check_launch();
         download_param(vout.p, out);

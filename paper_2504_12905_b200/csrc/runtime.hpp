@@ -85,11 +85,11 @@ void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);
 void launch_masks(const SampleArgs& a, cudaStream_t st);
 void launch_diag_raster(const DiagArgs& a, cudaStream_t st);
-void launch_tangents(const double* beta, const float* p, int G, int Gp, const DevCam* cams, int V,
+void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st);
-void launch_chain(const double* beta, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                   float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st);
-void launch_diag_finalize(const double* beta, int G, int Gp, const DevCam* cams, int V,
+void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V,
                           const float4* rec, float* diagacc, float* out, cudaStream_t st);
 void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
 void launch_soa32_to_aos64(const float* soa, int G, int Gp, double* aos, cudaStream_t st);
