@@ -4,27 +4,31 @@
 //                      one CTA per 16x16 tile, splat records staged in smem; writes
 //                      RGB, final T, contrib count and `last` (the list position
 //                      where blend_pixel stopped) and per-tile SSE vs ground truth.
-//  * k_masks           once per LM step: for every sampled pixel, one bit per tile-list
-//                      entry saying whether blend_pixel blends it (alpha gates passed
-//                      and before `last`).  The gates depend only on the state, not on
-//                      the probe p, so the per-product passes never re-evaluate the
-//                      ~85% of (pixel, entry) pairs that are skipped.
+//  * k_masks           once per (state, plan): for every sampled pixel one bit per
+//                      tile-list entry saying whether blend_pixel blends it (alpha
+//                      gates passed and before `last`).  The gates depend only on the
+//                      state, not on the probe p, so the per-product passes never
+//                      re-evaluate the ~85% of (pixel, entry) pairs that are skipped.
 //  * k_sample_raster   the sampled-pixel products, one warp per group of <=32 samples
-//                      of one tile.  The list is walked in windows of 32 entries; in a
-//                      window every lane iterates only over ITS OWN blended entries
-//                      (its mask word), so lanes do useful work instead of idling
-//                      through a shared entry loop:
+//                      of one tile, walking the list in windows of 32 entries:
 //        JVP   Jv      dual blend (jvp, jacobian.cpp:191-211)
 //        VJP   J^T u   reverse blend into the 9-float intermediate (vjp :219-247)
 //        GN    J^T W J p fused: Jv, *W, J^T in one kernel (gn_apply :339-344)
 //        RHS   J^T(-W r) with r read from the forward render (lm.cpp:99-121)
-//                      J^T contributions are added into a per-window smem tile
-//                      [32 entries][12] (lanes are mostly at different entries, so
-//                      the shared atomics rarely conflict) and flushed with one
-//                      vector red.global.add per 4 floats per entry.
 //  * k_diag_raster     diag(J^T W J) accumulators (jtj_diag :272-337), factored as a
-//                      per-(tile, Gaussian) 5x5 quadratic form, same
-//                      windowed walk with a [32][20] smem tile.
+//                      per-(tile, Gaussian) 5x5 quadratic form.
+//
+// Window walk (all sampled passes).  In window w every lane iterates only over
+// ITS OWN blended entries (its mask word), so lanes do blend work instead of
+// idling through a shared entry loop.  The J^T reduction over the 32 pixels
+// of an entry is done without atomics or 32-lane shuffles: phase A (lane =
+// pixel) keeps T and the colour prefix and writes two scalars per blended
+// (pixel, entry) pair into a smem [pixel][entry] tile; the 32x32 mask matrix is
+// transposed with a 5-stage shuffle bit transpose; phase B (lane = entry)
+// gathers its column of pixels, rebuilds the intermediate in registers and
+// adds it to HBM with vector red.global.add (one per 4 floats per entry).
+// The next window's mask and splat records are prefetched into registers
+// while the current window runs.
 //
 // The J^T passes sweep front-to-back: the reference's reverse sweep needs
 // suffix_c = sum_{j>k} w_j c_j (backward_pixel_vjp :67-94); with the pixel's
@@ -169,6 +173,20 @@ __device__ __forceinline__ bool setup_group(const Group* groups, int n_groups, c
     return true;
 }
 
+// 32x32 bit-matrix transpose across the warp: in, lane l holds row l (bit k =
+// column k); out, lane k holds column k (bit l = row l).  5 shuffle stages.
+__device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
+    const unsigned masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int j = 16 >> i;
+        const unsigned y = __shfl_xor_sync(0xffffffffu, x, j);
+        if (lane & j) x ^= ((y >> j) ^ x) & masks[i];
+        else x ^= (((x >> j) ^ y) & masks[i]) << j;
+    }
+    return x;
+}
+
 // ------------------------------------------------------------------ masks
 // One warp per group: bit k of word [w][lane] = entry 32w+k is blended at the
 // lane's pixel (same eval_alpha as k_render, and k < last).
@@ -206,12 +224,42 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
                  : "memory");
 }
 
+// Window prefetch: mask word and (speculatively, only entries < maxlast) the
+// splat record (and tangent record) of entry 32w+lane.
+struct Prefetch {
+    unsigned m;
+    int g;
+    float4 r0, r1, r2, t0, t1, t2;
+};
+
+template <bool TAN>
+__device__ __forceinline__ void prefetch(const GroupCtx& c, const float4* __restrict__ rec,
+                                         const float4* __restrict__ tan, int w, int nwin, int lane,
+                                         Prefetch& P) {
+    P.m = 0u;
+    if (w >= nwin) return;
+    P.m = c.active ? c.masks[w * 32 + lane] : 0u;
+    const int j = w * 32 + lane;
+    if (j < c.maxlast) {
+        P.g = c.list[j];
+        const size_t rg = c.vbase + P.g;
+        P.r0 = rec[3 * rg];
+        P.r1 = rec[3 * rg + 1];
+        P.r2 = rec[3 * rg + 2];
+        if (TAN) {
+            P.t0 = tan[3 * rg];
+            P.t1 = tan[3 * rg + 1];
+            P.t2 = tan[3 * rg + 2];
+        }
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     __shared__ float4 s_rec[4][32][3];
-    __shared__ float4 s_tan[4][32][3];
-    __shared__ float2 s_pair[4][32][33];  // [pixel lane][entry] (dL/dalpha, alpha*T), padded
-    __shared__ float4 s_pix[4][32];       // per pixel lane: (px+.5, py+.5, u0, u1)
+    // pass 1 stages tangent records here, pass 2 the [pixel][entry] pair tile
+    __shared__ __align__(16) unsigned char s_raw[4][32 * 33 * sizeof(float2)];
+    __shared__ float4 s_pix[4][32];  // per pixel lane: (px+.5, py+.5, u0, u1)
     __shared__ float s_pu2[4][32];
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -221,34 +269,35 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         return;
     constexpr float kLn2f = 0.69314718055994530942f;
     const int nwin = (c.maxlast + 31) >> 5;
+    float4(*s_tan)[3] = reinterpret_cast<float4(*)[3]>(s_raw[warp]);
+    float2(*s_pair)[33] = reinterpret_cast<float2(*)[33]>(s_raw[warp]);
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     if (MODE == kJvp || MODE == kGn) {
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
+        Prefetch P;
+        prefetch<true>(c, A.rec, A.tan, 0, nwin, lane, P);
         for (int w = 0; w < nwin; ++w) {
-            unsigned m = c.active ? c.masks[w * 32 + lane] : 0u;
+            unsigned m = P.m;
             const unsigned un = __reduce_or_sync(0xffffffffu, m);
-            if (!un) continue;
             if ((un >> lane) & 1u) {
-                const size_t rg = c.vbase + c.list[w * 32 + lane];
-                const float4* r = A.rec + 3 * rg;
-                const float4* t = A.tan + 3 * rg;
-                s_rec[warp][lane][0] = r[0];
-                s_rec[warp][lane][1] = r[1];
-                s_rec[warp][lane][2] = r[2];
-                s_tan[warp][lane][0] = t[0];
-                s_tan[warp][lane][1] = t[1];
-                s_tan[warp][lane][2] = t[2];
+                s_rec[warp][lane][0] = P.r0;
+                s_rec[warp][lane][1] = P.r1;
+                s_rec[warp][lane][2] = P.r2;
+                s_tan[lane][0] = P.t0;
+                s_tan[lane][1] = P.t1;
+                s_tan[lane][2] = P.t2;
             }
             __syncwarp();
+            prefetch<true>(c, A.rec, A.tan, w + 1, nwin, lane, P);
             while (m) {
                 const int k = __ffs(m) - 1;
                 m &= m - 1;
                 const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
                 Alpha a;
                 eval_alpha(r0, r1, c.pxc, c.pyc, a);  // blended: the mask already decided
-                const float4 t0 = s_tan[warp][k][0], t1 = s_tan[warp][k][1];
-                const float db = s_tan[warp][k][2].x;
+                const float4 t0 = s_tan[k][0], t1 = s_tan[k][1];
+                const float db = s_tan[k][2].x;
                 const float alpha = a.alpha, dx = a.dx, dy = a.dy;
                 float dalpha = 0.0f;
                 if (!a.clamped) {
@@ -295,38 +344,30 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         }
     }
 
-    // ---- J^T pass: front to back, suffix = C - inclusive prefix.
-    // Per 32-entry window: phase A (lane = pixel) walks the lane's own blended
-    // entries, keeping T and the colour prefix, and stores per pair
-    // (dL/dalpha, alpha*T) in a [pixel][entry] smem tile; phase B (lane =
-    // entry) gathers its column of pixels (ballot-transposed masks), rebuilds
-    // the 9-float intermediate in registers and adds it to HBM with vector reds.
-    // No shared atomics (they are CAS loops on sm_100a), no 32-lane shuffles.
+    // ---- J^T pass
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
     s_pix[warp][lane] = make_float4(c.pxc, c.pyc, u0, u1);
     s_pu2[warp][lane] = u2;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
+    Prefetch P;
+    prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
+    __syncwarp();
     for (int w = 0; w < nwin; ++w) {
-        const unsigned m0 = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned m0 = P.m;
         const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        if (!un) continue;
         const bool mine = (un >> lane) & 1u;
-        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0;
-        int gq = 0;
+        const float4 q0 = P.r0, q1 = P.r1;
+        const int gq = P.g;
         if (mine) {
-            gq = c.list[w * 32 + lane];
-            const float4* r = A.rec + 3 * (c.vbase + gq);
-            q0 = r[0];
-            q1 = r[1];
-            q2 = r[2];
-            s_rec[warp][lane][0] = q0;
-            s_rec[warp][lane][1] = q1;
-            s_rec[warp][lane][2] = q2;
+            s_rec[warp][lane][0] = P.r0;
+            s_rec[warp][lane][1] = P.r1;
+            s_rec[warp][lane][2] = P.r2;
         }
         __syncwarp();
-        // phase A
+        prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
+        // phase A (lane = pixel)
         for (unsigned m = m0; m; m &= m - 1) {
             const int k = __ffs(m) - 1;
             const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
@@ -340,21 +381,15 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             const float inv1m = 1.0f / (1.0f - alpha);
             const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) + u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
                                  u2 * (T * c2 - (Cf2 - n2) * inv1m);
-            s_pair[warp][lane][k] = make_float2(dalpha, wgt);
+            s_pair[lane][k] = make_float2(dalpha, wgt);
             S0 = n0;
             S1 = n1;
             S2 = n2;
             T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
         }
-        // transpose the masks: col = pixels that blend entry `lane`
-        unsigned col = 0u;
-        for (unsigned uu = un; uu; uu &= uu - 1) {
-            const int k = __ffs(uu) - 1;
-            const unsigned b = __ballot_sync(0xffffffffu, (m0 >> k) & 1u);
-            if (lane == k) col = b;
-        }
+        unsigned col = transpose32(m0, lane);  // pixels that blend entry `lane`
         __syncwarp();
-        // phase B
+        // phase B (lane = entry)
         if (mine) {
             const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
             float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
@@ -362,7 +397,7 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
                 const int p = __ffs(col) - 1;
                 const float4 pi = s_pix[warp][p];
                 const float pu2 = s_pu2[warp][p];
-                const float2 pr = s_pair[warp][p][lane];
+                const float2 pr = s_pair[p][lane];
                 Alpha a;
                 eval_alpha(q0, q1, pi.x, pi.y, a);
                 g6 += pi.z * pr.y;
@@ -419,24 +454,22 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     s_pix[warp][lane] = make_float4(c.pxc, c.pyc, W0, W1);
     s_pw2[warp][lane] = W2;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
+    Prefetch P;
+    prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
+    __syncwarp();
     for (int w = 0; w < nwin; ++w) {
-        const unsigned m0 = c.active ? c.masks[w * 32 + lane] : 0u;
+        const unsigned m0 = P.m;
         const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        if (!un) continue;
         const bool mine = (un >> lane) & 1u;
-        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, q2 = q0;
-        int gq = 0;
+        const float4 q0 = P.r0, q1 = P.r1;
+        const int gq = P.g;
         if (mine) {
-            gq = c.list[w * 32 + lane];
-            const float4* r = A.rec + 3 * (c.vbase + gq);
-            q0 = r[0];
-            q1 = r[1];
-            q2 = r[2];
-            s_rec[warp][lane][0] = q0;
-            s_rec[warp][lane][1] = q1;
-            s_rec[warp][lane][2] = q2;
+            s_rec[warp][lane][0] = P.r0;
+            s_rec[warp][lane][1] = P.r1;
+            s_rec[warp][lane][2] = P.r2;
         }
         __syncwarp();
+        prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
         for (unsigned m = m0; m; m &= m - 1) {
             const int k = __ffs(m) - 1;
             const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
@@ -457,12 +490,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             S2 = n2;
             T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
         }
-        unsigned col = 0u;
-        for (unsigned uu = un; uu; uu &= uu - 1) {
-            const int k = __ffs(uu) - 1;
-            const unsigned b = __ballot_sync(0xffffffffu, (m0 >> k) & 1u);
-            if (lane == k) col = b;
-        }
+        unsigned col = transpose32(m0, lane);
         __syncwarp();
         if (mine) {
             const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
