@@ -174,28 +174,14 @@ __device__ __forceinline__ void view_tangent(const View& V, const DevCam& cam, c
     out[4] = -(cb * cb * da + 2.0f * cb * cc * db + cc * cc * dc);
 }
 
-// Thread layout of K8 / K11: kLanes consecutive lanes per Gaussian, lane
-// `sub` owns views sub, sub + kLanes, ...; every lane recomputes the cheap
-// view-independent Geom (FP32), so all (view, Gaussian) loads are independent
-// and in flight at once (a thread walking its views serially was latency-bound).
-constexpr int kLanes = 8;
-
-__device__ __forceinline__ float grp_sum(float v) {
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    return v;
-}
-
 // ------------------------------------------------------------------ K8
-__global__ void __launch_bounds__(256) k_tangents(const float* __restrict__ beta, const float* __restrict__ p,
+__global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta, const float* __restrict__ p,
                                                   int G, int Gp, const DevCam* __restrict__ cams, int V,
                                                   const float4* __restrict__ rec, float4* __restrict__ tan,
                                                   const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = tid / kLanes, sub = tid % kLanes;
-    if (g >= G || sub >= V) return;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float pv[kP];
@@ -204,7 +190,7 @@ __global__ void __launch_bounds__(256) k_tangents(const float* __restrict__ beta
     dsigma(Gm, pv + 3, pv + 6, dS);
     const float dop = Gm.o * (1.0f - Gm.o) * pv[10];
     const float dr = Gm.dcol[0] * pv[11], dg = Gm.dcol[1] * pv[12], db = Gm.dcol[2] * pv[13];
-    for (int v = sub; v < V; v += kLanes) {
+    for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         if (rec[3 * vg + 2].y == 0.0f) continue;  // invalid (view, Gaussian)
         const DevCam& cam = cams[v];
@@ -222,20 +208,19 @@ __global__ void __launch_bounds__(256) k_tangents(const float* __restrict__ beta
 // ------------------------------------------------------------------ K11
 // out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
 // exact reverse mode of the projection; inter is zeroed after reading.
-__global__ void __launch_bounds__(256) k_chain(const float* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ rec, float* __restrict__ inter,
                                                const float* __restrict__ p, float lambda,
                                                float* __restrict__ out, const int* __restrict__ done_flag) {
     if (done_flag && *done_flag) return;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g = tid / kLanes, sub = tid % kLanes;
-    const bool ok = g < G;  // all lanes stay for the group shuffles
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
     Geom Gm;
-    if (ok) load_geom(beta, Gp, g, Gm);
+    load_geom(beta, Gp, g, Gm);
     float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
     float gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
-    for (int v = sub; ok && v < V; v += kLanes) {
+    for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         if (rec[3 * vg + 2].y == 0.0f) continue;
         float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
@@ -286,11 +271,6 @@ __global__ void __launch_bounds__(256) k_chain(const float* __restrict__ beta, i
         gmu1 += W[1] * gtx + W[4] * gty + W[7] * gtz;
         gmu2 += W[2] * gtx + W[5] * gty + W[8] * gtz;
     }
-    gs00 = grp_sum(gs00); gs01 = grp_sum(gs01); gs02 = grp_sum(gs02);
-    gs11 = grp_sum(gs11); gs12 = grp_sum(gs12); gs22 = grp_sum(gs22);
-    gmu0 = grp_sum(gmu0); gmu1 = grp_sum(gmu1); gmu2 = grp_sum(gmu2);
-    go = grp_sum(go); gc0 = grp_sum(gc0); gc1 = grp_sum(gc1); gc2 = grp_sum(gc2);
-    if (!ok) return;
     // Sigma = M M^T: gM = (gS + gS^T) M ; M = R diag(s)
     const float gSs[9] = {gs00, gs01, gs02, gs01, gs11, gs12, gs02, gs12, gs22};
     float gM[9];
@@ -326,7 +306,7 @@ __global__ void __launch_bounds__(256) k_chain(const float* __restrict__ beta, i
     res[11] = gc0 * Gm.dcol[0];
     res[12] = gc1 * Gm.dcol[1];
     res[13] = gc2 * Gm.dcol[2];
-    for (int k = sub; k < kP; k += kLanes) {
+    for (int k = 0; k < kP; ++k) {
         float val = res[k];
         if (p) val += lambda * p[k * Gp + g];
         out[k * Gp + g] = val;
@@ -408,13 +388,13 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
 void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st) {
     if (G == 0) return;
-    k_tangents<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
+    k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
 }
 
 void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                   float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st) {
     if (G == 0) return;
-    k_chain<<<(G * kLanes + 255) / 256, 256, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
+    k_chain<<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
 }
 
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
