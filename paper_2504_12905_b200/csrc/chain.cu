@@ -211,9 +211,13 @@ __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta
         load_view(Gm, cam, q0, q1, Vw);
         float o5[5];
         view_tangent(Vw, cam, pv, dS, o5);
+        // pre-combined so the raster's d(power) is 5 FMAs in (dx, dy):
+        // dpow = A1 dx + A2 dy + A3 dx^2 + A4 dx dy + A5 dy^2
+        const float A1 = -(Vw.ca * o5[0] + Vw.cb * o5[1]);
+        const float A2 = -(Vw.cb * o5[0] + Vw.cc * o5[1]);
         float4* t = tan + 3 * vg;
-        t[0] = make_float4(o5[0], o5[1], o5[2], o5[3]);
-        t[1] = make_float4(o5[4], dop, dr, dg);
+        t[0] = make_float4(A1, A2, -0.5f * o5[2], -o5[3]);
+        t[1] = make_float4(-0.5f * o5[4], dop, dr, dg);
         t[2] = make_float4(db, 0.f, 0.f, 0.f);
     }
 }

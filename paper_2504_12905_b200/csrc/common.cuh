@@ -9,7 +9,10 @@
 //     (A = -0.5*ca*log2e, B = -cb*log2e, C = -0.5*cc*log2e) so the raster
 //     evaluates alpha = o * 2^(A dx^2 + B dx dy + C dy^2) with one MUFU.EX2.
 //   * per (view, Gaussian) tangent record (Jv probe), f32 x 12:
-//       {dmx, dmy, dca, dcb, dcc, dopacity, dr, dg, db, -, -, -}
+//       {A1, A2, A3, A4, A5, dopacity, dr, dg, db, -, -, -}
+//     where d(power) = A1 dx + A2 dy + A3 dx^2 + A4 dx dy + A5 dy^2, i.e.
+//     A1 = -(ca dmx + cb dmy), A2 = -(cb dmx + cc dmy), A3 = -dca/2,
+//     A4 = -dcb, A5 = -dcc/2 (pre-combined by k_tangents)
 //   * per (view, Gaussian) J^T accumulator, f32 x 12:
 //       {g_mx, g_my, g_ca, g_cb, g_cc, g_opacity, g_r, g_g, g_b, -, -, -}
 //     (the 9-float intermediate of jacobian.cpp:63-65)
@@ -41,6 +44,7 @@ __device__ __forceinline__ int warp_max_i(int v) {
 // rounding: no kernel may contract these differently.
 struct Alpha {
     float alpha;
+    float e;  // 2^q = exp(power): the falloff before opacity, = alpha/o when not clamped
     float dx, dy;
     bool clamped;
 };
@@ -55,9 +59,10 @@ __device__ __forceinline__ bool eval_alpha(const float4 r0, const float4 r1, flo
     a.dx = dx;
     a.dy = dy;
     if (q > 0.0f) return false;  // power > 0: skip
-    float alpha;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(alpha) : "f"(q));
-    alpha = __fmul_rn(r1.y, alpha);
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q));
+    a.e = e;
+    float alpha = __fmul_rn(r1.y, e);
     a.clamped = alpha > 0.99f;
     if (a.clamped) alpha = 0.99f;
     a.alpha = alpha;

@@ -257,8 +257,10 @@ __device__ __forceinline__ void prefetch(const GroupCtx& c, const float4* __rest
 template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     __shared__ float4 s_rec[4][32][3];
-    // pass 1 stages tangent records here, pass 2 the [pixel][entry] pair tile
-    __shared__ __align__(16) unsigned char s_raw[4][32 * 33 * sizeof(float2)];
+    __shared__ int s_g[4][32];
+    // pass 1 stages tangent records here; pass 2 the half-window pair tile
+    // [3][pixel 32][entry 16 (+1 pad)]: (dL/dpower, dL/dalpha * e, alpha*T)
+    __shared__ __align__(16) float s_raw[4][3 * 32 * 17];
     __shared__ float4 s_pix[4][32];  // per pixel lane: (px+.5, py+.5, u0, u1)
     __shared__ float s_pu2[4][32];
     if (A.done_flag && *A.done_flag) return;
@@ -269,11 +271,14 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         return;
     constexpr float kLn2f = 0.69314718055994530942f;
     const int nwin = (c.maxlast + 31) >> 5;
-    float4(*s_tan)[3] = reinterpret_cast<float4(*)[3]>(s_raw[warp]);
-    float2(*s_pair)[33] = reinterpret_cast<float2(*)[33]>(s_raw[warp]);
+    float4(*s_tan)[3] = reinterpret_cast<float4(*)[3]>(&s_raw[warp][0]);
+    float(*t_dp)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][0]);
+    float(*t_de)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][32 * 17]);
+    float(*t_w)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][2 * 32 * 17]);
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     if (MODE == kJvp || MODE == kGn) {
+        // ---- Jv: dual blend over the lane's own blended entries
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
         Prefetch P;
         prefetch<true>(c, A.rec, A.tan, 0, nwin, lane, P);
@@ -297,20 +302,15 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
                 Alpha a;
                 eval_alpha(r0, r1, c.pxc, c.pyc, a);  // blended: the mask already decided
                 const float4 t0 = s_tan[k][0], t1 = s_tan[k][1];
-                const float db = s_tan[k][2].x;
+                const float c2 = s_rec[warp][k][2].x, db = s_tan[k][2].x;
                 const float alpha = a.alpha, dx = a.dx, dy = a.dy;
-                float dalpha = 0.0f;
-                if (!a.clamped) {
-                    const float ca = -2.0f * kLn2f * r0.z, cb = -kLn2f * r0.w, cc = -2.0f * kLn2f * r1.x;
-                    const float dpow = -(ca * dx + cb * dy) * t0.x - (cb * dx + cc * dy) * t0.y -
-                                       0.5f * dx * dx * t0.z - dx * dy * t0.w - 0.5f * dy * dy * t1.x;
-                    dalpha = alpha * dpow + (alpha / r1.y) * t1.y;
-                }
+                const float dpow = dx * (t0.x + dx * t0.z + dy * t0.w) + dy * (t0.y + dy * t1.x);
+                const float dalpha = a.clamped ? 0.0f : alpha * dpow + a.e * t1.y;
                 const float wgt = alpha * T;
                 const float dw = dalpha * T + alpha * dT;
                 dC0 += dw * r1.z + wgt * t1.z;
                 dC1 += dw * r1.w + wgt * t1.w;
-                dC2 += dw * s_rec[warp][k][2].x + wgt * db;
+                dC2 += dw * c2 + wgt * db;
                 dT = dT * (1.0f - alpha) - T * dalpha;
                 T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
             }
@@ -344,12 +344,19 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         }
     }
 
-    // ---- J^T pass
+    // ---- J^T pass, per half-window (16 entries):
+    //  phase A (lane = pixel): front-to-back over the lane's blended entries,
+    //    pair scalars into the [pixel][entry] tile;
+    //  phase B (lane = entry e + 16 * pixel-half): sum the column's pixels in
+    //    registers, combine the two pixel halves with one xor-16 shuffle per
+    //    accumulator, apply the entry's conic once, vector red.global.add.
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
     s_pix[warp][lane] = make_float4(c.pxc, c.pyc, u0, u1);
     s_pu2[warp][lane] = u2;
+    const int e16 = lane & 15, ph = lane >> 4;
+    const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
     prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
@@ -357,69 +364,83 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     for (int w = 0; w < nwin; ++w) {
         const unsigned m0 = P.m;
         const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        const bool mine = (un >> lane) & 1u;
-        const float4 q0 = P.r0, q1 = P.r1;
-        const int gq = P.g;
-        if (mine) {
+        if ((un >> lane) & 1u) {
             s_rec[warp][lane][0] = P.r0;
             s_rec[warp][lane][1] = P.r1;
             s_rec[warp][lane][2] = P.r2;
+            s_g[warp][lane] = P.g;
         }
         __syncwarp();
         prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
-        // phase A (lane = pixel)
-        for (unsigned m = m0; m; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
-            Alpha a;
-            eval_alpha(r0, r1, c.pxc, c.pyc, a);
-            const float alpha = a.alpha;
-            const float c2 = s_rec[warp][k][2].x;
-            const float wgt = __fmul_rn(alpha, T);
-            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
-                        n2 = __fmaf_rn(wgt, c2, S2);
-            const float inv1m = 1.0f / (1.0f - alpha);
-            const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) + u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
-                                 u2 * (T * c2 - (Cf2 - n2) * inv1m);
-            s_pair[lane][k] = make_float2(dalpha, wgt);
-            S0 = n0;
-            S1 = n1;
-            S2 = n2;
-            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        }
-        unsigned col = transpose32(m0, lane);  // pixels that blend entry `lane`
-        __syncwarp();
-        // phase B (lane = entry)
-        if (mine) {
-            const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
-            float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
-            for (; col; col &= col - 1) {
-                const int p = __ffs(col) - 1;
+        const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const unsigned hun = (un >> (16 * h)) & 0xFFFFu;
+            if (!hun) continue;
+            for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {  // phase A
+                const int kk = __ffs(m) - 1, k = 16 * h + kk;
+                const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
+                Alpha a;
+                eval_alpha(r0, r1, c.pxc, c.pyc, a);
+                const float alpha = a.alpha;
+                const float c2 = s_rec[warp][k][2].x;
+                const float wgt = __fmul_rn(alpha, T);
+                const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
+                            n2 = __fmaf_rn(wgt, c2, S2);
+                const float inv1m = __fdividef(1.0f, 1.0f - alpha);
+                const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) +
+                                     u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
+                                     u2 * (T * c2 - (Cf2 - n2) * inv1m);
+                t_dp[lane][kk] = a.clamped ? 0.0f : dalpha * alpha;
+                t_de[lane][kk] = a.clamped ? 0.0f : dalpha * a.e;
+                t_w[lane][kk] = wgt;
+                S0 = n0;
+                S1 = n1;
+                S2 = n2;
+                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+            }
+            const int k = 16 * h + e16;
+            const unsigned colk = __shfl_sync(0xffffffffu, col, k) & pmask;
+            __syncwarp();
+            // phase B
+            const float4 q0 = s_rec[warp][k][0];
+            float g6 = 0.f, g7 = 0.f, g8 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f, se = 0.f;
+            for (unsigned cc = colk; cc; cc &= cc - 1) {
+                const int p = __ffs(cc) - 1;
                 const float4 pi = s_pix[warp][p];
                 const float pu2 = s_pu2[warp][p];
-                const float2 pr = s_pair[p][lane];
-                Alpha a;
-                eval_alpha(q0, q1, pi.x, pi.y, a);
-                g6 += pi.z * pr.y;
-                g7 += pi.w * pr.y;
-                g8 += pu2 * pr.y;
-                if (!a.clamped) {
-                    const float dx = a.dx, dy = a.dy;
-                    const float dpow = pr.x * a.alpha;
-                    g0 += dpow * -(ca * dx + cb * dy);
-                    g1 += dpow * -(cb * dx + cc * dy);
-                    g2 += dpow * (-0.5f * dx * dx);
-                    g3 += dpow * (-dx * dy);
-                    g4 += dpow * (-0.5f * dy * dy);
-                    g5 += pr.x * (a.alpha / q1.y);
-                }
+                const float dp = t_dp[p][e16], de = t_de[p][e16], wg = t_w[p][e16];
+                const float dx = q0.x - pi.x, dy = q0.y - pi.y;
+                g6 += pi.z * wg;
+                g7 += pi.w * wg;
+                g8 += pu2 * wg;
+                const float dpx = dp * dx, dpy = dp * dy;
+                sx += dpx;
+                sy += dpy;
+                sxx += dpx * dx;
+                sxy += dpx * dy;
+                syy += dpy * dy;
+                se += de;
             }
-            float* dst = A.inter + (c.vbase + gq) * kRec;
-            red_add_v4(dst, g0, g1, g2, g3);
-            red_add_v4(dst + 4, g4, g5, g6, g7);
-            atomicAdd(dst + 8, g8);
+            g6 += __shfl_xor_sync(0xffffffffu, g6, 16);
+            g7 += __shfl_xor_sync(0xffffffffu, g7, 16);
+            g8 += __shfl_xor_sync(0xffffffffu, g8, 16);
+            sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+            sy += __shfl_xor_sync(0xffffffffu, sy, 16);
+            sxx += __shfl_xor_sync(0xffffffffu, sxx, 16);
+            sxy += __shfl_xor_sync(0xffffffffu, sxy, 16);
+            syy += __shfl_xor_sync(0xffffffffu, syy, 16);
+            se += __shfl_xor_sync(0xffffffffu, se, 16);
+            if (ph == 0 && ((hun >> e16) & 1u)) {
+                const float4 q1 = s_rec[warp][k][1];
+                const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
+                float* dst = A.inter + (c.vbase + s_g[warp][k]) * kRec;
+                red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
+                red_add_v4(dst + 4, -0.5f * syy, se, g6, g7);
+                atomicAdd(dst + 8, g8);
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 
