@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--gaussians", type=int, default=1_000_000)
     ap.add_argument("--diag", action="store_true")
     ap.add_argument("--lm", action="store_true")
+    ap.add_argument("--passes", action="store_true")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -39,6 +40,10 @@ def main():
     L.synchronize()
     if a.diag:
         jac.jtj_diag()
+    if a.passes:  # pass 1 alone (JVP) and pass 2 alone (VJP) through the host API
+        v = np.random.default_rng(0).uniform(-1, 1, jac.param_dim())
+        jv = jac.jvp(v)
+        jac.vjp(jv)
     if a.lm:
         gt = splatlm.Scene(L, bench.gt_scene(a.gaussians // 2))
         imgs = [gt.render(c)[0] for c in cams]
