@@ -366,19 +366,31 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
     for (int k = 0; k < kP; ++k) d[k] = 0.0f;
     const float zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const float zero3[3] = {0, 0, 0};
+    // software pipeline: next view's record and accumulators load during this view
+    float4 nr0, nr1, nr2, na[5];
+    auto fetch = [&](int v) {
+        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        nr0 = __ldg(rec + 3 * vg);
+        nr1 = __ldg(rec + 3 * vg + 1);
+        nr2 = __ldg(rec + 3 * vg + 2);
+        const float4* a4 = reinterpret_cast<const float4*>(diagacc + vg * kDiagRec);
+        for (int q4 = 0; q4 < 5; ++q4) na[q4] = a4[q4];
+    };
+    if (V > 0) fetch(0);
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        if (rec[3 * vg + 2].y == 0.0f) continue;
-        float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
+        const float4 q0 = nr0, q1 = nr1, q2 = nr2;
         float acc[20];
         for (int q4 = 0; q4 < 5; ++q4) {
-            const float4 a = acc4[q4];
-            acc[4 * q4] = a.x;
-            acc[4 * q4 + 1] = a.y;
-            acc[4 * q4 + 2] = a.z;
-            acc[4 * q4 + 3] = a.w;
-            acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[4 * q4] = na[q4].x;
+            acc[4 * q4 + 1] = na[q4].y;
+            acc[4 * q4 + 2] = na[q4].z;
+            acc[4 * q4 + 3] = na[q4].w;
         }
+        if (v + 1 < V) fetch(v + 1);
+        if (q2.y == 0.0f) continue;
+        float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
+        for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
         float M[5][5];
         int q = 0;
         for (int i = 0; i < 5; ++i)
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
             }
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, rec[3 * vg], rec[3 * vg + 1], Vw);
+        load_view(Gm, cam, q0, q1, Vw);
         for (int j = 0; j < 10; ++j) {
             float col[5];
             if (j < 3) {

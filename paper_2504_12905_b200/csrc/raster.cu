@@ -254,9 +254,24 @@ __device__ __forceinline__ void prefetch(const GroupCtx& c, const float4* __rest
     }
 }
 
+// Write a 9-float record (3 float4, first 9 used) as column `lane` of [9][32].
+__device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, float4 b, float4 c) {
+    dst[0][lane] = a.x;
+    dst[1][lane] = a.y;
+    dst[2][lane] = a.z;
+    dst[3][lane] = a.w;
+    dst[4][lane] = b.x;
+    dst[5][lane] = b.y;
+    dst[6][lane] = b.z;
+    dst[7][lane] = b.w;
+    dst[8][lane] = c.x;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
-    __shared__ float4 s_rec[4][32][3];
+    // window staging, struct-of-arrays so lanes reading different entries hit
+    // different banks: record fields (mx, my, A, B, C, o, r, g, b)
+    __shared__ float s_f[4][9][32];
     __shared__ int s_g[4][32];
     // pass 1 stages tangent records here; pass 2 the half-window pair tile
     // [3][pixel 32][entry 16 (+1 pad)]: (dL/dpower, dL/dalpha * e, alpha*T)
@@ -271,7 +286,8 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         return;
     constexpr float kLn2f = 0.69314718055994530942f;
     const int nwin = (c.maxlast + 31) >> 5;
-    float4(*s_tan)[3] = reinterpret_cast<float4(*)[3]>(&s_raw[warp][0]);
+    float(*s_t)[32] = reinterpret_cast<float(*)[32]>(&s_raw[warp][0]);  // tangent fields [9][32]
+    float(*sf)[32] = s_f[warp];
     float(*t_dp)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][0]);
     float(*t_de)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][32 * 17]);
     float(*t_w)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][2 * 32 * 17]);
@@ -286,23 +302,21 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             unsigned m = P.m;
             const unsigned un = __reduce_or_sync(0xffffffffu, m);
             if ((un >> lane) & 1u) {
-                s_rec[warp][lane][0] = P.r0;
-                s_rec[warp][lane][1] = P.r1;
-                s_rec[warp][lane][2] = P.r2;
-                s_tan[lane][0] = P.t0;
-                s_tan[lane][1] = P.t1;
-                s_tan[lane][2] = P.t2;
+                stage_rec(sf, lane, P.r0, P.r1, P.r2);
+                stage_rec(s_t, lane, P.t0, P.t1, P.t2);
             }
             __syncwarp();
             prefetch<true>(c, A.rec, A.tan, w + 1, nwin, lane, P);
             while (m) {
                 const int k = __ffs(m) - 1;
                 m &= m - 1;
-                const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
+                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
+                const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
                 Alpha a;
                 eval_alpha(r0, r1, c.pxc, c.pyc, a);  // blended: the mask already decided
-                const float4 t0 = s_tan[k][0], t1 = s_tan[k][1];
-                const float c2 = s_rec[warp][k][2].x, db = s_tan[k][2].x;
+                const float4 t0 = make_float4(s_t[0][k], s_t[1][k], s_t[2][k], s_t[3][k]);
+                const float4 t1 = make_float4(s_t[4][k], s_t[5][k], s_t[6][k], s_t[7][k]);
+                const float c2 = sf[8][k], db = s_t[8][k];
                 const float alpha = a.alpha, dx = a.dx, dy = a.dy;
                 const float dpow = dx * (t0.x + dx * t0.z + dy * t0.w) + dy * (t0.y + dy * t1.x);
                 const float dalpha = a.clamped ? 0.0f : alpha * dpow + a.e * t1.y;
@@ -365,9 +379,7 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         const unsigned m0 = P.m;
         const unsigned un = __reduce_or_sync(0xffffffffu, m0);
         if ((un >> lane) & 1u) {
-            s_rec[warp][lane][0] = P.r0;
-            s_rec[warp][lane][1] = P.r1;
-            s_rec[warp][lane][2] = P.r2;
+            stage_rec(sf, lane, P.r0, P.r1, P.r2);
             s_g[warp][lane] = P.g;
         }
         __syncwarp();
@@ -379,11 +391,12 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             if (!hun) continue;
             for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {  // phase A
                 const int kk = __ffs(m) - 1, k = 16 * h + kk;
-                const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
+                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
+                const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
                 Alpha a;
                 eval_alpha(r0, r1, c.pxc, c.pyc, a);
                 const float alpha = a.alpha;
-                const float c2 = s_rec[warp][k][2].x;
+                const float c2 = sf[8][k];
                 const float wgt = __fmul_rn(alpha, T);
                 const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
                             n2 = __fmaf_rn(wgt, c2, S2);
@@ -403,14 +416,14 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             const unsigned colk = __shfl_sync(0xffffffffu, col, k) & pmask;
             __syncwarp();
             // phase B
-            const float4 q0 = s_rec[warp][k][0];
+            const float qmx = sf[0][k], qmy = sf[1][k];
             float g6 = 0.f, g7 = 0.f, g8 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f, se = 0.f;
             for (unsigned cc = colk; cc; cc &= cc - 1) {
                 const int p = __ffs(cc) - 1;
                 const float4 pi = s_pix[warp][p];
                 const float pu2 = s_pu2[warp][p];
                 const float dp = t_dp[p][e16], de = t_de[p][e16], wg = t_w[p][e16];
-                const float dx = q0.x - pi.x, dy = q0.y - pi.y;
+                const float dx = qmx - pi.x, dy = qmy - pi.y;
                 g6 += pi.z * wg;
                 g7 += pi.w * wg;
                 g8 += pu2 * wg;
@@ -432,8 +445,7 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             syy += __shfl_xor_sync(0xffffffffu, syy, 16);
             se += __shfl_xor_sync(0xffffffffu, se, 16);
             if (ph == 0 && ((hun >> e16) & 1u)) {
-                const float4 q1 = s_rec[warp][k][1];
-                const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
+                const float ca = -2.0f * kLn2f * sf[2][k], cb = -kLn2f * sf[3][k], cc = -2.0f * kLn2f * sf[4][k];
                 float* dst = A.inter + (c.vbase + s_g[warp][k]) * kRec;
                 red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
                 red_add_v4(dst + 4, -0.5f * syy, se, g6, g7);
@@ -456,9 +468,12 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
 // Same two-phase window walk as the J^T pass; the pair scalars are
 // (sum_c W_c dalpha_c^2, alpha*T).
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
-    __shared__ float4 s_rec[4][32][3];
-    __shared__ float2 s_pair[4][32][33];
-    __shared__ float4 s_pix[4][32];
+    __shared__ float s_f[4][9][32];
+    __shared__ int s_g[4][32];
+    // half-window pair tile [3][pixel][entry]: (alpha^2 s, e^2 s, (alpha T)^2),
+    // s = sum_c W_c dalpha_c^2 (geometry / opacity terms zero when clamped)
+    __shared__ float s_t[4][3][32][17];
+    __shared__ float4 s_pix[4][32];  // (px+.5, py+.5, W0, W1)
     __shared__ float s_pw2[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     GroupCtx c;
@@ -467,6 +482,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
         return;
     constexpr float kLn2f = 0.69314718055994530942f;
     const int nwin = (c.maxlast + 31) >> 5;
+    float(*sf)[32] = s_f[warp];
     const float W0 = c.active ? A.sw[3 * c.s] : 0.f, W1 = c.active ? A.sw[3 * c.s + 1] : 0.f,
                 W2 = c.active ? A.sw[3 * c.s + 2] : 0.f;
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
@@ -474,6 +490,8 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
     s_pix[warp][lane] = make_float4(c.pxc, c.pyc, W0, W1);
     s_pw2[warp][lane] = W2;
+    const int e16 = lane & 15, ph = lane >> 4;
+    const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
     prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
@@ -481,76 +499,102 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     for (int w = 0; w < nwin; ++w) {
         const unsigned m0 = P.m;
         const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        const bool mine = (un >> lane) & 1u;
-        const float4 q0 = P.r0, q1 = P.r1;
-        const int gq = P.g;
-        if (mine) {
-            s_rec[warp][lane][0] = P.r0;
-            s_rec[warp][lane][1] = P.r1;
-            s_rec[warp][lane][2] = P.r2;
+        if ((un >> lane) & 1u) {
+            stage_rec(sf, lane, P.r0, P.r1, P.r2);
+            s_g[warp][lane] = P.g;
         }
         __syncwarp();
         prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
-        for (unsigned m = m0; m; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const float4 r0 = s_rec[warp][k][0], r1 = s_rec[warp][k][1];
-            Alpha a;
-            eval_alpha(r0, r1, c.pxc, c.pyc, a);
-            const float alpha = a.alpha;
-            const float c2 = s_rec[warp][k][2].x;
-            const float wgt = __fmul_rn(alpha, T);
-            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
-                        n2 = __fmaf_rn(wgt, c2, S2);
-            const float inv1m = 1.0f / (1.0f - alpha);
-            const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
-            const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
-            const float da2 = T * c2 - (Cf2 - n2) * inv1m;
-            s_pair[warp][lane][k] = make_float2(W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2, wgt);
-            S0 = n0;
-            S1 = n1;
-            S2 = n2;
-            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        }
-        unsigned col = transpose32(m0, lane);
-        __syncwarp();
-        if (mine) {
-            const float ca = -2.0f * kLn2f * q0.z, cb = -kLn2f * q0.w, cc = -2.0f * kLn2f * q1.x;
-            float acc[19];
-#pragma unroll
-            for (int i = 0; i < 19; ++i) acc[i] = 0.f;
-            for (; col; col &= col - 1) {
-                const int p = __ffs(col) - 1;
+        const unsigned col = transpose32(m0, lane);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const unsigned hun = (un >> (16 * h)) & 0xFFFFu;
+            if (!hun) continue;
+            for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {
+                const int kk = __ffs(m) - 1, k = 16 * h + kk;
+                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
+                const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
+                Alpha a;
+                eval_alpha(r0, r1, c.pxc, c.pyc, a);
+                const float alpha = a.alpha;
+                const float c2 = sf[8][k];
+                const float wgt = __fmul_rn(alpha, T);
+                const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
+                            n2 = __fmaf_rn(wgt, c2, S2);
+                const float inv1m = __fdividef(1.0f, 1.0f - alpha);
+                const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
+                const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
+                const float da2 = T * c2 - (Cf2 - n2) * inv1m;
+                const float sw2 = W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2;
+                s_t[warp][0][lane][kk] = a.clamped ? 0.0f : alpha * alpha * sw2;
+                s_t[warp][1][lane][kk] = a.clamped ? 0.0f : a.e * a.e * sw2;
+                s_t[warp][2][lane][kk] = wgt * wgt;
+                S0 = n0;
+                S1 = n1;
+                S2 = n2;
+                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+            }
+            const int k = 16 * h + e16;
+            const unsigned colk = __shfl_sync(0xffffffffu, col, k) & pmask;
+            __syncwarp();
+            const float qmx = sf[0][k], qmy = sf[1][k];
+            // sdp-weighted monomials in (dx, dy) up to degree 4, opacity, colours
+            float m2x = 0, mxy = 0, m2y = 0, m3x = 0, mx2y = 0, mxy2 = 0, m3y = 0;
+            float m4x = 0, mx3y = 0, mx2y2 = 0, mxy3 = 0, m4y = 0, aop = 0, ac0 = 0, ac1 = 0, ac2 = 0;
+            for (unsigned cc = colk; cc; cc &= cc - 1) {
+                const int p = __ffs(cc) - 1;
                 const float4 pi = s_pix[warp][p];
                 const float pw2 = s_pw2[warp][p];
-                const float2 pr = s_pair[warp][p][lane];
-                Alpha a;
-                eval_alpha(q0, q1, pi.x, pi.y, a);
-                const float w2 = pr.y * pr.y;
-                acc[16] += pi.z * w2;
-                acc[17] += pi.w * w2;
-                acc[18] += pw2 * w2;
-                if (!a.clamped) {
-                    const float dx = a.dx, dy = a.dy;
-                    const float gp[5] = {-(ca * dx + cb * dy), -(cb * dx + cc * dy), -0.5f * dx * dx, -dx * dy,
-                                         -0.5f * dy * dy};
-                    const float sdp = a.alpha * a.alpha * pr.x;
-                    int q = 0;
-#pragma unroll
-                    for (int i = 0; i < 5; ++i)
-#pragma unroll
-                        for (int jj = i; jj < 5; ++jj) acc[q++] += sdp * gp[i] * gp[jj];
-                    const float ao = a.alpha / q1.y;
-                    acc[15] += ao * ao * pr.x;
-                }
+                const float sdp = s_t[warp][0][p][e16], so = s_t[warp][1][p][e16], w2 = s_t[warp][2][p][e16];
+                const float X = qmx - pi.x, Y = qmy - pi.y;
+                const float XX = X * X, XY = X * Y, YY = Y * Y;
+                const float sXX = sdp * XX, sXY = sdp * XY, sYY = sdp * YY;
+                m2x += sXX;
+                mxy += sXY;
+                m2y += sYY;
+                m3x += sXX * X;
+                mx2y += sXX * Y;
+                mxy2 += sYY * X;
+                m3y += sYY * Y;
+                m4x += sXX * XX;
+                mx3y += sXX * XY;
+                mx2y2 += sXX * YY;
+                mxy3 += sXY * YY;
+                m4y += sYY * YY;
+                aop += so;
+                ac0 += pi.z * w2;
+                ac1 += pi.w * w2;
+                ac2 += pw2 * w2;
             }
-            float* dst = A.diagacc + (c.vbase + gq) * kDiagRec;
-            red_add_v4(dst, acc[0], acc[1], acc[2], acc[3]);
-            red_add_v4(dst + 4, acc[4], acc[5], acc[6], acc[7]);
-            red_add_v4(dst + 8, acc[8], acc[9], acc[10], acc[11]);
-            red_add_v4(dst + 12, acc[12], acc[13], acc[14], acc[15]);
-            red_add_v4(dst + 16, acc[16], acc[17], acc[18], 0.f);
+#define HSUM(v) v += __shfl_xor_sync(0xffffffffu, v, 16)
+            HSUM(m2x); HSUM(mxy); HSUM(m2y); HSUM(m3x); HSUM(mx2y); HSUM(mxy2); HSUM(m3y);
+            HSUM(m4x); HSUM(mx3y); HSUM(mx2y2); HSUM(mxy3); HSUM(m4y); HSUM(aop);
+            HSUM(ac0); HSUM(ac1); HSUM(ac2);
+#undef HSUM
+            if (ph == 0 && ((hun >> e16) & 1u)) {
+                const float ca = -2.0f * kLn2f * sf[2][k], cb = -kLn2f * sf[3][k], cc = -2.0f * kLn2f * sf[4][k];
+                // M_ij = sum sdp gp_i gp_j, gp = (-(ca X + cb Y), -(cb X + cc Y), -X^2/2, -XY, -Y^2/2)
+                const float M00 = ca * ca * m2x + 2.0f * ca * cb * mxy + cb * cb * m2y;
+                const float M01 = ca * cb * m2x + (ca * cc + cb * cb) * mxy + cb * cc * m2y;
+                const float M11 = cb * cb * m2x + 2.0f * cb * cc * mxy + cc * cc * m2y;
+                const float M02 = 0.5f * (ca * m3x + cb * mx2y);
+                const float M03 = ca * mx2y + cb * mxy2;
+                const float M04 = 0.5f * (ca * mxy2 + cb * m3y);
+                const float M12 = 0.5f * (cb * m3x + cc * mx2y);
+                const float M13 = cb * mx2y + cc * mxy2;
+                const float M14 = 0.5f * (cb * mxy2 + cc * m3y);
+                const float M22 = 0.25f * m4x, M23 = 0.5f * mx3y, M24 = 0.25f * mx2y2;
+                const float M33 = mx2y2, M34 = 0.5f * mxy3, M44 = 0.25f * m4y;
+                float* dst = A.diagacc + (c.vbase + s_g[warp][k]) * kDiagRec;
+                // upper-triangle order (00,01,02,03,04,11,12,13,14,22,23,24,33,34,44)
+                red_add_v4(dst, M00, M01, M02, M03);
+                red_add_v4(dst + 4, M04, M11, M12, M13);
+                red_add_v4(dst + 8, M14, M22, M23, M24);
+                red_add_v4(dst + 12, M33, M34, M44, aop);
+                red_add_v4(dst + 16, ac0, ac1, ac2, 0.f);
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
 }
 
