@@ -161,6 +161,7 @@ int slm_ring_camera(double angle, double radius, double height, int width, int h
  * so the caller's CUDA events bracket the library's kernels. */
 int slm_context_set_stream(slm_context* ctx, void* stream);
 int slm_context_set_timing(slm_context* ctx, int on);
+const char* slm_context_timing_names(slm_context* ctx); /* comma-separated stage names */
 long long slm_launch_count(void); /* kernels launched by this library so far */
 /* CUDA events around the three kernels of every J^T W J p product
  * (tangents, fused raster, chain); collect returns summed ms and the count. */

@@ -483,6 +483,7 @@ void launch_tile_sort(const int* offsets, int* entries, const unsigned long long
     if (n_tiles == 0) return;
     k_tile_sort<2048><<<n_tiles, 256, 0, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
                                                overflow_count); ++g_launches;
+    if (max_n <= 2048) return;  // no overflow tile: skip the persistent big-list kernel
     static bool attr = false;
     const int smem = kBigCap * (sizeof(unsigned long long) + sizeof(int));
     if (!attr) {

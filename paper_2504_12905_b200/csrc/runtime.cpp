@@ -17,6 +17,7 @@
 #include <limits>
 #include <memory>
 #include <numeric>
+#include <thread>
 
 #include <dlfcn.h>
 #include <nccl.h>
@@ -91,6 +92,7 @@ struct Context {
     DevBuf<float> fscalar;
     std::vector<std::pair<std::string, cudaEvent_t>> marks;
     std::vector<double> last_timings;
+    std::string last_timing_names;
     bool timing = false;
     bool prof = false;  // per-kernel CUDA events inside gn_apply_dev
     std::vector<std::array<cudaEvent_t, 4>> prof_events;
@@ -125,7 +127,9 @@ struct Context {
         if (!timing || marks.empty()) return;
         sync();
         last_timings.clear();
+        last_timing_names.clear();
         for (size_t i = 1; i < marks.size(); ++i) {
+            last_timing_names += marks[i].first + (i + 1 < marks.size() ? "," : "");
             float ms = 0.f;
             cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
             last_timings.push_back(ms);
@@ -297,6 +301,7 @@ struct Batch {
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p, tile_count.p, err.p, st);
         launch_scan_tiles(tile_count.p, n_tiles, tile_offsets.p, cursor.p, total.p, st);
         ctx->check_launch();
+        ctx->mark("prep:project+count+scan");
         long long hdr[2];
         std::vector<int> herr(1 + V);
         SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -310,7 +315,9 @@ struct Batch {
         n_entries = hdr[0];
         if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
         entries.ensure(std::max<long long>(n_entries, 1));
+        ctx->mark("prep:sync");
         launch_bin_scatter(G, Gp, V, cams.p, rect.p, cursor.p, entries.p, st);
+        ctx->mark("prep:scatter");
         max_list = hdr[1];
         // lists longer than the 16384-entry smem sort need chunk+merge scratch
         const int big_blocks = 148;
@@ -322,6 +329,7 @@ struct Batch {
                          overflow_count.p, max_list > 16384 ? scratch_k.p : nullptr,
                          max_list > 16384 ? scratch_v.p : nullptr, max_list, big_blocks, st);
         ctx->check_launch();
+        ctx->mark("prep:sort");
         rendered = false;
         has_gt = false;
     }
@@ -341,6 +349,7 @@ struct Batch {
                       with_gt ? sse_tile.p : nullptr, st);
         if (with_gt) launch_sse_views(cams.p, V, n_tiles, sse_tile.p, sse_view.p, st);
         ctx->check_launch();
+        ctx->mark("render");
         rendered = true;
         has_gt = with_gt;
     }
@@ -366,25 +375,33 @@ struct Samples {
     DevBuf<long long> mask_off;
     DevBuf<unsigned> masks;
     std::vector<int> order;  // group order -> plan sample index
+    std::vector<int> hpix, horig;
+    std::vector<float> hw;
     long long total = 0, mask_words = 0;
 
-    void build(Context* ctx, const slm_plan& plan, int view_lo, int view_hi,
-               const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets,
-               const std::vector<double>& weights3) {
+    // Host half (no CUDA calls; runs on the sampler thread in lm_step):
+    // group the plan's samples per view by tile in chunks of <= 32.
+    void group_host(const slm_plan& plan, int view_lo, int view_hi, const std::vector<slm_camera>& cams,
+                    const std::vector<double>& weights3) {
         hgroups.clear();
         order.clear();
         for (int v = view_lo; v < view_hi; ++v) {
-            const DevCam& c = cams[v - view_lo];
+            const slm_camera& c = cams[v - view_lo];
+            const int tiles = ((c.width + kTile - 1) / kTile) * ((c.height + kTile - 1) / kTile);
             const long long a = plan.view_offset[v], b = plan.view_offset[v + 1];
             std::vector<int> idx(b - a);
             std::iota(idx.begin(), idx.end(), static_cast<int>(a));
-            for (int s : idx) {
+            bool sorted = true;
+            for (long long i = 0; i < b - a; ++i) {
+                const int s = idx[i];
                 if (plan.px[s] < 0 || plan.px[s] >= c.width || plan.py[s] < 0 || plan.py[s] >= c.height)
                     throw std::invalid_argument("sample pixel outside the camera");
-                if (plan.tile[s] < 0 || plan.tile[s] >= c.tiles_x * c.tiles_y)
+                if (plan.tile[s] < 0 || plan.tile[s] >= tiles)
                     throw std::invalid_argument("sample tile outside the camera");
+                if (i > 0 && plan.tile[s] < plan.tile[idx[i - 1]]) sorted = false;
             }
-            std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return plan.tile[x] < plan.tile[y]; });
+            if (!sorted)  // reference plans are emitted tile-major already
+                std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return plan.tile[x] < plan.tile[y]; });
             size_t i = 0;
             while (i < idx.size()) {
                 const int t = plan.tile[idx[i]];
@@ -396,15 +413,20 @@ struct Samples {
             }
         }
         total = static_cast<long long>(order.size());
-        std::vector<int> hpix(order.size()), horig(order.size());
-        std::vector<float> hw(3 * order.size());
+        hpix.resize(order.size());
+        horig.resize(order.size());
+        hw.resize(3 * order.size());
+        const int base = static_cast<int>(plan.view_offset[view_lo]);
         for (size_t k = 0; k < order.size(); ++k) {
             const int s = order[k];
             hpix[k] = plan.px[s] | (plan.py[s] << 16);
-            horig[k] = s - static_cast<int>(plan.view_offset[view_lo]);
-            for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(s) + c]);
+            horig[k] = s - base;
+            for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(s - base) + c]);
         }
-        // blend bitmasks: 32 words (one per lane) per 32-entry window of the tile list
+    }
+
+    // Device half: mask offsets (need the tile-list lengths) and uploads.
+    void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets) {
         std::vector<long long> hoff(hgroups.size());
         mask_words = 0;
         for (size_t g = 0; g < hgroups.size(); ++g) {
@@ -416,23 +438,21 @@ struct Samples {
         cudaStream_t st = ctx->stream;
         mask_off.ensure(std::max<size_t>(hoff.size(), 1));
         masks.ensure(std::max<long long>(mask_words, 1));
-        SLM_CUDA_CHECK(cudaMemcpyAsync(mask_off.p, hoff.data(), sizeof(long long) * hoff.size(), cudaMemcpyHostToDevice, st));
         groups.ensure(std::max<size_t>(hgroups.size(), 1));
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
         sw.ensure(std::max<size_t>(3 * order.size(), 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(mask_off.p, hoff.data(), sizeof(long long) * hoff.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(groups.p, hgroups.data(), sizeof(Group) * hgroups.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(spix.p, hpix.data(), sizeof(int) * hpix.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sorig.p, horig.data(), sizeof(int) * horig.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, st));
-        ctx->sync();  // host staging vectors go out of scope
+        ctx->sync();  // hoff goes out of scope
     }
 
-    void upload_weights(Context* ctx, const std::vector<double>& weights3, long long plan_base) {
-        std::vector<float> hw(3 * order.size());
+    void upload_weights(Context* ctx, const std::vector<double>& weights3) {
         for (size_t k = 0; k < order.size(); ++k)
-            for (int c = 0; c < 3; ++c)
-                hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(order[k] - plan_base) + c]);
+            for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(horig[k]) + c]);
         SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, ctx->stream));
         ctx->sync();
     }
@@ -456,16 +476,22 @@ struct Jacobian {
     Jacobian(Context* c, Scene* s, Batch* b) : ctx(c), scene(s), batch(b) {}
 
     // plan views [lo, hi) are this rank's; the weights use the global N_total.
-    void init(const slm_plan& plan, int lo, int hi, double inv_total) {
+    // Host half: residual weights (jacobian.cpp:112-116) and sample grouping.
+    // Pure host work, safe to run concurrently with GPU work on the context.
+    void init_host(const slm_plan& plan, int lo, int hi, double inv_total, const std::vector<slm_camera>& cams) {
         rdim = 0;
         plan_base = plan.view_offset[lo];
         for (int v = lo; v < hi; ++v) rdim += 3 * (plan.view_offset[v + 1] - plan.view_offset[v]);
         weights.resize(rdim);
         for (long long s = plan.view_offset[lo], k = 0; s < plan.view_offset[hi]; ++s, ++k)
             for (int c = 0; c < 3; ++c) weights[3 * k + c] = plan.weight[s] * inv_total;
-        std::vector<double> w_by_plan(3 * static_cast<size_t>(plan.view_offset[hi]), 0.0);
-        std::copy(weights.begin(), weights.end(), w_by_plan.begin() + 3 * plan_base);
-        samples.build(ctx, plan, lo, hi, batch->hcams, batch->htile_offsets, w_by_plan);
+        samples.group_host(plan, lo, hi, cams, weights);
+    }
+
+    // Device half: uploads, zeroed accumulators, blend masks (needs the batch
+    // prepared and rendered).
+    void init_device() {
+        samples.upload(ctx, batch->hcams, batch->htile_offsets);
         const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
         tan.ensure(3 * VG);
         inter.ensure(VG * kRec);
@@ -985,22 +1011,48 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         my_cams.push_back(t.cams[batch[i]]);
         my_ids.push_back(batch[i]);
     }
-    // 2./3. forward render + residual fields of this rank's views (lm.cpp:75-78)
     StepBuffers& sb = step_buffers(ctx);
     Batch& B = sb.batch;
-    B.prepare(s, my_cams);
-    copy_gt(t, B, my_ids);
-    B.render(true);
+    Jacobian& J = sb.jac;
+    J.scene = &s;
+    // 4. (host) plan for the whole batch — every rank replays the same RNG
+    // stream (sample_plan.cpp:62-171) — and the sample grouping.  For the
+    // uniform distribution the plan does not depend on the render, so it runs
+    // on a host thread while the GPU prepares and renders the views.
+    std::unique_ptr<PlanH> plan;
+    std::exception_ptr plan_err;
+    auto make_plan = [&](const double* const* ai, const int32_t* const* ac, const double* const* ag) {
+        try {
+            plan = build_plan(all_cams.data(), VB, cfg.samples_per_tile, cfg.dist, cfg.sample_lane_width, rng,
+                              ai, ac, ag);
+            const long long total = plan->view_offset.back();
+            J.init_host(plan->view(), lo, hi, total > 0 ? 1.0 / static_cast<double>(total) : 0.0, my_cams);
+        } catch (...) {
+            plan_err = std::current_exception();
+        }
+    };
+    std::thread sampler;
+    const bool overlap = cfg.dist == SLM_DIST_UNIFORM;
+    if (overlap) sampler = std::thread(make_plan, nullptr, nullptr, nullptr);
+    // 2./3. forward render + residual fields of this rank's views (lm.cpp:75-78)
+    try {
+        B.prepare(s, my_cams);
+        copy_gt(t, B, my_ids);
+        B.render(true);
+    } catch (...) {
+        if (sampler.joinable()) sampler.join();
+        throw;
+    }
     ctx->mark("prepare+render");
-    // 4. plan for the whole batch; every rank replays the same RNG stream
-    std::vector<std::vector<double>> aux_img;
-    std::vector<std::vector<int32_t>> aux_cn;
-    std::vector<std::vector<double>> aux_gt;
-    std::vector<const double*> pi, pg;
-    std::vector<const int32_t*> pc;
-    if (cfg.dist != SLM_DIST_UNIFORM) {
+    if (overlap) {
+        sampler.join();
+    } else {  // weighted distributions need the render on the host (aux data)
         if (ctx->world > 1)
             throw std::invalid_argument("weighted residual distributions are single-rank only on the B200 path");
+        std::vector<std::vector<double>> aux_img, aux_gt;
+        std::vector<std::vector<int32_t>> aux_cn;
+        std::vector<const double*> pi, pg;
+        std::vector<const int32_t*> pc;
         for (int v = 0; v < VB; ++v) {
             const size_t np = static_cast<size_t>(all_cams[v].width) * all_cams[v].height;
             std::vector<float> fi(3 * np), fg(3 * np);
@@ -1017,13 +1069,9 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
             pc.push_back(aux_cn[v].data());
             pg.push_back(aux_gt[v].data());
         }
+        make_plan(pi.data(), pc.data(), pg.data());
     }
-    const auto plan = build_plan(all_cams.data(), VB, cfg.samples_per_tile, cfg.dist, cfg.sample_lane_width, rng,
-                                 pi.empty() ? nullptr : pi.data(), pc.empty() ? nullptr : pc.data(),
-                                 pg.empty() ? nullptr : pg.data());
-    const slm_plan pv = plan->view();
-    const long long total = plan->view_offset.back();
-    const double inv_total = total > 0 ? 1.0 / static_cast<double>(total) : 0.0;
+    if (plan_err) std::rethrow_exception(plan_err);
     // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
     double before = 0.0;
     {
@@ -1031,9 +1079,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         for (int v = 0; v < B.V; ++v)
             before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
     }
-    Jacobian& J = sb.jac;
-    J.scene = &s;
-    J.init(pv, lo, hi, inv_total);
+    J.init_device();
     ctx->mark("plan");
     const size_t P = s.P();
     sb.b.ensure(2 * P);  // [b | diag] contiguous for one fused allreduce
@@ -1148,7 +1194,8 @@ Jacobian* make_jacobian(Context* ctx, Scene* scene, const slm_camera* cams, int 
     holder->batch->render(false);
     holder->jac = std::make_unique<Jacobian>(ctx, scene, holder->batch.get());
     const long long total = plan.view_offset[plan.n_views];
-    holder->jac->init(plan, 0, plan.n_views, total > 0 ? 1.0 / static_cast<double>(total) : 0.0);
+    holder->jac->init_host(plan, 0, plan.n_views, total > 0 ? 1.0 / static_cast<double>(total) : 0.0, vc);
+    holder->jac->init_device();
     ctx->sync();
     return holder->jac.get();
 }
@@ -1191,6 +1238,7 @@ int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n) {
     });
 }
 long long slm_launch_count(void) { return g_launches.load(); }
+const char* slm_context_timing_names(slm_context* ctx) { return ctx->impl.last_timing_names.c_str(); }
 int slm_context_set_profiling(slm_context* ctx, int on) {
     return guarded([&] { ctx->impl.prof = on != 0; });
 }
@@ -1481,7 +1529,7 @@ int slm_jacobian_set_weights(slm_jacobian* j, const double* w) {
     return guarded([&] {
         Jacobian& J = *j->jac;
         J.weights.assign(w, w + J.rdim);
-        J.samples.upload_weights(J.ctx, J.weights, J.plan_base);
+        J.samples.upload_weights(J.ctx, J.weights);
     });
 }
 int slm_jacobian_gn_apply_dev(slm_jacobian* j, float lambda, const float* d_p, float* d_out) {

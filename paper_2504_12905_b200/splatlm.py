@@ -47,6 +47,7 @@ _SIGS = {
     "slm_context_set_stream": (C.c_int, [_vp, _vp]),
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
+    "slm_context_timing_names": (C.c_char_p, [_vp]),
     "slm_launch_count": (C.c_longlong, []),
     "slm_context_set_profiling": (C.c_int, [_vp, C.c_int]),
     "slm_context_profile_collect": (C.c_int, [_vp, _f64p, _i32p]),
@@ -303,11 +304,16 @@ class Lib(HostSampler):
     def set_timing(self, on: bool):
         self._check(self.dll.slm_context_set_timing(self.ctx, 1 if on else 0))
 
-    def timings(self) -> list:
-        buf = np.zeros(64)
+    def timings(self) -> dict:
+        """CUDA-event stage timings (ms) of the last lm_step with timing enabled."""
+        buf = np.zeros(256)
         n = C.c_int32()
-        self._check(self.dll.slm_context_timings(self.ctx, f64ptr(buf), 64, C.byref(n)))
-        return list(buf[:n.value])
+        self._check(self.dll.slm_context_timings(self.ctx, f64ptr(buf), 256, C.byref(n)))
+        names = self.dll.slm_context_timing_names(self.ctx).decode().split(",")
+        out: dict = {}
+        for name, ms in zip(names, buf[:n.value]):
+            out[name] = round(out.get(name, 0.0) + float(ms), 3)
+        return out
 
     def launch_count(self) -> int:
         return self.dll.slm_launch_count()
