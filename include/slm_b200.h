@@ -59,6 +59,12 @@ int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n);
 int slm_rng_create(uint64_t seed, slm_rng** out);
 void slm_rng_destroy(slm_rng* rng);
 uint64_t slm_rng_next(slm_rng* rng);
+/* Engine state in libstdc++'s text form (operator<< / >>), so a C++ caller's
+ * own std::mt19937_64 can drive lm_step / build_sample_plan. */
+int slm_rng_get_state(slm_rng* rng, char* buf, int64_t capacity, int64_t* length);
+int slm_rng_set_state(slm_rng* rng, const char* text);
+/* Contiguous slice [lo, hi) of an n-view batch owned by `rank` of `world`. */
+int slm_view_slice(int n, int rank, int world, int* lo, int* hi);
 
 /* ---- scene (GaussianSet) */
 int slm_scene_create(slm_context* ctx, const slm_gaussians* host, slm_scene** out);

@@ -17,6 +17,7 @@
 #include <limits>
 #include <memory>
 #include <numeric>
+#include <sstream>
 #include <thread>
 
 #include <dlfcn.h>
@@ -1002,8 +1003,8 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     // 1. view batch (lm.cpp:63)
     const std::vector<int> batch = view_batch(t.assign, t.k, rng);
     const int VB = static_cast<int>(batch.size());
-    const int lo = static_cast<int>(static_cast<long long>(VB) * ctx->rank / ctx->world);
-    const int hi = static_cast<int>(static_cast<long long>(VB) * (ctx->rank + 1) / ctx->world);
+    int lo = 0, hi = 0;
+    slm_view_slice(VB, ctx->rank, ctx->world, &lo, &hi);
     std::vector<slm_camera> all_cams, my_cams;
     std::vector<int> my_ids;
     for (int i = 0; i < VB; ++i) all_cams.push_back(t.cams[batch[i]]);
@@ -1279,6 +1280,31 @@ int slm_rng_create(uint64_t seed, slm_rng** out) {
 }
 void slm_rng_destroy(slm_rng* rng) { delete rng; }
 uint64_t slm_rng_next(slm_rng* rng) { return rng->eng(); }
+// std::mt19937_64 state as libstdc++'s operator<< text (312 words + index):
+// lets a C++ caller hand its own engine to lm_step across the C ABI.
+int slm_rng_get_state(slm_rng* rng, char* buf, int64_t capacity, int64_t* length) {
+    return guarded([&] {
+        std::ostringstream os;
+        os << rng->eng;
+        const std::string str = os.str();
+        *length = static_cast<int64_t>(str.size());
+        if (capacity > static_cast<int64_t>(str.size())) std::memcpy(buf, str.c_str(), str.size() + 1);
+    });
+}
+int slm_rng_set_state(slm_rng* rng, const char* text) {
+    return guarded([&] {
+        std::istringstream is(text);
+        is >> rng->eng;
+        if (is.fail()) throw std::invalid_argument("malformed mt19937_64 state");
+    });
+}
+// The contiguous view slice rank `rank` of `world` owns in a batch of n views.
+int slm_view_slice(int n, int rank, int world, int* lo, int* hi) {
+    if (world < 1 || rank < 0 || rank >= world || n < 0) return SLM_E_INVALID;
+    *lo = static_cast<int>(static_cast<long long>(n) * rank / world);
+    *hi = static_cast<int>(static_cast<long long>(n) * (rank + 1) / world);
+    return SLM_OK;
+}
 
 int slm_scene_create(slm_context* ctx, const slm_gaussians* host, slm_scene** out) {
     return guarded([&] {

@@ -1,0 +1,69 @@
+// adapter_parity.cpp — the reference's own C++ caller code, run twice: once on
+// the reference CPU path (splatlm::solver::lm_step) and once through the
+// drop-in adapter include/splatlm_b200.hpp (splatlm_b200::lm_step on the B200).
+// Built by oracle/Makefile (`make adapter`) against the reference sources;
+// run by tests/test_gpu_parity.py::test_cpp_adapter_drop_in.  Prints one JSON
+// line.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "splatlm/io/dataset.hpp"
+#include "splatlm/io/image_io.hpp"
+#include "splatlm/io/scene_gen.hpp"
+#include "splatlm_b200.hpp"
+
+using namespace splatlm;
+
+int main() {
+    // run.cpp:120-160 shaped setup: toy scene, random_init from the run RNG,
+    // TrainData with widened f32 images, k-means clusters.
+    std::mt19937_64 scene_rng(20214);
+    io::ToySceneConfig tc;
+    tc.gaussians = 20;
+    tc.train_cameras = 8;
+    tc.test_cameras = 2;
+    tc.image_size = 64;
+    const io::ToyScene scene = io::generate_toy_scene(tc, scene_rng);
+    solver::TrainData data;
+    data.cameras = scene.train.cameras;
+    for (const auto& img : scene.train.images) data.images.push_back(io::widen(img));
+    data.rebuild_clusters(8, 1ull ^ 0x9e3779b97f4a7c15ull);
+    solver::LmConfig cfg;
+    cfg.pcg_iters_initial = 8;
+
+    std::mt19937_64 rng_ref(1), rng_b2(1);
+    GaussianSet ref = io::random_init(40, {-1, -1, -1}, {1, 1, 1}, rng_ref);
+    GaussianSet b2 = io::random_init(40, {-1, -1, -1}, {1, 1, 1}, rng_b2);
+
+    splatlm_b200::Device dev(0);
+    bool batches_equal = true;
+    double worst = 0.0;
+    for (int it = 0; it < 6; ++it) {
+        const auto a = solver::lm_step(ref, data, cfg, it, rng_ref);
+        const auto b = splatlm_b200::lm_step(dev, b2, data, cfg, it, rng_b2);
+        batches_equal = batches_equal && a.batch == b.batch && a.pcg_iterations == b.pcg_iterations;
+        worst = std::max(worst, std::abs(a.loss_after - b.loss_after) / a.loss_after);
+        worst = std::max(worst, std::abs(a.loss_before - b.loss_before) / a.loss_before);
+    }
+    const bool rng_equal = rng_ref() == rng_b2();
+
+    // SampledJacobian::gn_apply through the adapter vs the reference class
+    std::mt19937_64 prng(5);
+    const std::vector<Camera> cams(data.cameras.begin(), data.cameras.begin() + 2);
+    const auto plan = sampling::build_sample_plan(cams, 32, sampling::ResidualDist::kUniform, {}, prng);
+    autodiff::SampledJacobian jr(ref, cams, plan);
+    splatlm_b200::SampledJacobian jb(dev, ref, cams, plan);
+    std::vector<double> p(jr.param_dim());
+    std::uniform_real_distribution<double> u(-1, 1);
+    for (double& v : p) v = u(prng);
+    const auto ga = jr.gn_apply(0.1, p), gb = jb.gn_apply(0.1, p);
+    double num = 0, den = 0;
+    for (size_t i = 0; i < ga.size(); ++i) {
+        num += (ga[i] - gb[i]) * (ga[i] - gb[i]);
+        den += ga[i] * ga[i];
+    }
+    std::printf("{\"batches_equal\": %s, \"rng_equal\": %s, \"worst_loss_rel\": %.3e, \"gn_apply_rel\": %.3e}\n",
+                batches_equal ? "true" : "false", rng_equal ? "true" : "false", worst, std::sqrt(num / den));
+    return 0;
+}

@@ -320,3 +320,22 @@ def test_long_tile_lists_sorted_exactly(gpu, port, count):
     og, ig = gpu.bin_and_sort(g, cam)
     assert int(np.max(np.diff(oo))) > (2048 if count < 10000 else 16384)
     assert np.array_equal(oo, og) and np.array_equal(io, ig)
+
+
+def test_cpp_adapter_drop_in(gpu):
+    """The reference's own C++ caller code (tests/cpp/adapter_parity.cpp) run
+    on the reference CPU path and through include/splatlm_b200.hpp: same view
+    batches and RNG stream, losses and gn_apply within 1e-4."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "adapter_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_parity not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    print(r)
+    assert r["batches_equal"] and r["rng_equal"]
+    assert r["worst_loss_rel"] < TOL and r["gn_apply_rel"] < TOL
