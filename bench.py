@@ -170,6 +170,17 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the
+    last committed `ncu --set full` capture (profiles/traffic.json, written by
+    tools/summarize_profiles.py), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f)[kernel]["bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -408,7 +419,7 @@ def run_b200(args):
                    "l2": "working set > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": "k_sample_raster<GN> (fused Jv -> W -> J^T)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": bytes_["raster"],
+                     "traffic": ncu_traffic("k_sample_raster<2>"), "algorithmic_bytes_per_launch": bytes_["raster"],
                      "avg_launch_ms": raster_ms, "peak_source": peak_src},
         "matvec_roofline": {"achieved": matvec_achieved, "peak": peak, "unit": "GB/s",
                             "frac": matvec_achieved / peak, "bytes_per_matvec": bytes_["matvec"],
