@@ -60,9 +60,16 @@ struct SampleArgs {
     float* out_res;       // JVP: Jv in plan order
     float* inter;         // J^T accumulators [(v*Gp+g)*12 + i]
     const int* done_flag; // optional: skip all work when *done_flag != 0 (PCG converged)
-    const unsigned* masks;      // blend bitmasks [group][window][lane] (k_masks)
-    const long long* mask_off;  // per-group offset into masks, in words
-    unsigned* masks_out;        // k_masks output (same buffer as masks)
+    // Per-group compacted window stream (k_masks, once per state/plan): the
+    // group's tile-list entries that at least one of its pixels blends, in
+    // list order, and per 32-entry window one blend bitmask per lane.
+    const unsigned* masks;      // [mask_off[g] + 32*w + lane], bit k = entry 32w+k blended
+    const int* glist;           // [mask_off[g] + j] = Gaussian index of compacted entry j
+    const int* gcount;          // [g] = compacted entries of the group
+    const long long* mask_off;  // per-group offset into masks / glist (32*ceil(list/32))
+    unsigned* masks_out;        // k_masks outputs (same buffers)
+    int* glist_out;
+    int* gcount_out;
 };
 
 struct DiagArgs {
@@ -79,6 +86,8 @@ struct DiagArgs {
     const int* last_img;
     float* diagacc;
     const unsigned* masks;
+    const int* glist;
+    const int* gcount;
     const long long* mask_off;
 };
 

@@ -139,37 +139,35 @@ __global__ void k_sse_views(const DevCam* __restrict__ cams, int V, int n_tiles_
 }
 
 // ------------------------------------------------------------------ group setup
+// One warp per group of <= 32 samples of one tile; lane = sample pixel.
 struct GroupCtx {
     bool active;
-    int s, orig, px, py, mylast, maxlast;
+    int s, orig;
     size_t pix, vbase;
-    const int* list;
-    float pxc, pyc;
-    const unsigned* masks;  // this group's mask words: [window][lane]
+    float pxc, pyc;  // pixel centre (x + 0.5, y + 0.5), rasterizer.cpp:82
+    float ox, oy;    // tile centre: origin of the local pixel coordinates of the J^T moments
+    int tile;        // batch tile index
 };
 
 __device__ __forceinline__ bool setup_group(const Group* groups, int n_groups, const DevCam* cams,
-                                            const int* tile_offsets, const int* entries,
-                                            const int* spix, const int* sorig, const int* last_img,
-                                            const unsigned* masks, const long long* mask_off, int Gp,
-                                            int gi, int lane, GroupCtx& c) {
+                                            const int* spix, const int* sorig, int Gp, int gi, int lane,
+                                            GroupCtx& c) {
     if (gi >= n_groups) return false;
     const Group grp = groups[gi];
     const DevCam& cam = cams[grp.view];
     c.active = lane < grp.count;
     c.s = grp.begin + (c.active ? lane : 0);
     const int packed = spix[c.s];
-    c.px = packed & 0xffff;
-    c.py = packed >> 16;
+    const int px = packed & 0xffff, py = packed >> 16;
     c.orig = sorig ? sorig[c.s] : 0;
-    c.pix = cam.pix_base + static_cast<size_t>(c.py) * cam.width + c.px;
-    c.mylast = c.active ? last_img[c.pix] : 0;
-    c.maxlast = __reduce_max_sync(0xffffffffu, c.mylast);
-    c.list = entries + tile_offsets[cam.tile_base + grp.tile];
+    c.pix = cam.pix_base + static_cast<size_t>(py) * cam.width + px;
     c.vbase = static_cast<size_t>(grp.view) * Gp;
-    c.pxc = (float)c.px + 0.5f;
-    c.pyc = (float)c.py + 0.5f;
-    c.masks = masks ? masks + mask_off[gi] : nullptr;
+    c.pxc = (float)px + 0.5f;
+    c.pyc = (float)py + 0.5f;
+    const int tx = grp.tile % cam.tiles_x, ty = grp.tile / cam.tiles_x;
+    c.ox = (float)(tx * kTile + kTile / 2);
+    c.oy = (float)(ty * kTile + kTile / 2);
+    c.tile = cam.tile_base + grp.tile;
     return true;
 }
 
@@ -188,33 +186,104 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 }
 
 // ------------------------------------------------------------------ masks
-// One warp per group: bit k of word [w][lane] = entry 32w+k is blended at the
-// lane's pixel (same eval_alpha as k_render, and k < last).
+// Once per (state, plan), one warp per group.  Walks the tile list up to the
+// group's furthest `last` in windows of 32 entries; bit k of a pixel's word =
+// entry k is blended there (same eval_alpha as k_render, and k < last).  The
+// window stream is then COMPACTED to the entries at least one of the group's
+// pixels blends (~72% at configs[2]): their Gaussian indices go to glist in
+// list order and the pixel bits are re-packed (column compaction through two
+// bit transposes) into 32-entry windows, so the per-product passes walk dense
+// windows and never stage an entry no lane uses.
 __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     __shared__ float4 s_rec[4][32][2];
+    __shared__ unsigned s_col[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * 4 + warp;
     GroupCtx c;
-    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, nullptr,
-                     A.last_img, nullptr, nullptr, A.Gp, blockIdx.x * 4 + warp, lane, c))
-        return;
-    unsigned* out = A.masks_out + A.mask_off[blockIdx.x * 4 + warp];
-    for (int base = 0, w = 0; base < c.maxlast; base += 32, ++w) {
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, gi, lane, c)) return;
+    const int mylast = c.active ? A.last_img[c.pix] : 0;
+    const int maxlast = __reduce_max_sync(0xffffffffu, mylast);
+    const int* tl = A.entries + A.tile_offsets[c.tile];
+    const long long off = A.mask_off[gi];
+    int* glist = A.glist_out + off;
+    unsigned* mout = A.masks_out + off;
+    int run = 0, nb = 0, cw = 0;
+    unsigned long long buf = 0ull;
+    for (int base = 0; base < maxlast; base += 32) {
         const int j = base + lane;
-        if (j < c.maxlast) {
-            const float4* r = A.rec + 3 * (c.vbase + c.list[j]);
+        int g = 0;
+        if (j < maxlast) {
+            g = tl[j];
+            const float4* r = A.rec + 3 * (c.vbase + g);
             s_rec[warp][lane][0] = r[0];
             s_rec[warp][lane][1] = r[1];
         }
         __syncwarp();
-        const int m = min(32, c.mylast - base);
+        const int mn = min(32, mylast - base);
         unsigned bits = 0u;
-        for (int k = 0; k < m; ++k) {
+        for (int k = 0; k < mn; ++k) {
             Alpha a;
             if (eval_alpha(s_rec[warp][k][0], s_rec[warp][k][1], c.pxc, c.pyc, a)) bits |= 1u << k;
         }
-        out[w * 32 + lane] = bits;
+        const unsigned un = __reduce_or_sync(0xffffffffu, bits);
+        const int rank = __popc(un & ((1u << lane) - 1u));
+        const unsigned col = transpose32(bits, lane);  // lane k: pixels blending entry k
+        if ((un >> lane) & 1u) {
+            glist[run + rank] = g;
+            s_col[warp][rank] = col;
+        }
+        __syncwarp();
+        const int nu = __popc(un);
+        const unsigned packed = transpose32(lane < nu ? s_col[warp][lane] : 0u, lane);
+        buf |= static_cast<unsigned long long>(packed) << nb;
+        nb += nu;
+        run += nu;
+        if (nb >= 32) {
+            mout[32 * cw + lane] = static_cast<unsigned>(buf);
+            ++cw;
+            buf >>= 32;
+            nb -= 32;
+        }
         __syncwarp();
     }
+    if (nb > 0) mout[32 * cw + lane] = static_cast<unsigned>(buf);
+    if (lane == 0) A.gcount_out[gi] = run;
+}
+
+// ------------------------------------------------------------------ mask statistics
+// Diagnostic (tools/mask_stats.py) over the compacted windows:
+// st[0] groups, [1] windows, [2] blended pairs, [3] sum_w max_lane popc (the
+// per-lane sparse walks' iteration count), [4] compacted entries, [5] sum over
+// 64-entry windows of max popc, [6] sum_w max column popc.
+__global__ void __launch_bounds__(32) k_mask_stats(SampleArgs A, unsigned long long* st) {
+    const int lane = threadIdx.x;
+    GroupCtx c;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, blockIdx.x, lane, c)) return;
+    const int nun = A.gcount[blockIdx.x];
+    const int ncw = (nun + 31) >> 5;
+    const unsigned* masks = A.masks + A.mask_off[blockIdx.x];
+    unsigned long long s[7] = {1ull, (unsigned long long)ncw, 0ull, 0ull, (unsigned long long)nun, 0ull, 0ull};
+    int pend = 0;
+    for (int w = 0; w < ncw; ++w) {
+        const unsigned m = c.active ? masks[32 * w + lane] : 0u;
+        s[2] += __popc(m);
+        s[3] += __reduce_max_sync(0xffffffffu, __popc(m));
+        s[6] += __reduce_max_sync(0xffffffffu, __popc(transpose32(m, lane)));
+        pend += __popc(m);
+        if ((w & 1) || w == ncw - 1) {
+            s[5] += __reduce_max_sync(0xffffffffu, pend);
+            pend = 0;
+        }
+    }
+    for (int o = 16; o; o >>= 1) s[2] += __shfl_xor_sync(0xffffffffu, s[2], o);
+    if (lane == 0)
+        for (int i = 0; i < 7; ++i)
+            if (s[i]) atomicAdd(st + i, s[i]);
+}
+
+void launch_mask_stats(const SampleArgs& a, unsigned long long* st, cudaStream_t stream) {
+    if (a.n_groups == 0) return;
+    k_mask_stats<<<a.n_groups, 32, 0, stream>>>(a, st); ++g_launches;
 }
 
 // ------------------------------------------------------------------ products
@@ -224,24 +293,40 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
                  : "memory");
 }
 
-// Window prefetch: mask word and (speculatively, only entries < maxlast) the
-// splat record (and tangent record) of entry 32w+lane.
+// Packed FP32 FMA (sm_100 FFMA2): d = a * b + c on two lanes of a float2.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+// Window prefetch (lane = compacted entry 32w+lane): mask word of the lane's
+// pixel and the entry's splat record (and tangent record).
 struct Prefetch {
     unsigned m;
     int g;
     float4 r0, r1, r2, t0, t1, t2;
 };
 
+struct WinCtx {
+    const int* list;
+    const unsigned* masks;
+    int nun, nwin;
+};
+
 template <bool TAN>
-__device__ __forceinline__ void prefetch(const GroupCtx& c, const float4* __restrict__ rec,
-                                         const float4* __restrict__ tan, int w, int nwin, int lane,
-                                         Prefetch& P) {
+__device__ __forceinline__ void prefetch(const GroupCtx& c, const WinCtx& W, const float4* __restrict__ rec,
+                                         const float4* __restrict__ tan, int w, int lane, Prefetch& P) {
     P.m = 0u;
-    if (w >= nwin) return;
-    P.m = c.active ? c.masks[w * 32 + lane] : 0u;
+    if (w >= W.nwin) return;
+    P.m = c.active ? W.masks[w * 32 + lane] : 0u;
     const int j = w * 32 + lane;
-    if (j < c.maxlast) {
-        P.g = c.list[j];
+    if (j < W.nun) {
+        P.g = W.list[j];
         const size_t rg = c.vbase + P.g;
         P.r0 = rec[3 * rg];
         P.r1 = rec[3 * rg + 1];
@@ -267,46 +352,55 @@ __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, 
     dst[8][lane] = c.x;
 }
 
+// The sampled-pixel products over the compacted window stream.
+//  pass 1 (JVP/GN, lane = pixel): dual blend over the lane's own blended
+//    entries of each window (jvp, jacobian.cpp:191-211);
+//  J^T (VJP/GN/RHS), per window:
+//    phase A (lane = pixel): front-to-back over the lane's blended entries,
+//      keeping T and the colour prefix S; suffix = C_final - S_incl gives
+//      dL/dalpha (backward_pixel_vjp :67-94); the pair scalars
+//      (dL/dpower, alpha T) go to a smem [pixel][entry] tile;
+//    phase B (lane = entry): dense walk over the 32 pixels with broadcast
+//      reads of the pixel's local coordinates and u, accumulating six moments
+//      sum dL/dpower * {1, x, y, x^2, xy, y^2} and sum alpha T u_c with packed
+//      FFMA2; the entry's conic turns the moments into the 9-float
+//      intermediate gradient once (dL/do = sum dL/dpower / o), one vector
+//      red.global.add per 4 floats.
 template <int MODE>
 __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     // window staging, struct-of-arrays so lanes reading different entries hit
     // different banks: record fields (mx, my, A, B, C, o, r, g, b)
     __shared__ float s_f[4][9][32];
-    __shared__ int s_g[4][32];
-    // pass 1 stages tangent records here; pass 2 the half-window pair tile
-    // [3][pixel 32][entry 16 (+1 pad)]: (dL/dpower, dL/dalpha * e, alpha*T)
-    __shared__ __align__(16) float s_raw[4][3 * 32 * 17];
-    __shared__ float4 s_pix[4][32];  // per pixel lane: (px+.5, py+.5, u0, u1)
-    __shared__ float s_pu2[4][32];
+    // pass 1 stages the tangent records here ([9][32]); the J^T pass the pair
+    // tile [pixel][entry (+1 pad)] of (dL/dpower, alpha T)
+    __shared__ __align__(16) float2 s_pair[4][32][33];
+    __shared__ float4 s_phi[4][32][2];  // per pixel: (x, y, x^2, xy), (y^2, u2, u0, u1), tile-centre coords
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * 4 + warp;
     GroupCtx c;
-    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, A.sorig,
-                     A.last_img, A.masks, A.mask_off, A.Gp, blockIdx.x * 4 + warp, lane, c))
-        return;
-    constexpr float kLn2f = 0.69314718055994530942f;
-    const int nwin = (c.maxlast + 31) >> 5;
-    float(*s_t)[32] = reinterpret_cast<float(*)[32]>(&s_raw[warp][0]);  // tangent fields [9][32]
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, A.sorig, A.Gp, gi, lane, c)) return;
+    WinCtx W;
+    W.nun = A.gcount[gi];
+    W.nwin = (W.nun + 31) >> 5;
+    W.list = A.glist + A.mask_off[gi];
+    W.masks = A.masks + A.mask_off[gi];
     float(*sf)[32] = s_f[warp];
-    float(*t_dp)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][0]);
-    float(*t_de)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][32 * 17]);
-    float(*t_w)[17] = reinterpret_cast<float(*)[17]>(&s_raw[warp][2 * 32 * 17]);
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     if (MODE == kJvp || MODE == kGn) {
-        // ---- Jv: dual blend over the lane's own blended entries
+        float(*s_t)[32] = reinterpret_cast<float(*)[32]>(&s_pair[warp][0][0]);  // tangent fields [9][32]
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
         Prefetch P;
-        prefetch<true>(c, A.rec, A.tan, 0, nwin, lane, P);
-        for (int w = 0; w < nwin; ++w) {
+        prefetch<true>(c, W, A.rec, A.tan, 0, lane, P);
+        for (int w = 0; w < W.nwin; ++w) {
             unsigned m = P.m;
-            const unsigned un = __reduce_or_sync(0xffffffffu, m);
-            if ((un >> lane) & 1u) {
+            if (w * 32 + lane < W.nun) {
                 stage_rec(sf, lane, P.r0, P.r1, P.r2);
                 stage_rec(s_t, lane, P.t0, P.t1, P.t2);
             }
             __syncwarp();
-            prefetch<true>(c, A.rec, A.tan, w + 1, nwin, lane, P);
+            prefetch<true>(c, W, A.rec, A.tan, w + 1, lane, P);
             while (m) {
                 const int k = __ffs(m) - 1;
                 m &= m - 1;
@@ -358,101 +452,84 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
         }
     }
 
-    // ---- J^T pass, per half-window (16 entries):
-    //  phase A (lane = pixel): front-to-back over the lane's blended entries,
-    //    pair scalars into the [pixel][entry] tile;
-    //  phase B (lane = entry e + 16 * pixel-half): sum the column's pixels in
-    //    registers, combine the two pixel halves with one xor-16 shuffle per
-    //    accumulator, apply the entry's conic once, vector red.global.add.
+    // ---- J^T pass
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
-    s_pix[warp][lane] = make_float4(c.pxc, c.pyc, u0, u1);
-    s_pu2[warp][lane] = u2;
-    const int e16 = lane & 15, ph = lane >> 4;
-    const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
+    {
+        const float lx = c.pxc - c.ox, ly = c.pyc - c.oy;
+        s_phi[warp][lane][0] = make_float4(lx, ly, lx * lx, lx * ly);
+        s_phi[warp][lane][1] = make_float4(ly * ly, u2, u0, u1);
+    }
+    float2(*pt)[33] = s_pair[warp];
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
-    prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
+    prefetch<false>(c, W, A.rec, nullptr, 0, lane, P);
     __syncwarp();
-    for (int w = 0; w < nwin; ++w) {
+    for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = P.m;
-        const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        if ((un >> lane) & 1u) {
-            stage_rec(sf, lane, P.r0, P.r1, P.r2);
-            s_g[warp][lane] = P.g;
+        const bool ent = w * 32 + lane < W.nun;
+        const float4 e0 = P.r0;  // this lane's entry: mx, my, A, B
+        const float e_c = P.r1.x, e_o = P.r1.y;
+        const int e_g = P.g;
+        if (ent) stage_rec(sf, lane, P.r0, P.r1, P.r2);
+        __syncwarp();
+        prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
+        const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
+        // phase A (lane = pixel)
+        for (unsigned m = m0; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
+            const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
+            Alpha a;
+            eval_alpha(r0, r1, c.pxc, c.pyc, a);
+            const float alpha = a.alpha;
+            const float c2 = sf[8][k];
+            const float wgt = __fmul_rn(alpha, T);
+            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
+                        n2 = __fmaf_rn(wgt, c2, S2);
+            const float inv1m = __fdividef(1.0f, 1.0f - alpha);
+            const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) +
+                                 u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
+                                 u2 * (T * c2 - (Cf2 - n2) * inv1m);
+            pt[lane][k] = make_float2(a.clamped ? 0.0f : dalpha * alpha, wgt);
+            S0 = n0;
+            S1 = n1;
+            S2 = n2;
+            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
         }
         __syncwarp();
-        prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
-        const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            const unsigned hun = (un >> (16 * h)) & 0xFFFFu;
-            if (!hun) continue;
-            for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {  // phase A
-                const int kk = __ffs(m) - 1, k = 16 * h + kk;
-                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
-                const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
-                Alpha a;
-                eval_alpha(r0, r1, c.pxc, c.pyc, a);
-                const float alpha = a.alpha;
-                const float c2 = sf[8][k];
-                const float wgt = __fmul_rn(alpha, T);
-                const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
-                            n2 = __fmaf_rn(wgt, c2, S2);
-                const float inv1m = __fdividef(1.0f, 1.0f - alpha);
-                const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) +
-                                     u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
-                                     u2 * (T * c2 - (Cf2 - n2) * inv1m);
-                t_dp[lane][kk] = a.clamped ? 0.0f : dalpha * alpha;
-                t_de[lane][kk] = a.clamped ? 0.0f : dalpha * a.e;
-                t_w[lane][kk] = wgt;
-                S0 = n0;
-                S1 = n1;
-                S2 = n2;
-                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-            }
-            const int k = 16 * h + e16;
-            const unsigned colk = __shfl_sync(0xffffffffu, col, k) & pmask;
-            __syncwarp();
-            // phase B
-            const float qmx = sf[0][k], qmy = sf[1][k];
-            float g6 = 0.f, g7 = 0.f, g8 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f, se = 0.f;
-            for (unsigned cc = colk; cc; cc &= cc - 1) {
-                const int p = __ffs(cc) - 1;
-                const float4 pi = s_pix[warp][p];
-                const float pu2 = s_pu2[warp][p];
-                const float dp = t_dp[p][e16], de = t_de[p][e16], wg = t_w[p][e16];
-                const float dx = qmx - pi.x, dy = qmy - pi.y;
-                g6 += pi.z * wg;
-                g7 += pi.w * wg;
-                g8 += pu2 * wg;
-                const float dpx = dp * dx, dpy = dp * dy;
-                sx += dpx;
-                sy += dpy;
-                sxx += dpx * dx;
-                sxy += dpx * dy;
-                syy += dpy * dy;
-                se += de;
-            }
-            g6 += __shfl_xor_sync(0xffffffffu, g6, 16);
-            g7 += __shfl_xor_sync(0xffffffffu, g7, 16);
-            g8 += __shfl_xor_sync(0xffffffffu, g8, 16);
-            sx += __shfl_xor_sync(0xffffffffu, sx, 16);
-            sy += __shfl_xor_sync(0xffffffffu, sy, 16);
-            sxx += __shfl_xor_sync(0xffffffffu, sxx, 16);
-            sxy += __shfl_xor_sync(0xffffffffu, sxy, 16);
-            syy += __shfl_xor_sync(0xffffffffu, syy, 16);
-            se += __shfl_xor_sync(0xffffffffu, se, 16);
-            if (ph == 0 && ((hun >> e16) & 1u)) {
-                const float ca = -2.0f * kLn2f * sf[2][k], cb = -kLn2f * sf[3][k], cc = -2.0f * kLn2f * sf[4][k];
-                float* dst = A.inter + (c.vbase + s_g[warp][k]) * kRec;
-                red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
-                red_add_v4(dst + 4, -0.5f * syy, se, g6, g7);
-                atomicAdd(dst + 8, g8);
-            }
-            __syncwarp();
+        // phase B (lane = entry), dense over the pixels
+        float M0 = 0.f;
+        float2 M12 = make_float2(0.f, 0.f), M34 = M12, M5G2 = M12, G01 = M12;
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            float2 v = pt[p][lane];
+            const bool b = (col >> p) & 1u;
+            v.x = b ? v.x : 0.0f;
+            v.y = b ? v.y : 0.0f;
+            const float4 f0 = s_phi[warp][p][0], f1 = s_phi[warp][p][1];
+            M12 = ffma2(make_float2(v.x, v.x), make_float2(f0.x, f0.y), M12);
+            M34 = ffma2(make_float2(v.x, v.x), make_float2(f0.z, f0.w), M34);
+            M5G2 = ffma2(v, make_float2(f1.x, f1.y), M5G2);
+            G01 = ffma2(make_float2(v.y, v.y), make_float2(f1.z, f1.w), G01);
+            M0 += v.x;
         }
+        if (ent) {
+            // moments about the tile centre -> sums over dx = mx - x, dy = my - y
+            const float mx = e0.x - c.ox, my = e0.y - c.oy;
+            const float sx = mx * M0 - M12.x, sy = my * M0 - M12.y;
+            const float sxx = mx * (mx * M0 - 2.0f * M12.x) + M34.x;
+            const float sxy = mx * (my * M0 - M12.y) - my * M12.x + M34.y;
+            const float syy = my * (my * M0 - 2.0f * M12.y) + M5G2.x;
+            constexpr float kLn2f = 0.69314718055994530942f;
+            const float ca = -2.0f * kLn2f * e0.z, cb = -kLn2f * e0.w, cc = -2.0f * kLn2f * e_c;
+            float* dst = A.inter + (c.vbase + e_g) * kRec;
+            red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
+            red_add_v4(dst + 4, -0.5f * syy, __fdividef(M0, e_o), G01.x, G01.y);
+            atomicAdd(dst + 8, M5G2.y);
+        }
+        __syncwarp();
     }
 }
 
@@ -465,23 +542,25 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
 // M = sum_pixels s gpow gpow^T (15 floats), sum W_c dalpha_c^2 (alpha/o)^2 (1),
 // and sum W_c (alpha T)^2 per channel (3); k_diag_finalize applies P_j,
 // dsig and dcol (chain.cu).  Layout per (view, Gaussian): 20 floats.
-// Same two-phase window walk as the J^T pass; the pair scalars are
-// (sum_c W_c dalpha_c^2, alpha*T).
+// Same compacted window walk as the J^T pass, in half-windows of 16 entries:
+// phase A (lane = pixel) writes (alpha^2 s, e^2 s, (alpha T)^2) per pair,
+// phase B (lane = entry x pixel half) sums its column as monomials in (dx, dy).
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     __shared__ float s_f[4][9][32];
     __shared__ int s_g[4][32];
-    // half-window pair tile [3][pixel][entry]: (alpha^2 s, e^2 s, (alpha T)^2),
-    // s = sum_c W_c dalpha_c^2 (geometry / opacity terms zero when clamped)
     __shared__ float s_t[4][3][32][17];
     __shared__ float4 s_pix[4][32];  // (px+.5, py+.5, W0, W1)
     __shared__ float s_pw2[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * 4 + warp;
     GroupCtx c;
-    if (!setup_group(A.groups, A.n_groups, A.cams, A.tile_offsets, A.entries, A.spix, nullptr,
-                     A.last_img, A.masks, A.mask_off, A.Gp, blockIdx.x * 4 + warp, lane, c))
-        return;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, gi, lane, c)) return;
+    WinCtx W;
+    W.nun = A.gcount[gi];
+    W.nwin = (W.nun + 31) >> 5;
+    W.list = A.glist + A.mask_off[gi];
+    W.masks = A.masks + A.mask_off[gi];
     constexpr float kLn2f = 0.69314718055994530942f;
-    const int nwin = (c.maxlast + 31) >> 5;
     float(*sf)[32] = s_f[warp];
     const float W0 = c.active ? A.sw[3 * c.s] : 0.f, W1 = c.active ? A.sw[3 * c.s + 1] : 0.f,
                 W2 = c.active ? A.sw[3 * c.s + 2] : 0.f;
@@ -494,22 +573,21 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
-    prefetch<false>(c, A.rec, nullptr, 0, nwin, lane, P);
+    prefetch<false>(c, W, A.rec, nullptr, 0, lane, P);
     __syncwarp();
-    for (int w = 0; w < nwin; ++w) {
+    for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = P.m;
-        const unsigned un = __reduce_or_sync(0xffffffffu, m0);
-        if ((un >> lane) & 1u) {
+        if (w * 32 + lane < W.nun) {
             stage_rec(sf, lane, P.r0, P.r1, P.r2);
             s_g[warp][lane] = P.g;
         }
         __syncwarp();
-        prefetch<false>(c, A.rec, nullptr, w + 1, nwin, lane, P);
+        prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
         const unsigned col = transpose32(m0, lane);
+        const int nent = min(32, W.nun - w * 32);
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-            const unsigned hun = (un >> (16 * h)) & 0xFFFFu;
-            if (!hun) continue;
+            if (16 * h >= nent) break;
             for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {
                 const int kk = __ffs(m) - 1, k = 16 * h + kk;
                 const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
@@ -571,7 +649,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             HSUM(m4x); HSUM(mx3y); HSUM(mx2y2); HSUM(mxy3); HSUM(m4y); HSUM(aop);
             HSUM(ac0); HSUM(ac1); HSUM(ac2);
 #undef HSUM
-            if (ph == 0 && ((hun >> e16) & 1u)) {
+            if (ph == 0 && k < nent) {
                 const float ca = -2.0f * kLn2f * sf[2][k], cb = -kLn2f * sf[3][k], cc = -2.0f * kLn2f * sf[4][k];
                 // M_ij = sum sdp gp_i gp_j, gp = (-(ca X + cb Y), -(cb X + cc Y), -X^2/2, -XY, -Y^2/2)
                 const float M00 = ca * ca * m2x + 2.0f * ca * cb * mxy + cb * cb * m2y;

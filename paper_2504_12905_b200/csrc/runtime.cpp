@@ -375,6 +375,7 @@ struct Samples {
     DevBuf<float> sw;
     DevBuf<long long> mask_off;
     DevBuf<unsigned> masks;
+    DevBuf<int> glist, gcount;
     std::vector<int> order;  // group order -> plan sample index
     std::vector<int> hpix, horig;
     std::vector<float> hw;
@@ -439,6 +440,8 @@ struct Samples {
         cudaStream_t st = ctx->stream;
         mask_off.ensure(std::max<size_t>(hoff.size(), 1));
         masks.ensure(std::max<long long>(mask_words, 1));
+        glist.ensure(std::max<long long>(mask_words, 1));
+        gcount.ensure(std::max<size_t>(hgroups.size(), 1));
         groups.ensure(std::max<size_t>(hgroups.size(), 1));
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
@@ -503,6 +506,8 @@ struct Jacobian {
         // the blend masks depend on the state only: computed once per (state, plan)
         SampleArgs a = args();
         a.masks_out = samples.masks.p;
+        a.glist_out = samples.glist.p;
+        a.gcount_out = samples.gcount.p;
         launch_masks(a, ctx->stream);
         ctx->check_launch();
     }
@@ -525,6 +530,8 @@ struct Jacobian {
         a.gt = batch->gt.p;
         a.inter = inter.p;
         a.masks = samples.masks.p;
+        a.glist = samples.glist.p;
+        a.gcount = samples.gcount.p;
         a.mask_off = samples.mask_off.p;
         return a;
     }
@@ -583,6 +590,8 @@ struct Jacobian {
         d.last_img = batch->last.p;
         d.diagacc = diagacc.p;
         d.masks = samples.masks.p;
+        d.glist = samples.glist.p;
+        d.gcount = samples.gcount.p;
         d.mask_off = samples.mask_off.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
@@ -1575,6 +1584,18 @@ int slm_jacobian_stats(slm_jacobian* j, int64_t* out) {
     out[4] = static_cast<int64_t>(j->jac->samples.hgroups.size());
     out[5] = b.n_tiles;
     return SLM_OK;
+}
+int slm_jacobian_mask_stats(slm_jacobian* j, uint64_t* out) {
+    return guarded([&] {
+        Jacobian& J = *j->jac;
+        J.ctx->activate();
+        DevBuf<unsigned long long> d;
+        d.ensure(16);
+        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 16 * sizeof(unsigned long long), J.ctx->stream));
+        launch_mask_stats(J.args(), d.p, J.ctx->stream);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(out, d.p, 13 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, J.ctx->stream));
+        J.ctx->sync();
+    });
 }
 int slm_jacobian_pcg(slm_jacobian* j, double lambda, const double* b, const double* minv, int max_iters,
                      double* x, slm_pcg_result* res) {

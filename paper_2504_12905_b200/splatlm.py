@@ -98,6 +98,7 @@ _SIGS = {
     "slm_jacobian_pcg": (C.c_int, [_vp, C.c_double, _f64p, _f64p, C.c_int, _f64p,
                                    C.POINTER(CPcgResult)]),
     "slm_jacobian_stats": (C.c_int, [_vp, _i64p]),
+    "slm_jacobian_mask_stats": (C.c_int, [_vp, _i64p]),
     "slm_pcg_solve": (C.c_int, [_vp, _APPLY, _vp, _f64p, _f64p, C.c_int64, C.c_int, _f64p,
                                 C.POINTER(CPcgResult)]),
     "slm_learning_rate": (C.c_int, [_vp, _f64p, C.c_int64, C.c_int, C.POINTER(CLmConfig), _f64p]),
@@ -595,6 +596,13 @@ class Jacobian:
         self.L.dll.slm_jacobian_stats(self.h, i64ptr(out))
         return dict(views=int(out[0]), valid=int(out[1]), entries=int(out[2]), samples=int(out[3]), groups=int(out[4]),
                     tiles=int(out[5]))
+
+    def mask_stats(self) -> dict:
+        """Diagnostic counters of the blend masks (raster.cu k_mask_stats)."""
+        out = np.zeros(13, np.int64)
+        self.L._check(self.L.dll.slm_jacobian_mask_stats(self.h, i64ptr(out)))
+        keys = ["groups", "windows", "pairs", "it_walk", "entries", "it_walk64", "it_col"]
+        return dict(zip(keys, (int(x) for x in out)))
 
 
 class TrainData:
