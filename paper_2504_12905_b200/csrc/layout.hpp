@@ -70,6 +70,14 @@ struct SampleArgs {
     unsigned* masks_out;        // k_masks outputs (same buffers)
     int* glist_out;
     int* gcount_out;
+    int* grows_out;             // k_masks: alpha-stream rows of the group (sum_w max_lane popc)
+    // Per-pair alpha stream (k_alpha, once per state/plan): window w of group g
+    // owns rows [srow_off[g] + r_w, + max_lane popc), row i = the lanes' i-th
+    // blended entry of the window, 32 floats (lane order); value = alpha, negated
+    // when alpha was clamped at 0.99 (frozen derivative).
+    const long long* srow_off;
+    const float* astream;
+    float* astream_out;
 };
 
 struct DiagArgs {

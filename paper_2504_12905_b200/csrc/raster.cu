@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     const long long off = A.mask_off[gi];
     int* glist = A.glist_out + off;
     unsigned* mout = A.masks_out + off;
-    int run = 0, nb = 0, cw = 0;
+    int run = 0, nb = 0, cw = 0, rows = 0;
     unsigned long long buf = 0ull;
     for (int base = 0; base < maxlast; base += 32) {
         const int j = base + lane;
@@ -239,15 +239,60 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
         nb += nu;
         run += nu;
         if (nb >= 32) {
-            mout[32 * cw + lane] = static_cast<unsigned>(buf);
+            const unsigned word = static_cast<unsigned>(buf);
+            mout[32 * cw + lane] = word;
+            rows += __reduce_max_sync(0xffffffffu, __popc(word));
             ++cw;
             buf >>= 32;
             nb -= 32;
         }
         __syncwarp();
     }
-    if (nb > 0) mout[32 * cw + lane] = static_cast<unsigned>(buf);
-    if (lane == 0) A.gcount_out[gi] = run;
+    if (nb > 0) {
+        const unsigned word = static_cast<unsigned>(buf);
+        mout[32 * cw + lane] = word;
+        rows += __reduce_max_sync(0xffffffffu, __popc(word));
+    }
+    if (lane == 0) {
+        A.gcount_out[gi] = run;
+        A.grows_out[gi] = rows;
+    }
+}
+
+// Once per (state, plan), after k_masks: the alpha of every blended pair in
+// the order the product passes consume them (SampleArgs::srow_off), so the
+// passes never re-evaluate the Gaussian falloff: alpha comes from a TMA-staged
+// row, and the geometry enters the derivative passes only through the
+// pre-combined tangent polynomial.  Same eval_alpha as k_render / k_masks.
+__global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
+    __shared__ float4 s_rec[4][32][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi = blockIdx.x * 4 + warp;
+    GroupCtx c;
+    if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, gi, lane, c)) return;
+    const int nun = A.gcount[gi];
+    const int* list = A.glist + A.mask_off[gi];
+    const unsigned* masks = A.masks + A.mask_off[gi];
+    float* out = A.astream_out + 32 * A.srow_off[gi];
+    for (int w = 0, row = 0; 32 * w < nun; ++w) {
+        const int j = 32 * w + lane;
+        if (j < nun) {
+            const float4* r = A.rec + 3 * (c.vbase + list[j]);
+            s_rec[warp][lane][0] = r[0];
+            s_rec[warp][lane][1] = r[1];
+        }
+        unsigned m = c.active ? masks[32 * w + lane] : 0u;
+        const int npc = __reduce_max_sync(0xffffffffu, __popc(m));
+        __syncwarp();
+        for (int i = 0; m; m &= m - 1, ++i) {
+            const int k = __ffs(m) - 1;
+            Alpha a;
+            eval_alpha(s_rec[warp][k][0], s_rec[warp][k][1], c.pxc, c.pyc, a);
+            out[32 * (row + i) + lane] = a.clamped ? -a.alpha : a.alpha;
+        }
+        row += npc;
+        __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ mask statistics
@@ -339,6 +384,64 @@ __device__ __forceinline__ void prefetch(const GroupCtx& c, const WinCtx& W, con
     }
 }
 
+// Two-stage window pipeline for the product passes: while window w runs, the
+// records of window w+1 and the mask word / list index of window w+2 are in
+// flight, so no load result is consumed in the window that issued it.
+struct WinPipe {
+    unsigned m_cur, m_nxt;  // mask words of windows w, w+1
+    int g_cur, g_nxt;       // Gaussian index of this lane's entry in windows w, w+1
+    float4 r0, r1, r2, t0, t1, t2;  // records of this lane's entry in window w
+};
+
+__device__ __forceinline__ void win_index(const GroupCtx& c, const WinCtx& W, int w, int lane, unsigned& m, int& g) {
+    m = 0u;
+    g = 0;
+    if (w < W.nwin) {
+        m = c.active ? W.masks[w * 32 + lane] : 0u;
+        if (w * 32 + lane < W.nun) g = W.list[w * 32 + lane];
+    }
+}
+
+template <bool TAN>
+__device__ __forceinline__ void win_records(const GroupCtx& c, const WinCtx& W, const float4* __restrict__ rec,
+                                            const float4* __restrict__ tan, int w, int g, int lane, WinPipe& P) {
+    if (w < W.nwin && w * 32 + lane < W.nun) {
+        const size_t rg = c.vbase + g;
+        P.r0 = rec[3 * rg];
+        P.r1 = rec[3 * rg + 1];
+        P.r2 = rec[3 * rg + 2];
+        if (TAN) {
+            P.t0 = tan[3 * rg];
+            P.t1 = tan[3 * rg + 1];
+            P.t2 = tan[3 * rg + 2];
+        }
+    }
+}
+
+template <bool TAN>
+__device__ __forceinline__ void win_start(const GroupCtx& c, const WinCtx& W, const float4* rec, const float4* tan,
+                                          int lane, WinPipe& P) {
+    win_index(c, W, 0, lane, P.m_cur, P.g_cur);
+    win_records<TAN>(c, W, rec, tan, 0, P.g_cur, lane, P);
+    win_index(c, W, 1, lane, P.m_nxt, P.g_nxt);
+}
+
+// After window w's records are staged: start window w+1's records and w+2's index.
+template <bool TAN>
+__device__ __forceinline__ void win_advance(const GroupCtx& c, const WinCtx& W, const float4* rec, const float4* tan,
+                                            int w, int lane, WinPipe& P) {
+    win_records<TAN>(c, W, rec, tan, w + 1, P.g_nxt, lane, P);
+    P.m_cur = P.m_nxt;
+    P.g_cur = P.g_nxt;
+    win_index(c, W, w + 2, lane, P.m_nxt, P.g_nxt);
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Write a 9-float record (3 float4, first 9 used) as column `lane` of [9][32].
 __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, float4 b, float4 c) {
     dst[0][lane] = a.x;
@@ -352,9 +455,62 @@ __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, 
     dst[8][lane] = c.x;
 }
 
+// ---- TMA bulk copies of alpha-stream rows into shared memory
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// One lane: arm the barrier with the byte count and start the copy.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Double-buffered alpha rows of one warp: window w's rows land in buf[w & 1],
+// the copy for window w+1 is in flight while window w runs.
+struct AlphaPipe {
+    float* buf0;
+    float* buf1;
+    uint64_t* bar;
+    const float* src;  // the group's first row
+    long long next;    // row of the next window to issue
+    uint32_t par;      // parity bit per buffer
+    __device__ __forceinline__ void issue(int w, int rows, int lane) {
+        if (lane == 0 && rows > 0)
+            bulk_load((w & 1) ? buf1 : buf0, src + 32 * next, 128u * rows, bar + (w & 1));
+        next += rows;
+    }
+    __device__ __forceinline__ const float* wait(int w, int rows) {
+        if (rows > 0) {
+            mbar_wait(bar + (w & 1), (par >> (w & 1)) & 1u);
+            par ^= 1u << (w & 1);
+        }
+        return (w & 1) ? buf1 : buf0;
+    }
+};
+
+__device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0xffffffffu, __popc(m)); }
+
 // The sampled-pixel products over the compacted window stream.
 //  pass 1 (JVP/GN, lane = pixel): dual blend over the lane's own blended
-//    entries of each window (jvp, jacobian.cpp:191-211);
+//    entries of each window (jvp, jacobian.cpp:191-211).  alpha comes from
+//    the stream; d alpha = alpha * Q(x, y) with Q the entry's tangent d(power)
+//    + do/o re-expanded as a quadratic in the pixel's tile-local coordinates
+//    (6 coefficients staged per window), so no per-pair geometry is recomputed;
 //  J^T (VJP/GN/RHS), per window:
 //    phase A (lane = pixel): front-to-back over the lane's blended entries,
 //      keeping T and the colour prefix S; suffix = C_final - S_incl gives
@@ -366,18 +522,21 @@ __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, 
 //      FFMA2; the entry's conic turns the moments into the 9-float
 //      intermediate gradient once (dL/do = sum dL/dpower / o), one vector
 //      red.global.add per 4 floats.
+constexpr int kRasterWarps = 2;
+
 template <int MODE>
-__global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
+__global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs A) {
+    constexpr int NW = kRasterWarps;
+    __shared__ __align__(128) float s_alpha[NW][2][32 * 32];
     // window staging, struct-of-arrays so lanes reading different entries hit
-    // different banks: record fields (mx, my, A, B, C, o, r, g, b)
-    __shared__ float s_f[4][9][32];
-    // pass 1 stages the tangent records here ([9][32]); the J^T pass the pair
-    // tile [pixel][entry (+1 pad)] of (dL/dpower, alpha T)
-    __shared__ __align__(16) float2 s_pair[4][32][33];
-    __shared__ float4 s_phi[4][32][2];  // per pixel: (x, y, x^2, xy), (y^2, u2, u0, u1), tile-centre coords
+    // different banks: pass 1 (tau0..5, r, g, b, dr, dg, db); J^T rows 6..8 (r, g, b)
+    __shared__ float s_f[NW][12][32];
+    __shared__ __align__(16) float2 s_pair[NW][32][33];  // [pixel][entry]: (dL/dpower, alpha T)
+    __shared__ float4 s_phi[NW][32][2];  // per pixel: (x, y, x^2, xy), (y^2, u2, u0, u1), tile-centre coords
+    __shared__ uint64_t s_bar[NW][2];
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gi = blockIdx.x * 4 + warp;
+    const int gi = blockIdx.x * NW + warp;
     GroupCtx c;
     if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, A.sorig, A.Gp, gi, lane, c)) return;
     WinCtx W;
@@ -386,41 +545,67 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     W.list = A.glist + A.mask_off[gi];
     W.masks = A.masks + A.mask_off[gi];
     float(*sf)[32] = s_f[warp];
+    if (lane == 0) {
+        mbar_init(&s_bar[warp][0], 1);
+        mbar_init(&s_bar[warp][1], 1);
+    }
+    __syncwarp();
+    AlphaPipe ap{s_alpha[warp][0], s_alpha[warp][1], s_bar[warp], A.astream + 32 * A.srow_off[gi], 0, 0u};
+    const float lx = c.pxc - c.ox, ly = c.pyc - c.oy;
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
     if (MODE == kJvp || MODE == kGn) {
-        float(*s_t)[32] = reinterpret_cast<float(*)[32]>(&s_pair[warp][0][0]);  // tangent fields [9][32]
+        const float lxx = lx * lx, lxy = lx * ly, lyy = ly * ly;
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
-        Prefetch P;
-        prefetch<true>(c, W, A.rec, A.tan, 0, lane, P);
+        WinPipe P;
+        win_start<true>(c, W, A.rec, A.tan, lane, P);
+        int rows = max_popc(P.m_cur);
+        ap.issue(0, rows, lane);
         for (int w = 0; w < W.nwin; ++w) {
-            unsigned m = P.m;
+            unsigned m = P.m_cur;
+            const int cur = rows;
             if (w * 32 + lane < W.nun) {
-                stage_rec(sf, lane, P.r0, P.r1, P.r2);
-                stage_rec(s_t, lane, P.t0, P.t1, P.t2);
+                // Q(x, y) = d(power) + do/o about the tile centre: with dx = mx - x,
+                // d(power) = A1 dx + A2 dy + A3 dx^2 + A4 dx dy + A5 dy^2
+                const float mx = P.r0.x - c.ox, my = P.r0.y - c.oy;
+                const float A1 = P.t0.x, A2 = P.t0.y, A3 = P.t0.z, A4 = P.t0.w, A5 = P.t1.x;
+                sf[0][lane] = A1 * mx + A2 * my + mx * (A3 * mx + A4 * my) + A5 * my * my +
+                              __fdividef(P.t1.y, P.r1.y);
+                sf[1][lane] = -A1 - 2.0f * A3 * mx - A4 * my;
+                sf[2][lane] = -A2 - A4 * mx - 2.0f * A5 * my;
+                sf[3][lane] = A3;
+                sf[4][lane] = A4;
+                sf[5][lane] = A5;
+                sf[6][lane] = P.r1.z;
+                sf[7][lane] = P.r1.w;
+                sf[8][lane] = P.r2.x;
+                sf[9][lane] = P.t1.z;
+                sf[10][lane] = P.t1.w;
+                sf[11][lane] = P.t2.x;
             }
             __syncwarp();
-            prefetch<true>(c, W, A.rec, A.tan, w + 1, lane, P);
-            while (m) {
+            rows = max_popc(P.m_nxt);
+            ap.issue(w + 1, rows, lane);
+            win_advance<true>(c, W, A.rec, A.tan, w, lane, P);
+            const float* sp = ap.wait(w, cur) + lane;
+            for (; m; m &= m - 1, sp += 32) {
                 const int k = __ffs(m) - 1;
-                m &= m - 1;
-                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
-                const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
-                Alpha a;
-                eval_alpha(r0, r1, c.pxc, c.pyc, a);  // blended: the mask already decided
-                const float4 t0 = make_float4(s_t[0][k], s_t[1][k], s_t[2][k], s_t[3][k]);
-                const float4 t1 = make_float4(s_t[4][k], s_t[5][k], s_t[6][k], s_t[7][k]);
-                const float c2 = sf[8][k], db = s_t[8][k];
-                const float alpha = a.alpha, dx = a.dx, dy = a.dy;
-                const float dpow = dx * (t0.x + dx * t0.z + dy * t0.w) + dy * (t0.y + dy * t1.x);
-                const float dalpha = a.clamped ? 0.0f : alpha * dpow + a.e * t1.y;
+                const float av = *sp;
+                const float alpha = fabsf(av);
+                const float Q = sf[0][k] + lx * sf[1][k] + ly * sf[2][k] + lxx * sf[3][k] + lxy * sf[4][k] +
+                                lyy * sf[5][k];
+                const float dalpha = av < 0.0f ? 0.0f : alpha * Q;
                 const float wgt = alpha * T;
-                const float dw = dalpha * T + alpha * dT;
-                dC0 += dw * r1.z + wgt * t1.z;
-                dC1 += dw * r1.w + wgt * t1.w;
-                dC2 += dw * c2 + wgt * db;
-                dT = dT * (1.0f - alpha) - T * dalpha;
-                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                const float dw = fmaf(dalpha, T, alpha * dT);
+                dC0 = fmaf(dw, sf[6][k], dC0);
+                dC0 = fmaf(wgt, sf[9][k], dC0);
+                dC1 = fmaf(dw, sf[7][k], dC1);
+                dC1 = fmaf(wgt, sf[10][k], dC1);
+                dC2 = fmaf(dw, sf[8][k], dC2);
+                dC2 = fmaf(wgt, sf[11][k], dC2);
+                const float om = __fsub_rn(1.0f, alpha);
+                dT = fmaf(dT, om, -T * dalpha);
+                T = __fmul_rn(T, om);
             }
             __syncwarp();
         }
@@ -437,6 +622,7 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
             u1 = A.sw[3 * c.s + 1] * dC1;
             u2 = A.sw[3 * c.s + 2] * dC2;
         }
+        ap.next = 0;
     } else if (MODE == kVjp) {
         if (c.active) {
             u0 = A.in_res[3 * c.orig];
@@ -456,47 +642,47 @@ __global__ void __launch_bounds__(128) k_sample_raster(SampleArgs A) {
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
-    {
-        const float lx = c.pxc - c.ox, ly = c.pyc - c.oy;
-        s_phi[warp][lane][0] = make_float4(lx, ly, lx * lx, lx * ly);
-        s_phi[warp][lane][1] = make_float4(ly * ly, u2, u0, u1);
-    }
+    s_phi[warp][lane][0] = make_float4(lx, ly, lx * lx, lx * ly);
+    s_phi[warp][lane][1] = make_float4(ly * ly, u2, u0, u1);
     float2(*pt)[33] = s_pair[warp];
-    float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
-    Prefetch P;
-    prefetch<false>(c, W, A.rec, nullptr, 0, lane, P);
+    const float uC = u0 * Cf0 + u1 * Cf1 + u2 * Cf2;
+    float T = 1.0f, uS = 0.f;
+    WinPipe P;
+    win_start<false>(c, W, A.rec, nullptr, lane, P);
+    int rows = max_popc(P.m_cur);
+    ap.issue(0, rows, lane);
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
-        const unsigned m0 = P.m;
+        const unsigned m0 = P.m_cur;
+        const int cur = rows;
         const bool ent = w * 32 + lane < W.nun;
         const float4 e0 = P.r0;  // this lane's entry: mx, my, A, B
         const float e_c = P.r1.x, e_o = P.r1.y;
-        const int e_g = P.g;
-        if (ent) stage_rec(sf, lane, P.r0, P.r1, P.r2);
+        const int e_g = P.g_cur;
+        if (ent) {
+            sf[6][lane] = P.r1.z;
+            sf[7][lane] = P.r1.w;
+            sf[8][lane] = P.r2.x;
+        }
         __syncwarp();
-        prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
+        rows = max_popc(P.m_nxt);
+        ap.issue(w + 1, rows, lane);
+        win_advance<false>(c, W, A.rec, nullptr, w, lane, P);
         const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
-        // phase A (lane = pixel)
-        for (unsigned m = m0; m; m &= m - 1) {
+        const float* sp = ap.wait(w, cur) + lane;
+        // phase A (lane = pixel); with u.S_incl kept as one running scalar:
+        // dL/dalpha = sum_c u_c (T c_c - (C_c - S_incl,c) / (1 - alpha))
+        for (unsigned m = m0; m; m &= m - 1, sp += 32) {
             const int k = __ffs(m) - 1;
-            const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
-            const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
-            Alpha a;
-            eval_alpha(r0, r1, c.pxc, c.pyc, a);
-            const float alpha = a.alpha;
-            const float c2 = sf[8][k];
+            const float av = *sp;
+            const float alpha = fabsf(av);
+            const float uc = u0 * sf[6][k] + u1 * sf[7][k] + u2 * sf[8][k];
             const float wgt = __fmul_rn(alpha, T);
-            const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
-                        n2 = __fmaf_rn(wgt, c2, S2);
-            const float inv1m = __fdividef(1.0f, 1.0f - alpha);
-            const float dalpha = u0 * (T * r1.z - (Cf0 - n0) * inv1m) +
-                                 u1 * (T * r1.w - (Cf1 - n1) * inv1m) +
-                                 u2 * (T * c2 - (Cf2 - n2) * inv1m);
-            pt[lane][k] = make_float2(a.clamped ? 0.0f : dalpha * alpha, wgt);
-            S0 = n0;
-            S1 = n1;
-            S2 = n2;
-            T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+            uS = fmaf(wgt, uc, uS);
+            const float om = __fsub_rn(1.0f, alpha);
+            const float dalpha = fmaf(T, uc, -(uC - uS) * rcp_approx(om));
+            pt[lane][k] = make_float2(av < 0.0f ? 0.0f : dalpha * alpha, wgt);
+            T = __fmul_rn(T, om);
         }
         __syncwarp();
         // phase B (lane = entry), dense over the pixels
@@ -696,14 +882,19 @@ void launch_masks(const SampleArgs& a, cudaStream_t st) {
     k_masks<<<(a.n_groups + 3) / 4, 128, 0, st>>>(a); ++g_launches;
 }
 
+void launch_alpha(const SampleArgs& a, cudaStream_t st) {
+    if (a.n_groups == 0) return;
+    k_alpha<<<(a.n_groups + 3) / 4, 128, 0, st>>>(a); ++g_launches;
+}
+
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st) {
     if (a.n_groups == 0) return;
-    const int blocks = (a.n_groups + 3) / 4;
+    const int blocks = (a.n_groups + kRasterWarps - 1) / kRasterWarps;
     switch (mode) {
-        case kJvp: k_sample_raster<kJvp><<<blocks, 128, 0, st>>>(a); ++g_launches; break;
-        case kVjp: k_sample_raster<kVjp><<<blocks, 128, 0, st>>>(a); ++g_launches; break;
-        case kGn: k_sample_raster<kGn><<<blocks, 128, 0, st>>>(a); ++g_launches; break;
-        default: k_sample_raster<kRhs><<<blocks, 128, 0, st>>>(a); ++g_launches; break;
+        case kJvp: k_sample_raster<kJvp><<<blocks, 32 * kRasterWarps, 0, st>>>(a); ++g_launches; break;
+        case kVjp: k_sample_raster<kVjp><<<blocks, 32 * kRasterWarps, 0, st>>>(a); ++g_launches; break;
+        case kGn: k_sample_raster<kGn><<<blocks, 32 * kRasterWarps, 0, st>>>(a); ++g_launches; break;
+        default: k_sample_raster<kRhs><<<blocks, 32 * kRasterWarps, 0, st>>>(a); ++g_launches; break;
     }
 }
 

@@ -375,7 +375,11 @@ struct Samples {
     DevBuf<float> sw;
     DevBuf<long long> mask_off;
     DevBuf<unsigned> masks;
-    DevBuf<int> glist, gcount;
+    DevBuf<int> glist, gcount, grows;
+    DevBuf<long long> srow_off;
+    DevBuf<float> astream;
+    std::vector<int> hrows;
+    std::vector<long long> hrow_off;
     std::vector<int> order;  // group order -> plan sample index
     std::vector<int> hpix, horig;
     std::vector<float> hw;
@@ -442,6 +446,8 @@ struct Samples {
         masks.ensure(std::max<long long>(mask_words, 1));
         glist.ensure(std::max<long long>(mask_words, 1));
         gcount.ensure(std::max<size_t>(hgroups.size(), 1));
+        grows.ensure(std::max<size_t>(hgroups.size(), 1));
+        srow_off.ensure(std::max<size_t>(hgroups.size(), 1));
         groups.ensure(std::max<size_t>(hgroups.size(), 1));
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
@@ -508,8 +514,29 @@ struct Jacobian {
         a.masks_out = samples.masks.p;
         a.glist_out = samples.glist.p;
         a.gcount_out = samples.gcount.p;
+        a.grows_out = samples.grows.p;
         launch_masks(a, ctx->stream);
         ctx->check_launch();
+        // alpha-stream layout: rows per group -> offsets (host scan), then the stream
+        const size_t ng = samples.hgroups.size();
+        samples.hrows.resize(ng);
+        samples.hrow_off.resize(ng);
+        if (ng) SLM_CUDA_CHECK(cudaMemcpyAsync(samples.hrows.data(), samples.grows.p, sizeof(int) * ng,
+                                               cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        long long rows = 0;
+        for (size_t g = 0; g < ng; ++g) {
+            samples.hrow_off[g] = rows;
+            rows += samples.hrows[g];
+        }
+        samples.astream.ensure(std::max<long long>(32 * rows, 1));
+        if (ng) SLM_CUDA_CHECK(cudaMemcpyAsync(samples.srow_off.p, samples.hrow_off.data(), sizeof(long long) * ng,
+                                               cudaMemcpyHostToDevice, ctx->stream));
+        SampleArgs b = args();
+        b.astream_out = samples.astream.p;
+        launch_alpha(b, ctx->stream);
+        ctx->check_launch();
+        ctx->sync();  // hrow_off is read by the async copy
     }
 
     SampleArgs args() const {
@@ -533,6 +560,8 @@ struct Jacobian {
         a.glist = samples.glist.p;
         a.gcount = samples.gcount.p;
         a.mask_off = samples.mask_off.p;
+        a.srow_off = samples.srow_off.p;
+        a.astream = samples.astream.p;
         return a;
     }
 

@@ -84,6 +84,7 @@ void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_
                       cudaStream_t st);
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);
 void launch_masks(const SampleArgs& a, cudaStream_t st);
+void launch_alpha(const SampleArgs& a, cudaStream_t st);
 void launch_mask_stats(const SampleArgs& a, unsigned long long* st, cudaStream_t stream);
 void launch_diag_raster(const DiagArgs& a, cudaStream_t st);
 void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
