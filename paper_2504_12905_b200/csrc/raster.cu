@@ -308,17 +308,19 @@ __global__ void __launch_bounds__(32) k_mask_stats(SampleArgs A, unsigned long l
     const int ncw = (nun + 31) >> 5;
     const unsigned* masks = A.masks + A.mask_off[blockIdx.x];
     unsigned long long s[7] = {1ull, (unsigned long long)ncw, 0ull, 0ull, (unsigned long long)nun, 0ull, 0ull};
-    int pend = 0;
+    int pend = 0, rem = c.active ? __popc(masks[lane]) : 0;
     for (int w = 0; w < ncw; ++w) {
         const unsigned m = c.active ? masks[32 * w + lane] : 0u;
+        {   // run-ahead simulation: lanes done with window w continue into w+1
+            const int nxt = (c.active && w + 1 < ncw) ? __popc(masks[32 * (w + 1) + lane]) : 0;
+            const int steps = __reduce_max_sync(0xffffffffu, rem);
+            s[5] += steps;
+            rem = nxt - min(steps - rem, nxt);
+        }
         s[2] += __popc(m);
         s[3] += __reduce_max_sync(0xffffffffu, __popc(m));
         s[6] += __reduce_max_sync(0xffffffffu, __popc(transpose32(m, lane)));
-        pend += __popc(m);
-        if ((w & 1) || w == ncw - 1) {
-            s[5] += __reduce_max_sync(0xffffffffu, pend);
-            pend = 0;
-        }
+
     }
     for (int o = 16; o; o >>= 1) s[2] += __shfl_xor_sync(0xffffffffu, s[2], o);
     if (lane == 0)

@@ -19,7 +19,7 @@ from .types import (CCamera, CGaussians, CLmConfig, CPcgResult, CPlan, CStepRepo
                     GaussianSet, LmConfig, PcgResult, SamplePlan, StepReport, cameras_to_c, f32ptr,
                     f64ptr, i32ptr, i64ptr)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslm_b200.so")
+LIB_PATH = os.environ.get("SLM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslm_b200.so")
 
 _vp = C.c_void_p
 _f64p = C.POINTER(C.c_double)
@@ -601,7 +601,8 @@ class Jacobian:
         """Diagnostic counters of the blend masks (raster.cu k_mask_stats)."""
         out = np.zeros(13, np.int64)
         self.L._check(self.L.dll.slm_jacobian_mask_stats(self.h, i64ptr(out)))
-        keys = ["groups", "windows", "pairs", "it_walk", "entries", "it_walk64", "it_col"]
+        keys = ["groups", "windows", "pairs", "it_walk", "entries", "it_walk64", "it_col",
+                "rows_le8", "rows_le16", "rows_le20", "rows_le24", "rows_le28", "rows_le32"]
         return dict(zip(keys, (int(x) for x in out)))
 
 
