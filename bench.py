@@ -340,14 +340,17 @@ def run_b200(args):
 
     # e2e through the drop-in host API (SampledJacobian::gn_apply on host f64 vectors)
     host_jac = L.jacobian(state, [cams[i] for i in batch[lo:hi]], my_plan)
-    ph = np.random.default_rng(0).uniform(-1, 1, host_jac.param_dim())
-    host_jac.gn_apply(0.1, ph)
+    # host ParamVectors in pinned memory (the e2e contract's host buffers)
+    ph = torch.empty(host_jac.param_dim(), dtype=torch.float64, pin_memory=True).numpy()
+    ph[:] = np.random.default_rng(0).uniform(-1, 1, host_jac.param_dim())
+    oh = torch.empty(host_jac.param_dim(), dtype=torch.float64, pin_memory=True).numpy()
+    host_jac.gn_apply(0.1, ph, out=oh)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        host_jac.gn_apply(0.1, ph)
+        host_jac.gn_apply(0.1, ph, out=oh)
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if dist:
         t = torch.tensor([e2e_s], device="cuda")
@@ -428,7 +431,7 @@ def run_b200(args):
         "breakdown_ms": {"tangents": prof["tangents_ms"] / n, "raster": raster_ms, "chain": prof["chain_ms"] / n},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * 14 * args.gaussians,
                 "d2h_bytes_per_step": 8 * 14 * args.gaussians,
-                "path": "slm_jacobian_gn_apply (host f64 ParamVector in/out)"},
+                "path": "slm_jacobian_gn_apply (host f64 ParamVector in/out, pinned host buffers)"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,

@@ -46,72 +46,97 @@ namespace slm { extern std::atomic<long long> g_launches; }
 namespace slm {
 
 // ------------------------------------------------------------------ K6
-__global__ void __launch_bounds__(256) k_render(
+// One CTA of 64 threads per 16x16 tile; thread t owns the 4 pixels of column
+// t & 15 at rows (t >> 4) + 4i, so every broadcast read of a staged splat record
+// serves 4 pixels (the 1-pixel-per-thread form is bound by the shared-memory
+// pipe on those broadcasts).  Per pixel the arithmetic is blend_pixel's.
+constexpr int kRenderThreads = 64;
+constexpr int kRenderPix = 4;      // pixels per thread
+constexpr int kRenderStage = 128;  // records staged per round
+
+__global__ void __launch_bounds__(kRenderThreads) k_render(
     const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
     const int* __restrict__ tile_offsets, const int* __restrict__ entries,
     const float4* __restrict__ rec, int Gp, const float* __restrict__ gt,
     float* __restrict__ image, float* __restrict__ trans, int* __restrict__ contrib,
     int* __restrict__ last_out, double* __restrict__ sse_tile) {
-    __shared__ float4 s_rec[256][3];
-    __shared__ double s_red[8];
+    __shared__ float4 s_rec[kRenderStage][3];
+    __shared__ double s_red[kRenderThreads / 32];
     const int tile = blockIdx.x;
     const int v = tile_view[tile];
     const DevCam& cam = cams[v];
     const int lt = tile - cam.tile_base;
     const int tx = lt % cam.tiles_x, ty = lt / cam.tiles_x;
-    const int x = tx * kTile + (threadIdx.x & 15), y = ty * kTile + (threadIdx.x >> 4);
-    const bool inside = x < cam.width && y < cam.height;
-    const float pxc = (float)x + 0.5f, pyc = (float)y + 0.5f;
+    const int x = tx * kTile + (threadIdx.x & 15);
+    const int y0 = ty * kTile + (threadIdx.x >> 4);
+    const float pxc = (float)x + 0.5f;
     const int b = tile_offsets[tile], n = tile_offsets[tile + 1] - b;
     const size_t vbase = static_cast<size_t>(v) * Gp;
 
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    int cnt = 0, last = n;
-    bool done = !inside;
-    for (int start = 0; start < n; start += 256) {
-        if (__syncthreads_count(done) == 256) break;
-        const int j = start + threadIdx.x;
-        if (j < n) {
-            const float4* r = rec + 3 * (vbase + entries[b + j]);
-            s_rec[threadIdx.x][0] = r[0];
-            s_rec[threadIdx.x][1] = r[1];
-            s_rec[threadIdx.x][2] = r[2];
+    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix], pyc[kRenderPix];
+    int cnt[kRenderPix], last[kRenderPix];
+    unsigned live = 0u;  // bit i: pixel i still blending
+#pragma unroll
+    for (int i = 0; i < kRenderPix; ++i) {
+        const int y = y0 + 4 * i;
+        T[i] = 1.0f;
+        C0[i] = C1[i] = C2[i] = 0.0f;
+        cnt[i] = 0;
+        last[i] = n;
+        pyc[i] = (float)y + 0.5f;
+        if (x < cam.width && y < cam.height) live |= 1u << i;
+    }
+    for (int start = 0; start < n; start += kRenderStage) {
+        if (__syncthreads_count(live != 0u) == 0) break;
+        for (int j = threadIdx.x; j < kRenderStage && start + j < n; j += kRenderThreads) {
+            const float4* r = rec + 3 * (vbase + entries[b + start + j]);
+            s_rec[j][0] = r[0];
+            s_rec[j][1] = r[1];
+            s_rec[j][2] = r[2];
         }
         __syncthreads();
-        const int m = min(256, n - start);
-        for (int k = 0; k < m && !done; ++k) {
+        const int m = min(kRenderStage, n - start);
+        for (int k = 0; k < m && live; ++k) {
             const float4 r0 = s_rec[k][0], r1 = s_rec[k][1];
-            Alpha a;
-            if (!eval_alpha(r0, r1, pxc, pyc, a)) continue;
-            float tt;
-            if (terminates(T, a.alpha, tt)) {
-                done = true;
-                last = start + k;
-                break;
-            }
-            const float w = __fmul_rn(a.alpha, T);
             const float c2 = s_rec[k][2].x;
-            C0 = __fmaf_rn(w, r1.z, C0);
-            C1 = __fmaf_rn(w, r1.w, C1);
-            C2 = __fmaf_rn(w, c2, C2);
-            T = tt;
-            ++cnt;
+#pragma unroll
+            for (int i = 0; i < kRenderPix; ++i) {
+                if (!((live >> i) & 1u)) continue;
+                Alpha a;
+                if (!eval_alpha(r0, r1, pxc, pyc[i], a)) continue;
+                float tt;
+                if (terminates(T[i], a.alpha, tt)) {
+                    live &= ~(1u << i);
+                    last[i] = start + k;
+                    continue;
+                }
+                const float w = __fmul_rn(a.alpha, T[i]);
+                C0[i] = __fmaf_rn(w, r1.z, C0[i]);
+                C1[i] = __fmaf_rn(w, r1.w, C1[i]);
+                C2[i] = __fmaf_rn(w, c2, C2[i]);
+                T[i] = tt;
+                ++cnt[i];
+            }
         }
     }
     double sq = 0.0;
-    if (inside) {
-        const size_t pix = cam.pix_base + static_cast<size_t>(y) * cam.width + x;
-        image[3 * pix] = C0;
-        image[3 * pix + 1] = C1;
-        image[3 * pix + 2] = C2;
-        trans[pix] = T;
-        contrib[pix] = cnt;
-        last_out[pix] = last;
-        if (gt) {
-            const float* gp = gt + 3 * pix;
-            const double d0 = (double)C0 - (double)gp[0], d1 = (double)C1 - (double)gp[1],
-                         d2 = (double)C2 - (double)gp[2];
-            sq = d0 * d0 + d1 * d1 + d2 * d2;
+#pragma unroll
+    for (int i = 0; i < kRenderPix; ++i) {
+        const int y = y0 + 4 * i;
+        if (x < cam.width && y < cam.height) {
+            const size_t pix = cam.pix_base + static_cast<size_t>(y) * cam.width + x;
+            image[3 * pix] = C0[i];
+            image[3 * pix + 1] = C1[i];
+            image[3 * pix + 2] = C2[i];
+            trans[pix] = T[i];
+            contrib[pix] = cnt[i];
+            last_out[pix] = last[i];
+            if (gt) {
+                const float* gp = gt + 3 * pix;
+                const double d0 = (double)C0[i] - (double)gp[0], d1 = (double)C1[i] - (double)gp[1],
+                             d2 = (double)C2[i] - (double)gp[2];
+                sq += d0 * d0 + d1 * d1 + d2 * d2;
+            }
         }
     }
     if (sse_tile) {
@@ -120,7 +145,7 @@ __global__ void __launch_bounds__(256) k_render(
         __syncthreads();
         if (threadIdx.x == 0) {
             double s = 0.0;
-            for (int i = 0; i < 8; ++i) s += s_red[i];
+            for (int i = 0; i < kRenderThreads / 32; ++i) s += s_red[i];
             sse_tile[tile] = s;
         }
     }
@@ -869,7 +894,7 @@ void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const 
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,
                    float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st) {
     if (n_tiles == 0) return;
-    k_render<<<n_tiles, 256, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
+    k_render<<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
                                       trans, contrib, last, sse_tile); ++g_launches;
 }
 

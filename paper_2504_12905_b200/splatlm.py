@@ -559,11 +559,16 @@ class Jacobian:
         self.L._check(self.L.dll.slm_jacobian_jtj_diag(self.h, f64ptr(out)))
         return out
 
-    def gn_apply(self, lam: float, p) -> np.ndarray:
+    def gn_apply(self, lam: float, p, out=None) -> np.ndarray:
+        """J^T W J p + lam p on host f64 ParamVectors; `out` (optional, f64
+        contiguous, e.g. a pinned buffer) receives the result in place."""
         p = np.ascontiguousarray(p, np.float64)
         if p.size != self.pdim:
             raise ValueError("gn_apply: probe vector length mismatch")
-        out = np.zeros(self.pdim)
+        if out is None:
+            out = np.zeros(self.pdim)
+        elif out.dtype != np.float64 or out.size != self.pdim or not out.flags.c_contiguous:
+            raise ValueError("gn_apply: out must be a contiguous f64 vector of param_dim")
         self.L._check(self.L.dll.slm_jacobian_gn_apply(self.h, lam, f64ptr(p), f64ptr(out)))
         return out
 
