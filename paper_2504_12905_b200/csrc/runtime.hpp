@@ -45,19 +45,22 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
-    // Grow-only allocation; contents are undefined after a reallocation.
+    // Grow-only allocation with 25% headroom (sizes such as the tile-list length
+    // drift from one LM step to the next; cudaFree/cudaMalloc synchronise the
+    // device); contents are undefined after a reallocation.
     T* ensure(size_t count) {
         if (count <= n && p) return p;
         release();
-        const size_t bytes = (count > 0 ? count : 1) * sizeof(T);
+        const size_t cap = count + count / 4;
+        const size_t bytes = (cap > 0 ? cap : 1) * sizeof(T);
         SLM_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&p), bytes));
-        n = count;
+        n = cap;
         return p;
     }
     T* ensure_zero(size_t count, cudaStream_t st) {
         const bool fresh = count > n || !p;
         ensure(count);
-        if (fresh) SLM_CUDA_CHECK(cudaMemsetAsync(p, 0, (count > 0 ? count : 1) * sizeof(T), st));
+        if (fresh) SLM_CUDA_CHECK(cudaMemsetAsync(p, 0, (n > 0 ? n : 1) * sizeof(T), st));
         return p;
     }
 };
