@@ -29,6 +29,7 @@ CU_SOURCES = {
     "raster.cu": [],
     "chain.cu": [],
     "cg.cu": [],
+    "sort.cu": [],
 }
 CPP_SOURCES = ["runtime.cpp"]
 HEADERS = ["common.cuh", "layout.hpp", "runtime.hpp"]

@@ -99,6 +99,16 @@ struct DiagArgs {
     const long long* mask_off;
 };
 
+// Scratch of the radix tile-list construction (sort.cu), sized by the runtime:
+// n = V*Gp (k64*, v32*, k32*, count), E = tile-list entries (t32*),
+// hist = 256 * ceil(max(n, E) / 4096), part = scan partials.
+struct TileSortBuffers {
+    unsigned long long *k64a, *k64b;
+    unsigned *v32a, *v32b, *k32a, *k32b, *count;
+    unsigned *t32a, *t32b, *t32va, *t32vb;
+    unsigned *hist, *part;
+};
+
 struct CgState {
     double rz, pu, alpha, beta, rr, bnorm;
     int iterations, breakdown, done, pad;

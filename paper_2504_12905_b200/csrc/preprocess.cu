@@ -210,202 +210,7 @@ __global__ void k_scan_tiles(const int* __restrict__ count, int n, int* __restri
     }
 }
 
-// ------------------------------------------------------------------ K3 emit
-__global__ void k_bin_scatter(int G, int Gp, int V, const DevCam* __restrict__ cams,
-                              const short4* __restrict__ rect, int* __restrict__ cursor,
-                              int* __restrict__ entries) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int v = blockIdx.y;
-    if (g >= G) return;
-    const short4 r = rect[static_cast<size_t>(v) * Gp + g];
-    if (r.x > r.y) return;
-    const int base = cams[v].tile_base, tx_n = cams[v].tiles_x;
-    for (int ty = r.z; ty <= r.w; ++ty)
-        for (int tx = r.x; tx <= r.y; ++tx) {
-            const int slot = atomicAdd(&cursor[base + ty * tx_n + tx], 1);
-            entries[slot] = g;
-        }
-}
-
-// ------------------------------------------------------------------ K4 sort
-// Per-tile sort by (depth, index) — the reference's std::sort comparator
-// (rasterizer.cpp:43-48).  (key, index) pairs are unique, so any correct sort
-// reproduces the reference order exactly.
-__device__ __forceinline__ bool pair_gt(unsigned long long ka, int va, unsigned long long kb, int vb) {
-    return ka > kb || (ka == kb && va > vb);
-}
-
-__device__ void bitonic_smem(unsigned long long* key, int* val, int np2) {
-    for (int k = 2; k <= np2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const bool up = (i & k) == 0;
-                    const unsigned long long ka = key[i], kb = key[ixj];
-                    const int va = val[i], vb = val[ixj];
-                    if (pair_gt(ka, va, kb, vb) == up) {
-                        key[i] = kb;
-                        key[ixj] = ka;
-                        val[i] = vb;
-                        val[ixj] = va;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-__device__ __forceinline__ int next_pow2(int n) {
-    int p = 1;
-    while (p < n) p <<= 1;
-    return p;
-}
-
-template <int CAP>
-__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ offsets,
-                                                   int* __restrict__ entries,
-                                                   const unsigned long long* __restrict__ keys,
-                                                   const int* __restrict__ tile_view, int Gp,
-                                                   int* __restrict__ overflow,
-                                                   int* __restrict__ overflow_count) {
-    __shared__ unsigned long long skey[CAP];
-    __shared__ int sval[CAP];
-    const int tile = blockIdx.x;
-    const int b = offsets[tile], n = offsets[tile + 1] - b;
-    if (n <= 1) return;
-    if (n > CAP) {
-        if (threadIdx.x == 0) overflow[atomicAdd(overflow_count, 1)] = tile;
-        return;
-    }
-    const size_t vbase = static_cast<size_t>(tile_view[tile]) * Gp;
-    const int np2 = next_pow2(n);
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < n) {
-            const int g = entries[b + i];
-            skey[i] = keys[vbase + g];
-            sval[i] = g;
-        } else {
-            skey[i] = ~0ull;
-            sval[i] = 0x7fffffff;
-        }
-    }
-    __syncthreads();
-    bitonic_smem(skey, sval, np2);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = sval[i];
-}
-
-// Overflow tiles (n > 2048): persistent CTAs with up to 16384 entries sorted
-// in dynamic shared memory.  Longer lists are sorted in 16384-entry chunks in
-// smem and then merged pairwise in global scratch with a merge-path split
-// per thread (log2(n/16384) passes), so any list length is handled.
-constexpr int kBigCap = 16384;
-
-__device__ __forceinline__ void load_pad(const int* __restrict__ src, int n, int np2,
-                                         const unsigned long long* __restrict__ keys, size_t vbase,
-                                         unsigned long long* skey, int* sval) {
-    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
-        if (i < n) {
-            const int g = src[i];
-            skey[i] = keys[vbase + g];
-            sval[i] = g;
-        } else {
-            skey[i] = ~0ull;
-            sval[i] = 0x7fffffff;
-        }
-    }
-    __syncthreads();
-}
-
-// Merge sorted runs A=[a0,a1) and B=[a1,b1) of (ka,va) into (kd,vd), whole CTA.
-__device__ void merge_runs(const unsigned long long* __restrict__ ka, const int* __restrict__ va,
-                           unsigned long long* __restrict__ kd, int* __restrict__ vd, int a0, int a1,
-                           int b1) {
-    const int la = a1 - a0, lb = b1 - a1, m = la + lb;
-    const int T = blockDim.x;
-    const int d0 = static_cast<int>(static_cast<long long>(m) * threadIdx.x / T);
-    const int d1 = static_cast<int>(static_cast<long long>(m) * (threadIdx.x + 1) / T);
-    auto split = [&](int d) {  // number of A elements among the first d merged outputs
-        int lo = max(0, d - lb), hi = min(d, la);
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            const int j = d - 1 - mid;
-            if (!pair_gt(ka[a0 + mid], va[a0 + mid], ka[a1 + j], va[a1 + j])) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo;
-    };
-    int i = split(d0), j = d0 - i;
-    for (int d = d0; d < d1; ++d) {
-        bool take_a;
-        if (i >= la) take_a = false;
-        else if (j >= lb) take_a = true;
-        else take_a = !pair_gt(ka[a0 + i], va[a0 + i], ka[a1 + j], va[a1 + j]);
-        if (take_a) {
-            kd[a0 + d] = ka[a0 + i];
-            vd[a0 + d] = va[a0 + i];
-            ++i;
-        } else {
-            kd[a0 + d] = ka[a1 + j];
-            vd[a0 + d] = va[a1 + j];
-            ++j;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_tile_sort_big(const int* __restrict__ offsets,
-                                                        int* __restrict__ entries,
-                                                        const unsigned long long* __restrict__ keys,
-                                                        const int* __restrict__ tile_view, int Gp,
-                                                        const int* __restrict__ overflow,
-                                                        const int* __restrict__ overflow_count,
-                                                        unsigned long long* __restrict__ scratch_k,
-                                                        int* __restrict__ scratch_v, long long max_n) {
-    extern __shared__ unsigned char smem_raw[];
-    unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem_raw);
-    int* sval = reinterpret_cast<int*>(smem_raw + sizeof(unsigned long long) * kBigCap);
-    const int cnt = *overflow_count;
-    unsigned long long* kA = scratch_k ? scratch_k + 2 * max_n * blockIdx.x : nullptr;
-    unsigned long long* kB = kA ? kA + max_n : nullptr;
-    int* vA = scratch_v ? scratch_v + 2 * max_n * blockIdx.x : nullptr;
-    int* vB = vA ? vA + max_n : nullptr;
-    for (int w = blockIdx.x; w < cnt; w += gridDim.x) {
-        const int tile = overflow[w];
-        const int b = offsets[tile], n = offsets[tile + 1] - b;
-        const size_t vbase = static_cast<size_t>(tile_view[tile]) * Gp;
-        if (n <= kBigCap) {
-            load_pad(entries + b, n, next_pow2(n), keys, vbase, skey, sval);
-            bitonic_smem(skey, sval, next_pow2(n));
-            for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = sval[i];
-            __syncthreads();
-            continue;
-        }
-        for (int c0 = 0; c0 < n; c0 += kBigCap) {  // sorted chunks -> scratch A
-            const int cn = min(kBigCap, n - c0);
-            load_pad(entries + b + c0, cn, next_pow2(cn), keys, vbase, skey, sval);
-            bitonic_smem(skey, sval, next_pow2(cn));
-            for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-                kA[c0 + i] = skey[i];
-                vA[c0 + i] = sval[i];
-            }
-            __syncthreads();
-        }
-        unsigned long long *ks = kA, *kd = kB;
-        int *vs = vA, *vd = vB;
-        for (int width = kBigCap; width < n; width <<= 1) {
-            for (int a0 = 0; a0 < n; a0 += 2 * width) {
-                const int a1 = min(a0 + width, n), b1 = min(a0 + 2 * width, n);
-                merge_runs(ks, vs, kd, vd, a0, a1, b1);
-            }
-            __syncthreads();
-            unsigned long long* tk = ks; ks = kd; kd = tk;
-            int* tv = vs; vs = vd; vd = tv;
-        }
-        for (int i = threadIdx.x; i < n; i += blockDim.x) entries[b + i] = vs[i];
-        __syncthreads();
-    }
-}
+// K3 emit and K4 sort: sort.cu (stable radix passes, no per-tile sort).
 
 // ------------------------------------------------------------------ K15 update
 // GaussianSet::apply_update (types.cpp:48-60) + renormalize_rotations
@@ -467,31 +272,6 @@ void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V
 void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total,
                        cudaStream_t st) {
     k_scan_tiles<<<1, 1024, 0, st>>>(count, n, offsets, cursor, total); ++g_launches;
-}
-
-void launch_bin_scatter(int G, int Gp, int V, const DevCam* cams, const short4* rect, int* cursor,
-                        int* entries, cudaStream_t st) {
-    if (G == 0 || V == 0) return;
-    dim3 grid((G + 255) / 256, V);
-    k_bin_scatter<<<grid, 256, 0, st>>>(G, Gp, V, cams, rect, cursor, entries); ++g_launches;
-}
-
-void launch_tile_sort(const int* offsets, int* entries, const unsigned long long* keys,
-                      const int* tile_view, int n_tiles, int Gp, int* overflow, int* overflow_count,
-                      unsigned long long* scratch_k, int* scratch_v, long long max_n, int big_blocks,
-                      cudaStream_t st) {
-    if (n_tiles == 0) return;
-    k_tile_sort<2048><<<n_tiles, 256, 0, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
-                                               overflow_count); ++g_launches;
-    if (max_n <= 2048) return;  // no overflow tile: skip the persistent big-list kernel
-    static bool attr = false;
-    const int smem = kBigCap * (sizeof(unsigned long long) + sizeof(int));
-    if (!attr) {
-        cudaFuncSetAttribute(k_tile_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    k_tile_sort_big<<<big_blocks, 1024, smem, st>>>(offsets, entries, keys, tile_view, Gp, overflow,
-                                                    overflow_count, scratch_k, scratch_v, max_n); ++g_launches;
 }
 
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta,

@@ -233,7 +233,7 @@ struct Batch {
     std::vector<int> htile_view;
     std::vector<int> htile_offsets;  // CSR offsets of the tile lists (host copy)
     DevBuf<DevCam> cams;
-    DevBuf<int> tile_view, tile_count, tile_offsets, cursor, entries, overflow, overflow_count, err;
+    DevBuf<int> tile_view, tile_count, tile_offsets, cursor, entries, err;
     DevBuf<long long> total;
     DevBuf<float4> rec;
     DevBuf<unsigned long long> keys;
@@ -244,8 +244,9 @@ struct Batch {
     bool rendered = false, has_gt = false;
     std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
     long long max_list = 0;        // longest tile list of the batch
-    DevBuf<unsigned long long> scratch_k;
-    DevBuf<int> scratch_v;
+    // radix tile-list construction scratch (sort.cu)
+    DevBuf<unsigned long long> rk64a, rk64b, and_or;
+    DevBuf<unsigned> rv32a, rv32b, rk32a, rk32b, rcount, rt32a, rt32b, rt32va, rt32vb, rhist, rpart;
 
     explicit Batch(Context* c) : ctx(c) {}
 
@@ -294,18 +295,26 @@ struct Batch {
         cursor.ensure(n_tiles + 1);
         total.ensure(2);
         err.ensure(1 + std::max(V, 1));
-        overflow.ensure(n_tiles + 1);
-        overflow_count.ensure(1);
         SLM_CUDA_CHECK(cudaMemsetAsync(tile_count.p, 0, sizeof(int) * (n_tiles + 1), st));
         SLM_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int) * (1 + V), st));
-        SLM_CUDA_CHECK(cudaMemsetAsync(overflow_count.p, 0, sizeof(int), st));
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p, tile_count.p, err.p, st);
         launch_scan_tiles(tile_count.p, n_tiles, tile_offsets.p, cursor.p, total.p, st);
+        // depth-sort keys in index order + the AND/OR of the valid keys (which
+        // key bytes need a radix pass)
+        const long long nvg = static_cast<long long>(V) * Gp;
+        rk64a.ensure(std::max<long long>(nvg, 1));
+        rk64b.ensure(std::max<long long>(nvg, 1));
+        rv32a.ensure(std::max<long long>(nvg, 1));
+        rv32b.ensure(std::max<long long>(nvg, 1));
+        and_or.ensure(2);
+        launch_depth_init(keys.p, rect.p, G, Gp, V, rk64a.p, rv32a.p, and_or.p, st);
         ctx->check_launch();
         ctx->mark("prep:project+count+scan");
         long long hdr[2];
+        unsigned long long hao[2] = {0ull, 0ull};
         std::vector<int> herr(1 + V);
         SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(hao, and_or.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(herr.data(), err.p, sizeof(int) * (1 + V), cudaMemcpyDeviceToHost, st));
         htile_offsets.resize(n_tiles + 1);
         SLM_CUDA_CHECK(cudaMemcpyAsync(htile_offsets.data(), tile_offsets.p, sizeof(int) * (n_tiles + 1),
@@ -316,19 +325,23 @@ struct Batch {
         n_entries = hdr[0];
         if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
         entries.ensure(std::max<long long>(n_entries, 1));
-        ctx->mark("prep:sync");
-        launch_bin_scatter(G, Gp, V, cams.p, rect.p, cursor.p, entries.p, st);
-        ctx->mark("prep:scatter");
         max_list = hdr[1];
-        // lists longer than the 16384-entry smem sort need chunk+merge scratch
-        const int big_blocks = 148;
-        if (max_list > 16384) {
-            scratch_k.ensure(static_cast<size_t>(2) * big_blocks * max_list);
-            scratch_v.ensure(static_cast<size_t>(2) * big_blocks * max_list);
-        }
-        launch_tile_sort(tile_offsets.p, entries.p, keys.p, tile_view.p, n_tiles, Gp, overflow.p,
-                         overflow_count.p, max_list > 16384 ? scratch_k.p : nullptr,
-                         max_list > 16384 ? scratch_v.p : nullptr, max_list, big_blocks, st);
+        ctx->mark("prep:sync");
+        // tile lists by stable radix passes (sort.cu): depth ranks, emit, sort by tile
+        const long long ne = std::max<long long>(n_entries, 1);
+        rk32a.ensure(std::max<long long>(nvg, 1));
+        rk32b.ensure(std::max<long long>(nvg, 1));
+        rcount.ensure(std::max<long long>(nvg, 1));
+        rt32a.ensure(ne);
+        rt32b.ensure(ne);
+        rt32va.ensure(ne);
+        rt32vb.ensure(ne);
+        const long long hmax = radix_hist_size(std::max<long long>(nvg, ne));
+        rhist.ensure(hmax);
+        rpart.ensure(scan_scratch(std::max<long long>(hmax, nvg)));
+        TileSortBuffers tb{rk64a.p, rk64b.p, rv32a.p, rv32b.p, rk32a.p, rk32b.p, rcount.p,
+                           rt32a.p, rt32b.p, rt32va.p, rt32vb.p, rhist.p, rpart.p};
+        build_tile_lists(keys.p, rect.p, cams.p, G, Gp, V, n_tiles, n_entries, hao[0], hao[1], tb, entries.p, st);
         ctx->check_launch();
         ctx->mark("prep:sort");
         rendered = false;

@@ -69,12 +69,13 @@ struct DevBuf {
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
                     unsigned long long* keys, short4* rect, int* tile_count, int* err, cudaStream_t st);
 void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total, cudaStream_t st);
-void launch_bin_scatter(int G, int Gp, int V, const DevCam* cams, const short4* rect, int* cursor,
-                        int* entries, cudaStream_t st);
-void launch_tile_sort(const int* offsets, int* entries, const unsigned long long* keys,
-                      const int* tile_view, int n_tiles, int Gp, int* overflow, int* overflow_count,
-                      unsigned long long* scratch_k, int* scratch_v, long long max_n, int big_blocks,
-                      cudaStream_t st);
+void launch_depth_init(const unsigned long long* keys, const short4* rect, int G, int Gp, int V,
+                       unsigned long long* kout, unsigned* vout, unsigned long long* and_or, cudaStream_t st);
+void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,
+                      int n_tiles, long long n_entries, unsigned long long and_k, unsigned long long or_k,
+                      const TileSortBuffers& b, int* entries, cudaStream_t st);
+long long radix_hist_size(long long n);
+long long scan_scratch(long long n);
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta, float* beta32,
                          cudaStream_t st);
 void launch_apply_update_f64(double* beta, const double* delta_aos, int G, int Gp, double eta,

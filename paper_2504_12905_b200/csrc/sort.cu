@@ -1,0 +1,333 @@
+// sort.cu — tile-list construction by stable LSD radix sorting.
+//
+// The reference builds each tile's list by appending Gaussians in index order
+// and std::sort-ing it by (depth, index) (rasterizer.cpp:21-50).  Here the
+// same order comes out of three device-wide stable passes, with no per-tile
+// sort at all:
+//   1. depth ranks: every (view, Gaussian) is sorted by its orderable 64-bit
+//      depth key (only the key bytes that vary among the valid Gaussians are
+//      sorted), then by view.  Input in index order + stable passes = ties in
+//      depth broken by index, exactly the reference comparator;
+//   2. emit: in that order, each Gaussian writes its (tile, index) pairs (its
+//      tile rect in raster order) at an exclusive-scan offset;
+//   3. a stable sort of the pairs by tile id leaves every tile's entries in
+//      (depth, index) order at the tile's CSR offset.
+// One radix pass = digit histogram per 4096-element block (warp-aggregated
+// smem counters), an exclusive scan of the digit-major histogram, and a
+// stable scatter that ranks each 256-element chunk with __match_any_sync and
+// per-warp digit counts.
+#include <cstdint>
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace slm { extern std::atomic<long long> g_launches; }
+
+namespace slm {
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;
+
+template <typename K>
+__device__ __forceinline__ unsigned digit_of(K k, int shift) {
+    return static_cast<unsigned>(k >> shift) & 0xFFu;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restrict__ keys, long long n, int shift,
+                                                              unsigned* __restrict__ hist, int nblocks) {
+    __shared__ unsigned h[256];
+    const int t = threadIdx.x, lane = t & 31;
+    h[t] = 0u;
+    __syncthreads();
+    const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
+#pragma unroll 4
+    for (int i = 0; i < kRadixItems; ++i) {
+        const long long idx = base + i * kRadixThreads + t;
+        const bool valid = idx < n;
+        const unsigned d = valid ? digit_of(keys[idx], shift) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&h[d], __popc(peers));
+    }
+    __syncthreads();
+    hist[static_cast<size_t>(t) * nblocks + blockIdx.x] = h[t];
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __restrict__ kin,
+                                                                 const unsigned* __restrict__ vin,
+                                                                 K* __restrict__ kout, unsigned* __restrict__ vout,
+                                                                 long long n, int shift,
+                                                                 const unsigned* __restrict__ offs, int nblocks) {
+    constexpr int NW = kRadixThreads / 32;
+    __shared__ unsigned s_base[256];
+    __shared__ unsigned s_wc[NW][256];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    s_base[t] = offs[static_cast<size_t>(t) * nblocks + blockIdx.x];
+    const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int i = 0; i < kRadixItems; ++i) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s_wc[w][t] = 0u;
+        __syncthreads();
+        const long long idx = base + i * kRadixThreads + t;
+        const bool valid = idx < n;
+        K key = 0;
+        unsigned val = 0u;
+        if (valid) {
+            key = kin[idx];
+            val = vin[idx];
+        }
+        const unsigned d = valid ? digit_of(key, shift) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned wrank = __popc(peers & lt);
+        if (valid && wrank == 0u) s_wc[warp][d] = __popc(peers);
+        __syncthreads();
+        unsigned run = 0u;  // thread t owns digit t: exclusive prefix over the warps
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const unsigned c = s_wc[w][t];
+            s_wc[w][t] = run;
+            run += c;
+        }
+        __syncthreads();
+        if (valid) {
+            const unsigned pos = s_base[d] + s_wc[warp][d] + wrank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+        s_base[t] += run;
+    }
+}
+
+// ---- exclusive scan of u32 (n < 2^31; totals fit u32)
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* s_warp, unsigned& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned s = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        s_warp[lane] = s;  // inclusive per-warp totals
+    }
+    __syncthreads();
+    total = s_warp[(blockDim.x >> 5) - 1];
+    const unsigned before = warp ? s_warp[warp - 1] : 0u;
+    __syncthreads();
+    return before + x - v;
+}
+
+// Pass 1: per-tile sums.
+__global__ void __launch_bounds__(kScanThreads) k_scan_partials(const unsigned* __restrict__ in, long long n,
+                                                                unsigned* __restrict__ part) {
+    __shared__ unsigned s_warp[32];
+    const long long base = static_cast<long long>(blockIdx.x) * kScanTile + static_cast<long long>(threadIdx.x) * kScanItems;
+    unsigned s = 0u;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+        if (base + i < n) s += in[base + i];
+    unsigned total;
+    block_exclusive_scan(s, s_warp, total);
+    if (threadIdx.x == 0) part[blockIdx.x] = total;
+}
+
+// Pass 2: exclusive scan of the partials in one CTA (any count).
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(unsigned* __restrict__ part, int m, unsigned* __restrict__ total_out) {
+    __shared__ unsigned s_warp[32];
+    unsigned carry = 0u;
+    for (int b = 0; b < m; b += kScanThreads) {
+        const int i = b + threadIdx.x;
+        const unsigned v = i < m ? part[i] : 0u;
+        unsigned total;
+        const unsigned ex = block_exclusive_scan(v, s_warp, total);
+        if (i < m) part[i] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0 && total_out) *total_out = carry;
+}
+
+// Pass 3: per-tile exclusive scan plus the tile's offset.
+// (in-place safe: every element is read and written by the same thread)
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const unsigned* in, long long n,
+                                                             const unsigned* __restrict__ part, unsigned* out) {
+    __shared__ unsigned s_warp[32];
+    const long long base = static_cast<long long>(blockIdx.x) * kScanTile + static_cast<long long>(threadIdx.x) * kScanItems;
+    unsigned v[kScanItems];
+    unsigned s = 0u;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = base + i < n ? in[base + i] : 0u;
+        s += v[i];
+    }
+    unsigned total;
+    unsigned run = part[blockIdx.x] + block_exclusive_scan(s, s_warp, total);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i)
+        if (base + i < n) {
+            out[base + i] = run;
+            run += v[i];
+        }
+}
+
+void launch_exclusive_scan(const unsigned* in, unsigned* out, long long n, unsigned* part, unsigned* total,
+                           cudaStream_t st) {
+    if (n <= 0) return;
+    const int nb = static_cast<int>((n + kScanTile - 1) / kScanTile);
+    k_scan_partials<<<nb, kScanThreads, 0, st>>>(in, n, part); ++g_launches;
+    k_scan_top<<<1, kScanThreads, 0, st>>>(part, nb, total); ++g_launches;
+    k_scan_apply<<<nb, kScanThreads, 0, st>>>(in, n, part, out); ++g_launches;
+}
+
+long long scan_scratch(long long n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+// One stable LSD pass over 8 key bits starting at `shift`.
+template <typename K>
+void radix_pass(const K* kin, const unsigned* vin, K* kout, unsigned* vout, long long n, int shift,
+                unsigned* hist, unsigned* part, cudaStream_t st) {
+    const int nb = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
+    k_radix_hist<K><<<nb, kRadixThreads, 0, st>>>(kin, n, shift, hist, nb); ++g_launches;
+    launch_exclusive_scan(hist, hist, 256ll * nb, part, nullptr, st);
+    k_radix_scatter<K><<<nb, kRadixThreads, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb); ++g_launches;
+}
+
+long long radix_hist_size(long long n) { return 256ll * ((n + kRadixTile - 1) / kRadixTile); }
+
+// ---- tile-list construction kernels
+// Sort keys for the depth passes: index order, culled / padding Gaussians get
+// key 0 and produce no entries (their position is irrelevant).
+__global__ void k_depth_init(const unsigned long long* __restrict__ keys, const short4* __restrict__ rect, int G,
+                             int Gp, long long n, unsigned long long* __restrict__ kout, unsigned* __restrict__ vout,
+                             unsigned long long* __restrict__ and_or) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool valid = false;
+    unsigned long long k = 0ull;
+    if (i < n) {
+        const int g = static_cast<int>(i % Gp);
+        valid = g < G && rect[i].x <= rect[i].y;
+        k = valid ? keys[i] : 0ull;
+        kout[i] = k;
+        vout[i] = static_cast<unsigned>(i);
+    }
+    // AND / OR of the valid keys: bytes where they agree need no pass
+    unsigned long long a = valid ? k : ~0ull, o = valid ? k : 0ull;
+#pragma unroll
+    for (int s = 16; s; s >>= 1) {
+        a &= __shfl_xor_sync(0xffffffffu, a, s);
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAnd(&and_or[0], a);
+        atomicOr(&and_or[1], o);
+    }
+}
+
+void launch_depth_init(const unsigned long long* keys, const short4* rect, int G, int Gp, int V,
+                       unsigned long long* kout, unsigned* vout, unsigned long long* and_or, cudaStream_t st) {
+    const long long n = static_cast<long long>(V) * Gp;
+    if (n == 0) return;
+    const unsigned long long init[2] = {~0ull, 0ull};
+    cudaMemcpyAsync(and_or, init, sizeof init, cudaMemcpyHostToDevice, st);
+    k_depth_init<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, rect, G, Gp, n, kout, vout, and_or); ++g_launches;
+}
+
+__global__ void k_view_key(const unsigned* __restrict__ vals, long long n, int Gp, unsigned* __restrict__ vkey) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) vkey[i] = vals[i] / static_cast<unsigned>(Gp);
+}
+
+__global__ void k_emit_count(const unsigned* __restrict__ order, long long n, int G, int Gp,
+                             const short4* __restrict__ rect, unsigned* __restrict__ count) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned vg = order[i];
+    const int g = static_cast<int>(vg % static_cast<unsigned>(Gp));
+    unsigned c = 0u;
+    if (g < G) {
+        const short4 r = rect[vg];
+        if (r.x <= r.y) c = static_cast<unsigned>(r.y - r.x + 1) * static_cast<unsigned>(r.w - r.z + 1);
+    }
+    count[i] = c;
+}
+
+__global__ void k_emit(const unsigned* __restrict__ order, long long n, int G, int Gp, const DevCam* __restrict__ cams,
+                       const short4* __restrict__ rect, const unsigned* __restrict__ start,
+                       unsigned* __restrict__ tkey, unsigned* __restrict__ tval) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned vg = order[i];
+    const int v = static_cast<int>(vg / static_cast<unsigned>(Gp)), g = static_cast<int>(vg % static_cast<unsigned>(Gp));
+    if (g >= G) return;
+    const short4 r = rect[vg];
+    if (r.x > r.y) return;
+    const int base = cams[v].tile_base, tx_n = cams[v].tiles_x;
+    unsigned o = start[i];
+    for (int ty = r.z; ty <= r.w; ++ty)
+        for (int tx = r.x; tx <= r.y; ++tx, ++o) {
+            tkey[o] = static_cast<unsigned>(base + ty * tx_n + tx);
+            tval[o] = static_cast<unsigned>(g);
+        }
+}
+
+// Host driver (runtime.cpp keeps the buffers).  Returns nothing; `entries`
+// receives the per-tile sorted lists at the CSR offsets of k_scan_tiles.
+void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,
+                      int n_tiles, long long n_entries, unsigned long long and_k, unsigned long long or_k,
+                      const TileSortBuffers& b, int* entries, cudaStream_t st) {
+    const long long n = static_cast<long long>(V) * Gp;
+    if (n == 0 || n_entries == 0) return;
+    // 1. depth passes over the varying key bytes, then the view
+    const unsigned long long vary = and_k ^ or_k;
+    unsigned long long *ka = b.k64a, *kb = b.k64b;
+    unsigned *va = b.v32a, *vb = b.v32b;
+    for (int byte = 0; byte < 8; ++byte) {
+        if (((vary >> (8 * byte)) & 0xFFull) == 0ull) continue;
+        radix_pass<unsigned long long>(ka, va, kb, vb, n, 8 * byte, b.hist, b.part, st);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (V > 1) {
+        k_view_key<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, Gp, b.k32a); ++g_launches;
+        unsigned *k32a = b.k32a, *k32b = b.k32b;
+        for (int s = 0; (1ll << s) < V; s += 8) {
+            radix_pass<unsigned>(k32a, va, k32b, vb, n, s, b.hist, b.part, st);
+            std::swap(k32a, k32b);
+            std::swap(va, vb);
+        }
+    }
+    // 2. emit (tile, index) pairs in (view, depth, index) order
+    k_emit_count<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, rect, b.count); ++g_launches;
+    launch_exclusive_scan(b.count, b.count, n, b.part, nullptr, st);
+    unsigned *tka = b.t32a, *tkb = b.t32b, *tva = b.t32va, *tvb = b.t32vb;
+    k_emit<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, cams, rect, b.count, tka, tva); ++g_launches;
+    // 3. stable sort by tile id; the last pass writes the values into `entries`
+    int passes = 0;
+    for (int s = 0; (1ll << s) < n_tiles; s += 8) ++passes;
+    for (int p = 0; p < passes; ++p) {
+        const bool last = p == passes - 1;
+        radix_pass<unsigned>(tka, tva, tkb, last ? reinterpret_cast<unsigned*>(entries) : tvb, n_entries, 8 * p,
+                             b.hist, b.part, st);
+        std::swap(tka, tkb);
+        std::swap(tva, tvb);
+    }
+    if (passes == 0)  // a single tile: already in order
+        cudaMemcpyAsync(entries, tva, sizeof(unsigned) * n_entries, cudaMemcpyDeviceToDevice, st);
+}
+
+}  // namespace slm
