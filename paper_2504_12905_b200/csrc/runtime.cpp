@@ -511,10 +511,24 @@ struct Jacobian {
         samples.group_host(plan, lo, hi, cams, weights);
     }
 
+    // Adopt the host half computed by another (host-only) Jacobian.
+    void take_host(Jacobian& o) {
+        std::swap(rdim, o.rdim);
+        std::swap(plan_base, o.plan_base);
+        weights.swap(o.weights);
+        samples.hgroups.swap(o.samples.hgroups);
+        samples.order.swap(o.samples.order);
+        samples.hpix.swap(o.samples.hpix);
+        samples.horig.swap(o.samples.horig);
+        samples.hw.swap(o.samples.hw);
+        std::swap(samples.total, o.samples.total);
+    }
+
     // Device half: uploads, zeroed accumulators, blend masks (needs the batch
     // prepared and rendered).
     void init_device() {
         samples.upload(ctx, batch->hcams, batch->htile_offsets);
+        ctx->mark("plan:upload");
         const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
         tan.ensure(3 * VG);
         inter.ensure(VG * kRec);
@@ -530,6 +544,7 @@ struct Jacobian {
         a.grows_out = samples.grows.p;
         launch_masks(a, ctx->stream);
         ctx->check_launch();
+        ctx->mark("plan:masks");
         // alpha-stream layout: rows per group -> offsets (host scan), then the stream
         const size_t ng = samples.hgroups.size();
         samples.hrows.resize(ng);
@@ -1028,12 +1043,38 @@ static void copy_gt(Train& t, Batch& b, const std::vector<int>& cam_ids) {
     }
 }
 
+// The next lm_step's view batch + sample plan + sample grouping, computed on a
+// host thread while this step's PCG runs.  For the uniform distribution they
+// depend only on the RNG state, the view clusters and the cameras, so the
+// result is used iff the caller's RNG (and clusters, cameras, config) at the
+// next call equal the snapshot taken here; otherwise it is discarded and the
+// step draws as usual.  The RNG stream is the reference's either way.
+struct Speculation {
+    std::thread th;
+    std::exception_ptr err;
+    std::mt19937_64 rng_before, rng_after;
+    std::vector<int> assign;
+    int k = 0, spt = 0, dist = 0, lane = 0;
+    std::vector<slm_camera> cams;
+    std::vector<int> batch;
+    std::unique_ptr<PlanH> plan;
+    std::unique_ptr<Jacobian> hj;  // host half only
+    ~Speculation() {
+        if (th.joinable()) th.join();
+    }
+};
+
 struct StepBuffers {  // per-context persistent lm_step workspace (no per-step cudaMalloc)
     Batch batch;
     Jacobian jac;
     DevBuf<float> b, x, maxabs;
+    std::unique_ptr<Speculation> spec;
     explicit StepBuffers(Context* c) : batch(c), jac(c, nullptr, &batch) {}
 };
+
+static bool same_cams(const std::vector<slm_camera>& a, const std::vector<slm_camera>& b) {
+    return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), sizeof(slm_camera) * a.size()) == 0);
+}
 
 void destroy_step(StepBuffers* s) { delete s; }
 
@@ -1051,8 +1092,18 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         throw std::invalid_argument("lm_step: only the mse loss is on the B200 path (mse+ssim is out of scope)");
     ctx->mark("start");
     rep.iteration = iteration;
+    StepBuffers& sb = step_buffers(ctx);
+    // the previous step's speculative draw of this step's batch + plan (see Speculation)
+    std::unique_ptr<Speculation> spec = std::move(sb.spec);
+    bool use_spec = false;
+    if (spec) {
+        if (spec->th.joinable()) spec->th.join();
+        use_spec = !spec->err && cfg.dist == SLM_DIST_UNIFORM && spec->rng_before == rng && spec->k == t.k &&
+                   spec->assign == t.assign && spec->spt == cfg.samples_per_tile && spec->dist == cfg.dist &&
+                   spec->lane == cfg.sample_lane_width && same_cams(spec->cams, t.cams);
+    }
     // 1. view batch (lm.cpp:63)
-    const std::vector<int> batch = view_batch(t.assign, t.k, rng);
+    const std::vector<int> batch = use_spec ? spec->batch : view_batch(t.assign, t.k, rng);
     const int VB = static_cast<int>(batch.size());
     int lo = 0, hi = 0;
     slm_view_slice(VB, ctx->rank, ctx->world, &lo, &hi);
@@ -1063,7 +1114,6 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         my_cams.push_back(t.cams[batch[i]]);
         my_ids.push_back(batch[i]);
     }
-    StepBuffers& sb = step_buffers(ctx);
     Batch& B = sb.batch;
     Jacobian& J = sb.jac;
     J.scene = &s;
@@ -1085,7 +1135,14 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     };
     std::thread sampler;
     const bool overlap = cfg.dist == SLM_DIST_UNIFORM;
-    if (overlap) sampler = std::thread(make_plan, nullptr, nullptr, nullptr);
+    if (use_spec) {
+        plan = std::move(spec->plan);
+        J.take_host(*spec->hj);
+        rng = spec->rng_after;
+    } else if (overlap) {
+        sampler = std::thread(make_plan, nullptr, nullptr, nullptr);
+    }
+    spec.reset();
     // 2./3. forward render + residual fields of this rank's views (lm.cpp:75-78)
     try {
         B.prepare(s, my_cams);
@@ -1097,7 +1154,8 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     }
     ctx->mark("prepare+render");
     if (overlap) {
-        sampler.join();
+        if (sampler.joinable()) sampler.join();
+        ctx->mark("plan:host");
     } else {  // weighted distributions need the render on the host (aux data)
         if (ctx->world > 1)
             throw std::invalid_argument("weighted residual distributions are single-rank only on the B200 path");
@@ -1133,6 +1191,38 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     }
     J.init_device();
     ctx->mark("plan");
+    if (cfg.dist == SLM_DIST_UNIFORM) {  // speculate the next step's batch + plan while this one solves
+        auto sp = std::make_unique<Speculation>();
+        sp->rng_before = rng;
+        sp->assign = t.assign;
+        sp->k = t.k;
+        sp->spt = cfg.samples_per_tile;
+        sp->dist = cfg.dist;
+        sp->lane = cfg.sample_lane_width;
+        sp->cams = t.cams;
+        sp->hj = std::make_unique<Jacobian>(ctx, nullptr, nullptr);
+        Speculation* q = sp.get();
+        const int rank = ctx->rank, world = ctx->world;
+        q->th = std::thread([q, rank, world] {
+            try {
+                std::mt19937_64 r = q->rng_before;
+                q->batch = view_batch(q->assign, q->k, r);
+                const int nb = static_cast<int>(q->batch.size());
+                int l = 0, h = 0;
+                slm_view_slice(nb, rank, world, &l, &h);
+                std::vector<slm_camera> all, mine;
+                for (int i = 0; i < nb; ++i) all.push_back(q->cams[q->batch[i]]);
+                for (int i = l; i < h; ++i) mine.push_back(q->cams[q->batch[i]]);
+                q->plan = build_plan(all.data(), nb, q->spt, q->dist, q->lane, r, nullptr, nullptr, nullptr);
+                const long long total = q->plan->view_offset.back();
+                q->hj->init_host(q->plan->view(), l, h, total > 0 ? 1.0 / static_cast<double>(total) : 0.0, mine);
+                q->rng_after = r;
+            } catch (...) {
+                q->err = std::current_exception();
+            }
+        });
+        sb.spec = std::move(sp);
+    }
     const size_t P = s.P();
     sb.b.ensure(2 * P);  // [b | diag] contiguous for one fused allreduce
     sb.x.ensure(P);
