@@ -377,13 +377,16 @@ def run_b200(args):
         L.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)  # same stream position as train_run
         L.set_timing(True)
         with torch.cuda.stream(stream):
+            # two untimed steps: the first fills the pinned host buffers and
+            # starts the speculative plan of the next step (lm_step's steady state)
             rep = lm_scene.lm_step(td, cfg, 0, rng)
+            lm_scene.lm_step(td, cfg, 1, rng)
             torch.cuda.synchronize()
             if dist:
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            reps = [lm_scene.lm_step(td, cfg, 1 + i, rng) for i in range(args.lm_steps)]
+            reps = [lm_scene.lm_step(td, cfg, 2 + i, rng) for i in range(args.lm_steps)]
             e1.record(stream)
         torch.cuda.synchronize()
         lm_ms = e0.elapsed_time(e1) / args.lm_steps

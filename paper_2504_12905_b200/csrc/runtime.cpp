@@ -377,12 +377,34 @@ struct Batch {
     }
 };
 
+// Page-locked host allocator: the per-step sample arrays are uploaded with
+// cudaMemcpyAsync at DMA speed (grow-only vectors keep their capacity).
+template <class T>
+struct PinnedAlloc {
+    using value_type = T;
+    PinnedAlloc() = default;
+    template <class U>
+    PinnedAlloc(const PinnedAlloc<U>&) {}
+    T* allocate(size_t n) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable) != cudaSuccess) throw std::bad_alloc();
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t) { cudaFreeHost(p); }
+    template <class U>
+    bool operator==(const PinnedAlloc<U>&) const { return true; }
+    template <class U>
+    bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
+
 // =========================================================================== Samples
 // A plan laid out for the warp-per-group raster: per view, samples grouped
 // by tile in chunks of <= 32 (the reference emits them tile-major already,
 // sample_plan.cpp:96-168, so this is a no-op permutation for its plans).
 struct Samples {
-    std::vector<Group> hgroups;
+    pinned_vector<Group> hgroups;
     DevBuf<Group> groups;
     DevBuf<int> spix, sorig;
     DevBuf<float> sw;
@@ -394,8 +416,8 @@ struct Samples {
     std::vector<int> hrows;
     std::vector<long long> hrow_off;
     std::vector<int> order;  // group order -> plan sample index
-    std::vector<int> hpix, horig;
-    std::vector<float> hw;
+    pinned_vector<int> hpix, horig;
+    pinned_vector<float> hw;
     long long total = 0, mask_words = 0;
 
     // Host half (no CUDA calls; runs on the sampler thread in lm_step):
@@ -445,8 +467,9 @@ struct Samples {
     }
 
     // Device half: mask offsets (need the tile-list lengths) and uploads.
+    pinned_vector<long long> hoff;
     void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets) {
-        std::vector<long long> hoff(hgroups.size());
+        hoff.resize(hgroups.size());
         mask_words = 0;
         for (size_t g = 0; g < hgroups.size(); ++g) {
             const int t = cams[hgroups[g].view].tile_base + hgroups[g].tile;
@@ -470,7 +493,7 @@ struct Samples {
         SLM_CUDA_CHECK(cudaMemcpyAsync(spix.p, hpix.data(), sizeof(int) * hpix.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sorig.p, horig.data(), sizeof(int) * horig.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, st));
-        ctx->sync();  // hoff goes out of scope
+        // (host arrays are pinned members, rewritten only after later syncs)
     }
 
     void upload_weights(Context* ctx, const std::vector<double>& weights3) {
@@ -1058,7 +1081,7 @@ struct Speculation {
     std::vector<slm_camera> cams;
     std::vector<int> batch;
     std::unique_ptr<PlanH> plan;
-    std::unique_ptr<Jacobian> hj;  // host half only
+    Jacobian* hj = nullptr;  // host half only (StepBuffers::spare)
     ~Speculation() {
         if (th.joinable()) th.join();
     }
@@ -1068,8 +1091,10 @@ struct StepBuffers {  // per-context persistent lm_step workspace (no per-step c
     Batch batch;
     Jacobian jac;
     DevBuf<float> b, x, maxabs;
+    Jacobian spare;  // host half of the speculated next step (vectors keep their pinned capacity)
     std::unique_ptr<Speculation> spec;
-    explicit StepBuffers(Context* c) : batch(c), jac(c, nullptr, &batch) {}
+    explicit StepBuffers(Context* c) : batch(c), jac(c, nullptr, &batch), spare(c, nullptr, nullptr) {}
+    ~StepBuffers() { spec.reset(); }
 };
 
 static bool same_cams(const std::vector<slm_camera>& a, const std::vector<slm_camera>& b) {
@@ -1200,7 +1225,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         sp->dist = cfg.dist;
         sp->lane = cfg.sample_lane_width;
         sp->cams = t.cams;
-        sp->hj = std::make_unique<Jacobian>(ctx, nullptr, nullptr);
+        sp->hj = &sb.spare;
         Speculation* q = sp.get();
         const int rank = ctx->rank, world = ctx->world;
         q->th = std::thread([q, rank, world] {
