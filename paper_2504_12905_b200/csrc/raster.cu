@@ -46,13 +46,29 @@ namespace slm { extern std::atomic<long long> g_launches; }
 namespace slm {
 
 // ------------------------------------------------------------------ K6
-// One CTA of 64 threads per 16x16 tile; thread t owns the 4 pixels of column
-// t & 15 at rows (t >> 4) + 4i, so every broadcast read of a staged splat record
-// serves 4 pixels (the 1-pixel-per-thread form is bound by the shared-memory
-// pipe on those broadcasts).  Per pixel the arithmetic is blend_pixel's.
+// One CTA of 64 threads per 16x16 tile; warp w owns the 16x8 half-tile of rows
+// 8w..8w+7, thread (lane l) the 4 pixels of column l & 15 at rows
+// 8w + (l >> 4) + 2i, so every broadcast read of a staged splat record serves
+// 4 pixels.  Per staged entry, the bounding box of its alpha >= 1/255 ellipse
+// (conservatively widened) lets a warp skip the entry when the box misses its
+// half-tile: every pixel there would fail the reference's alpha gate anyway.
+// Per pixel the arithmetic is blend_pixel's (eval_alpha).
 constexpr int kRenderThreads = 64;
 constexpr int kRenderPix = 4;      // pixels per thread
 constexpr int kRenderStage = 128;  // records staged per round
+
+// Bounding box of {alpha >= 1/255} for a record (A, B, C: log2-domain conic,
+// o: opacity): q = A dx^2 + B dx dy + C dy^2 >= L = log2(1/(255 o)).
+__device__ __forceinline__ float4 alpha_box(float4 r0, float4 r1) {
+    const float A = r0.z, B = r0.w, C = r1.x, o = r1.y;
+    const float det = A * C - 0.25f * B * B;  // > 0 for a valid (negative-definite) conic
+    const float L = -__log2f(255.0f * o);     // <= 0 when o >= 1/255
+    if (!(det > 0.0f) || !(L < 0.0f)) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never blends
+    // half-widths sqrt(L * C / det), sqrt(L * A / det) (all three signs negative), widened
+    const float hx = sqrtf(fmaxf(L * C / det, 0.0f)) * 1.001f + 0.05f;
+    const float hy = sqrtf(fmaxf(L * A / det, 0.0f)) * 1.001f + 0.05f;
+    return make_float4(r0.x - hx, r0.x + hx, r0.y - hy, r0.y + hy);
+}
 
 __global__ void __launch_bounds__(kRenderThreads) k_render(
     const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
@@ -61,15 +77,20 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
     float* __restrict__ image, float* __restrict__ trans, int* __restrict__ contrib,
     int* __restrict__ last_out, double* __restrict__ sse_tile) {
     __shared__ float4 s_rec[kRenderStage][3];
+    __shared__ float4 s_box[kRenderStage];
     __shared__ double s_red[kRenderThreads / 32];
     const int tile = blockIdx.x;
     const int v = tile_view[tile];
     const DevCam& cam = cams[v];
     const int lt = tile - cam.tile_base;
     const int tx = lt % cam.tiles_x, ty = lt / cam.tiles_x;
-    const int x = tx * kTile + (threadIdx.x & 15);
-    const int y0 = ty * kTile + (threadIdx.x >> 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = tx * kTile + (lane & 15);
+    const int y0 = ty * kTile + 8 * warp + (lane >> 4);
     const float pxc = (float)x + 0.5f;
+    // this warp's half-tile in pixel-centre coordinates
+    const float wx0 = (float)(tx * kTile) + 0.5f, wx1 = wx0 + 15.0f;
+    const float wy0 = (float)(ty * kTile + 8 * warp) + 0.5f, wy1 = wy0 + 7.0f;
     const int b = tile_offsets[tile], n = tile_offsets[tile + 1] - b;
     const size_t vbase = static_cast<size_t>(v) * Gp;
 
@@ -78,7 +99,7 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
     unsigned live = 0u;  // bit i: pixel i still blending
 #pragma unroll
     for (int i = 0; i < kRenderPix; ++i) {
-        const int y = y0 + 4 * i;
+        const int y = y0 + 2 * i;
         T[i] = 1.0f;
         C0[i] = C1[i] = C2[i] = 0.0f;
         cnt[i] = 0;
@@ -90,13 +111,17 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
         if (__syncthreads_count(live != 0u) == 0) break;
         for (int j = threadIdx.x; j < kRenderStage && start + j < n; j += kRenderThreads) {
             const float4* r = rec + 3 * (vbase + entries[b + start + j]);
-            s_rec[j][0] = r[0];
-            s_rec[j][1] = r[1];
+            const float4 r0 = r[0], r1 = r[1];
+            s_rec[j][0] = r0;
+            s_rec[j][1] = r1;
             s_rec[j][2] = r[2];
+            s_box[j] = alpha_box(r0, r1);
         }
         __syncthreads();
         const int m = min(kRenderStage, n - start);
         for (int k = 0; k < m && live; ++k) {
+            const float4 bx = s_box[k];
+            if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
             const float4 r0 = s_rec[k][0], r1 = s_rec[k][1];
             const float c2 = s_rec[k][2].x;
 #pragma unroll
@@ -122,7 +147,7 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
     double sq = 0.0;
 #pragma unroll
     for (int i = 0; i < kRenderPix; ++i) {
-        const int y = y0 + 4 * i;
+        const int y = y0 + 2 * i;
         if (x < cam.width && y < cam.height) {
             const size_t pix = cam.pix_base + static_cast<size_t>(y) * cam.width + x;
             image[3 * pix] = C0[i];
