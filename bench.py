@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--lm-steps", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-psnr", action="store_true", help="skip the configs[0] time-to-PSNR run")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
     return ap.parse_args()
 
@@ -234,6 +235,66 @@ def cpu_sample(args, views: int, steps: int, warmup: int):
     return value, times, meta
 
 
+PSNR_TARGET = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "psnr_cfg0.json")
+
+
+def cfg0_scene(L, c):
+    """configs[0] as io::train_run builds the toy scene (run.cpp:26-36, scene_gen.cpp:38-86):
+    ground truth from the reference's generator (bit-exact), ring cameras, images rendered here."""
+    from paper_2504_12905_b200 import splatlm
+
+    gt = splatlm.Scene(L, L.toy_gaussians(c["toy_gaussians"], c["scene_seed"]))
+    train = [L.ring_camera(2.0 * math.pi * i / c["train"], 3.2, 1.1, c["size"]) for i in range(c["train"])]
+    test = [L.ring_camera(0.37 + 2.0 * math.pi * i / c["test"], 3.2, 1.6, c["size"]) for i in range(c["test"])]
+    timgs = [gt.render(cam)[0] for cam in train]
+    simgs = [gt.render(cam)[0] for cam in test]
+    return train, timgs, test, simgs
+
+
+def psnr(a, b) -> float:  # metrics::psnr (image_metrics.cpp:108-119)
+    m = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return 100.0 if m < 1e-10 else 10.0 * math.log10(1.0 / m)
+
+
+def time_to_psnr(L, stream):
+    """configs[0]: wall time of lm_step iterations until the mean test PSNR reaches the
+    reference's final PSNR - 0.05 dB (tests/golden/psnr_cfg0.json, the reference itself
+    run on the same inputs); evaluation renders are outside the timed region."""
+    import torch
+    from paper_2504_12905_b200 import splatlm
+
+    ref = json.load(open(PSNR_TARGET))
+    c = ref["config"]
+    train, timgs, test, simgs = cfg0_scene(L, c)
+    td = L.train_data(train, timgs)
+    td.set_clusters(L.kmeans_cameras(train, min(c["batch"], len(train)), c["seed"] ^ KMEANS_SALT))
+    rng = L.rng(c["seed"])
+    scene = splatlm.Scene(L, L.random_init(c["gaussians"], [-1, -1, -1], [1, 1, 1], rng))
+    cfg = LmConfig(pcg_iters_initial=c["pcg"], pcg_iters_late=c["pcg"], batch_size_initial=c["batch"],
+                   batch_size_late=c["batch"], samples_per_tile=c["spt"])
+    target = ref["psnr"][-1] - 0.05
+    elapsed, reached, curve = 0.0, None, []
+    with torch.cuda.stream(stream):
+        for it in range(len(ref["psnr"])):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            scene.lm_step(td, cfg, it, rng)
+            torch.cuda.synchronize()
+            elapsed += time.perf_counter() - t0
+            curve.append(float(np.mean([psnr(scene.render(cam)[0], im) for cam, im in zip(test, simgs)])))
+            if reached is None and curve[-1] >= target:
+                reached = elapsed
+    ref_t = float(np.cumsum(ref["wall_s"])[-1])
+    return {"config": "configs[0]: toy scene 5000 GT / 10k random_init Gaussians, 8 train + 4 test views "
+                      "256x256, full pixels (N=256), PCG 8, 10 LM iterations",
+            "target_db": round(target, 4), "time_to_psnr_s": reached, "iterations": len(curve),
+            "psnr_curve_db": [round(x, 4) for x in curve],
+            "max_abs_psnr_diff_vs_reference_db": round(max(abs(a - b) for a, b in zip(curve, ref["psnr"])), 5),
+            "reference_time_s": round(ref_t, 1), "reference_threads": ref.get("threads"),
+            "reference_note": "wall time of the reference CPU run (oracle/_ref) that produced the target, "
+                              "measured where tests/golden/make_psnr_target.py ran"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -398,6 +459,12 @@ def run_b200(args):
         lm = {"lm_iters_per_s": 1000.0 / lm_ms, "ms_per_lm_step": lm_ms, "pcg_iters": 8,
               "loss_before_first": rep.loss_before, "loss_after_last": reps[-1].loss_after}
 
+    ttp = None
+    if not args.no_psnr and os.path.exists(PSNR_TARGET):
+        ttp = time_to_psnr(L, stream)
+        log(f"time-to-PSNR: {ttp['time_to_psnr_s']} s (target {ttp['target_db']} dB, "
+            f"max |dPSNR| vs reference {ttp['max_abs_psnr_diff_vs_reference_db']} dB)")
+
     if rank != 0:
         return
     cpu = None
@@ -439,6 +506,7 @@ def run_b200(args):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "lm": lm,
+        "time_to_psnr": ttp,
         "setup_s": round(setup_s, 1),
     }
     print(json.dumps(line), flush=True)

@@ -159,6 +159,9 @@ int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cams, int n, doubl
 /* ---- io helpers the harness uses (io/dataset.cpp:138-166, io/scene_gen.cpp) */
 int slm_random_init(int count, const double* cube_min, const double* cube_max, slm_rng* rng,
                     slm_gaussians* out);
+/* io::generate_toy_scene's ground-truth Gaussians (scene_gen.cpp:38-71), seeded
+ * std::mt19937_64(seed); cameras: slm_ring_camera, images: slm_render. */
+int slm_toy_gaussians(int count, uint64_t seed, slm_gaussians* out);
 int slm_ring_camera(double angle, double radius, double height, int width, int height_px,
                     slm_camera* out);
 

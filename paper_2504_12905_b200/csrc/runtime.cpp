@@ -1947,6 +1947,38 @@ int slm_random_init(int count, const double* lo, const double* hi, slm_rng* rng,
     });
 }
 
+int slm_toy_gaussians(int count, uint64_t seed, slm_gaussians* out) {
+    return guarded([&] {  // io::generate_toy_scene's ground truth (scene_gen.cpp:38-71)
+        if (count < 1) throw std::invalid_argument("toy scene needs at least one Gaussian");
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> upos(-0.8, 0.8);
+        std::uniform_real_distribution<double> uscale(std::log(0.12), std::log(0.35));
+        std::uniform_real_distribution<double> uquat(-1.0, 1.0);
+        std::uniform_real_distribution<double> uopacity(0.4, 0.9);
+        std::uniform_real_distribution<double> ucolor(-1.2, 1.2);
+        for (int i = 0; i < count; ++i) {
+            for (int c = 0; c < 3; ++c) {
+                out->means[3 * i + c] = upos(rng);
+                out->log_scales[3 * i + c] = uscale(rng);
+                out->colors[3 * i + c] = ucolor(rng);
+            }
+            double q[4], norm = 0.0;
+            do {
+                norm = 0.0;
+                for (double& v : q) {
+                    v = uquat(rng);
+                    norm += v * v;
+                }
+            } while (norm < 1e-4);
+            const double o = uopacity(rng);
+            out->opacity_logits[i] = std::log(o / (1.0 - o));
+            // GaussianSet::renormalize_rotations (types.cpp:62-73)
+            const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            for (int c = 0; c < 4; ++c) out->rotations[4 * i + c] = q[c] / n;
+        }
+    });
+}
+
 int slm_ring_camera(double angle, double radius, double height, int width, int height_px, slm_camera* out) {
     return guarded([&] {  // io::ring_camera (scene_gen.cpp:11-36), W x H allowed
         const double pos[3] = {radius * std::cos(angle), height, radius * std::sin(angle)};

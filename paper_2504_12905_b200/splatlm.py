@@ -98,6 +98,7 @@ _SIGS = {
     "slm_jacobian_pcg": (C.c_int, [_vp, C.c_double, _f64p, _f64p, C.c_int, _f64p,
                                    C.POINTER(CPcgResult)]),
     "slm_jacobian_stats": (C.c_int, [_vp, _i64p]),
+    "slm_toy_gaussians": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(CGaussians)]),
     "slm_jacobian_mask_stats": (C.c_int, [_vp, _i64p]),
     "slm_pcg_solve": (C.c_int, [_vp, _APPLY, _vp, _f64p, _f64p, C.c_int64, C.c_int, _f64p,
                                 C.POINTER(CPcgResult)]),
@@ -189,6 +190,13 @@ class HostSampler:
         hi = np.asarray(cube_max, np.float64)
         cg = g.to_c()
         self._check(self.dll.slm_random_init(count, f64ptr(lo), f64ptr(hi), rng.h, C.byref(cg)))
+        return g
+
+    def toy_gaussians(self, count: int, seed: int = 20214) -> GaussianSet:
+        """io::generate_toy_scene's ground truth (scene_gen.cpp:38-71)."""
+        g = GaussianSet(count)
+        cg = g.to_c()
+        self._check(self.dll.slm_toy_gaussians(count, seed, C.byref(cg)))
         return g
 
     def ring_camera(self, angle, radius, height, width, height_px=0) -> Camera:

@@ -339,3 +339,31 @@ def test_cpp_adapter_drop_in(gpu):
     print(r)
     assert r["batches_equal"] and r["rng_equal"]
     assert r["worst_loss_rel"] < TOL and r["gn_apply_rel"] < TOL
+
+
+@pytest.mark.gpu
+def test_cfg0_psnr_curve_matches_reference(gpu):
+    """configs[0] (toy scene, 10k Gaussians, 8 x 256^2 full pixels, PCG 8): the test-split
+    PSNR after each of the 10 LM iterations is within +-0.05 dB of the reference's own run
+    (tests/golden/psnr_cfg0.json, made by tests/golden/make_psnr_target.py)."""
+    import json
+
+    import bench
+    from paper_2504_12905_b200 import splatlm
+    from paper_2504_12905_b200.types import LmConfig
+
+    ref = json.load(open(bench.PSNR_TARGET))
+    c = ref["config"]
+    L = gpu
+    train, timgs, test, simgs = bench.cfg0_scene(L, c)
+    td = L.train_data(train, timgs)
+    td.set_clusters(L.kmeans_cameras(train, c["batch"], c["seed"] ^ bench.KMEANS_SALT))
+    rng = L.rng(c["seed"])
+    scene = splatlm.Scene(L, L.random_init(c["gaussians"], [-1, -1, -1], [1, 1, 1], rng))
+    cfg = LmConfig(pcg_iters_initial=c["pcg"], pcg_iters_late=c["pcg"], batch_size_initial=c["batch"],
+                   batch_size_late=c["batch"], samples_per_tile=c["spt"])
+    for it, (rp, rl) in enumerate(zip(ref["psnr"], ref["loss_after"])):
+        rep = scene.lm_step(td, cfg, it, rng)
+        p = np.mean([bench.psnr(scene.render(cam)[0], im) for cam, im in zip(test, simgs)])
+        assert abs(p - rp) <= 0.05, f"iteration {it}: PSNR {p:.4f} vs reference {rp:.4f}"
+        assert abs(rep.loss_after - rl) <= 1e-3 * rl, f"iteration {it}: loss {rep.loss_after} vs {rl}"
