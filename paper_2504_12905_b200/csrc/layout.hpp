@@ -78,7 +78,15 @@ struct SampleArgs {
     const long long* srow_off;
     const float* astream;
     float* astream_out;
+    // Per-window record blocks (k_alpha, once per state/plan): window w of group g
+    // holds its 32 entries' state-only splat fields as [9][32] floats
+    // (mx, my, A, B, C, o, r, g, b) at rstream[kRecBlock * (wbase[g] + w)].
+    const long long* wbase;
+    const float* rstream;
+    float* rstream_out;
 };
+
+constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)
 
 struct DiagArgs {
     const Group* groups;

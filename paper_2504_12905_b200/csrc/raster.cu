@@ -314,6 +314,8 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
 // passes never re-evaluate the Gaussian falloff: alpha comes from a TMA-staged
 // row, and the geometry enters the derivative passes only through the
 // pre-combined tangent polynomial.  Same eval_alpha as k_render / k_masks.
+// Also writes each window's record block (SampleArgs::rstream), so the
+// products gather no state-only record: it arrives by TMA with the rows.
 __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
     __shared__ float4 s_rec[4][32][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -324,13 +326,28 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
     const int* list = A.glist + A.mask_off[gi];
     const unsigned* masks = A.masks + A.mask_off[gi];
     float* out = A.astream_out + 32 * A.srow_off[gi];
-    for (int w = 0, row = 0; 32 * w < nun; ++w) {
+    float* blk = A.rstream_out + static_cast<size_t>(kRecBlock) * A.wbase[gi];
+    for (int w = 0, row = 0; 32 * w < nun; ++w, blk += kRecBlock) {
         const int j = 32 * w + lane;
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+        float rb = 0.f;
         if (j < nun) {
             const float4* r = A.rec + 3 * (c.vbase + list[j]);
-            s_rec[warp][lane][0] = r[0];
-            s_rec[warp][lane][1] = r[1];
+            r0 = r[0];
+            r1 = r[1];
+            rb = r[2].x;
+            s_rec[warp][lane][0] = r0;
+            s_rec[warp][lane][1] = r1;
         }
+        blk[0 * 32 + lane] = r0.x;
+        blk[1 * 32 + lane] = r0.y;
+        blk[2 * 32 + lane] = r0.z;
+        blk[3 * 32 + lane] = r0.w;
+        blk[4 * 32 + lane] = r1.x;
+        blk[5 * 32 + lane] = r1.y;
+        blk[6 * 32 + lane] = r1.z;
+        blk[7 * 32 + lane] = r1.w;
+        blk[8 * 32 + lane] = rb;
         unsigned m = c.active ? masks[32 * w + lane] : 0u;
         const int npc = __reduce_max_sync(0xffffffffu, __popc(m));
         __syncwarp();
@@ -442,7 +459,7 @@ __device__ __forceinline__ void prefetch(const GroupCtx& c, const WinCtx& W, con
 struct WinPipe {
     unsigned m_cur, m_nxt;  // mask words of windows w, w+1
     int g_cur, g_nxt;       // Gaussian index of this lane's entry in windows w, w+1
-    float4 r0, r1, r2, t0, t1, t2;  // records of this lane's entry in window w
+    float4 t0, t1, t2;      // tangent record of this lane's entry in window w
 };
 
 __device__ __forceinline__ void win_index(const GroupCtx& c, const WinCtx& W, int w, int lane, unsigned& m, int& g) {
@@ -455,34 +472,28 @@ __device__ __forceinline__ void win_index(const GroupCtx& c, const WinCtx& W, in
 }
 
 template <bool TAN>
-__device__ __forceinline__ void win_records(const GroupCtx& c, const WinCtx& W, const float4* __restrict__ rec,
-                                            const float4* __restrict__ tan, int w, int g, int lane, WinPipe& P) {
+__device__ __forceinline__ void win_records(const GroupCtx& c, const WinCtx& W, const float4* __restrict__ tan, int w,
+                                            int g, int lane, WinPipe& P) {
     if (w < W.nwin && w * 32 + lane < W.nun) {
         const size_t rg = c.vbase + g;
-        P.r0 = rec[3 * rg];
-        P.r1 = rec[3 * rg + 1];
-        P.r2 = rec[3 * rg + 2];
-        if (TAN) {
-            P.t0 = tan[3 * rg];
-            P.t1 = tan[3 * rg + 1];
-            P.t2 = tan[3 * rg + 2];
-        }
+        P.t0 = tan[3 * rg];
+        P.t1 = tan[3 * rg + 1];
+        P.t2 = tan[3 * rg + 2];
     }
 }
 
 template <bool TAN>
-__device__ __forceinline__ void win_start(const GroupCtx& c, const WinCtx& W, const float4* rec, const float4* tan,
-                                          int lane, WinPipe& P) {
+__device__ __forceinline__ void win_start(const GroupCtx& c, const WinCtx& W, const float4* tan, int lane, WinPipe& P) {
     win_index(c, W, 0, lane, P.m_cur, P.g_cur);
-    win_records<TAN>(c, W, rec, tan, 0, P.g_cur, lane, P);
+    win_records<TAN>(c, W, tan, 0, P.g_cur, lane, P);
     win_index(c, W, 1, lane, P.m_nxt, P.g_nxt);
 }
 
-// After window w's records are staged: start window w+1's records and w+2's index.
+// After window w's tangents are staged: start window w+1's tangents and w+2's index.
 template <bool TAN>
-__device__ __forceinline__ void win_advance(const GroupCtx& c, const WinCtx& W, const float4* rec, const float4* tan,
-                                            int w, int lane, WinPipe& P) {
-    win_records<TAN>(c, W, rec, tan, w + 1, P.g_nxt, lane, P);
+__device__ __forceinline__ void win_advance(const GroupCtx& c, const WinCtx& W, const float4* tan, int w, int lane,
+                                            WinPipe& P) {
+    win_records<TAN>(c, W, tan, w + 1, P.g_nxt, lane, P);
     P.m_cur = P.m_nxt;
     P.g_cur = P.g_nxt;
     win_index(c, W, w + 2, lane, P.m_nxt, P.g_nxt);
@@ -524,6 +535,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// Copy only (the barrier is armed separately).
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -532,27 +550,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// Double-buffered alpha rows of one warp: window w's rows land in buf[w & 1],
-// the copy for window w+1 is in flight while window w runs.
+// Double-buffered window inputs of one warp: window w's alpha rows and record
+// block land in buffer w & 1 (one mbarrier per buffer, one transaction count),
+// the copies for window w+1 are in flight while window w runs.
 struct AlphaPipe {
     float* buf0;
     float* buf1;
+    float* rbuf0;
+    float* rbuf1;
     uint64_t* bar;
-    const float* src;  // the group's first row
-    long long next;    // row of the next window to issue
-    uint32_t par;      // parity bit per buffer
+    const float* src;   // the group's first alpha row
+    const float* rsrc;  // the group's first record block
+    long long next;     // row of the next window to issue
+    uint32_t par;       // parity bit per buffer
     __device__ __forceinline__ void issue(int w, int rows, int lane) {
-        if (lane == 0 && rows > 0)
-            bulk_load((w & 1) ? buf1 : buf0, src + 32 * next, 128u * rows, bar + (w & 1));
+        if (lane == 0) {
+            uint64_t* b = bar + (w & 1);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                         "r"(128u * rows + 4u * kRecBlock)
+                         : "memory");
+            if (rows > 0) bulk_copy((w & 1) ? buf1 : buf0, src + 32 * next, 128u * rows, b);
+            bulk_copy((w & 1) ? rbuf1 : rbuf0, rsrc + static_cast<size_t>(kRecBlock) * w, 4u * kRecBlock, b);
+        }
         next += rows;
     }
-    __device__ __forceinline__ const float* wait(int w, int rows) {
-        if (rows > 0) {
-            mbar_wait(bar + (w & 1), (par >> (w & 1)) & 1u);
-            par ^= 1u << (w & 1);
-        }
+    __device__ __forceinline__ const float* wait(int w) {
+        mbar_wait(bar + (w & 1), (par >> (w & 1)) & 1u);
+        par ^= 1u << (w & 1);
         return (w & 1) ? buf1 : buf0;
     }
+    __device__ __forceinline__ const float* block(int w) const { return (w & 1) ? rbuf1 : rbuf0; }
 };
 
 __device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0xffffffffu, __popc(m)); }
@@ -580,9 +607,10 @@ template <int MODE>
 __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs A) {
     constexpr int NW = kRasterWarps;
     __shared__ __align__(128) float s_alpha[NW][2][32 * 32];
-    // window staging, struct-of-arrays so lanes reading different entries hit
-    // different banks: pass 1 (tau0..5, r, g, b, dr, dg, db); J^T rows 6..8 (r, g, b)
-    __shared__ float s_f[NW][12][32];
+    __shared__ __align__(128) float s_blk[NW][2][kRecBlock];  // record blocks [9][32] (TMA)
+    // pass-1 staging, struct-of-arrays so lanes reading different entries hit
+    // different banks: tau0..5, dr, dg, db
+    __shared__ float s_f[NW][9][32];
     __shared__ __align__(16) float2 s_pair[NW][32][33];  // [pixel][entry]: (dL/dpower, alpha T)
     __shared__ float4 s_phi[NW][32][2];  // per pixel: (x, y, x^2, xy), (y^2, u2, u0, u1), tile-centre coords
     __shared__ uint64_t s_bar[NW][2];
@@ -602,7 +630,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         mbar_init(&s_bar[warp][1], 1);
     }
     __syncwarp();
-    AlphaPipe ap{s_alpha[warp][0], s_alpha[warp][1], s_bar[warp], A.astream + 32 * A.srow_off[gi], 0, 0u};
+    AlphaPipe ap{s_alpha[warp][0], s_alpha[warp][1], s_blk[warp][0], s_blk[warp][1], s_bar[warp],
+                 A.astream + 32 * A.srow_off[gi], A.rstream + static_cast<size_t>(kRecBlock) * A.wbase[gi], 0, 0u};
     const float lx = c.pxc - c.ox, ly = c.pyc - c.oy;
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
@@ -610,36 +639,33 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         const float lxx = lx * lx, lxy = lx * ly, lyy = ly * ly;
         float T = 1.0f, dT = 0.0f, dC0 = 0.f, dC1 = 0.f, dC2 = 0.f;
         WinPipe P;
-        win_start<true>(c, W, A.rec, A.tan, lane, P);
+        win_start<true>(c, W, A.tan, lane, P);
         int rows = max_popc(P.m_cur);
-        ap.issue(0, rows, lane);
+        if (W.nwin > 0) ap.issue(0, rows, lane);
         for (int w = 0; w < W.nwin; ++w) {
             unsigned m = P.m_cur;
-            const int cur = rows;
+            const float* sp = ap.wait(w) + lane;
+            const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
             if (w * 32 + lane < W.nun) {
                 // Q(x, y) = d(power) + do/o about the tile centre: with dx = mx - x,
                 // d(power) = A1 dx + A2 dy + A3 dx^2 + A4 dx dy + A5 dy^2
-                const float mx = P.r0.x - c.ox, my = P.r0.y - c.oy;
+                const float mx = blk[0][lane] - c.ox, my = blk[1][lane] - c.oy;
                 const float A1 = P.t0.x, A2 = P.t0.y, A3 = P.t0.z, A4 = P.t0.w, A5 = P.t1.x;
                 sf[0][lane] = A1 * mx + A2 * my + mx * (A3 * mx + A4 * my) + A5 * my * my +
-                              __fdividef(P.t1.y, P.r1.y);
+                              __fdividef(P.t1.y, blk[5][lane]);
                 sf[1][lane] = -A1 - 2.0f * A3 * mx - A4 * my;
                 sf[2][lane] = -A2 - A4 * mx - 2.0f * A5 * my;
                 sf[3][lane] = A3;
                 sf[4][lane] = A4;
                 sf[5][lane] = A5;
-                sf[6][lane] = P.r1.z;
-                sf[7][lane] = P.r1.w;
-                sf[8][lane] = P.r2.x;
-                sf[9][lane] = P.t1.z;
-                sf[10][lane] = P.t1.w;
-                sf[11][lane] = P.t2.x;
+                sf[6][lane] = P.t1.z;
+                sf[7][lane] = P.t1.w;
+                sf[8][lane] = P.t2.x;
             }
             __syncwarp();
             rows = max_popc(P.m_nxt);
-            ap.issue(w + 1, rows, lane);
-            win_advance<true>(c, W, A.rec, A.tan, w, lane, P);
-            const float* sp = ap.wait(w, cur) + lane;
+            if (w + 1 < W.nwin) ap.issue(w + 1, rows, lane);
+            win_advance<true>(c, W, A.tan, w, lane, P);
             for (; m; m &= m - 1, sp += 32) {
                 const int k = __ffs(m) - 1;
                 const float av = *sp;
@@ -649,12 +675,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 const float dalpha = av < 0.0f ? 0.0f : alpha * Q;
                 const float wgt = alpha * T;
                 const float dw = fmaf(dalpha, T, alpha * dT);
-                dC0 = fmaf(dw, sf[6][k], dC0);
-                dC0 = fmaf(wgt, sf[9][k], dC0);
-                dC1 = fmaf(dw, sf[7][k], dC1);
-                dC1 = fmaf(wgt, sf[10][k], dC1);
-                dC2 = fmaf(dw, sf[8][k], dC2);
-                dC2 = fmaf(wgt, sf[11][k], dC2);
+                dC0 = fmaf(dw, blk[6][k], dC0);
+                dC0 = fmaf(wgt, sf[6][k], dC0);
+                dC1 = fmaf(dw, blk[7][k], dC1);
+                dC1 = fmaf(wgt, sf[7][k], dC1);
+                dC2 = fmaf(dw, blk[8][k], dC2);
+                dC2 = fmaf(wgt, sf[8][k], dC2);
                 const float om = __fsub_rn(1.0f, alpha);
                 dT = fmaf(dT, om, -T * dalpha);
                 T = __fmul_rn(T, om);
@@ -699,36 +725,32 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     float2(*pt)[33] = s_pair[warp];
     const float uC = u0 * Cf0 + u1 * Cf1 + u2 * Cf2;
     float T = 1.0f, uS = 0.f;
-    WinPipe P;
-    win_start<false>(c, W, A.rec, nullptr, lane, P);
-    int rows = max_popc(P.m_cur);
-    ap.issue(0, rows, lane);
+    unsigned m_cur = 0u, m_nxt = 0u;
+    int g_cur = 0, g_nxt = 0;
+    win_index(c, W, 0, lane, m_cur, g_cur);
+    win_index(c, W, 1, lane, m_nxt, g_nxt);
+    int rows = max_popc(m_cur);
+    if (W.nwin > 0) ap.issue(0, rows, lane);
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
-        const unsigned m0 = P.m_cur;
-        const int cur = rows;
+        const unsigned m0 = m_cur;
         const bool ent = w * 32 + lane < W.nun;
-        const float4 e0 = P.r0;  // this lane's entry: mx, my, A, B
-        const float e_c = P.r1.x, e_o = P.r1.y;
-        const int e_g = P.g_cur;
-        if (ent) {
-            sf[6][lane] = P.r1.z;
-            sf[7][lane] = P.r1.w;
-            sf[8][lane] = P.r2.x;
-        }
-        __syncwarp();
-        rows = max_popc(P.m_nxt);
-        ap.issue(w + 1, rows, lane);
-        win_advance<false>(c, W, A.rec, nullptr, w, lane, P);
+        const int e_g = g_cur;
+        rows = max_popc(m_nxt);
+        if (w + 1 < W.nwin) ap.issue(w + 1, rows, lane);
+        m_cur = m_nxt;
+        g_cur = g_nxt;
+        win_index(c, W, w + 2, lane, m_nxt, g_nxt);
         const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
-        const float* sp = ap.wait(w, cur) + lane;
+        const float* sp = ap.wait(w) + lane;
+        const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
         // dL/dalpha = sum_c u_c (T c_c - (C_c - S_incl,c) / (1 - alpha))
         for (unsigned m = m0; m; m &= m - 1, sp += 32) {
             const int k = __ffs(m) - 1;
             const float av = *sp;
             const float alpha = fabsf(av);
-            const float uc = u0 * sf[6][k] + u1 * sf[7][k] + u2 * sf[8][k];
+            const float uc = u0 * blk[6][k] + u1 * blk[7][k] + u2 * blk[8][k];
             const float wgt = __fmul_rn(alpha, T);
             uS = fmaf(wgt, uc, uS);
             const float om = __fsub_rn(1.0f, alpha);
@@ -755,16 +777,16 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         }
         if (ent) {
             // moments about the tile centre -> sums over dx = mx - x, dy = my - y
-            const float mx = e0.x - c.ox, my = e0.y - c.oy;
+            const float mx = blk[0][lane] - c.ox, my = blk[1][lane] - c.oy;
             const float sx = mx * M0 - M12.x, sy = my * M0 - M12.y;
             const float sxx = mx * (mx * M0 - 2.0f * M12.x) + M34.x;
             const float sxy = mx * (my * M0 - M12.y) - my * M12.x + M34.y;
             const float syy = my * (my * M0 - 2.0f * M12.y) + M5G2.x;
             constexpr float kLn2f = 0.69314718055994530942f;
-            const float ca = -2.0f * kLn2f * e0.z, cb = -kLn2f * e0.w, cc = -2.0f * kLn2f * e_c;
+            const float ca = -2.0f * kLn2f * blk[2][lane], cb = -kLn2f * blk[3][lane], cc = -2.0f * kLn2f * blk[4][lane];
             float* dst = A.inter + (c.vbase + e_g) * kRec;
             red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
-            red_add_v4(dst + 4, -0.5f * syy, __fdividef(M0, e_o), G01.x, G01.y);
+            red_add_v4(dst + 4, -0.5f * syy, __fdividef(M0, blk[5][lane]), G01.x, G01.y);
             atomicAdd(dst + 8, M5G2.y);
         }
         __syncwarp();

@@ -411,10 +411,10 @@ struct Samples {
     DevBuf<long long> mask_off;
     DevBuf<unsigned> masks;
     DevBuf<int> glist, gcount, grows;
-    DevBuf<long long> srow_off;
-    DevBuf<float> astream;
-    std::vector<int> hrows;
-    std::vector<long long> hrow_off;
+    DevBuf<long long> srow_off, wbase;
+    DevBuf<float> astream, rstream;
+    std::vector<int> hrows, hcount;
+    std::vector<long long> hrow_off, hwbase;
     std::vector<int> order;  // group order -> plan sample index
     pinned_vector<int> hpix, horig;
     pinned_vector<float> hw;
@@ -484,6 +484,7 @@ struct Samples {
         gcount.ensure(std::max<size_t>(hgroups.size(), 1));
         grows.ensure(std::max<size_t>(hgroups.size(), 1));
         srow_off.ensure(std::max<size_t>(hgroups.size(), 1));
+        wbase.ensure(std::max<size_t>(hgroups.size(), 1));
         groups.ensure(std::max<size_t>(hgroups.size(), 1));
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
@@ -571,20 +572,34 @@ struct Jacobian {
         // alpha-stream layout: rows per group -> offsets (host scan), then the stream
         const size_t ng = samples.hgroups.size();
         samples.hrows.resize(ng);
+        samples.hcount.resize(ng);
         samples.hrow_off.resize(ng);
-        if (ng) SLM_CUDA_CHECK(cudaMemcpyAsync(samples.hrows.data(), samples.grows.p, sizeof(int) * ng,
-                                               cudaMemcpyDeviceToHost, ctx->stream));
+        samples.hwbase.resize(ng);
+        if (ng) {
+            SLM_CUDA_CHECK(cudaMemcpyAsync(samples.hrows.data(), samples.grows.p, sizeof(int) * ng,
+                                           cudaMemcpyDeviceToHost, ctx->stream));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(samples.hcount.data(), samples.gcount.p, sizeof(int) * ng,
+                                           cudaMemcpyDeviceToHost, ctx->stream));
+        }
         ctx->sync();
-        long long rows = 0;
+        long long rows = 0, wins = 0;
         for (size_t g = 0; g < ng; ++g) {
             samples.hrow_off[g] = rows;
             rows += samples.hrows[g];
+            samples.hwbase[g] = wins;
+            wins += (samples.hcount[g] + 31) / 32;
         }
         samples.astream.ensure(std::max<long long>(32 * rows, 1));
-        if (ng) SLM_CUDA_CHECK(cudaMemcpyAsync(samples.srow_off.p, samples.hrow_off.data(), sizeof(long long) * ng,
-                                               cudaMemcpyHostToDevice, ctx->stream));
+        samples.rstream.ensure(std::max<long long>(static_cast<long long>(kRecBlock) * wins, 1));
+        if (ng) {
+            SLM_CUDA_CHECK(cudaMemcpyAsync(samples.srow_off.p, samples.hrow_off.data(), sizeof(long long) * ng,
+                                           cudaMemcpyHostToDevice, ctx->stream));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(samples.wbase.p, samples.hwbase.data(), sizeof(long long) * ng,
+                                           cudaMemcpyHostToDevice, ctx->stream));
+        }
         SampleArgs b = args();
         b.astream_out = samples.astream.p;
+        b.rstream_out = samples.rstream.p;
         launch_alpha(b, ctx->stream);
         ctx->check_launch();
         ctx->sync();  // hrow_off is read by the async copy
@@ -613,6 +628,8 @@ struct Jacobian {
         a.mask_off = samples.mask_off.p;
         a.srow_off = samples.srow_off.p;
         a.astream = samples.astream.p;
+        a.wbase = samples.wbase.p;
+        a.rstream = samples.rstream.p;
         return a;
     }
 
