@@ -666,9 +666,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
             rows = max_popc(P.m_nxt);
             if (w + 1 < W.nwin) ap.issue(w + 1, rows, lane);
             win_advance<true>(c, W, A.tan, w, lane, P);
-            for (; m; m &= m - 1, sp += 32) {
-                const int k = __ffs(m) - 1;
-                const float av = *sp;
+            // two pairs per iteration (the second predicated: alpha = 0 is neutral
+            // in the dual blend), so the loads of both overlap
+            auto pair = [&](int k, float av) {
                 const float alpha = fabsf(av);
                 const float Q = sf[0][k] + lx * sf[1][k] + ly * sf[2][k] + lxx * sf[3][k] + lxy * sf[4][k] +
                                 lyy * sf[5][k];
@@ -684,6 +684,18 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 const float om = __fsub_rn(1.0f, alpha);
                 dT = fmaf(dT, om, -T * dalpha);
                 T = __fmul_rn(T, om);
+            };
+            while (m) {
+                const int k1 = __ffs(m) - 1;
+                m &= m - 1;
+                const bool two = m != 0u;
+                const int k2 = two ? __ffs(m) - 1 : k1;
+                m = two ? (m & (m - 1)) : m;
+                const float av1 = sp[0];
+                const float av2 = two ? sp[32] : 0.0f;
+                sp += two ? 64 : 32;
+                pair(k1, av1);
+                pair(k2, av2);
             }
             __syncwarp();
         }
@@ -746,17 +758,33 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
         // dL/dalpha = sum_c u_c (T c_c - (C_c - S_incl,c) / (1 - alpha))
-        for (unsigned m = m0; m; m &= m - 1, sp += 32) {
-            const int k = __ffs(m) - 1;
-            const float av = *sp;
-            const float alpha = fabsf(av);
-            const float uc = u0 * blk[6][k] + u1 * blk[7][k] + u2 * blk[8][k];
-            const float wgt = __fmul_rn(alpha, T);
-            uS = fmaf(wgt, uc, uS);
-            const float om = __fsub_rn(1.0f, alpha);
-            const float dalpha = fmaf(T, uc, -(uC - uS) * rcp_approx(om));
-            pt[lane][k] = make_float2(av < 0.0f ? 0.0f : dalpha * alpha, wgt);
-            T = __fmul_rn(T, om);
+        {
+            unsigned m = m0;
+            while (m) {  // two pairs per iteration, the second predicated
+                const int k1 = __ffs(m) - 1;
+                m &= m - 1;
+                const bool two = m != 0u;
+                const int k2 = two ? __ffs(m) - 1 : k1;
+                m = two ? (m & (m - 1)) : m;
+                const float av1 = sp[0];
+                const float av2 = two ? sp[32] : 0.0f;
+                sp += two ? 64 : 32;
+                const float a1 = fabsf(av1), a2 = fabsf(av2);
+                const float uc1 = u0 * blk[6][k1] + u1 * blk[7][k1] + u2 * blk[8][k1];
+                const float uc2 = u0 * blk[6][k2] + u1 * blk[7][k2] + u2 * blk[8][k2];
+                const float w1 = __fmul_rn(a1, T);
+                uS = fmaf(w1, uc1, uS);
+                const float om1 = __fsub_rn(1.0f, a1);
+                const float d1 = fmaf(T, uc1, -(uC - uS) * rcp_approx(om1));
+                pt[lane][k1] = make_float2(av1 < 0.0f ? 0.0f : d1 * a1, w1);
+                T = __fmul_rn(T, om1);
+                const float w2 = __fmul_rn(a2, T);
+                uS = fmaf(w2, uc2, uS);
+                const float om2 = __fsub_rn(1.0f, a2);
+                const float d2 = fmaf(T, uc2, -(uC - uS) * rcp_approx(om2));
+                if (two) pt[lane][k2] = make_float2(av2 < 0.0f ? 0.0f : d2 * a2, w2);
+                T = __fmul_rn(T, om2);
+            }
         }
         __syncwarp();
         // phase B (lane = entry), dense over the pixels
