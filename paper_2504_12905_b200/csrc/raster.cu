@@ -418,6 +418,15 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     return d;
 }
 
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
 // Window prefetch (lane = compacted entry 32w+lane): mask word of the lane's
 // pixel and the entry's splat record (and tangent record).
 struct Prefetch {
@@ -612,7 +621,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     // different banks: tau0..5, dr, dg, db
     __shared__ float s_f[NW][9][32];
     __shared__ __align__(16) float2 s_pair[NW][32][33];  // [pixel][entry]: (dL/dpower, alpha T)
-    __shared__ float4 s_phi[NW][32][2];  // per pixel: (x, y, x^2, xy), (y^2, u2, u0, u1), tile-centre coords
+    __shared__ float4 s_phi[NW][32];  // per pixel: (x, y, u0, u1), tile-centre coords
+    __shared__ float s_u2[NW][32];
     __shared__ uint64_t s_bar[NW][2];
     if (A.done_flag && *A.done_flag) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -732,8 +742,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
     const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
     const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
-    s_phi[warp][lane][0] = make_float4(lx, ly, lx * lx, lx * ly);
-    s_phi[warp][lane][1] = make_float4(ly * ly, u2, u0, u1);
+    s_phi[warp][lane] = make_float4(lx, ly, u0, u1);
+    s_u2[warp][lane] = u2;
     float2(*pt)[33] = s_pair[warp];
     const float uC = u0 * Cf0 + u1 * Cf1 + u2 * Cf2;
     float T = 1.0f, uS = 0.f;
@@ -796,11 +806,13 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
             const bool b = (col >> p) & 1u;
             v.x = b ? v.x : 0.0f;
             v.y = b ? v.y : 0.0f;
-            const float4 f0 = s_phi[warp][p][0], f1 = s_phi[warp][p][1];
+            const float4 f0 = s_phi[warp][p];  // (x, y, u0, u1): 2 broadcast wavefronts
+            const float fu2 = s_u2[warp][p];
+            const float2 sq = fmul2(make_float2(f0.x, f0.x), make_float2(f0.x, f0.y));  // (x^2, xy)
             M12 = ffma2(make_float2(v.x, v.x), make_float2(f0.x, f0.y), M12);
-            M34 = ffma2(make_float2(v.x, v.x), make_float2(f0.z, f0.w), M34);
-            M5G2 = ffma2(v, make_float2(f1.x, f1.y), M5G2);
-            G01 = ffma2(make_float2(v.y, v.y), make_float2(f1.z, f1.w), G01);
+            M34 = ffma2(make_float2(v.x, v.x), sq, M34);
+            M5G2 = ffma2(v, make_float2(f0.y * f0.y, fu2), M5G2);
+            G01 = ffma2(make_float2(v.y, v.y), make_float2(f0.z, f0.w), G01);
             M0 += v.x;
         }
         if (ent) {
