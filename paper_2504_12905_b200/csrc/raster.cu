@@ -562,25 +562,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Double-buffered window inputs of one warp: window w's alpha rows and record
 // block land in buffer w & 1 (one mbarrier per buffer, one transaction count),
 // the copies for window w+1 are in flight while window w runs.
+constexpr int kAlphaRows = 22;  // rows staged per window (~98% of windows at configs[2] need <= 22)
+
 struct AlphaPipe {
     float* buf0;
     float* buf1;
     float* rbuf0;
     float* rbuf1;
     uint64_t* bar;
-    const float* src;   // the group's first alpha row
-    const float* rsrc;  // the group's first record block
-    long long next;     // row of the next window to issue
-    uint32_t par;       // parity bit per buffer
+    const float* src;      // the group's first alpha row
+    const float* rsrc;     // the group's first record block
+    long long next;        // row of the next window to issue
+    long long row0, row1;  // first row of the window held in each buffer
+    uint32_t par;          // parity bit per buffer
     __device__ __forceinline__ void issue(int w, int rows, int lane) {
+        const int staged = min(rows, kAlphaRows);
         if (lane == 0) {
             uint64_t* b = bar + (w & 1);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-                         "r"(128u * rows + 4u * kRecBlock)
+                         "r"(128u * staged + 4u * kRecBlock)
                          : "memory");
-            if (rows > 0) bulk_copy((w & 1) ? buf1 : buf0, src + 32 * next, 128u * rows, b);
+            if (staged > 0) bulk_copy((w & 1) ? buf1 : buf0, src + 32 * next, 128u * staged, b);
             bulk_copy((w & 1) ? rbuf1 : rbuf0, rsrc + static_cast<size_t>(kRecBlock) * w, 4u * kRecBlock, b);
         }
+        if (w & 1) row1 = next;
+        else row0 = next;
         next += rows;
     }
     __device__ __forceinline__ const float* wait(int w) {
@@ -589,7 +595,19 @@ struct AlphaPipe {
         return (w & 1) ? buf1 : buf0;
     }
     __device__ __forceinline__ const float* block(int w) const { return (w & 1) ? rbuf1 : rbuf0; }
+    // rows beyond kAlphaRows are read from global memory (rare)
+    __device__ __forceinline__ const float* overflow(int w) const {
+        return src + 32 * (((w & 1) ? row1 : row0) + kAlphaRows);
+    }
 };
+
+// The set bits of m up to and including its kAlphaRows-th.
+__device__ __forceinline__ unsigned first_rows(unsigned m) {
+    unsigned t = m;
+#pragma unroll 1
+    for (int i = 0; i < kAlphaRows && t; ++i) t &= t - 1;
+    return m & ~t;
+}
 
 __device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0xffffffffu, __popc(m)); }
 
@@ -615,7 +633,7 @@ constexpr int kRasterWarps = 2;
 template <int MODE>
 __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs A) {
     constexpr int NW = kRasterWarps;
-    __shared__ __align__(128) float s_alpha[NW][2][32 * 32];
+    __shared__ __align__(128) float s_alpha[NW][2][kAlphaRows * 32];
     __shared__ __align__(128) float s_blk[NW][2][kRecBlock];  // record blocks [9][32] (TMA)
     // pass-1 staging, struct-of-arrays so lanes reading different entries hit
     // different banks: tau0..5, dr, dg, db
@@ -641,7 +659,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     }
     __syncwarp();
     AlphaPipe ap{s_alpha[warp][0], s_alpha[warp][1], s_blk[warp][0], s_blk[warp][1], s_bar[warp],
-                 A.astream + 32 * A.srow_off[gi], A.rstream + static_cast<size_t>(kRecBlock) * A.wbase[gi], 0, 0u};
+                 A.astream + 32 * A.srow_off[gi], A.rstream + static_cast<size_t>(kRecBlock) * A.wbase[gi], 0, 0, 0, 0u};
     const float lx = c.pxc - c.ox, ly = c.pyc - c.oy;
 
     float u0 = 0.f, u1 = 0.f, u2 = 0.f;
@@ -653,7 +671,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         int rows = max_popc(P.m_cur);
         if (W.nwin > 0) ap.issue(0, rows, lane);
         for (int w = 0; w < W.nwin; ++w) {
-            unsigned m = P.m_cur;
+            const unsigned m = P.m_cur;
+            const int cur = rows;
             const float* sp = ap.wait(w) + lane;
             const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
             if (w * 32 + lane < W.nun) {
@@ -695,17 +714,26 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 dT = fmaf(dT, om, -T * dalpha);
                 T = __fmul_rn(T, om);
             };
-            while (m) {
-                const int k1 = __ffs(m) - 1;
-                m &= m - 1;
-                const bool two = m != 0u;
-                const int k2 = two ? __ffs(m) - 1 : k1;
-                m = two ? (m & (m - 1)) : m;
-                const float av1 = sp[0];
-                const float av2 = two ? sp[32] : 0.0f;
-                sp += two ? 64 : 32;
-                pair(k1, av1);
-                pair(k2, av2);
+            auto walk = [&](unsigned mm, const float* q) {
+                while (mm) {
+                    const int k1 = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const bool two = mm != 0u;
+                    const int k2 = two ? __ffs(mm) - 1 : k1;
+                    mm = two ? (mm & (mm - 1)) : mm;
+                    const float av1 = q[0];
+                    const float av2 = two ? q[32] : 0.0f;
+                    q += two ? 64 : 32;
+                    pair(k1, av1);
+                    pair(k2, av2);
+                }
+            };
+            if (cur > kAlphaRows) {
+                const unsigned lo = first_rows(m);
+                walk(lo, sp);
+                walk(m & ~lo, ap.overflow(w) + lane);
+            } else {
+                walk(m, sp);
             }
             __syncwarp();
         }
@@ -756,6 +784,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = m_cur;
+        const int cur = rows;
         const bool ent = w * 32 + lane < W.nun;
         const int e_g = g_cur;
         rows = max_popc(m_nxt);
@@ -768,17 +797,16 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
         // dL/dalpha = sum_c u_c (T c_c - (C_c - S_incl,c) / (1 - alpha))
-        {
-            unsigned m = m0;
+        auto walk = [&](unsigned m, const float* q) {
             while (m) {  // two pairs per iteration, the second predicated
                 const int k1 = __ffs(m) - 1;
                 m &= m - 1;
                 const bool two = m != 0u;
                 const int k2 = two ? __ffs(m) - 1 : k1;
                 m = two ? (m & (m - 1)) : m;
-                const float av1 = sp[0];
-                const float av2 = two ? sp[32] : 0.0f;
-                sp += two ? 64 : 32;
+                const float av1 = q[0];
+                const float av2 = two ? q[32] : 0.0f;
+                q += two ? 64 : 32;
                 const float a1 = fabsf(av1), a2 = fabsf(av2);
                 const float uc1 = u0 * blk[6][k1] + u1 * blk[7][k1] + u2 * blk[8][k1];
                 const float uc2 = u0 * blk[6][k2] + u1 * blk[7][k2] + u2 * blk[8][k2];
@@ -795,6 +823,13 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 if (two) pt[lane][k2] = make_float2(av2 < 0.0f ? 0.0f : d2 * a2, w2);
                 T = __fmul_rn(T, om2);
             }
+        };
+        if (cur > kAlphaRows) {
+            const unsigned lo = first_rows(m0);
+            walk(lo, sp);
+            walk(m0 & ~lo, ap.overflow(w) + lane);
+        } else {
+            walk(m0, sp);
         }
         __syncwarp();
         // phase B (lane = entry), dense over the pixels
