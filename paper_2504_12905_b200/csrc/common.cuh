@@ -38,35 +38,56 @@ __device__ __forceinline__ int warp_max_i(int v) {
     return __reduce_max_sync(0xffffffffu, v);
 }
 
-// The single gate/alpha evaluation every raster kernel shares, so the forward
-// render and all derivative passes make identical FP32 decisions
-// (blend_pixel rasterizer.hpp:110-124).  Explicit _rn intrinsics pin the
-// rounding: no kernel may contract these differently.
-struct Alpha {
-    float alpha;
-    float e;  // 2^q = exp(power): the falloff before opacity, = alpha/o when not clamped
-    float dx, dy;
-    bool clamped;
+// The single gate / alpha evaluation every raster kernel shares (blend_pixel,
+// rasterizer.hpp:110-124), so the forward render, the blend masks, the alpha
+// stream and the diag make identical FP32 decisions.  Per (entry, tile) the
+// log2 of the unclamped alpha is a quadratic in the pixel centre (x, y)
+// relative to the tile centre:
+//   q' = log2(o) + power log2(e) = g0 + g1 x + g2 y + g3 x^2 + g4 x y + g5 y^2
+// (A, B, C of the record are the conic pre-scaled to the log2 domain), so
+// alpha = 2^q' takes one MUFU.EX2, the skip gate alpha < 1/255 is
+// q' < log2(1/255) -- no exponential for the ~85% of pairs it rejects -- and
+// power > 0 is q' > log2(o).  Explicit _rn intrinsics pin the rounding: no
+// kernel may contract these differently.
+struct Gate {
+    float g0, g1, g2, g3, g4, g5, lo;  // lo = log2(o)
 };
+constexpr float kLog2Skip = -7.99435343685885793f;  // log2(1/255)
 
-__device__ __forceinline__ bool eval_alpha(const float4 r0, const float4 r1, float pxc, float pyc,
-                                           Alpha& a) {
+__device__ __forceinline__ Gate make_gate(const float4 r0, const float4 r1, float ox, float oy) {
     // r0 = {mx, my, A, B}, r1 = {C, opacity, r, g}
-    const float dx = __fsub_rn(r0.x, pxc);
-    const float dy = __fsub_rn(r0.y, pyc);
-    const float q = __fmaf_rn(__fmul_rn(r0.z, dx), dx,
-                              __fmaf_rn(__fmul_rn(r1.x, dy), dy, __fmul_rn(__fmul_rn(r0.w, dx), dy)));
-    a.dx = dx;
-    a.dy = dy;
-    if (q > 0.0f) return false;  // power > 0: skip
+    const float mx = __fsub_rn(r0.x, ox), my = __fsub_rn(r0.y, oy);
+    const float A = r0.z, B = r0.w, C = r1.x;
+    Gate g;
+    g.lo = log2f(r1.y);
+    const float ax = __fmul_rn(A, mx), cy = __fmul_rn(C, my);
+    g.g0 = __fadd_rn(__fmaf_rn(ax, mx, __fmaf_rn(__fmul_rn(B, mx), my, __fmul_rn(cy, my))), g.lo);
+    g.g1 = -__fmaf_rn(B, my, __fmul_rn(2.0f, ax));
+    g.g2 = -__fmaf_rn(B, mx, __fmul_rn(2.0f, cy));
+    g.g3 = A;
+    g.g4 = B;
+    g.g5 = C;
+    return g;
+}
+
+struct PixQ {  // pixel centre relative to the tile centre (half-integers) and its monomials
+    float x, y, xx, xy, yy;
+};
+__device__ __forceinline__ PixQ pix_q(float x, float y) {
+    return PixQ{x, y, __fmul_rn(x, x), __fmul_rn(x, y), __fmul_rn(y, y)};
+}
+__device__ __forceinline__ float gate_q(const Gate& g, const PixQ& p) {
+    return __fmaf_rn(g.g5, p.yy,
+                     __fmaf_rn(g.g4, p.xy, __fmaf_rn(g.g3, p.xx, __fmaf_rn(g.g2, p.y, __fmaf_rn(g.g1, p.x, g.g0)))));
+}
+// alpha (clamped at 0.99, rasterizer.hpp:15) of a pair from q'; false: a gate skips it.
+__device__ __forceinline__ bool gate_alpha(float q, float lo, float& alpha, bool& clamped) {
+    if (q > lo || q < kLog2Skip) return false;  // power > 0, or alpha < 1/255
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q));
-    a.e = e;
-    float alpha = __fmul_rn(r1.y, e);
-    a.clamped = alpha > 0.99f;
-    if (a.clamped) alpha = 0.99f;
-    a.alpha = alpha;
-    return alpha >= (float)(1.0 / 255.0);  // alpha < 1/255: skip
+    clamped = e > 0.99f;
+    alpha = clamped ? 0.99f : e;
+    return true;
 }
 
 // Termination test (rasterizer.hpp:121-122): the entry that would push T

@@ -70,7 +70,7 @@ __device__ __forceinline__ float4 alpha_box(float4 r0, float4 r1) {
     return make_float4(r0.x - hx, r0.x + hx, r0.y - hy, r0.y + hy);
 }
 
-__global__ void __launch_bounds__(kRenderThreads) k_render(
+__global__ void __launch_bounds__(kRenderThreads, 16) k_render(
     const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
     const int* __restrict__ tile_offsets, const int* __restrict__ entries,
     const float4* __restrict__ rec, int Gp, const float* __restrict__ gt,
@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
     const int b = tile_offsets[tile], n = tile_offsets[tile + 1] - b;
     const size_t vbase = static_cast<size_t>(v) * Gp;
 
-    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix], pyc[kRenderPix];
+    const float tcx = (float)(tx * kTile + kTile / 2), tcy = (float)(ty * kTile + kTile / 2);
+    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix];
+    PixQ pq[kRenderPix];
     int cnt[kRenderPix], last[kRenderPix];
     unsigned live = 0u;  // bit i: pixel i still blending
 #pragma unroll
@@ -104,17 +106,18 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
         C0[i] = C1[i] = C2[i] = 0.0f;
         cnt[i] = 0;
         last[i] = n;
-        pyc[i] = (float)y + 0.5f;
+        pq[i] = pix_q(pxc - tcx, (float)y + 0.5f - tcy);
         if (x < cam.width && y < cam.height) live |= 1u << i;
     }
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
         for (int j = threadIdx.x; j < kRenderStage && start + j < n; j += kRenderThreads) {
             const float4* r = rec + 3 * (vbase + entries[b + start + j]);
-            const float4 r0 = r[0], r1 = r[1];
-            s_rec[j][0] = r0;
-            s_rec[j][1] = r1;
-            s_rec[j][2] = r[2];
+            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
+            const Gate g = make_gate(r0, r1, tcx, tcy);
+            s_rec[j][0] = make_float4(g.g0, g.g1, g.g2, g.g3);
+            s_rec[j][1] = make_float4(g.g4, g.g5, g.lo, r1.z);
+            s_rec[j][2] = make_float4(r1.w, r2.x, 0.f, 0.f);
             s_box[j] = alpha_box(r0, r1);
         }
         __syncthreads();
@@ -122,23 +125,24 @@ __global__ void __launch_bounds__(kRenderThreads) k_render(
         for (int k = 0; k < m && live; ++k) {
             const float4 bx = s_box[k];
             if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
-            const float4 r0 = s_rec[k][0], r1 = s_rec[k][1];
-            const float c2 = s_rec[k][2].x;
+            const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
+            const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
 #pragma unroll
             for (int i = 0; i < kRenderPix; ++i) {
                 if (!((live >> i) & 1u)) continue;
-                Alpha a;
-                if (!eval_alpha(r0, r1, pxc, pyc[i], a)) continue;
+                float alpha;
+                bool cl;
+                if (!gate_alpha(gate_q(g, pq[i]), g.lo, alpha, cl)) continue;
                 float tt;
-                if (terminates(T[i], a.alpha, tt)) {
+                if (terminates(T[i], alpha, tt)) {
                     live &= ~(1u << i);
                     last[i] = start + k;
                     continue;
                 }
-                const float w = __fmul_rn(a.alpha, T[i]);
-                C0[i] = __fmaf_rn(w, r1.z, C0[i]);
-                C1[i] = __fmaf_rn(w, r1.w, C1[i]);
-                C2[i] = __fmaf_rn(w, c2, C2[i]);
+                const float w = __fmul_rn(alpha, T[i]);
+                C0[i] = __fmaf_rn(w, q1.w, C0[i]);
+                C1[i] = __fmaf_rn(w, q2.x, C1[i]);
+                C2[i] = __fmaf_rn(w, q2.y, C2[i]);
                 T[i] = tt;
                 ++cnt[i];
             }
@@ -253,6 +257,7 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, gi, lane, c)) return;
     const int mylast = c.active ? A.last_img[c.pix] : 0;
     const int maxlast = __reduce_max_sync(0xffffffffu, mylast);
+    const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
     const int* tl = A.entries + A.tile_offsets[c.tile];
     const long long off = A.mask_off[gi];
     int* glist = A.glist_out + off;
@@ -265,15 +270,19 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
         if (j < maxlast) {
             g = tl[j];
             const float4* r = A.rec + 3 * (c.vbase + g);
-            s_rec[warp][lane][0] = r[0];
-            s_rec[warp][lane][1] = r[1];
+            const Gate gt = make_gate(r[0], r[1], c.ox, c.oy);
+            s_rec[warp][lane][0] = make_float4(gt.g0, gt.g1, gt.g2, gt.g3);
+            s_rec[warp][lane][1] = make_float4(gt.g4, gt.g5, gt.lo, 0.f);
         }
         __syncwarp();
         const int mn = min(32, mylast - base);
         unsigned bits = 0u;
         for (int k = 0; k < mn; ++k) {
-            Alpha a;
-            if (eval_alpha(s_rec[warp][k][0], s_rec[warp][k][1], c.pxc, c.pyc, a)) bits |= 1u << k;
+            const float4 q0 = s_rec[warp][k][0], q1 = s_rec[warp][k][1];
+            const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
+            float alpha;
+            bool cl;
+            if (gate_alpha(gate_q(gt, pq), gt.lo, alpha, cl)) bits |= 1u << k;
         }
         const unsigned un = __reduce_or_sync(0xffffffffu, bits);
         const int rank = __popc(un & ((1u << lane) - 1u));
@@ -326,6 +335,7 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
     const int* list = A.glist + A.mask_off[gi];
     const unsigned* masks = A.masks + A.mask_off[gi];
     float* out = A.astream_out + 32 * A.srow_off[gi];
+    const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
     float* blk = A.rstream_out + static_cast<size_t>(kRecBlock) * A.wbase[gi];
     for (int w = 0, row = 0; 32 * w < nun; ++w, blk += kRecBlock) {
         const int j = 32 * w + lane;
@@ -336,8 +346,9 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
             r0 = r[0];
             r1 = r[1];
             rb = r[2].x;
-            s_rec[warp][lane][0] = r0;
-            s_rec[warp][lane][1] = r1;
+            const Gate gt = make_gate(r0, r1, c.ox, c.oy);
+            s_rec[warp][lane][0] = make_float4(gt.g0, gt.g1, gt.g2, gt.g3);
+            s_rec[warp][lane][1] = make_float4(gt.g4, gt.g5, gt.lo, 0.f);
         }
         blk[0 * 32 + lane] = r0.x;
         blk[1 * 32 + lane] = r0.y;
@@ -353,9 +364,12 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
         __syncwarp();
         for (int i = 0; m; m &= m - 1, ++i) {
             const int k = __ffs(m) - 1;
-            Alpha a;
-            eval_alpha(s_rec[warp][k][0], s_rec[warp][k][1], c.pxc, c.pyc, a);
-            out[32 * (row + i) + lane] = a.clamped ? -a.alpha : a.alpha;
+            const float4 q0 = s_rec[warp][k][0], q1 = s_rec[warp][k][1];
+            const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
+            float alpha = 0.0f;
+            bool cl = false;
+            gate_alpha(gate_q(gt, pq), gt.lo, alpha, cl);  // blended: the mask already decided
+            out[32 * (row + i) + lane] = cl ? -alpha : alpha;
         }
         row += npc;
         __syncwarp();
@@ -375,7 +389,7 @@ __global__ void __launch_bounds__(32) k_mask_stats(SampleArgs A, unsigned long l
     const int ncw = (nun + 31) >> 5;
     const unsigned* masks = A.masks + A.mask_off[blockIdx.x];
     unsigned long long s[7] = {1ull, (unsigned long long)ncw, 0ull, 0ull, (unsigned long long)nun, 0ull, 0ull};
-    int pend = 0, rem = c.active ? __popc(masks[lane]) : 0;
+    int rem = c.active ? __popc(masks[lane]) : 0;
     for (int w = 0; w < ncw; ++w) {
         const unsigned m = c.active ? masks[32 * w + lane] : 0u;
         {   // run-ahead simulation: lanes done with window w continue into w+1
@@ -882,6 +896,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
 // phase B (lane = entry x pixel half) sums its column as monomials in (dx, dy).
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     __shared__ float s_f[4][9][32];
+    __shared__ float s_gate[4][7][32];  // the entries' gate polynomials (make_gate)
     __shared__ int s_g[4][32];
     __shared__ float s_t[4][3][32][17];
     __shared__ float4 s_pix[4][32];  // (px+.5, py+.5, W0, W1)
@@ -906,6 +921,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     s_pw2[warp][lane] = W2;
     const int e16 = lane & 15, ph = lane >> 4;
     const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
+    const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
     prefetch<false>(c, W, A.rec, nullptr, 0, lane, P);
@@ -915,6 +931,14 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
         if (w * 32 + lane < W.nun) {
             stage_rec(sf, lane, P.r0, P.r1, P.r2);
             s_g[warp][lane] = P.g;
+            const Gate gt = make_gate(P.r0, P.r1, c.ox, c.oy);
+            s_gate[warp][0][lane] = gt.g0;
+            s_gate[warp][1][lane] = gt.g1;
+            s_gate[warp][2][lane] = gt.g2;
+            s_gate[warp][3][lane] = gt.g3;
+            s_gate[warp][4][lane] = gt.g4;
+            s_gate[warp][5][lane] = gt.g5;
+            s_gate[warp][6][lane] = gt.lo;
         }
         __syncwarp();
         prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
@@ -925,11 +949,13 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             if (16 * h >= nent) break;
             for (unsigned m = (m0 >> (16 * h)) & 0xFFFFu; m; m &= m - 1) {
                 const int kk = __ffs(m) - 1, k = 16 * h + kk;
-                const float4 r0 = make_float4(sf[0][k], sf[1][k], sf[2][k], sf[3][k]);
+                const Gate gt{s_gate[warp][0][k], s_gate[warp][1][k], s_gate[warp][2][k], s_gate[warp][3][k],
+                              s_gate[warp][4][k], s_gate[warp][5][k], s_gate[warp][6][k]};
+                float alpha = 0.0f;
+                bool clamped = false;
+                gate_alpha(gate_q(gt, pq), gt.lo, alpha, clamped);  // blended: the mask already decided
+                const float e = __fdividef(alpha, sf[5][k]);  // the falloff before opacity (unclamped)
                 const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
-                Alpha a;
-                eval_alpha(r0, r1, c.pxc, c.pyc, a);
-                const float alpha = a.alpha;
                 const float c2 = sf[8][k];
                 const float wgt = __fmul_rn(alpha, T);
                 const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
@@ -939,8 +965,8 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
                 const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
                 const float da2 = T * c2 - (Cf2 - n2) * inv1m;
                 const float sw2 = W0 * da0 * da0 + W1 * da1 * da1 + W2 * da2 * da2;
-                s_t[warp][0][lane][kk] = a.clamped ? 0.0f : alpha * alpha * sw2;
-                s_t[warp][1][lane][kk] = a.clamped ? 0.0f : a.e * a.e * sw2;
+                s_t[warp][0][lane][kk] = clamped ? 0.0f : alpha * alpha * sw2;
+                s_t[warp][1][lane][kk] = clamped ? 0.0f : e * e * sw2;
                 s_t[warp][2][lane][kk] = wgt * wgt;
                 S0 = n0;
                 S1 = n1;
