@@ -190,22 +190,20 @@ __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta
     dsigma(Gm, pv + 3, pv + 6, dS);
     const float dop = Gm.o * (1.0f - Gm.o) * pv[10];
     const float dr = Gm.dcol[0] * pv[11], dg = Gm.dcol[1] * pv[12], db = Gm.dcol[2] * pv[13];
-    float4 nr0, nr1, nr2;  // next view's record, prefetched
+    float4 nr0, nr1;  // next view's record (first 32 B: mean, conic, opacity), prefetched
     if (V > 0) {
         nr0 = __ldg(rec + 3 * static_cast<size_t>(g));
         nr1 = __ldg(rec + 3 * static_cast<size_t>(g) + 1);
-        nr2 = __ldg(rec + 3 * static_cast<size_t>(g) + 2);
     }
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        const float4 q0 = nr0, q1 = nr1, q2 = nr2;
+        const float4 q0 = nr0, q1 = nr1;
         if (v + 1 < V) {
             const size_t ng = vg + Gp;
             nr0 = __ldg(rec + 3 * ng);
             nr1 = __ldg(rec + 3 * ng + 1);
-            nr2 = __ldg(rec + 3 * ng + 2);
         }
-        if (q2.y == 0.0f) continue;  // invalid (view, Gaussian)
+        if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
         const DevCam& cam = cams[v];
         View Vw;
         load_view(Gm, cam, q0, q1, Vw);
@@ -239,12 +237,11 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     float gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
     // Software pipeline: view v+1's record and intermediate are loaded
     // (unconditionally; invalid pairs hold zeros) while view v is processed.
-    float4 nr0, nr1, nr2, ni0, ni1, ni2;
+    float4 nr0, nr1, ni0, ni1, ni2;
     auto fetch = [&](int v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         nr0 = __ldg(rec + 3 * vg);
         nr1 = __ldg(rec + 3 * vg + 1);
-        nr2 = __ldg(rec + 3 * vg + 2);
         const float4* ip = reinterpret_cast<const float4*>(inter + vg * kRec);
         ni0 = ip[0];
         ni1 = ip[1];
@@ -253,9 +250,9 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     if (V > 0) fetch(0);
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        const float4 q0 = nr0, q1 = nr1, q2 = nr2, i0 = ni0, i1 = ni1, i2 = ni2;
+        const float4 q0 = nr0, q1 = nr1, i0 = ni0, i1 = ni1, i2 = ni2;
         if (v + 1 < V) fetch(v + 1);
-        if (q2.y == 0.0f) continue;
+        if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
         float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
         ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
         ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
