@@ -34,21 +34,30 @@ __device__ __forceinline__ double sym2_max_eig(double a, double b, double c) {  
     return mid + disc;
 }
 
-__device__ Prepared prepare_value(const double* __restrict__ beta, int Gp, int g, const DevCam& cam) {
-    Prepared out;
-    out.valid = false;
-    out.zero_quat = false;
-    out.radius = 0.0;
-    const double mu[3] = {beta[0 * Gp + g], beta[1 * Gp + g], beta[2 * Gp + g]};
+// View-independent part (quat_to_rotation, covariance_3d, sigmoid, colour):
+// computed once per Gaussian, exactly the operations of the per-view path.
+struct GaussCommon {
+    double mu[3], sig[9], o, col[3];
+    bool zero_quat;
+};
+
+__device__ GaussCommon prepare_common(const double* __restrict__ beta, int Gp, int g) {
+    GaussCommon gc;
+    gc.zero_quat = false;
+    for (int k = 0; k < 3; ++k) gc.mu[k] = beta[k * Gp + g];
     const double ls[3] = {beta[3 * Gp + g], beta[4 * Gp + g], beta[5 * Gp + g]};
     const double q[4] = {beta[6 * Gp + g], beta[7 * Gp + g], beta[8 * Gp + g], beta[9 * Gp + g]};
     const double logit = beta[10 * Gp + g];
-
+    gc.o = 1.0 / (1.0 + exp(-logit));  // dual.hpp:74
+    for (int k = 0; k < 3; ++k) {
+        const double raw = 0.5 + kColorC0 * beta[(11 + k) * Gp + g];
+        gc.col[k] = raw > 0.0 ? raw : 0.0;
+    }
     // quat_to_rotation (geometry.hpp:21-39)
     const double nsq = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
     if (nsq == 0.0) {
-        out.zero_quat = true;
-        return out;
+        gc.zero_quat = true;
+        return gc;
     }
     const double inv = 1.0 / sqrt(nsq);
     const double w = q[0] * inv, x = q[1] * inv, y = q[2] * inv, z = q[3] * inv;
@@ -64,12 +73,24 @@ __device__ Prepared prepare_value(const double* __restrict__ beta, int Gp, int g
     r[8] = 1.0 - 2.0 * (x * x + y * y);
     // covariance_3d (geometry.hpp:43-57)
     const double s[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
-    double m[9], sig[9];
+    double m[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) m[3 * i + j] = r[3 * i + j] * s[j];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
-            sig[3 * i + j] = m[3 * i] * m[3 * j] + m[3 * i + 1] * m[3 * j + 1] + m[3 * i + 2] * m[3 * j + 2];
+            gc.sig[3 * i + j] = m[3 * i] * m[3 * j] + m[3 * i + 1] * m[3 * j + 1] + m[3 * i + 2] * m[3 * j + 2];
+    return gc;
+}
+
+__device__ Prepared prepare_view(const GaussCommon& gc, const DevCam& cam) {
+    Prepared out;
+    out.valid = false;
+    out.zero_quat = gc.zero_quat;
+    out.radius = 0.0;
+    out.depth = 0.0;
+    if (gc.zero_quat) return out;
+    const double* mu = gc.mu;
+    const double* sig = gc.sig;
     // project_gaussian (geometry.hpp:71-108)
     const double* W = cam.R;
     const double tx = W[0] * mu[0] + W[1] * mu[1] + W[2] * mu[2] + cam.t[0];
@@ -107,11 +128,8 @@ __device__ Prepared prepare_value(const double* __restrict__ beta, int Gp, int g
     out.ca = c * inv_det;
     out.cb = -b * inv_det;
     out.cc = a * inv_det;
-    out.o = 1.0 / (1.0 + exp(-logit));  // dual.hpp:74
-    for (int k = 0; k < 3; ++k) {
-        const double raw = 0.5 + kColorC0 * beta[(11 + k) * Gp + g];
-        out.col[k] = raw > 0.0 ? raw : 0.0;
-    }
+    out.o = gc.o;
+    for (int k = 0; k < 3; ++k) out.col[k] = gc.col[k];
     if (out.o <= kAlphaSkipD) return out;
     const double lam = sym2_max_eig(a, b, c);
     out.radius = sqrt(2.0 * log(255.0 * out.o) * lam) * (1.0 + 1e-6) + 1e-6;
@@ -127,47 +145,50 @@ __device__ __forceinline__ unsigned long long depth_key(double d) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// grid (ceil(G/256), V): one thread per (view, Gaussian).
-__global__ void k_prepare(const double* __restrict__ beta, int G, int Gp,
-                          const DevCam* __restrict__ cams, float4* __restrict__ rec,
-                          unsigned long long* __restrict__ keys, short4* __restrict__ rect,
-                          int* __restrict__ tile_count, int* __restrict__ err) {
+// One thread per Gaussian, looping over the views: the view-independent FP64
+// work (rotation, covariance, sigmoid) is done once per Gaussian.
+__global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta, int G, int Gp,
+                                                 const DevCam* __restrict__ cams, int V, float4* __restrict__ rec,
+                                                 unsigned long long* __restrict__ keys, short4* __restrict__ rect,
+                                                 int* __restrict__ tile_count, int* __restrict__ err) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int v = blockIdx.y;
     if (g >= G) return;
-    const DevCam cam = cams[v];
-    const Prepared p = prepare_value(beta, Gp, g, cam);
-    const size_t vg = static_cast<size_t>(v) * Gp + g;
-    if (p.zero_quat) atomicOr(err, 1);
-    {  // err[1 + v] = G_v, the valid (view, Gaussian) count (warp-aggregated)
-        const unsigned am = __activemask();
-        const unsigned vm = __ballot_sync(am, p.valid);
-        if (vm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&err[1 + v], __popc(vm));
+    const GaussCommon gc = prepare_common(beta, Gp, g);
+    if (gc.zero_quat) atomicOr(err, 1);
+    for (int v = 0; v < V; ++v) {
+        const DevCam& cam = cams[v];
+        const Prepared p = prepare_view(gc, cam);
+        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        {  // err[1 + v] = G_v, the valid (view, Gaussian) count (warp-aggregated)
+            const unsigned am = __activemask();
+            const unsigned vm = __ballot_sync(am, p.valid);
+            if (vm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(&err[1 + v], __popc(vm));
+        }
+        keys[vg] = depth_key(p.depth);
+        float4* R = rec + 3 * vg;
+        if (!p.valid) {
+            R[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            R[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            R[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            rect[vg] = make_short4(1, 0, 1, 0);
+            continue;
+        }
+        R[0] = make_float4((float)p.mx, (float)p.my, (float)(-0.5 * p.ca * kLog2e), (float)(-p.cb * kLog2e));
+        R[1] = make_float4((float)(-0.5 * p.cc * kLog2e), (float)p.o, (float)p.col[0], (float)p.col[1]);
+        R[2] = make_float4((float)p.col[2], 1.0f, 0.f, 0.f);  // .y = valid marker
+        // tile rect (rasterizer.cpp:29-36)
+        int x0 = (int)floor((p.mx - p.radius) / kTile);
+        int x1 = (int)floor((p.mx + p.radius) / kTile);
+        int y0 = (int)floor((p.my - p.radius) / kTile);
+        int y1 = (int)floor((p.my + p.radius) / kTile);
+        x0 = x0 < 0 ? 0 : x0;
+        y0 = y0 < 0 ? 0 : y0;
+        x1 = x1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : x1;
+        y1 = y1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : y1;
+        rect[vg] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+        for (int ty = y0; ty <= y1; ++ty)
+            for (int tx = x0; tx <= x1; ++tx) atomicAdd(&tile_count[cam.tile_base + ty * cam.tiles_x + tx], 1);
     }
-    keys[vg] = depth_key(p.depth);
-    float4* R = rec + 3 * vg;
-    if (!p.valid) {
-        R[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        R[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        R[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        rect[vg] = make_short4(1, 0, 1, 0);
-        return;
-    }
-    R[0] = make_float4((float)p.mx, (float)p.my, (float)(-0.5 * p.ca * kLog2e), (float)(-p.cb * kLog2e));
-    R[1] = make_float4((float)(-0.5 * p.cc * kLog2e), (float)p.o, (float)p.col[0], (float)p.col[1]);
-    R[2] = make_float4((float)p.col[2], 1.0f, 0.f, 0.f);  // .y = valid marker
-    // tile rect (rasterizer.cpp:29-36)
-    int x0 = (int)floor((p.mx - p.radius) / kTile);
-    int x1 = (int)floor((p.mx + p.radius) / kTile);
-    int y0 = (int)floor((p.my - p.radius) / kTile);
-    int y1 = (int)floor((p.my + p.radius) / kTile);
-    x0 = x0 < 0 ? 0 : x0;
-    y0 = y0 < 0 ? 0 : y0;
-    x1 = x1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : x1;
-    y1 = y1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : y1;
-    rect[vg] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
-    for (int ty = y0; ty <= y1; ++ty)
-        for (int tx = x0; tx <= x1; ++tx) atomicAdd(&tile_count[cam.tile_base + ty * cam.tiles_x + tx], 1);
 }
 
 // ------------------------------------------------------------------ K3 scan
@@ -265,8 +286,7 @@ void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V
                     unsigned long long* keys, short4* rect, int* tile_count, int* err,
                     cudaStream_t st) {
     if (G == 0 || V == 0) return;
-    dim3 grid((G + 255) / 256, V);
-    k_prepare<<<grid, 256, 0, st>>>(beta, G, Gp, cams, rec, keys, rect, tile_count, err); ++g_launches;
+    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, tile_count, err); ++g_launches;
 }
 
 void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total,
