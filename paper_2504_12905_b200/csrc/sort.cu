@@ -274,6 +274,70 @@ void launch_depth_init(const unsigned long long* keys, const short4* rect, int G
     k_depth_init<<<static_cast<unsigned>((n + 1023) / 1024), 1024, 0, st>>>(keys, rect, G, Gp, n, kout, vout, and_or); ++g_launches;
 }
 
+// After the passes over the key's upper 32 bits: runs of equal upper halves
+// (depths within a relative 2^-20 -- a few per cent of the Gaussians, runs of
+// 2-3) are put in (full key, index) order by the thread at each run start:
+// insertion sort, heapsort for a (pathological) long run.  Key 0 marks culled
+// Gaussians (valid keys have the top bit set); their order is irrelevant.
+__device__ __forceinline__ bool kv_less(unsigned long long ka, unsigned va, unsigned long long kb, unsigned vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+
+__device__ void heap_sift(unsigned long long* k, unsigned* v, long long root, long long len) {
+    while (true) {
+        long long c = 2 * root + 1;
+        if (c >= len) return;
+        if (c + 1 < len && kv_less(k[c], v[c], k[c + 1], v[c + 1])) ++c;
+        if (!kv_less(k[root], v[root], k[c], v[c])) return;
+        const unsigned long long tk = k[root];
+        const unsigned tv = v[root];
+        k[root] = k[c];
+        v[root] = v[c];
+        k[c] = tk;
+        v[c] = tv;
+        root = c;
+    }
+}
+
+__global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __restrict__ vals, long long n) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
+    if (hi == 0u) return;                                                 // culled
+    if (i > 0 && static_cast<unsigned>(keys[i - 1] >> 32) == hi) return;  // not a run start
+    long long e = i + 1;
+    while (e < n && static_cast<unsigned>(keys[e] >> 32) == hi) ++e;
+    const long long len = e - i;
+    if (len <= 1) return;
+    unsigned long long* k = keys + i;
+    unsigned* v = vals + i;
+    if (len <= 32) {
+        for (long long a = 1; a < len; ++a) {  // insertion sort by (key, index)
+            const unsigned long long ka = k[a];
+            const unsigned va = v[a];
+            long long b = a - 1;
+            while (b >= 0 && kv_less(ka, va, k[b], v[b])) {
+                k[b + 1] = k[b];
+                v[b + 1] = v[b];
+                --b;
+            }
+            k[b + 1] = ka;
+            v[b + 1] = va;
+        }
+        return;
+    }
+    for (long long r = len / 2 - 1; r >= 0; --r) heap_sift(k, v, r, len);
+    for (long long end = len - 1; end > 0; --end) {
+        const unsigned long long tk = k[0];
+        const unsigned tv = v[0];
+        k[0] = k[end];
+        v[0] = v[end];
+        k[end] = tk;
+        v[end] = tv;
+        heap_sift(k, v, 0, end);
+    }
+}
+
 __global__ void k_view_key(const unsigned* __restrict__ vals, long long n, int Gp, unsigned* __restrict__ vkey) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) vkey[i] = vals[i] / static_cast<unsigned>(Gp);
@@ -323,11 +387,16 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
     const unsigned long long vary = and_k ^ or_k;
     unsigned long long *ka = b.k64a, *kb = b.k64b;
     unsigned *va = b.v32a, *vb = b.v32b;
-    for (int byte = 0; byte < 8; ++byte) {
+    // LSD passes over the varying bytes of the upper 32 bits, then a run fix-up
+    // for the (rare, short) runs of equal upper halves
+    for (int byte = 4; byte < 8; ++byte) {
         if (((vary >> (8 * byte)) & 0xFFull) == 0ull) continue;
         radix_pass<unsigned long long>(ka, va, kb, vb, n, 8 * byte, b.hist, b.part, st);
         std::swap(ka, kb);
         std::swap(va, vb);
+    }
+    if (vary & 0xFFFFFFFFull) {
+        k_fix_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ka, va, n); ++g_launches;
     }
     // then by view (not needed for the order -- a tile's entries belong to one
     // view -- but the view-major emit keeps the tile passes' scatter local: measured

@@ -13,10 +13,12 @@ Bars (BASELINE.json north_star):
   clamp, 1e-4 termination) may take the other branch; the tolerance absorbs
   that and the tests report the worst case they see.
 """
+import math
+
 import numpy as np
 import pytest
 
-from paper_2504_12905_b200.types import LmConfig, SamplePlan
+from paper_2504_12905_b200.types import GaussianSet, LmConfig, SamplePlan
 from support import (MT64, g_cams, g_plan, g_set, golden, norm_rel, random_scene, rel_error)
 from support import test_camera as tcam
 
@@ -367,3 +369,27 @@ def test_cfg0_psnr_curve_matches_reference(gpu):
         p = np.mean([bench.psnr(scene.render(cam)[0], im) for cam, im in zip(test, simgs)])
         assert abs(p - rp) <= 0.05, f"iteration {it}: PSNR {p:.4f} vs reference {rp:.4f}"
         assert abs(rep.loss_after - rl) <= 1e-3 * rl, f"iteration {it}: loss {rep.loss_after} vs {rl}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spread", [0.0, 1e-12, 1e-9, 1e-7])
+def test_tile_lists_bit_exact_near_equal_depths(gpu, spread):
+    """Depth ties and near-ties (equal upper 32 key bits, distinct doubles): the
+    radix tile-list construction sorts the upper halves, then fixes up runs; the
+    order must still be the reference's (depth, index) order, bit for bit."""
+    from oracle.cpu_bind import port
+
+    rng = np.random.default_rng(11)
+    n = 300
+    g = GaussianSet.zeros(n)
+    g.means = np.column_stack([rng.uniform(-0.6, 0.6, n), rng.uniform(-0.6, 0.6, n),
+                               np.full(n, 0.25) + spread * rng.integers(0, 5, n)]).reshape(-1)
+    g.log_scales = np.full(3 * n, math.log(0.2))
+    g.rotations = np.tile([1.0, 0.0, 0.0, 0.0], n)
+    g.opacity_logits = rng.uniform(-0.5, 1.0, n)
+    g.colors = rng.uniform(-1, 1, 3 * n)
+    cam = tcam(64)
+    o_off, o_idx = port().bin_and_sort(g, cam)
+    off, idx = gpu.bin_and_sort(g, cam)
+    assert np.array_equal(off, o_off)
+    assert np.array_equal(idx, o_idx)
