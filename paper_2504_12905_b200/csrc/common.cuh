@@ -43,7 +43,7 @@ __device__ __forceinline__ int warp_max_i(int v) {
 // stream and the diag make identical FP32 decisions.  Per (entry, tile) the
 // log2 of the unclamped alpha is a quadratic in the pixel centre (x, y)
 // relative to the tile centre:
-//   q' = log2(o) + power log2(e) = g0 + g1 x + g2 y + g3 x^2 + g4 x y + g5 y^2
+//   q' = log2(o) + power log2(e) = (g0 + g1 x + g3 x^2) + (g2 + g4 x) y + g5 y^2
 // (A, B, C of the record are the conic pre-scaled to the log2 domain), so
 // alpha = 2^q' takes one MUFU.EX2, the skip gate alpha < 1/255 is
 // q' < log2(1/255) -- no exponential for the ~85% of pairs it rejects -- and
@@ -70,15 +70,22 @@ __device__ __forceinline__ Gate make_gate(const float4 r0, const float4 r1, floa
     return g;
 }
 
-struct PixQ {  // pixel centre relative to the tile centre (half-integers) and its monomials
-    float x, y, xx, xy, yy;
+struct PixQ {  // pixel centre relative to the tile centre (half-integers) and its squares
+    float x, y, xx, yy;
 };
-__device__ __forceinline__ PixQ pix_q(float x, float y) {
-    return PixQ{x, y, __fmul_rn(x, x), __fmul_rn(x, y), __fmul_rn(y, y)};
+__device__ __forceinline__ PixQ pix_q(float x, float y) { return PixQ{x, y, __fmul_rn(x, x), __fmul_rn(y, y)}; }
+// q' factored by column: the x-only parts (gx0 = g0 + g1 x + g3 x^2, gx1 = g2 + g4 x)
+// are shared by every pixel of a column (the render evaluates 4 pixels of one
+// column per entry); every kernel uses exactly these operations.
+__device__ __forceinline__ float gate_x0(const Gate& g, float x, float xx) {
+    return __fmaf_rn(g.g3, xx, __fmaf_rn(g.g1, x, g.g0));
+}
+__device__ __forceinline__ float gate_x1(const Gate& g, float x) { return __fmaf_rn(g.g4, x, g.g2); }
+__device__ __forceinline__ float gate_qy(const Gate& g, float gx0, float gx1, float y, float yy) {
+    return __fmaf_rn(g.g5, yy, __fmaf_rn(gx1, y, gx0));
 }
 __device__ __forceinline__ float gate_q(const Gate& g, const PixQ& p) {
-    return __fmaf_rn(g.g5, p.yy,
-                     __fmaf_rn(g.g4, p.xy, __fmaf_rn(g.g3, p.xx, __fmaf_rn(g.g2, p.y, __fmaf_rn(g.g1, p.x, g.g0)))));
+    return gate_qy(g, gate_x0(g, p.x, p.xx), gate_x1(g, p.x), p.y, p.yy);
 }
 // alpha (clamped at 0.99, rasterizer.hpp:15) of a pair from q'; false: a gate skips it.
 __device__ __forceinline__ bool gate_alpha(float q, float lo, float& alpha, bool& clamped) {

@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
     const size_t vbase = static_cast<size_t>(v) * Gp;
 
     const float tcx = (float)(tx * kTile + kTile / 2), tcy = (float)(ty * kTile + kTile / 2);
-    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix];
-    PixQ pq[kRenderPix];
+    const float qx = pxc - tcx, qxx = __fmul_rn(qx, qx);
+    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix], qy[kRenderPix], qyy[kRenderPix];
     int cnt[kRenderPix], last[kRenderPix];
     unsigned live = 0u;  // bit i: pixel i still blending
 #pragma unroll
@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
         C0[i] = C1[i] = C2[i] = 0.0f;
         cnt[i] = 0;
         last[i] = n;
-        pq[i] = pix_q(pxc - tcx, (float)y + 0.5f - tcy);
+        qy[i] = (float)y + 0.5f - tcy;
+        qyy[i] = __fmul_rn(qy[i], qy[i]);
         if (x < cam.width && y < cam.height) live |= 1u << i;
     }
     for (int start = 0; start < n; start += kRenderStage) {
@@ -127,12 +128,13 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
             if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
+            const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column
 #pragma unroll
             for (int i = 0; i < kRenderPix; ++i) {
                 if (!((live >> i) & 1u)) continue;
                 float alpha;
                 bool cl;
-                if (!gate_alpha(gate_q(g, pq[i]), g.lo, alpha, cl)) continue;
+                if (!gate_alpha(gate_qy(g, gx0, gx1, qy[i], qyy[i]), g.lo, alpha, cl)) continue;
                 float tt;
                 if (terminates(T[i], alpha, tt)) {
                     live &= ~(1u << i);
