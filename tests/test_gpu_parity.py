@@ -292,6 +292,31 @@ def test_lm_trajectory_vs_reference(gpu):
     assert norm_rel(st.pack(), g_set(d, "lm_final").pack()) < 1e-3
 
 
+def test_lm_speculation_discarded_when_inputs_change(gpu, port):
+    """lm_step draws the next step's batch + plan speculatively during its PCG; a
+    caller that touches the RNG or rebuilds the clusters between steps must get
+    exactly the reference's draws (the speculation is discarded)."""
+    gt, tc, ti, _, _ = port.toy_scene(20, 8, 1, 64, 20214)
+    rg, ro = gpu.rng(5), port.rng(5)
+    sg = gpu.random_init(60, [-1, -1, -1], [1, 1, 1], rg)
+    so = port.random_init(60, [-1, -1, -1], [1, 1, 1], ro)
+    tdg, tdo = gpu.train_data(tc, list(ti)), port.train_data(tc, list(ti))
+    for td in (tdg, tdo):
+        td.rebuild_clusters(4, 7)
+    cfg = LmConfig(batch_size_initial=4, pcg_iters_initial=4)
+    for it in range(5):
+        if it == 2:  # the caller consumes the RNG between steps
+            assert rg() == ro()
+        if it == 3:  # ... and rebuilds the clusters (batch size change, run.cpp:145-153)
+            for td in (tdg, tdo):
+                td.rebuild_clusters(3, 11)
+            cfg = LmConfig(batch_size_initial=3, pcg_iters_initial=4)
+        a, b = gpu.lm_step(sg, tdg, cfg, it, rg), port.lm_step(so, tdo, cfg, it, ro)
+        assert a.batch == b.batch, f"step {it}: batch {a.batch} vs {b.batch}"
+        assert rel_error(a.loss_after, b.loss_after) < TOL
+    assert rg() == ro()  # same RNG position
+
+
 def test_lm_step_fixed_point(gpu, port):
     """test_solver.cpp:132: at zero residual the step does not move the state."""
     gt, tc, ti, sc, si = port.toy_scene(8, 4, 1, 32, 93)
