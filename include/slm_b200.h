@@ -156,6 +156,14 @@ int slm_lm_step_host(slm_context* ctx, slm_gaussians* state, slm_train* t,
 /* batch_loss (lm.cpp:39-54), MSE; cameras index the TrainData. */
 int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cams, int n, double* out);
 
+/* ---- metrics (metrics/image_metrics.hpp, io/run.cpp:77-92), computed on the device */
+/* metrics::evaluate (image_metrics.cpp:180-186) on two interleaved-RGB f64 images. */
+int slm_evaluate(slm_context* ctx, const double* rendered, const double* ground_truth, int width,
+                 int height, slm_metric_report* out);
+/* io::evaluate_split: render every camera of the split (TrainData images are
+ * the ground truth) and average mse / psnr / ssim over the cameras. */
+int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out);
+
 /* ---- io helpers the harness uses (io/dataset.cpp:138-166, io/scene_gen.cpp) */
 int slm_random_init(int count, const double* cube_min, const double* cube_max, slm_rng* rng,
                     slm_gaussians* out);

@@ -102,6 +102,13 @@ typedef struct slm_pcg_result {
     double rel_residual;
 } slm_pcg_result;
 
+/* MetricReport (metrics/image_metrics.hpp:7-11). */
+typedef struct slm_metric_report {
+    double mse;
+    double psnr;
+    double ssim;
+} slm_metric_report;
+
 #ifdef __cplusplus
 }
 #endif

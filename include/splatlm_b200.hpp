@@ -25,6 +25,8 @@
 #include "slm_b200.h"
 #include "splatlm/autodiff/jacobian.hpp"
 #include "splatlm/core/types.hpp"
+#include "splatlm/io/dataset.hpp"
+#include "splatlm/metrics/image_metrics.hpp"
 #include "splatlm/sampling/sample_plan.hpp"
 #include "splatlm/solver/lm.hpp"
 #include "splatlm/solver/pcg.hpp"
@@ -255,6 +257,48 @@ inline solver::PcgResult pcg_solve(Device& dev, const solver::ApplyFn& apply, co
     res.breakdown = r.breakdown != 0;
     res.rel_residual = r.rel_residual;
     return res;
+}
+
+// metrics::evaluate (image_metrics.cpp:180-186) on the device.
+inline metrics::MetricReport evaluate(Device& dev, const Image& rendered, const Image& ground_truth) {
+    if (rendered.width != ground_truth.width || rendered.height != ground_truth.height)
+        throw std::invalid_argument("metrics: image shapes differ");
+    slm_metric_report r{};
+    check(slm_evaluate(dev.get(), rendered.data.data(), ground_truth.data.data(), rendered.width,
+                       rendered.height, &r));
+    metrics::MetricReport out;
+    out.mse = r.mse;
+    out.psnr = r.psnr;
+    out.ssim = r.ssim;
+    return out;
+}
+
+// io::evaluate_split (run.cpp:77-92): every camera of the split rendered and
+// scored on the device, mean mse / psnr / ssim.
+inline metrics::MetricReport evaluate_split(Device& dev, const GaussianSet& state, const io::SceneDataset& split) {
+    metrics::MetricReport out;
+    if (split.cameras.empty()) return out;
+    std::vector<slm_camera> cams;
+    std::vector<float> imgs;
+    for (size_t i = 0; i < split.cameras.size(); ++i) {
+        cams.push_back(to_c(split.cameras[i]));
+        imgs.insert(imgs.end(), split.images[i].data.begin(), split.images[i].data.end());
+    }
+    GaussianSet g = state;
+    slm_gaussians cg = to_c(g);
+    slm_scene* s = nullptr;
+    slm_train* t = nullptr;
+    check(slm_scene_create(dev.get(), &cg, &s));
+    const int rc = slm_train_create(dev.get(), cams.data(), static_cast<int>(cams.size()), imgs.data(), &t);
+    slm_metric_report r{};
+    const int rc2 = rc == SLM_OK ? slm_evaluate_split(s, t, &r) : rc;
+    if (t) slm_train_destroy(t);
+    slm_scene_destroy(s);
+    check(rc2);
+    out.mse = r.mse;
+    out.psnr = r.psnr;
+    out.ssim = r.ssim;
+    return out;
 }
 
 }  // namespace splatlm_b200

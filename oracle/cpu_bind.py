@@ -97,6 +97,7 @@ class CpuLib:
                                      C.POINTER(C.c_float), _f64p]),
             "mse": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
             "psnr": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
+            "ssim": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(self.lib, prefix + name)
@@ -301,6 +302,11 @@ class CpuLib:
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
         return self._psnr(f64ptr(a), f64ptr(b), a.shape[1], a.shape[0])
+
+    def ssim(self, a, b) -> float:
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        return self._ssim(f64ptr(a), f64ptr(b), a.shape[1], a.shape[0])
 
 
 class Rng:

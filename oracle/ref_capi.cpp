@@ -588,5 +588,11 @@ double ref_psnr(const double* a, const double* b, int w, int h) {
     std::copy(b, b + ib.data.size(), ib.data.begin());
     return metrics::psnr(ia, ib);
 }
+double ref_ssim(const double* a, const double* b, int w, int h) {
+    Image ia(w, h), ib(w, h);
+    std::copy(a, a + ia.data.size(), ia.data.begin());
+    std::copy(b, b + ib.data.size(), ib.data.begin());
+    return metrics::ssim(ia, ib);
+}
 
 }  // extern "C"

@@ -1607,6 +1607,76 @@ double orc_psnr(const double* a, const double* b, int w, int h) {
     return 10.0 * log10(1.0 / m);
 }
 
+/* metrics::ssim (image_metrics.cpp:14-67,86-106,121-139): 11-tap Gaussian
+ * window (sigma 1.5), separable filter with single reflect padding, C1 =
+ * 0.01^2, C2 = 0.03^2, mean of the local SSIM over pixels and channels. */
+#define SSIM_WIN 11
+#define SSIM_HALF 5
+static void ssim_window(double* w) {
+    double sum = 0.0;
+    for (int i = 0; i < SSIM_WIN; ++i) {
+        const double d = i - SSIM_HALF;
+        w[i] = exp(-0.5 * d * d / (1.5 * 1.5));
+        sum += w[i];
+    }
+    for (int i = 0; i < SSIM_WIN; ++i) w[i] /= sum;
+}
+static int ssim_reflect(int i, int n) {
+    if (i < 0) i = -i - 1;
+    if (i >= n) i = 2 * n - i - 1;
+    return i;
+}
+static void ssim_filter(const double* win, const double* src, int w, int h, double* tmp, double* dst) {
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double acc = 0.0;
+            for (int k = -SSIM_HALF; k <= SSIM_HALF; ++k)
+                acc += win[k + SSIM_HALF] * src[(size_t)y * w + ssim_reflect(x + k, w)];
+            tmp[(size_t)y * w + x] = acc;
+        }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double acc = 0.0;
+            for (int k = -SSIM_HALF; k <= SSIM_HALF; ++k)
+                acc += win[k + SSIM_HALF] * tmp[(size_t)ssim_reflect(y + k, h) * w + x];
+            dst[(size_t)y * w + x] = acc;
+        }
+}
+double orc_ssim(const double* a, const double* b, int w, int h) {
+    const size_t n = (size_t)w * h;
+    if (n == 0) return 1.0;
+    double win[SSIM_WIN];
+    ssim_window(win);
+    double* buf = (double*)malloc(sizeof(double) * n * 9);
+    double *pa = buf, *pb = buf + n, *sq = buf + 2 * n, *tmp = buf + 3 * n, *ma = buf + 4 * n,
+           *mb = buf + 5 * n, *eaa = buf + 6 * n, *ebb = buf + 7 * n, *eab = buf + 8 * n;
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    double total = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        for (size_t i = 0; i < n; ++i) {
+            pa[i] = a[3 * i + c];
+            pb[i] = b[3 * i + c];
+        }
+        ssim_filter(win, pa, w, h, tmp, ma);
+        ssim_filter(win, pb, w, h, tmp, mb);
+        for (size_t i = 0; i < n; ++i) sq[i] = pa[i] * pa[i];
+        ssim_filter(win, sq, w, h, tmp, eaa);
+        for (size_t i = 0; i < n; ++i) sq[i] = pb[i] * pb[i];
+        ssim_filter(win, sq, w, h, tmp, ebb);
+        for (size_t i = 0; i < n; ++i) sq[i] = pa[i] * pb[i];
+        ssim_filter(win, sq, w, h, tmp, eab);
+        for (size_t i = 0; i < n; ++i) {
+            const double va = eaa[i] - ma[i] * ma[i], vb = ebb[i] - mb[i] * mb[i];
+            const double cov = eab[i] - ma[i] * mb[i];
+            const double num = (2.0 * ma[i] * mb[i] + c1) * (2.0 * cov + c2);
+            const double den = (ma[i] * ma[i] + mb[i] * mb[i] + c1) * (va + vb + c2);
+            total += num / den;
+        }
+    }
+    free(buf);
+    return total / (3.0 * (double)n);
+}
+
 /* batch_loss, MSE only (lm.cpp:39-54) */
 static int batch_loss_d(const slm_gaussians* g, const slm_camera* cams, const int* batch, int nb,
                         double* const* gts, double* out) {

@@ -84,6 +84,7 @@ int orc_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n_cams, c
                    double* out);
 double orc_mse(const double* a, const double* b, int w, int h);
 double orc_psnr(const double* a, const double* b, int w, int h);
+double orc_ssim(const double* a, const double* b, int w, int h);
 
 #ifdef __cplusplus
 }

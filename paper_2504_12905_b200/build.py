@@ -30,6 +30,7 @@ CU_SOURCES = {
     "chain.cu": [],
     "cg.cu": [],
     "sort.cu": [],
+    "metrics.cu": [],
 }
 CPP_SOURCES = ["runtime.cpp"]
 HEADERS = ["common.cuh", "layout.hpp", "runtime.hpp"]

@@ -124,6 +124,17 @@ struct CgState {
 
 enum Mode { kJvp = 0, kVjp = 1, kGn = 2, kRhs = 3 };
 
+// One image of a metrics launch (metrics.cu): interleaved RGB at elements
+// [off, off + 3*w*h), its 32x32 output tiles at partial[tile_base, +tiles).
+struct ImgDesc {
+    long long off;
+    int w, h, tiles_x, tiles, tile_base;
+};
+constexpr int kMetricWin = 11;  // image_metrics.cpp:14
+struct MetricWindow {
+    double w[kMetricWin];
+};
+
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
 

@@ -1322,6 +1322,64 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     if (!std::isfinite(rep.loss_after)) throw std::runtime_error("lm_step: non-finite loss after update");
 }
 
+// ---- metrics (metrics/image_metrics.cpp, io/run.cpp:77-92) on device (metrics.cu)
+static MetricWindow metric_window() {  // gaussian_window (image_metrics.cpp:25-35)
+    MetricWindow w{};
+    double sum = 0.0;
+    for (int i = 0; i < kMetricWin; ++i) {
+        const double d = i - kMetricWin / 2;
+        w.w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+        sum += w.w[i];
+    }
+    for (double& v : w.w) v /= sum;
+    return w;
+}
+
+struct ImageRef {
+    long long off;  // element offset of the interleaved RGB image
+    int w, h;
+};
+
+// {sum of squared differences, sum of local SSIM} per image, both over the 3 channels.
+template <typename T>
+static std::vector<double2> image_metrics(Context* c, const T* a, const T* b, const std::vector<ImageRef>& imgs) {
+    const int n = static_cast<int>(imgs.size());
+    std::vector<ImgDesc> hd(n);
+    int base = 0, max_tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        ImgDesc& d = hd[i];
+        d.off = imgs[i].off;
+        d.w = imgs[i].w;
+        d.h = imgs[i].h;
+        d.tiles = metric_tiles(d.w, d.h, &d.tiles_x);
+        d.tile_base = base;
+        base += d.tiles;
+        max_tiles = std::max(max_tiles, d.tiles);
+    }
+    std::vector<double2> out(n);
+    if (n == 0) return out;
+    DevBuf<ImgDesc> dd;
+    DevBuf<double2> part, dout;
+    dd.ensure(n);
+    part.ensure(std::max(base, 1));
+    dout.ensure(n);
+    SLM_CUDA_CHECK(cudaMemcpyAsync(dd.p, hd.data(), sizeof(ImgDesc) * n, cudaMemcpyHostToDevice, c->stream));
+    launch_image_metrics(a, b, dd.p, n, max_tiles, part.p, dout.p, metric_window(), c->stream);
+    c->check_launch();
+    SLM_CUDA_CHECK(cudaMemcpyAsync(out.data(), dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return out;
+}
+
+// metrics::evaluate (image_metrics.cpp:180-186) from the device sums.
+static slm_metric_report metric_report(double2 s, int w, int h) {
+    slm_metric_report r{};
+    const double n = static_cast<double>(w) * h;
+    r.mse = n == 0 ? 0.0 : s.x / (3.0 * n);                  // :108-113
+    r.psnr = r.mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / r.mse);  // :115-119
+    r.ssim = n == 0 ? 1.0 : s.y / (3.0 * n);                 // :121-139
+    return r;
+}
 }  // namespace slm
 
 // =========================================================================== C ABI
@@ -1937,6 +1995,62 @@ int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, do
         double acc = 0.0;
         for (int v = 0; v < n; ++v) acc += sse[v] / (3.0 * cv[v].width * cv[v].height);
         *out = n == 0 ? 0.0 : acc / n;
+    });
+}
+
+int slm_evaluate(slm_context* ctx, const double* rendered, const double* gt, int width, int height,
+                 slm_metric_report* out) {
+    return guarded([&] {
+        if (width < 0 || height < 0) throw std::invalid_argument("metrics: image shapes differ");
+        Context* c = &ctx->impl;
+        c->activate();
+        const size_t n = 3 * static_cast<size_t>(width) * height;
+        DevBuf<double> da, db;
+        da.ensure(std::max<size_t>(n, 1));
+        db.ensure(std::max<size_t>(n, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(da.p, rendered, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(db.p, gt, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        const auto s = image_metrics<double>(c, da.p, db.p, {ImageRef{0, width, height}});
+        *out = metric_report(s[0], width, height);
+    });
+}
+
+int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out) {
+    return guarded([&] {  // io::evaluate_split (run.cpp:77-92): render_full + evaluate per camera, mean
+        Context* c = s->impl.ctx;
+        c->activate();
+        Train& t = split->impl;
+        const int n = static_cast<int>(t.cams.size());
+        slm_metric_report mean{};
+        constexpr int kChunk = 8;  // views rendered per batch (bounds the batch buffers)
+        for (int lo = 0; lo < n; lo += kChunk) {
+            const int hi = std::min(n, lo + kChunk);
+            std::vector<int> ids;
+            std::vector<slm_camera> cv;
+            for (int i = lo; i < hi; ++i) {
+                ids.push_back(i);
+                cv.push_back(t.cams[i]);
+            }
+            Batch b(c);
+            b.prepare(s->impl, cv);
+            copy_gt(t, b, ids);
+            b.render(false);
+            std::vector<ImageRef> imgs;
+            for (int v = 0; v < b.V; ++v) imgs.push_back({3 * b.hcams[v].pix_base, cv[v].width, cv[v].height});
+            const auto sums = image_metrics<float>(c, b.image.p, b.gt.p, imgs);
+            for (int v = 0; v < b.V; ++v) {
+                const slm_metric_report r = metric_report(sums[v], cv[v].width, cv[v].height);
+                mean.mse += r.mse;
+                mean.psnr += r.psnr;
+                mean.ssim += r.ssim;
+            }
+        }
+        if (n > 0) {
+            mean.mse /= n;
+            mean.psnr /= n;
+            mean.ssim /= n;
+        }
+        *out = mean;
     });
 }
 

@@ -111,6 +111,11 @@ void launch_cg_pu(const float* p, const float* u, long long n, double* partial, 
 void launch_cg_update(float* x, float* r, float* z, float* p, const float* u, const float* minv,
                       long long n, double* partial, CgState* s, cudaStream_t st);
 void launch_minv(float* d, long long n, float lambda, cudaStream_t st);
+int metric_tiles(int w, int h, int* tiles_x);
+void launch_image_metrics(const float* a, const float* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                          double2* partial, double2* out, const MetricWindow& win, cudaStream_t st);
+void launch_image_metrics(const double* a, const double* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                          double2* partial, double2* out, const MetricWindow& win, cudaStream_t st);
 void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
 
 }  // namespace slm

@@ -15,8 +15,8 @@ import os
 
 import numpy as np
 
-from .types import (CCamera, CGaussians, CLmConfig, CPcgResult, CPlan, CStepReport, Camera,
-                    GaussianSet, LmConfig, PcgResult, SamplePlan, StepReport, cameras_to_c, f32ptr,
+from .types import (CCamera, CGaussians, CLmConfig, CMetricReport, CPcgResult, CPlan, CStepReport, Camera,
+                    GaussianSet, LmConfig, MetricReport, PcgResult, SamplePlan, StepReport, cameras_to_c, f32ptr,
                     f64ptr, i32ptr, i64ptr)
 
 LIB_PATH = os.environ.get("SLM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslm_b200.so")
@@ -114,6 +114,8 @@ _SIGS = {
     "slm_lm_step_host": (C.c_int, [_vp, C.POINTER(CGaussians), _vp, C.POINTER(CLmConfig), C.c_int,
                                    _vp, C.POINTER(CStepReport)]),
     "slm_batch_loss": (C.c_int, [_vp, _vp, _i32p, C.c_int, _f64p]),
+    "slm_evaluate": (C.c_int, [_vp, _f64p, _f64p, C.c_int, C.c_int, C.POINTER(CMetricReport)]),
+    "slm_evaluate_split": (C.c_int, [_vp, _vp, C.POINTER(CMetricReport)]),
     "slm_random_init": (C.c_int, [C.c_int, _f64p, _f64p, _vp, C.POINTER(CGaussians)]),
     "slm_ring_camera": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                   C.POINTER(CCamera)]),
@@ -445,6 +447,21 @@ class Lib(HostSampler):
     def batch_loss(self, g: GaussianSet, data: "TrainData", cam_ids) -> float:
         return Scene(self, g).batch_loss(data, cam_ids)
 
+    def evaluate(self, rendered, ground_truth) -> MetricReport:
+        """metrics::evaluate (image_metrics.cpp:180-186): mse, psnr, ssim of two H x W x 3
+        images, computed on the device in f64."""
+        a = np.ascontiguousarray(rendered, np.float64)
+        b = np.ascontiguousarray(ground_truth, np.float64)
+        if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+            raise ValueError("metrics: image shapes differ")
+        r = CMetricReport()
+        self._check(self.dll.slm_evaluate(self.ctx, f64ptr(a), f64ptr(b), a.shape[1], a.shape[0],
+                                          C.byref(r)))
+        return MetricReport(r.mse, r.psnr, r.ssim)
+
+    def evaluate_split(self, g: GaussianSet, split: "TrainData") -> MetricReport:
+        return Scene(self, g).evaluate_split(split)
+
 
 def _report(rep: CStepReport, batch) -> StepReport:
     return StepReport(rep.iteration, rep.loss_before, rep.loss_after, rep.eta, rep.pcg_iterations,
@@ -511,6 +528,13 @@ class Scene:
 
     def jacobian(self, cams, plan: SamplePlan) -> "Jacobian":
         return Jacobian(self.L, None, cams, plan, scene=self)
+
+    def evaluate_split(self, split: "TrainData") -> MetricReport:
+        """io::evaluate_split (run.cpp:77-92): mean mse / psnr / ssim over the split's cameras,
+        rendered and scored on the device."""
+        r = CMetricReport()
+        self.L._check(self.L.dll.slm_evaluate_split(self.h, split.h, C.byref(r)))
+        return MetricReport(r.mse, r.psnr, r.ssim)
 
 
 class Jacobian:

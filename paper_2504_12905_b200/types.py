@@ -64,6 +64,10 @@ class CStepReport(C.Structure):
                 ("batch_capacity", C.c_int32)]
 
 
+class CMetricReport(C.Structure):
+    _fields_ = [("mse", C.c_double), ("psnr", C.c_double), ("ssim", C.c_double)]
+
+
 class CPcgResult(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("breakdown", C.c_int32),
                 ("rel_residual", C.c_double)]
@@ -337,6 +341,14 @@ class StepReport:
     pcg_iterations: int = 0
     breakdown: bool = False
     batch: list = field(default_factory=list)
+
+
+@dataclass
+class MetricReport:
+    """metrics::MetricReport (image_metrics.hpp:7-11)."""
+    mse: float = 0.0
+    psnr: float = 0.0
+    ssim: float = 0.0
 
 
 @dataclass

@@ -11,6 +11,8 @@
 #include "splatlm/io/dataset.hpp"
 #include "splatlm/io/image_io.hpp"
 #include "splatlm/io/scene_gen.hpp"
+#include "splatlm/metrics/image_metrics.hpp"
+#include "splatlm/render/rasterizer.hpp"
 #include "splatlm_b200.hpp"
 
 using namespace splatlm;
@@ -63,7 +65,25 @@ int main() {
         num += (ga[i] - gb[i]) * (ga[i] - gb[i]);
         den += ga[i] * ga[i];
     }
-    std::printf("{\"batches_equal\": %s, \"rng_equal\": %s, \"worst_loss_rel\": %.3e, \"gn_apply_rel\": %.3e}\n",
-                batches_equal ? "true" : "false", rng_equal ? "true" : "false", worst, std::sqrt(num / den));
+    // io::evaluate_split (run.cpp:77-92) as the run driver computes it, vs the adapter
+    metrics::MetricReport er;
+    for (size_t i = 0; i < scene.test.cameras.size(); ++i) {
+        const auto r = metrics::evaluate(render::render_full(ref, scene.test.cameras[i]).image,
+                                         io::widen(scene.test.images[i]));
+        er.mse += r.mse / scene.test.cameras.size();
+        er.psnr += r.psnr / scene.test.cameras.size();
+        er.ssim += r.ssim / scene.test.cameras.size();
+    }
+    const auto eb = splatlm_b200::evaluate_split(dev, ref, scene.test);
+    // metrics::evaluate on two f64 images
+    const Image ia = render::render_full(ref, scene.test.cameras[0]).image;
+    const Image ib = io::widen(scene.test.images[0]);
+    const auto ma = metrics::evaluate(ia, ib), mb = splatlm_b200::evaluate(dev, ia, ib);
+    std::printf("{\"batches_equal\": %s, \"rng_equal\": %s, \"worst_loss_rel\": %.3e, \"gn_apply_rel\": %.3e, "
+                "\"split_psnr_diff\": %.3e, \"split_ssim_diff\": %.3e, \"eval_ssim_diff\": %.3e, "
+                "\"eval_mse_rel\": %.3e}\n",
+                batches_equal ? "true" : "false", rng_equal ? "true" : "false", worst, std::sqrt(num / den),
+                std::abs(er.psnr - eb.psnr), std::abs(er.ssim - eb.ssim), std::abs(ma.ssim - mb.ssim),
+                std::abs(ma.mse - mb.mse) / ma.mse);
     return 0;
 }

@@ -181,11 +181,38 @@ def lm_cases(R):
     return out
 
 
+def metrics_cases(R):
+    """metrics::mse / psnr / ssim (image_metrics.cpp:108-139) on seeded image pairs, and the
+    per-camera evaluate of the toy LM run's final state on its test split (run.cpp:77-92)."""
+    out = {}
+    rng = np.random.default_rng(2504)
+    shapes = [(6, 6), (17, 33), (40, 24), (64, 64), (7, 90)]
+    for i, (h, w) in enumerate(shapes):
+        a = rng.random((h, w, 3))
+        b = np.clip(a + rng.normal(0.0, 0.05 * (i + 1), a.shape), 0.0, 1.0)
+        out[f"m{i}_a"], out[f"m{i}_b"] = a, b
+        out[f"m{i}_ref"] = np.array([R.mse(a, b), R.psnr(a, b), R.ssim(a, b)])
+        out[f"m{i}_self"] = np.array([R.mse(a, a), R.psnr(a, a), R.ssim(a, a)])
+    d = np.load(os.path.join(HERE, "lm.npz"))
+    from support import g_cams, g_set
+    st = g_set(d, "lm_final")
+    rows = []
+    for cam, img in zip(g_cams(d["toy_test_cams"]), d["toy_test_imgs"]):
+        ren, _, _ = R.render_full(st, cam)
+        gt = np.asarray(img, np.float64)
+        rows.append([R.mse(ren, gt), R.psnr(ren, gt), R.ssim(ren, gt)])
+    out["split_metrics"] = np.array(rows)
+    return out
+
+
 def main():
     R = ref()
     groups = {"render": render_cases, "sampling": sampling_cases, "jacobian": jacobian_cases,
-              "lm": lm_cases}
+              "lm": lm_cases, "metrics": metrics_cases}
+    only = sys.argv[1:]  # optional group names: regenerate just those
     for name, fn in groups.items():
+        if only and name not in only:
+            continue
         arrs = fn(R)
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **arrs)

@@ -366,6 +366,8 @@ def test_cpp_adapter_drop_in(gpu):
     print(r)
     assert r["batches_equal"] and r["rng_equal"]
     assert r["worst_loss_rel"] < TOL and r["gn_apply_rel"] < TOL
+    assert r["split_psnr_diff"] < 1e-3 and r["split_ssim_diff"] < 1e-5
+    assert r["eval_ssim_diff"] <= 1e-12 and r["eval_mse_rel"] <= 1e-12
 
 
 @pytest.mark.gpu
@@ -389,9 +391,12 @@ def test_cfg0_psnr_curve_matches_reference(gpu):
     scene = splatlm.Scene(L, L.random_init(c["gaussians"], [-1, -1, -1], [1, 1, 1], rng))
     cfg = LmConfig(pcg_iters_initial=c["pcg"], pcg_iters_late=c["pcg"], batch_size_initial=c["batch"],
                    batch_size_late=c["batch"], samples_per_tile=c["spt"])
+    sd = L.train_data(test, simgs)
     for it, (rp, rl) in enumerate(zip(ref["psnr"], ref["loss_after"])):
         rep = scene.lm_step(td, cfg, it, rng)
         p = np.mean([bench.psnr(scene.render(cam)[0], im) for cam, im in zip(test, simgs)])
+        ev = scene.evaluate_split(sd)  # device evaluate_split agrees with the host PSNR
+        assert abs(ev.psnr - p) <= 1e-6
         assert abs(p - rp) <= 0.05, f"iteration {it}: PSNR {p:.4f} vs reference {rp:.4f}"
         assert abs(rep.loss_after - rl) <= 1e-3 * rl, f"iteration {it}: loss {rep.loss_after} vs {rl}"
 
@@ -418,3 +423,49 @@ def test_tile_lists_bit_exact_near_equal_depths(gpu, spread):
     off, idx = gpu.bin_and_sort(g, cam)
     assert np.array_equal(off, o_off)
     assert np.array_equal(idx, o_idx)
+
+
+# ----------------------------------------------------------------- metrics
+@pytest.mark.parametrize("i", range(5))
+def test_evaluate_matches_reference(gpu, i):
+    """metrics::evaluate on the device (metrics.cu) vs the reference's own mse / psnr /
+    ssim (tests/golden/metrics.npz).  Every filtered moment and local SSIM value is
+    computed in the reference's f64 operation order; only the pixel sums are ordered
+    differently, hence 1e-12."""
+    d = golden("metrics")
+    a, b = d[f"m{i}_a"], d[f"m{i}_b"]
+    mse, psnr, ssim = d[f"m{i}_ref"]
+    r = gpu.evaluate(a, b)
+    assert abs(r.ssim - ssim) <= 1e-12
+    assert r.mse == pytest.approx(mse, rel=1e-12)
+    assert r.psnr == pytest.approx(psnr, rel=1e-12)
+    s = gpu.evaluate(a, a)
+    assert (s.mse, s.psnr, s.ssim) == tuple(d[f"m{i}_self"])
+
+
+def test_evaluate_full_size_matches_oracle(gpu, port):
+    """A 1280x720 pair (configs[2] view size; tile edges not multiples of 32) vs the C
+    restatement, which is bitwise equal to the reference's ssim."""
+    rng = np.random.default_rng(3)
+    a = rng.random((720, 1280, 3))
+    b = np.clip(a + rng.normal(0, 0.03, a.shape), 0, 1)
+    r = gpu.evaluate(a, b)
+    assert abs(r.ssim - port.ssim(a, b)) <= 1e-12
+    assert r.mse == pytest.approx(port.mse(a, b), rel=1e-12)
+    with pytest.raises(Exception):
+        gpu.evaluate(a, b[:10])
+
+
+def test_evaluate_split_matches_reference(gpu):
+    """io::evaluate_split (run.cpp:77-92) of the toy LM run's final state on its 4 test
+    views: device renders (f32) + device metrics vs the reference's f64 render_full +
+    evaluate.  The render is f32, so the bars are 1e-3 dB PSNR and 1e-5 SSIM."""
+    d = golden("lm")
+    g = g_set(d, "lm_final")
+    split = gpu.train_data(g_cams(d["toy_test_cams"]), list(d["toy_test_imgs"]))
+    ref = golden("metrics")["split_metrics"].mean(axis=0)
+    r = gpu.evaluate_split(g, split)
+    print(r, ref)
+    assert r.mse == pytest.approx(ref[0], rel=1e-4)
+    assert abs(r.psnr - ref[1]) <= 1e-3
+    assert abs(r.ssim - ref[2]) <= 1e-5

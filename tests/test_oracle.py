@@ -194,3 +194,25 @@ def test_live_reference_cross_check(port, reflib):
     p = np.random.default_rng(0).uniform(-1, 1, ja.param_dim())
     assert np.array_equal(ja.gn_apply(0.1, p), jb.gn_apply(0.1, p))
     assert np.array_equal(ja.jtj_diag(), jb.jtj_diag())
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_image_metrics_known_answers(port, i):
+    """metrics::mse / psnr / ssim (image_metrics.cpp:108-139) on the reference's own
+    outputs (tests/golden/metrics.npz): the SSIM restatement keeps the reference's
+    operation order (bitwise); the MSE sum order differs from the AVX2 kernel (1e-12)."""
+    d = golden("metrics")
+    a, b = d[f"m{i}_a"], d[f"m{i}_b"]
+    mse, psnr, ssim = d[f"m{i}_ref"]
+    assert port.ssim(a, b) == ssim
+    assert port.mse(a, b) == pytest.approx(mse, rel=1e-12)
+    assert port.psnr(a, b) == pytest.approx(psnr, rel=1e-12)
+    assert [port.mse(a, a), port.psnr(a, a), port.ssim(a, a)] == list(d[f"m{i}_self"])
+
+
+def test_ssim_live_reference(port, reflib):
+    rng = np.random.default_rng(9)
+    for h, w in [(6, 11), (33, 20), (128, 96)]:
+        a = rng.random((h, w, 3))
+        b = np.clip(a + rng.normal(0, 0.1, a.shape), 0, 1)
+        assert port.ssim(a, b) == reflib.ssim(a, b)
