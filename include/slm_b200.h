@@ -155,11 +155,18 @@ int slm_lm_step_host(slm_context* ctx, slm_gaussians* state, slm_train* t,
                      slm_step_report* report);
 /* batch_loss (lm.cpp:39-54), MSE; cameras index the TrainData. */
 int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cams, int n, double* out);
+/* batch_loss with the loss kind (SLM_LOSS_MSE / SLM_LOSS_MSE_SSIM) and SSIM weight. */
+int slm_batch_loss_kind(slm_scene* s, slm_train* t, const int32_t* cams, int n, int loss, double ssim_weight,
+                        double* out);
 
 /* ---- metrics (metrics/image_metrics.hpp, io/run.cpp:77-92), computed on the device */
 /* metrics::evaluate (image_metrics.cpp:180-186) on two interleaved-RGB f64 images. */
 int slm_evaluate(slm_context* ctx, const double* rendered, const double* ground_truth, int width,
                  int height, slm_metric_report* out);
+/* metrics::ssim_diag_residuals (image_metrics.cpp:141-178): per pixel and channel
+ * s = sqrt(max(0, 1 - local SSIM)) and ds/d(centre pixel of a); H*W*3 f64 each. */
+int slm_ssim_diag_residuals(slm_context* ctx, const double* a, const double* b, int width, int height,
+                            double* residual, double* d_center);
 /* io::evaluate_split: render every camera of the split (TrainData images are
  * the ground truth) and average mse / psnr / ssim over the cameras. */
 int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out);

@@ -94,10 +94,11 @@ class CpuLib:
             "lm_step": (C.c_int, [C.POINTER(CGaussians), _vp, C.POINTER(CLmConfig), C.c_int, _vp,
                                   C.POINTER(CStepReport)]),
             "batch_loss": (C.c_int, [C.POINTER(CGaussians), C.POINTER(CCamera), C.c_int,
-                                     C.POINTER(C.c_float), _f64p]),
+                                     C.POINTER(C.c_float), C.c_int, C.c_double, _f64p]),
             "mse": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
             "psnr": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
             "ssim": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
+            "ssim_diag_residuals": (None, [_f64p, _f64p, C.c_int, C.c_int, _f64p, _f64p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(self.lib, prefix + name)
@@ -285,12 +286,12 @@ class CpuLib:
         return StepReport(rep.iteration, rep.loss_before, rep.loss_after, rep.eta,
                           rep.pcg_iterations, bool(rep.breakdown), list(batch[:rep.batch_size]))
 
-    def batch_loss(self, g: GaussianSet, cams, gts_f32) -> float:
+    def batch_loss(self, g: GaussianSet, cams, gts_f32, loss: int = 0, ssim_weight: float = 0.0) -> float:
         gts = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float32).reshape(-1) for x in gts_f32]))
         out = C.c_double()
         cg = g.to_c()
         self._check(self._batch_loss(C.byref(cg), cameras_to_c(cams), len(cams), f32ptr(gts),
-                                     C.byref(out)))
+                                     loss, ssim_weight, C.byref(out)))
         return out.value
 
     def mse(self, a, b) -> float:
@@ -307,6 +308,14 @@ class CpuLib:
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
         return self._ssim(f64ptr(a), f64ptr(b), a.shape[1], a.shape[0])
+
+    def ssim_diag_residuals(self, a, b):
+        """metrics::ssim_diag_residuals -> (residual, d_center), both H x W x 3."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        r, d = np.zeros_like(a), np.zeros_like(a)
+        self._ssim_diag_residuals(f64ptr(a), f64ptr(b), a.shape[1], a.shape[0], f64ptr(r), f64ptr(d))
+        return r, d
 
 
 class Rng:

@@ -560,7 +560,7 @@ int ref_lm_step(slm_gaussians* g, void* t, const slm_lm_config* cfg, int iterati
 
 // solver::batch_loss (lm.cpp:39-54); gts are float32 dataset buffers
 int ref_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n_cams, const float* gts,
-                   double* out) {
+                   int loss, double ssim_weight, double* out) {
     return guarded([&] {
         const auto cv = to_cams(cams, n_cams);
         std::vector<Image> imgs;
@@ -571,7 +571,7 @@ int ref_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n_cams, c
             src += img.data.size();
             imgs.push_back(std::move(img));
         }
-        *out = solver::batch_loss(to_set(*g), cv, imgs, solver::LossKind::kMse, 0.0);
+        *out = solver::batch_loss(to_set(*g), cv, imgs, static_cast<solver::LossKind>(loss), ssim_weight);
     });
 }
 
@@ -593,6 +593,15 @@ double ref_ssim(const double* a, const double* b, int w, int h) {
     std::copy(a, a + ia.data.size(), ia.data.begin());
     std::copy(b, b + ib.data.size(), ib.data.begin());
     return metrics::ssim(ia, ib);
+}
+void ref_ssim_diag_residuals(const double* a, const double* b, int w, int h, double* residual,
+                             double* d_center) {
+    Image ia(w, h), ib(w, h);
+    std::copy(a, a + ia.data.size(), ia.data.begin());
+    std::copy(b, b + ib.data.size(), ib.data.begin());
+    const auto r = metrics::ssim_diag_residuals(ia, ib);
+    std::copy(r.residual.data.begin(), r.residual.data.end(), residual);
+    std::copy(r.d_center.data.begin(), r.d_center.data.end(), d_center);
 }
 
 }  // extern "C"

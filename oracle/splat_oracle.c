@@ -1677,9 +1677,82 @@ double orc_ssim(const double* a, const double* b, int w, int h) {
     return total / (3.0 * (double)n);
 }
 
-/* batch_loss, MSE only (lm.cpp:39-54) */
+/* effective_center_weights (image_metrics.cpp:69-78) */
+static void ssim_center_weights(const double* win, int n, double* out) {
+    for (int i = 0; i < n; ++i) {
+        out[i] = 0.0;
+        for (int k = -SSIM_HALF; k <= SSIM_HALF; ++k)
+            if (ssim_reflect(i + k, n) == i) out[i] += win[k + SSIM_HALF];
+    }
+}
+
+/* metrics::ssim_diag_residuals (image_metrics.cpp:141-178): per pixel and
+ * channel s = sqrt(max(0, 1 - local SSIM)) and the derivative of s with
+ * respect to the centre pixel of a (diagonal approximation). */
+void orc_ssim_diag_residuals(const double* a, const double* b, int w, int h, double* residual,
+                             double* d_center) {
+    const size_t n = (size_t)w * h;
+    double win[SSIM_WIN];
+    ssim_window(win);
+    double* wx = (double*)malloc(sizeof(double) * (w + 1));
+    double* wy = (double*)malloc(sizeof(double) * (h + 1));
+    ssim_center_weights(win, w, wx);
+    ssim_center_weights(win, h, wy);
+    double* buf = (double*)malloc(sizeof(double) * (n * 9 + 1));
+    double *pa = buf, *pb = buf + n, *sq = buf + 2 * n, *tmp = buf + 3 * n, *ma = buf + 4 * n,
+           *mb = buf + 5 * n, *eaa = buf + 6 * n, *ebb = buf + 7 * n, *eab = buf + 8 * n;
+    const double c1 = 0.01 * 0.01, c2 = 0.03 * 0.03;
+    for (size_t i = 0; i < 3 * n; ++i) residual[i] = d_center[i] = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        for (size_t i = 0; i < n; ++i) {
+            pa[i] = a[3 * i + c];
+            pb[i] = b[3 * i + c];
+        }
+        ssim_filter(win, pa, w, h, tmp, ma);
+        ssim_filter(win, pb, w, h, tmp, mb);
+        for (size_t i = 0; i < n; ++i) sq[i] = pa[i] * pa[i];
+        ssim_filter(win, sq, w, h, tmp, eaa);
+        for (size_t i = 0; i < n; ++i) sq[i] = pb[i] * pb[i];
+        ssim_filter(win, sq, w, h, tmp, ebb);
+        for (size_t i = 0; i < n; ++i) sq[i] = pa[i] * pb[i];
+        ssim_filter(win, sq, w, h, tmp, eab);
+        for (size_t i = 0; i < n; ++i) {
+            const double mua = ma[i], mub = mb[i];
+            const double va = eaa[i] - mua * mua, vb = ebb[i] - mub * mub;
+            const double cov = eab[i] - mua * mub;
+            const double a1 = 2.0 * mua * mub + c1, a2 = 2.0 * cov + c2;
+            const double b1 = mua * mua + mub * mub + c1, b2 = va + vb + c2;
+            const double local = (a1 * a2) / (b1 * b2);
+            const double sval = sqrt(1.0 - local > 0.0 ? 1.0 - local : 0.0);
+            residual[3 * i + c] = sval;
+            if (sval < 1e-12) continue;
+            const double av = a[3 * i + c], bv = b[3 * i + c];
+            const double wc = wx[i % w] * wy[i / w];
+            const double dnum = mub * a2 + a1 * (bv - mub);
+            const double dden = mua * b2 + b1 * (av - mua);
+            const double dlocal = 2.0 * wc * (dnum * b1 * b2 - a1 * a2 * dden) / (b1 * b2 * b1 * b2);
+            d_center[3 * i + c] = -dlocal / (2.0 * sval);
+        }
+    }
+    free(buf);
+    free(wx);
+    free(wy);
+}
+
+/* the mse+ssim loss term of one image (lm.cpp:44-49, 143-147): w * sum(s^2) / (3n) */
+static double ssim_loss_term(const double* img, const double* gt, int w, int h, double weight) {
+    const size_t n3 = 3 * (size_t)w * h;
+    double* r = (double*)malloc(sizeof(double) * (2 * n3 + 1));
+    orc_ssim_diag_residuals(img, gt, w, h, r, r + n3);
+    double ssq = 0.0;
+    for (size_t i = 0; i < n3; ++i) ssq += r[i] * r[i];
+    free(r);
+    return weight * ssq / (double)n3;
+}
+
+/* batch_loss (lm.cpp:39-54) */
 static int batch_loss_d(const slm_gaussians* g, const slm_camera* cams, const int* batch, int nb,
-                        double* const* gts, double* out) {
+                        double* const* gts, int loss, double ssim_weight, double* out) {
     double acc = 0.0;
     for (int i = 0; i < nb; ++i) {
         const slm_camera* cam = &cams[batch[i]];
@@ -1690,7 +1763,9 @@ static int batch_loss_d(const slm_gaussians* g, const slm_camera* cams, const in
             free(img);
             return rc;
         }
-        acc += orc_mse(img, gts[i], cam->width, cam->height);
+        double term = orc_mse(img, gts[i], cam->width, cam->height);
+        if (loss == SLM_LOSS_MSE_SSIM) term += ssim_loss_term(img, gts[i], cam->width, cam->height, ssim_weight);
+        acc += term;
         free(img);
     }
     *out = nb == 0 ? 0.0 : acc / (double)nb;
@@ -1698,7 +1773,7 @@ static int batch_loss_d(const slm_gaussians* g, const slm_camera* cams, const in
 }
 
 int orc_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n, const float* gts,
-                   double* out) {
+                   int loss, double ssim_weight, double* out) {
     double** imgs = (double**)calloc(n + 1, sizeof(double*));
     int* batch = (int*)malloc(sizeof(int) * (n + 1));
     const float* src = gts;
@@ -1709,20 +1784,21 @@ int orc_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n, const 
         src += sz;
         batch[i] = i;
     }
-    const int rc = batch_loss_d(g, cams, batch, n, imgs, out);
+    const int rc = batch_loss_d(g, cams, batch, n, imgs, loss, ssim_weight, out);
     for (int i = 0; i < n; ++i) free(imgs[i]);
     free(imgs);
     free(batch);
     return rc;
 }
 
-/* lm_step (lm.cpp:56-157), MSE loss only (the mse+ssim fold-in is out of scope) */
+/* lm_step (lm.cpp:56-157), both losses: with mse+ssim the diagonal SSIM rows
+ * fold into the rhs and per-channel weights (lm.cpp:86-119) */
 int orc_lm_step(slm_gaussians* g, void* tp, const slm_lm_config* cfg, int iteration, void* rngp,
                 slm_step_report* rep) {
     train_t* t = (train_t*)tp;
     rng64* rng = (rng64*)rngp;
     if (t->k < 1) return set_err(E_INVALID, "lm_step: no view clusters");
-    if (cfg->loss != SLM_LOSS_MSE) return set_err(E_INVALID, "oracle: mse+ssim loss not restated");
+    const int ssim = cfg->loss == SLM_LOSS_MSE_SSIM;
     rep->iteration = iteration;
     /* 1. one camera per cluster (sample_view_batch, view_sampler.cpp:173-184) */
     const int nb = t->k;
@@ -1765,17 +1841,42 @@ int orc_lm_step(slm_gaussians* g, void* tp, const slm_lm_config* cfg, int iterat
                    plan->view_offset, plan->px, plan->py, plan->tile, plan->weight};
     jac_t* jac = (jac_t*)orc_jac_new(g, cams, nb, &cp);
     if (!jac) return E_DOMAIN;
-    /* rhs = -w r (lm.cpp:99-118) */
+    /* rhs = -w (r + ssim_weight sp sv), weights w (1 + ssim_weight sp^2) (lm.cpp:86-119) */
+    double** sres = (double**)calloc(nb + 1, sizeof(double*));
+    double* sterm = (double*)calloc(nb + 1, sizeof(double));
+    if (ssim)
+        for (int v = 0; v < nb; ++v) {
+            const size_t n3 = 3 * (size_t)cams[v].width * cams[v].height;
+            sres[v] = (double*)malloc(sizeof(double) * (2 * n3 + 1));
+            orc_ssim_diag_residuals(renders[v], gts[v], cams[v].width, cams[v].height, sres[v], sres[v] + n3);
+            double ssq = 0.0;
+            for (size_t i = 0; i < n3; ++i) ssq += sres[v][i] * sres[v][i];
+            sterm[v] = cfg->ssim_weight * ssq / (double)n3;
+        }
     double* rhs = (double*)malloc(sizeof(double) * (jac->rdim + 1));
+    double* w2 = (double*)malloc(sizeof(double) * (jac->rdim + 1));
     for (int v = 0; v < plan->n_views; ++v) {
         const int w = cams[v].width;
+        const size_t n3 = 3 * (size_t)w * cams[v].height;
         for (int64_t s = plan->view_offset[v]; s < plan->view_offset[v + 1]; ++s)
             for (int c = 0; c < 3; ++c) {
                 const size_t e = ((size_t)plan->py[s] * w + plan->px[s]) * 3 + c;
                 const double r = renders[v][e] - gts[v][e];
-                rhs[3 * s + c] = -jac->weights[3 * s + c] * r;
+                const double bw = jac->weights[3 * s + c];
+                double u = r;
+                w2[3 * s + c] = bw;
+                if (ssim) {
+                    const double sv = sres[v][e], sp = sres[v][n3 + e];
+                    u += cfg->ssim_weight * sp * sv;
+                    w2[3 * s + c] = bw * (1.0 + cfg->ssim_weight * sp * sp);
+                }
+                rhs[3 * s + c] = -bw * u;
             }
     }
+    if (ssim) orc_jac_set_weights(jac, w2);
+    free(w2);
+    for (int v = 0; v < nb; ++v) free(sres[v]);
+    free(sres);
     const size_t P = (size_t)jac->pdim;
     double* b = (double*)malloc(sizeof(double) * (P + 1));
     double* minv = (double*)malloc(sizeof(double) * (P + 1));
@@ -1793,10 +1894,13 @@ int orc_lm_step(slm_gaussians* g, void* tp, const slm_lm_config* cfg, int iterat
     orc_apply_update(g, x, rep->eta);
     double before = 0.0;
     for (int i = 0; i < nb; ++i) before += orc_mse(renders[i], gts[i], cams[i].width, cams[i].height);
+    if (ssim)
+        for (int i = 0; i < nb; ++i) before += sterm[i];
+    free(sterm);
     rep->loss_before = before / (double)nb;
     int* idx = (int*)malloc(sizeof(int) * nb);
     for (int i = 0; i < nb; ++i) idx[i] = i;
-    const int rc = batch_loss_d(g, cams, idx, nb, gts, &rep->loss_after);
+    const int rc = batch_loss_d(g, cams, idx, nb, gts, cfg->loss, cfg->ssim_weight, &rep->loss_after);
     free(idx);
     rep->batch_size = nb;
     for (int i = 0; i < nb && i < rep->batch_capacity; ++i) rep->batch[i] = batch[i];

@@ -81,10 +81,12 @@ int orc_train_set_clusters(void* t, const int32_t* assign, int n_cams, int k);
 int orc_lm_step(slm_gaussians* g, void* t, const slm_lm_config* cfg, int iteration, void* rng,
                 slm_step_report* report);
 int orc_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n_cams, const float* gts,
-                   double* out);
+                   int loss, double ssim_weight, double* out);
 double orc_mse(const double* a, const double* b, int w, int h);
 double orc_psnr(const double* a, const double* b, int w, int h);
 double orc_ssim(const double* a, const double* b, int w, int h);
+void orc_ssim_diag_residuals(const double* a, const double* b, int w, int h, double* residual,
+                             double* d_center);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,13 @@
 // Window weights are computed on the host with the reference's formula
 // (gaussian_window, :25-35) and passed by value.
 //
+// The same kernel in diag mode is metrics::ssim_diag_residuals (:141-178):
+// per pixel and channel s = sqrt(max(0, 1 - local SSIM)) and its derivative
+// with respect to the centre pixel (diagonal approximation, effective centre
+// weights :69-78), written as planes, with sum(s^2) per image for the
+// mse+ssim loss.  k_ssim_fold then folds the diagonal SSIM rows into the
+// sampled rhs and per-channel weights of lm_step (lm.cpp:86-119).
+//
 // The work is tiny next to the LM step (about 250 f64 flops and 2 input reads
 // per pixel and channel); it exists so evaluation of a test split needs no
 // image download.
@@ -44,14 +51,32 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {
     return min(max(i, 0), n - 1);
 }
 
+// effective_center_weights (image_metrics.cpp:69-78): the window weight a
+// pixel contributes to its own window, reflect padding included (the
+// unclamped reflection: only compared, never dereferenced).
+__device__ __forceinline__ double center_weight(int i, int n, const MetricWindow& win) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = -kHalf; k <= kHalf; ++k) {
+        int j = i + k;
+        if (j < 0) j = -j - 1;
+        if (j >= n) j = 2 * n - j - 1;
+        if (j == i) s = __dadd_rn(s, win.w[k + kHalf]);
+    }
+    return s;
+}
+
 __device__ __forceinline__ double fma_free(double acc, double w, double v) {
     return __dadd_rn(acc, __dmul_rn(w, v));
 }
 
-template <typename T>
+// DIAG = false: partial = {sse, sum of local SSIM}; DIAG = true: partial =
+// {sse, sum of s^2} and, when res/dcen are given, the residual planes.
+template <typename T, typename O, bool DIAG>
 __global__ void __launch_bounds__(kMetricThreads)
 k_image_metrics(const T* __restrict__ a, const T* __restrict__ b, const ImgDesc* __restrict__ imgs,
-                double2* __restrict__ partial, const MetricWindow win) {
+                double2* __restrict__ partial, const MetricWindow win, O* __restrict__ res,
+                O* __restrict__ dcen) {
     extern __shared__ double sm[];
     double* sa = sm;                   // [kMH][kMH]
     double* sb = sa + kMH * kMH;       // [kMH][kMH]
@@ -115,15 +140,37 @@ k_image_metrics(const T* __restrict__ a, const T* __restrict__ b, const ImgDesc*
             const double var_a = __dsub_rn(e_aa, __dmul_rn(mu_a, mu_a));
             const double var_b = __dsub_rn(e_bb, __dmul_rn(mu_b, mu_b));
             const double cov = __dsub_rn(e_ab, __dmul_rn(mu_a, mu_b));
-            const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, mu_a), mu_b), kC1),
-                                         __dadd_rn(__dmul_rn(2.0, cov), kC2));
-            const double den =
-                __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(mu_a, mu_a), __dmul_rn(mu_b, mu_b)), kC1),
-                          __dadd_rn(__dadd_rn(var_a, var_b), kC2));
-            ssim += __ddiv_rn(num, den);
+            const double a1 = __dadd_rn(__dmul_rn(__dmul_rn(2.0, mu_a), mu_b), kC1);
+            const double a2 = __dadd_rn(__dmul_rn(2.0, cov), kC2);
+            const double b1 = __dadd_rn(__dadd_rn(__dmul_rn(mu_a, mu_a), __dmul_rn(mu_b, mu_b)), kC1);
+            const double b2 = __dadd_rn(__dadd_rn(var_a, var_b), kC2);
+            const double local = __ddiv_rn(__dmul_rn(a1, a2), __dmul_rn(b1, b2));
             const int ctr = (r + kHalf) * kMH + q + kHalf;
-            const double e = sa[ctr] - sb[ctr];
+            const double av = sa[ctr], bv = sb[ctr];
+            const double e = av - bv;
             sse += e * e;
+            if (!DIAG) {
+                ssim += local;
+                continue;
+            }
+            // ssim_diag_residuals (:158-175)
+            const double om = __dsub_rn(1.0, local);
+            const double sval = __dsqrt_rn(0.0 < om ? om : 0.0);
+            ssim += sval * sval;
+            if (res == nullptr) continue;
+            double dc = 0.0;
+            if (!(sval < 1e-12)) {
+                const double wc = __dmul_rn(center_weight(x0 + q, d.w, win), center_weight(y0 + r, d.h, win));
+                const double dnum = __dadd_rn(__dmul_rn(mu_b, a2), __dmul_rn(a1, __dsub_rn(bv, mu_b)));
+                const double dden = __dadd_rn(__dmul_rn(mu_a, b2), __dmul_rn(b1, __dsub_rn(av, mu_a)));
+                const double t = __dsub_rn(__dmul_rn(__dmul_rn(dnum, b1), b2), __dmul_rn(__dmul_rn(a1, a2), dden));
+                const double dlocal = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, wc), t),
+                                                __dmul_rn(__dmul_rn(__dmul_rn(b1, b2), b1), b2));
+                dc = __ddiv_rn(-dlocal, __dmul_rn(2.0, sval));
+            }
+            const long long o = d.off + 3 * (static_cast<long long>(y0 + r) * d.w + x0 + q) + c;
+            res[o] = static_cast<O>(sval);
+            dcen[o] = static_cast<O>(dc);
         }
         __syncthreads();
     }
@@ -174,18 +221,46 @@ k_metrics_reduce(const ImgDesc* __restrict__ imgs, const double2* __restrict__ p
     }
 }
 
-template <typename T>
+template <typename T, typename O, bool DIAG>
 void launch_metrics_impl(const T* a, const T* b, const ImgDesc* imgs, int n_img, int max_tiles,
-                         double2* partial, double2* out, const MetricWindow& win, cudaStream_t st) {
+                         double2* partial, double2* out, const MetricWindow& win, O* res, O* dcen,
+                         cudaStream_t st) {
     if (n_img == 0) return;
     if (max_tiles > 0) {
-        cudaFuncSetAttribute(k_image_metrics<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kMetricSmem));
-        k_image_metrics<T><<<dim3(max_tiles, n_img), kMetricThreads, kMetricSmem, st>>>(a, b, imgs, partial, win);
+        auto* k = k_image_metrics<T, O, DIAG>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMetricSmem));
+        k<<<dim3(max_tiles, n_img), kMetricThreads, kMetricSmem, st>>>(a, b, imgs, partial, win, res, dcen);
         ++g_launches;
     }
     k_metrics_reduce<<<n_img, kMetricThreads, 0, st>>>(imgs, partial, out);
     ++g_launches;
+}
+
+// lm.cpp:99-119 on the device, one thread per sample (group order): the rhs
+// u = -w (r + ssim_weight sp sv) in plan order for the J^T pass, then the
+// per-channel weights w (1 + ssim_weight sp^2) in place for diag / products.
+__global__ void k_ssim_fold(const Group* __restrict__ groups, int n_groups, const DevCam* __restrict__ cams,
+                            const int* __restrict__ spix, const int* __restrict__ sorig, float* __restrict__ sw,
+                            const float* __restrict__ image, const float* __restrict__ gt,
+                            const float* __restrict__ sres, const float* __restrict__ sdc, float ssim_weight,
+                            float* __restrict__ rhs) {
+    const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= n_groups) return;
+    const Group gr = groups[g];
+    if (lane >= gr.count) return;
+    const int k = gr.begin + lane;
+    const DevCam& cam = cams[gr.view];
+    const int p = spix[k];
+    const long long pix = cam.pix_base + static_cast<long long>(p >> 16) * cam.width + (p & 0xffff);
+    const int o = sorig[k];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const long long e = 3 * pix + c;
+        const float w = sw[3 * k + c], sp = sdc[e];
+        rhs[3 * o + c] = -w * ((image[e] - gt[e]) + ssim_weight * sp * sres[e]);
+        sw[3 * k + c] = w * (1.0f + ssim_weight * sp * sp);
+    }
 }
 
 }  // namespace
@@ -197,12 +272,34 @@ int metric_tiles(int w, int h, int* tiles_x) {
 
 void launch_image_metrics(const float* a, const float* b, const ImgDesc* imgs, int n_img, int max_tiles,
                           double2* partial, double2* out, const MetricWindow& win, cudaStream_t st) {
-    launch_metrics_impl(a, b, imgs, n_img, max_tiles, partial, out, win, st);
+    launch_metrics_impl<float, float, false>(a, b, imgs, n_img, max_tiles, partial, out, win, nullptr, nullptr, st);
 }
 
 void launch_image_metrics(const double* a, const double* b, const ImgDesc* imgs, int n_img, int max_tiles,
                           double2* partial, double2* out, const MetricWindow& win, cudaStream_t st) {
-    launch_metrics_impl(a, b, imgs, n_img, max_tiles, partial, out, win, st);
+    launch_metrics_impl<double, double, false>(a, b, imgs, n_img, max_tiles, partial, out, win, nullptr, nullptr,
+                                               st);
+}
+
+void launch_ssim_diag(const float* a, const float* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                      double2* partial, double2* out, const MetricWindow& win, float* res, float* dcen,
+                      cudaStream_t st) {
+    launch_metrics_impl<float, float, true>(a, b, imgs, n_img, max_tiles, partial, out, win, res, dcen, st);
+}
+
+void launch_ssim_diag(const double* a, const double* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                      double2* partial, double2* out, const MetricWindow& win, double* res, double* dcen,
+                      cudaStream_t st) {
+    launch_metrics_impl<double, double, true>(a, b, imgs, n_img, max_tiles, partial, out, win, res, dcen, st);
+}
+
+void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, const int* spix, const int* sorig,
+                      float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
+                      float ssim_weight, float* rhs, cudaStream_t st) {
+    if (n_groups == 0) return;
+    k_ssim_fold<<<(n_groups + 3) / 4, 128, 0, st>>>(groups, n_groups, cams, spix, sorig, sw, image, gt, sres, sdc,
+                                                     ssim_weight, rhs);
+    ++g_launches;
 }
 
 }  // namespace slm

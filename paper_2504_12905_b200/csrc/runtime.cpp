@@ -241,6 +241,7 @@ struct Batch {
     DevBuf<float> image, trans, gt;
     DevBuf<int> contrib, last;
     DevBuf<double> sse_tile, sse_view;
+    DevBuf<float> ssim_res, ssim_dc;  // mse+ssim loss: s and ds/dcentre per pixel and channel
     bool rendered = false, has_gt = false;
     std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
     long long max_list = 0;        // longest tile list of the batch
@@ -661,6 +662,22 @@ struct Jacobian {
             ctx->prof_record(ev, 3);
             ctx->prof_events.push_back(ev);
         }
+        ctx->check_launch();
+    }
+
+    // mse+ssim (lm.cpp:86-121): u = -w (r + ssim_weight sp sv) at the samples
+    // from the batch's SSIM planes, then w <- w (1 + ssim_weight sp^2) for the
+    // diag and the products; b = J^T u.
+    void rhs_ssim_dev(float* dout, float ssim_weight) {
+        res_in.ensure(std::max<long long>(rdim, 1));
+        launch_ssim_fold(samples.groups.p, static_cast<int>(samples.hgroups.size()), batch->cams.p, samples.spix.p,
+                         samples.sorig.p, samples.sw.p, batch->image.p, batch->gt.p, batch->ssim_res.p,
+                         batch->ssim_dc.p, ssim_weight, res_in.p, ctx->stream);
+        SampleArgs a = args();
+        a.in_res = res_in.p;
+        launch_sample_raster(kVjp, a, ctx->stream);
+        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+                     inter.p, nullptr, 0.f, dout, nullptr, ctx->stream);
         ctx->check_launch();
     }
 
@@ -1125,13 +1142,90 @@ static StepBuffers& step_buffers(Context* ctx) {
     return *ctx->step;
 }
 
+// ---- metrics (metrics/image_metrics.cpp, io/run.cpp:77-92) on device (metrics.cu)
+static MetricWindow metric_window() {  // gaussian_window (image_metrics.cpp:25-35)
+    MetricWindow w{};
+    double sum = 0.0;
+    for (int i = 0; i < kMetricWin; ++i) {
+        const double d = i - kMetricWin / 2;
+        w.w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
+        sum += w.w[i];
+    }
+    for (double& v : w.w) v /= sum;
+    return w;
+}
+
+struct ImageRef {
+    long long off;  // element offset of the interleaved RGB image
+    int w, h;
+};
+
+// {sum of squared differences, sum of local SSIM} per image, both over the 3 channels.
+// diag: metrics::ssim_diag_residuals mode ({sse, sum of s^2}; planes when res != nullptr).
+template <typename T>
+static std::vector<double2> image_metrics(Context* c, const T* a, const T* b, const std::vector<ImageRef>& imgs,
+                                          bool diag = false, T* res = nullptr, T* dcen = nullptr) {
+    const int n = static_cast<int>(imgs.size());
+    std::vector<ImgDesc> hd(n);
+    int base = 0, max_tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        ImgDesc& d = hd[i];
+        d.off = imgs[i].off;
+        d.w = imgs[i].w;
+        d.h = imgs[i].h;
+        d.tiles = metric_tiles(d.w, d.h, &d.tiles_x);
+        d.tile_base = base;
+        base += d.tiles;
+        max_tiles = std::max(max_tiles, d.tiles);
+    }
+    std::vector<double2> out(n);
+    if (n == 0) return out;
+    DevBuf<ImgDesc> dd;
+    DevBuf<double2> part, dout;
+    dd.ensure(n);
+    part.ensure(std::max(base, 1));
+    dout.ensure(n);
+    SLM_CUDA_CHECK(cudaMemcpyAsync(dd.p, hd.data(), sizeof(ImgDesc) * n, cudaMemcpyHostToDevice, c->stream));
+    if (diag)
+        launch_ssim_diag(a, b, dd.p, n, max_tiles, part.p, dout.p, metric_window(), res, dcen, c->stream);
+    else
+        launch_image_metrics(a, b, dd.p, n, max_tiles, part.p, dout.p, metric_window(), c->stream);
+    c->check_launch();
+    SLM_CUDA_CHECK(cudaMemcpyAsync(out.data(), dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return out;
+}
+
+// metrics::evaluate (image_metrics.cpp:180-186) from the device sums.
+// Per view {sse, sum of s^2} of the batch render vs truth
+// (metrics::ssim_diag_residuals); with planes, B.ssim_res / B.ssim_dc get s and
+// ds/dcentre per pixel and channel.
+static std::vector<double2> batch_ssim(Batch& B, bool planes) {
+    std::vector<ImageRef> imgs;
+    for (int v = 0; v < B.V; ++v) imgs.push_back({3 * B.hcams[v].pix_base, B.hcams[v].width, B.hcams[v].height});
+    if (planes) {
+        B.ssim_res.ensure(3 * std::max<long long>(B.n_pix, 1));
+        B.ssim_dc.ensure(3 * std::max<long long>(B.n_pix, 1));
+    }
+    return image_metrics<float>(B.ctx, B.image.p, B.gt.p, imgs, true, planes ? B.ssim_res.p : nullptr,
+                                planes ? B.ssim_dc.p : nullptr);
+}
+
+static slm_metric_report metric_report(double2 s, int w, int h) {
+    slm_metric_report r{};
+    const double n = static_cast<double>(w) * h;
+    r.mse = n == 0 ? 0.0 : s.x / (3.0 * n);                  // :108-113
+    r.psnr = r.mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / r.mse);  // :115-119
+    r.ssim = n == 0 ? 1.0 : s.y / (3.0 * n);                 // :121-139
+    return r;
+}
 static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration, std::mt19937_64& rng,
                     slm_step_report& rep) {
     Context* ctx = s.ctx;
     ctx->activate();
     if (t.k < 1) throw std::invalid_argument("lm_step: no view clusters");
-    if (cfg.loss != SLM_LOSS_MSE)
-        throw std::invalid_argument("lm_step: only the mse loss is on the B200 path (mse+ssim is out of scope)");
+    if (cfg.loss != SLM_LOSS_MSE && cfg.loss != SLM_LOSS_MSE_SSIM) throw std::invalid_argument("lm_step: unknown loss");
+    const bool ssim = cfg.loss == SLM_LOSS_MSE_SSIM;
     ctx->mark("start");
     rep.iteration = iteration;
     StepBuffers& sb = step_buffers(ctx);
@@ -1231,6 +1325,12 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         for (int v = 0; v < B.V; ++v)
             before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
     }
+    if (ssim) {  // + ssim_weight * mean s^2 per view (lm.cpp:143-147); planes for the rhs fold
+        const auto ss = batch_ssim(B, true);
+        for (int v = 0; v < B.V; ++v)
+            before += cfg.ssim_weight * ss[v].y / (3.0 * my_cams[v].width * my_cams[v].height);
+        ctx->mark("ssim");
+    }
     J.init_device();
     ctx->mark("plan");
     if (cfg.dist == SLM_DIST_UNIFORM) {  // speculate the next step's batch + plan while this one solves
@@ -1273,7 +1373,10 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     float* dd = sb.b.p + P;
     SLM_CUDA_CHECK(cudaMemsetAsync(sb.b.p, 0, 2 * P * sizeof(float), ctx->stream));
     // 5. b = J^T(-W r) and diag(J^T W J) (lm.cpp:121-125)
-    J.rhs_dev(db);
+    if (ssim)
+        J.rhs_ssim_dev(db, static_cast<float>(cfg.ssim_weight));
+    else
+        J.rhs_dev(db);
     ctx->mark("rhs");
     J.diag_dev(dd);
     ctx->allreduce(sb.b.p, 2 * P);
@@ -1301,7 +1404,14 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     double after = 0.0;
     {
         const auto sse = B.view_sse();
-        for (int v = 0; v < B.V; ++v) after += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
+        std::vector<double2> ss;
+        if (ssim) ss = batch_ssim(B, false);
+        for (int v = 0; v < B.V; ++v) {
+            const double n3 = 3.0 * my_cams[v].width * my_cams[v].height;
+            double term = sse[v] / n3;
+            if (ssim) term += cfg.ssim_weight * ss[v].y / n3;  // batch_loss (lm.cpp:44-50)
+            after += term;
+        }
     }
     if (ctx->world > 1) {
         double h[2] = {before, after};
@@ -1322,64 +1432,6 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     if (!std::isfinite(rep.loss_after)) throw std::runtime_error("lm_step: non-finite loss after update");
 }
 
-// ---- metrics (metrics/image_metrics.cpp, io/run.cpp:77-92) on device (metrics.cu)
-static MetricWindow metric_window() {  // gaussian_window (image_metrics.cpp:25-35)
-    MetricWindow w{};
-    double sum = 0.0;
-    for (int i = 0; i < kMetricWin; ++i) {
-        const double d = i - kMetricWin / 2;
-        w.w[i] = std::exp(-0.5 * d * d / (1.5 * 1.5));
-        sum += w.w[i];
-    }
-    for (double& v : w.w) v /= sum;
-    return w;
-}
-
-struct ImageRef {
-    long long off;  // element offset of the interleaved RGB image
-    int w, h;
-};
-
-// {sum of squared differences, sum of local SSIM} per image, both over the 3 channels.
-template <typename T>
-static std::vector<double2> image_metrics(Context* c, const T* a, const T* b, const std::vector<ImageRef>& imgs) {
-    const int n = static_cast<int>(imgs.size());
-    std::vector<ImgDesc> hd(n);
-    int base = 0, max_tiles = 0;
-    for (int i = 0; i < n; ++i) {
-        ImgDesc& d = hd[i];
-        d.off = imgs[i].off;
-        d.w = imgs[i].w;
-        d.h = imgs[i].h;
-        d.tiles = metric_tiles(d.w, d.h, &d.tiles_x);
-        d.tile_base = base;
-        base += d.tiles;
-        max_tiles = std::max(max_tiles, d.tiles);
-    }
-    std::vector<double2> out(n);
-    if (n == 0) return out;
-    DevBuf<ImgDesc> dd;
-    DevBuf<double2> part, dout;
-    dd.ensure(n);
-    part.ensure(std::max(base, 1));
-    dout.ensure(n);
-    SLM_CUDA_CHECK(cudaMemcpyAsync(dd.p, hd.data(), sizeof(ImgDesc) * n, cudaMemcpyHostToDevice, c->stream));
-    launch_image_metrics(a, b, dd.p, n, max_tiles, part.p, dout.p, metric_window(), c->stream);
-    c->check_launch();
-    SLM_CUDA_CHECK(cudaMemcpyAsync(out.data(), dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    return out;
-}
-
-// metrics::evaluate (image_metrics.cpp:180-186) from the device sums.
-static slm_metric_report metric_report(double2 s, int w, int h) {
-    slm_metric_report r{};
-    const double n = static_cast<double>(w) * h;
-    r.mse = n == 0 ? 0.0 : s.x / (3.0 * n);                  // :108-113
-    r.psnr = r.mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / r.mse);  // :115-119
-    r.ssim = n == 0 ? 1.0 : s.y / (3.0 * n);                 // :121-139
-    return r;
-}
 }  // namespace slm
 
 // =========================================================================== C ABI
@@ -1978,7 +2030,13 @@ int slm_lm_step_host(slm_context* ctx, slm_gaussians* state, slm_train* t, const
 }
 
 int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, double* out) {
+    return slm_batch_loss_kind(s, t, cam_ids, n, SLM_LOSS_MSE, 0.0, out);
+}
+
+int slm_batch_loss_kind(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, int loss, double ssim_weight,
+                        double* out) {
     return guarded([&] {
+        if (loss != SLM_LOSS_MSE && loss != SLM_LOSS_MSE_SSIM) throw std::invalid_argument("batch_loss: unknown loss");
         Context* c = s->impl.ctx;
         c->activate();
         std::vector<slm_camera> cv;
@@ -1992,8 +2050,15 @@ int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, do
         copy_gt(t->impl, b, ids);
         b.render(true);
         const auto sse = b.view_sse();
+        std::vector<double2> ss;
+        if (loss == SLM_LOSS_MSE_SSIM) ss = batch_ssim(b, false);
         double acc = 0.0;
-        for (int v = 0; v < n; ++v) acc += sse[v] / (3.0 * cv[v].width * cv[v].height);
+        for (int v = 0; v < n; ++v) {
+            const double n3 = 3.0 * cv[v].width * cv[v].height;
+            double term = sse[v] / n3;
+            if (loss == SLM_LOSS_MSE_SSIM) term += ssim_weight * ss[v].y / n3;
+            acc += term;
+        }
         *out = n == 0 ? 0.0 : acc / n;
     });
 }
@@ -2012,6 +2077,24 @@ int slm_evaluate(slm_context* ctx, const double* rendered, const double* gt, int
         SLM_CUDA_CHECK(cudaMemcpyAsync(db.p, gt, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         const auto s = image_metrics<double>(c, da.p, db.p, {ImageRef{0, width, height}});
         *out = metric_report(s[0], width, height);
+    });
+}
+
+int slm_ssim_diag_residuals(slm_context* ctx, const double* a, const double* b, int width, int height,
+                            double* residual, double* d_center) {
+    return guarded([&] {
+        if (width < 0 || height < 0) throw std::invalid_argument("metrics: image shapes differ");
+        Context* c = &ctx->impl;
+        c->activate();
+        const size_t n = 3 * static_cast<size_t>(width) * height;
+        DevBuf<double> da, db, dr, dd;
+        for (DevBuf<double>* p : {&da, &db, &dr, &dd}) p->ensure(std::max<size_t>(n, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(da.p, a, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(db.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        image_metrics<double>(c, da.p, db.p, {ImageRef{0, width, height}}, true, dr.p, dd.p);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(residual, dr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(d_center, dd.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
     });
 }
 

@@ -116,6 +116,15 @@ void launch_image_metrics(const float* a, const float* b, const ImgDesc* imgs, i
                           double2* partial, double2* out, const MetricWindow& win, cudaStream_t st);
 void launch_image_metrics(const double* a, const double* b, const ImgDesc* imgs, int n_img, int max_tiles,
                           double2* partial, double2* out, const MetricWindow& win, cudaStream_t st);
+void launch_ssim_diag(const float* a, const float* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                      double2* partial, double2* out, const MetricWindow& win, float* res, float* dcen,
+                      cudaStream_t st);
+void launch_ssim_diag(const double* a, const double* b, const ImgDesc* imgs, int n_img, int max_tiles,
+                      double2* partial, double2* out, const MetricWindow& win, double* res, double* dcen,
+                      cudaStream_t st);
+void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, const int* spix, const int* sorig,
+                      float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
+                      float ssim_weight, float* rhs, cudaStream_t st);
 void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
 
 }  // namespace slm

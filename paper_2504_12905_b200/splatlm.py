@@ -114,6 +114,8 @@ _SIGS = {
     "slm_lm_step_host": (C.c_int, [_vp, C.POINTER(CGaussians), _vp, C.POINTER(CLmConfig), C.c_int,
                                    _vp, C.POINTER(CStepReport)]),
     "slm_batch_loss": (C.c_int, [_vp, _vp, _i32p, C.c_int, _f64p]),
+    "slm_batch_loss_kind": (C.c_int, [_vp, _vp, _i32p, C.c_int, C.c_int, C.c_double, _f64p]),
+    "slm_ssim_diag_residuals": (C.c_int, [_vp, _f64p, _f64p, C.c_int, C.c_int, _f64p, _f64p]),
     "slm_evaluate": (C.c_int, [_vp, _f64p, _f64p, C.c_int, C.c_int, C.POINTER(CMetricReport)]),
     "slm_evaluate_split": (C.c_int, [_vp, _vp, C.POINTER(CMetricReport)]),
     "slm_random_init": (C.c_int, [C.c_int, _f64p, _f64p, _vp, C.POINTER(CGaussians)]),
@@ -444,8 +446,9 @@ class Lib(HostSampler):
                                               rng.h, C.byref(rep)))
         return _report(rep, batch)
 
-    def batch_loss(self, g: GaussianSet, data: "TrainData", cam_ids) -> float:
-        return Scene(self, g).batch_loss(data, cam_ids)
+    def batch_loss(self, g: GaussianSet, data: "TrainData", cam_ids, loss: int = 0,
+                   ssim_weight: float = 0.0) -> float:
+        return Scene(self, g).batch_loss(data, cam_ids, loss, ssim_weight)
 
     def evaluate(self, rendered, ground_truth) -> MetricReport:
         """metrics::evaluate (image_metrics.cpp:180-186): mse, psnr, ssim of two H x W x 3
@@ -461,6 +464,18 @@ class Lib(HostSampler):
 
     def evaluate_split(self, g: GaussianSet, split: "TrainData") -> MetricReport:
         return Scene(self, g).evaluate_split(split)
+
+    def ssim_diag_residuals(self, a, b):
+        """metrics::ssim_diag_residuals (image_metrics.cpp:141-178) on the device:
+        (residual, d_center), each H x W x 3 f64."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+            raise ValueError("metrics: image shapes differ")
+        r, d = np.zeros_like(a), np.zeros_like(a)
+        self._check(self.dll.slm_ssim_diag_residuals(self.ctx, f64ptr(a), f64ptr(b), a.shape[1], a.shape[0],
+                                                     f64ptr(r), f64ptr(d)))
+        return r, d
 
 
 def _report(rep: CStepReport, batch) -> StepReport:
@@ -520,10 +535,12 @@ class Scene:
         self.L._check(self.L.dll.slm_lm_step(self.h, data.h, C.byref(cc), iteration, rng.h, C.byref(rep)))
         return _report(rep, batch)
 
-    def batch_loss(self, data: "TrainData", cam_ids) -> float:
+    def batch_loss(self, data: "TrainData", cam_ids, loss: int = 0, ssim_weight: float = 0.0) -> float:
+        """solver::batch_loss (lm.cpp:39-54); loss 1 = mse+ssim (diagonal SSIM residuals)."""
         ids = np.ascontiguousarray(cam_ids, np.int32)
         out = C.c_double()
-        self.L._check(self.L.dll.slm_batch_loss(self.h, data.h, i32ptr(ids), ids.size, C.byref(out)))
+        self.L._check(self.L.dll.slm_batch_loss_kind(self.h, data.h, i32ptr(ids), ids.size, loss, ssim_weight,
+                                                     C.byref(out)))
         return out.value
 
     def jacobian(self, cams, plan: SamplePlan) -> "Jacobian":

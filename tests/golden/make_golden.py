@@ -193,6 +193,7 @@ def metrics_cases(R):
         out[f"m{i}_a"], out[f"m{i}_b"] = a, b
         out[f"m{i}_ref"] = np.array([R.mse(a, b), R.psnr(a, b), R.ssim(a, b)])
         out[f"m{i}_self"] = np.array([R.mse(a, a), R.psnr(a, a), R.ssim(a, a)])
+        out[f"m{i}_sres"], out[f"m{i}_sdc"] = R.ssim_diag_residuals(a, b)
     d = np.load(os.path.join(HERE, "lm.npz"))
     from support import g_cams, g_set
     st = g_set(d, "lm_final")
@@ -205,10 +206,34 @@ def metrics_cases(R):
     return out
 
 
+def lm_ssim_cases(R):
+    """The same toy LM run with the mse+ssim loss (lm.cpp:86-119, ssim_weight 0.2)."""
+    out = {}
+    d = np.load(os.path.join(HERE, "lm.npz"))
+    from support import g_cams
+    tc, ti = g_cams(d["toy_train_cams"]), list(d["toy_train_imgs"])
+    rng = R.rng(1)
+    st = R.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    td = R.train_data(tc, ti)
+    td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, loss=1, ssim_weight=0.2)
+    reps = []
+    for it in range(8):
+        r = R.lm_step(st, td, cfg, it, rng)
+        reps.append([r.iteration, r.loss_before, r.loss_after, r.eta, r.pcg_iterations,
+                     r.breakdown] + [int(b) for b in r.batch])
+    out["lms_reports"] = np.array(reps, np.float64)
+    out.update(set_arrs("lms_final", st))
+    out["lms_rng_next"] = np.array([rng()], np.uint64)
+    # batch_loss with the mse+ssim loss on the final state, all train views
+    out["lms_batch_loss"] = np.array([R.batch_loss(st, tc, ti, loss=1, ssim_weight=0.2)])
+    return out
+
+
 def main():
     R = ref()
     groups = {"render": render_cases, "sampling": sampling_cases, "jacobian": jacobian_cases,
-              "lm": lm_cases, "metrics": metrics_cases}
+              "lm": lm_cases, "metrics": metrics_cases, "lm_ssim": lm_ssim_cases}
     only = sys.argv[1:]  # optional group names: regenerate just those
     for name, fn in groups.items():
         if only and name not in only:

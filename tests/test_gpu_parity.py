@@ -469,3 +469,43 @@ def test_evaluate_split_matches_reference(gpu):
     assert r.mse == pytest.approx(ref[0], rel=1e-4)
     assert abs(r.psnr - ref[1]) <= 1e-3
     assert abs(r.ssim - ref[2]) <= 1e-5
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_ssim_diag_residuals_match_reference(gpu, i):
+    """metrics::ssim_diag_residuals on the device vs the reference's outputs: every
+    value is computed in the reference's f64 operation order, so bit for bit."""
+    d = golden("metrics")
+    r, dc = gpu.ssim_diag_residuals(d[f"m{i}_a"], d[f"m{i}_b"])
+    print("max |dres|", np.abs(r - d[f"m{i}_sres"]).max(), "max |ddc|", np.abs(dc - d[f"m{i}_sdc"]).max())
+    assert np.array_equal(r, d[f"m{i}_sres"])
+    assert np.array_equal(dc, d[f"m{i}_sdc"])
+
+
+def test_lm_trajectory_mse_ssim_vs_reference(gpu):
+    """8 LM steps with the mse+ssim loss (lm.cpp:86-119: diagonal SSIM rows folded into
+    the rhs and the per-channel weights) vs the reference's run: identical batches,
+    losses within 1e-4, then batch_loss(mse+ssim) of the final state."""
+    d = golden("lm_ssim")
+    dl = golden("lm")
+    tc = g_cams(dl["toy_train_cams"])
+    imgs = list(dl["toy_train_imgs"])
+    rng = gpu.rng(1)
+    st = gpu.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    td = gpu.train_data(tc, imgs)
+    td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, loss=1, ssim_weight=0.2)
+    worst = 0.0
+    for it, row in enumerate(d["lms_reports"]):
+        r = gpu.lm_step(st, td, cfg, it, rng)
+        assert r.batch == [int(b) for b in row[6:]]
+        assert r.pcg_iterations == int(row[4]) and r.breakdown == bool(row[5])
+        assert r.eta == pytest.approx(row[3], rel=1e-6)
+        worst = max(worst, rel_error(r.loss_before, row[1]), rel_error(r.loss_after, row[2]))
+    print("worst per-iteration loss rel err", worst)
+    assert worst < TOL
+    assert rng() == int(d["lms_rng_next"][0])
+    assert norm_rel(st.pack(), g_set(d, "lms_final").pack()) < 1e-3
+    ref_final = g_set(d, "lms_final")
+    bl = gpu.batch_loss(ref_final, td, list(range(len(tc))), loss=1, ssim_weight=0.2)
+    assert rel_error(bl, float(d["lms_batch_loss"][0])) < TOL

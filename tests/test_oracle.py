@@ -216,3 +216,40 @@ def test_ssim_live_reference(port, reflib):
         a = rng.random((h, w, 3))
         b = np.clip(a + rng.normal(0, 0.1, a.shape), 0, 1)
         assert port.ssim(a, b) == reflib.ssim(a, b)
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_ssim_diag_residuals_known_answers(port, i):
+    """metrics::ssim_diag_residuals (image_metrics.cpp:141-178): residual s and centre
+    derivative, bitwise against the reference's outputs."""
+    d = golden("metrics")
+    r, dc = port.ssim_diag_residuals(d[f"m{i}_a"], d[f"m{i}_b"])
+    assert np.array_equal(r, d[f"m{i}_sres"])
+    assert np.array_equal(dc, d[f"m{i}_sdc"])
+    # identical images: zero residuals and derivatives (test_metrics.cpp:120-126)
+    z, zd = port.ssim_diag_residuals(d[f"m{i}_a"], d[f"m{i}_a"])
+    assert not z.any() and not zd.any()
+
+
+def test_lm_trajectory_mse_ssim(port):
+    """lm_step with the mse+ssim loss (lm.cpp:86-119): the diagonal SSIM rows fold into the
+    rhs and the per-channel weights; losses and state against the reference's run."""
+    d = golden("lm_ssim")
+    dl = golden("lm")
+    tc = g_cams(dl["toy_train_cams"])
+    rng = port.rng(1)
+    st = port.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    td = port.train_data(tc, list(dl["toy_train_imgs"]))
+    td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, loss=1, ssim_weight=0.2)
+    for it, row in enumerate(d["lms_reports"]):
+        r = port.lm_step(st, td, cfg, it, rng)
+        assert r.batch == [int(b) for b in row[6:]]
+        assert r.pcg_iterations == int(row[4]) and r.breakdown == bool(row[5])
+        assert r.eta == row[3]
+        assert abs(r.loss_before - row[1]) <= 1e-12 * row[1]
+        assert abs(r.loss_after - row[2]) <= 1e-12 * row[2]
+    assert np.max(np.abs(st.pack() - g_set(d, "lms_final").pack())) <= 1e-12
+    assert rng() == int(d["lms_rng_next"][0])
+    bl = port.batch_loss(st, tc, list(dl["toy_train_imgs"]), loss=1, ssim_weight=0.2)
+    assert bl == pytest.approx(float(d["lms_batch_loss"][0]), rel=1e-12)
