@@ -31,6 +31,7 @@ CU_SOURCES = {
     "cg.cu": [],
     "sort.cu": [],
     "metrics.cu": [],
+    "sampler.cu": [],
 }
 CPP_SOURCES = ["runtime.cpp"]
 HEADERS = ["common.cuh", "layout.hpp", "runtime.hpp"]

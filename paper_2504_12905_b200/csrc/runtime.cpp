@@ -420,11 +420,13 @@ struct Samples {
     pinned_vector<int> hpix, horig;
     pinned_vector<float> hw;
     long long total = 0, mask_words = 0;
+    bool device_drawn = false;  // spix / sw written on the device (weighted distributions)
 
     // Host half (no CUDA calls; runs on the sampler thread in lm_step):
     // group the plan's samples per view by tile in chunks of <= 32.
     void group_host(const slm_plan& plan, int view_lo, int view_hi, const std::vector<slm_camera>& cams,
                     const std::vector<double>& weights3) {
+        device_drawn = false;
         hgroups.clear();
         order.clear();
         for (int v = view_lo; v < view_hi; ++v) {
@@ -467,6 +469,38 @@ struct Samples {
         }
     }
 
+    // Host half of a device-drawn plan (weighted distributions): min(N, m)
+    // draws per tile in plan order (tile-major), grouped in chunks of <= 32;
+    // the pixels and weights are filled in by k_weighted_draw.  Returns the
+    // first sample of every tile (batch tile order).
+    std::vector<int> group_tiles_host(const std::vector<slm_camera>& cams, int spt) {
+        device_drawn = true;
+        hgroups.clear();
+        order.clear();
+        std::vector<int> sbase;
+        for (int v = 0; v < static_cast<int>(cams.size()); ++v) {
+            const slm_camera& c = cams[v];
+            const int txn = (c.width + kTile - 1) / kTile, tyn = (c.height + kTile - 1) / kTile;
+            for (int t = 0; t < txn * tyn; ++t) {
+                const int w = std::min(c.width - (t % txn) * kTile, kTile);
+                const int h = std::min(c.height - (t / txn) * kTile, kTile);
+                const int n = std::min(spt, w * h);
+                sbase.push_back(static_cast<int>(order.size()));
+                for (int i = 0; i < n; i += 32) {
+                    const int cnt = std::min(32, n - i);
+                    hgroups.push_back(Group{v, t, static_cast<int>(order.size()), cnt});
+                    for (int k = 0; k < cnt; ++k) order.push_back(static_cast<int>(order.size()));
+                }
+            }
+        }
+        total = static_cast<long long>(order.size());
+        horig.resize(order.size());
+        for (size_t k = 0; k < order.size(); ++k) horig[k] = static_cast<int>(k);
+        hpix.assign(order.size(), 0);
+        hw.assign(3 * order.size(), 0.f);
+        return sbase;
+    }
+
     // Device half: mask offsets (need the tile-list lengths) and uploads.
     pinned_vector<long long> hoff;
     void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets) {
@@ -492,9 +526,11 @@ struct Samples {
         sw.ensure(std::max<size_t>(3 * order.size(), 1));
         SLM_CUDA_CHECK(cudaMemcpyAsync(mask_off.p, hoff.data(), sizeof(long long) * hoff.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(groups.p, hgroups.data(), sizeof(Group) * hgroups.size(), cudaMemcpyHostToDevice, st));
-        SLM_CUDA_CHECK(cudaMemcpyAsync(spix.p, hpix.data(), sizeof(int) * hpix.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sorig.p, horig.data(), sizeof(int) * horig.size(), cudaMemcpyHostToDevice, st));
-        SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, st));
+        if (!device_drawn) {
+            SLM_CUDA_CHECK(cudaMemcpyAsync(spix.p, hpix.data(), sizeof(int) * hpix.size(), cudaMemcpyHostToDevice, st));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(sw.p, hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice, st));
+        }
         // (host arrays are pinned members, rewritten only after later syncs)
     }
 
@@ -527,6 +563,7 @@ struct Jacobian {
     // Host half: residual weights (jacobian.cpp:112-116) and sample grouping.
     // Pure host work, safe to run concurrently with GPU work on the context.
     void init_host(const slm_plan& plan, int lo, int hi, double inv_total, const std::vector<slm_camera>& cams) {
+        draw.on = false;
         rdim = 0;
         plan_base = plan.view_offset[lo];
         for (int v = lo; v < hi; ++v) rdim += 3 * (plan.view_offset[v + 1] - plan.view_offset[v]);
@@ -536,8 +573,67 @@ struct Jacobian {
         samples.group_host(plan, lo, hi, cams, weights);
     }
 
+    // Weighted residual distributions (sample_plan.cpp:127-165): the host draws
+    // the uniforms from the caller's RNG in the reference's order, the device
+    // picks the pixels from the per-tile CDFs of the render (sampler.cu).
+    struct Draw {
+        bool on = false;
+        int dist = 0, spt = 0;
+        double n_total = 0.0, inv_total = 0.0;
+        pinned_vector<double> hU;
+        std::vector<int> hsbase;
+        DevBuf<double> U;
+        DevBuf<int> sbase;
+    } draw;
+
+    void init_host_weighted(const std::vector<slm_camera>& all, int lo, int hi, int spt, int dist, int lane,
+                            std::mt19937_64& rng) {
+        if (spt < 1) throw std::invalid_argument("samples_per_tile must be positive");
+        if (spt > kTile * kTile) throw std::invalid_argument("samples_per_tile exceeds the pixels in a tile");
+        if (lane < 1 || spt % lane != 0)
+            throw std::invalid_argument("samples_per_tile must be a multiple of the lane width");
+        if (dist != SLM_DIST_RESIDUAL && dist != SLM_DIST_GAUSSIAN_COUNT)
+            throw std::invalid_argument("unknown residual distribution");
+        long long total = 0, off_lo = 0, off_hi = 0;
+        for (int v = 0; v < static_cast<int>(all.size()); ++v) {
+            if (v == lo) off_lo = total;
+            const int txn = (all[v].width + kTile - 1) / kTile, tyn = (all[v].height + kTile - 1) / kTile;
+            for (int ty = 0; ty < tyn; ++ty)
+                for (int tx = 0; tx < txn; ++tx)
+                    total += std::min(spt, std::min(all[v].width - tx * kTile, kTile) *
+                                               std::min(all[v].height - ty * kTile, kTile));
+            if (v + 1 == hi) off_hi = total;
+        }
+        if (lo >= hi) off_lo = off_hi = 0;
+        // one uniform per draw, every rank replays the whole batch (draw_from_cdf, :53-58)
+        std::uniform_real_distribution<double> uni(0.0, 1.0);
+        draw.hU.resize(std::max<long long>(off_hi - off_lo, 1));
+        for (long long i = 0; i < total; ++i) {
+            const double u = uni(rng);
+            if (i >= off_lo && i < off_hi) draw.hU[i - off_lo] = u;
+        }
+        draw.on = true;
+        draw.dist = dist;
+        draw.spt = spt;
+        draw.n_total = static_cast<double>(total);
+        draw.inv_total = total > 0 ? 1.0 / static_cast<double>(total) : 0.0;
+        const std::vector<slm_camera> mine(all.begin() + lo, all.begin() + hi);
+        draw.hsbase = samples.group_tiles_host(mine, spt);
+        rdim = 3 * samples.total;
+        plan_base = off_lo;
+        weights.clear();  // drawn on the device (lm_step's Jacobian never reads them on the host)
+    }
+
     // Adopt the host half computed by another (host-only) Jacobian.
     void take_host(Jacobian& o) {
+        std::swap(draw.on, o.draw.on);
+        std::swap(draw.dist, o.draw.dist);
+        std::swap(draw.spt, o.draw.spt);
+        std::swap(draw.n_total, o.draw.n_total);
+        std::swap(draw.inv_total, o.draw.inv_total);
+        draw.hU.swap(o.draw.hU);
+        draw.hsbase.swap(o.draw.hsbase);
+        std::swap(samples.device_drawn, o.samples.device_drawn);
         std::swap(rdim, o.rdim);
         std::swap(plan_base, o.plan_base);
         weights.swap(o.weights);
@@ -553,6 +649,18 @@ struct Jacobian {
     // prepared and rendered).
     void init_device() {
         samples.upload(ctx, batch->hcams, batch->htile_offsets);
+        if (draw.on) {  // weighted distributions: pixels + weights from the render's CDFs
+            draw.U.ensure(draw.hU.size());
+            draw.sbase.ensure(std::max<size_t>(draw.hsbase.size(), 1));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(draw.U.p, draw.hU.data(), sizeof(double) * draw.hU.size(),
+                                           cudaMemcpyHostToDevice, ctx->stream));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(draw.sbase.p, draw.hsbase.data(), sizeof(int) * draw.hsbase.size(),
+                                           cudaMemcpyHostToDevice, ctx->stream));
+            launch_weighted_draw(batch->cams.p, batch->n_tiles, batch->tile_view.p, draw.sbase.p, batch->image.p,
+                                 batch->gt.p, batch->contrib.p, draw.dist, draw.spt, draw.U.p, draw.n_total,
+                                 draw.inv_total, samples.spix.p, samples.sw.p, ctx->stream);
+            ctx->check_launch();
+        }
         ctx->mark("plan:upload");
         const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
         tan.ensure(3 * VG);
@@ -1234,7 +1342,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     bool use_spec = false;
     if (spec) {
         if (spec->th.joinable()) spec->th.join();
-        use_spec = !spec->err && cfg.dist == SLM_DIST_UNIFORM && spec->rng_before == rng && spec->k == t.k &&
+        use_spec = !spec->err && spec->rng_before == rng && spec->k == t.k &&
                    spec->assign == t.assign && spec->spt == cfg.samples_per_tile && spec->dist == cfg.dist &&
                    spec->lane == cfg.sample_lane_width && same_cams(spec->cams, t.cams);
     }
@@ -1259,24 +1367,35 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     // on a host thread while the GPU prepares and renders the views.
     std::unique_ptr<PlanH> plan;
     std::exception_ptr plan_err;
-    auto make_plan = [&](const double* const* ai, const int32_t* const* ac, const double* const* ag) {
+    auto make_plan = [&] {
         try {
             plan = build_plan(all_cams.data(), VB, cfg.samples_per_tile, cfg.dist, cfg.sample_lane_width, rng,
-                              ai, ac, ag);
+                              nullptr, nullptr, nullptr);
             const long long total = plan->view_offset.back();
             J.init_host(plan->view(), lo, hi, total > 0 ? 1.0 / static_cast<double>(total) : 0.0, my_cams);
         } catch (...) {
             plan_err = std::current_exception();
         }
     };
+    // Weighted distributions: the host draws the uniforms (the whole RNG
+    // consumption of the plan), the device picks the pixels from the render
+    // (Jacobian::Draw) -- so this overlaps with the render too.
+    auto make_weighted = [&] {
+        try {
+            J.init_host_weighted(all_cams, lo, hi, cfg.samples_per_tile, cfg.dist, cfg.sample_lane_width, rng);
+        } catch (...) {
+            plan_err = std::current_exception();
+        }
+    };
     std::thread sampler;
-    const bool overlap = cfg.dist == SLM_DIST_UNIFORM;
     if (use_spec) {
         plan = std::move(spec->plan);
         J.take_host(*spec->hj);
         rng = spec->rng_after;
-    } else if (overlap) {
-        sampler = std::thread(make_plan, nullptr, nullptr, nullptr);
+    } else if (cfg.dist == SLM_DIST_UNIFORM) {
+        sampler = std::thread(make_plan);
+    } else {
+        sampler = std::thread(make_weighted);
     }
     spec.reset();
     // 2./3. forward render + residual fields of this rank's views (lm.cpp:75-78)
@@ -1289,34 +1408,8 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         throw;
     }
     ctx->mark("prepare+render");
-    if (overlap) {
-        if (sampler.joinable()) sampler.join();
-        ctx->mark("plan:host");
-    } else {  // weighted distributions need the render on the host (aux data)
-        if (ctx->world > 1)
-            throw std::invalid_argument("weighted residual distributions are single-rank only on the B200 path");
-        std::vector<std::vector<double>> aux_img, aux_gt;
-        std::vector<std::vector<int32_t>> aux_cn;
-        std::vector<const double*> pi, pg;
-        std::vector<const int32_t*> pc;
-        for (int v = 0; v < VB; ++v) {
-            const size_t np = static_cast<size_t>(all_cams[v].width) * all_cams[v].height;
-            std::vector<float> fi(3 * np), fg(3 * np);
-            aux_cn.emplace_back(np);
-            SLM_CUDA_CHECK(cudaMemcpyAsync(fi.data(), B.image.p + 3 * B.hcams[v].pix_base, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, ctx->stream));
-            SLM_CUDA_CHECK(cudaMemcpyAsync(fg.data(), B.gt.p + 3 * B.hcams[v].pix_base, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, ctx->stream));
-            SLM_CUDA_CHECK(cudaMemcpyAsync(aux_cn.back().data(), B.contrib.p + B.hcams[v].pix_base, sizeof(int) * np, cudaMemcpyDeviceToHost, ctx->stream));
-            ctx->sync();
-            aux_img.emplace_back(fi.begin(), fi.end());
-            aux_gt.emplace_back(fg.begin(), fg.end());
-        }
-        for (int v = 0; v < VB; ++v) {
-            pi.push_back(aux_img[v].data());
-            pc.push_back(aux_cn[v].data());
-            pg.push_back(aux_gt[v].data());
-        }
-        make_plan(pi.data(), pc.data(), pg.data());
-    }
+    if (sampler.joinable()) sampler.join();
+    ctx->mark("plan:host");
     if (plan_err) std::rethrow_exception(plan_err);
     // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
     double before = 0.0;
@@ -1333,7 +1426,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     }
     J.init_device();
     ctx->mark("plan");
-    if (cfg.dist == SLM_DIST_UNIFORM) {  // speculate the next step's batch + plan while this one solves
+    {  // speculate the next step's batch + plan (uniform) or uniforms (weighted) while this one solves
         auto sp = std::make_unique<Speculation>();
         sp->rng_before = rng;
         sp->assign = t.assign;
@@ -1355,9 +1448,14 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
                 std::vector<slm_camera> all, mine;
                 for (int i = 0; i < nb; ++i) all.push_back(q->cams[q->batch[i]]);
                 for (int i = l; i < h; ++i) mine.push_back(q->cams[q->batch[i]]);
-                q->plan = build_plan(all.data(), nb, q->spt, q->dist, q->lane, r, nullptr, nullptr, nullptr);
-                const long long total = q->plan->view_offset.back();
-                q->hj->init_host(q->plan->view(), l, h, total > 0 ? 1.0 / static_cast<double>(total) : 0.0, mine);
+                if (q->dist == SLM_DIST_UNIFORM) {
+                    q->plan = build_plan(all.data(), nb, q->spt, q->dist, q->lane, r, nullptr, nullptr, nullptr);
+                    const long long total = q->plan->view_offset.back();
+                    q->hj->init_host(q->plan->view(), l, h, total > 0 ? 1.0 / static_cast<double>(total) : 0.0,
+                                     mine);
+                } else {
+                    q->hj->init_host_weighted(all, l, h, q->spt, q->dist, q->lane, r);
+                }
                 q->rng_after = r;
             } catch (...) {
                 q->err = std::current_exception();

@@ -125,6 +125,10 @@ void launch_ssim_diag(const double* a, const double* b, const ImgDesc* imgs, int
 void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, const int* spix, const int* sorig,
                       float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
                       float ssim_weight, float* rhs, cudaStream_t st);
+void launch_weighted_draw(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
+                          const float* image, const float* gt, const int* contrib, int dist, int spt,
+                          const double* U, double n_total, double inv_total, int* spix, float* sw,
+                          cudaStream_t st);
 void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
 
 }  // namespace slm

@@ -292,7 +292,8 @@ def test_lm_trajectory_vs_reference(gpu):
     assert norm_rel(st.pack(), g_set(d, "lm_final").pack()) < 1e-3
 
 
-def test_lm_speculation_discarded_when_inputs_change(gpu, port):
+@pytest.mark.parametrize("dist", [0, 1])
+def test_lm_speculation_discarded_when_inputs_change(gpu, port, dist):
     """lm_step draws the next step's batch + plan speculatively during its PCG; a
     caller that touches the RNG or rebuilds the clusters between steps must get
     exactly the reference's draws (the speculation is discarded)."""
@@ -303,14 +304,14 @@ def test_lm_speculation_discarded_when_inputs_change(gpu, port):
     tdg, tdo = gpu.train_data(tc, list(ti)), port.train_data(tc, list(ti))
     for td in (tdg, tdo):
         td.rebuild_clusters(4, 7)
-    cfg = LmConfig(batch_size_initial=4, pcg_iters_initial=4)
+    cfg = LmConfig(batch_size_initial=4, pcg_iters_initial=4, dist=dist)
     for it in range(5):
         if it == 2:  # the caller consumes the RNG between steps
             assert rg() == ro()
         if it == 3:  # ... and rebuilds the clusters (batch size change, run.cpp:145-153)
             for td in (tdg, tdo):
                 td.rebuild_clusters(3, 11)
-            cfg = LmConfig(batch_size_initial=3, pcg_iters_initial=4)
+            cfg = LmConfig(batch_size_initial=3, pcg_iters_initial=4, dist=dist)
         a, b = gpu.lm_step(sg, tdg, cfg, it, rg), port.lm_step(so, tdo, cfg, it, ro)
         assert a.batch == b.batch, f"step {it}: batch {a.batch} vs {b.batch}"
         assert rel_error(a.loss_after, b.loss_after) < TOL
@@ -509,3 +510,29 @@ def test_lm_trajectory_mse_ssim_vs_reference(gpu):
     ref_final = g_set(d, "lms_final")
     bl = gpu.batch_loss(ref_final, td, list(range(len(tc))), loss=1, ssim_weight=0.2)
     assert rel_error(bl, float(d["lms_batch_loss"][0])) < TOL
+
+
+@pytest.mark.parametrize("dist", [1, 2])
+def test_lm_weighted_distributions_vs_oracle(gpu, port, dist):
+    """lm_step with the weighted residual distributions (sample_plan.cpp:127-165:
+    kResidual softmax, kGaussianCount): the host draws the uniforms from the caller's
+    RNG in the reference's order, the device builds the per-tile CDFs from the render
+    and picks the pixels.  Batches and the RNG position are exact; the pixel picks
+    use the f32 render's CDF (the reference's is f64), so a draw landing within
+    rounding of a CDF step may pick the neighbour -- losses agree to 1e-4."""
+    gt, tc, ti, _, _ = port.toy_scene(20, 8, 1, 64, 20214)
+    rg, ro = gpu.rng(3), port.rng(3)
+    sg = gpu.random_init(60, [-1, -1, -1], [1, 1, 1], rg)
+    so = port.random_init(60, [-1, -1, -1], [1, 1, 1], ro)
+    tdg, tdo = gpu.train_data(tc, list(ti)), port.train_data(tc, list(ti))
+    for td in (tdg, tdo):
+        td.rebuild_clusters(8, 5)
+    cfg = LmConfig(pcg_iters_initial=8, samples_per_tile=32, dist=dist)
+    worst = 0.0
+    for it in range(6):
+        a, b = gpu.lm_step(sg, tdg, cfg, it, rg), port.lm_step(so, tdo, cfg, it, ro)
+        assert a.batch == b.batch
+        worst = max(worst, rel_error(a.loss_before, b.loss_before), rel_error(a.loss_after, b.loss_after))
+    print("dist", dist, "worst loss rel err", worst)
+    assert worst < TOL
+    assert rg() == ro()

@@ -12,6 +12,8 @@ from paper_2504_12905_b200.types import LmConfig  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+    dist = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # residual distribution
+    loss = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # 1 = mse+ssim
     args = bench.parse_args_for(1_000_000)
     L = splatlm.Lib(0)
     state, cams, clusters, batch, plan = bench.host_inputs(L, args, 1)
@@ -21,7 +23,8 @@ def main():
     td = L.train_data(cams, imgs)
     td.set_clusters(clusters)
     scene = splatlm.Scene(L, state)
-    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, batch_size_initial=8, batch_size_late=8, samples_per_tile=32)
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, batch_size_initial=8, batch_size_late=8, samples_per_tile=32,
+                   dist=dist, loss=loss)
     rng = L.rng(1)
     L.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)
     L.set_timing(True)
