@@ -159,6 +159,24 @@ int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cams, int n, doubl
 int slm_batch_loss_kind(slm_scene* s, slm_train* t, const int32_t* cams, int n, int loss, double ssim_weight,
                         double* out);
 
+/* ---- first-order baselines (baselines/first_order.hpp) on the device */
+typedef struct slm_first_order slm_first_order; /* FirstOrderState: f64 moments in HBM + step */
+void slm_default_first_order_config(slm_first_order_config* cfg);
+/* full_gradient (first_order.cpp:11-44) over every camera of the TrainData:
+ * exhaustive plan, dL/dr = 2/M (r + w s s'), J^T on the device; AoS f64 out. */
+int slm_full_gradient(slm_scene* s, slm_train* t, int loss, double ssim_weight, double* grad_aos);
+/* Optimizer state bound to a device-resident scene (zero moments, step 0). */
+int slm_first_order_create(slm_scene* s, slm_first_order** out);
+void slm_first_order_destroy(slm_first_order* f);
+int slm_first_order_moments(slm_first_order* f, double* m1_aos, double* m2_aos, int64_t* step);
+int slm_first_order_set_moments(slm_first_order* f, const double* m1_aos, const double* m2_aos, int64_t step);
+/* first_order_step (first_order.cpp:115-122) with a caller gradient (AoS f64). */
+int slm_first_order_apply(slm_first_order* f, const double* grad_aos, const slm_first_order_config* cfg);
+/* One train_run iteration (run.cpp:176-182): full_gradient + step + batch_loss
+ * over all TrainData cameras (train_loss may be NULL to skip the loss). */
+int slm_first_order_step(slm_first_order* f, slm_train* t, const slm_first_order_config* cfg,
+                         double* train_loss);
+
 /* ---- metrics (metrics/image_metrics.hpp, io/run.cpp:77-92), computed on the device */
 /* metrics::evaluate (image_metrics.cpp:180-186) on two interleaved-RGB f64 images. */
 int slm_evaluate(slm_context* ctx, const double* rendered, const double* ground_truth, int width,

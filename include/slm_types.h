@@ -102,6 +102,28 @@ typedef struct slm_pcg_result {
     double rel_residual;
 } slm_pcg_result;
 
+/* baselines::FirstOrderConfig (baselines/first_order.hpp:12-37); per-group
+ * learning rates in raw (pre-activation) coordinates. */
+enum { SLM_FO_ADAM = 0, SLM_FO_RMSPROP = 1, SLM_FO_SGD_MOMENTUM = 2 };
+typedef struct slm_first_order_config {
+    int32_t kind;                 /* SLM_FO_ADAM */
+    double lr_mean;               /* 1.6e-3 */
+    double lr_color;              /* 2.5e-2 */
+    double lr_opacity;            /* 5e-2 */
+    double lr_scale;              /* 5e-3 */
+    double lr_rotation;           /* 1e-3 */
+    double adam_beta1;            /* 0.9 */
+    double adam_beta2;            /* 0.999 */
+    double adam_eps;              /* 1e-15 */
+    double rms_decay;             /* 0.99 */
+    double rms_eps;               /* 1e-15 */
+    double momentum;              /* 0.99 */
+    double mean_lr_final_factor;  /* 0.01 */
+    int32_t decay_iterations;     /* 0 = no decay */
+    int32_t loss;                 /* SLM_LOSS_MSE */
+    double ssim_weight;           /* 0.2 */
+} slm_first_order_config;
+
 /* MetricReport (metrics/image_metrics.hpp:7-11). */
 typedef struct slm_metric_report {
     double mse;

@@ -24,6 +24,7 @@
 
 #include "slm_b200.h"
 #include "splatlm/autodiff/jacobian.hpp"
+#include "splatlm/baselines/first_order.hpp"
 #include "splatlm/core/types.hpp"
 #include "splatlm/io/dataset.hpp"
 #include "splatlm/metrics/image_metrics.hpp"
@@ -257,6 +258,59 @@ inline solver::PcgResult pcg_solve(Device& dev, const solver::ApplyFn& apply, co
     res.breakdown = r.breakdown != 0;
     res.rel_residual = r.rel_residual;
     return res;
+}
+
+// baselines::full_gradient (first_order.cpp:11-44) on the device.
+inline ParamVector full_gradient(Device& dev, const GaussianSet& state, std::span<const Camera> cams,
+                                 std::span<const Image> gts, solver::LossKind loss, double ssim_weight) {
+    if (cams.size() != gts.size()) throw std::invalid_argument("full_gradient: camera/image count mismatch");
+    std::vector<slm_camera> cc;
+    std::vector<float> imgs;
+    for (size_t i = 0; i < cams.size(); ++i) {
+        cc.push_back(to_c(cams[i]));
+        for (double v : gts[i].data) imgs.push_back(static_cast<float>(v));
+    }
+    GaussianSet g = state;
+    slm_gaussians cg = to_c(g);
+    slm_scene* s = nullptr;
+    slm_train* t = nullptr;
+    check(slm_scene_create(dev.get(), &cg, &s));
+    ParamVector out(static_cast<size_t>(state.param_count()));
+    int rc = slm_train_create(dev.get(), cc.data(), static_cast<int>(cc.size()), imgs.data(), &t);
+    if (rc == SLM_OK) rc = slm_full_gradient(s, t, static_cast<int>(loss), ssim_weight, out.data());
+    if (t) slm_train_destroy(t);
+    slm_scene_destroy(s);
+    check(rc);
+    return out;
+}
+
+inline slm_first_order_config to_c(const baselines::FirstOrderConfig& c) {
+    return slm_first_order_config{static_cast<int32_t>(c.kind), c.lrs.mean, c.lrs.color, c.lrs.opacity,
+                                  c.lrs.scale, c.lrs.rotation, c.adam_beta1, c.adam_beta2, c.adam_eps,
+                                  c.rms_decay, c.rms_eps, c.momentum, c.mean_lr_final_factor,
+                                  c.decay_iterations, static_cast<int32_t>(c.loss), c.ssim_weight};
+}
+
+// baselines::first_order_step (first_order.cpp:115-122): the step runs on the
+// device in f64 with the reference's operation order (bitwise equal results).
+inline void first_order_step(Device& dev, baselines::FirstOrderState& st, GaussianSet& state,
+                             const ParamVector& grad, const baselines::FirstOrderConfig& cfg) {
+    if (grad.size() != static_cast<size_t>(state.param_count())) throw std::invalid_argument("gradient length mismatch");
+    slm_gaussians cg = to_c(state);
+    slm_scene* s = nullptr;
+    slm_first_order* f = nullptr;
+    check(slm_scene_create(dev.get(), &cg, &s));
+    const slm_first_order_config c = to_c(cfg);
+    int64_t step = st.step;
+    int rc = slm_first_order_create(s, &f);
+    if (rc == SLM_OK) rc = slm_first_order_set_moments(f, st.m1.data(), st.m2.data(), step);
+    if (rc == SLM_OK) rc = slm_first_order_apply(f, grad.data(), &c);
+    if (rc == SLM_OK) rc = slm_first_order_moments(f, st.m1.data(), st.m2.data(), &step);
+    if (rc == SLM_OK) rc = slm_scene_download(s, &cg);
+    if (f) slm_first_order_destroy(f);
+    slm_scene_destroy(s);
+    check(rc);
+    st.step = static_cast<long>(step);
 }
 
 // metrics::evaluate (image_metrics.cpp:180-186) on the device.

@@ -13,7 +13,7 @@ import os
 
 import numpy as np
 
-from paper_2504_12905_b200.types import (CCamera, CGaussians, CLmConfig, CPcgResult, CPlan,
+from paper_2504_12905_b200.types import (CCamera, CFirstOrderConfig, CGaussians, CLmConfig, CPcgResult, CPlan,
                                          CStepReport, Camera, GaussianSet, LmConfig,
                                          PcgResult, SamplePlan, StepReport, cameras_to_c,
                                          f32ptr, f64ptr, i32ptr, i64ptr)
@@ -98,6 +98,10 @@ class CpuLib:
             "mse": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
             "psnr": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
             "ssim": (C.c_double, [_f64p, _f64p, C.c_int, C.c_int]),
+            "full_gradient": (C.c_int, [C.POINTER(CGaussians), C.POINTER(CCamera), C.c_int,
+                                        C.POINTER(C.c_float), C.c_int, C.c_double, _f64p]),
+            "first_order_step": (C.c_int, [C.POINTER(CGaussians), _f64p, _f64p, C.POINTER(C.c_int64),
+                                           _f64p, C.POINTER(CFirstOrderConfig)]),
             "ssim_diag_residuals": (None, [_f64p, _f64p, C.c_int, C.c_int, _f64p, _f64p]),
         }
         for name, (res, args) in sig.items():
@@ -308,6 +312,25 @@ class CpuLib:
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
         return self._ssim(f64ptr(a), f64ptr(b), a.shape[1], a.shape[0])
+
+    def full_gradient(self, g: GaussianSet, cams, gts_f32, loss: int = 0, ssim_weight: float = 0.2) -> np.ndarray:
+        """baselines::full_gradient (first_order.cpp:11-44) -> ParamVector (AoS, 14 per Gaussian)."""
+        gts = np.ascontiguousarray(np.concatenate([np.asarray(x, np.float32).reshape(-1) for x in gts_f32]))
+        out = np.zeros(14 * g.count)
+        cg = g.to_c()
+        self._check(self._full_gradient(C.byref(cg), cameras_to_c(cams), len(cams), f32ptr(gts), loss,
+                                        ssim_weight, f64ptr(out)))
+        return out
+
+    def first_order_step(self, g: GaussianSet, m1: np.ndarray, m2: np.ndarray, step: int, grad: np.ndarray,
+                         cfg) -> int:
+        """baselines::first_order_step on caller-held moments (updated in place); returns the new step."""
+        st = C.c_int64(step)
+        grad = np.ascontiguousarray(grad, np.float64)
+        cg, cc = g.to_c(), cfg.to_c()
+        self._check(self._first_order_step(C.byref(cg), f64ptr(m1), f64ptr(m2), C.byref(st), f64ptr(grad),
+                                           C.byref(cc)))
+        return st.value
 
     def ssim_diag_residuals(self, a, b):
         """metrics::ssim_diag_residuals -> (residual, d_center), both H x W x 3."""

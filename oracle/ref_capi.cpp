@@ -18,6 +18,7 @@
 
 #include "slm_types.h"
 #include "splatlm/autodiff/jacobian.hpp"
+#include "splatlm/baselines/first_order.hpp"
 #include "splatlm/core/parallel.hpp"
 #include "splatlm/io/dataset.hpp"
 #include "splatlm/io/scene_gen.hpp"
@@ -602,6 +603,67 @@ void ref_ssim_diag_residuals(const double* a, const double* b, int w, int h, dou
     const auto r = metrics::ssim_diag_residuals(ia, ib);
     std::copy(r.residual.data.begin(), r.residual.data.end(), residual);
     std::copy(r.d_center.data.begin(), r.d_center.data.end(), d_center);
+}
+// baselines::full_gradient (first_order.cpp:11-44); gts are float32 dataset buffers
+int ref_full_gradient(const slm_gaussians* g, const slm_camera* cams, int n_cams, const float* gts, int loss,
+                      double ssim_weight, double* out) {
+    return guarded([&] {
+        const auto cv = to_cams(cams, n_cams);
+        std::vector<Image> imgs;
+        const float* src = gts;
+        for (const auto& cam : cv) {
+            Image img(cam.width, cam.height);
+            for (size_t k = 0; k < img.data.size(); ++k) img.data[k] = src[k];
+            src += img.data.size();
+            imgs.push_back(std::move(img));
+        }
+        const auto grad = baselines::full_gradient(to_set(*g), cv, imgs, static_cast<solver::LossKind>(loss),
+                                                   ssim_weight);
+        std::copy(grad.begin(), grad.end(), out);
+    });
+}
+
+static baselines::FirstOrderConfig to_fo(const slm_first_order_config& c) {
+    baselines::FirstOrderConfig f;
+    f.kind = static_cast<baselines::FirstOrderKind>(c.kind);
+    f.lrs = {c.lr_mean, c.lr_color, c.lr_opacity, c.lr_scale, c.lr_rotation};
+    f.adam_beta1 = c.adam_beta1;
+    f.adam_beta2 = c.adam_beta2;
+    f.adam_eps = c.adam_eps;
+    f.rms_decay = c.rms_decay;
+    f.rms_eps = c.rms_eps;
+    f.momentum = c.momentum;
+    f.mean_lr_final_factor = c.mean_lr_final_factor;
+    f.decay_iterations = c.decay_iterations;
+    f.loss = static_cast<solver::LossKind>(c.loss);
+    f.ssim_weight = c.ssim_weight;
+    return f;
+}
+
+void ref_default_first_order_config(slm_first_order_config* out) {
+    const baselines::FirstOrderConfig f;
+    *out = slm_first_order_config{static_cast<int32_t>(f.kind), f.lrs.mean, f.lrs.color, f.lrs.opacity,
+                                  f.lrs.scale, f.lrs.rotation, f.adam_beta1, f.adam_beta2, f.adam_eps,
+                                  f.rms_decay, f.rms_eps, f.momentum, f.mean_lr_final_factor,
+                                  f.decay_iterations, static_cast<int32_t>(f.loss), f.ssim_weight};
+}
+
+// baselines::first_order_step (first_order.cpp:115-122) on caller-held moments
+int ref_first_order_step(slm_gaussians* g, double* m1, double* m2, int64_t* step, const double* grad,
+                         const slm_first_order_config* cfg) {
+    return guarded([&] {
+        GaussianSet s = to_set(*g);
+        const size_t n = static_cast<size_t>(s.param_count());
+        baselines::FirstOrderState st;
+        st.m1.assign(m1, m1 + n);
+        st.m2.assign(m2, m2 + n);
+        st.step = static_cast<long>(*step);
+        baselines::first_order_step(st, s, ParamVector(grad, grad + n), to_fo(*cfg));
+        from_set(s, *g);
+        std::copy(st.m1.begin(), st.m1.end(), m1);
+        std::copy(st.m2.begin(), st.m2.end(), m2);
+        *step = st.step;
+    });
 }
 
 }  // extern "C"

@@ -1923,3 +1923,119 @@ int orc_lm_step(slm_gaussians* g, void* tp, const slm_lm_config* cfg, int iterat
     if (!isfinite(rep->loss_after)) return set_err(E_RUNTIME, "lm_step: non-finite loss after update");
     return 0;
 }
+
+/* ------------------------------------------------ first-order baselines */
+/* baselines::full_gradient (first_order.cpp:11-44): exhaustive plan, dL/dr =
+ * 2/M (r + w s s') at every pixel channel, J^T of that. */
+int orc_full_gradient(const slm_gaussians* g, const slm_camera* cams, int n, const float* gts, int loss,
+                      double ssim_weight, double* out) {
+    plan_t* plan = (plan_t*)orc_exhaustive_plan(cams, n);
+    slm_plan cp = {plan->n_views, plan->samples_per_tile, plan->dist, plan->view_camera,
+                   plan->view_offset, plan->px, plan->py, plan->tile, plan->weight};
+    jac_t* jac = (jac_t*)orc_jac_new(g, cams, n, &cp);
+    if (!jac) {
+        orc_plan_free(plan);
+        return E_DOMAIN;
+    }
+    double entries = 0.0;
+    for (int v = 0; v < n; ++v) entries += 3.0 * cams[v].width * cams[v].height;
+    const double scale = 2.0 / entries;
+    double* u = (double*)malloc(sizeof(double) * (jac->rdim + 1));
+    const float* src = gts;
+    size_t entry = 0;
+    for (int v = 0; v < n; ++v) {
+        const int w = cams[v].width, h = cams[v].height;
+        const size_t n3 = 3 * (size_t)w * h;
+        double* img = (double*)malloc(sizeof(double) * (4 * n3 + 1));
+        double *gt = img + n3, *sres = img + 2 * n3, *sdc = img + 3 * n3;
+        for (size_t e = 0; e < n3; ++e) gt[e] = (double)src[e];
+        src += n3;
+        const int rc = orc_render_full(g, &cams[v], img, NULL, NULL);
+        if (rc) return rc;
+        if (loss == SLM_LOSS_MSE_SSIM) orc_ssim_diag_residuals(img, gt, w, h, sres, sdc);
+        for (int64_t s = plan->view_offset[v]; s < plan->view_offset[v + 1]; ++s)
+            for (int c = 0; c < 3; ++c, ++entry) {
+                const size_t e = ((size_t)plan->py[s] * w + plan->px[s]) * 3 + c;
+                double r = img[e] - gt[e];
+                if (loss == SLM_LOSS_MSE_SSIM) r += ssim_weight * sdc[e] * sres[e];
+                u[entry] = scale * r;
+            }
+        free(img);
+    }
+    const int rc = orc_jac_vjp(jac, u, out);
+    free(u);
+    orc_jac_free(jac);
+    orc_plan_free(plan);
+    return rc;
+}
+
+/* GaussianSet::pack / unpack (types.cpp:20-46) */
+static void orc_pack(const slm_gaussians* g, double* p) {
+    for (int i = 0; i < g->count; ++i) {
+        double* b = p + (size_t)NP * i;
+        for (int k = 0; k < 3; ++k) b[k] = g->means[3 * i + k];
+        for (int k = 0; k < 3; ++k) b[3 + k] = g->log_scales[3 * i + k];
+        for (int k = 0; k < 4; ++k) b[6 + k] = g->rotations[4 * i + k];
+        b[10] = g->opacity_logits[i];
+        for (int k = 0; k < 3; ++k) b[11 + k] = g->colors[3 * i + k];
+    }
+}
+static void orc_unpack(const double* p, slm_gaussians* g) {
+    for (int i = 0; i < g->count; ++i) {
+        const double* b = p + (size_t)NP * i;
+        for (int k = 0; k < 3; ++k) g->means[3 * i + k] = b[k];
+        for (int k = 0; k < 3; ++k) g->log_scales[3 * i + k] = b[3 + k];
+        for (int k = 0; k < 4; ++k) g->rotations[4 * i + k] = b[6 + k];
+        g->opacity_logits[i] = b[10];
+        for (int k = 0; k < 3; ++k) g->colors[3 * i + k] = b[11 + k];
+    }
+}
+
+/* group_lr (first_order.cpp:46-52) */
+static double fo_group_lr(const slm_first_order_config* c, int k) {
+    if (k < 3) return c->lr_mean;
+    if (k < 6) return c->lr_scale;
+    if (k < 10) return c->lr_rotation;
+    if (k == 10) return c->lr_opacity;
+    return c->lr_color;
+}
+
+/* adam / rmsprop / sgd_momentum steps (first_order.cpp:56-122) on the packed
+ * ParamVector, then renormalize_rotations. */
+int orc_first_order_step(slm_gaussians* g, double* m1, double* m2, int64_t* step, const double* grad,
+                         const slm_first_order_config* cfg) {
+    const size_t P = (size_t)NP * g->count;
+    double* p = (double*)malloc(sizeof(double) * (P + 1));
+    orc_pack(g, p);
+    ++*step;
+    const long t = (long)(*step - 1);
+    double mean_factor = 1.0;
+    if (cfg->decay_iterations > 0) {
+        const double tt = (double)t / cfg->decay_iterations;
+        mean_factor = pow(cfg->mean_lr_final_factor, tt < 1.0 ? tt : 1.0);
+    }
+    const double c1 = 1.0 - pow(cfg->adam_beta1, (double)*step);
+    const double c2 = 1.0 - pow(cfg->adam_beta2, (double)*step);
+    for (size_t j = 0; j < P; ++j) {
+        const int k = (int)(j % NP);
+        double lr = fo_group_lr(cfg, k);
+        if (k < 3) lr *= mean_factor;
+        const double gj = grad[j];
+        if (cfg->kind == SLM_FO_ADAM) {
+            m1[j] = cfg->adam_beta1 * m1[j] + (1.0 - cfg->adam_beta1) * gj;
+            m2[j] = cfg->adam_beta2 * m2[j] + (1.0 - cfg->adam_beta2) * gj * gj;
+            const double mhat = m1[j] / c1, vhat = m2[j] / c2;
+            p[j] -= lr * mhat / (sqrt(vhat) + cfg->adam_eps);
+        } else if (cfg->kind == SLM_FO_RMSPROP) {
+            m2[j] = cfg->rms_decay * m2[j] + (1.0 - cfg->rms_decay) * gj * gj;
+            p[j] -= lr * gj / (sqrt(m2[j]) + cfg->rms_eps);
+        } else {
+            m1[j] = cfg->momentum * m1[j] - lr * gj;
+            p[j] += m1[j];
+        }
+    }
+    orc_unpack(p, g);
+    renormalize(g);
+    free(p);
+    return 0;
+}

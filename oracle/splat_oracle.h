@@ -85,6 +85,10 @@ int orc_batch_loss(const slm_gaussians* g, const slm_camera* cams, int n_cams, c
 double orc_mse(const double* a, const double* b, int w, int h);
 double orc_psnr(const double* a, const double* b, int w, int h);
 double orc_ssim(const double* a, const double* b, int w, int h);
+int orc_full_gradient(const slm_gaussians* g, const slm_camera* cams, int n_cams, const float* gts, int loss,
+                      double ssim_weight, double* out);
+int orc_first_order_step(slm_gaussians* g, double* m1, double* m2, int64_t* step, const double* grad,
+                         const slm_first_order_config* cfg);
 void orc_ssim_diag_residuals(const double* a, const double* b, int w, int h, double* residual,
                              double* d_center);
 

@@ -32,6 +32,7 @@ CU_SOURCES = {
     "sort.cu": [],
     "metrics.cu": [],
     "sampler.cu": [],
+    "first_order.cu": [],
 }
 CPP_SOURCES = ["runtime.cpp"]
 HEADERS = ["common.cuh", "layout.hpp", "runtime.hpp"]

@@ -135,6 +135,15 @@ struct MetricWindow {
     double w[kMetricWin];
 };
 
+// One first-order step (first_order.cu): per-row learning rates (group rate,
+// mean rows already scaled by the decay factor), and the kind's constants:
+// Adam b1/b2/eps + bias corrections c1/c2, RMSprop b2 = decay, SGD b1 = momentum.
+struct FirstOrderParams {
+    int kind;
+    double lr[kP];
+    double b1, b2, eps, c1, c2;
+};
+
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
 

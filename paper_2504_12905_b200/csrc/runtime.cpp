@@ -564,6 +564,7 @@ struct Jacobian {
     // Pure host work, safe to run concurrently with GPU work on the context.
     void init_host(const slm_plan& plan, int lo, int hi, double inv_total, const std::vector<slm_camera>& cams) {
         draw.on = false;
+        draw.exhaustive = false;
         rdim = 0;
         plan_base = plan.view_offset[lo];
         for (int v = lo; v < hi; ++v) rdim += 3 * (plan.view_offset[v + 1] - plan.view_offset[v]);
@@ -578,6 +579,10 @@ struct Jacobian {
     // picks the pixels from the per-tile CDFs of the render (sampler.cu).
     struct Draw {
         bool on = false;
+        bool exhaustive = false;  // full_gradient: every pixel + u = 2/M (r + w s s') (first_order.cu)
+        const float* sres = nullptr;
+        const float* sdc = nullptr;
+        float ssim_weight = 0.f, scale = 0.f;
         int dist = 0, spt = 0;
         double n_total = 0.0, inv_total = 0.0;
         pinned_vector<double> hU;
@@ -613,6 +618,7 @@ struct Jacobian {
             if (i >= off_lo && i < off_hi) draw.hU[i - off_lo] = u;
         }
         draw.on = true;
+        draw.exhaustive = false;
         draw.dist = dist;
         draw.spt = spt;
         draw.n_total = static_cast<double>(total);
@@ -624,9 +630,27 @@ struct Jacobian {
         weights.clear();  // drawn on the device (lm_step's Jacobian never reads them on the host)
     }
 
+    // Host half of full_gradient's exhaustive plan (sample_plan.cpp:173-197)
+    // over these cameras, laid out tile-major for the raster; u is filled on
+    // the device (first_order.cu) in the same order.
+    void init_host_exhaustive(const std::vector<slm_camera>& cams, const float* sres, const float* sdc,
+                              float ssim_weight, float scale) {
+        draw.hsbase = samples.group_tiles_host(cams, kTile * kTile);
+        draw.on = true;
+        draw.exhaustive = true;
+        draw.sres = sres;
+        draw.sdc = sdc;
+        draw.ssim_weight = ssim_weight;
+        draw.scale = scale;
+        rdim = 3 * samples.total;
+        plan_base = 0;
+        weights.clear();
+    }
+
     // Adopt the host half computed by another (host-only) Jacobian.
     void take_host(Jacobian& o) {
         std::swap(draw.on, o.draw.on);
+        std::swap(draw.exhaustive, o.draw.exhaustive);
         std::swap(draw.dist, o.draw.dist);
         std::swap(draw.spt, o.draw.spt);
         std::swap(draw.n_total, o.draw.n_total);
@@ -649,7 +673,16 @@ struct Jacobian {
     // prepared and rendered).
     void init_device() {
         samples.upload(ctx, batch->hcams, batch->htile_offsets);
-        if (draw.on) {  // weighted distributions: pixels + weights from the render's CDFs
+        if (draw.on && draw.exhaustive) {  // exhaustive plan: pixels + dL/dr in sample order
+            draw.sbase.ensure(std::max<size_t>(draw.hsbase.size(), 1));
+            res_in.ensure(std::max<long long>(rdim, 1));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(draw.sbase.p, draw.hsbase.data(), sizeof(int) * draw.hsbase.size(),
+                                           cudaMemcpyHostToDevice, ctx->stream));
+            launch_exhaustive_residual(batch->cams.p, batch->n_tiles, batch->tile_view.p, draw.sbase.p,
+                                       batch->image.p, batch->gt.p, draw.sres, draw.sdc, draw.ssim_weight,
+                                       draw.scale, samples.spix.p, res_in.p, ctx->stream);
+            ctx->check_launch();
+        } else if (draw.on) {  // weighted distributions: pixels + weights from the render's CDFs
             draw.U.ensure(draw.hU.size());
             draw.sbase.ensure(std::max<size_t>(draw.hsbase.size(), 1));
             SLM_CUDA_CHECK(cudaMemcpyAsync(draw.U.p, draw.hU.data(), sizeof(double) * draw.hU.size(),
@@ -1318,6 +1351,133 @@ static std::vector<double2> batch_ssim(Batch& B, bool planes) {
     return image_metrics<float>(B.ctx, B.image.p, B.gt.p, imgs, true, planes ? B.ssim_res.p : nullptr,
                                 planes ? B.ssim_dc.p : nullptr);
 }
+
+constexpr int kEvalChunk = 8;  // cameras per device batch outside lm_step (bounds the batch buffers)
+
+// batch_loss (lm.cpp:39-54) over the given TrainData cameras, on the device.
+static double batch_loss_dev(Scene& s, Train& t, const std::vector<int>& ids, int loss, double ssim_weight,
+                             Batch& b) {
+    if (loss != SLM_LOSS_MSE && loss != SLM_LOSS_MSE_SSIM) throw std::invalid_argument("batch_loss: unknown loss");
+    double acc = 0.0;
+    for (size_t lo = 0; lo < ids.size(); lo += kEvalChunk) {
+        const size_t hi = std::min(ids.size(), lo + kEvalChunk);
+        std::vector<int> chunk(ids.begin() + lo, ids.begin() + hi);
+        std::vector<slm_camera> cv;
+        for (int i : chunk) {
+            if (i < 0 || i >= static_cast<int>(t.cams.size())) throw std::invalid_argument("camera index");
+            cv.push_back(t.cams[i]);
+        }
+        b.prepare(s, cv);
+        copy_gt(t, b, chunk);
+        b.render(true);
+        const auto sse = b.view_sse();
+        std::vector<double2> ss;
+        if (loss == SLM_LOSS_MSE_SSIM) ss = batch_ssim(b, false);
+        for (int v = 0; v < b.V; ++v) {
+            const double n3 = 3.0 * cv[v].width * cv[v].height;
+            double term = sse[v] / n3;
+            if (loss == SLM_LOSS_MSE_SSIM) term += ssim_weight * ss[v].y / n3;
+            acc += term;
+        }
+    }
+    return ids.empty() ? 0.0 : acc / static_cast<double>(ids.size());
+}
+
+// baselines::full_gradient (first_order.cpp:11-44) over every TrainData camera:
+// exhaustive plan, u = 2/M (r + w s s'), J^T u, accumulated over camera chunks
+// into grad (f32 SoA [14][Gp]).
+static void full_gradient_dev(Scene& s, Train& t, int loss, double ssim_weight, Batch& B, Jacobian& J,
+                              DevBuf<float>& chunk, float* grad) {
+    if (loss != SLM_LOSS_MSE && loss != SLM_LOSS_MSE_SSIM) throw std::invalid_argument("full_gradient: unknown loss");
+    Context* ctx = s.ctx;
+    const size_t P = s.P();
+    chunk.ensure(P);
+    SLM_CUDA_CHECK(cudaMemsetAsync(grad, 0, P * sizeof(float), ctx->stream));
+    double entries = 0.0;
+    for (const auto& c : t.cams) entries += 3.0 * c.width * c.height;
+    const float scale = static_cast<float>(2.0 / entries);
+    J.scene = &s;
+    for (size_t lo = 0; lo < t.cams.size(); lo += kEvalChunk) {
+        const size_t hi = std::min(t.cams.size(), lo + kEvalChunk);
+        std::vector<int> ids;
+        std::vector<slm_camera> cv;
+        for (size_t i = lo; i < hi; ++i) {
+            ids.push_back(static_cast<int>(i));
+            cv.push_back(t.cams[i]);
+        }
+        B.prepare(s, cv);
+        copy_gt(t, B, ids);
+        B.render(false);
+        if (loss == SLM_LOSS_MSE_SSIM) batch_ssim(B, true);
+        J.init_host_exhaustive(cv, loss == SLM_LOSS_MSE_SSIM ? B.ssim_res.p : nullptr, B.ssim_dc.p,
+                               static_cast<float>(ssim_weight), scale);
+        J.init_device();
+        SampleArgs a = J.args();
+        a.in_res = J.res_in.p;
+        launch_sample_raster(kVjp, a, ctx->stream);
+        launch_chain(s.beta32.p, s.G, s.Gp, B.cams.p, B.V, B.rec.p, J.inter.p, nullptr, 0.f, chunk.p, nullptr,
+                     ctx->stream);
+        launch_axpy(grad, chunk.p, static_cast<long long>(P), 1.0f, ctx->stream);
+        ctx->check_launch();
+    }
+}
+
+// first_order_step (first_order.cpp:54-122) parameters for step number `step` (1-based after ++).
+static FirstOrderParams first_order_params(const slm_first_order_config& c, long long step) {
+    if (c.kind < SLM_FO_ADAM || c.kind > SLM_FO_SGD_MOMENTUM) throw std::invalid_argument("unknown first-order optimizer");
+    FirstOrderParams fp{};
+    fp.kind = c.kind;
+    double mean_factor = 1.0;  // mean_lr_factor(cfg, step - 1) (:54-58)
+    if (c.decay_iterations > 0) {
+        const double t = std::min(1.0, static_cast<double>(step - 1) / c.decay_iterations);
+        mean_factor = std::pow(c.mean_lr_final_factor, t);
+    }
+    for (int k = 0; k < kP; ++k) {  // group_lr (:46-52)
+        double lr = k < 3 ? c.lr_mean : k < 6 ? c.lr_scale : k < 10 ? c.lr_rotation : k == 10 ? c.lr_opacity : c.lr_color;
+        if (k < 3) lr *= mean_factor;
+        fp.lr[k] = lr;
+    }
+    if (c.kind == SLM_FO_ADAM) {
+        fp.b1 = c.adam_beta1;
+        fp.b2 = c.adam_beta2;
+        fp.eps = c.adam_eps;
+        fp.c1 = 1.0 - std::pow(c.adam_beta1, static_cast<double>(step));
+        fp.c2 = 1.0 - std::pow(c.adam_beta2, static_cast<double>(step));
+    } else if (c.kind == SLM_FO_RMSPROP) {
+        fp.b2 = c.rms_decay;
+        fp.eps = c.rms_eps;
+    } else {
+        fp.b1 = c.momentum;
+    }
+    return fp;
+}
+
+// FirstOrderState (first_order.hpp:39-51) on the device + the workspaces of
+// full_gradient and batch_loss.
+struct FirstOrder {
+    Scene* scene;
+    DevBuf<double> m1, m2, g64;
+    long long step = 0;
+    Batch batch;
+    Jacobian jac;
+    DevBuf<float> grad, chunk;
+    FirstOrder(const FirstOrder&) = delete;
+    FirstOrder& operator=(const FirstOrder&) = delete;
+    explicit FirstOrder(Scene* s) : scene(s), batch(s->ctx), jac(s->ctx, s, &batch) {
+        const size_t P = s->P();
+        m1.ensure(P);
+        m2.ensure(P);
+        SLM_CUDA_CHECK(cudaMemsetAsync(m1.p, 0, P * sizeof(double), s->ctx->stream));
+        SLM_CUDA_CHECK(cudaMemsetAsync(m2.p, 0, P * sizeof(double), s->ctx->stream));
+    }
+    void apply(const float* g32, const double* g64_aos, const slm_first_order_config& c) {
+        const FirstOrderParams fp = first_order_params(c, step + 1);
+        ++step;
+        launch_first_order_step(scene->beta.p, scene->beta32.p, m1.p, m2.p, g32, g64_aos, scene->G, scene->Gp, fp,
+                                scene->ctx->stream);
+        scene->ctx->check_launch();
+    }
+};
 
 static slm_metric_report metric_report(double2 s, int w, int h) {
     slm_metric_report r{};
@@ -2134,30 +2294,121 @@ int slm_batch_loss(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, do
 int slm_batch_loss_kind(slm_scene* s, slm_train* t, const int32_t* cam_ids, int n, int loss, double ssim_weight,
                         double* out) {
     return guarded([&] {
-        if (loss != SLM_LOSS_MSE && loss != SLM_LOSS_MSE_SSIM) throw std::invalid_argument("batch_loss: unknown loss");
         Context* c = s->impl.ctx;
         c->activate();
-        std::vector<slm_camera> cv;
-        std::vector<int> ids(cam_ids, cam_ids + n);
-        for (int i : ids) {
-            if (i < 0 || i >= static_cast<int>(t->impl.cams.size())) throw std::invalid_argument("camera index");
-            cv.push_back(t->impl.cams[i]);
-        }
         Batch b(c);
-        b.prepare(s->impl, cv);
-        copy_gt(t->impl, b, ids);
-        b.render(true);
-        const auto sse = b.view_sse();
-        std::vector<double2> ss;
-        if (loss == SLM_LOSS_MSE_SSIM) ss = batch_ssim(b, false);
-        double acc = 0.0;
-        for (int v = 0; v < n; ++v) {
-            const double n3 = 3.0 * cv[v].width * cv[v].height;
-            double term = sse[v] / n3;
-            if (loss == SLM_LOSS_MSE_SSIM) term += ssim_weight * ss[v].y / n3;
-            acc += term;
+        *out = batch_loss_dev(s->impl, t->impl, std::vector<int>(cam_ids, cam_ids + n), loss, ssim_weight, b);
+    });
+}
+
+// ---- first-order baselines (baselines/first_order.hpp) on the device
+struct slm_first_order {
+    FirstOrder impl;  // built in place: its Jacobian points at its own Batch
+    explicit slm_first_order(Scene* s) : impl(s) {}
+};
+
+void slm_default_first_order_config(slm_first_order_config* c) {
+    *c = slm_first_order_config{SLM_FO_ADAM, 1.6e-3, 2.5e-2, 5e-2, 5e-3, 1e-3, 0.9, 0.999, 1e-15, 0.99, 1e-15,
+                                0.99, 0.01, 0, SLM_LOSS_MSE, 0.2};
+}
+
+int slm_full_gradient(slm_scene* s, slm_train* t, int loss, double ssim_weight, double* grad_aos) {
+    return guarded([&] {
+        Context* c = s->impl.ctx;
+        c->activate();
+        Batch b(c);
+        Jacobian j(c, &s->impl, &b);
+        DevBuf<float> grad, chunk;
+        grad.ensure(s->impl.P());
+        full_gradient_dev(s->impl, t->impl, loss, ssim_weight, b, j, chunk, grad.p);
+        DevBuf<double> stage;
+        stage.ensure(std::max<size_t>(static_cast<size_t>(kP) * s->impl.G, 1));
+        launch_soa32_to_aos64(grad.p, s->impl.G, s->impl.Gp, stage.p, c->stream);
+        c->check_launch();
+        SLM_CUDA_CHECK(cudaMemcpyAsync(grad_aos, stage.p, sizeof(double) * kP * s->impl.G, cudaMemcpyDeviceToHost,
+                                       c->stream));
+        c->sync();
+    });
+}
+
+int slm_first_order_create(slm_scene* s, slm_first_order** out) {
+    return guarded([&] {
+        s->impl.ctx->activate();
+        *out = new slm_first_order(&s->impl);
+    });
+}
+
+void slm_first_order_destroy(slm_first_order* f) {
+    if (f) {
+        f->impl.scene->ctx->activate();
+        delete f;
+    }
+}
+
+static void soa64_to_aos(const FirstOrder& f, const DevBuf<double>& m, double* out) {
+    const int G = f.scene->G, Gp = f.scene->Gp;
+    std::vector<double> h(static_cast<size_t>(kP) * Gp);
+    SLM_CUDA_CHECK(cudaMemcpyAsync(h.data(), m.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, f.scene->ctx->stream));
+    f.scene->ctx->sync();
+    for (int g = 0; g < G; ++g)
+        for (int k = 0; k < kP; ++k) out[static_cast<size_t>(g) * kP + k] = h[static_cast<size_t>(k) * Gp + g];
+}
+
+static void aos_to_soa64(FirstOrder& f, const double* in, DevBuf<double>& m) {
+    const int G = f.scene->G, Gp = f.scene->Gp;
+    std::vector<double> h(static_cast<size_t>(kP) * Gp, 0.0);
+    for (int g = 0; g < G; ++g)
+        for (int k = 0; k < kP; ++k) h[static_cast<size_t>(k) * Gp + g] = in[static_cast<size_t>(g) * kP + k];
+    SLM_CUDA_CHECK(cudaMemcpyAsync(m.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, f.scene->ctx->stream));
+    f.scene->ctx->sync();
+}
+
+int slm_first_order_moments(slm_first_order* f, double* m1, double* m2, int64_t* step) {
+    return guarded([&] {
+        f->impl.scene->ctx->activate();
+        if (m1) soa64_to_aos(f->impl, f->impl.m1, m1);
+        if (m2) soa64_to_aos(f->impl, f->impl.m2, m2);
+        if (step) *step = f->impl.step;
+    });
+}
+
+int slm_first_order_set_moments(slm_first_order* f, const double* m1, const double* m2, int64_t step) {
+    return guarded([&] {
+        f->impl.scene->ctx->activate();
+        if (step < 0) throw std::invalid_argument("first-order step must be non-negative");
+        aos_to_soa64(f->impl, m1, f->impl.m1);
+        aos_to_soa64(f->impl, m2, f->impl.m2);
+        f->impl.step = step;
+    });
+}
+
+int slm_first_order_apply(slm_first_order* f, const double* grad_aos, const slm_first_order_config* cfg) {
+    return guarded([&] {
+        FirstOrder& F = f->impl;
+        Context* c = F.scene->ctx;
+        c->activate();
+        const size_t n = static_cast<size_t>(kP) * F.scene->G;
+        F.g64.ensure(std::max<size_t>(n, 1));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(F.g64.p, grad_aos, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        F.apply(nullptr, F.g64.p, *cfg);
+        c->sync();
+    });
+}
+
+int slm_first_order_step(slm_first_order* f, slm_train* t, const slm_first_order_config* cfg, double* train_loss) {
+    return guarded([&] {  // one train_run iteration of a first-order optimizer (run.cpp:176-182)
+        FirstOrder& F = f->impl;
+        Context* c = F.scene->ctx;
+        c->activate();
+        F.grad.ensure(F.scene->P());
+        full_gradient_dev(*F.scene, t->impl, cfg->loss, cfg->ssim_weight, F.batch, F.jac, F.chunk, F.grad.p);
+        F.apply(F.grad.p, nullptr, *cfg);
+        if (train_loss) {
+            std::vector<int> ids(t->impl.cams.size());
+            std::iota(ids.begin(), ids.end(), 0);
+            *train_loss = batch_loss_dev(*F.scene, t->impl, ids, cfg->loss, cfg->ssim_weight, F.batch);
         }
-        *out = n == 0 ? 0.0 : acc / n;
+        c->sync();
     });
 }
 

@@ -129,6 +129,11 @@ void launch_weighted_draw(const DevCam* cams, int n_tiles, const int* tile_view,
                           const float* image, const float* gt, const int* contrib, int dist, int spt,
                           const double* U, double n_total, double inv_total, int* spix, float* sw,
                           cudaStream_t st);
+void launch_exhaustive_residual(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
+                                const float* image, const float* gt, const float* sres, const float* sdc,
+                                float ssim_weight, float scale, int* spix, float* u, cudaStream_t st);
+void launch_first_order_step(double* beta, float* beta32, double* m1, double* m2, const float* grad32,
+                             const double* grad64_aos, int G, int Gp, const FirstOrderParams& fp, cudaStream_t st);
 void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
 
 }  // namespace slm

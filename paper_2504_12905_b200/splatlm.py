@@ -15,7 +15,7 @@ import os
 
 import numpy as np
 
-from .types import (CCamera, CGaussians, CLmConfig, CMetricReport, CPcgResult, CPlan, CStepReport, Camera,
+from .types import (CCamera, CFirstOrderConfig, CGaussians, CLmConfig, CMetricReport, CPcgResult, CPlan, CStepReport, Camera,
                     GaussianSet, LmConfig, MetricReport, PcgResult, SamplePlan, StepReport, cameras_to_c, f32ptr,
                     f64ptr, i32ptr, i64ptr)
 
@@ -114,6 +114,14 @@ _SIGS = {
     "slm_lm_step_host": (C.c_int, [_vp, C.POINTER(CGaussians), _vp, C.POINTER(CLmConfig), C.c_int,
                                    _vp, C.POINTER(CStepReport)]),
     "slm_batch_loss": (C.c_int, [_vp, _vp, _i32p, C.c_int, _f64p]),
+    "slm_default_first_order_config": (None, [C.POINTER(CFirstOrderConfig)]),
+    "slm_full_gradient": (C.c_int, [_vp, _vp, C.c_int, C.c_double, _f64p]),
+    "slm_first_order_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "slm_first_order_destroy": (None, [_vp]),
+    "slm_first_order_moments": (C.c_int, [_vp, _f64p, _f64p, _i64p]),
+    "slm_first_order_set_moments": (C.c_int, [_vp, _f64p, _f64p, C.c_int64]),
+    "slm_first_order_apply": (C.c_int, [_vp, _f64p, C.POINTER(CFirstOrderConfig)]),
+    "slm_first_order_step": (C.c_int, [_vp, _vp, C.POINTER(CFirstOrderConfig), _f64p]),
     "slm_batch_loss_kind": (C.c_int, [_vp, _vp, _i32p, C.c_int, C.c_int, C.c_double, _f64p]),
     "slm_ssim_diag_residuals": (C.c_int, [_vp, _f64p, _f64p, C.c_int, C.c_int, _f64p, _f64p]),
     "slm_evaluate": (C.c_int, [_vp, _f64p, _f64p, C.c_int, C.c_int, C.POINTER(CMetricReport)]),
@@ -465,6 +473,23 @@ class Lib(HostSampler):
     def evaluate_split(self, g: GaussianSet, split: "TrainData") -> MetricReport:
         return Scene(self, g).evaluate_split(split)
 
+    def full_gradient(self, g: GaussianSet, data: "TrainData", loss: int = 0, ssim_weight: float = 0.2) -> np.ndarray:
+        """baselines::full_gradient (first_order.cpp:11-44) -> ParamVector (AoS, 14 per Gaussian)."""
+        return Scene(self, g).full_gradient(data, loss, ssim_weight)
+
+    def first_order_step(self, g: GaussianSet, m1: np.ndarray, m2: np.ndarray, step: int, grad: np.ndarray,
+                         cfg) -> int:
+        """baselines::first_order_step (first_order.cpp:115-122), drop-in host form: the state
+        and the caller's moments (AoS, updated in place) go through the device; returns the step."""
+        scene = Scene(self, g)
+        fo = FirstOrder(self, scene)
+        fo.set_moments(m1, m2, step)
+        fo.apply(grad, cfg)
+        a, b, st = fo.moments()
+        m1[:], m2[:] = a, b
+        scene.download(g)
+        return st
+
     def ssim_diag_residuals(self, a, b):
         """metrics::ssim_diag_residuals (image_metrics.cpp:141-178) on the device:
         (residual, d_center), each H x W x 3 f64."""
@@ -546,12 +571,56 @@ class Scene:
     def jacobian(self, cams, plan: SamplePlan) -> "Jacobian":
         return Jacobian(self.L, None, cams, plan, scene=self)
 
+    def full_gradient(self, data: "TrainData", loss: int = 0, ssim_weight: float = 0.2) -> np.ndarray:
+        out = np.zeros(14 * self.count)
+        self.L._check(self.L.dll.slm_full_gradient(self.h, data.h, loss, ssim_weight, f64ptr(out)))
+        return out
+
     def evaluate_split(self, split: "TrainData") -> MetricReport:
         """io::evaluate_split (run.cpp:77-92): mean mse / psnr / ssim over the split's cameras,
         rendered and scored on the device."""
         r = CMetricReport()
         self.L._check(self.L.dll.slm_evaluate_split(self.h, split.h, C.byref(r)))
         return MetricReport(r.mse, r.psnr, r.ssim)
+
+
+class FirstOrder:
+    """baselines::FirstOrderState (first_order.hpp:39-51) in HBM, bound to a device scene."""
+
+    def __init__(self, L: Lib, scene: Scene):
+        self.L, self.scene = L, scene
+        h = _vp()
+        L._check(L.dll.slm_first_order_create(scene.h, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            self.L.dll.slm_first_order_destroy(self.h)
+        except Exception:
+            pass
+
+    def step(self, data: "TrainData", cfg) -> float:
+        """full_gradient + first_order_step + batch_loss (run.cpp:176-182); returns the train loss."""
+        out = C.c_double()
+        cc = cfg.to_c()
+        self.L._check(self.L.dll.slm_first_order_step(self.h, data.h, C.byref(cc), C.byref(out)))
+        return out.value
+
+    def apply(self, grad, cfg) -> None:
+        g = np.ascontiguousarray(grad, np.float64)
+        cc = cfg.to_c()
+        self.L._check(self.L.dll.slm_first_order_apply(self.h, f64ptr(g), C.byref(cc)))
+
+    def moments(self):
+        n = 14 * self.scene.count
+        m1, m2, st = np.zeros(n), np.zeros(n), C.c_int64()
+        self.L._check(self.L.dll.slm_first_order_moments(self.h, f64ptr(m1), f64ptr(m2), C.byref(st)))
+        return m1, m2, st.value
+
+    def set_moments(self, m1, m2, step: int) -> None:
+        a = np.ascontiguousarray(m1, np.float64)
+        b = np.ascontiguousarray(m2, np.float64)
+        self.L._check(self.L.dll.slm_first_order_set_moments(self.h, f64ptr(a), f64ptr(b), step))
 
 
 class Jacobian:

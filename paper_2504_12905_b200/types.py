@@ -57,6 +57,15 @@ class CLmConfig(C.Structure):
                 ("dist", C.c_int32), ("loss", C.c_int32), ("ssim_weight", C.c_double)]
 
 
+class CFirstOrderConfig(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lr_mean", C.c_double), ("lr_color", C.c_double),
+                ("lr_opacity", C.c_double), ("lr_scale", C.c_double), ("lr_rotation", C.c_double),
+                ("adam_beta1", C.c_double), ("adam_beta2", C.c_double), ("adam_eps", C.c_double),
+                ("rms_decay", C.c_double), ("rms_eps", C.c_double), ("momentum", C.c_double),
+                ("mean_lr_final_factor", C.c_double), ("decay_iterations", C.c_int32),
+                ("loss", C.c_int32), ("ssim_weight", C.c_double)]
+
+
 class CStepReport(C.Structure):
     _fields_ = [("iteration", C.c_int32), ("loss_before", C.c_double),
                 ("loss_after", C.c_double), ("eta", C.c_double), ("pcg_iterations", C.c_int32),
@@ -341,6 +350,41 @@ class StepReport:
     pcg_iterations: int = 0
     breakdown: bool = False
     batch: list = field(default_factory=list)
+
+
+FO_ADAM, FO_RMSPROP, FO_SGD_MOMENTUM = 0, 1, 2
+
+
+@dataclass
+class FirstOrderConfig:
+    """baselines::FirstOrderConfig (first_order.hpp:12-37)."""
+    kind: int = FO_ADAM
+    lr_mean: float = 1.6e-3
+    lr_color: float = 2.5e-2
+    lr_opacity: float = 5e-2
+    lr_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-15
+    rms_decay: float = 0.99
+    rms_eps: float = 1e-15
+    momentum: float = 0.99
+    mean_lr_final_factor: float = 0.01
+    decay_iterations: int = 0
+    loss: int = LOSS_MSE
+    ssim_weight: float = 0.2
+
+    @staticmethod
+    def sgd_paper_lrs() -> dict:
+        """first_order.hpp:36 (mean, color, opacity, scale, rotation)."""
+        return dict(lr_mean=0.16, lr_color=0.2, lr_opacity=0.1, lr_scale=0.1, lr_rotation=0.1)
+
+    def to_c(self) -> CFirstOrderConfig:
+        c = CFirstOrderConfig()
+        for name, _ in CFirstOrderConfig._fields_:
+            setattr(c, name, getattr(self, name))
+        return c
 
 
 @dataclass

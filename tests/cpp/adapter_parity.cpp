@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <random>
 
+#include "splatlm/baselines/first_order.hpp"
 #include "splatlm/io/dataset.hpp"
 #include "splatlm/io/image_io.hpp"
 #include "splatlm/io/scene_gen.hpp"
@@ -79,11 +80,27 @@ int main() {
     const Image ia = render::render_full(ref, scene.test.cameras[0]).image;
     const Image ib = io::widen(scene.test.images[0]);
     const auto ma = metrics::evaluate(ia, ib), mb = splatlm_b200::evaluate(dev, ia, ib);
+    // baselines: full_gradient + two Adam steps through the adapter vs the reference
+    const auto fa = baselines::full_gradient(ref, data.cameras, data.images, solver::LossKind::kMse, 0.2);
+    const auto fb = splatlm_b200::full_gradient(dev, ref, data.cameras, data.images, solver::LossKind::kMse, 0.2);
+    double gnum = 0, gden = 0;
+    for (size_t i = 0; i < fa.size(); ++i) {
+        gnum += (fa[i] - fb[i]) * (fa[i] - fb[i]);
+        gden += fa[i] * fa[i];
+    }
+    baselines::FirstOrderConfig fcfg;
+    auto sa = baselines::FirstOrderState::zeros(ref.param_count()), sb = sa;
+    GaussianSet sta = ref, stb = ref;
+    for (int k = 0; k < 2; ++k) {
+        baselines::first_order_step(sa, sta, fa, fcfg);
+        splatlm_b200::first_order_step(dev, sb, stb, fa, fcfg);
+    }
+    const bool fo_equal = sta.pack() == stb.pack() && sa.m1 == sb.m1 && sa.m2 == sb.m2 && sa.step == sb.step;
     std::printf("{\"batches_equal\": %s, \"rng_equal\": %s, \"worst_loss_rel\": %.3e, \"gn_apply_rel\": %.3e, "
                 "\"split_psnr_diff\": %.3e, \"split_ssim_diff\": %.3e, \"eval_ssim_diff\": %.3e, "
-                "\"eval_mse_rel\": %.3e}\n",
+                "\"eval_mse_rel\": %.3e, \"full_gradient_rel\": %.3e, \"first_order_equal\": %s}\n",
                 batches_equal ? "true" : "false", rng_equal ? "true" : "false", worst, std::sqrt(num / den),
                 std::abs(er.psnr - eb.psnr), std::abs(er.ssim - eb.ssim), std::abs(ma.ssim - mb.ssim),
-                std::abs(ma.mse - mb.mse) / ma.mse);
+                std::abs(ma.mse - mb.mse) / ma.mse, std::sqrt(gnum / gden), fo_equal ? "true" : "false");
     return 0;
 }

@@ -230,10 +230,38 @@ def lm_ssim_cases(R):
     return out
 
 
+def first_order_cases(R):
+    """baselines::full_gradient and the Adam / RMSprop / SGD-momentum steps
+    (first_order.cpp) on the toy LM scene, as train_run drives them (run.cpp:176-182)."""
+    from paper_2504_12905_b200.types import FirstOrderConfig
+    out = {}
+    d = np.load(os.path.join(HERE, "lm.npz"))
+    from support import g_cams, g_set
+    tc, ti = g_cams(d["toy_train_cams"]), list(d["toy_train_imgs"])
+    st0 = g_set(d, "lm_init")
+    out["fo_grad_mse"] = R.full_gradient(st0, tc, ti, 0)
+    out["fo_grad_ssim"] = R.full_gradient(st0, tc, ti, 1, 0.2)
+    for kind in (0, 1, 2):
+        extra = FirstOrderConfig.sgd_paper_lrs() if kind == 2 else {}
+        cfg = FirstOrderConfig(kind=kind, decay_iterations=6, **extra)
+        st = st0.copy()
+        m1, m2, step = np.zeros(st.count * 14), np.zeros(st.count * 14), 0
+        losses = []
+        for it in range(6):
+            grad = R.full_gradient(st, tc, ti, 0)
+            step = R.first_order_step(st, m1, m2, step, grad, cfg)
+            losses.append(R.batch_loss(st, tc, ti))
+        out[f"fo{kind}_losses"] = np.array(losses)
+        out.update(set_arrs(f"fo{kind}_final", st))
+        out[f"fo{kind}_m1"], out[f"fo{kind}_m2"] = m1, m2
+    return out
+
+
 def main():
     R = ref()
     groups = {"render": render_cases, "sampling": sampling_cases, "jacobian": jacobian_cases,
-              "lm": lm_cases, "metrics": metrics_cases, "lm_ssim": lm_ssim_cases}
+              "lm": lm_cases, "metrics": metrics_cases, "lm_ssim": lm_ssim_cases,
+              "first_order": first_order_cases}
     only = sys.argv[1:]  # optional group names: regenerate just those
     for name, fn in groups.items():
         if only and name not in only:

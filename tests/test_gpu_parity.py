@@ -369,6 +369,7 @@ def test_cpp_adapter_drop_in(gpu):
     assert r["worst_loss_rel"] < TOL and r["gn_apply_rel"] < TOL
     assert r["split_psnr_diff"] < 1e-3 and r["split_ssim_diff"] < 1e-5
     assert r["eval_ssim_diff"] <= 1e-12 and r["eval_mse_rel"] <= 1e-12
+    assert r["full_gradient_rel"] < TOL and r["first_order_equal"]
 
 
 @pytest.mark.gpu
@@ -536,3 +537,59 @@ def test_lm_weighted_distributions_vs_oracle(gpu, port, dist):
     print("dist", dist, "worst loss rel err", worst)
     assert worst < TOL
     assert rg() == ro()
+
+
+# ----------------------------------------------------------------- first-order baselines (§8f rank 4)
+@pytest.mark.parametrize("loss", [0, 1])
+def test_full_gradient_vs_reference(gpu, loss):
+    """baselines::full_gradient on the device (exhaustive plan laid out tile-major,
+    u = 2/M (r + w s s'), the LM path's J^T pass) vs the reference's gradient."""
+    d = golden("first_order")
+    dl = golden("lm")
+    split = gpu.train_data(g_cams(dl["toy_train_cams"]), list(dl["toy_train_imgs"]))
+    g = gpu.full_gradient(g_set(dl, "lm_init"), split, loss, 0.2)
+    err = norm_rel(g, d["fo_grad_ssim" if loss else "fo_grad_mse"])
+    print("full_gradient rel err", err)
+    assert err < TOL
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_first_order_step_bitwise(gpu, port, kind):
+    """first_order_step on the device on a given gradient: f64 state and moments, the
+    reference's operation order, so state and moments are bitwise the C restatement's
+    (which is bitwise the reference's, tests/test_oracle.py)."""
+    from paper_2504_12905_b200.types import FirstOrderConfig
+    d = golden("first_order")
+    st0 = g_set(golden("lm"), "lm_init")
+    cfg = FirstOrderConfig(kind=kind, decay_iterations=3)
+    a, b = st0.copy(), st0.copy()
+    n = 14 * st0.count
+    ma1, ma2, mb1, mb2, sa, sb = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(n), 0, 0
+    for it in range(4):
+        grad = d["fo_grad_mse"] * (1.0 + 0.5 * it)
+        sa = gpu.first_order_step(a, ma1, ma2, sa, grad, cfg)
+        sb = port.first_order_step(b, mb1, mb2, sb, grad, cfg)
+    assert sa == sb == 4
+    assert np.array_equal(a.pack(), b.pack())
+    assert np.array_equal(ma1, mb1) and np.array_equal(ma2, mb2)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_first_order_training_vs_reference(gpu, kind):
+    """Six train_run iterations of a first-order optimizer entirely on the device
+    (full_gradient + step + batch_loss, run.cpp:176-182) vs the reference's losses."""
+    from paper_2504_12905_b200 import splatlm
+    from paper_2504_12905_b200.types import FirstOrderConfig
+    d = golden("first_order")
+    dl = golden("lm")
+    data = gpu.train_data(g_cams(dl["toy_train_cams"]), list(dl["toy_train_imgs"]))
+    scene = splatlm.Scene(gpu, g_set(dl, "lm_init"))
+    fo = splatlm.FirstOrder(gpu, scene)
+    extra = FirstOrderConfig.sgd_paper_lrs() if kind == 2 else {}
+    cfg = FirstOrderConfig(kind=kind, decay_iterations=6, **extra)
+    worst = 0.0
+    for it in range(6):
+        worst = max(worst, rel_error(fo.step(data, cfg), d[f"fo{kind}_losses"][it]))
+    print("kind", kind, "worst loss rel err", worst)
+    assert worst < TOL
+    assert norm_rel(scene.download().pack(), g_set(d, f"fo{kind}_final").pack()) < 1e-3

@@ -253,3 +253,39 @@ def test_lm_trajectory_mse_ssim(port):
     assert rng() == int(d["lms_rng_next"][0])
     bl = port.batch_loss(st, tc, list(dl["toy_train_imgs"]), loss=1, ssim_weight=0.2)
     assert bl == pytest.approx(float(d["lms_batch_loss"][0]), rel=1e-12)
+
+
+def test_first_order_baselines_vs_reference(port):
+    """baselines::full_gradient and the Adam / RMSprop / SGD-momentum trajectories
+    (first_order.cpp) on the toy scene vs the reference's outputs (golden)."""
+    from paper_2504_12905_b200.types import FirstOrderConfig
+    d = golden("first_order")
+    dl = golden("lm")
+    tc, ti = g_cams(dl["toy_train_cams"]), list(dl["toy_train_imgs"])
+    st0 = g_set(dl, "lm_init")
+    assert norm_rel(port.full_gradient(st0, tc, ti, 0), d["fo_grad_mse"]) < 1e-12
+    assert norm_rel(port.full_gradient(st0, tc, ti, 1, 0.2), d["fo_grad_ssim"]) < 1e-12
+    for kind in (0, 1, 2):
+        extra = FirstOrderConfig.sgd_paper_lrs() if kind == 2 else {}
+        cfg = FirstOrderConfig(kind=kind, decay_iterations=6, **extra)
+        st = st0.copy()
+        m1, m2, step = np.zeros(st.count * 14), np.zeros(st.count * 14), 0
+        for it in range(6):
+            step = port.first_order_step(st, m1, m2, step, port.full_gradient(st, tc, ti, 0), cfg)
+            assert port.batch_loss(st, tc, ti) == pytest.approx(d[f"fo{kind}_losses"][it], rel=1e-12)
+        assert norm_rel(st.pack(), g_set(d, f"fo{kind}_final").pack()) < 1e-12
+        assert norm_rel(m1, d[f"fo{kind}_m1"]) < 1e-12 or not d[f"fo{kind}_m1"].any()
+
+
+def test_first_order_default_config(reflib):
+    """FirstOrderConfig defaults (first_order.hpp:12-37) match the reference's."""
+    import ctypes as C
+    from paper_2504_12905_b200.types import CFirstOrderConfig, FirstOrderConfig
+    fn = reflib.lib.ref_default_first_order_config
+    fn.argtypes = [C.POINTER(CFirstOrderConfig)]
+    fn.restype = None
+    c = CFirstOrderConfig()
+    fn(C.byref(c))
+    mine = FirstOrderConfig().to_c()
+    for name, _ in CFirstOrderConfig._fields_:
+        assert getattr(c, name) == getattr(mine, name), name
