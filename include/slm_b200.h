@@ -189,6 +189,11 @@ int slm_ssim_diag_residuals(slm_context* ctx, const double* a, const double* b, 
  * the ground truth) and average mse / psnr / ssim over the cameras. */
 int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out);
 
+/* ---- checkpoints (io/checkpoint.hpp; byte format SPLMGS01, checkpoint.cpp:12-82) */
+int slm_save_checkpoint(const char* path, const slm_gaussians* g); /* + path.meta.txt */
+int slm_checkpoint_count(const char* path, int* count);
+int slm_load_checkpoint(const char* path, slm_gaussians* out);     /* out->count must match */
+
 /* ---- io helpers the harness uses (io/dataset.cpp:138-166, io/scene_gen.cpp) */
 int slm_random_init(int count, const double* cube_min, const double* cube_max, slm_rng* rng,
                     slm_gaussians* out);

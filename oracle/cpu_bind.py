@@ -332,6 +332,38 @@ class CpuLib:
                                            C.byref(cc)))
         return st.value
 
+    # ---- reference-only entry points (oracle/_ref): run driver and checkpoints
+    def train_run_toy(self, out_dir: str, optimizer: str, iterations: int, lm, fo, seed: int = 1,
+                      gaussians: int = 0, eval_every: int = 50, deterministic: bool = True,
+                      scene_seed: int = 20214, toy=(20, 8, 4, 64)):
+        """io::train_run (run.cpp:120-212) on the toy scene; returns (final_train_loss, [mse, psnr, ssim])."""
+        fn = self.lib.ref_train_run_toy
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                       C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(CLmConfig), C.POINTER(CFirstOrderConfig),
+                       _f64p, _f64p]
+        loss, test = C.c_double(), np.zeros(3)
+        lc, fc = lm.to_c(), fo.to_c()
+        self._check(fn(os.fsencode(out_dir), optimizer.encode(), iterations, seed, gaussians, eval_every,
+                       int(deterministic), scene_seed, *toy, C.byref(lc), C.byref(fc), C.byref(loss), f64ptr(test)))
+        return loss.value, test
+
+    def save_checkpoint(self, path: str, g: GaussianSet) -> None:
+        fn = self.lib.ref_save_checkpoint
+        fn.restype, fn.argtypes = C.c_int, [C.c_char_p, _f64p, C.c_int64]
+        p = np.ascontiguousarray(g.pack())
+        self._check(fn(os.fsencode(path), f64ptr(p), g.count))
+
+    def load_checkpoint(self, path: str) -> GaussianSet:
+        fn = self.lib.ref_load_checkpoint
+        fn.restype, fn.argtypes = C.c_int, [C.c_char_p, _f64p, C.c_int64, C.POINTER(C.c_int64)]
+        n = C.c_int64()
+        empty = np.zeros(1)
+        self._check(fn(os.fsencode(path), f64ptr(empty), 0, C.byref(n)))
+        p = np.zeros(14 * n.value)
+        self._check(fn(os.fsencode(path), f64ptr(p), p.size, C.byref(n)))
+        return GaussianSet.unpack(p)
+
     def ssim_diag_residuals(self, a, b):
         """metrics::ssim_diag_residuals -> (residual, d_center), both H x W x 3."""
         a = np.ascontiguousarray(a, np.float64)

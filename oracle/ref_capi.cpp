@@ -20,7 +20,9 @@
 #include "splatlm/autodiff/jacobian.hpp"
 #include "splatlm/baselines/first_order.hpp"
 #include "splatlm/core/parallel.hpp"
+#include "splatlm/io/checkpoint.hpp"
 #include "splatlm/io/dataset.hpp"
+#include "splatlm/io/run.hpp"
 #include "splatlm/io/scene_gen.hpp"
 #include "splatlm/metrics/image_metrics.hpp"
 #include "splatlm/render/rasterizer.hpp"
@@ -663,6 +665,50 @@ int ref_first_order_step(slm_gaussians* g, double* m1, double* m2, int64_t* step
         std::copy(st.m1.begin(), st.m1.end(), m1);
         std::copy(st.m2.begin(), st.m2.end(), m2);
         *step = st.step;
+    });
+}
+// io::train_run (run.cpp:120-212) on the toy scene; outputs under out_dir
+int ref_train_run_toy(const char* out_dir, const char* optimizer, int iterations, uint64_t seed, int gaussians,
+                      int eval_every, int deterministic, uint64_t scene_seed, int toy_gaussians, int train_cams,
+                      int test_cams, int image_size, const slm_lm_config* lm, const slm_first_order_config* fo,
+                      double* final_train_loss, double* final_test) {
+    return guarded([&] {
+        io::RunConfig cfg;
+        cfg.scene = "toy";
+        cfg.optimizer = optimizer;
+        cfg.iterations = iterations;
+        cfg.seed = seed;
+        cfg.out_dir = out_dir;
+        cfg.gaussians = gaussians;
+        cfg.lm = to_cfg(*lm);
+        cfg.first_order = to_fo(*fo);
+        cfg.eval_every = eval_every;
+        cfg.deterministic = deterministic != 0;
+        cfg.scene_seed = scene_seed;
+        cfg.toy.gaussians = toy_gaussians;
+        cfg.toy.train_cameras = train_cams;
+        cfg.toy.test_cameras = test_cams;
+        cfg.toy.image_size = image_size;
+        const auto r = io::train_run(cfg);
+        *final_train_loss = r.final_train_loss;
+        final_test[0] = r.final_test.mse;
+        final_test[1] = r.final_test.psnr;
+        final_test[2] = r.final_test.ssim;
+    });
+}
+
+// io::load_checkpoint / save_checkpoint (checkpoint.cpp:45-82)
+int ref_load_checkpoint(const char* path, double* params_aos, int64_t capacity, int64_t* count) {
+    return guarded([&] {
+        const GaussianSet g = io::load_checkpoint(path);
+        *count = g.count;
+        const auto p = g.pack();
+        if (static_cast<int64_t>(p.size()) <= capacity) std::copy(p.begin(), p.end(), params_aos);
+    });
+}
+int ref_save_checkpoint(const char* path, const double* params_aos, int64_t count) {
+    return guarded([&] {
+        io::save_checkpoint(path, GaussianSet::unpack(ParamVector(params_aos, params_aos + 14 * count)));
     });
 }
 

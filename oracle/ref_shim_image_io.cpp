@@ -1,7 +1,8 @@
 // TEST INFRASTRUCTURE ONLY: stands in for the reference's io/image_io.cpp,
 // which needs libpng (absent here).  Provides the two float<->double image
 // conversions the hot path uses (image_io.hpp:22-23, semantics of
-// image_io.cpp:12-25: element-wise static_cast) and PNG stubs that throw.
+// image_io.cpp:12-25: element-wise static_cast), a no-op 8-bit PNG writer
+// and PNG stubs that throw.
 #include <stdexcept>
 
 #include "splatlm/io/image_io.hpp"
@@ -23,9 +24,9 @@ ImageF narrow(const Image& img) {
     return out;
 }
 
-void write_png8(const std::filesystem::path&, const Image&) {
-    throw std::runtime_error("PNG output is not available in the oracle build");
-}
+// train_run writes test renders after each evaluation (run.cpp:95-104); the
+// oracle build has no libpng, so they are skipped (nothing else depends on them).
+void write_png8(const std::filesystem::path&, const Image&) {}
 void write_png16(const std::filesystem::path&, const Image&) {
     throw std::runtime_error("PNG output is not available in the oracle build");
 }

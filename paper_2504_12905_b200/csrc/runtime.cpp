@@ -13,6 +13,7 @@
 #include <array>
 #include <chrono>
 #include <cstdlib>
+#include <fstream>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -2483,6 +2484,102 @@ int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out) {
             mean.ssim /= n;
         }
         *out = mean;
+    });
+}
+
+// ---- checkpoints (io/checkpoint.cpp:12-82): "SPLMGS01", u32 version 1,
+// u64 count, then the ParamVector as little-endian f64 (14 per Gaussian), plus
+// the .meta.txt sidecar -- byte-identical to the reference's files.
+namespace {
+constexpr char kCkptMagic[8] = {'S', 'P', 'L', 'M', 'G', 'S', '0', '1'};
+constexpr uint32_t kCkptVersion = 1;
+
+void put_le(std::ostream& out, uint64_t v, int bytes) {
+    char b[8];
+    for (int i = 0; i < bytes; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
+    out.write(b, bytes);
+}
+uint64_t get_le(std::istream& in, int bytes) {
+    unsigned char b[8] = {};
+    in.read(reinterpret_cast<char*>(b), bytes);
+    uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(b[i]) << (8 * i);
+    return v;
+}
+void pack_set(const slm_gaussians& g, std::vector<double>& p) {  // GaussianSet::pack (types.cpp:20-33)
+    p.resize(static_cast<size_t>(kP) * g.count);
+    for (int i = 0; i < g.count; ++i) {
+        double* b = p.data() + static_cast<size_t>(kP) * i;
+        for (int k = 0; k < 3; ++k) b[k] = g.means[3 * i + k];
+        for (int k = 0; k < 3; ++k) b[3 + k] = g.log_scales[3 * i + k];
+        for (int k = 0; k < 4; ++k) b[6 + k] = g.rotations[4 * i + k];
+        b[10] = g.opacity_logits[i];
+        for (int k = 0; k < 3; ++k) b[11 + k] = g.colors[3 * i + k];
+    }
+}
+// reads the header; returns the Gaussian count (stream positioned at the parameters)
+uint64_t read_header(std::ifstream& in, const std::string& path) {
+    char magic[8];
+    in.read(magic, 8);
+    if (!in || std::memcmp(magic, kCkptMagic, 8) != 0) throw std::runtime_error("not a splatlm checkpoint: " + path);
+    if (get_le(in, 4) != kCkptVersion) throw std::runtime_error("unsupported checkpoint version in " + path);
+    return get_le(in, 8);
+}
+}  // namespace
+
+int slm_save_checkpoint(const char* path, const slm_gaussians* g) {
+    return guarded([&] {
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw std::runtime_error(std::string("cannot write checkpoint: ") + path);
+        out.write(kCkptMagic, sizeof kCkptMagic);
+        put_le(out, kCkptVersion, 4);
+        put_le(out, static_cast<uint64_t>(g->count), 8);
+        std::vector<double> p;
+        pack_set(*g, p);
+        for (double d : p) {
+            uint64_t u;
+            std::memcpy(&u, &d, 8);
+            put_le(out, u, 8);
+        }
+        if (!out) throw std::runtime_error(std::string("checkpoint write failed: ") + path);
+        std::ofstream meta(std::string(path) + ".meta.txt");
+        meta << "splatlm checkpoint v" << kCkptVersion << "\n"
+             << "gaussians: " << g->count << "\n"
+             << "parameters: " << p.size() << "\n"
+             << "layout: per-Gaussian [mean(3), log_scale(3), rotation wxyz(4), "
+                "opacity_logit(1), color(3)], little-endian float64\n";
+    });
+}
+
+int slm_checkpoint_count(const char* path, int* count) {
+    return guarded([&] {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw std::runtime_error(std::string("cannot read checkpoint: ") + path);
+        *count = static_cast<int>(read_header(in, path));
+    });
+}
+
+int slm_load_checkpoint(const char* path, slm_gaussians* out) {
+    return guarded([&] {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw std::runtime_error(std::string("cannot read checkpoint: ") + path);
+        const uint64_t count = read_header(in, path);
+        if (static_cast<int64_t>(count) != out->count)
+            throw std::invalid_argument("load_checkpoint: output GaussianSet has the wrong count");
+        std::vector<double> p(static_cast<size_t>(kP) * count);
+        for (double& d : p) {
+            const uint64_t u = get_le(in, 8);
+            std::memcpy(&d, &u, 8);
+        }
+        if (!in) throw std::runtime_error(std::string("truncated checkpoint: ") + path);
+        for (uint64_t i = 0; i < count; ++i) {  // GaussianSet::unpack (types.cpp:35-46)
+            const double* b = p.data() + kP * i;
+            for (int k = 0; k < 3; ++k) out->means[3 * i + k] = b[k];
+            for (int k = 0; k < 3; ++k) out->log_scales[3 * i + k] = b[3 + k];
+            for (int k = 0; k < 4; ++k) out->rotations[4 * i + k] = b[6 + k];
+            out->opacity_logits[i] = b[10];
+            for (int k = 0; k < 3; ++k) out->colors[3 * i + k] = b[11 + k];
+        }
     });
 }
 

@@ -114,6 +114,9 @@ _SIGS = {
     "slm_lm_step_host": (C.c_int, [_vp, C.POINTER(CGaussians), _vp, C.POINTER(CLmConfig), C.c_int,
                                    _vp, C.POINTER(CStepReport)]),
     "slm_batch_loss": (C.c_int, [_vp, _vp, _i32p, C.c_int, _f64p]),
+    "slm_save_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(CGaussians)]),
+    "slm_checkpoint_count": (C.c_int, [C.c_char_p, _i32p]),
+    "slm_load_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(CGaussians)]),
     "slm_default_first_order_config": (None, [C.POINTER(CFirstOrderConfig)]),
     "slm_full_gradient": (C.c_int, [_vp, _vp, C.c_int, C.c_double, _f64p]),
     "slm_first_order_create": (C.c_int, [_vp, C.POINTER(_vp)]),
@@ -472,6 +475,20 @@ class Lib(HostSampler):
 
     def evaluate_split(self, g: GaussianSet, split: "TrainData") -> MetricReport:
         return Scene(self, g).evaluate_split(split)
+
+    def save_checkpoint(self, path: str, g: GaussianSet) -> None:
+        """io::save_checkpoint (checkpoint.cpp:45-66): SPLMGS01 file + .meta.txt sidecar."""
+        cg = g.to_c()
+        self._check(self.dll.slm_save_checkpoint(os.fsencode(path), C.byref(cg)))
+
+    def load_checkpoint(self, path: str) -> GaussianSet:
+        """io::load_checkpoint (checkpoint.cpp:68-82)."""
+        n = C.c_int32()
+        self._check(self.dll.slm_checkpoint_count(os.fsencode(path), C.byref(n)))
+        g = GaussianSet(n.value)
+        cg = g.to_c()
+        self._check(self.dll.slm_load_checkpoint(os.fsencode(path), C.byref(cg)))
+        return g
 
     def full_gradient(self, g: GaussianSet, data: "TrainData", loss: int = 0, ssim_weight: float = 0.2) -> np.ndarray:
         """baselines::full_gradient (first_order.cpp:11-44) -> ParamVector (AoS, 14 per Gaussian)."""

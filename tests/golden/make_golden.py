@@ -257,11 +257,34 @@ def first_order_cases(R):
     return out
 
 
+RUN_CASES = {  # io::train_run on the toy scene, deterministic mode
+    "lm": dict(optimizer="lm", iterations=6, eval_every=3),
+    "adam": dict(optimizer="adam", iterations=4, eval_every=2),
+}
+
+
+def run_cases(R):
+    """io::train_run outputs (metrics.csv, summary.json, checkpoint.bin + .meta.txt) for the
+    toy scene, stored as bytes (run.cpp:120-212, checkpoint.cpp:45-66)."""
+    import tempfile
+
+    from paper_2504_12905_b200.types import FirstOrderConfig
+    out = {}
+    for name, c in RUN_CASES.items():
+        with tempfile.TemporaryDirectory() as d:
+            R.train_run_toy(d, c["optimizer"], c["iterations"], LmConfig(pcg_iters_initial=8), FirstOrderConfig(),
+                            eval_every=c["eval_every"], deterministic=True)
+            for f in ("metrics.csv", "summary.json", "checkpoint.bin", "checkpoint.bin.meta.txt"):
+                with open(os.path.join(d, f), "rb") as fh:
+                    out[f"{name}_{f}"] = np.frombuffer(fh.read(), np.uint8)
+    return out
+
+
 def main():
     R = ref()
     groups = {"render": render_cases, "sampling": sampling_cases, "jacobian": jacobian_cases,
               "lm": lm_cases, "metrics": metrics_cases, "lm_ssim": lm_ssim_cases,
-              "first_order": first_order_cases}
+              "first_order": first_order_cases, "run": run_cases}
     only = sys.argv[1:]  # optional group names: regenerate just those
     for name, fn in groups.items():
         if only and name not in only:

@@ -116,3 +116,50 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(splatlm.CudaUnavailable):
         splatlm.Lib()
+
+
+# ---- run-driver wire formats: host code, no GPU needed
+def _golden_bytes(name):
+    return bytes(golden("run")[name])
+
+
+def test_checkpoint_bytes_match_reference(tmp_path):
+    """io::save_checkpoint / load_checkpoint (checkpoint.cpp:12-82): a file written by the
+    reference loads here bit for bit, and writing it back reproduces the reference's bytes
+    and .meta.txt exactly."""
+    import ctypes as C
+
+    from paper_2504_12905_b200.types import CGaussians, GaussianSet
+    dll = splatlm.load_library()
+    src = tmp_path / "ref.bin"
+    src.write_bytes(_golden_bytes("lm_checkpoint.bin"))
+    n = C.c_int32()
+    assert dll.slm_checkpoint_count(os.fsencode(str(src)), C.byref(n)) == 0 and n.value == 40
+    g = GaussianSet(n.value)
+    cg = g.to_c()
+    assert dll.slm_load_checkpoint(os.fsencode(str(src)), C.byref(cg)) == 0
+    raw = np.frombuffer(_golden_bytes("lm_checkpoint.bin")[20:], "<f8")
+    assert np.array_equal(g.pack(), raw)
+    out = tmp_path / "mine.bin"
+    assert dll.slm_save_checkpoint(os.fsencode(str(out)), C.byref(cg)) == 0
+    assert out.read_bytes() == _golden_bytes("lm_checkpoint.bin")
+    assert (tmp_path / "mine.bin.meta.txt").read_bytes() == _golden_bytes("lm_checkpoint.bin.meta.txt")
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"NOTSPLAT" + bytes(12))
+    assert dll.slm_checkpoint_count(os.fsencode(str(bad)), C.byref(n)) != 0
+    assert b"not a splatlm checkpoint" in dll.slm_last_error()
+    g2 = GaussianSet(3)
+    cg2 = g2.to_c()
+    assert dll.slm_load_checkpoint(os.fsencode(str(src)), C.byref(cg2)) != 0  # count mismatch
+
+
+def test_summary_json_layout_matches_reference():
+    """summary.json is nlohmann dump(2): sorted keys, shortest round-trip doubles; the
+    driver's writer reproduces the reference's bytes from the same values."""
+    import json
+
+    from paper_2504_12905_b200.run import METRICS_CSV_HEADER, _json_dump
+    for case in ("lm", "adam"):
+        ref = _golden_bytes(f"{case}_summary.json").decode()
+        assert _json_dump(json.loads(ref)) == ref
+        assert _golden_bytes(f"{case}_metrics.csv").decode().splitlines()[0] == METRICS_CSV_HEADER

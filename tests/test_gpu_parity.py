@@ -593,3 +593,51 @@ def test_first_order_training_vs_reference(gpu, kind):
     print("kind", kind, "worst loss rel err", worst)
     assert worst < TOL
     assert norm_rel(scene.download().pack(), g_set(d, f"fo{kind}_final").pack()) < 1e-3
+
+
+# ----------------------------------------------------------------- run driver (§8f rank 3)
+@pytest.mark.parametrize("case", ["lm", "adam"])
+def test_train_run_matches_reference(gpu, tmp_path, case):
+    """io::train_run on the toy scene, deterministic mode, every step on the device vs the
+    reference's own run (tests/golden/run.npz): metrics.csv has the same header, rows and
+    empty-field pattern with values within tolerance, summary.json the same keys and
+    settings, checkpoint.bin the same header and .meta.txt with parameters close."""
+    import json
+
+    from paper_2504_12905_b200.run import RunConfig, train_run
+    from paper_2504_12905_b200.types import GaussianSet
+    iters, every = (6, 3) if case == "lm" else (4, 2)
+    cfg = RunConfig(optimizer=case, iterations=iters, eval_every=every, out_dir=str(tmp_path),
+                    deterministic=True, lm=LmConfig(pcg_iters_initial=8))
+    res = train_run(gpu, cfg)
+    g = golden("run")
+    mine = (tmp_path / "metrics.csv").read_text().splitlines()
+    ref = bytes(g[f"{case}_metrics.csv"]).decode().splitlines()
+    assert mine[0] == ref[0] and len(mine) == len(ref)
+    for a, b in zip(mine[1:], ref[1:]):
+        fa, fb = a.split(","), b.split(",")
+        assert [x == "" for x in fa] == [x == "" for x in fb], (a, b)
+        assert fa[0] == fb[0] and fa[6:] == fb[6:]  # iter, pcg_iters, breakdown
+        assert rel_error(float(fa[2]), float(fb[2])) < TOL  # train_loss
+        if fb[3]:
+            assert abs(float(fa[3]) - float(fb[3])) < 0.01 and abs(float(fa[4]) - float(fb[4])) < 1e-3
+        if fb[5]:
+            assert float(fa[5]) == pytest.approx(float(fb[5]), rel=1e-6)
+    sm, sr = json.loads((tmp_path / "summary.json").read_text()), json.loads(bytes(g[f"{case}_summary.json"]))
+    assert sm.keys() == sr.keys()
+    for k, v in sr.items():
+        if isinstance(v, float) and k not in ("damping",):
+            assert abs(sm[k] - v) <= 1e-3 * max(1.0, abs(v)), k
+        else:
+            assert sm[k] == v, k
+    ck = (tmp_path / "checkpoint.bin").read_bytes()
+    ref_ck = bytes(g[f"{case}_checkpoint.bin"])
+    assert ck[:20] == ref_ck[:20] and len(ck) == len(ref_ck)
+    assert (tmp_path / "checkpoint.bin.meta.txt").read_bytes() == bytes(g[f"{case}_checkpoint.bin.meta.txt"])
+    assert norm_rel(np.frombuffer(ck[20:], "<f8"), np.frombuffer(ref_ck[20:], "<f8")) < 1e-3
+    assert res.final_train_loss == pytest.approx(sr["final_train_loss"], rel=TOL)
+    # eval_run on the checkpoint reproduces the final test metrics
+    from paper_2504_12905_b200.run import eval_run
+    ev = eval_run(gpu, RunConfig(out_dir=str(tmp_path / "eval")), res.checkpoint)
+    assert ev.psnr == pytest.approx(res.final_test.psnr, abs=1e-9)
+    assert GaussianSet  # noqa
