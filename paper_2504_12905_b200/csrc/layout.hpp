@@ -84,6 +84,10 @@ struct SampleArgs {
     const long long* wbase;
     const float* rstream;
     float* rstream_out;
+    // Per-window column masks (k_alpha, once per state/plan), same indexing as
+    // masks: lane k's word = the pixels that blend compacted entry k.
+    const unsigned* cols;
+    unsigned* cols_out;
 };
 
 constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)
@@ -105,6 +109,7 @@ struct DiagArgs {
     const int* glist;
     const int* gcount;
     const long long* mask_off;
+    const unsigned* cols;  // column masks (SampleArgs::cols)
 };
 
 // Scratch of the radix tile-list construction (sort.cu), sized by the runtime:

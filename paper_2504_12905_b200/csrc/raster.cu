@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
         blk[8 * 32 + lane] = rb;
         unsigned m = c.active ? masks[32 * w + lane] : 0u;
         const int npc = __reduce_max_sync(0xffffffffu, __popc(m));
+        A.cols_out[A.mask_off[gi] + 32 * w + lane] = transpose32(m, lane);
         __syncwarp();
         for (int i = 0; m; m &= m - 1, ++i) {
             const int k = __ffs(m) - 1;
@@ -797,6 +798,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     win_index(c, W, 1, lane, m_nxt, g_nxt);
     int rows = max_popc(m_cur);
     if (W.nwin > 0) ap.issue(0, rows, lane);
+    const unsigned* cols = A.cols + A.mask_off[gi];
+    unsigned col_nxt = W.nwin > 0 ? cols[lane] : 0u;
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = m_cur;
@@ -808,7 +811,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         m_cur = m_nxt;
         g_cur = g_nxt;
         win_index(c, W, w + 2, lane, m_nxt, g_nxt);
-        const unsigned col = transpose32(m0, lane);  // lane k: pixels that blend entry k
+        const unsigned col = col_nxt;  // lane k: pixels that blend entry k
+        if (w + 1 < W.nwin) col_nxt = cols[32 * (w + 1) + lane];
         const float* sp = ap.wait(w) + lane;
         const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
@@ -944,7 +948,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
         }
         __syncwarp();
         prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
-        const unsigned col = transpose32(m0, lane);
+        const unsigned col = A.cols[A.mask_off[gi] + 32 * w + lane];
         const int nent = min(32, W.nun - w * 32);
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {

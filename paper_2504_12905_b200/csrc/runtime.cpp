@@ -411,7 +411,7 @@ struct Samples {
     DevBuf<int> spix, sorig;
     DevBuf<float> sw;
     DevBuf<long long> mask_off;
-    DevBuf<unsigned> masks;
+    DevBuf<unsigned> masks, cols;
     DevBuf<int> glist, gcount, grows;
     DevBuf<long long> srow_off, wbase;
     DevBuf<float> astream, rstream;
@@ -516,6 +516,7 @@ struct Samples {
         cudaStream_t st = ctx->stream;
         mask_off.ensure(std::max<size_t>(hoff.size(), 1));
         masks.ensure(std::max<long long>(mask_words, 1));
+        cols.ensure(std::max<long long>(mask_words, 1));
         glist.ensure(std::max<long long>(mask_words, 1));
         gcount.ensure(std::max<size_t>(hgroups.size(), 1));
         grows.ensure(std::max<size_t>(hgroups.size(), 1));
@@ -743,6 +744,7 @@ struct Jacobian {
         SampleArgs b = args();
         b.astream_out = samples.astream.p;
         b.rstream_out = samples.rstream.p;
+        b.cols_out = samples.cols.p;
         launch_alpha(b, ctx->stream);
         ctx->check_launch();
         ctx->sync();  // hrow_off is read by the async copy
@@ -773,6 +775,7 @@ struct Jacobian {
         a.astream = samples.astream.p;
         a.wbase = samples.wbase.p;
         a.rstream = samples.rstream.p;
+        a.cols = samples.cols.p;
         return a;
     }
 
@@ -849,6 +852,7 @@ struct Jacobian {
         d.glist = samples.glist.p;
         d.gcount = samples.gcount.p;
         d.mask_off = samples.mask_off.p;
+        d.cols = samples.cols.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
                              batch->rec.p, diagacc.p, dout, ctx->stream);
