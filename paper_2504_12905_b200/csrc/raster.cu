@@ -320,6 +320,15 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     }
 }
 
+// An alpha-stream word: the pair's alpha (negated when clamped) rounded to a
+// multiple of 32 ulp (<= 16 ulp = 1e-6 relative), its compacted entry index k
+// in the low 5 bits, so the product walks need no bit iteration over masks.
+__device__ __forceinline__ float alpha_word(float a, int k) {
+    return __uint_as_float(((__float_as_uint(a) + 16u) & ~31u) | static_cast<unsigned>(k));
+}
+__device__ __forceinline__ int word_entry(float w) { return static_cast<int>(__float_as_uint(w) & 31u); }
+__device__ __forceinline__ float word_alpha(float w) { return __uint_as_float(__float_as_uint(w) & ~31u); }
+
 // Once per (state, plan), after k_masks: the alpha of every blended pair in
 // the order the product passes consume them (SampleArgs::srow_off), so the
 // passes never re-evaluate the Gaussian falloff: alpha comes from a TMA-staged
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
             float alpha = 0.0f;
             bool cl = false;
             gate_alpha(gate_q(gt, pq), gt.lo, alpha, cl);  // blended: the mask already decided
-            out[32 * (row + i) + lane] = cl ? -alpha : alpha;
+            out[32 * (row + i) + lane] = alpha_word(cl ? -alpha : alpha, k);
         }
         row += npc;
         __syncwarp();
@@ -618,14 +627,6 @@ struct AlphaPipe {
     }
 };
 
-// The set bits of m up to and including its kAlphaRows-th.
-__device__ __forceinline__ unsigned first_rows(unsigned m) {
-    unsigned t = m;
-#pragma unroll 1
-    for (int i = 0; i < kAlphaRows && t; ++i) t &= t - 1;
-    return m & ~t;
-}
-
 __device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0xffffffffu, __popc(m)); }
 
 // The sampled-pixel products over the compacted window stream.
@@ -731,27 +732,22 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 dT = fmaf(dT, om, -T * dalpha);
                 T = __fmul_rn(T, om);
             };
-            auto walk = [&](unsigned mm, const float* q) {
-                while (mm) {
-                    const int k1 = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    const bool two = mm != 0u;
-                    const int k2 = two ? __ffs(mm) - 1 : k1;
-                    mm = two ? (mm & (mm - 1)) : mm;
-                    const float av1 = q[0];
-                    const float av2 = two ? q[32] : 0.0f;
-                    q += two ? 64 : 32;
-                    pair(k1, av1);
-                    pair(k2, av2);
+            // n pairs from q (row stride 32): the words carry the entry index;
+            // the next iteration's two words are loaded one iteration ahead
+            auto walk = [&](int n, const float* q) {
+                float nx1 = n > 0 ? q[0] : 0.0f, nx2 = n > 1 ? q[32] : 0.0f;
+                for (int i = 0; i < n; i += 2) {
+                    const float w1 = nx1, w2 = nx2;
+                    q += 64;
+                    nx1 = i + 2 < n ? q[0] : 0.0f;
+                    nx2 = i + 3 < n ? q[32] : 0.0f;
+                    pair(word_entry(w1), word_alpha(w1));
+                    pair(word_entry(w2), word_alpha(w2));  // 0 (neutral) past the lane's last pair
                 }
             };
-            if (cur > kAlphaRows) {
-                const unsigned lo = first_rows(m);
-                walk(lo, sp);
-                walk(m & ~lo, ap.overflow(w) + lane);
-            } else {
-                walk(m, sp);
-            }
+            const int npair = __popc(m);
+            walk(min(npair, kAlphaRows), sp);
+            if (cur > kAlphaRows) walk(npair - min(npair, kAlphaRows), ap.overflow(w) + lane);
             __syncwarp();
         }
         if (MODE == kJvp) {
@@ -817,16 +813,15 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
         // dL/dalpha = sum_c u_c (T c_c - (C_c - S_incl,c) / (1 - alpha))
-        auto walk = [&](unsigned m, const float* q) {
-            while (m) {  // two pairs per iteration, the second predicated
-                const int k1 = __ffs(m) - 1;
-                m &= m - 1;
-                const bool two = m != 0u;
-                const int k2 = two ? __ffs(m) - 1 : k1;
-                m = two ? (m & (m - 1)) : m;
-                const float av1 = q[0];
-                const float av2 = two ? q[32] : 0.0f;
-                q += two ? 64 : 32;
+        auto walk = [&](int n, const float* q) {
+            float nx1 = n > 0 ? q[0] : 0.0f, nx2 = n > 1 ? q[32] : 0.0f;
+            for (int i = 0; i < n; i += 2) {  // two pairs per iteration, the second predicated
+                const bool two = i + 1 < n;
+                const int k1 = word_entry(nx1), k2 = word_entry(nx2);
+                const float av1 = word_alpha(nx1), av2 = word_alpha(nx2);
+                q += 64;
+                nx1 = i + 2 < n ? q[0] : 0.0f;
+                nx2 = i + 3 < n ? q[32] : 0.0f;
                 const float a1 = fabsf(av1), a2 = fabsf(av2);
                 const float uc1 = u0 * blk[6][k1] + u1 * blk[7][k1] + u2 * blk[8][k1];
                 const float uc2 = u0 * blk[6][k2] + u1 * blk[7][k2] + u2 * blk[8][k2];
@@ -844,13 +839,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
                 T = __fmul_rn(T, om2);
             }
         };
-        if (cur > kAlphaRows) {
-            const unsigned lo = first_rows(m0);
-            walk(lo, sp);
-            walk(m0 & ~lo, ap.overflow(w) + lane);
-        } else {
-            walk(m0, sp);
-        }
+        const int npair = __popc(m0);
+        walk(min(npair, kAlphaRows), sp);
+        if (cur > kAlphaRows) walk(npair - min(npair, kAlphaRows), ap.overflow(w) + lane);
         __syncwarp();
         // phase B (lane = entry), dense over the pixels
         float M0 = 0.f;
