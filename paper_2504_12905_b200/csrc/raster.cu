@@ -588,7 +588,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Double-buffered window inputs of one warp: window w's alpha rows and record
 // block land in buffer w & 1 (one mbarrier per buffer, one transaction count),
 // the copies for window w+1 are in flight while window w runs.
-constexpr int kAlphaRows = 22;  // rows staged per window (~98% of windows at configs[2] need <= 22)
+// Rows staged per window by TMA; the rest (windows whose busiest lane blends
+// more than 18 entries) are prefetched into L2 with the window and read from
+// global.  18 (not the ~98th-percentile 22) so the product CTA fits 7 per SM.
+constexpr int kAlphaRows = 18;
 
 struct AlphaPipe {
     float* buf0;
@@ -609,6 +612,10 @@ struct AlphaPipe {
                          "r"(128u * staged + 4u * kRecBlock)
                          : "memory");
             if (staged > 0) bulk_copy((w & 1) ? buf1 : buf0, src + 32 * next, 128u * staged, b);
+            if (rows > staged)  // the overflow rows, read later from global: warm them into L2
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + 32 * (next + staged)),
+                             "r"(128u * (rows - staged))
+                             : "memory");
             bulk_copy((w & 1) ? rbuf1 : rbuf0, rsrc + static_cast<size_t>(kRecBlock) * w, 4u * kRecBlock, b);
         }
         if (w & 1) row1 = next;
@@ -655,8 +662,10 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     __shared__ __align__(128) float s_blk[NW][2][kRecBlock];  // record blocks [9][32] (TMA)
     // pass-1 staging, struct-of-arrays so lanes reading different entries hit
     // different banks: tau0..5, dr, dg, db
-    __shared__ float s_f[NW][9][32];
-    __shared__ __align__(16) float2 s_pair[NW][32][33];  // [pixel][entry]: (dL/dpower, alpha T)
+    // [pixel][entry]: (dL/dpower, alpha T); pass 1's [9][32] staging lives in
+    // the same memory (the passes never overlap), which with 18 staged alpha
+    // rows keeps a 2-warp CTA at 32 KB: 7 CTAs (14 warps) per SM
+    __shared__ __align__(16) float2 s_pair[NW][32][33];
     __shared__ float4 s_phi[NW][32];  // per pixel: (x, y, u0, u1), tile-centre coords
     __shared__ float s_u2[NW][32];
     __shared__ uint64_t s_bar[NW][2];
@@ -670,7 +679,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     W.nwin = (W.nun + 31) >> 5;
     W.list = A.glist + A.mask_off[gi];
     W.masks = A.masks + A.mask_off[gi];
-    float(*sf)[32] = s_f[warp];
+    float(*sf)[32] = reinterpret_cast<float(*)[32]>(&s_pair[warp][0][0]);
     if (lane == 0) {
         mbar_init(&s_bar[warp][0], 1);
         mbar_init(&s_bar[warp][1], 1);
