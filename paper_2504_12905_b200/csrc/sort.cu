@@ -15,7 +15,8 @@
 // One radix pass = digit histogram per 4096-element block (warp-aggregated
 // smem counters), an exclusive scan of the digit-major histogram, and a
 // stable scatter that ranks each 256-element chunk with __match_any_sync and
-// per-warp digit counts.
+// per-warp digit counts, stages the block's elements in shared memory in digit
+// order and writes each digit's run out coalesced.
 #include <cstdint>
 
 #include <atomic>
@@ -55,68 +56,84 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
     hist[static_cast<size_t>(t) * nblocks + blockIdx.x] = h[t];
 }
 
-// Stable scatter.  Each round covers RR = 4 x 256 consecutive elements
-// (element j*256 + t of the round is thread t's j-th); local ranks come from
-// __match_any_sync within a warp and per-(j, warp) digit counts in smem, with
-// three block barriers per round.
-constexpr int kRadixRound = 1;
-
+// Stable scatter, block-staged: the block's 4096 elements are first placed in
+// shared memory in (digit, input) order, then written out so consecutive
+// threads write consecutive positions of each digit's run (coalesced), instead
+// of 256 scattered 4-byte writes per round.
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __restrict__ kin,
-                                                                 const unsigned* __restrict__ vin,
-                                                                 K* __restrict__ kout, unsigned* __restrict__ vout,
-                                                                 long long n, int shift,
-                                                                 const unsigned* __restrict__ offs, int nblocks) {
+                                                                  const unsigned* __restrict__ vin,
+                                                                  K* __restrict__ kout, unsigned* __restrict__ vout,
+                                                                  long long n, int shift,
+                                                                  const unsigned* __restrict__ offs, int nblocks) {
     constexpr int NW = kRadixThreads / 32;
-    constexpr int NS = kRadixRound * NW;  // (j, warp) slots per round
-    __shared__ unsigned s_base[256];
-    __shared__ unsigned s_wc[NS][256];
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    K* s_key = reinterpret_cast<K*>(s_raw);
+    unsigned* s_val = reinterpret_cast<unsigned*>(s_key + kRadixTile);
+    __shared__ unsigned s_gbase[256], s_lbase[256], s_run[256], s_warp[NW];
+    __shared__ unsigned s_wc[NW][256];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    s_base[t] = offs[static_cast<size_t>(t) * nblocks + blockIdx.x];
     const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
+    const int cnt = static_cast<int>(n - base < kRadixTile ? n - base : kRadixTile);
+    const size_t idx0 = static_cast<size_t>(t) * nblocks + blockIdx.x;
+    const unsigned g0 = offs[idx0];
+    const unsigned g1 = idx0 + 1 < 256ull * nblocks ? offs[idx0 + 1] : static_cast<unsigned>(n);
+    s_gbase[t] = g0;
+    {   // block-local digit starts: exclusive scan of this block's digit counts
+        unsigned x = g1 - g0, incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        unsigned wo = 0u;
+        for (int w = 0; w < warp; ++w) wo += s_warp[w];
+        s_lbase[t] = wo + incl - x;
+        s_run[t] = 0u;
+    }
     const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < kRadixItems; r += kRadixRound) {
+    for (int r = 0; r < kRadixItems; ++r) {
 #pragma unroll
-        for (int w = 0; w < NS; ++w) s_wc[w][t] = 0u;
+        for (int w = 0; w < NW; ++w) s_wc[w][t] = 0u;
         __syncthreads();
-        K key[kRadixRound];
-        unsigned val[kRadixRound], d[kRadixRound], wrank[kRadixRound];
-#pragma unroll
-        for (int j = 0; j < kRadixRound; ++j) {
-            const long long idx = base + (r + j) * kRadixThreads + t;
-            const bool valid = idx < n;
-            key[j] = 0;
-            val[j] = 0u;
-            if (valid) {
-                key[j] = kin[idx];
-                val[j] = vin[idx];
-            }
-            d[j] = valid ? digit_of(key[j], shift) : 256u;
+        const int li = r * kRadixThreads + t;
+        const bool valid = li < cnt;
+        K key = 0;
+        unsigned val = 0u;
+        if (valid) {
+            key = kin[base + li];
+            val = vin[base + li];
         }
-#pragma unroll
-        for (int j = 0; j < kRadixRound; ++j) {
-            const unsigned peers = __match_any_sync(0xffffffffu, d[j]);
-            wrank[j] = __popc(peers & lt);
-            if (d[j] < 256u && wrank[j] == 0u) s_wc[j * NW + warp][d[j]] = __popc(peers);
-        }
+        const unsigned d = valid ? digit_of(key, shift) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned wrank = __popc(peers & lt);
+        if (d < 256u && wrank == 0u) s_wc[warp][d] = __popc(peers);
         __syncthreads();
-        unsigned run = 0u;  // thread t owns digit t: exclusive prefix over the (j, warp) slots
+        unsigned run = 0u;
 #pragma unroll
-        for (int w = 0; w < NS; ++w) {
+        for (int w = 0; w < NW; ++w) {
             const unsigned c = s_wc[w][t];
             s_wc[w][t] = run;
             run += c;
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kRadixRound; ++j)
-            if (d[j] < 256u) {
-                const unsigned pos = s_base[d[j]] + s_wc[j * NW + warp][d[j]] + wrank[j];
-                kout[pos] = key[j];
-                vout[pos] = val[j];
-            }
+        if (d < 256u) {
+            const unsigned lpos = s_lbase[d] + s_run[d] + s_wc[warp][d] + wrank;
+            s_key[lpos] = key;
+            s_val[lpos] = val;
+        }
         __syncthreads();
-        s_base[t] += run;
+        s_run[t] += run;
+    }
+    __syncthreads();
+    for (int i = t; i < cnt; i += kRadixThreads) {
+        const K key = s_key[i];
+        const unsigned d = digit_of(key, shift);
+        const unsigned pos = s_gbase[d] + (static_cast<unsigned>(i) - s_lbase[d]);
+        kout[pos] = key;
+        vout[pos] = s_val[i];
     }
 }
 
@@ -221,7 +238,9 @@ void radix_pass(const K* kin, const unsigned* vin, K* kout, unsigned* vout, long
     const int nb = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
     k_radix_hist<K><<<nb, kRadixThreads, 0, st>>>(kin, n, shift, hist, nb); ++g_launches;
     launch_exclusive_scan(hist, hist, 256ll * nb, part, nullptr, st);
-    k_radix_scatter<K><<<nb, kRadixThreads, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb); ++g_launches;
+    constexpr size_t smem = (sizeof(K) + sizeof(unsigned)) * kRadixTile;
+    cudaFuncSetAttribute(k_radix_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_radix_scatter<K><<<nb, kRadixThreads, smem, st>>>(kin, vin, kout, vout, n, shift, hist, nb); ++g_launches;
 }
 
 long long radix_hist_size(long long n) { return 256ll * ((n + kRadixTile - 1) / kRadixTile); }

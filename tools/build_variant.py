@@ -1,7 +1,8 @@
-"""Build an experimental libslm_b200 variant: raster.cu recompiled with extra
-flags (e.g. -DSLM_E1), linked with the normal objects, written to exp/NAME.so.
+"""Build an experimental libslm_b200 variant: one .cu (raster.cu, or $SRC)
+recompiled with extra flags (e.g. -DSLM_E1), linked with the normal objects,
+written to exp/NAME.so.
 
-    python tools/build_variant.py NAME [-DFLAG ...]
+    [SRC=sort.cu] python tools/build_variant.py NAME [-DFLAG ...]
 """
 import os
 import subprocess
@@ -16,10 +17,12 @@ def main():
     name, flags = sys.argv[1], sys.argv[2:]
     B.build()
     os.makedirs(os.path.join(ROOT, "exp"), exist_ok=True)
-    obj = os.path.join(ROOT, "exp", f"{name}_raster.o")
+    src = os.environ.get("SRC", "raster.cu")
+    obj = os.path.join(ROOT, "exp", f"{name}_{src}.o")
     B._run([B.NVCC, "-std=c++17", "-O3", "-lineinfo", *B.ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-            f"-I{B.INCLUDE}", f"-I{B.CSRC}", *flags, "-c", os.path.join(B.CSRC, "raster.cu"), "-o", obj])
-    objs = [obj if s == "raster.cu" else os.path.join(B.BUILD, s + ".o") for s in B.CU_SOURCES]
+            f"-I{B.INCLUDE}", f"-I{B.CSRC}", *B.CU_SOURCES[src], *flags, "-c", os.path.join(B.CSRC, src),
+            "-o", obj])
+    objs = [obj if s == src else os.path.join(B.BUILD, s + ".o") for s in B.CU_SOURCES]
     objs += [os.path.join(B.BUILD, s + ".o") for s in B.CPP_SOURCES]
     out = os.path.join(ROOT, "exp", f"{name}.so")
     B._run([B.NVCC, "-shared", *B.ARCH, "-cudart", "static", "-o", out, *objs, "-ldl"])
