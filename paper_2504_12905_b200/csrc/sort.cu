@@ -12,10 +12,10 @@
 //      tile rect in raster order) at an exclusive-scan offset;
 //   3. a stable sort of the pairs by tile id leaves every tile's entries in
 //      (depth, index) order at the tile's CSR offset.
-// One radix pass = digit histogram per 4096-element block (warp-aggregated
-// smem counters), an exclusive scan of the digit-major histogram, and a
-// stable scatter that ranks each 256-element chunk with __match_any_sync and
-// per-warp digit counts, stages the block's elements in shared memory in digit
+// One radix pass = digit histogram per 4096-element block (per-warp smem
+// counters), an exclusive scan of the digit-major histogram, and a
+// stable scatter that ranks each 256-element chunk with nine ballots (equal
+// digits within a warp) and per-warp digit counts, stages the block's elements in shared memory in digit
 // order and writes each digit's run out coalesced.
 #include <cstdint>
 
@@ -39,9 +39,10 @@ __device__ __forceinline__ unsigned digit_of(K k, int shift) {
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restrict__ keys, long long n, int shift,
                                                               unsigned* __restrict__ hist, int nblocks) {
-    __shared__ unsigned h[256];
-    const int t = threadIdx.x, lane = t & 31;
-    h[t] = 0u;
+    __shared__ unsigned hw[kRadixThreads / 32][256];  // per-warp digit counters
+#pragma unroll
+    for (int w = 0; w < kRadixThreads / 32; ++w) hw[w][threadIdx.x] = 0u;
+    const int t = threadIdx.x;
     __syncthreads();
     const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
 #pragma unroll 4
@@ -49,11 +50,13 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
         const long long idx = base + i * kRadixThreads + t;
         const bool valid = idx < n;
         const unsigned d = valid ? digit_of(keys[idx], shift) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&h[d], __popc(peers));
+        if (valid) atomicAdd(&hw[t >> 5][d], 1u);
     }
     __syncthreads();
-    hist[static_cast<size_t>(t) * nblocks + blockIdx.x] = h[t];
+    unsigned sum = 0u;
+#pragma unroll
+    for (int w = 0; w < kRadixThreads / 32; ++w) sum += hw[w][t];
+    hist[static_cast<size_t>(t) * nblocks + blockIdx.x] = sum;
 }
 
 // Stable scatter, block-staged: the block's 4096 elements are first placed in
@@ -107,7 +110,12 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
             val = vin[base + li];
         }
         const unsigned d = valid ? digit_of(key, shift) : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned peers = 0xffffffffu;  // lanes with the same digit, from nine ballots
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bal : ~bal;
+        }
         const unsigned wrank = __popc(peers & lt);
         if (d < 256u && wrank == 0u) s_wc[warp][d] = __popc(peers);
         __syncthreads();
