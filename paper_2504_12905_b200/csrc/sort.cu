@@ -63,15 +63,19 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
 // shared memory in (digit, input) order, then written out so consecutive
 // threads write consecutive positions of each digit's run (coalesced), instead
 // of 256 scattered 4-byte writes per round.
+// `pin`/`pout` (optional) carry a 64-bit payload per element along.
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __restrict__ kin,
                                                                   const unsigned* __restrict__ vin,
                                                                   K* __restrict__ kout, unsigned* __restrict__ vout,
                                                                   long long n, int shift,
-                                                                  const unsigned* __restrict__ offs, int nblocks) {
+                                                                  const unsigned* __restrict__ offs, int nblocks,
+                                                                  const unsigned long long* __restrict__ pin,
+                                                                  unsigned long long* __restrict__ pout) {
     constexpr int NW = kRadixThreads / 32;
     extern __shared__ __align__(16) unsigned char s_raw[];
-    K* s_key = reinterpret_cast<K*>(s_raw);
+    unsigned long long* s_pay = reinterpret_cast<unsigned long long*>(s_raw);  // used only with a payload
+    K* s_key = reinterpret_cast<K*>(s_raw + (pin ? sizeof(unsigned long long) * kRadixTile : 0));
     unsigned* s_val = reinterpret_cast<unsigned*>(s_key + kRadixTile);
     __shared__ unsigned s_gbase[256], s_lbase[256], s_run[256], s_warp[NW];
     __shared__ unsigned s_wc[NW][256];
@@ -105,9 +109,11 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
         const bool valid = li < cnt;
         K key = 0;
         unsigned val = 0u;
+        unsigned long long pay = 0ull;
         if (valid) {
             key = kin[base + li];
             val = vin[base + li];
+            if (pin) pay = pin[base + li];
         }
         const unsigned d = valid ? digit_of(key, shift) : 256u;
         unsigned peers = 0xffffffffu;  // lanes with the same digit, from nine ballots
@@ -131,6 +137,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
             const unsigned lpos = s_lbase[d] + s_run[d] + s_wc[warp][d] + wrank;
             s_key[lpos] = key;
             s_val[lpos] = val;
+            if (pin) s_pay[lpos] = pay;
         }
         __syncthreads();
         s_run[t] += run;
@@ -142,6 +149,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
         const unsigned pos = s_gbase[d] + (static_cast<unsigned>(i) - s_lbase[d]);
         kout[pos] = key;
         vout[pos] = s_val[i];
+        if (pin) pout[pos] = s_pay[i];
     }
 }
 
@@ -242,13 +250,23 @@ long long scan_scratch(long long n) { return (n + kScanTile - 1) / kScanTile + 1
 // One stable LSD pass over 8 key bits starting at `shift`.
 template <typename K>
 void radix_pass(const K* kin, const unsigned* vin, K* kout, unsigned* vout, long long n, int shift,
-                unsigned* hist, unsigned* part, cudaStream_t st) {
+                unsigned* hist, unsigned* part, cudaStream_t st, const unsigned long long* pin = nullptr,
+                unsigned long long* pout = nullptr) {
     const int nb = static_cast<int>((n + kRadixTile - 1) / kRadixTile);
     k_radix_hist<K><<<nb, kRadixThreads, 0, st>>>(kin, n, shift, hist, nb); ++g_launches;
     launch_exclusive_scan(hist, hist, 256ll * nb, part, nullptr, st);
-    constexpr size_t smem = (sizeof(K) + sizeof(unsigned)) * kRadixTile;
-    cudaFuncSetAttribute(k_radix_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_radix_scatter<K><<<nb, kRadixThreads, smem, st>>>(kin, vin, kout, vout, n, shift, hist, nb); ++g_launches;
+    const size_t smem = (sizeof(K) + sizeof(unsigned) + (pin ? sizeof(unsigned long long) : 0)) * kRadixTile;
+    cudaFuncSetAttribute(k_radix_scatter<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>((sizeof(K) + sizeof(unsigned) + sizeof(unsigned long long)) * kRadixTile));
+    k_radix_scatter<K><<<nb, kRadixThreads, smem, st>>>(kin, vin, kout, vout, n, shift, hist, nb, pin, pout);
+    ++g_launches;
+}
+
+// A u32-key pass that also carries a 64-bit payload (the depth keys through the view pass).
+void radix_pass_kv(const unsigned* kin, const unsigned* vin, const unsigned long long* pin, unsigned* kout,
+                   unsigned* vout, unsigned long long* pout, long long n, int shift, unsigned* hist, unsigned* part,
+                   cudaStream_t st) {
+    radix_pass<unsigned>(kin, vin, kout, vout, n, shift, hist, part, st, pin, pout);
 }
 
 long long radix_hist_size(long long n) { return 256ll * ((n + kRadixTile - 1) / kRadixTile); }
@@ -326,14 +344,19 @@ __device__ void heap_sift(unsigned long long* k, unsigned* v, long long root, lo
     }
 }
 
-__global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __restrict__ vals, long long n) {
+// Runs are maximal stretches of equal (view, upper key half); after the view
+// pass only same-view keys can share a run (ties across views never matter).
+__global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __restrict__ vals, long long n,
+                           unsigned Gp) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
-    if (hi == 0u) return;                                                 // culled
-    if (i > 0 && static_cast<unsigned>(keys[i - 1] >> 32) == hi) return;  // not a run start
+    if (hi == 0u) return;  // culled
+    const unsigned view = vals[i] / Gp;
+    auto same = [&](long long j) { return static_cast<unsigned>(keys[j] >> 32) == hi && vals[j] / Gp == view; };
+    if (i > 0 && same(i - 1)) return;  // not a run start
     long long e = i + 1;
-    while (e < n && static_cast<unsigned>(keys[e] >> 32) == hi) ++e;
+    while (e < n && same(e)) ++e;
     const long long len = e - i;
     if (len <= 1) return;
     unsigned long long* k = keys + i;
@@ -422,20 +445,23 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
         std::swap(ka, kb);
         std::swap(va, vb);
     }
-    if (vary & 0xFFFFFFFFull) {
-        k_fix_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ka, va, n); ++g_launches;
-    }
     // then by view (not needed for the order -- a tile's entries belong to one
     // view -- but the view-major emit keeps the tile passes' scatter local: measured
-    // 0.4 ms faster per batch at configs[2])
+    // 0.4 ms faster per batch at configs[2]); the 64-bit keys ride along so the
+    // run fix-up below only sees same-view runs
     if (V > 1) {
         k_view_key<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, Gp, b.k32a); ++g_launches;
         unsigned *k32a = b.k32a, *k32b = b.k32b;
         for (int s = 0; (1ll << s) < V; s += 8) {
-            radix_pass<unsigned>(k32a, va, k32b, vb, n, s, b.hist, b.part, st);
+            radix_pass_kv(k32a, va, ka, k32b, vb, kb, n, s, b.hist, b.part, st);
             std::swap(k32a, k32b);
             std::swap(va, vb);
+            std::swap(ka, kb);
         }
+    }
+    if (vary & 0xFFFFFFFFull) {
+        k_fix_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ka, va, n, static_cast<unsigned>(Gp));
+        ++g_launches;
     }
     // 2. emit (tile, index) pairs in (view, depth, index) order
     k_emit_count<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, rect, b.count); ++g_launches;
