@@ -109,6 +109,10 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
         qy[i] = (float)y + 0.5f - tcy;
         qyy[i] = __fmul_rn(qy[i], qy[i]);
         if (x < cam.width && y < cam.height) live |= 1u << i;
+        else {  // a dead pixel's gate is -huge: every pair skips it
+            qy[i] = 0.0f;
+            qyy[i] = 1e30f;
+        }
     }
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
@@ -129,16 +133,29 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column
+            // the gates of the 4 pixels as two packed FMA chains (fma.rn.f32x2 rounds
+            // each lane like __fmaf_rn: the same q' as gate_qy); terminated pixels
+            // carry qyy = 1e30, so they fail the gate without a live test
+            float qv[kRenderPix];
+#pragma unroll
+            for (int i = 0; i < kRenderPix; i += 2) {
+                const float2 qq = ffma2(make_float2(g.g5, g.g5), make_float2(qyy[i], qyy[i + 1]),
+                                        ffma2(make_float2(gx1, gx1), make_float2(qy[i], qy[i + 1]),
+                                              make_float2(gx0, gx0)));
+                qv[i] = qq.x;
+                qv[i + 1] = qq.y;
+            }
 #pragma unroll
             for (int i = 0; i < kRenderPix; ++i) {
-                if (!((live >> i) & 1u)) continue;
                 float alpha;
                 bool cl;
-                if (!gate_alpha(gate_qy(g, gx0, gx1, qy[i], qyy[i]), g.lo, alpha, cl)) continue;
+                if (!gate_alpha(qv[i], g.lo, alpha, cl)) continue;
                 float tt;
                 if (terminates(T[i], alpha, tt)) {
                     live &= ~(1u << i);
                     last[i] = start + k;
+                    qy[i] = 0.0f;
+                    qyy[i] = 1e30f;
                     continue;
                 }
                 const float w = __fmul_rn(alpha, T[i]);
@@ -433,25 +450,6 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
                  : "memory");
 }
 
-// Packed FP32 FMA (sm_100 FFMA2): d = a * b + c on two lanes of a float2.
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    float2 d;
-    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
-}
-
-__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
-    float2 d;
-    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
 
 // Window prefetch (lane = compacted entry 32w+lane): mask word of the lane's
 // pixel and the entry's splat record (and tangent record).
