@@ -86,6 +86,8 @@ struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = true;
+    cudaStream_t aux = nullptr;       // copy stream overlapping uploads with kernels on `stream`
+    cudaEvent_t aux_done = nullptr;
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
     DevBuf<double> partial;
@@ -113,6 +115,15 @@ struct Context {
         for (auto& m : marks) cudaEventDestroy(m.second);
         if (comm) nccl().CommDestroy(comm);
         if (stream && own_stream) cudaStreamDestroy(stream);
+        if (aux) cudaStreamDestroy(aux);
+        if (aux_done) cudaEventDestroy(aux_done);
+    }
+    cudaStream_t aux_stream() {
+        if (!aux) {
+            SLM_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+            SLM_CUDA_CHECK(cudaEventCreateWithFlags(&aux_done, cudaEventDisableTiming));
+        }
+        return aux;
     }
     void activate() const { SLM_CUDA_CHECK(cudaSetDevice(device)); }
     void sync() const { SLM_CUDA_CHECK(cudaStreamSynchronize(stream)); }
@@ -504,7 +515,8 @@ struct Samples {
 
     // Device half: mask offsets (need the tile-list lengths) and uploads.
     pinned_vector<long long> hoff;
-    void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets) {
+    void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets,
+                cudaStream_t st) {
         hoff.resize(hgroups.size());
         mask_words = 0;
         for (size_t g = 0; g < hgroups.size(); ++g) {
@@ -513,7 +525,7 @@ struct Samples {
             hoff[g] = mask_words;
             mask_words += 32 * ((n + 31) / 32);
         }
-        cudaStream_t st = ctx->stream;
+        (void)ctx;
         mask_off.ensure(std::max<size_t>(hoff.size(), 1));
         masks.ensure(std::max<long long>(mask_words, 1));
         cols.ensure(std::max<long long>(mask_words, 1));
@@ -673,8 +685,23 @@ struct Jacobian {
 
     // Device half: uploads, zeroed accumulators, blend masks (needs the batch
     // prepared and rendered).
+    // The plan's H2D uploads on the context's copy stream, so they overlap
+    // whatever runs on the main stream (lm_step: the render); init_device waits.
+    bool preuploaded = false;
+    void upload_early() {
+        cudaStream_t a = ctx->aux_stream();
+        samples.upload(ctx, batch->hcams, batch->htile_offsets, a);
+        SLM_CUDA_CHECK(cudaEventRecord(ctx->aux_done, a));
+        preuploaded = true;
+    }
+
     void init_device() {
-        samples.upload(ctx, batch->hcams, batch->htile_offsets);
+        if (preuploaded) {
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+            preuploaded = false;
+        } else {
+            samples.upload(ctx, batch->hcams, batch->htile_offsets, ctx->stream);
+        }
         if (draw.on && draw.exhaustive) {  // exhaustive plan: pixels + dL/dr in sample order
             draw.sbase.ensure(std::max<size_t>(draw.hsbase.size(), 1));
             res_in.ensure(std::max<long long>(rdim, 1));
@@ -1576,6 +1603,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     if (sampler.joinable()) sampler.join();
     ctx->mark("plan:host");
     if (plan_err) std::rethrow_exception(plan_err);
+    J.upload_early();  // overlaps the render still running on the main stream
     // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
     double before = 0.0;
     {
