@@ -982,33 +982,31 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             __syncwarp();
             const float qmx = sf[0][k], qmy = sf[1][k];
             // sdp-weighted monomials in (dx, dy) up to degree 4, opacity, colours
-            float m2x = 0, mxy = 0, m2y = 0, m3x = 0, mx2y = 0, mxy2 = 0, m3y = 0;
-            float m4x = 0, mx3y = 0, mx2y2 = 0, mxy3 = 0, m4y = 0, aop = 0, ac0 = 0, ac1 = 0, ac2 = 0;
+            // packed FFMA2 / FADD2 / FMUL2 pairs; every lane does the scalar code's
+            // operations in the same order (so the sums round identically)
+            float2 Pa = make_float2(0.f, 0.f), Pb = Pa, Pc = Pa, Pd = Pa, Pe = Pa, Pf = Pa, Pg = Pa, Ph = Pa;
             for (unsigned cc = colk; cc; cc &= cc - 1) {
                 const int p = __ffs(cc) - 1;
                 const float4 pi = s_pix[warp][p];
                 const float pw2 = s_pw2[warp][p];
                 const float sdp = s_t[warp][0][p][e16], so = s_t[warp][1][p][e16], w2 = s_t[warp][2][p][e16];
                 const float X = qmx - pi.x, Y = qmy - pi.y;
-                const float XX = X * X, XY = X * Y, YY = Y * Y;
-                const float sXX = sdp * XX, sXY = sdp * XY, sYY = sdp * YY;
-                m2x += sXX;
-                mxy += sXY;
-                m2y += sYY;
-                m3x += sXX * X;
-                mx2y += sXX * Y;
-                mxy2 += sYY * X;
-                m3y += sYY * Y;
-                m4x += sXX * XX;
-                mx3y += sXX * XY;
-                mx2y2 += sXX * YY;
-                mxy3 += sXY * YY;
-                m4y += sYY * YY;
-                aop += so;
-                ac0 += pi.z * w2;
-                ac1 += pi.w * w2;
-                ac2 += pw2 * w2;
+                const float2 XY2 = make_float2(X, Y);
+                const float2 xx_xy = fmul2(make_float2(X, X), XY2);  // (XX, XY)
+                const float YY = Y * Y;
+                const float2 s_xx_xy = fmul2(make_float2(sdp, sdp), xx_xy);  // (sXX, sXY)
+                const float sYY = sdp * YY;
+                Pa = fadd2(Pa, s_xx_xy);                                              // (m2x, mxy)
+                Pb = fadd2(Pb, make_float2(sYY, so));                                 // (m2y, aop)
+                Pc = ffma2(make_float2(s_xx_xy.x, s_xx_xy.x), XY2, Pc);             // (m3x, mx2y)
+                Pd = ffma2(make_float2(sYY, sYY), XY2, Pd);                           // (mxy2, m3y)
+                Pe = ffma2(make_float2(s_xx_xy.x, s_xx_xy.x), xx_xy, Pe);             // (m4x, mx3y)
+                Pf = ffma2(make_float2(s_xx_xy.x, sYY), make_float2(YY, YY), Pf);     // (mx2y2, m4y)
+                Pg = ffma2(make_float2(s_xx_xy.y, pw2), make_float2(YY, w2), Pg);   // (mxy3, ac2)
+                Ph = ffma2(make_float2(pi.z, pi.w), make_float2(w2, w2), Ph);         // (ac0, ac1)
             }
+            float m2x = Pa.x, mxy = Pa.y, m2y = Pb.x, aop = Pb.y, m3x = Pc.x, mx2y = Pc.y, mxy2 = Pd.x, m3y = Pd.y;
+            float m4x = Pe.x, mx3y = Pe.y, mx2y2 = Pf.x, m4y = Pf.y, mxy3 = Pg.x, ac2 = Pg.y, ac0 = Ph.x, ac1 = Ph.y;
 #define HSUM(v) v += __shfl_xor_sync(0xffffffffu, v, 16)
             HSUM(m2x); HSUM(mxy); HSUM(m2y); HSUM(m3x); HSUM(mx2y); HSUM(mxy2); HSUM(m3y);
             HSUM(m4x); HSUM(mx3y); HSUM(mx2y2); HSUM(mxy3); HSUM(m4y); HSUM(aop);
