@@ -150,9 +150,10 @@ __device__ __forceinline__ unsigned long long depth_key(double d) {
 __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta, int G, int Gp,
                                                  const DevCam* __restrict__ cams, int V, float4* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys, short4* __restrict__ rect,
-                                                 int* __restrict__ tile_count, int* __restrict__ err) {
+                                                 unsigned long long* __restrict__ n_entries, int* __restrict__ err) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    unsigned long long area = 0ull;  // this Gaussian's tile-list entries over the views
+    if (g < G) {
     const GaussCommon gc = prepare_common(beta, Gp, g);
     if (gc.zero_quat) atomicOr(err, 1);
     for (int v = 0; v < V; ++v) {
@@ -186,56 +187,14 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         x1 = x1 > cam.tiles_x - 1 ? cam.tiles_x - 1 : x1;
         y1 = y1 > cam.tiles_y - 1 ? cam.tiles_y - 1 : y1;
         rect[vg] = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
-        for (int ty = y0; ty <= y1; ++ty)
-            for (int tx = x0; tx <= x1; ++tx) atomicAdd(&tile_count[cam.tile_base + ty * cam.tiles_x + tx], 1);
+        if (x0 <= x1 && y0 <= y1) area += static_cast<unsigned long long>(x1 - x0 + 1) * (y1 - y0 + 1);
     }
+    }
+    // n_entries += sum of the block's areas (one atomic per warp)
+    for (int o = 16; o; o >>= 1) area += __shfl_xor_sync(0xffffffffu, area, o);
+    if ((threadIdx.x & 31) == 0 && area) atomicAdd(n_entries, area);
 }
 
-// ------------------------------------------------------------------ K3 scan
-// Exclusive scan of the batch-concatenated tile counts (single CTA, n is at
-// most a few 10^4 tiles).  offsets[n] = total entries.
-__global__ void k_scan_tiles(const int* __restrict__ count, int n, int* __restrict__ offsets,
-                             int* __restrict__ cursor, long long* __restrict__ total_out) {
-    __shared__ long long part[1024];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    __shared__ int smax;
-    const int per = (n + nt - 1) / nt;
-    const int lo = tid * per, hi = min(n, lo + per);
-    long long s = 0;
-    int mx = 0;
-    if (tid == 0) smax = 0;
-    __syncthreads();
-    for (int i = lo; i < hi; ++i) {
-        s += count[i];
-        mx = max(mx, count[i]);
-    }
-    atomicMax(&smax, mx);
-    part[tid] = s;
-    __syncthreads();
-    for (int off = 1; off < nt; off <<= 1) {  // Hillis-Steele inclusive scan of partials
-        const long long add = tid >= off ? part[tid - off] : 0;
-        __syncthreads();
-        part[tid] += add;
-        __syncthreads();
-    }
-    long long run = tid == 0 ? 0 : part[tid - 1];
-    for (int i = lo; i < hi; ++i) {
-        offsets[i] = (int)run;
-        cursor[i] = (int)run;
-        run += count[i];
-    }
-    if (tid == nt - 1) {
-        offsets[n] = (int)part[nt - 1];
-        total_out[0] = part[nt - 1];
-        total_out[1] = smax;  // longest tile list: sizes the big-tile sort scratch
-    }
-}
-
-// K3 emit and K4 sort: sort.cu (stable radix passes, no per-tile sort).
-
-// ------------------------------------------------------------------ K15 update
-// GaussianSet::apply_update (types.cpp:48-60) + renormalize_rotations
-// (types.cpp:62-73): beta += eta * delta in f64, then q /= |q|.
 __global__ void k_apply_update(double* __restrict__ beta, const float* __restrict__ delta, int G,
                                int Gp, double eta, float* __restrict__ beta32) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -283,16 +242,12 @@ __global__ void k_beta_mirror(const double* __restrict__ beta, float* __restrict
 
 // ------------------------------------------------------------------ host launchers
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
-                    unsigned long long* keys, short4* rect, int* tile_count, int* err,
+                    unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err,
                     cudaStream_t st) {
     if (G == 0 || V == 0) return;
-    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, tile_count, err); ++g_launches;
+    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, n_entries, err); ++g_launches;
 }
 
-void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total,
-                       cudaStream_t st) {
-    k_scan_tiles<<<1, 1024, 0, st>>>(count, n, offsets, cursor, total); ++g_launches;
-}
 
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta,
                          float* beta32, cudaStream_t st) {

@@ -234,6 +234,28 @@ struct Scene {
     size_t P() const { return static_cast<size_t>(kP) * Gp; }
 };
 
+// Page-locked host allocator: the per-step sample arrays are uploaded with
+// cudaMemcpyAsync at DMA speed (grow-only vectors keep their capacity).
+template <class T>
+struct PinnedAlloc {
+    using value_type = T;
+    PinnedAlloc() = default;
+    template <class U>
+    PinnedAlloc(const PinnedAlloc<U>&) {}
+    T* allocate(size_t n) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable) != cudaSuccess) throw std::bad_alloc();
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t) { cudaFreeHost(p); }
+    template <class U>
+    bool operator==(const PinnedAlloc<U>&) const { return true; }
+    template <class U>
+    bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
+
 // =========================================================================== Batch
 // The prepared views of one scene state: splat records, tile lists (K1, K3,
 // K4) and, after render(), the per-pixel forward state (K6).
@@ -243,9 +265,10 @@ struct Batch {
     long long n_pix = 0, n_entries = 0;
     std::vector<DevCam> hcams;
     std::vector<int> htile_view;
-    std::vector<int> htile_offsets;  // CSR offsets of the tile lists (host copy)
+    pinned_vector<int> htile_offsets;  // CSR offsets of the tile lists (host copy, see wait_offsets)
+    cudaEvent_t offs_ready = nullptr;
     DevBuf<DevCam> cams;
-    DevBuf<int> tile_view, tile_count, tile_offsets, cursor, entries, err;
+    DevBuf<int> tile_view, tile_offsets, entries, err;
     DevBuf<long long> total;
     DevBuf<float4> rec;
     DevBuf<unsigned long long> keys;
@@ -261,7 +284,22 @@ struct Batch {
     DevBuf<unsigned long long> rk64a, rk64b, and_or;
     DevBuf<unsigned> rv32a, rv32b, rk32a, rk32b, rcount, rt32a, rt32b, rt32va, rt32vb, rhist, rpart;
 
+    bool offsets_pending = false;
     explicit Batch(Context* c) : ctx(c) {}
+    Batch(const Batch&) = delete;
+    Batch& operator=(const Batch&) = delete;
+    ~Batch() {
+        if (offs_ready) cudaEventDestroy(offs_ready);
+    }
+    // htile_offsets / max_list are valid after this
+    void wait_offsets() {
+        if (!offsets_pending) return;
+        SLM_CUDA_CHECK(cudaEventSynchronize(offs_ready));
+        offsets_pending = false;
+        max_list = 0;
+        for (int t = 0; t < n_tiles; ++t)
+            max_list = std::max<long long>(max_list, htile_offsets[t + 1] - htile_offsets[t]);
+    }
 
     void prepare(const Scene& s, const std::vector<slm_camera>& cv) {
         ctx->activate();
@@ -303,15 +341,15 @@ struct Batch {
         rec.ensure(3 * VG);
         keys.ensure(VG);
         rect.ensure(VG);
-        tile_count.ensure(n_tiles + 1);
         tile_offsets.ensure(n_tiles + 1);
-        cursor.ensure(n_tiles + 1);
         total.ensure(2);
         err.ensure(1 + std::max(V, 1));
-        SLM_CUDA_CHECK(cudaMemsetAsync(tile_count.p, 0, sizeof(int) * (n_tiles + 1), st));
+        SLM_CUDA_CHECK(cudaMemsetAsync(total.p, 0, sizeof(long long) * 2, st));
         SLM_CUDA_CHECK(cudaMemsetAsync(err.p, 0, sizeof(int) * (1 + V), st));
-        launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p, tile_count.p, err.p, st);
-        launch_scan_tiles(tile_count.p, n_tiles, tile_offsets.p, cursor.p, total.p, st);
+        // K1 + the entry total (sum of tile-rect areas); the per-tile offsets come
+        // out of the sorted tile ids (build_tile_lists), so no per-tile atomics
+        launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p,
+                       reinterpret_cast<unsigned long long*>(total.p), err.p, st);
         // depth-sort keys in index order + the AND/OR of the valid keys (which
         // key bytes need a radix pass)
         const long long nvg = static_cast<long long>(V) * Gp;
@@ -329,16 +367,12 @@ struct Batch {
         SLM_CUDA_CHECK(cudaMemcpyAsync(hdr, total.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(hao, and_or.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(herr.data(), err.p, sizeof(int) * (1 + V), cudaMemcpyDeviceToHost, st));
-        htile_offsets.resize(n_tiles + 1);
-        SLM_CUDA_CHECK(cudaMemcpyAsync(htile_offsets.data(), tile_offsets.p, sizeof(int) * (n_tiles + 1),
-                                       cudaMemcpyDeviceToHost, st));
         ctx->sync();
         if (herr[0]) throw std::domain_error("zero-norm quaternion");
         valid_count.assign(herr.begin() + 1, herr.end());
         n_entries = hdr[0];
         if (n_entries >= (1ll << 31)) throw std::runtime_error("tile-list entries exceed 2^31");
         entries.ensure(std::max<long long>(n_entries, 1));
-        max_list = hdr[1];
         ctx->mark("prep:sync");
         // tile lists by stable radix passes (sort.cu): depth ranks, emit, sort by tile
         const long long ne = std::max<long long>(n_entries, 1);
@@ -354,8 +388,17 @@ struct Batch {
         rpart.ensure(scan_scratch(std::max<long long>(hmax, nvg)));
         TileSortBuffers tb{rk64a.p, rk64b.p, rv32a.p, rv32b.p, rk32a.p, rk32b.p, rcount.p,
                            rt32a.p, rt32b.p, rt32va.p, rt32vb.p, rhist.p, rpart.p};
-        build_tile_lists(keys.p, rect.p, cams.p, G, Gp, V, n_tiles, n_entries, hao[0], hao[1], tb, entries.p, st);
+        build_tile_lists(keys.p, rect.p, cams.p, G, Gp, V, n_tiles, n_entries, hao[0], hao[1], tb, entries.p,
+                         tile_offsets.p, st);
         ctx->check_launch();
+        // host copy of the offsets (Samples::upload needs them): async into pinned
+        // memory, waited for only where it is read (wait_offsets)
+        htile_offsets.resize(n_tiles + 1);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(htile_offsets.data(), tile_offsets.p, sizeof(int) * (n_tiles + 1),
+                                       cudaMemcpyDeviceToHost, st));
+        if (!offs_ready) SLM_CUDA_CHECK(cudaEventCreateWithFlags(&offs_ready, cudaEventDisableTiming));
+        SLM_CUDA_CHECK(cudaEventRecord(offs_ready, st));
+        offsets_pending = true;
         ctx->mark("prep:sort");
         rendered = false;
         has_gt = false;
@@ -390,27 +433,6 @@ struct Batch {
     }
 };
 
-// Page-locked host allocator: the per-step sample arrays are uploaded with
-// cudaMemcpyAsync at DMA speed (grow-only vectors keep their capacity).
-template <class T>
-struct PinnedAlloc {
-    using value_type = T;
-    PinnedAlloc() = default;
-    template <class U>
-    PinnedAlloc(const PinnedAlloc<U>&) {}
-    T* allocate(size_t n) {
-        void* p = nullptr;
-        if (cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable) != cudaSuccess) throw std::bad_alloc();
-        return static_cast<T*>(p);
-    }
-    void deallocate(T* p, size_t) { cudaFreeHost(p); }
-    template <class U>
-    bool operator==(const PinnedAlloc<U>&) const { return true; }
-    template <class U>
-    bool operator!=(const PinnedAlloc<U>&) const { return false; }
-};
-template <class T>
-using pinned_vector = std::vector<T, PinnedAlloc<T>>;
 
 // =========================================================================== Samples
 // A plan laid out for the warp-per-group raster: per view, samples grouped
@@ -515,7 +537,7 @@ struct Samples {
 
     // Device half: mask offsets (need the tile-list lengths) and uploads.
     pinned_vector<long long> hoff;
-    void upload(Context* ctx, const std::vector<DevCam>& cams, const std::vector<int>& tile_offsets,
+    void upload(Context* ctx, const std::vector<DevCam>& cams, const pinned_vector<int>& tile_offsets,
                 cudaStream_t st) {
         hoff.resize(hgroups.size());
         mask_words = 0;
@@ -690,6 +712,7 @@ struct Jacobian {
     bool preuploaded = false;
     void upload_early() {
         cudaStream_t a = ctx->aux_stream();
+        batch->wait_offsets();
         samples.upload(ctx, batch->hcams, batch->htile_offsets, a);
         SLM_CUDA_CHECK(cudaEventRecord(ctx->aux_done, a));
         preuploaded = true;
@@ -700,6 +723,7 @@ struct Jacobian {
             SLM_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
             preuploaded = false;
         } else {
+            batch->wait_offsets();
             samples.upload(ctx, batch->hcams, batch->htile_offsets, ctx->stream);
         }
         if (draw.on && draw.exhaustive) {  // exhaustive plan: pixels + dL/dr in sample order

@@ -67,13 +67,12 @@ struct DevBuf {
 
 // ---- launchers (defined in the .cu files)
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
-                    unsigned long long* keys, short4* rect, int* tile_count, int* err, cudaStream_t st);
-void launch_scan_tiles(const int* count, int n, int* offsets, int* cursor, long long* total, cudaStream_t st);
+                    unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err, cudaStream_t st);
 void launch_depth_init(const unsigned long long* keys, const short4* rect, int G, int Gp, int V,
                        unsigned long long* kout, unsigned* vout, unsigned long long* and_or, cudaStream_t st);
 void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,
                       int n_tiles, long long n_entries, unsigned long long and_k, unsigned long long or_k,
-                      const TileSortBuffers& b, int* entries, cudaStream_t st);
+                      const TileSortBuffers& b, int* entries, int* tile_offsets, cudaStream_t st);
 long long radix_hist_size(long long n);
 long long scan_scratch(long long n);
 void launch_apply_update(double* beta, const float* delta, int G, int Gp, double eta, float* beta32,

@@ -427,12 +427,28 @@ __global__ void k_emit(const unsigned* __restrict__ order, long long n, int G, i
 }
 
 // Host driver (runtime.cpp keeps the buffers).  Returns nothing; `entries`
-// receives the per-tile sorted lists at the CSR offsets of k_scan_tiles.
+// receives the per-tile sorted lists; tile_offsets (n_tiles + 1) their CSR offsets.
+// CSR offsets from the sorted tile ids: offsets[t] = first entry with tile >= t.
+__global__ void k_tile_offsets(const unsigned* __restrict__ tiles, long long n, int n_tiles, int* __restrict__ offsets) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > n_tiles) return;
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (tiles[mid] < static_cast<unsigned>(t)) lo = mid + 1;
+        else hi = mid;
+    }
+    offsets[t] = static_cast<int>(lo);
+}
+
 void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,
                       int n_tiles, long long n_entries, unsigned long long and_k, unsigned long long or_k,
-                      const TileSortBuffers& b, int* entries, cudaStream_t st) {
+                      const TileSortBuffers& b, int* entries, int* tile_offsets, cudaStream_t st) {
     const long long n = static_cast<long long>(V) * Gp;
-    if (n == 0 || n_entries == 0) return;
+    if (n == 0 || n_entries == 0) {
+        cudaMemsetAsync(tile_offsets, 0, sizeof(int) * (n_tiles + 1), st);
+        return;
+    }
     // 1. depth passes over the varying key bytes, then the view
     const unsigned long long vary = and_k ^ or_k;
     unsigned long long *ka = b.k64a, *kb = b.k64b;
@@ -480,6 +496,7 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
     }
     if (passes == 0)  // a single tile: already in order
         cudaMemcpyAsync(entries, tva, sizeof(unsigned) * n_entries, cudaMemcpyDeviceToDevice, st);
+    k_tile_offsets<<<(n_tiles + 1 + 255) / 256, 256, 0, st>>>(tka, n_entries, n_tiles, tile_offsets); ++g_launches;
 }
 
 }  // namespace slm
