@@ -407,23 +407,54 @@ __global__ void k_emit_count(const unsigned* __restrict__ order, long long n, in
     count[i] = c;
 }
 
-__global__ void k_emit(const unsigned* __restrict__ order, long long n, int G, int Gp, const DevCam* __restrict__ cams,
-                       const short4* __restrict__ rect, const unsigned* __restrict__ start,
-                       unsigned* __restrict__ tkey, unsigned* __restrict__ tval) {
+// The block's 256 consecutive (view, Gaussian)s own one contiguous output
+// range; their pairs are staged in shared memory and written out coalesced
+// (pairs past the staging capacity go straight to global memory).
+constexpr int kEmitStage = 4096;
+
+__global__ void __launch_bounds__(256) k_emit(const unsigned* __restrict__ order, long long n, int G, int Gp,
+                                              const DevCam* __restrict__ cams, const short4* __restrict__ rect,
+                                              const unsigned* __restrict__ start, long long n_entries,
+                                              unsigned* __restrict__ tkey, unsigned* __restrict__ tval) {
+    __shared__ unsigned s_key[kEmitStage], s_val[kEmitStage];
+    __shared__ unsigned s_lo, s_hi;
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned vg = order[i];
-    const int v = static_cast<int>(vg / static_cast<unsigned>(Gp)), g = static_cast<int>(vg % static_cast<unsigned>(Gp));
-    if (g >= G) return;
-    const short4 r = rect[vg];
-    if (r.x > r.y) return;
-    const int base = cams[v].tile_base, tx_n = cams[v].tiles_x;
-    unsigned o = start[i];
-    for (int ty = r.z; ty <= r.w; ++ty)
-        for (int tx = r.x; tx <= r.y; ++tx, ++o) {
-            tkey[o] = static_cast<unsigned>(base + ty * tx_n + tx);
-            tval[o] = static_cast<unsigned>(g);
+    const long long first = static_cast<long long>(blockIdx.x) * blockDim.x;
+    const long long lastp1 = first + blockDim.x < n ? first + blockDim.x : n;
+    if (threadIdx.x == 0) {
+        s_lo = start[first];
+        s_hi = lastp1 < n ? start[lastp1] : static_cast<unsigned>(n_entries);
+    }
+    __syncthreads();
+    const unsigned lo = s_lo, hi = s_hi;
+    if (i < n) {
+        const unsigned vg = order[i];
+        const int v = static_cast<int>(vg / static_cast<unsigned>(Gp)), g = static_cast<int>(vg % static_cast<unsigned>(Gp));
+        if (g < G) {
+            const short4 r = rect[vg];
+            if (r.x <= r.y) {
+                const int base = cams[v].tile_base, tx_n = cams[v].tiles_x;
+                unsigned o = start[i];
+                for (int ty = r.z; ty <= r.w; ++ty)
+                    for (int tx = r.x; tx <= r.y; ++tx, ++o) {
+                        const unsigned key = static_cast<unsigned>(base + ty * tx_n + tx);
+                        if (o - lo < static_cast<unsigned>(kEmitStage)) {
+                            s_key[o - lo] = key;
+                            s_val[o - lo] = static_cast<unsigned>(g);
+                        } else {
+                            tkey[o] = key;
+                            tval[o] = static_cast<unsigned>(g);
+                        }
+                    }
+            }
         }
+    }
+    __syncthreads();
+    const unsigned m = min(hi - lo, static_cast<unsigned>(kEmitStage));
+    for (unsigned j = threadIdx.x; j < m; j += blockDim.x) {
+        tkey[lo + j] = s_key[j];
+        tval[lo + j] = s_val[j];
+    }
 }
 
 // Host driver (runtime.cpp keeps the buffers).  Returns nothing; `entries`
@@ -483,7 +514,9 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
     k_emit_count<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, rect, b.count); ++g_launches;
     launch_exclusive_scan(b.count, b.count, n, b.part, nullptr, st);
     unsigned *tka = b.t32a, *tkb = b.t32b, *tva = b.t32va, *tvb = b.t32vb;
-    k_emit<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, cams, rect, b.count, tka, tva); ++g_launches;
+    k_emit<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(va, n, G, Gp, cams, rect, b.count, n_entries, tka,
+                                                                    tva);
+    ++g_launches;
     // 3. stable sort by tile id; the last pass writes the values into `entries`
     int passes = 0;
     for (int s = 0; (1ll << s) < n_tiles; s += 8) ++passes;
