@@ -126,6 +126,15 @@ __device__ __forceinline__ bool gate_alpha(float q, float lo, float& alpha, bool
     return true;
 }
 
+// alpha of a pair the FP64 decision (k_masks) already blends: no gate test,
+// so a pair sitting within FP32 rounding of a gate keeps its alpha.
+__device__ __forceinline__ void blended_alpha(float q, float& alpha, bool& clamped) {
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q));
+    clamped = e > 0.99f;
+    alpha = clamped ? 0.99f : e;
+}
+
 // Termination test (rasterizer.hpp:121-122): the entry that would push T
 // under 1e-4 is not blended and ends the pixel.
 __device__ __forceinline__ bool terminates(float T, float alpha, float& test_t) {

@@ -88,6 +88,12 @@ struct SampleArgs {
     // masks: lane k's word = the pixels that blend compacted entry k.
     const unsigned* cols;
     unsigned* cols_out;
+    // Exact blend decisions (k_masks): the FP64 geometry per (view, Gaussian)
+    // [mx, my, a, b, c, o] and, per sample (group order), the final colour of
+    // the reference's FP64 blend, which the J^T passes use as C_final.
+    const double* rec64;
+    const float* scol;
+    float* scol_out;
 };
 
 constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)
@@ -110,6 +116,7 @@ struct DiagArgs {
     const int* gcount;
     const long long* mask_off;
     const unsigned* cols;  // column masks (SampleArgs::cols)
+    const float* scol;     // per-sample final colour (SampleArgs::scol)
 };
 
 // Scratch of the radix tile-list construction (sort.cu), sized by the runtime:

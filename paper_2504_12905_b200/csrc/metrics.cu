@@ -243,7 +243,7 @@ __global__ void k_ssim_fold(const Group* __restrict__ groups, int n_groups, cons
                             const int* __restrict__ spix, const int* __restrict__ sorig, float* __restrict__ sw,
                             const float* __restrict__ image, const float* __restrict__ gt,
                             const float* __restrict__ sres, const float* __restrict__ sdc, float ssim_weight,
-                            float* __restrict__ rhs) {
+                            float* __restrict__ rhs, const float* __restrict__ scol) {
     const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (g >= n_groups) return;
@@ -258,7 +258,8 @@ __global__ void k_ssim_fold(const Group* __restrict__ groups, int n_groups, cons
     for (int c = 0; c < 3; ++c) {
         const long long e = 3 * pix + c;
         const float w = sw[3 * k + c], sp = sdc[e];
-        rhs[3 * o + c] = -w * ((image[e] - gt[e]) + ssim_weight * sp * sres[e]);
+        const float rendered = scol ? scol[3 * k + c] : image[e];  // C_final of the FP64 blend at the sample
+        rhs[3 * o + c] = -w * ((rendered - gt[e]) + ssim_weight * sp * sres[e]);
         sw[3 * k + c] = w * (1.0f + ssim_weight * sp * sp);
     }
 }
@@ -295,10 +296,10 @@ void launch_ssim_diag(const double* a, const double* b, const ImgDesc* imgs, int
 
 void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, const int* spix, const int* sorig,
                       float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
-                      float ssim_weight, float* rhs, cudaStream_t st) {
+                      float ssim_weight, float* rhs, const float* scol, cudaStream_t st) {
     if (n_groups == 0) return;
     k_ssim_fold<<<(n_groups + 3) / 4, 128, 0, st>>>(groups, n_groups, cams, spix, sorig, sw, image, gt, sres, sdc,
-                                                     ssim_weight, rhs);
+                                                     ssim_weight, rhs, scol);
     ++g_launches;
 }
 

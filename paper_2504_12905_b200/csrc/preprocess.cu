@@ -150,7 +150,8 @@ __device__ __forceinline__ unsigned long long depth_key(double d) {
 __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta, int G, int Gp,
                                                  const DevCam* __restrict__ cams, int V, float4* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys, short4* __restrict__ rect,
-                                                 unsigned long long* __restrict__ n_entries, int* __restrict__ err) {
+                                                 unsigned long long* __restrict__ n_entries, int* __restrict__ err,
+                                                 double* __restrict__ rec64) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long area = 0ull;  // this Gaussian's tile-list entries over the views
     if (g < G) {
@@ -167,6 +168,13 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         }
         keys[vg] = depth_key(p.depth);
         float4* R = rec + 3 * vg;
+        double* R64 = rec64 + 6 * vg;  // FP64 geometry for the exact blend decisions (k_masks)
+        R64[0] = p.valid ? p.mx : 0.0;
+        R64[1] = p.valid ? p.my : 0.0;
+        R64[2] = p.valid ? p.ca : 0.0;
+        R64[3] = p.valid ? p.cb : 0.0;
+        R64[4] = p.valid ? p.cc : 0.0;
+        R64[5] = p.valid ? p.o : 0.0;
         if (!p.valid) {
             R[0] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -243,9 +251,10 @@ __global__ void k_beta_mirror(const double* __restrict__ beta, float* __restrict
 // ------------------------------------------------------------------ host launchers
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
                     unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err,
-                    cudaStream_t st) {
+                    double* rec64, cudaStream_t st) {
     if (G == 0 || V == 0) return;
-    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, n_entries, err); ++g_launches;
+    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, n_entries, err, rec64);
+    ++g_launches;
 }
 
 

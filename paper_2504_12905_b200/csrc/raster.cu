@@ -268,40 +268,65 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 // bit transposes) into 32-entry windows, so the per-product passes walk dense
 // windows and never stage an entry no lane uses.
 __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
-    __shared__ float4 s_rec[4][32][2];
+    __shared__ double s_r[4][32][6];  // staged entries: FP64 mx, my, a, b, c, o
+    __shared__ float s_c[4][32][3];   // their colours
     __shared__ unsigned s_col[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gi = blockIdx.x * 4 + warp;
     GroupCtx c;
     if (!setup_group(A.groups, A.n_groups, A.cams, A.spix, nullptr, A.Gp, gi, lane, c)) return;
-    const int mylast = c.active ? A.last_img[c.pix] : 0;
-    const int maxlast = __reduce_max_sync(0xffffffffu, mylast);
-    const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
+    // blend_pixel (rasterizer.hpp:100-130) in FP64 with the reference's operation
+    // order (no contraction), so blended sets, termination and C_final are the
+    // reference's decisions, not the FP32 render's
+    const double px = static_cast<double>(c.pxc), py = static_cast<double>(c.pyc);
     const int* tl = A.entries + A.tile_offsets[c.tile];
+    const int n = A.tile_offsets[c.tile + 1] - A.tile_offsets[c.tile];
     const long long off = A.mask_off[gi];
     int* glist = A.glist_out + off;
     unsigned* mout = A.masks_out + off;
     int run = 0, nb = 0, cw = 0, rows = 0;
     unsigned long long buf = 0ull;
-    for (int base = 0; base < maxlast; base += 32) {
+    bool live = c.active;
+    double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+    for (int base = 0; base < n; base += 32) {
+        if (!__any_sync(0xffffffffu, live)) break;
         const int j = base + lane;
         int g = 0;
-        if (j < maxlast) {
+        if (j < n) {
             g = tl[j];
-            const float4* r = A.rec + 3 * (c.vbase + g);
-            const Gate gt = make_gate(r[0], r[1], c.ox, c.oy);
-            s_rec[warp][lane][0] = make_float4(gt.g0, gt.g1, gt.g2, gt.g3);
-            s_rec[warp][lane][1] = make_float4(gt.g4, gt.g5, gt.lo, 0.f);
+            const float4* rf = A.rec + 3 * (c.vbase + g);
+            const float4 r1 = rf[1];
+            s_c[warp][lane][0] = r1.z;
+            s_c[warp][lane][1] = r1.w;
+            s_c[warp][lane][2] = rf[2].x;
+            const double* r = A.rec64 + 6 * (c.vbase + g);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) s_r[warp][lane][q] = r[q];
         }
         __syncwarp();
-        const int mn = min(32, mylast - base);
+        const int mn = min(32, n - base);
         unsigned bits = 0u;
-        for (int k = 0; k < mn; ++k) {
-            const float4 q0 = s_rec[warp][k][0], q1 = s_rec[warp][k][1];
-            const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
-            float alpha;
-            bool cl;
-            if (gate_alpha(gate_q(gt, pq), gt.lo, alpha, cl)) bits |= 1u << k;
+        for (int k = 0; k < mn && live; ++k) {
+            const double* e = s_r[warp][k];
+            const double dx = __dsub_rn(e[0], px), dy = __dsub_rn(e[1], py);
+            const double power =
+                __dsub_rn(__dmul_rn(-0.5, __dadd_rn(__dmul_rn(__dmul_rn(e[2], dx), dx), __dmul_rn(__dmul_rn(e[4], dy), dy))),
+                          __dmul_rn(__dmul_rn(e[3], dx), dy));
+            if (power > 0.0) continue;
+            double alpha = __dmul_rn(e[5], exp(power));
+            if (alpha > kAlphaClampD) alpha = kAlphaClampD;
+            if (alpha < kAlphaSkipD) continue;
+            const double test_t = __dmul_rn(T, __dsub_rn(1.0, alpha));
+            if (test_t < kTFloorD) {
+                live = false;  // not blended; the pixel stops
+                break;
+            }
+            const double w = __dmul_rn(alpha, T);
+            C0 = __dadd_rn(C0, __dmul_rn(w, static_cast<double>(s_c[warp][k][0])));
+            C1 = __dadd_rn(C1, __dmul_rn(w, static_cast<double>(s_c[warp][k][1])));
+            C2 = __dadd_rn(C2, __dmul_rn(w, static_cast<double>(s_c[warp][k][2])));
+            T = test_t;
+            bits |= 1u << k;
         }
         const unsigned un = __reduce_or_sync(0xffffffffu, bits);
         const int rank = __popc(un & ((1u << lane) - 1u));
@@ -330,6 +355,11 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
         const unsigned word = static_cast<unsigned>(buf);
         mout[32 * cw + lane] = word;
         rows += __reduce_max_sync(0xffffffffu, __popc(word));
+    }
+    if (c.active) {
+        A.scol_out[3 * c.s] = static_cast<float>(C0);
+        A.scol_out[3 * c.s + 1] = static_cast<float>(C1);
+        A.scol_out[3 * c.s + 2] = static_cast<float>(C2);
     }
     if (lane == 0) {
         A.gcount_out[gi] = run;
@@ -397,7 +427,7 @@ __global__ void __launch_bounds__(128) k_alpha(SampleArgs A) {
             const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             float alpha = 0.0f;
             bool cl = false;
-            gate_alpha(gate_q(gt, pq), gt.lo, alpha, cl);  // blended: the mask already decided
+            blended_alpha(gate_q(gt, pq), alpha, cl);  // blended: the mask already decided
             out[32 * (row + i) + lane] = alpha_word(cl ? -alpha : alpha, k);
         }
         row += npc;
@@ -780,16 +810,16 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     } else {  // kRhs: u = -w (rendered - truth)
         if (c.active) {
             const float* gp = A.gt + 3 * c.pix;
-            u0 = -A.sw[3 * c.s] * (A.image[3 * c.pix] - gp[0]);
-            u1 = -A.sw[3 * c.s + 1] * (A.image[3 * c.pix + 1] - gp[1]);
-            u2 = -A.sw[3 * c.s + 2] * (A.image[3 * c.pix + 2] - gp[2]);
+            u0 = -A.sw[3 * c.s] * (A.scol[3 * c.s] - gp[0]);
+            u1 = -A.sw[3 * c.s + 1] * (A.scol[3 * c.s + 1] - gp[1]);
+            u2 = -A.sw[3 * c.s + 2] * (A.scol[3 * c.s + 2] - gp[2]);
         }
     }
 
     // ---- J^T pass
-    const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
-    const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
-    const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
+    const float Cf0 = c.active ? A.scol[3 * c.s] : 0.f;  // C_final of the FP64 blend (k_masks)
+    const float Cf1 = c.active ? A.scol[3 * c.s + 1] : 0.f;
+    const float Cf2 = c.active ? A.scol[3 * c.s + 2] : 0.f;
     s_phi[warp][lane] = make_float4(lx, ly, u0, u1);
     s_u2[warp][lane] = u2;
     float2(*pt)[33] = s_pair[warp];
@@ -918,9 +948,9 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     float(*sf)[32] = s_f[warp];
     const float W0 = c.active ? A.sw[3 * c.s] : 0.f, W1 = c.active ? A.sw[3 * c.s + 1] : 0.f,
                 W2 = c.active ? A.sw[3 * c.s + 2] : 0.f;
-    const float Cf0 = c.active ? A.image[3 * c.pix] : 0.f;
-    const float Cf1 = c.active ? A.image[3 * c.pix + 1] : 0.f;
-    const float Cf2 = c.active ? A.image[3 * c.pix + 2] : 0.f;
+    const float Cf0 = c.active ? A.scol[3 * c.s] : 0.f;  // C_final of the FP64 blend (k_masks)
+    const float Cf1 = c.active ? A.scol[3 * c.s + 1] : 0.f;
+    const float Cf2 = c.active ? A.scol[3 * c.s + 2] : 0.f;
     s_pix[warp][lane] = make_float4(c.pxc, c.pyc, W0, W1);
     s_pw2[warp][lane] = W2;
     const int e16 = lane & 15, ph = lane >> 4;
@@ -957,7 +987,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
                               s_gate[warp][4][k], s_gate[warp][5][k], s_gate[warp][6][k]};
                 float alpha = 0.0f;
                 bool clamped = false;
-                gate_alpha(gate_q(gt, pq), gt.lo, alpha, clamped);  // blended: the mask already decided
+                blended_alpha(gate_q(gt, pq), alpha, clamped);  // blended: the mask already decided
                 const float e = __fdividef(alpha, sf[5][k]);  // the falloff before opacity (unclamped)
                 const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
                 const float c2 = sf[8][k];

@@ -271,6 +271,7 @@ struct Batch {
     DevBuf<int> tile_view, tile_offsets, entries, err;
     DevBuf<long long> total;
     DevBuf<float4> rec;
+    DevBuf<double> rec64;  // FP64 [mx, my, a, b, c, o] per (view, Gaussian): exact blend decisions
     DevBuf<unsigned long long> keys;
     DevBuf<short4> rect;
     DevBuf<float> image, trans, gt;
@@ -339,6 +340,7 @@ struct Batch {
         SLM_CUDA_CHECK(cudaMemcpyAsync(tile_view.p, htile_view.data(), sizeof(int) * n_tiles, cudaMemcpyHostToDevice, st));
         const size_t VG = static_cast<size_t>(V) * Gp;
         rec.ensure(3 * VG);
+        rec64.ensure(6 * VG);
         keys.ensure(VG);
         rect.ensure(VG);
         tile_offsets.ensure(n_tiles + 1);
@@ -349,7 +351,7 @@ struct Batch {
         // K1 + the entry total (sum of tile-rect areas); the per-tile offsets come
         // out of the sorted tile ids (build_tile_lists), so no per-tile atomics
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p,
-                       reinterpret_cast<unsigned long long*>(total.p), err.p, st);
+                       reinterpret_cast<unsigned long long*>(total.p), err.p, rec64.p, st);
         // depth-sort keys in index order + the AND/OR of the valid keys (which
         // key bytes need a radix pass)
         const long long nvg = static_cast<long long>(V) * Gp;
@@ -442,7 +444,7 @@ struct Samples {
     pinned_vector<Group> hgroups;
     DevBuf<Group> groups;
     DevBuf<int> spix, sorig;
-    DevBuf<float> sw;
+    DevBuf<float> sw, scol;  // scol: per-sample C_final of the FP64 blend (k_masks)
     DevBuf<long long> mask_off;
     DevBuf<unsigned> masks, cols;
     DevBuf<int> glist, gcount, grows;
@@ -560,6 +562,7 @@ struct Samples {
         spix.ensure(std::max<size_t>(order.size(), 1));
         sorig.ensure(std::max<size_t>(order.size(), 1));
         sw.ensure(std::max<size_t>(3 * order.size(), 1));
+        scol.ensure(std::max<size_t>(3 * order.size(), 1));
         SLM_CUDA_CHECK(cudaMemcpyAsync(mask_off.p, hoff.data(), sizeof(long long) * hoff.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(groups.p, hgroups.data(), sizeof(Group) * hgroups.size(), cudaMemcpyHostToDevice, st));
         SLM_CUDA_CHECK(cudaMemcpyAsync(sorig.p, horig.data(), sizeof(int) * horig.size(), cudaMemcpyHostToDevice, st));
@@ -757,6 +760,7 @@ struct Jacobian {
         SLM_CUDA_CHECK(cudaMemsetAsync(tan.p, 0, 3 * VG * sizeof(float4), ctx->stream));
         // the blend masks depend on the state only: computed once per (state, plan)
         SampleArgs a = args();
+        a.scol_out = samples.scol.p;
         a.masks_out = samples.masks.p;
         a.glist_out = samples.glist.p;
         a.gcount_out = samples.gcount.p;
@@ -827,6 +831,8 @@ struct Jacobian {
         a.wbase = samples.wbase.p;
         a.rstream = samples.rstream.p;
         a.cols = samples.cols.p;
+        a.rec64 = batch->rec64.p;
+        a.scol = samples.scol.p;
         return a;
     }
 
@@ -868,7 +874,7 @@ struct Jacobian {
         res_in.ensure(std::max<long long>(rdim, 1));
         launch_ssim_fold(samples.groups.p, static_cast<int>(samples.hgroups.size()), batch->cams.p, samples.spix.p,
                          samples.sorig.p, samples.sw.p, batch->image.p, batch->gt.p, batch->ssim_res.p,
-                         batch->ssim_dc.p, ssim_weight, res_in.p, ctx->stream);
+                         batch->ssim_dc.p, ssim_weight, res_in.p, samples.scol.p, ctx->stream);
         SampleArgs a = args();
         a.in_res = res_in.p;
         launch_sample_raster(kVjp, a, ctx->stream);
@@ -904,6 +910,7 @@ struct Jacobian {
         d.gcount = samples.gcount.p;
         d.mask_off = samples.mask_off.p;
         d.cols = samples.cols.p;
+        d.scol = samples.scol.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
                              batch->rec.p, diagacc.p, dout, ctx->stream);

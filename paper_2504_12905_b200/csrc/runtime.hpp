@@ -67,7 +67,8 @@ struct DevBuf {
 
 // ---- launchers (defined in the .cu files)
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
-                    unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err, cudaStream_t st);
+                    unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err,
+                    double* rec64, cudaStream_t st);
 void launch_depth_init(const unsigned long long* keys, const short4* rect, int G, int Gp, int V,
                        unsigned long long* kout, unsigned* vout, unsigned long long* and_or, cudaStream_t st);
 void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,
@@ -123,7 +124,7 @@ void launch_ssim_diag(const double* a, const double* b, const ImgDesc* imgs, int
                       cudaStream_t st);
 void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, const int* spix, const int* sorig,
                       float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
-                      float ssim_weight, float* rhs, cudaStream_t st);
+                      float ssim_weight, float* rhs, const float* scol, cudaStream_t st);
 void launch_weighted_draw(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
                           const float* image, const float* gt, const int* contrib, int dist, int spt,
                           const double* U, double n_total, double inv_total, int* spix, float* sw,
