@@ -269,6 +269,7 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 // windows and never stage an entry no lane uses.
 __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     __shared__ double s_r[4][32][6];  // staged entries: FP64 mx, my, a, b, c, o
+    __shared__ double s_thr[4][32];   // power below which alpha < 1/255 for sure
     __shared__ float s_c[4][32][3];   // their colours
     __shared__ unsigned s_col[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -302,6 +303,10 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
             const double* r = A.rec64 + 6 * (c.vbase + g);
 #pragma unroll
             for (int q = 0; q < 6; ++q) s_r[warp][lane][q] = r[q];
+            // o exp(power) < 1/255 whenever power < log(1/(255 o)) by more than the
+            // rounding of log/exp/multiply: those pairs skip without the exponential
+            // (the decision is unchanged; pairs near the edge take the exact path)
+            s_thr[warp][lane] = r[5] > 0.0 ? log(kAlphaSkipD / r[5]) - 1e-9 : -1e300;
         }
         __syncwarp();
         const int mn = min(32, n - base);
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
             const double power =
                 __dsub_rn(__dmul_rn(-0.5, __dadd_rn(__dmul_rn(__dmul_rn(e[2], dx), dx), __dmul_rn(__dmul_rn(e[4], dy), dy))),
                           __dmul_rn(__dmul_rn(e[3], dx), dy));
-            if (power > 0.0) continue;
+            if (power > 0.0 || power < s_thr[warp][k]) continue;
             double alpha = __dmul_rn(e[5], exp(power));
             if (alpha > kAlphaClampD) alpha = kAlphaClampD;
             if (alpha < kAlphaSkipD) continue;
