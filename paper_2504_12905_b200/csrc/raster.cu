@@ -270,6 +270,7 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     __shared__ double s_r[4][32][6];  // staged entries: FP64 mx, my, a, b, c, o
     __shared__ double s_thr[4][32];   // power below which alpha < 1/255 for sure
+    __shared__ float4 s_g[4][32][2];  // FP32 gate polynomials (pre-filter)
     __shared__ float s_c[4][32][3];   // their colours
     __shared__ unsigned s_col[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
     // order (no contraction), so blended sets, termination and C_final are the
     // reference's decisions, not the FP32 render's
     const double px = static_cast<double>(c.pxc), py = static_cast<double>(c.pyc);
+    const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
     const int* tl = A.entries + A.tile_offsets[c.tile];
     const int n = A.tile_offsets[c.tile + 1] - A.tile_offsets[c.tile];
     const long long off = A.mask_off[gi];
@@ -296,22 +298,39 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
         if (j < n) {
             g = tl[j];
             const float4* rf = A.rec + 3 * (c.vbase + g);
-            const float4 r1 = rf[1];
+            const float4 r0 = rf[0], r1 = rf[1];
             s_c[warp][lane][0] = r1.z;
             s_c[warp][lane][1] = r1.w;
             s_c[warp][lane][2] = rf[2].x;
+            const Gate gt = make_gate(r0, r1, c.ox, c.oy);
+            s_g[warp][lane][0] = make_float4(gt.g0, gt.g1, gt.g2, gt.g3);
+            s_g[warp][lane][1] = make_float4(gt.g4, gt.g5, gt.lo, 0.f);
+        }
+        __syncwarp();
+        const int mn = min(32, n - base);
+        // FP32 pre-filter (the shared gate): a pair whose q' is below log2(1/255) by
+        // far more than FP32 rounding cannot blend; the others are decided in FP64,
+        // and only entries some lane may blend get their FP64 record staged
+        unsigned cand = 0u;
+        if (live)
+            for (int k = 0; k < mn; ++k) {
+                const float4 q0 = s_g[warp][k][0], q1 = s_g[warp][k][1];
+                const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
+                if (gate_q(gt, pq) >= kLog2Skip - 0.5f) cand |= 1u << k;  // FP32 q' error < 1e-3 measured
+            }
+        const unsigned any_cand = __reduce_or_sync(0xffffffffu, cand);
+        if (j < n && ((any_cand >> lane) & 1u)) {
             const double* r = A.rec64 + 6 * (c.vbase + g);
 #pragma unroll
             for (int q = 0; q < 6; ++q) s_r[warp][lane][q] = r[q];
             // o exp(power) < 1/255 whenever power < log(1/(255 o)) by more than the
             // rounding of log/exp/multiply: those pairs skip without the exponential
-            // (the decision is unchanged; pairs near the edge take the exact path)
             s_thr[warp][lane] = r[5] > 0.0 ? log(kAlphaSkipD / r[5]) - 1e-9 : -1e300;
         }
         __syncwarp();
-        const int mn = min(32, n - base);
         unsigned bits = 0u;
-        for (int k = 0; k < mn && live; ++k) {
+        for (unsigned cm = cand; cm && live; cm &= cm - 1) {
+            const int k = __ffs(cm) - 1;
             const double* e = s_r[warp][k];
             const double dx = __dsub_rn(e[0], px), dy = __dsub_rn(e[1], py);
             const double power =
