@@ -689,3 +689,29 @@ def test_full_size_batch_properties(gpu):
     ga, gb = jac.gn_apply(0.1, a), jac.gn_apply(0.1, b)
     assert rel_error(float(np.dot(a, gb)), float(np.dot(b, ga))) < TOL
     assert norm_rel(jac.gn_apply(0.1, a + 2.0 * b), ga + 2.0 * gb) < TOL
+
+
+def test_evaluate_edge_cases(gpu):
+    """metrics::evaluate on identical, constant and empty images (test_metrics.cpp:88-99):
+    ssim(a, a) == 1, psnr capped at 100 dB, empty images give mse 0 / ssim 1."""
+    a = np.full((9, 13, 3), 0.25)
+    r = gpu.evaluate(a, a)
+    assert (r.mse, r.psnr, r.ssim) == (0.0, 100.0, 1.0)
+    b = np.full((9, 13, 3), 0.75)
+    c = gpu.evaluate(a, b)
+    assert c.mse == pytest.approx(0.25) and c.psnr == pytest.approx(10 * math.log10(4.0))
+    e = gpu.evaluate(np.zeros((0, 0, 3)), np.zeros((0, 0, 3)))
+    assert (e.mse, e.psnr, e.ssim) == (0.0, 100.0, 1.0)
+
+
+def test_train_run_wall_clock_column(gpu, tmp_path):
+    """Non-deterministic mode fills wall_ms with %.3f (run.cpp:54-75)."""
+    from paper_2504_12905_b200.run import METRICS_CSV_HEADER, RunConfig, train_run
+    train_run(gpu, RunConfig(optimizer="sgd", iterations=2, eval_every=0, out_dir=str(tmp_path),
+                             deterministic=False))
+    rows = (tmp_path / "metrics.csv").read_text().splitlines()
+    assert rows[0] == METRICS_CSV_HEADER and len(rows) == 3
+    for row in rows[1:]:
+        f = row.split(",")
+        assert len(f) == 8 and f[1] and len(f[1].split(".")[1]) == 3 and f[5] == f[6] == f[7] == ""
+    assert rows[-1].split(",")[3]  # the last iteration is always evaluated
