@@ -1093,6 +1093,71 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     }
 }
 
+// ------------------------------------------------------------------ exact render
+// render_full's drop-in form (rasterizer.cpp:62-104): blend_pixel replayed in
+// FP64 per pixel (the reference's operation order, FP64 geometry from
+// k_prepare, colours from the record), one thread per pixel.  Slower than
+// k_render; used by slm_render_full so the API returns the reference's
+// decisions (contrib, T) exactly.
+__global__ void __launch_bounds__(128) k_render_exact(const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
+                                                      int n_tiles, const int* __restrict__ tile_offsets,
+                                                      const int* __restrict__ entries, const double* __restrict__ rec64,
+                                                      const float4* __restrict__ rec, int Gp, double* __restrict__ image,
+                                                      double* __restrict__ trans, int* __restrict__ contrib) {
+    const int tile = blockIdx.y;
+    if (tile >= n_tiles) return;
+    const int v = tile_view[tile];
+    const DevCam& cam = cams[v];
+    const int lt = tile - cam.tile_base;
+    const int tx = lt % cam.tiles_x, ty = lt / cam.tiles_x;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // pixel of the 16x16 tile
+    if (idx >= kTile * kTile) return;
+    const int x = tx * kTile + idx % kTile, y = ty * kTile + idx / kTile;
+    if (x >= cam.width || y >= cam.height) return;
+    const double px = x + 0.5, py = y + 0.5;
+    const int b = tile_offsets[tile], n = tile_offsets[tile + 1] - b;
+    const size_t vbase = static_cast<size_t>(v) * Gp;
+    double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+    int cnt = 0;
+    for (int k = 0; k < n; ++k) {
+        const int g = entries[b + k];
+        const double* e = rec64 + 6 * (vbase + g);
+        const double dx = __dsub_rn(e[0], px), dy = __dsub_rn(e[1], py);
+        const double power =
+            __dsub_rn(__dmul_rn(-0.5, __dadd_rn(__dmul_rn(__dmul_rn(e[2], dx), dx), __dmul_rn(__dmul_rn(e[4], dy), dy))),
+                      __dmul_rn(__dmul_rn(e[3], dx), dy));
+        if (power > 0.0) continue;
+        double alpha = __dmul_rn(e[5], exp(power));
+        if (alpha > kAlphaClampD) alpha = kAlphaClampD;
+        if (alpha < kAlphaSkipD) continue;
+        const double test_t = __dmul_rn(T, __dsub_rn(1.0, alpha));
+        if (test_t < kTFloorD) break;
+        const double w = __dmul_rn(alpha, T);
+        const float4* r = rec + 3 * (vbase + g);
+        const float4 r1 = r[1];
+        C0 = __dadd_rn(C0, __dmul_rn(w, static_cast<double>(r1.z)));
+        C1 = __dadd_rn(C1, __dmul_rn(w, static_cast<double>(r1.w)));
+        C2 = __dadd_rn(C2, __dmul_rn(w, static_cast<double>(r[2].x)));
+        T = test_t;
+        ++cnt;
+    }
+    const size_t pix = cam.pix_base + static_cast<size_t>(y) * cam.width + x;
+    image[3 * pix] = C0;
+    image[3 * pix + 1] = C1;
+    image[3 * pix + 2] = C2;
+    trans[pix] = T;
+    contrib[pix] = cnt;
+}
+
+void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
+                         const int* entries, const double* rec64, const float4* rec, int Gp, double* image,
+                         double* trans, int* contrib, cudaStream_t st) {
+    if (n_tiles == 0) return;
+    k_render_exact<<<dim3(2, n_tiles), 128, 0, st>>>(cams, tile_view, n_tiles, tile_offsets, entries, rec64, rec, Gp,
+                                                     image, trans, contrib);
+    ++g_launches;
+}
+
 // ------------------------------------------------------------------ launchers
 void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,

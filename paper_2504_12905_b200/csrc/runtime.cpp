@@ -2023,15 +2023,22 @@ int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* 
         Scene s(c, *g);
         Batch b(c);
         b.prepare(s, {*cam});
-        b.render(false);
+        // the reference's blend replayed in FP64 (k_render_exact): contrib / T are
+        // its decisions, the image its values up to FP32-stored colours
         const size_t np = static_cast<size_t>(cam->width) * cam->height;
-        std::vector<float> img(3 * np), tr(np);
-        SLM_CUDA_CHECK(cudaMemcpyAsync(img.data(), b.image.p, sizeof(float) * 3 * np, cudaMemcpyDeviceToHost, c->stream));
-        SLM_CUDA_CHECK(cudaMemcpyAsync(tr.data(), b.trans.p, sizeof(float) * np, cudaMemcpyDeviceToHost, c->stream));
-        if (contrib) SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, b.contrib.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c->stream));
+        DevBuf<double> dimg, dtr;
+        DevBuf<int> dcn;
+        dimg.ensure(std::max<size_t>(3 * np, 1));
+        dtr.ensure(std::max<size_t>(np, 1));
+        dcn.ensure(std::max<size_t>(np, 1));
+        launch_render_exact(b.cams.p, b.tile_view.p, b.n_tiles, b.tile_offsets.p, b.entries.p, b.rec64.p, b.rec.p, b.Gp,
+                            dimg.p, dtr.p, dcn.p, c->stream);
+        c->check_launch();
+        if (image) SLM_CUDA_CHECK(cudaMemcpyAsync(image, dimg.p, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost, c->stream));
+        if (transmittance)
+            SLM_CUDA_CHECK(cudaMemcpyAsync(transmittance, dtr.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+        if (contrib) SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, dcn.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c->stream));
         c->sync();
-        if (image) for (size_t i = 0; i < 3 * np; ++i) image[i] = img[i];
-        if (transmittance) for (size_t i = 0; i < np; ++i) transmittance[i] = tr[i];
     });
 }
 

@@ -84,6 +84,9 @@ void launch_beta_mirror(const double* beta, float* beta32, int n, cudaStream_t s
 void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,
                    float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st);
+void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
+                         const int* entries, const double* rec64, const float4* rec, int Gp, double* image,
+                         double* trans, int* contrib, cudaStream_t st);
 void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile, double* sse_view,
                       cudaStream_t st);
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);
