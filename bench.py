@@ -486,7 +486,7 @@ def run_b200(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 raster + f64 per-Gaussian linearisation",
+        "dtype": "f32 (raster, linearisation, CG vectors; f64 projection, blend decisions and parameters)",
         "data": "synthetic (random_init state, ring cameras; BASELINE configs[2] shape)",
         "config": {"workload": "configs[2]: 1M Gaussians (SH-0), 200 views 1280x720, 8-view LM batch per rank, "
                                "N=32 samples/tile, lambda=0.1",
