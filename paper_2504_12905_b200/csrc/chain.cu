@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
-__global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
                                                        const float4* __restrict__ rec,
                                                        float* __restrict__ diagacc, float* __restrict__ out) {
@@ -353,12 +353,6 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
     if (g >= G) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
-    float dSj[7][9];  // dSigma for the 3 log-scale + 4 quaternion unit probes
-    for (int j = 0; j < 7; ++j) {
-        float dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0};
-        if (j < 3) dls[j] = 1.0f; else dq[j - 3] = 1.0f;
-        dsigma(Gm, dls, dq, dSj[j]);
-    }
     float d[kP];
     for (int k = 0; k < kP; ++k) d[k] = 0.0f;
     const float zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -399,6 +393,10 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
         const DevCam& cam = cams[v];
         View Vw;
         load_view(Gm, cam, q0, q1, Vw);
+        // the 10 geometry probes, unrolled so every array index is static (the
+        // 3 log-scale + 4 quaternion dSigma are recomputed per view rather than
+        // kept as a 63-float array in local memory)
+#pragma unroll
         for (int j = 0; j < 10; ++j) {
             float col[5];
             if (j < 3) {
@@ -406,7 +404,11 @@ __global__ void __launch_bounds__(128) k_diag_finalize(const float* __restrict__
                 dmu[j] = 1.0f;
                 view_tangent(Vw, cam, dmu, zero9, col);
             } else {
-                view_tangent(Vw, cam, zero3, dSj[j - 3], col);
+                float dls[3] = {0, 0, 0}, dq[4] = {0, 0, 0, 0}, dS[9];
+                if (j < 6) dls[j - 3] = 1.0f;
+                else dq[j - 6] = 1.0f;
+                dsigma(Gm, dls, dq, dS);
+                view_tangent(Vw, cam, zero3, dS, col);
             }
             float qf = 0.0f;
             for (int a = 0; a < 5; ++a) {
