@@ -670,7 +670,7 @@ def _cfg2_inputs(views):
 
 def test_full_size_products_vs_reference(gpu):
     """configs[2] at full size (1M Gaussians, 1280x720, N = 32) on one of the batch
-    views: gn_apply and diag(J^T W J) through the device vs the reference library
+    views: Jv, J^T u, gn_apply and diag(J^T W J) through the device vs the reference library
     itself (oracle/_ref, all host threads; the C port where it was not built).
     Exercises the size-dependent paths (long tile lists, alpha rows beyond the
     staged 18, large groups) that the small fixtures do not reach."""
@@ -681,11 +681,15 @@ def test_full_size_products_vs_reference(gpu):
     state, cams, plan = _cfg2_inputs(1)
     jr = lib.jacobian(state, cams, plan)
     jg = gpu.jacobian(state, cams, plan)
-    p = np.random.default_rng(0).uniform(-1, 1, jr.param_dim())
+    r = np.random.default_rng(0)
+    p = r.uniform(-1, 1, jr.param_dim())
+    u = r.uniform(-1, 1, jr.residual_dim())
+    e_jv = norm_rel(jg.jvp(p), jr.jvp(p))
+    e_vj = norm_rel(jg.vjp(u), jr.vjp(u))
     e_gn = norm_rel(jg.gn_apply(0.1, p), jr.gn_apply(0.1, p))
     e_d = norm_rel(jg.jtj_diag(), jr.jtj_diag())
-    print("full-size gn_apply rel", e_gn, "diag rel", e_d)
-    assert e_gn < TOL and e_d < TOL
+    print("full-size jvp", e_jv, "vjp", e_vj, "gn_apply", e_gn, "diag", e_d)
+    assert max(e_jv, e_vj, e_gn, e_d) < TOL
 
 
 def test_full_size_batch_properties(gpu):
