@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-psnr", action="store_true", help="skip the configs[0] time-to-PSNR run")
     ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
+    ap.add_argument("--accumulate", default="ordered", choices=["ordered", "atomic"],
+                    help="J^T / diag accumulation: fixed per-plan order (bitwise reproducible, default) "
+                         "or float red.global.add")
     return ap.parse_args()
 
 
@@ -334,6 +337,7 @@ def run_b200(args):
             pass
     from paper_2504_12905_b200 import splatlm
     L = splatlm.Lib(local)
+    L.set_deterministic(args.accumulate == "ordered")
     stream = torch.cuda.Stream()
     L.set_stream(stream.cuda_stream)
     if world > 1:
@@ -493,7 +497,8 @@ def run_b200(args):
                    "gaussians": args.gaussians, "views": args.views, "width": args.width,
                    "height": args.height, "batch_views_per_rank": args.batch, "samples_per_tile": args.spt,
                    "parallelism": f"view-sharded x{world}, NCCL allreduce per product" if world > 1 else "1 GPU",
-                   "l2": "working set > 126 MB L2 (no flush needed)"},
+                   "l2": "working set > 126 MB L2 (no flush needed)",
+                   "accumulation": args.accumulate},
         "roofline": {"bound": "hbm", "kernel": "k_sample_raster<GN> (fused Jv -> W -> J^T)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("k_sample_raster<2>"), "algorithmic_bytes_per_launch": bytes_["raster"],

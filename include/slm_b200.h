@@ -52,6 +52,13 @@ int slm_context_synchronize(slm_context* ctx);
 int slm_nccl_unique_id(uint8_t out[128]);
 int slm_context_init_comm(slm_context* ctx, const uint8_t id[128], int rank, int world);
 int slm_context_rank(slm_context* ctx, int* rank, int* world);
+/* J^T / diag(J^T W J) accumulation order.  on (the default): every (view,
+ * Gaussian)'s per-entry contributions are summed in a fixed per-plan order, so
+ * jvp / vjp / jtj_diag / gn_apply / pcg / lm_step are bitwise reproducible run
+ * to run (the reference's determinism contract, jacobian.cpp:19-21,246-247,
+ * test_solver.cpp:268-286).  off: float red.global.add (order follows the
+ * scheduler).  Takes effect at the next plan (Jacobian / lm_step). */
+int slm_context_set_deterministic(slm_context* ctx, int on);
 /* Per-stage CUDA-event timings of the last lm_step / gn_apply (ms). */
 int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n);
 

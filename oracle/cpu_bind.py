@@ -109,6 +109,11 @@ class CpuLib:
             fn.restype = res
             fn.argtypes = args
             setattr(self, "_" + name, fn)
+        if hasattr(self.lib, prefix + "sample_view_batch"):  # the reference library only
+            fn = getattr(self.lib, prefix + "sample_view_batch")
+            fn.restype = C.c_int
+            fn.argtypes = [_i32p, C.c_int, C.c_int, _vp, _i32p]
+            self._sample_view_batch = fn
 
     # ---- helpers ----
     def _check(self, rc: int):
@@ -244,6 +249,16 @@ class CpuLib:
         assign = np.zeros(len(cams), np.int32)
         self._check(self._kmeans_cameras(cameras_to_c(cams), len(cams), k, seed, i32ptr(assign)))
         return [list(np.nonzero(assign == c)[0]) for c in range(k)]
+
+    def sample_view_batch(self, clusters, rng: "Rng") -> list:
+        """sampling::sample_view_batch (view_sampler.cpp:173-184)."""
+        n = sum(len(c) for c in clusters)
+        assign = np.zeros(n, np.int32)
+        for c, m in enumerate(clusters):
+            assign[list(m)] = c
+        out = np.zeros(len(clusters), np.int32)
+        self._check(self._sample_view_batch(i32ptr(assign), n, len(clusters), rng.h, i32ptr(out)))
+        return [int(x) for x in out]
 
     def camera_features(self, cams) -> np.ndarray:
         f = np.zeros((len(cams), 6))

@@ -374,6 +374,17 @@ int ref_kmeans_cameras(const slm_camera* cams, int n_cams, int k, uint64_t seed,
     });
 }
 
+// sampling::sample_view_batch (view_sampler.cpp:173-184) over the clusters
+// given as assign[n_cams] in [0, k) (each cluster's members in index order).
+int ref_sample_view_batch(const int32_t* assign, int n_cams, int k, void* rng, int32_t* batch) {
+    return guarded([&] {
+        std::vector<std::vector<int>> clusters(k);
+        for (int i = 0; i < n_cams; ++i) clusters.at(assign[i]).push_back(i);
+        const auto b = sampling::sample_view_batch(clusters, *static_cast<std::mt19937_64*>(rng));
+        for (size_t i = 0; i < b.size(); ++i) batch[i] = b[i];
+    });
+}
+
 int ref_camera_features(const slm_camera* cams, int n_cams, double* feats) {
     return guarded([&] {
         const auto f = sampling::camera_features(to_cams(cams, n_cams));

@@ -322,4 +322,21 @@ void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st
     k_axpy<<<kRedBlocks, 256, 0, st>>>(y, x, n, a); ++g_launches;
 }
 
+// f32 <-> f64 element copies (the truth images widened for the FP64 metrics,
+// FP64 SSIM planes narrowed for the f32 products)
+template <typename A, typename B>
+__global__ void k_convert(const A* __restrict__ x, B* __restrict__ y, long long n) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        y[i] = static_cast<B>(x[i]);
+}
+void launch_widen(const float* x, double* y, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_convert<float, double><<<kRedBlocks, 256, 0, st>>>(x, y, n); ++g_launches;
+}
+void launch_narrow(const double* x, float* y, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_convert<double, float><<<kRedBlocks, 256, 0, st>>>(x, y, n); ++g_launches;
+}
+
 }  // namespace slm

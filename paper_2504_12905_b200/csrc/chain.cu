@@ -220,17 +220,86 @@ __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta
     }
 }
 
+// ------------------------------------------------------------------ deterministic sums
+// The (view, Gaussian)s of one warp -- view v, Gaussians g0..g0+31 -- own the
+// contiguous range [seg[vg0], seg[vg0 + 32]) of the sorted slot list, so the
+// warp walks it SPL*32 slots at a time: coalesced perm reads, then every
+// lane's SPL partials gathered at once (all loads of a chunk in flight
+// together) into shared memory, then each lane adds the slots of its own
+// segment in slot order.  The order is a function of the plan only, so every
+// product rounds identically (the reference's contract: results independent
+// of scheduling, jacobian.cpp:19-21,246-247).  The segment bounds of the next
+// view are loaded one view ahead (DetSeg), so a view costs two dependent
+// round trips (perm, partials) per chunk -- typically one chunk.
+struct DetSeg {
+    unsigned a, b;  // this lane's segment [a, b)
+};
+__device__ __forceinline__ DetSeg det_seg(const DetOrder& D, size_t vg) {
+    return DetSeg{__ldg(D.seg + vg), __ldg(D.seg + vg + 1)};
+}
+
+template <int NF4, int SPL>
+__device__ __forceinline__ void det_gather(const DetOrder& D, DetSeg sg, int lane, float4 (*stage)[NF4],
+                                           float4 acc[NF4]) {
+    const unsigned r0 = __shfl_sync(0xffffffffu, sg.a, 0), r1 = __shfl_sync(0xffffffffu, sg.b, 31);
+#pragma unroll
+    for (int q = 0; q < NF4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* part = reinterpret_cast<const float4*>(D.partial);
+    for (unsigned base = r0; base < r1; base += 32 * SPL) {
+        unsigned sl[SPL];
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) {
+            const unsigned i = base + 32 * k + lane;
+            sl[k] = i < r1 ? __ldg(D.perm + i) : 0xffffffffu;
+        }
+        // global -> shared without a register round trip (LDGSTS), all in flight
+#pragma unroll
+        for (int k = 0; k < SPL; ++k)
+            if (sl[k] != 0xffffffffu)
+#pragma unroll
+                for (int q = 0; q < NF4; ++q) {
+                    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&stage[32 * k + lane][q]));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                                 "l"(part + static_cast<size_t>(sl[k]) * NF4 + q)
+                                 : "memory");
+                }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const unsigned a = sg.a > base ? sg.a : base, b = sg.b < base + 32 * SPL ? sg.b : base + 32 * SPL;
+        for (unsigned j = a; j < b; ++j)
+#pragma unroll
+            for (int q = 0; q < NF4; ++q) {
+                const float4 v = stage[j - base][q];
+                acc[q].x += v.x;
+                acc[q].y += v.y;
+                acc[q].z += v.z;
+                acc[q].w += v.w;
+            }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ K11
 // out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
-// exact reverse mode of the projection; inter is zeroed after reading.
+// exact reverse mode of the projection.  Atomic mode: inter (red.global.add
+// sums) is zeroed after reading.  Deterministic mode (D.partial): inter_v[g]
+// is the ordered sum of the (view, Gaussian)'s slots (det_gather).
+template <bool DET>
 __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ rec, float* __restrict__ inter,
-                                               const float* __restrict__ p, float lambda,
+                                               DetOrder D, const float* __restrict__ p, float lambda,
                                                float* __restrict__ out, const int* __restrict__ done_flag) {
+    constexpr int SPL = 4;
+    __shared__ float4 s_stage[4][32 * SPL][3];
     if (done_flag && *done_flag) return;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int lane = threadIdx.x & 31;
+    if (DET) {
+        if (g - lane >= G) return;  // whole warp past the end (the gather is warp-cooperative)
+    } else if (g >= G) {
+        return;
+    }
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
@@ -242,21 +311,37 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         nr0 = __ldg(rec + 3 * vg);
         nr1 = __ldg(rec + 3 * vg + 1);
-        const float4* ip = reinterpret_cast<const float4*>(inter + vg * kRec);
-        ni0 = ip[0];
-        ni1 = ip[1];
-        ni2 = ip[2];
+        if (!DET) {
+            const float4* ip = reinterpret_cast<const float4*>(inter + vg * kRec);
+            ni0 = ip[0];
+            ni1 = ip[1];
+            ni2 = ip[2];
+        }
     };
     if (V > 0) fetch(0);
+    DetSeg sn{0u, 0u};
+    if (DET && V > 0) sn = det_seg(D, g);
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        const float4 q0 = nr0, q1 = nr1, i0 = ni0, i1 = ni1, i2 = ni2;
+        float4 i0 = ni0, i1 = ni1, i2 = ni2;
+        if (DET) {  // warp-uniform: every lane of the warp is here
+            const DetSeg sg = sn;
+            if (v + 1 < V) sn = det_seg(D, vg + Gp);
+            float4 acc[3];
+            det_gather<3, SPL>(D, sg, lane, s_stage[threadIdx.x >> 5], acc);
+            i0 = acc[0];
+            i1 = acc[1];
+            i2 = acc[2];
+        }
+        const float4 q0 = nr0, q1 = nr1;
         if (v + 1 < V) fetch(v + 1);
         if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
-        float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
-        ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ip[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!DET) {
+            float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
+            ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ip[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         const float gmx = i0.x, gmy = i0.y, gca = i0.z, gcb = i0.w, gcc = i1.x;
         go += i1.y;
         gc0 += i1.z;
@@ -335,6 +420,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     res[11] = gc0 * Gm.dcol[0];
     res[12] = gc1 * Gm.dcol[1];
     res[13] = gc2 * Gm.dcol[2];
+    if (g >= G) return;
     for (int k = 0; k < kP; ++k) {
         float val = res[k];
         if (p) val += lambda * p[k * Gp + g];
@@ -345,12 +431,21 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
+template <bool DET>
 __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
                                                        const float4* __restrict__ rec,
-                                                       float* __restrict__ diagacc, float* __restrict__ out) {
+                                                       float* __restrict__ diagacc, DetOrder D,
+                                                       float* __restrict__ out) {
+    constexpr int SPL = 4;
+    __shared__ float4 s_stage[4][32 * SPL][5];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int lane = threadIdx.x & 31;
+    if (DET) {
+        if (g - lane >= G) return;
+    } else if (g >= G) {
+        return;
+    }
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float d[kP];
@@ -364,12 +459,21 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         nr0 = __ldg(rec + 3 * vg);
         nr1 = __ldg(rec + 3 * vg + 1);
         nr2 = __ldg(rec + 3 * vg + 2);
-        const float4* a4 = reinterpret_cast<const float4*>(diagacc + vg * kDiagRec);
-        for (int q4 = 0; q4 < 5; ++q4) na[q4] = a4[q4];
+        if (!DET) {
+            const float4* a4 = reinterpret_cast<const float4*>(diagacc + vg * kDiagRec);
+            for (int q4 = 0; q4 < 5; ++q4) na[q4] = a4[q4];
+        }
     };
     if (V > 0) fetch(0);
+    DetSeg sn{0u, 0u};
+    if (DET && V > 0) sn = det_seg(D, g);
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
+        if (DET) {  // warp-uniform
+            const DetSeg sg = sn;
+            if (v + 1 < V) sn = det_seg(D, vg + Gp);
+            det_gather<5, SPL>(D, sg, lane, s_stage[threadIdx.x >> 5], na);
+        }
         const float4 q0 = nr0, q1 = nr1, q2 = nr2;
         float acc[20];
         for (int q4 = 0; q4 < 5; ++q4) {
@@ -380,8 +484,10 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         }
         if (v + 1 < V) fetch(v + 1);
         if (q2.y == 0.0f) continue;
-        float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
-        for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!DET) {
+            float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
+            for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         float M[5][5];
         int q = 0;
         for (int i = 0; i < 5; ++i)
@@ -424,7 +530,10 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         d[12] += acc[17] * Gm.dcol[1] * Gm.dcol[1];
         d[13] += acc[18] * Gm.dcol[2] * Gm.dcol[2];
     }
-    for (int k = 0; k < kP; ++k) out[k * Gp + g] = d[k];
+    if (g >= G) return;
+    // each row is a sum of squares (jtj_diag, jacobian.cpp:272-337); the quadratic
+    // form P^T M P of rounded moment sums can dip a few ulp below zero -- clamp
+    for (int k = 0; k < kP; ++k) out[k * Gp + g] = fmaxf(d[k], 0.0f);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -435,15 +544,24 @@ void launch_tangents(const float* beta32, const float* p, int G, int Gp, const D
 }
 
 void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
-                  float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st) {
+                  float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
+                  cudaStream_t st) {
     if (G == 0) return;
-    k_chain<<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, p, lambda, out, done); ++g_launches;
+    if (det.partial)
+        k_chain<true><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    else
+        k_chain<false><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    ++g_launches;
 }
 
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
-                          float* diagacc, float* out, cudaStream_t st) {
+                          float* diagacc, const DetOrder& det, float* out, cudaStream_t st) {
     if (G == 0) return;
-    k_diag_finalize<<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, out); ++g_launches;
+    if (det.partial)
+        k_diag_finalize<true><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    else
+        k_diag_finalize<false><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    ++g_launches;
 }
 
 }  // namespace slm

@@ -94,6 +94,21 @@ struct SampleArgs {
     const double* rec64;
     const float* scol;
     float* scol_out;
+    // Deterministic accumulation (the default): instead of red.global.add into
+    // `inter`, the J^T pass writes each compacted entry's 9-float contribution
+    // to its own slot, slot = 32 * wbase[g] + j (12 floats per slot); the chain
+    // kernel sums a (view, Gaussian)'s slots in slot order (DetOrder).
+    float* partial;
+};
+
+// Per-plan order of the deterministic accumulation (sort.cu build_slot_order):
+// perm = the slots sorted by (view * Gp + Gaussian), stable, so each
+// (view, Gaussian)'s slots are the contiguous range [seg[vg], seg[vg + 1]) in
+// slot order.  Fixed per plan -> every product sums in the same order.
+struct DetOrder {
+    const unsigned* perm;
+    const unsigned* seg;
+    const float* partial;  // kRec floats per slot (J^T) or kDiagRec (diag)
 };
 
 constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)
@@ -117,6 +132,8 @@ struct DiagArgs {
     const long long* mask_off;
     const unsigned* cols;  // column masks (SampleArgs::cols)
     const float* scol;     // per-sample final colour (SampleArgs::scol)
+    const long long* wbase;  // deterministic mode: slot base per group (SampleArgs::wbase)
+    float* partial;          // deterministic mode: kDiagRec floats per slot
 };
 
 // Scratch of the radix tile-list construction (sort.cu), sized by the runtime:

@@ -857,6 +857,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     if (W.nwin > 0) ap.issue(0, rows, lane);
     const unsigned* cols = A.cols + A.mask_off[gi];
     unsigned col_nxt = W.nwin > 0 ? cols[lane] : 0u;
+    const long long slot0 = 32 * A.wbase[gi];  // deterministic mode: first slot of the group
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = m_cur;
@@ -931,10 +932,19 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
             const float syy = my * (my * M0 - 2.0f * M12.y) + M5G2.x;
             constexpr float kLn2f = 0.69314718055994530942f;
             const float ca = -2.0f * kLn2f * blk[2][lane], cb = -kLn2f * blk[3][lane], cc = -2.0f * kLn2f * blk[4][lane];
-            float* dst = A.inter + (c.vbase + e_g) * kRec;
-            red_add_v4(dst, -(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
-            red_add_v4(dst + 4, -0.5f * syy, __fdividef(M0, blk[5][lane]), G01.x, G01.y);
-            atomicAdd(dst + 8, M5G2.y);
+            const float4 o0 = make_float4(-(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
+            const float4 o1 = make_float4(-0.5f * syy, __fdividef(M0, blk[5][lane]), G01.x, G01.y);
+            if (A.partial) {  // deterministic: this entry's own slot, summed in slot order by k_chain
+                float4* dst = reinterpret_cast<float4*>(A.partial) + 3 * (slot0 + 32 * w + lane);
+                dst[0] = o0;
+                dst[1] = o1;
+                dst[2] = make_float4(M5G2.y, 0.f, 0.f, 0.f);
+            } else {
+                float* dst = A.inter + (c.vbase + e_g) * kRec;
+                red_add_v4(dst, o0.x, o0.y, o0.z, o0.w);
+                red_add_v4(dst + 4, o1.x, o1.y, o1.z, o1.w);
+                atomicAdd(dst + 8, M5G2.y);
+            }
         }
         __syncwarp();
     }
@@ -980,6 +990,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     const int e16 = lane & 15, ph = lane >> 4;
     const unsigned pmask = ph ? 0xFFFF0000u : 0x0000FFFFu;
     const PixQ pq = pix_q(c.pxc - c.ox, c.pyc - c.oy);
+    const long long slot0 = A.partial ? 32 * A.wbase[gi] : 0;  // deterministic mode: first slot of the group
     float T = 1.0f, S0 = 0.f, S1 = 0.f, S2 = 0.f;
     Prefetch P;
     prefetch<false>(c, W, A.rec, nullptr, 0, lane, P);
@@ -1080,13 +1091,22 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
                 const float M14 = 0.5f * (cb * mxy2 + cc * m3y);
                 const float M22 = 0.25f * m4x, M23 = 0.5f * mx3y, M24 = 0.25f * mx2y2;
                 const float M33 = mx2y2, M34 = 0.5f * mxy3, M44 = 0.25f * m4y;
-                float* dst = A.diagacc + (c.vbase + s_g[warp][k]) * kDiagRec;
                 // upper-triangle order (00,01,02,03,04,11,12,13,14,22,23,24,33,34,44)
-                red_add_v4(dst, M00, M01, M02, M03);
-                red_add_v4(dst + 4, M04, M11, M12, M13);
-                red_add_v4(dst + 8, M14, M22, M23, M24);
-                red_add_v4(dst + 12, M33, M34, M44, aop);
-                red_add_v4(dst + 16, ac0, ac1, ac2, 0.f);
+                if (A.partial) {  // deterministic: own slot, summed in slot order by k_diag_finalize
+                    float4* dst = reinterpret_cast<float4*>(A.partial) + 5 * (slot0 + 32 * w + k);
+                    dst[0] = make_float4(M00, M01, M02, M03);
+                    dst[1] = make_float4(M04, M11, M12, M13);
+                    dst[2] = make_float4(M14, M22, M23, M24);
+                    dst[3] = make_float4(M33, M34, M44, aop);
+                    dst[4] = make_float4(ac0, ac1, ac2, 0.f);
+                } else {
+                    float* dst = A.diagacc + (c.vbase + s_g[warp][k]) * kDiagRec;
+                    red_add_v4(dst, M00, M01, M02, M03);
+                    red_add_v4(dst + 4, M04, M11, M12, M13);
+                    red_add_v4(dst + 8, M14, M22, M23, M24);
+                    red_add_v4(dst + 12, M33, M34, M44, aop);
+                    red_add_v4(dst + 16, ac0, ac1, ac2, 0.f);
+                }
             }
             __syncwarp();
         }
@@ -1104,13 +1124,13 @@ __global__ void __launch_bounds__(128) k_render_exact(const DevCam* __restrict__
                                                       const int* __restrict__ entries, const double* __restrict__ rec64,
                                                       const float4* __restrict__ rec, int Gp, double* __restrict__ image,
                                                       double* __restrict__ trans, int* __restrict__ contrib) {
-    const int tile = blockIdx.y;
+    const int tile = static_cast<int>(blockIdx.x >> 1);  // two 128-pixel halves per tile, tiles on x (no 65535 cap)
     if (tile >= n_tiles) return;
     const int v = tile_view[tile];
     const DevCam& cam = cams[v];
     const int lt = tile - cam.tile_base;
     const int tx = lt % cam.tiles_x, ty = lt / cam.tiles_x;
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // pixel of the 16x16 tile
+    const int idx = (blockIdx.x & 1) * blockDim.x + threadIdx.x;  // pixel of the 16x16 tile
     if (idx >= kTile * kTile) return;
     const int x = tx * kTile + idx % kTile, y = ty * kTile + idx / kTile;
     if (x >= cam.width || y >= cam.height) return;
@@ -1153,7 +1173,7 @@ void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, 
                          const int* entries, const double* rec64, const float4* rec, int Gp, double* image,
                          double* trans, int* contrib, cudaStream_t st) {
     if (n_tiles == 0) return;
-    k_render_exact<<<dim3(2, n_tiles), 128, 0, st>>>(cams, tile_view, n_tiles, tile_offsets, entries, rec64, rec, Gp,
+    k_render_exact<<<2u * static_cast<unsigned>(n_tiles), 128, 0, st>>>(cams, tile_view, n_tiles, tile_offsets, entries, rec64, rec, Gp,
                                                      image, trans, contrib);
     ++g_launches;
 }

@@ -99,6 +99,9 @@ struct Context {
     std::string last_timing_names;
     bool timing = false;
     bool prof = false;  // per-kernel CUDA events inside gn_apply_dev
+    // J^T / diag accumulation in a fixed per-plan order (DetOrder) instead of
+    // float red.global.add: bitwise run-to-run reproducible (the default)
+    bool deterministic = true;
     std::vector<std::array<cudaEvent_t, 4>> prof_events;
     StepBuffers* step = nullptr;  // persistent lm_step workspace
 
@@ -278,7 +281,12 @@ struct Batch {
     DevBuf<int> contrib, last;
     DevBuf<double> sse_tile, sse_view;
     DevBuf<float> ssim_res, ssim_dc;  // mse+ssim loss: s and ds/dcentre per pixel and channel
-    bool rendered = false, has_gt = false;
+    // FP64 replay of the reference's blend (k_render_exact): the mse+ssim loss
+    // terms and SSIM planes and the weighted-distribution CDFs read it, so they
+    // see the reference's render, not the FP32 one
+    DevBuf<double> image64, trans64, gt64, ssim_res64, ssim_dc64;
+    DevBuf<int> contrib64;
+    bool rendered = false, has_gt = false, exact_rendered = false;
     std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
     long long max_list = 0;        // longest tile list of the batch
     // radix tile-list construction scratch (sort.cu)
@@ -404,6 +412,25 @@ struct Batch {
         ctx->mark("prep:sort");
         rendered = false;
         has_gt = false;
+        exact_rendered = false;
+    }
+
+    // render_full (rasterizer.cpp:93-95) of every pixel in FP64 (k_render_exact)
+    void render_exact() {
+        if (exact_rendered) return;
+        image64.ensure(3 * std::max<long long>(n_pix, 1));
+        trans64.ensure(std::max<long long>(n_pix, 1));
+        contrib64.ensure(std::max<long long>(n_pix, 1));
+        launch_render_exact(cams.p, tile_view.p, n_tiles, tile_offsets.p, entries.p, rec64.p, rec.p, Gp, image64.p,
+                            trans64.p, contrib64.p, ctx->stream);
+        ctx->check_launch();
+        ctx->mark("render_exact");
+        exact_rendered = true;
+    }
+    // the truth images widened to f64 (after copy_gt)
+    void widen_gt() {
+        gt64.ensure(3 * std::max<long long>(n_pix, 1));
+        launch_widen(gt.p, gt64.p, 3 * n_pix, ctx->stream);
     }
 
     // Forward render of every pixel of every view (K6); gt (concatenated f32
@@ -450,6 +477,10 @@ struct Samples {
     DevBuf<int> glist, gcount, grows;
     DevBuf<long long> srow_off, wbase;
     DevBuf<float> astream, rstream;
+    // deterministic accumulation (DetOrder): slot sort scratch, order, partials
+    DevBuf<unsigned> dka, dkb, dva, dvb, dhist, dpart, perm, seg;
+    DevBuf<float> partial;
+    long long n_slots = 0;
     std::vector<int> hrows, hcount;
     std::vector<long long> hrow_off, hwbase;
     std::vector<int> order;  // group order -> plan sample index
@@ -745,18 +776,22 @@ struct Jacobian {
                                            cudaMemcpyHostToDevice, ctx->stream));
             SLM_CUDA_CHECK(cudaMemcpyAsync(draw.sbase.p, draw.hsbase.data(), sizeof(int) * draw.hsbase.size(),
                                            cudaMemcpyHostToDevice, ctx->stream));
-            launch_weighted_draw(batch->cams.p, batch->n_tiles, batch->tile_view.p, draw.sbase.p, batch->image.p,
-                                 batch->gt.p, batch->contrib.p, draw.dist, draw.spt, draw.U.p, draw.n_total,
+            batch->render_exact();  // the reference's CDFs come from its f64 render_full (sample_plan.cpp:127-165)
+            launch_weighted_draw(batch->cams.p, batch->n_tiles, batch->tile_view.p, draw.sbase.p, batch->image64.p,
+                                 batch->gt.p, batch->contrib64.p, draw.dist, draw.spt, draw.U.p, draw.n_total,
                                  draw.inv_total, samples.spix.p, samples.sw.p, ctx->stream);
             ctx->check_launch();
         }
         ctx->mark("plan:upload");
         const size_t VG = static_cast<size_t>(batch->V) * scene->Gp;
         tan.ensure(3 * VG);
-        inter.ensure(VG * kRec);
-        diagacc.ensure(VG * kDiagRec);
-        SLM_CUDA_CHECK(cudaMemsetAsync(inter.p, 0, VG * kRec * sizeof(float), ctx->stream));
-        SLM_CUDA_CHECK(cudaMemsetAsync(diagacc.p, 0, VG * kDiagRec * sizeof(float), ctx->stream));
+        det = ctx->deterministic;
+        if (!det) {  // red.global.add accumulators (k_chain / k_diag_finalize re-zero them)
+            inter.ensure(VG * kRec);
+            diagacc.ensure(VG * kDiagRec);
+            SLM_CUDA_CHECK(cudaMemsetAsync(inter.p, 0, VG * kRec * sizeof(float), ctx->stream));
+            SLM_CUDA_CHECK(cudaMemsetAsync(diagacc.p, 0, VG * kDiagRec * sizeof(float), ctx->stream));
+        }
         SLM_CUDA_CHECK(cudaMemsetAsync(tan.p, 0, 3 * VG * sizeof(float4), ctx->stream));
         // the blend masks depend on the state only: computed once per (state, plan)
         SampleArgs a = args();
@@ -802,7 +837,38 @@ struct Jacobian {
         b.cols_out = samples.cols.p;
         launch_alpha(b, ctx->stream);
         ctx->check_launch();
+        if (det) {  // the fixed summation order of this plan's J^T / diag slots
+            const long long ns = 32 * wins;
+            samples.n_slots = ns;
+            const long long nk = static_cast<long long>(batch->V) * scene->Gp;
+            const long long n1 = std::max<long long>(ns, 1);
+            samples.dka.ensure(n1);
+            samples.dkb.ensure(n1);
+            samples.dva.ensure(n1);
+            samples.dvb.ensure(n1);
+            samples.perm.ensure(n1);
+            samples.seg.ensure(nk + 1);
+            const long long hs = radix_hist_size(n1);
+            samples.dhist.ensure(hs);
+            samples.dpart.ensure(scan_scratch(hs));
+            samples.partial.ensure(static_cast<size_t>(kDiagRec) * n1);  // J^T (kRec) and diag (kDiagRec) share it
+            build_slot_order(samples.groups.p, static_cast<int>(ng), samples.gcount.p, samples.glist.p,
+                             samples.mask_off.p, samples.wbase.p, scene->Gp, batch->V, ns, samples.dka.p,
+                             samples.dkb.p, samples.dva.p, samples.dvb.p, samples.dhist.p, samples.dpart.p,
+                             samples.perm.p, samples.seg.p, ctx->stream);
+            ctx->check_launch();
+        }
         ctx->sync();  // hrow_off is read by the async copy
+    }
+
+    bool det = true;  // this plan's accumulation mode (Context::deterministic at init_device)
+    DetOrder det_order() const {
+        return det ? DetOrder{samples.perm.p, samples.seg.p, samples.partial.p} : DetOrder{nullptr, nullptr, nullptr};
+    }
+    // out = sum_v chain_v^T inter_v (+ lambda p): the J^T chain of the last J^T pass
+    void chain(const float* p, float lambda, float* out, const int* done = nullptr) {
+        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+                     det_order(), p, lambda, out, done, ctx->stream);
     }
 
     SampleArgs args() const {
@@ -822,6 +888,7 @@ struct Jacobian {
         a.last_img = batch->last.p;
         a.gt = batch->gt.p;
         a.inter = inter.p;
+        a.partial = det ? samples.partial.p : nullptr;
         a.masks = samples.masks.p;
         a.glist = samples.glist.p;
         a.gcount = samples.gcount.p;
@@ -852,13 +919,11 @@ struct Jacobian {
         launch_sample_raster(kGn, a, st);
         if (prof) ctx->prof_record(ev, 2);
         if (ctx->world > 1) {
-            launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
-                         inter.p, nullptr, 0.f, dout, done, st);
+            chain(nullptr, 0.f, dout, done);
             ctx->allreduce(dout, P());
             launch_axpy(dout, dp, static_cast<long long>(P()), lambda, st);
         } else {
-            launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
-                         inter.p, dp, lambda, dout, done, st);
+            chain(dp, lambda, dout, done);
         }
         if (prof) {
             ctx->prof_record(ev, 3);
@@ -878,16 +943,14 @@ struct Jacobian {
         SampleArgs a = args();
         a.in_res = res_in.p;
         launch_sample_raster(kVjp, a, ctx->stream);
-        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
-                     inter.p, nullptr, 0.f, dout, nullptr, ctx->stream);
+        chain(nullptr, 0.f, dout);
         ctx->check_launch();
     }
 
     // b = J^T(-W r), r = render - truth at the samples (lm.cpp:99-121)
     void rhs_dev(float* dout) {
         launch_sample_raster(kRhs, args(), ctx->stream);
-        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
-                     inter.p, nullptr, 0.f, dout, nullptr, ctx->stream);
+        chain(nullptr, 0.f, dout);
         ctx->check_launch();
     }
 
@@ -911,9 +974,11 @@ struct Jacobian {
         d.mask_off = samples.mask_off.p;
         d.cols = samples.cols.p;
         d.scol = samples.scol.p;
+        d.wbase = samples.wbase.p;
+        d.partial = det ? samples.partial.p : nullptr;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
-                             batch->rec.p, diagacc.p, dout, ctx->stream);
+                             batch->rec.p, diagacc.p, det_order(), dout, ctx->stream);
         ctx->check_launch();
     }
 
@@ -958,8 +1023,7 @@ struct Jacobian {
         SampleArgs a = args();
         a.in_res = res_in.p;
         launch_sample_raster(kVjp, a, ctx->stream);
-        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
-                     nullptr, 0.f, vout.p, nullptr, ctx->stream);
+        chain(nullptr, 0.f, vout.p);
         ctx->check_launch();
         download_param(vout.p, out);
     }
@@ -1404,15 +1468,34 @@ static std::vector<double2> image_metrics(Context* c, const T* a, const T* b, co
 // Per view {sse, sum of s^2} of the batch render vs truth
 // (metrics::ssim_diag_residuals); with planes, B.ssim_res / B.ssim_dc get s and
 // ds/dcentre per pixel and channel.
-static std::vector<double2> batch_ssim(Batch& B, bool planes) {
+// exact: of the FP64 render (k_render_exact) vs the widened truth, as the
+// reference computes them (lm.cpp:39-54,86-119 on render_full's f64 image);
+// the planes are then narrowed to f32 for the products.
+static std::vector<double2> batch_ssim(Batch& B, bool planes, bool exact = false) {
     std::vector<ImageRef> imgs;
     for (int v = 0; v < B.V; ++v) imgs.push_back({3 * B.hcams[v].pix_base, B.hcams[v].width, B.hcams[v].height});
+    const long long n3 = 3 * std::max<long long>(B.n_pix, 1);
     if (planes) {
-        B.ssim_res.ensure(3 * std::max<long long>(B.n_pix, 1));
-        B.ssim_dc.ensure(3 * std::max<long long>(B.n_pix, 1));
+        B.ssim_res.ensure(n3);
+        B.ssim_dc.ensure(n3);
     }
-    return image_metrics<float>(B.ctx, B.image.p, B.gt.p, imgs, true, planes ? B.ssim_res.p : nullptr,
-                                planes ? B.ssim_dc.p : nullptr);
+    if (!exact)
+        return image_metrics<float>(B.ctx, B.image.p, B.gt.p, imgs, true, planes ? B.ssim_res.p : nullptr,
+                                    planes ? B.ssim_dc.p : nullptr);
+    B.render_exact();
+    B.widen_gt();
+    if (planes) {
+        B.ssim_res64.ensure(n3);
+        B.ssim_dc64.ensure(n3);
+    }
+    auto out = image_metrics<double>(B.ctx, B.image64.p, B.gt64.p, imgs, true, planes ? B.ssim_res64.p : nullptr,
+                                     planes ? B.ssim_dc64.p : nullptr);
+    if (planes) {
+        launch_narrow(B.ssim_res64.p, B.ssim_res.p, 3 * B.n_pix, B.ctx->stream);
+        launch_narrow(B.ssim_dc64.p, B.ssim_dc.p, 3 * B.n_pix, B.ctx->stream);
+        B.ctx->check_launch();
+    }
+    return out;
 }
 
 constexpr int kEvalChunk = 8;  // cameras per device batch outside lm_step (bounds the batch buffers)
@@ -1433,9 +1516,12 @@ static double batch_loss_dev(Scene& s, Train& t, const std::vector<int>& ids, in
         b.prepare(s, cv);
         copy_gt(t, b, chunk);
         b.render(true);
-        const auto sse = b.view_sse();
+        auto sse = b.view_sse();
         std::vector<double2> ss;
-        if (loss == SLM_LOSS_MSE_SSIM) ss = batch_ssim(b, false);
+        if (loss == SLM_LOSS_MSE_SSIM) {  // both terms of the FP64 render, like the reference's
+            ss = batch_ssim(b, false, true);
+            for (int v = 0; v < b.V; ++v) sse[v] = ss[v].x;
+        }
         for (int v = 0; v < b.V; ++v) {
             const double n3 = 3.0 * cv[v].width * cv[v].height;
             double term = sse[v] / n3;
@@ -1478,8 +1564,7 @@ static void full_gradient_dev(Scene& s, Train& t, int loss, double ssim_weight, 
         SampleArgs a = J.args();
         a.in_res = J.res_in.p;
         launch_sample_raster(kVjp, a, ctx->stream);
-        launch_chain(s.beta32.p, s.G, s.Gp, B.cams.p, B.V, B.rec.p, J.inter.p, nullptr, 0.f, chunk.p, nullptr,
-                     ctx->stream);
+        J.chain(nullptr, 0.f, chunk.p);
         launch_axpy(grad, chunk.p, static_cast<long long>(P), 1.0f, ctx->stream);
         ctx->check_launch();
     }
@@ -1637,16 +1722,15 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     J.upload_early();  // overlaps the render still running on the main stream
     // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
     double before = 0.0;
-    {
+    if (ssim) {  // mse + ssim_weight * mean s^2 per view (lm.cpp:143-147) of the FP64 render; planes for the rhs fold
+        const auto ss = batch_ssim(B, true, true);
+        for (int v = 0; v < B.V; ++v)
+            before += (ss[v].x + cfg.ssim_weight * ss[v].y) / (3.0 * my_cams[v].width * my_cams[v].height);
+        ctx->mark("ssim");
+    } else {
         const auto sse = B.view_sse();
         for (int v = 0; v < B.V; ++v)
             before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
-    }
-    if (ssim) {  // + ssim_weight * mean s^2 per view (lm.cpp:143-147); planes for the rhs fold
-        const auto ss = batch_ssim(B, true);
-        for (int v = 0; v < B.V; ++v)
-            before += cfg.ssim_weight * ss[v].y / (3.0 * my_cams[v].width * my_cams[v].height);
-        ctx->mark("ssim");
     }
     J.init_device();
     ctx->mark("plan");
@@ -1725,13 +1809,16 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     B.render(true);
     double after = 0.0;
     {
-        const auto sse = B.view_sse();
+        auto sse = B.view_sse();
         std::vector<double2> ss;
-        if (ssim) ss = batch_ssim(B, false);
+        if (ssim) {  // both terms of the FP64 render (batch_loss, lm.cpp:44-50)
+            ss = batch_ssim(B, false, true);
+            for (int v = 0; v < B.V; ++v) sse[v] = ss[v].x;
+        }
         for (int v = 0; v < B.V; ++v) {
             const double n3 = 3.0 * my_cams[v].width * my_cams[v].height;
             double term = sse[v] / n3;
-            if (ssim) term += cfg.ssim_weight * ss[v].y / n3;  // batch_loss (lm.cpp:44-50)
+            if (ssim) term += cfg.ssim_weight * ss[v].y / n3;
             after += term;
         }
     }
@@ -1842,6 +1929,9 @@ int slm_context_set_stream(slm_context* ctx, void* stream) {
         c.stream = static_cast<cudaStream_t>(stream);
         c.own_stream = false;
     });
+}
+int slm_context_set_deterministic(slm_context* ctx, int on) {
+    return guarded([&] { ctx->impl.deterministic = on != 0; });
 }
 int slm_context_set_timing(slm_context* ctx, int on) {
     return guarded([&] { ctx->impl.timing = on != 0; });

@@ -97,9 +97,14 @@ void launch_diag_raster(const DiagArgs& a, cudaStream_t st);
 void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st);
 void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
-                  float* inter, const float* p, float lambda, float* out, const int* done, cudaStream_t st);
+                  float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
+                  cudaStream_t st);
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V,
-                          const float4* rec, float* diagacc, float* out, cudaStream_t st);
+                          const float4* rec, float* diagacc, const DetOrder& det, float* out, cudaStream_t st);
+void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
+                      const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
+                      unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
+                      unsigned* perm, unsigned* seg, cudaStream_t st);
 void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
 void launch_soa32_to_aos64(const float* soa, int G, int Gp, double* aos, cudaStream_t st);
 void launch_set_to_beta(const double* m, const double* ls, const double* rot, const double* logit,
@@ -129,7 +134,7 @@ void launch_ssim_fold(const Group* groups, int n_groups, const DevCam* cams, con
                       float* sw, const float* image, const float* gt, const float* sres, const float* sdc,
                       float ssim_weight, float* rhs, const float* scol, cudaStream_t st);
 void launch_weighted_draw(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
-                          const float* image, const float* gt, const int* contrib, int dist, int spt,
+                          const double* image, const float* gt, const int* contrib, int dist, int spt,
                           const double* U, double n_total, double inv_total, int* spix, float* sw,
                           cudaStream_t st);
 void launch_exhaustive_residual(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
@@ -138,5 +143,7 @@ void launch_exhaustive_residual(const DevCam* cams, int n_tiles, const int* tile
 void launch_first_order_step(double* beta, float* beta32, double* m1, double* m2, const float* grad32,
                              const double* grad64_aos, int G, int Gp, const FirstOrderParams& fp, cudaStream_t st);
 void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st);
+void launch_widen(const float* x, double* y, long long n, cudaStream_t st);
+void launch_narrow(const double* x, float* y, long long n, cudaStream_t st);
 
 }  // namespace slm

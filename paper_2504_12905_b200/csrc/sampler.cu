@@ -10,7 +10,9 @@
 // order (view, tile, draw) from the caller's std::mt19937_64 — one
 // generate_canonical call per draw, exactly what the reference consumes —
 // while the GPU renders; this kernel then builds the densities and CDFs from
-// the device-resident render and picks the pixels, so no image leaves HBM.
+// the device-resident FP64 render (k_render_exact: the reference's blend
+// decisions and colours, so the densities and CDFs are the reference's) and
+// picks the pixels, so no image leaves HBM.
 // One warp per tile, the tile's density and CDF in shared memory (2 KB each);
 // sums and the CDF run sequentially in pixel order like std::partial_sum.
 //
@@ -33,7 +35,7 @@ constexpr double kMinDensity = 1e-12;  // sample_plan.cpp:27
 
 __global__ void __launch_bounds__(32 * kDrawWarps)
 k_weighted_draw(const DevCam* __restrict__ cams, int n_tiles, const int* __restrict__ tile_view,
-                const int* __restrict__ tile_sbase, const float* __restrict__ image, const float* __restrict__ gt,
+                const int* __restrict__ tile_sbase, const double* __restrict__ image, const float* __restrict__ gt,
                 const int* __restrict__ contrib, int dist, int spt, const double* __restrict__ U, double n_total,
                 double inv_total, int* __restrict__ spix, float* __restrict__ sw) {
     __shared__ double s_den[kDrawWarps][kTilePix];
@@ -60,7 +62,7 @@ k_weighted_draw(const DevCam* __restrict__ cams, int n_tiles, const int* __restr
         if (dist == 1) {  // kResidual: mean |residual| over the channels
             double a = 0.0;
             for (int c = 0; c < 3; ++c)
-                a += fabs(static_cast<double>(image[3 * pix + c]) - static_cast<double>(gt[3 * pix + c]));
+                a += fabs(image[3 * pix + c] - static_cast<double>(gt[3 * pix + c]));
             d = a / 3.0;
             vmax = fmax(vmax, d);
         } else {  // kGaussianCount
@@ -109,7 +111,7 @@ k_weighted_draw(const DevCam* __restrict__ cams, int n_tiles, const int* __restr
 }  // namespace
 
 void launch_weighted_draw(const DevCam* cams, int n_tiles, const int* tile_view, const int* tile_sbase,
-                          const float* image, const float* gt, const int* contrib, int dist, int spt,
+                          const double* image, const float* gt, const int* contrib, int dist, int spt,
                           const double* U, double n_total, double inv_total, int* spix, float* sw,
                           cudaStream_t st) {
     if (n_tiles == 0) return;

@@ -532,4 +532,66 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
     k_tile_offsets<<<(n_tiles + 1 + 255) / 256, 256, 0, st>>>(tka, n_entries, n_tiles, tile_offsets); ++g_launches;
 }
 
+// ---- deterministic accumulation order (DetOrder, layout.hpp)
+// Slot keys: slot 32 * wbase[g] + j of group g holds compacted entry j; its key
+// is the (view, Gaussian) it accumulates into, the window padding sorts last.
+__global__ void __launch_bounds__(128) k_slot_keys(const Group* __restrict__ groups, int n_groups,
+                                                   const int* __restrict__ gcount, const int* __restrict__ glist,
+                                                   const long long* __restrict__ mask_off,
+                                                   const long long* __restrict__ wbase, int Gp, unsigned sentinel,
+                                                   unsigned* __restrict__ key, unsigned* __restrict__ val) {
+    const int gi = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (gi >= n_groups) return;
+    const int nun = gcount[gi];
+    const int n = 32 * ((nun + 31) >> 5);
+    const long long s0 = 32 * wbase[gi], off = mask_off[gi];
+    const unsigned vb = static_cast<unsigned>(groups[gi].view) * static_cast<unsigned>(Gp);
+    for (int j = lane; j < n; j += 32) {
+        key[s0 + j] = j < nun ? vb + static_cast<unsigned>(glist[off + j]) : sentinel;
+        val[s0 + j] = static_cast<unsigned>(s0 + j);
+    }
+}
+
+// seg[k] = first sorted slot with key >= k, k in [0, n_keys]
+__global__ void k_seg_bounds(const unsigned* __restrict__ keys, long long n, long long n_keys,
+                             unsigned* __restrict__ seg) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k > n_keys) return;
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (keys[mid] < static_cast<unsigned>(k)) lo = mid + 1;
+        else hi = mid;
+    }
+    seg[k] = static_cast<unsigned>(lo);
+}
+
+// perm (n_slots) and seg (V * Gp + 1) of a plan: stable LSD radix passes over
+// the key bits of (view * Gp + Gaussian), so equal keys keep slot order.
+void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
+                      const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
+                      unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
+                      unsigned* perm, unsigned* seg, cudaStream_t st) {
+    const long long n_keys = static_cast<long long>(V) * Gp;
+    if (n_slots == 0) {
+        cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
+        return;
+    }
+    const unsigned sentinel = static_cast<unsigned>(n_keys);
+    k_slot_keys<<<(n_groups + 3) / 4, 128, 0, st>>>(groups, n_groups, gcount, glist, mask_off, wbase, Gp, sentinel,
+                                                    ka, va);
+    ++g_launches;
+    int bits = 0;
+    while ((1ull << bits) <= sentinel) ++bits;
+    const int passes = (bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) {
+        const bool last = p == passes - 1;
+        radix_pass<unsigned>(ka, va, kb, last ? perm : vb, n_slots, 8 * p, hist, part, st);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    k_seg_bounds<<<static_cast<unsigned>((n_keys + 1 + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
+    ++g_launches;
+}
+
 }  // namespace slm

@@ -46,6 +46,7 @@ _SIGS = {
     "slm_context_synchronize": (C.c_int, [_vp]),
     "slm_context_set_stream": (C.c_int, [_vp, _vp]),
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
+    "slm_context_set_deterministic": (C.c_int, [_vp, C.c_int]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
     "slm_context_timing_names": (C.c_char_p, [_vp]),
     "slm_launch_count": (C.c_longlong, []),
@@ -324,6 +325,11 @@ class Lib(HostSampler):
 
     def set_stream(self, stream_handle: int):
         self._check(self.dll.slm_context_set_stream(self.ctx, _vp(stream_handle)))
+
+    def set_deterministic(self, on: bool):
+        """Fixed-order J^T / diag accumulation (default on): bitwise reproducible
+        products, PCG solutions and LM trajectories.  Off: float atomics."""
+        self._check(self.dll.slm_context_set_deterministic(self.ctx, 1 if on else 0))
 
     def set_timing(self, on: bool):
         self._check(self.dll.slm_context_set_timing(self.ctx, 1 if on else 0))

@@ -659,55 +659,7 @@ def test_train_run_matches_reference(gpu, tmp_path, case):
     assert GaussianSet  # noqa
 
 
-# ----------------------------------------------------------------- full-size (configs[2]) checks
-def _cfg2_inputs(views):
-    import bench
-    from paper_2504_12905_b200 import splatlm
-    args = bench.parse_args_for(1_000_000)
-    state, cams, clusters, batch, plan = bench.host_inputs(splatlm.HostSampler(), args, 1)
-    return state, [cams[i] for i in batch[:views]], bench.sub_plan(plan, 0, views)
-
-
-def test_full_size_products_vs_reference(gpu):
-    """configs[2] at full size (1M Gaussians, 1280x720, N = 32) on one of the batch
-    views: Jv, J^T u, gn_apply and diag(J^T W J) through the device vs the reference library
-    itself (oracle/_ref, all host threads; the C port where it was not built).
-    Exercises the size-dependent paths (long tile lists, alpha rows beyond the
-    staged 18, large groups) that the small fixtures do not reach."""
-    import oracle
-    from oracle.cpu_bind import port, ref
-    lib = ref() if oracle.have_ref() else port()
-    lib.set_threads(os.cpu_count() or 1)
-    state, cams, plan = _cfg2_inputs(1)
-    jr = lib.jacobian(state, cams, plan)
-    jg = gpu.jacobian(state, cams, plan)
-    r = np.random.default_rng(0)
-    p = r.uniform(-1, 1, jr.param_dim())
-    u = r.uniform(-1, 1, jr.residual_dim())
-    e_jv = norm_rel(jg.jvp(p), jr.jvp(p))
-    e_vj = norm_rel(jg.vjp(u), jr.vjp(u))
-    e_gn = norm_rel(jg.gn_apply(0.1, p), jr.gn_apply(0.1, p))
-    e_d = norm_rel(jg.jtj_diag(), jr.jtj_diag())
-    print("full-size jvp", e_jv, "vjp", e_vj, "gn_apply", e_gn, "diag", e_d)
-    assert max(e_jv, e_vj, e_gn, e_d) < TOL
-
-
-def test_full_size_batch_properties(gpu):
-    """The 8-view configs[2] product (the bench workload): adjoint identity
-    <Jv, u> = <v, J^T u>, symmetry <a, G b> = <b, G a> and linearity of
-    G = J^T W J + lambda I, through the host-vector API (FP32 raster: 1e-4)."""
-    state, cams, plan = _cfg2_inputs(8)
-    jac = gpu.jacobian(state, cams, plan)
-    r = np.random.default_rng(5)
-    v = r.uniform(-1, 1, jac.param_dim())
-    u = r.uniform(-1, 1, jac.residual_dim())
-    assert rel_error(float(np.dot(jac.jvp(v), u)), float(np.dot(v, jac.vjp(u)))) < TOL
-    a, b = r.uniform(-1, 1, jac.param_dim()), r.uniform(-1, 1, jac.param_dim())
-    ga, gb = jac.gn_apply(0.1, a), jac.gn_apply(0.1, b)
-    assert rel_error(float(np.dot(a, gb)), float(np.dot(b, ga))) < TOL
-    assert norm_rel(jac.gn_apply(0.1, a + 2.0 * b), ga + 2.0 * gb) < TOL
-
-
+# ----------------------------------------------------------------- misc
 def test_evaluate_edge_cases(gpu):
     """metrics::evaluate on identical, constant and empty images (test_metrics.cpp:88-99):
     ssim(a, a) == 1, psnr capped at 100 dB, empty images give mse 0 / ssim 1."""
