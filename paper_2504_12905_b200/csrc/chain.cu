@@ -221,61 +221,53 @@ __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta
 }
 
 // ------------------------------------------------------------------ deterministic sums
-// The (view, Gaussian)s of one warp -- view v, Gaussians g0..g0+31 -- own the
-// contiguous range [seg[vg0], seg[vg0 + 32]) of the sorted slot list, so the
-// warp walks it SPL*32 slots at a time: coalesced perm reads, then every
-// lane's SPL partials gathered at once (all loads of a chunk in flight
-// together) into shared memory, then each lane adds the slots of its own
-// segment in slot order.  The order is a function of the plan only, so every
+// A (view, Gaussian)'s partial records -- one per compacted tile-list entry
+// that carries it, written by the raster at their position in the per-plan
+// (view, Gaussian, slot) order -- are the contiguous range [seg[vg],
+// seg[vg + 1]); the thread adds them front to back (two records' loads in
+// flight per step).  The order is a function of the plan only, so every
 // product rounds identically (the reference's contract: results independent
-// of scheduling, jacobian.cpp:19-21,246-247).  The segment bounds of the next
-// view are loaded one view ahead (DetSeg), so a view costs two dependent
-// round trips (perm, partials) per chunk -- typically one chunk.
+// of scheduling, jacobian.cpp:19-21,246-247).  The bounds of the next view
+// are loaded one view ahead.
 struct DetSeg {
-    unsigned a, b;  // this lane's segment [a, b)
+    unsigned a, b;  // this thread's records [a, b)
 };
 __device__ __forceinline__ DetSeg det_seg(const DetOrder& D, size_t vg) {
     return DetSeg{__ldg(D.seg + vg), __ldg(D.seg + vg + 1)};
 }
 
-template <int NF4, int SPL>
-__device__ __forceinline__ void det_gather(const DetOrder& D, DetSeg sg, int lane, float4 (*stage)[NF4],
-                                           float4 acc[NF4]) {
-    const unsigned r0 = __shfl_sync(0xffffffffu, sg.a, 0), r1 = __shfl_sync(0xffffffffu, sg.b, 31);
+template <int STRIDE4, int NF4>  // record stride and used float4s
+__device__ __forceinline__ void det_sum(const DetOrder& D, DetSeg sg, float4 acc[NF4]) {
 #pragma unroll
     for (int q = 0; q < NF4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4* part = reinterpret_cast<const float4*>(D.partial);
-    for (unsigned base = r0; base < r1; base += 32 * SPL) {
-        unsigned sl[SPL];
+    auto add = [&](const float4* v) {
 #pragma unroll
-        for (int k = 0; k < SPL; ++k) {
-            const unsigned i = base + 32 * k + lane;
-            sl[k] = i < r1 ? __ldg(D.perm + i) : 0xffffffffu;
+        for (int q = 0; q < NF4; ++q) {
+            acc[q].x += v[q].x;
+            acc[q].y += v[q].y;
+            acc[q].z += v[q].z;
+            acc[q].w += v[q].w;
         }
-        // global -> shared without a register round trip (LDGSTS), all in flight
+    };
+    unsigned j = sg.a;
+    for (; j + 1 < sg.b; j += 2) {
+        float4 r0[NF4], r1[NF4];
+        const float4* p0 = part + static_cast<size_t>(j) * STRIDE4;
 #pragma unroll
-        for (int k = 0; k < SPL; ++k)
-            if (sl[k] != 0xffffffffu)
+        for (int q = 0; q < NF4; ++q) {
+            r0[q] = __ldcs(p0 + q);
+            r1[q] = __ldcs(p0 + STRIDE4 + q);
+        }
+        add(r0);
+        add(r1);
+    }
+    if (j < sg.b) {
+        float4 r0[NF4];
+        const float4* p0 = part + static_cast<size_t>(j) * STRIDE4;
 #pragma unroll
-                for (int q = 0; q < NF4; ++q) {
-                    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&stage[32 * k + lane][q]));
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                                 "l"(part + static_cast<size_t>(sl[k]) * NF4 + q)
-                                 : "memory");
-                }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        const unsigned a = sg.a > base ? sg.a : base, b = sg.b < base + 32 * SPL ? sg.b : base + 32 * SPL;
-        for (unsigned j = a; j < b; ++j)
-#pragma unroll
-            for (int q = 0; q < NF4; ++q) {
-                const float4 v = stage[j - base][q];
-                acc[q].x += v.x;
-                acc[q].y += v.y;
-                acc[q].z += v.z;
-                acc[q].w += v.w;
-            }
-        __syncwarp();
+        for (int q = 0; q < NF4; ++q) r0[q] = __ldcs(p0 + q);
+        add(r0);
     }
 }
 
@@ -290,16 +282,9 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
                                                const float4* __restrict__ rec, float* __restrict__ inter,
                                                DetOrder D, const float* __restrict__ p, float lambda,
                                                float* __restrict__ out, const int* __restrict__ done_flag) {
-    constexpr int SPL = 4;
-    __shared__ float4 s_stage[4][32 * SPL][3];
     if (done_flag && *done_flag) return;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    if (DET) {
-        if (g - lane >= G) return;  // whole warp past the end (the gather is warp-cooperative)
-    } else if (g >= G) {
-        return;
-    }
+    if (g >= G) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
@@ -324,11 +309,11 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
         float4 i0 = ni0, i1 = ni1, i2 = ni2;
-        if (DET) {  // warp-uniform: every lane of the warp is here
+        if (DET) {
             const DetSeg sg = sn;
             if (v + 1 < V) sn = det_seg(D, vg + Gp);
             float4 acc[3];
-            det_gather<3, SPL>(D, sg, lane, s_stage[threadIdx.x >> 5], acc);
+            det_sum<kDetRec / 4, 3>(D, sg, acc);
             i0 = acc[0];
             i1 = acc[1];
             i2 = acc[2];
@@ -420,7 +405,6 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     res[11] = gc0 * Gm.dcol[0];
     res[12] = gc1 * Gm.dcol[1];
     res[13] = gc2 * Gm.dcol[2];
-    if (g >= G) return;
     for (int k = 0; k < kP; ++k) {
         float val = res[k];
         if (p) val += lambda * p[k * Gp + g];
@@ -437,15 +421,8 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
                                                        const float4* __restrict__ rec,
                                                        float* __restrict__ diagacc, DetOrder D,
                                                        float* __restrict__ out) {
-    constexpr int SPL = 4;
-    __shared__ float4 s_stage[4][32 * SPL][5];
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    if (DET) {
-        if (g - lane >= G) return;
-    } else if (g >= G) {
-        return;
-    }
+    if (g >= G) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float d[kP];
@@ -469,10 +446,10 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
     if (DET && V > 0) sn = det_seg(D, g);
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        if (DET) {  // warp-uniform
+        if (DET) {
             const DetSeg sg = sn;
             if (v + 1 < V) sn = det_seg(D, vg + Gp);
-            det_gather<5, SPL>(D, sg, lane, s_stage[threadIdx.x >> 5], na);
+            det_sum<kDetDiagRec / 4, 5>(D, sg, na);
         }
         const float4 q0 = nr0, q1 = nr1, q2 = nr2;
         float acc[20];
@@ -530,7 +507,6 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         d[12] += acc[17] * Gm.dcol[1] * Gm.dcol[1];
         d[13] += acc[18] * Gm.dcol[2] * Gm.dcol[2];
     }
-    if (g >= G) return;
     // each row is a sum of squares (jtj_diag, jacobian.cpp:272-337); the quadratic
     // form P^T M P of rounded moment sums can dip a few ulp below zero -- clamp
     for (int k = 0; k < kP; ++k) out[k * Gp + g] = fmaxf(d[k], 0.0f);

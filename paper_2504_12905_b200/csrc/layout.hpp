@@ -96,19 +96,25 @@ struct SampleArgs {
     float* scol_out;
     // Deterministic accumulation (the default): instead of red.global.add into
     // `inter`, the J^T pass writes each compacted entry's 9-float contribution
-    // to its own slot, slot = 32 * wbase[g] + j (12 floats per slot); the chain
-    // kernel sums a (view, Gaussian)'s slots in slot order (DetOrder).
+    // (slot = 32 * wbase[g] + j) as one record at position dest[slot] of
+    // `partial`; the chain kernel sums a (view, Gaussian)'s records in order
+    // (DetOrder).
+    const unsigned* dest;
     float* partial;
 };
 
+constexpr int kDetRec = 12;      // floats per J^T partial record (9 used)
+constexpr int kDetDiagRec = 24;  // floats per diag partial record (19 used): three full sectors
+
 // Per-plan order of the deterministic accumulation (sort.cu build_slot_order):
-// perm = the slots sorted by (view * Gp + Gaussian), stable, so each
-// (view, Gaussian)'s slots are the contiguous range [seg[vg], seg[vg + 1]) in
-// slot order.  Fixed per plan -> every product sums in the same order.
+// the slots sorted by (view * Gp + Gaussian), stable (slot order within a
+// key); dest[slot] = the slot's position in that order, so the partial
+// records of (view, Gaussian) vg are the contiguous range [seg[vg], seg[vg+1])
+// and are summed front to back.  Fixed per plan -> every product rounds the
+// same way.
 struct DetOrder {
-    const unsigned* perm;
     const unsigned* seg;
-    const float* partial;  // kRec floats per slot (J^T) or kDiagRec (diag)
+    const float* partial;  // kDetRec floats per record (J^T) or kDetDiagRec (diag)
 };
 
 constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)
@@ -133,7 +139,8 @@ struct DiagArgs {
     const unsigned* cols;  // column masks (SampleArgs::cols)
     const float* scol;     // per-sample final colour (SampleArgs::scol)
     const long long* wbase;  // deterministic mode: slot base per group (SampleArgs::wbase)
-    float* partial;          // deterministic mode: kDiagRec floats per slot
+    const unsigned* dest;    // deterministic mode: record position per slot (SampleArgs::dest)
+    float* partial;          // deterministic mode: kDetDiagRec floats per record
 };
 
 // Scratch of the radix tile-list construction (sort.cu), sized by the runtime:

@@ -858,6 +858,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
     const unsigned* cols = A.cols + A.mask_off[gi];
     unsigned col_nxt = W.nwin > 0 ? cols[lane] : 0u;
     const long long slot0 = 32 * A.wbase[gi];  // deterministic mode: first slot of the group
+    unsigned dest_nxt = (A.partial && W.nwin > 0 && lane < W.nun) ? A.dest[slot0 + lane] : 0u;
     __syncwarp();
     for (int w = 0; w < W.nwin; ++w) {
         const unsigned m0 = m_cur;
@@ -871,6 +872,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
         win_index(c, W, w + 2, lane, m_nxt, g_nxt);
         const unsigned col = col_nxt;  // lane k: pixels that blend entry k
         if (w + 1 < W.nwin) col_nxt = cols[32 * (w + 1) + lane];
+        const unsigned dest_w = dest_nxt;  // deterministic mode: this entry's record position
+        if (A.partial && w + 1 < W.nwin && (w + 1) * 32 + lane < W.nun) dest_nxt = A.dest[slot0 + 32 * (w + 1) + lane];
         const float* sp = ap.wait(w) + lane;
         const float(*blk)[32] = reinterpret_cast<const float(*)[32]>(ap.block(w));
         // phase A (lane = pixel); with u.S_incl kept as one running scalar:
@@ -934,11 +937,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs 
             const float ca = -2.0f * kLn2f * blk[2][lane], cb = -kLn2f * blk[3][lane], cc = -2.0f * kLn2f * blk[4][lane];
             const float4 o0 = make_float4(-(ca * sx + cb * sy), -(cb * sx + cc * sy), -0.5f * sxx, -sxy);
             const float4 o1 = make_float4(-0.5f * syy, __fdividef(M0, blk[5][lane]), G01.x, G01.y);
-            if (A.partial) {  // deterministic: this entry's own slot, summed in slot order by k_chain
-                float4* dst = reinterpret_cast<float4*>(A.partial) + 3 * (slot0 + 32 * w + lane);
+            if (A.partial) {  // deterministic: this entry's own record, summed in order by k_chain
+                float4* dst = reinterpret_cast<float4*>(A.partial) + (kDetRec / 4) * static_cast<size_t>(dest_w);
                 dst[0] = o0;
                 dst[1] = o1;
                 dst[2] = make_float4(M5G2.y, 0.f, 0.f, 0.f);
+                if (kDetRec == 16) dst[3] = make_float4(0.f, 0.f, 0.f, 0.f);  // full sectors
             } else {
                 float* dst = A.inter + (c.vbase + e_g) * kRec;
                 red_add_v4(dst, o0.x, o0.y, o0.z, o0.w);
@@ -1092,13 +1096,15 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
                 const float M22 = 0.25f * m4x, M23 = 0.5f * mx3y, M24 = 0.25f * mx2y2;
                 const float M33 = mx2y2, M34 = 0.5f * mxy3, M44 = 0.25f * m4y;
                 // upper-triangle order (00,01,02,03,04,11,12,13,14,22,23,24,33,34,44)
-                if (A.partial) {  // deterministic: own slot, summed in slot order by k_diag_finalize
-                    float4* dst = reinterpret_cast<float4*>(A.partial) + 5 * (slot0 + 32 * w + k);
+                if (A.partial) {  // deterministic: own record, summed in order by k_diag_finalize
+                    float4* dst = reinterpret_cast<float4*>(A.partial) +
+                                  (kDetDiagRec / 4) * static_cast<size_t>(A.dest[slot0 + 32 * w + k]);
                     dst[0] = make_float4(M00, M01, M02, M03);
                     dst[1] = make_float4(M04, M11, M12, M13);
                     dst[2] = make_float4(M14, M22, M23, M24);
                     dst[3] = make_float4(M33, M34, M44, aop);
                     dst[4] = make_float4(ac0, ac1, ac2, 0.f);
+                    dst[5] = make_float4(0.f, 0.f, 0.f, 0.f);  // full sectors
                 } else {
                     float* dst = A.diagacc + (c.vbase + s_g[warp][k]) * kDiagRec;
                     red_add_v4(dst, M00, M01, M02, M03);

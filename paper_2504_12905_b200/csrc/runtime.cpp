@@ -478,7 +478,7 @@ struct Samples {
     DevBuf<long long> srow_off, wbase;
     DevBuf<float> astream, rstream;
     // deterministic accumulation (DetOrder): slot sort scratch, order, partials
-    DevBuf<unsigned> dka, dkb, dva, dvb, dhist, dpart, perm, seg;
+    DevBuf<unsigned> dka, dkb, dva, dvb, dhist, dpart, perm, seg, dest;
     DevBuf<float> partial;
     long long n_slots = 0;
     std::vector<int> hrows, hcount;
@@ -847,15 +847,16 @@ struct Jacobian {
             samples.dva.ensure(n1);
             samples.dvb.ensure(n1);
             samples.perm.ensure(n1);
+            samples.dest.ensure(n1);
             samples.seg.ensure(nk + 1);
             const long long hs = radix_hist_size(n1);
             samples.dhist.ensure(hs);
             samples.dpart.ensure(scan_scratch(hs));
-            samples.partial.ensure(static_cast<size_t>(kDiagRec) * n1);  // J^T (kRec) and diag (kDiagRec) share it
+            samples.partial.ensure(static_cast<size_t>(kDetDiagRec) * n1);  // J^T and diag records share it
             build_slot_order(samples.groups.p, static_cast<int>(ng), samples.gcount.p, samples.glist.p,
                              samples.mask_off.p, samples.wbase.p, scene->Gp, batch->V, ns, samples.dka.p,
                              samples.dkb.p, samples.dva.p, samples.dvb.p, samples.dhist.p, samples.dpart.p,
-                             samples.perm.p, samples.seg.p, ctx->stream);
+                             samples.perm.p, samples.seg.p, samples.dest.p, ctx->stream);
             ctx->check_launch();
         }
         ctx->sync();  // hrow_off is read by the async copy
@@ -863,7 +864,7 @@ struct Jacobian {
 
     bool det = true;  // this plan's accumulation mode (Context::deterministic at init_device)
     DetOrder det_order() const {
-        return det ? DetOrder{samples.perm.p, samples.seg.p, samples.partial.p} : DetOrder{nullptr, nullptr, nullptr};
+        return det ? DetOrder{samples.seg.p, samples.partial.p} : DetOrder{nullptr, nullptr};
     }
     // out = sum_v chain_v^T inter_v (+ lambda p): the J^T chain of the last J^T pass
     void chain(const float* p, float lambda, float* out, const int* done = nullptr) {
@@ -889,6 +890,7 @@ struct Jacobian {
         a.gt = batch->gt.p;
         a.inter = inter.p;
         a.partial = det ? samples.partial.p : nullptr;
+        a.dest = samples.dest.p;
         a.masks = samples.masks.p;
         a.glist = samples.glist.p;
         a.gcount = samples.gcount.p;
@@ -976,6 +978,7 @@ struct Jacobian {
         d.scol = samples.scol.p;
         d.wbase = samples.wbase.p;
         d.partial = det ? samples.partial.p : nullptr;
+        d.dest = samples.dest.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
                              batch->rec.p, diagacc.p, det_order(), dout, ctx->stream);

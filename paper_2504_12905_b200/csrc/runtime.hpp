@@ -104,7 +104,7 @@ void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams
 void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
                       const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
                       unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
-                      unsigned* perm, unsigned* seg, cudaStream_t st);
+                      unsigned* perm, unsigned* seg, unsigned* dest, cudaStream_t st);
 void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
 void launch_soa32_to_aos64(const float* soa, int G, int Gp, double* aos, cudaStream_t st);
 void launch_set_to_beta(const double* m, const double* ls, const double* rot, const double* logit,

@@ -566,12 +566,18 @@ __global__ void k_seg_bounds(const unsigned* __restrict__ keys, long long n, lon
     seg[k] = static_cast<unsigned>(lo);
 }
 
-// perm (n_slots) and seg (V * Gp + 1) of a plan: stable LSD radix passes over
-// the key bits of (view * Gp + Gaussian), so equal keys keep slot order.
+__global__ void k_invert_perm(const unsigned* __restrict__ perm, long long n, unsigned* __restrict__ dest) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dest[perm[i]] = static_cast<unsigned>(i);
+}
+
+// dest (n_slots) and seg (V * Gp + 1) of a plan: stable LSD radix passes over
+// the key bits of (view * Gp + Gaussian), so equal keys keep slot order; dest
+// inverts the sorted slot list.
 void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
                       const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
                       unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
-                      unsigned* perm, unsigned* seg, cudaStream_t st) {
+                      unsigned* perm, unsigned* seg, unsigned* dest, cudaStream_t st) {
     const long long n_keys = static_cast<long long>(V) * Gp;
     if (n_slots == 0) {
         cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
@@ -591,6 +597,8 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
         std::swap(va, vb);
     }
     k_seg_bounds<<<static_cast<unsigned>((n_keys + 1 + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
+    ++g_launches;
+    k_invert_perm<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(perm, n_slots, dest);
     ++g_launches;
 }
 
