@@ -31,7 +31,6 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2504_12905_b200.types import GaussianSet, LmConfig, SamplePlan, ring_camera  # noqa: E402
 
 METRIC = "JTWJp matvecs/s (8-view LM batch, 1M Gaussians)"
 UNIT = "matvec/s"
@@ -54,7 +53,6 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-psnr", action="store_true", help="skip the configs[0] time-to-PSNR run")
-    ap.add_argument("--cpu-views", type=int, default=1, help="views in the CPU baseline sample")
     ap.add_argument("--accumulate", default="ordered", choices=["ordered", "atomic"],
                     help="J^T / diag accumulation: fixed per-plan order (bitwise reproducible, default) "
                          "or float red.global.add")
@@ -72,6 +70,32 @@ def parse_args_for(gaussians: int):
 
 
 T0 = time.perf_counter()
+DATA_TEXT = "synthetic (random_init state, ring cameras; BASELINE configs[2] shape)"
+CFG0_TEXT = ("configs[0]: toy scene 5000 GT / 10k random_init Gaussians, 8 train + 4 test views 256x256, "
+             "full pixels (N=256), PCG 8, 10 LM iterations")
+
+
+def workload_config(args) -> dict:
+    """The workload both arms run (identical dict for --impl b200 and reference)."""
+    return {"workload": "configs[2]: 1M Gaussians (SH-0), 200 views 1280x720, 8-view LM batch per rank, "
+                        "N=32 samples/tile, lambda=0.1",
+            "gaussians": args.gaussians, "views": args.views, "width": args.width, "height": args.height,
+            "batch_views_per_rank": args.batch, "samples_per_tile": args.spt,
+            "l2": "working set > 126 MB L2 (no flush needed)"}
+
+
+def lm_step_bytes(st: dict) -> int:
+    """SURVEY 8(d) algorithmic bytes of one lm_step from its own counters
+    (Lib.step_stats): k * B_matvec + B_diag + B_rhs + two full-image renders, with
+    B_matvec = 4 (88 G + 19 E + 4 S), B_diag = 4 (68 G + 64 E + 4 S),
+    B_rhs = 4 (51 G + 10 E + 4 S) (B_matvec without the Jv half) and a render
+    4 (10 E + 8 W H)."""
+    G, E, S, k, pix = st["valid"], st["entries"], st["samples"], st["pcg_iterations"], st["pixels"]
+    matvec = 4 * (88 * G + 19 * E + 4 * S)
+    diag = 4 * (68 * G + 64 * E + 4 * S)
+    rhs = 4 * (51 * G + 10 * E + 4 * S)
+    renders = 4 * (10 * E + 8 * pix) + 4 * (10 * st["entries_after"] + 8 * pix)
+    return k * matvec + diag + rhs + renders
 
 
 def log(msg: str) -> None:
@@ -83,8 +107,14 @@ def dist_env():
 
 
 def cameras(args):
+    from paper_2504_12905_b200.types import ring_camera
     return [ring_camera(2.0 * math.pi * i / args.views, 3.2, 1.1, args.width, args.height)
             for i in range(args.views)]
+
+
+def LmConfig(**kw):
+    from paper_2504_12905_b200.types import LmConfig as _L
+    return _L(**kw)
 
 
 def host_inputs(H, args, world):
@@ -99,28 +129,26 @@ def host_inputs(H, args, world):
     return state, cams, clusters, batch, plan
 
 
-def sub_plan(plan: SamplePlan, lo: int, hi: int) -> SamplePlan:
+def sub_plan(plan, lo: int, hi: int):
+    from paper_2504_12905_b200.types import SamplePlan
     a, b = int(plan.view_offset[lo]), int(plan.view_offset[hi])
     return SamplePlan(np.arange(hi - lo, dtype=np.int32), plan.view_offset[lo:hi + 1] - a,
                       plan.px[a:b], plan.py[a:b], plan.tile[a:b], plan.weight[a:b], plan.samples_per_tile)
 
 
-def gt_scene(count: int, seed: int = 20214) -> GaussianSet:
-    """Ground-truth scene with generate_toy_scene's distributions (scene_gen.cpp:47-66),
-    scales shrunk by (20/count)^(1/3) so the scene keeps the toy scene's density
-    (20 Gaussians): the toy scales at 500k Gaussians would cover every pixel with
-    ~10^4 splats, which is not a scene anyone fits."""
-    r = np.random.default_rng(seed)
-    g = GaussianSet(count)
-    s = (20.0 / count) ** (1.0 / 3.0)
-    g.means = r.uniform(-0.8, 0.8, 3 * count)
-    g.log_scales = r.uniform(math.log(0.12 * s), math.log(0.35 * s), 3 * count)
-    g.colors = r.uniform(-1.2, 1.2, 3 * count)
-    q = r.uniform(-1, 1, (count, 4))
-    q /= np.linalg.norm(q, axis=1, keepdims=True)
-    g.rotations = q.reshape(-1).copy()
-    o = r.uniform(0.4, 0.9, count)
-    g.opacity_logits = np.log(o / (1 - o))
+def gt_scene(count: int, seed: int = 20214, H=None):
+    """Ground truth of the LM-step workload: io::generate_toy_scene's Gaussians
+    (scene_gen.cpp:38-71, mt19937_64(seed), bit-exact) with the log-scales shifted
+    by log(20/count)/3, i.e. scales x (20/count)^(1/3), so the scene keeps the toy
+    scene's density (20 Gaussians) -- the toy scales at 500k Gaussians would cover
+    every pixel with ~10^4 splats.  oracle/ref_bench.cpp builds the identical set
+    with the reference's own generator for the CPU arm."""
+    if H is None:
+        from paper_2504_12905_b200 import splatlm
+        H = splatlm.HostSampler()
+    g = H.toy_gaussians(count, seed)
+    shift = math.log(20.0 / count) / 3.0
+    g.log_scales = g.log_scales + shift
     return g
 
 
@@ -204,38 +232,66 @@ def algorithmic_bytes(stats: dict) -> dict:
 
 
 # ---------------------------------------------------------------------------- CPU
-def cpu_sample(args, views: int, steps: int, warmup: int):
-    """Reference SampledJacobian::gn_apply (oracle/_ref, else the C port) on the
-    same state/cameras/plan restricted to `views` of the batch, all host threads.
-    Returns (matvecs/s scaled to the 8-view batch, per-step seconds, meta)."""
-    import oracle
-    from oracle.cpu_bind import port, ref
-    lib = ref() if oracle.have_ref() else port()
-    cores = os.cpu_count() or 1
-    lib.set_threads(cores)
-    # Inputs come from the library's host sampler, which replays the reference's
-    # RNG stream bit for bit (tests/test_abi.py); the timed call is the reference's.
-    from paper_2504_12905_b200 import splatlm
-    state, cams, clusters, batch, plan = host_inputs(splatlm.HostSampler(), args, 1)
-    sp = sub_plan(plan, 0, views)
-    t0 = time.perf_counter()
-    jac = lib.jacobian(state, [cams[i] for i in batch[:views]], sp)
-    ctor = time.perf_counter() - t0
-    p = np.random.default_rng(0).uniform(-1, 1, jac.param_dim())
-    for _ in range(warmup):
-        jac.gn_apply(0.1, p)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        jac.gn_apply(0.1, p)
-        times.append(time.perf_counter() - t0)
-    per_view = float(np.mean(times)) / views
-    value = 1.0 / (per_view * args.batch)
-    meta = {"kind": lib.kind, "cores": cores, "ctor_s": round(ctor, 2),
-            "sample": f"gn_apply over {views} of the {args.batch} batch views "
-                      f"({args.width}x{args.height}, N={args.spt}), {len(times)} timed after {warmup} warm-up, "
-                      f"per-view time scaled x{args.batch} to the 8-view matvec"}
-    return value, times, meta
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+
+
+def ref_bench(args, steps: int, warmup: int, lm_steps: int, psnr: bool, timeout: float = 1700.0) -> dict:
+    """The UNMODIFIED reference timed on this host (oracle/ref_bench.cpp linked to the
+    reference objects only): its own random_init / ring cameras / k-means batch /
+    build_sample_plan draw the workload, SampledJacobian::gn_apply is timed over
+    the whole view batch, solver::lm_step at the same shape, and the configs[0]
+    toy run for time-to-PSNR.  All host threads.  Nothing of libslm_b200 is loaded."""
+    import subprocess
+    if not os.path.exists(REF_BENCH):
+        raise FileNotFoundError(f"{REF_BENCH} not built (make -C oracle refbench, needs /root/reference)")
+    cmd = [REF_BENCH, "--gaussians", args.gaussians, "--views", args.views, "--width", args.width,
+           "--height", args.height, "--batch", args.batch, "--spt", args.spt, "--steps", steps,
+           "--warmup", warmup, "--lm-steps", lm_steps, "--psnr", int(psnr)]
+    out = subprocess.run([str(c) for c in cmd], capture_output=True, text=True, timeout=timeout, check=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def ref_time_to_psnr(r: dict):
+    """configs[0] time-to-PSNR of the reference run inside ref_bench (same target as the
+    GPU arm: the reference's own final test PSNR after 10 iterations - 0.05 dB)."""
+    if not r.get("psnr_curve_db"):
+        return None
+    target = json.load(open(PSNR_TARGET))["psnr"][-1] - 0.05
+    t, reached = 0.0, None
+    for p, w in zip(r["psnr_curve_db"], r["psnr_wall_s"]):
+        t += w
+        if reached is None and p >= target:
+            reached = t
+    return {"config": CFG0_TEXT, "target_db": round(target, 4), "time_to_psnr_s": reached,
+            "iterations": len(r["psnr_curve_db"]), "psnr_curve_db": [round(x, 4) for x in r["psnr_curve_db"]],
+            "wall_per_iteration_s": r["psnr_wall_s"]}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    r = ref_bench(args, args.steps, args.warmup, 1 if args.lm_steps > 0 else 0, not args.no_psnr)
+    value = 1.0 / r["gn_apply_mean_s"]
+    lm = None
+    if r["lm_step_s"]:
+        lm = {"lm_iters_per_s": 1.0 / float(np.mean(r["lm_step_s"])), "ms_per_lm_step": 1000 * float(np.mean(r["lm_step_s"])),
+              "pcg_iters": 8, "steps_timed": len(r["lm_step_s"])}
+    sample = (f"SampledJacobian::gn_apply over the whole {args.batch}-view batch ({args.width}x{args.height}, "
+              f"N={args.spt}, {args.gaussians} Gaussians): {args.steps} timed after {args.warmup} warm-up, "
+              f"median {r['gn_apply_median_s']:.3f} s; inputs drawn by the reference itself")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * r["gn_apply_mean_s"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA_TEXT,
+            "impl": "reference", "config": workload_config(args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["threads"], "kind": "reference",
+                             "sample": sample, "cpu_model": r["cpu_model"], "nproc": r["nproc"],
+                             "smt_active": r["smt_active"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "lm": lm, "time_to_psnr": ref_time_to_psnr(r),
+            "reference": {"batch": r["batch"], "samples": r["samples"], "ctor_s": r["ctor_s"],
+                          "gn_apply_s": r["gn_apply_s"], "lm_gt_render_s": r["lm_gt_render_s"], "total_s": r["total_s"]}}
+    print(json.dumps(line), flush=True)
 
 
 PSNR_TARGET = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "psnr_cfg0.json")
@@ -277,7 +333,7 @@ def time_to_psnr(L, stream):
                    batch_size_late=c["batch"], samples_per_tile=c["spt"])
     target = ref["psnr"][-1] - 0.05
     sd = L.train_data(test, simgs)
-    elapsed, reached, curve, ssim_curve = 0.0, None, [], []
+    elapsed, reached, curve, ssim_curve, nbytes, bytes_at = 0.0, None, [], [], 0, None
     with torch.cuda.stream(stream):
         for it in range(len(ref["psnr"])):
             torch.cuda.synchronize()
@@ -285,39 +341,24 @@ def time_to_psnr(L, stream):
             scene.lm_step(td, cfg, it, rng)
             torch.cuda.synchronize()
             elapsed += time.perf_counter() - t0
+            nbytes += lm_step_bytes(L.step_stats())
             ev = scene.evaluate_split(sd)  # io::evaluate_split on the device
             curve.append(ev.psnr)
             ssim_curve.append(ev.ssim)
             if reached is None and curve[-1] >= target:
-                reached = elapsed
-    ref_t = float(np.cumsum(ref["wall_s"])[-1])
-    return {"config": "configs[0]: toy scene 5000 GT / 10k random_init Gaussians, 8 train + 4 test views "
-                      "256x256, full pixels (N=256), PCG 8, 10 LM iterations",
+                reached, bytes_at = elapsed, nbytes
+    peak, _ = measured_peaks()
+    roof = None
+    if reached:  # algorithmic bytes of the steps until the target / the time they took
+        ach = bytes_at / reached / 1e9
+        roof = {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "bytes": bytes_at,
+                "roofline_time_s": bytes_at / (peak * 1e9)}
+    return {"config": CFG0_TEXT,
             "target_db": round(target, 4), "time_to_psnr_s": reached, "iterations": len(curve),
             "psnr_curve_db": [round(x, 4) for x in curve],
             "ssim_curve": [round(x, 5) for x in ssim_curve],
             "max_abs_psnr_diff_vs_reference_db": round(max(abs(a - b) for a, b in zip(curve, ref["psnr"])), 5),
-            "reference_time_s": round(ref_t, 1), "reference_threads": ref.get("threads"),
-            "reference_note": "wall time of the reference CPU run (oracle/_ref) that produced the target, "
-                              "measured where tests/golden/make_psnr_target.py ran"}
-
-
-def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    value, times, meta = cpu_sample(args, args.cpu_views, args.steps, args.warmup)
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "configs[2]: 1M Gaussians, 1280x720, 8-view LM batch, N=32",
-                       "gaussians": args.gaussians, "views": args.views, "width": args.width,
-                       "height": args.height, "batch_views": args.batch, "samples_per_tile": args.spt},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": meta["cores"], "kind": meta["kind"],
-                             "sample": meta["sample"]},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+            "roofline": roof}
 
 
 # ---------------------------------------------------------------------------- B200
@@ -432,7 +473,7 @@ def run_b200(args):
     # LM iterations/s on the device-resident scene (lm_step, lm.cpp:56-157)
     lm = None
     if args.lm_steps > 0:
-        gt = splatlm.Scene(L, gt_scene(args.gaussians // 2))
+        gt = splatlm.Scene(L, gt_scene(args.gaussians // 2, H=L))
         imgs = [gt.render(c)[0] for c in cams]
         del gt
         log("ground truth rendered")
@@ -455,7 +496,10 @@ def run_b200(args):
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            reps = [lm_scene.lm_step(td, cfg, 2 + i, rng) for i in range(args.lm_steps)]
+            reps, lm_bytes = [], 0
+            for i in range(args.lm_steps):
+                reps.append(lm_scene.lm_step(td, cfg, 2 + i, rng))
+                lm_bytes += lm_step_bytes(L.step_stats())
             e1.record(stream)
         torch.cuda.synchronize()
         lm_ms = e0.elapsed_time(e1) / args.lm_steps
@@ -464,8 +508,14 @@ def run_b200(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             lm_ms = float(t.item())
         log(f"lm_step: {lm_ms:.1f} ms/step, stages {L.timings()}")
+        peak, _ = measured_peaks()
+        step_bytes = lm_bytes / args.lm_steps  # this rank's views
+        ach = step_bytes / (lm_ms / 1000.0) / 1e9
         lm = {"lm_iters_per_s": 1000.0 / lm_ms, "ms_per_lm_step": lm_ms, "pcg_iters": 8,
-              "loss_before_first": rep.loss_before, "loss_after_last": reps[-1].loss_after}
+              "loss_before_first": rep.loss_before, "loss_after_last": reps[-1].loss_after,
+              "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                           "bytes_per_step": step_bytes, "roofline_lm_iters_per_s": peak * 1e9 / step_bytes,
+                           "formula": "k*B_matvec + B_diag + B_rhs + 2 renders (SURVEY 8d), counted per step"}}
 
     ttp = None
     if not args.no_psnr and os.path.exists(PSNR_TARGET):
@@ -478,11 +528,14 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            log("cpu baseline")
-            cval, ctimes, meta = cpu_sample(args, args.cpu_views, 2, 1)
-            log(f"cpu baseline: {cval:.4f} matvec/s ({meta['kind']}, {meta['cores']} cores)")
-            cpu = {"value": cval, "unit": UNIT, "cores": meta["cores"], "kind": meta["kind"],
-                   "sample": meta["sample"]}
+            log("cpu baseline (oracle/_ref/ref_bench)")
+            r = ref_bench(args, 2, 1, 0, False, timeout=600)
+            cval = 1.0 / r["gn_apply_mean_s"]
+            log(f"cpu baseline: {cval:.4f} matvec/s (reference, {r['threads']} threads)")
+            cpu = {"value": cval, "unit": UNIT, "cores": r["threads"], "kind": "reference",
+                   "sample": f"SampledJacobian::gn_apply over the whole {args.batch}-view batch, 2 timed after "
+                             f"1 warm-up ({r['gn_apply_s']} s), inputs drawn by the reference itself",
+                   "cpu_model": r["cpu_model"], "nproc": r["nproc"], "smt_active": r["smt_active"]}
         except Exception as e:  # the checker is optional on a box without the build
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": f"{type(e).__name__}: {e}"}
@@ -491,14 +544,10 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 (raster, linearisation, CG vectors; f64 projection, blend decisions and parameters)",
-        "data": "synthetic (random_init state, ring cameras; BASELINE configs[2] shape)",
-        "config": {"workload": "configs[2]: 1M Gaussians (SH-0), 200 views 1280x720, 8-view LM batch per rank, "
-                               "N=32 samples/tile, lambda=0.1",
-                   "gaussians": args.gaussians, "views": args.views, "width": args.width,
-                   "height": args.height, "batch_views_per_rank": args.batch, "samples_per_tile": args.spt,
-                   "parallelism": f"view-sharded x{world}, NCCL allreduce per product" if world > 1 else "1 GPU",
-                   "l2": "working set > 126 MB L2 (no flush needed)",
-                   "accumulation": args.accumulate},
+        "data": DATA_TEXT,
+        "config": workload_config(args),
+        "parallelism": f"view-sharded x{world}, NCCL allreduce per product" if world > 1 else "1 GPU",
+        "accumulation": args.accumulate,
         "roofline": {"bound": "hbm", "kernel": "k_sample_raster<GN> (fused Jv -> W -> J^T)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("k_sample_raster<2>"), "algorithmic_bytes_per_launch": bytes_["raster"],

@@ -59,6 +59,9 @@ int slm_context_rank(slm_context* ctx, int* rank, int* world);
  * test_solver.cpp:268-286).  off: float red.global.add (order follows the
  * scheduler).  Takes effect at the next plan (Jacobian / lm_step). */
 int slm_context_set_deterministic(slm_context* ctx, int on);
+/* Counters of this context's last lm_step: [views, sum_v G_v, tile-list entries,
+ * samples, pixels, PCG iterations, sum_v G_v and entries after the update]. */
+int slm_context_step_stats(slm_context* ctx, int64_t out[8]);
 /* Per-stage CUDA-event timings of the last lm_step / gn_apply (ms). */
 int slm_context_timings(slm_context* ctx, double* out, int capacity, int* n);
 

@@ -104,6 +104,10 @@ struct Context {
     bool deterministic = true;
     std::vector<std::array<cudaEvent_t, 4>> prof_events;
     StepBuffers* step = nullptr;  // persistent lm_step workspace
+    // counters of the last lm_step (for the bench's per-step algorithmic bytes):
+    // [views, sum G_v, tile-list entries, samples, pixels, PCG iterations,
+    //  sum G_v after the update, entries after the update]
+    long long step_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
     explicit Context(int dev) : device(dev) {
         SLM_CUDA_CHECK(cudaSetDevice(dev));
@@ -1797,6 +1801,12 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     rep.pcg_iterations = cs.iterations;
     rep.breakdown = cs.breakdown;
     ctx->mark("pcg");
+    ctx->step_stats[0] = B.V;
+    ctx->step_stats[1] = std::accumulate(B.valid_count.begin(), B.valid_count.end(), 0ll);
+    ctx->step_stats[2] = B.n_entries;
+    ctx->step_stats[3] = J.samples.total;
+    ctx->step_stats[4] = B.n_pix;
+    ctx->step_stats[5] = cs.iterations;
     // 8./9./10. learning rate and update (lm.cpp:135-137)
     launch_color_maxabs(sb.x.p, s.G, s.Gp, sb.maxabs.p, ctx->stream);
     float m = 0.f;
@@ -1810,6 +1820,8 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     // loss_after = batch_loss of the updated state (lm.cpp:149-153)
     B.prepare(s, my_cams);
     B.render(true);
+    ctx->step_stats[6] = std::accumulate(B.valid_count.begin(), B.valid_count.end(), 0ll);
+    ctx->step_stats[7] = B.n_entries;
     double after = 0.0;
     {
         auto sse = B.view_sse();
@@ -1931,6 +1943,11 @@ int slm_context_set_stream(slm_context* ctx, void* stream) {
         if (c.stream && c.own_stream) cudaStreamDestroy(c.stream);
         c.stream = static_cast<cudaStream_t>(stream);
         c.own_stream = false;
+    });
+}
+int slm_context_step_stats(slm_context* ctx, int64_t out[8]) {
+    return guarded([&] {
+        for (int i = 0; i < 8; ++i) out[i] = ctx->impl.step_stats[i];
     });
 }
 int slm_context_set_deterministic(slm_context* ctx, int on) {

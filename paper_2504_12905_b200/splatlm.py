@@ -47,6 +47,7 @@ _SIGS = {
     "slm_context_set_stream": (C.c_int, [_vp, _vp]),
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
     "slm_context_set_deterministic": (C.c_int, [_vp, C.c_int]),
+    "slm_context_step_stats": (C.c_int, [_vp, _i64p]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
     "slm_context_timing_names": (C.c_char_p, [_vp]),
     "slm_launch_count": (C.c_longlong, []),
@@ -330,6 +331,15 @@ class Lib(HostSampler):
         """Fixed-order J^T / diag accumulation (default on): bitwise reproducible
         products, PCG solutions and LM trajectories.  Off: float atomics."""
         self._check(self.dll.slm_context_set_deterministic(self.ctx, 1 if on else 0))
+
+    def step_stats(self) -> dict:
+        """Counters of the last lm_step on this context (views, sum G_v, entries,
+        samples, pixels, PCG iterations; G_v / entries after the update)."""
+        out = np.zeros(8, np.int64)
+        self._check(self.dll.slm_context_step_stats(self.ctx, i64ptr(out)))
+        return dict(views=int(out[0]), valid=int(out[1]), entries=int(out[2]), samples=int(out[3]),
+                    pixels=int(out[4]), pcg_iterations=int(out[5]), valid_after=int(out[6]),
+                    entries_after=int(out[7]))
 
     def set_timing(self, on: bool):
         self._check(self.dll.slm_context_set_timing(self.ctx, 1 if on else 0))
