@@ -271,12 +271,82 @@ __device__ __forceinline__ void det_sum(const DetOrder& D, DetSeg sg, float4 acc
     }
 }
 
+// Deterministic segmented reduction, parallel over records: one warp per 32
+// consecutive keys (view, Gaussian) -- their records are the contiguous range
+// [seg[k0], seg[k0 + 32]) -- walked in chunks of 32 records (one per lane,
+// coalesced).  Within a chunk a Hillis-Steele segmented inclusive scan (heads
+// = the keys' first records, fixed shuffle pattern) gives each key's chunk
+// partial at its last record; the key's lane adds the chunk partials in chunk
+// order.  Every addition is fixed by the plan, so the sums are bitwise
+// reproducible.  Writes all keys (zero for empty segments) with OSTRIDE4
+// float4 per key (the inter / diagacc layouts).
+template <int NF4, int STRIDE4, int OSTRIDE4>
+__global__ void __launch_bounds__(256) k_det_reduce(const unsigned* __restrict__ seg, const float4* __restrict__ part,
+                                                    long long n_keys, float4* __restrict__ out) {
+    const long long k0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ll;
+    const int lane = threadIdx.x & 31;
+    if (k0 >= n_keys) return;
+    const long long k = k0 + lane;
+    const bool live = k < n_keys;
+    const unsigned a = live ? __ldg(seg + k) : __ldg(seg + n_keys), b = live ? __ldg(seg + k + 1) : __ldg(seg + n_keys);
+    const unsigned r0 = __shfl_sync(0xffffffffu, a, 0), r1 = __shfl_sync(0xffffffffu, b, 31);
+    float4 acc[NF4];
+#pragma unroll
+    for (int q = 0; q < NF4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (unsigned base = r0; base < r1; base += 32) {
+        const unsigned i = base + lane;
+        float4 v[NF4];
+#pragma unroll
+        for (int q = 0; q < NF4; ++q)
+            v[q] = i < r1 ? __ldcs(part + static_cast<size_t>(i) * STRIDE4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool starts = a < b && a >= base && a < base + 32;
+        const unsigned heads = __reduce_or_sync(0xffffffffu, starts ? 1u << (a - base) : 0u) | 1u;
+        const int h = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));  // this record's segment head
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int q = 0; q < NF4; ++q) {
+                const float x = __shfl_up_sync(0xffffffffu, v[q].x, d), y = __shfl_up_sync(0xffffffffu, v[q].y, d);
+                const float z = __shfl_up_sync(0xffffffffu, v[q].z, d), w = __shfl_up_sync(0xffffffffu, v[q].w, d);
+                if (lane - d >= h) {
+                    v[q].x += x;
+                    v[q].y += y;
+                    v[q].z += z;
+                    v[q].w += w;
+                }
+            }
+        }
+        const bool hit = a < b && a < base + 32 && b > base;  // this key has records in the chunk
+        const int e = static_cast<int>((b < base + 32 ? b : base + 32) - 1 - base);
+        const int src = hit ? e : lane;
+#pragma unroll
+        for (int q = 0; q < NF4; ++q) {
+            const float x = __shfl_sync(0xffffffffu, v[q].x, src), y = __shfl_sync(0xffffffffu, v[q].y, src);
+            const float z = __shfl_sync(0xffffffffu, v[q].z, src), w = __shfl_sync(0xffffffffu, v[q].w, src);
+            if (hit) {
+                acc[q].x += x;
+                acc[q].y += y;
+                acc[q].z += z;
+                acc[q].w += w;
+            }
+        }
+    }
+    if (live) {
+        float4* o = out + static_cast<size_t>(k) * OSTRIDE4;
+#pragma unroll
+        for (int q = 0; q < NF4; ++q) o[q] = acc[q];
+#pragma unroll
+        for (int q = NF4; q < OSTRIDE4; ++q) o[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 // ------------------------------------------------------------------ K11
 // out[k][g] = lambda p[k][g] + sum_v (dconic, dmean2d, ... / dbeta)^T inter_v[g],
-// exact reverse mode of the projection.  Atomic mode: inter (red.global.add
-// sums) is zeroed after reading.  Deterministic mode (D.partial): inter_v[g]
-// is the ordered sum of the (view, Gaussian)'s slots (det_gather).
-template <bool DET>
+// exact reverse mode of the projection.  MODE 0 (atomic): inter holds the
+// red.global.add sums and is zeroed after reading.  MODE 1 (deterministic,
+// fused): inter_v[g] is the ordered sum of the (view, Gaussian)'s records
+// (det_sum).  MODE 2 (deterministic, k_det_reduce first): inter is read as is.
+template <int MODE>
 __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ rec, float* __restrict__ inter,
@@ -291,6 +361,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     float gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
     // Software pipeline: view v+1's record and intermediate are loaded
     // (unconditionally; invalid pairs hold zeros) while view v is processed.
+    constexpr bool DET = MODE == 1;
     float4 nr0, nr1, ni0, ni1, ni2;
     auto fetch = [&](int v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
@@ -321,7 +392,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
         const float4 q0 = nr0, q1 = nr1;
         if (v + 1 < V) fetch(v + 1);
         if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
-        if (!DET) {
+        if (MODE == 0) {
             float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
             ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
             ip[1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -415,7 +486,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
-template <bool DET>
+template <int MODE>
 __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
                                                        const float4* __restrict__ rec,
@@ -430,6 +501,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
     const float zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const float zero3[3] = {0, 0, 0};
     // software pipeline: next view's record and accumulators load during this view
+    constexpr bool DET = MODE == 1;
     float4 nr0, nr1, nr2, na[5];
     auto fetch = [&](int v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
@@ -461,7 +533,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         }
         if (v + 1 < V) fetch(v + 1);
         if (q2.y == 0.0f) continue;
-        if (!DET) {
+        if (MODE == 0) {
             float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
             for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -523,20 +595,36 @@ void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V,
                   float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
                   cudaStream_t st) {
     if (G == 0) return;
-    if (det.partial)
-        k_chain<true><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
-    else
-        k_chain<false><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    const unsigned nb = (G + 127) / 128;
+    if (!det.partial) {
+        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    } else if (det.fused) {
+        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    } else {
+        const long long nk = static_cast<long long>(V) * Gp;
+        k_det_reduce<kRec / 4, kDetRec / 4, kRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
+            det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(inter));
+        ++g_launches;
+        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
+    }
     ++g_launches;
 }
 
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                           float* diagacc, const DetOrder& det, float* out, cudaStream_t st) {
     if (G == 0) return;
-    if (det.partial)
-        k_diag_finalize<true><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
-    else
-        k_diag_finalize<false><<<(G + 127) / 128, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    const unsigned nb = (G + 127) / 128;
+    if (!det.partial) {
+        k_diag_finalize<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    } else if (det.fused) {
+        k_diag_finalize<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    } else {
+        const long long nk = static_cast<long long>(V) * Gp;
+        k_det_reduce<5, kDetDiagRec / 4, kDiagRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
+            det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(diagacc));
+        ++g_launches;
+        k_diag_finalize<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+    }
     ++g_launches;
 }
 

@@ -115,6 +115,12 @@ constexpr int kDetDiagRec = 24;  // floats per diag partial record (19 used): th
 struct DetOrder {
     const unsigned* seg;
     const float* partial;  // kDetRec floats per record (J^T) or kDetDiagRec (diag)
+    // 1: the chain kernel's thread sums its (view, Gaussian)'s records itself
+    //    (few records per key, many Gaussians: configs[2]);
+    // 0: k_det_reduce first sums every key's records with a warp-segmented
+    //    reduction (parallel over records: many records per key / few
+    //    Gaussians, configs[0]) into inter / diagacc, which the chain reads.
+    int fused;
 };
 
 constexpr int kRecBlock = 9 * 32;  // floats per window record block (1152 B)

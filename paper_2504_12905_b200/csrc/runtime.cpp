@@ -857,6 +857,15 @@ struct Jacobian {
             samples.dhist.ensure(hs);
             samples.dpart.ensure(scan_scratch(hs));
             samples.partial.ensure(static_cast<size_t>(kDetDiagRec) * n1);  // J^T and diag records share it
+            // summation path (DetOrder::fused): the chain thread sums its own keys when
+            // keys carry few records each, else a record-parallel segmented reduction
+            // first (few Gaussians, many records per key; SLM_DET_PATH=fused|reduce overrides)
+            const char* env = std::getenv("SLM_DET_PATH");
+            det_fused = env ? std::strcmp(env, "reduce") != 0 : ns <= 4 * static_cast<long long>(batch->V) * scene->G;
+            if (!det_fused) {
+                inter.ensure(static_cast<size_t>(nk) * kRec);
+                diagacc.ensure(static_cast<size_t>(nk) * kDiagRec);
+            }
             build_slot_order(samples.groups.p, static_cast<int>(ng), samples.gcount.p, samples.glist.p,
                              samples.mask_off.p, samples.wbase.p, scene->Gp, batch->V, ns, samples.dka.p,
                              samples.dkb.p, samples.dva.p, samples.dvb.p, samples.dhist.p, samples.dpart.p,
@@ -867,8 +876,9 @@ struct Jacobian {
     }
 
     bool det = true;  // this plan's accumulation mode (Context::deterministic at init_device)
+    bool det_fused = true;
     DetOrder det_order() const {
-        return det ? DetOrder{samples.seg.p, samples.partial.p} : DetOrder{nullptr, nullptr};
+        return det ? DetOrder{samples.seg.p, samples.partial.p, det_fused ? 1 : 0} : DetOrder{nullptr, nullptr, 0};
     }
     // out = sum_v chain_v^T inter_v (+ lambda p): the J^T chain of the last J^T pass
     void chain(const float* p, float lambda, float* out, const int* done = nullptr) {
