@@ -52,6 +52,14 @@ int slm_context_synchronize(slm_context* ctx);
 int slm_nccl_unique_id(uint8_t out[128]);
 int slm_context_init_comm(slm_context* ctx, const uint8_t id[128], int rank, int world);
 int slm_context_rank(slm_context* ctx, int* rank, int* world);
+/* In-process rank group: `world` contexts of ONE process (on one GPU or several),
+ * each driven by its own host thread, joined with slm_context_init_local; their
+ * collectives sum the ranks' vectors in rank order.  The same view-sharded code
+ * path as NCCL, runnable on a single GPU (tests). */
+typedef struct slm_local_group slm_local_group;
+int slm_local_group_create(int world, slm_local_group** out);
+void slm_local_group_destroy(slm_local_group* group);
+int slm_context_init_local(slm_context* ctx, slm_local_group* group, int rank);
 /* J^T / diag(J^T W J) accumulation order.  on (the default): every (view,
  * Gaussian)'s per-entry contributions are summed in a fixed per-plan order, so
  * jvp / vjp / jtj_diag / gn_apply / pcg / lm_step are bitwise reproducible run

@@ -322,6 +322,31 @@ void launch_axpy(float* y, const float* x, long long n, float a, cudaStream_t st
     k_axpy<<<kRedBlocks, 256, 0, st>>>(y, x, n, a); ++g_launches;
 }
 
+// LocalComm's reduction: dst[i] = sum over ranks k = 0 .. world-1 (in order) of
+// src_k[i] (the staging slots; peers' slots over NVLink when on other GPUs)
+struct RankPtrs {
+    const void* p[64];
+};
+template <typename T>
+__global__ void k_sum_ranks(RankPtrs s, int world, T* __restrict__ dst, long long n) {
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        T acc = static_cast<const T*>(s.p[0])[i];
+        for (int k = 1; k < world; ++k) acc += static_cast<const T*>(s.p[k])[i];
+        dst[i] = acc;
+    }
+}
+void launch_sum_ranks(void* const* srcs, int world, void* dst, size_t n, bool f64, cudaStream_t st) {
+    if (n == 0) return;
+    RankPtrs s{};
+    for (int k = 0; k < world && k < 64; ++k) s.p[k] = srcs[k];
+    if (f64)
+        k_sum_ranks<double><<<kRedBlocks, 256, 0, st>>>(s, world, static_cast<double*>(dst), static_cast<long long>(n));
+    else
+        k_sum_ranks<float><<<kRedBlocks, 256, 0, st>>>(s, world, static_cast<float*>(dst), static_cast<long long>(n));
+    ++g_launches;
+}
+
 // f32 <-> f64 element copies (the truth images widened for the FP64 metrics,
 // FP64 SSIM planes narrowed for the f32 products)
 template <typename A, typename B>

@@ -17,6 +17,8 @@
 #include <cmath>
 #include <limits>
 #include <memory>
+#include <mutex>
+#include <condition_variable>
 #include <numeric>
 #include <sstream>
 #include <thread>
@@ -78,6 +80,104 @@ const NcclApi& nccl() {
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 }  // namespace
 
+// =========================================================================== collectives
+// The view-sharded path's collective seam: a sum-allreduce of f32 or
+// f64 device vectors on the context's stream.  NcclComm: one process per GPU
+// (the deployment).  LocalComm: a group of contexts inside ONE process -- on one
+// GPU or several -- each rank driven by its own host thread; it sums the ranks'
+// buffers in rank order (deterministic for a given world size), so the world > 1
+// code path (view slices, [b | diag], products, loss scalars) runs and is tested
+// on a single B200.
+struct Comm {
+    virtual ~Comm() = default;
+    virtual void allreduce(void* p, size_t n, bool f64, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+    ncclComm_t c = nullptr;
+    ~NcclComm() override {
+        if (c) nccl().CommDestroy(c);
+    }
+    void allreduce(void* p, size_t n, bool f64, cudaStream_t st) override {
+        SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, f64 ? ncclFloat64 : ncclFloat32, ncclSum, c, st));
+    }
+};
+
+// Host rendezvous + per-rank staging slots and events.  One allreduce round:
+//   1. wait until every rank finished reading the staging slots of the last round
+//   2. copy the rank's vector into its slot, record `ready`
+//   3. barrier; wait for every rank's `ready`; sum the slots in rank order into
+//      the rank's own vector (k_sum_ranks); record `done`; barrier.
+struct LocalGroup {
+    int world;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long generation = 0;
+    std::vector<void*> slot;
+    std::vector<size_t> slot_bytes;
+    std::vector<int> slot_dev;
+    std::vector<cudaEvent_t> ready, done;
+    explicit LocalGroup(int w) : world(w), slot(w, nullptr), slot_bytes(w, 0), slot_dev(w, 0), ready(w, nullptr),
+                                 done(w, nullptr) {}
+    ~LocalGroup() {
+        for (int r = 0; r < world; ++r) {
+            if (slot[r]) cudaFree(slot[r]);
+            if (ready[r]) cudaEventDestroy(ready[r]);
+            if (done[r]) cudaEventDestroy(done[r]);
+        }
+    }
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const long long gen = generation;
+        if (++arrived == world) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+void launch_sum_ranks(void* const* srcs, int world, void* dst, size_t n, bool f64, cudaStream_t st);
+
+struct LocalComm : Comm {
+    std::shared_ptr<LocalGroup> g;
+    int rank;
+    int device;
+    LocalComm(std::shared_ptr<LocalGroup> grp, int r, int dev) : g(std::move(grp)), rank(r), device(dev) {
+        SLM_CUDA_CHECK(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+        SLM_CUDA_CHECK(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
+        g->slot_dev[rank] = dev;
+    }
+    void allreduce(void* p, size_t n, bool f64, cudaStream_t st) override {
+        const size_t bytes = n * (f64 ? 8 : 4);
+        for (int k = 0; k < g->world; ++k)  // 1. the last round's readers are done with the slots
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(st, g->done[k], 0));
+        if (g->slot_bytes[rank] < bytes) {  // grow this rank's slot (nobody reads it now)
+            SLM_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (g->slot[rank]) SLM_CUDA_CHECK(cudaFree(g->slot[rank]));
+            SLM_CUDA_CHECK(cudaMalloc(&g->slot[rank], bytes));
+            g->slot_bytes[rank] = bytes;
+        }
+        SLM_CUDA_CHECK(cudaMemcpyAsync(g->slot[rank], p, bytes, cudaMemcpyDeviceToDevice, st));
+        SLM_CUDA_CHECK(cudaEventRecord(g->ready[rank], st));
+        g->barrier();
+        for (int k = 0; k < g->world; ++k) {
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(st, g->ready[k], 0));
+            if (g->slot_dev[k] != device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(g->slot_dev[k], 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) SLM_CUDA_CHECK(e);
+                cudaGetLastError();
+            }
+        }
+        launch_sum_ranks(g->slot.data(), g->world, p, n, f64, st);
+        SLM_CUDA_CHECK(cudaEventRecord(g->done[rank], st));
+        g->barrier();
+    }
+};
+
 // =========================================================================== Context
 struct StepBuffers;
 void destroy_step(StepBuffers*);
@@ -88,7 +188,7 @@ struct Context {
     bool own_stream = true;
     cudaStream_t aux = nullptr;       // copy stream overlapping uploads with kernels on `stream`
     cudaEvent_t aux_done = nullptr;
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<Comm> comm;  // world > 1: NCCL (one process per GPU) or an in-process LocalGroup
     int rank = 0, world = 1;
     DevBuf<double> partial;
     DevBuf<CgState> cg;
@@ -120,7 +220,7 @@ struct Context {
     ~Context() {
         destroy_step(step);
         for (auto& m : marks) cudaEventDestroy(m.second);
-        if (comm) nccl().CommDestroy(comm);
+        comm.reset();
         if (stream && own_stream) cudaStreamDestroy(stream);
         if (aux) cudaStreamDestroy(aux);
         if (aux_done) cudaEventDestroy(aux_done);
@@ -181,11 +281,11 @@ struct Context {
 
     void allreduce(float* p, size_t n) {
         if (world <= 1 || n == 0) return;
-        SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, ncclFloat32, ncclSum, comm, stream));
+        comm->allreduce(p, n, false, stream);
     }
     void allreduce(double* p, size_t n) {
         if (world <= 1 || n == 0) return;
-        SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, ncclFloat64, ncclSum, comm, stream));
+        comm->allreduce(p, n, true, stream);
     }
 };
 
@@ -1995,11 +2095,36 @@ int slm_context_init_comm(slm_context* ctx, const uint8_t id[128], int rank, int
         Context& c = ctx->impl;
         c.activate();
         if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
+        c.comm.reset();
         if (world > 1) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, 128);
-            SLM_NCCL_CHECK(nccl().CommInitRank(&c.comm, world, uid, rank));
+            auto nc = std::make_unique<NcclComm>();
+            SLM_NCCL_CHECK(nccl().CommInitRank(&nc->c, world, uid, rank));
+            c.comm = std::move(nc);
         }
+        c.rank = rank;
+        c.world = world;
+    });
+}
+struct slm_local_group {
+    std::shared_ptr<LocalGroup> g;
+};
+int slm_local_group_create(int world, slm_local_group** out) {
+    return guarded([&] {
+        if (world < 1 || world > 64) throw std::invalid_argument("local group: world must be in [1, 64]");
+        *out = new slm_local_group{std::make_shared<LocalGroup>(world)};
+    });
+}
+void slm_local_group_destroy(slm_local_group* g) { delete g; }
+int slm_context_init_local(slm_context* ctx, slm_local_group* group, int rank) {
+    return guarded([&] {
+        Context& c = ctx->impl;
+        c.activate();
+        const int world = group->g->world;
+        if (rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
+        c.comm.reset();
+        if (world > 1) c.comm = std::make_unique<LocalComm>(group->g, rank, c.device);
         c.rank = rank;
         c.world = world;
     });

@@ -55,6 +55,9 @@ _SIGS = {
     "slm_context_profile_collect": (C.c_int, [_vp, _f64p, _i32p]),
     "slm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "slm_context_init_comm": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
+    "slm_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "slm_local_group_destroy": (None, [_vp]),
+    "slm_context_init_local": (C.c_int, [_vp, _vp, C.c_int]),
     "slm_context_rank": (C.c_int, [_vp, _i32p, _i32p]),
     "slm_rng_create": (C.c_int, [C.c_uint64, C.POINTER(_vp)]),
     "slm_rng_destroy": (None, [_vp]),
@@ -295,6 +298,23 @@ class HostSampler:
 
 
 
+class LocalGroup:
+    """slm_local_group: `world` contexts of this process acting as ranks."""
+
+    def __init__(self, world: int):
+        self.dll = dll()
+        h = _vp()
+        _check(self.dll.slm_local_group_create(world, C.byref(h)))
+        self.h = h
+        self.world = world
+
+    def __del__(self):
+        try:
+            self.dll.slm_local_group_destroy(self.h)
+        except Exception:
+            pass
+
+
 class Lib(HostSampler):
     """One CUDA context (device + stream) driving the B200 kernels."""
 
@@ -376,6 +396,12 @@ class Lib(HostSampler):
         if rc != 0:
             raise SlmError(dll.slm_last_error().decode())
         return bytes(buf)
+
+    def init_local(self, group: "LocalGroup", rank: int):
+        """Join an in-process rank group (slm_context_init_local): the view-sharded
+        lm_step / products with the group's rank-order sums as the collectives."""
+        self._check(self.dll.slm_context_init_local(self.ctx, group.h, rank))
+        self._group = group  # keep the group alive while this context uses it
 
     def init_comm(self, uid: bytes, rank: int, world: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

@@ -1,0 +1,74 @@
+"""The view-sharded multi-rank path on ONE GPU (GPU).
+
+Two contexts of this process act as ranks 0 and 1 of an in-process group
+(slm_local_group, the collective seam's single-process implementation; the
+deployment uses NCCL with one process per GPU).  Each rank replays
+the host RNG for the whole batch, owns its slice of the views, and the
+J^T W J p products, the fused [b | diag] and the loss scalars are summed over
+the ranks -- exactly the world > 1 code path of lm_step.  The world-2 run must
+draw the same batches, end at the same RNG position, keep the ranks' states
+bitwise identical, and match the world-1 run to the float tolerance (the sums
+over views are associated differently).
+"""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from paper_2504_12905_b200.types import LmConfig
+from support import g_cams, golden, norm_rel, rel_error
+
+pytestmark = pytest.mark.gpu
+STEPS = 8
+
+
+def _setup(L):
+    d = golden("lm")
+    tc = g_cams(d["toy_train_cams"])
+    rng = L.rng(1)
+    st = L.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    td = L.train_data(tc, list(d["toy_train_imgs"]))
+    td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
+    return st, td, rng
+
+
+def _run(L, cfg):
+    st, td, rng = _setup(L)
+    reps = [L.lm_step(st, td, cfg, it, rng) for it in range(STEPS)]
+    return [(r.loss_before, r.loss_after, r.eta, r.pcg_iterations, tuple(r.batch)) for r in reps], st.pack(), rng()
+
+
+def _world2(cfg):
+    from paper_2504_12905_b200 import splatlm
+    group = splatlm.LocalGroup(2)
+    libs = [splatlm.Lib(0), splatlm.Lib(0)]
+    for r, L in enumerate(libs):
+        L.init_local(group, r)
+    with ThreadPoolExecutor(2) as ex:
+        out = list(ex.map(lambda L: _run(L, cfg), libs))
+    return out
+
+
+@pytest.mark.parametrize("loss", [0, 1])
+def test_two_ranks_match_one(loss):
+    from paper_2504_12905_b200 import splatlm
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, loss=loss, ssim_weight=0.2)
+    one = _run(splatlm.Lib(0), cfg)
+    r0, r1 = _world2(cfg)
+    # the ranks agree bit for bit (replicated CG vectors, rank-order sums)
+    assert r0[0] == r1[0] and np.array_equal(r0[1], r1[1]) and r0[2] == r1[2]
+    # same batches and RNG position as one rank; losses and state to the float tolerance
+    worst = 0.0
+    for a, b in zip(r0[0], one[0]):
+        assert a[4] == b[4] and a[3] == b[3]
+        worst = max(worst, rel_error(a[0], b[0]), rel_error(a[1], b[1]))
+    print("world 2 vs 1: worst loss rel err", worst, "state", norm_rel(r0[1], one[1]))
+    assert worst < 1e-4
+    assert r0[2] == one[2]
+    assert norm_rel(r0[1], one[1]) < 1e-4
+
+
+def test_two_ranks_bitwise_reproducible():
+    cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8)
+    a, b = _world2(cfg), _world2(cfg)
+    assert a[0][0] == b[0][0] and np.array_equal(a[0][1], b[0][1])
