@@ -60,6 +60,9 @@ typedef struct slm_local_group slm_local_group;
 int slm_local_group_create(int world, slm_local_group** out);
 void slm_local_group_destroy(slm_local_group* group);
 int slm_context_init_local(slm_context* ctx, slm_local_group* group, int rank);
+/* world > 1: the J^T W J p product's chain runs over this many Gaussian chunks,
+ * each chunk's allreduce overlapping the next chunk (default 4). */
+int slm_context_set_comm_chunks(slm_context* ctx, int chunks);
 /* J^T / diag(J^T W J) accumulation order.  on (the default): every (view,
  * Gaussian)'s per-entry contributions are summed in a fixed per-plan order, so
  * jvp / vjp / jtj_diag / gn_apply / pcg / lm_step are bitwise reproducible run

@@ -351,10 +351,11 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ rec, float* __restrict__ inter,
                                                DetOrder D, const float* __restrict__ p, float lambda,
-                                               float* __restrict__ out, const int* __restrict__ done_flag) {
+                                               float* __restrict__ out, const int* __restrict__ done_flag, int g0,
+                                               int g1) {
     if (done_flag && *done_flag) return;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= g1) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
@@ -591,23 +592,35 @@ void launch_tangents(const float* beta32, const float* p, int G, int Gp, const D
     k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
 }
 
+// The chain over Gaussians [g0, g1) (the multi-rank path runs it in chunks,
+// each chunk's allreduce overlapping the next chunk); `reduce`: run the
+// record-parallel k_det_reduce first (deterministic path 0, all keys at once).
+void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                        float* inter, const DetOrder& det, const float* p, float lambda, float* out,
+                        const int* done, int g0, int g1, bool reduce, cudaStream_t st) {
+    g1 = g1 < G ? g1 : G;
+    if (g1 <= g0) return;
+    const unsigned nb = (g1 - g0 + 127) / 128;
+    if (!det.partial) {
+        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+    } else if (det.fused) {
+        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+    } else {
+        if (reduce) {
+            const long long nk = static_cast<long long>(V) * Gp;
+            k_det_reduce<kRec / 4, kDetRec / 4, kRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
+                det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(inter));
+            ++g_launches;
+        }
+        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+    }
+    ++g_launches;
+}
+
 void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                   float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
                   cudaStream_t st) {
-    if (G == 0) return;
-    const unsigned nb = (G + 127) / 128;
-    if (!det.partial) {
-        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
-    } else if (det.fused) {
-        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
-    } else {
-        const long long nk = static_cast<long long>(V) * Gp;
-        k_det_reduce<kRec / 4, kDetRec / 4, kRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
-            det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(inter));
-        ++g_launches;
-        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done);
-    }
-    ++g_launches;
+    launch_chain_range(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, 0, G, true, st);
 }
 
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,

@@ -49,6 +49,8 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -65,7 +67,10 @@ const NcclApi& nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString)
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString ||
+        !api.GroupStart || !api.GroupEnd)
         throw NcclError("NCCL library lacks required symbols");
     loaded = true;
     return api;
@@ -91,6 +96,8 @@ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 struct Comm {
     virtual ~Comm() = default;
     virtual void allreduce(void* p, size_t n, bool f64, cudaStream_t st) = 0;
+    // f32 rows [base + r * pitch, + len), r < rows: one Gaussian chunk of a [14][Gp] vector
+    virtual void allreduce_rows(float* base, size_t pitch, int rows, size_t len, cudaStream_t st) = 0;
 };
 
 struct NcclComm : Comm {
@@ -100,6 +107,12 @@ struct NcclComm : Comm {
     }
     void allreduce(void* p, size_t n, bool f64, cudaStream_t st) override {
         SLM_NCCL_CHECK(nccl().AllReduce(p, p, n, f64 ? ncclFloat64 : ncclFloat32, ncclSum, c, st));
+    }
+    void allreduce_rows(float* base, size_t pitch, int rows, size_t len, cudaStream_t st) override {
+        SLM_NCCL_CHECK(nccl().GroupStart());
+        for (int r = 0; r < rows; ++r)
+            SLM_NCCL_CHECK(nccl().AllReduce(base + r * pitch, base + r * pitch, len, ncclFloat32, ncclSum, c, st));
+        SLM_NCCL_CHECK(nccl().GroupEnd());
     }
 };
 
@@ -176,6 +189,25 @@ struct LocalComm : Comm {
         SLM_CUDA_CHECK(cudaEventRecord(g->done[rank], st));
         g->barrier();
     }
+    float* rows_tmp = nullptr;
+    size_t rows_cap = 0;
+    ~LocalComm() override {
+        if (rows_tmp) cudaFree(rows_tmp);
+    }
+    void allreduce_rows(float* base, size_t pitch, int rows, size_t len, cudaStream_t st) override {
+        const size_t n = static_cast<size_t>(rows) * len;
+        if (rows_cap < n) {
+            SLM_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (rows_tmp) SLM_CUDA_CHECK(cudaFree(rows_tmp));
+            SLM_CUDA_CHECK(cudaMalloc(&rows_tmp, n * sizeof(float)));
+            rows_cap = n;
+        }
+        SLM_CUDA_CHECK(cudaMemcpy2DAsync(rows_tmp, len * sizeof(float), base, pitch * sizeof(float), len * sizeof(float),
+                                         rows, cudaMemcpyDeviceToDevice, st));
+        allreduce(rows_tmp, n, false, st);
+        SLM_CUDA_CHECK(cudaMemcpy2DAsync(base, pitch * sizeof(float), rows_tmp, len * sizeof(float), len * sizeof(float),
+                                         rows, cudaMemcpyDeviceToDevice, st));
+    }
 };
 
 // =========================================================================== Context
@@ -224,6 +256,29 @@ struct Context {
         if (stream && own_stream) cudaStreamDestroy(stream);
         if (aux) cudaStreamDestroy(aux);
         if (aux_done) cudaEventDestroy(aux_done);
+        for (auto e : chunk_ev) cudaEventDestroy(e);
+        if (comm_done) cudaEventDestroy(comm_done);
+        if (comm_st) cudaStreamDestroy(comm_st);
+    }
+    // the chunked product allreduce: a comm stream and one event per chunk
+    cudaStream_t comm_st = nullptr;
+    std::vector<cudaEvent_t> chunk_ev;
+    cudaEvent_t comm_done = nullptr;
+    int comm_chunks = 4;
+    cudaStream_t comm_stream() {
+        if (!comm_st) {
+            SLM_CUDA_CHECK(cudaStreamCreateWithFlags(&comm_st, cudaStreamNonBlocking));
+            SLM_CUDA_CHECK(cudaEventCreateWithFlags(&comm_done, cudaEventDisableTiming));
+        }
+        return comm_st;
+    }
+    cudaEvent_t chunk_event(int i) {
+        while (static_cast<int>(chunk_ev.size()) <= i) {
+            cudaEvent_t e;
+            SLM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            chunk_ev.push_back(e);
+        }
+        return chunk_ev[i];
     }
     cudaStream_t aux_stream() {
         if (!aux) {
@@ -1035,9 +1090,26 @@ struct Jacobian {
         launch_sample_raster(kGn, a, st);
         if (prof) ctx->prof_record(ev, 2);
         if (ctx->world > 1) {
-            chain(nullptr, 0.f, dout, done);
-            ctx->allreduce(dout, P());
-            launch_axpy(dout, dp, static_cast<long long>(P()), lambda, st);
+            // chunk-pipelined chain + allreduce: the chain runs over
+            // Gaussian chunks on the main stream; each finished chunk's 14 rows are
+            // allreduced on the comm stream while the next chunk computes.  Rank 0
+            // adds lambda p inside its chain, so the sum carries it exactly once.
+            cudaStream_t cs = ctx->comm_stream();
+            const int G = scene->G, Gp = scene->Gp;
+            const int nch = std::max(1, ctx->comm_chunks);
+            const int step = round_up((G + nch - 1) / nch, 256);
+            const float* pp = ctx->rank == 0 ? dp : nullptr;
+            int c = 0;
+            for (int g0 = 0; g0 < G; g0 += step, ++c) {
+                const int g1 = std::min(G, g0 + step);
+                launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+                                   det_order(), pp, lambda, dout, done, g0, g1, c == 0, st);
+                SLM_CUDA_CHECK(cudaEventRecord(ctx->chunk_event(c), st));
+                SLM_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->chunk_event(c), 0));
+                ctx->comm->allreduce_rows(dout + g0, static_cast<size_t>(Gp), kP, static_cast<size_t>(g1 - g0), cs);
+            }
+            SLM_CUDA_CHECK(cudaEventRecord(ctx->comm_done, cs));
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->comm_done, 0));
         } else {
             chain(dp, lambda, dout, done);
         }
@@ -2058,6 +2130,12 @@ int slm_context_set_stream(slm_context* ctx, void* stream) {
 int slm_context_step_stats(slm_context* ctx, int64_t out[8]) {
     return guarded([&] {
         for (int i = 0; i < 8; ++i) out[i] = ctx->impl.step_stats[i];
+    });
+}
+int slm_context_set_comm_chunks(slm_context* ctx, int chunks) {
+    return guarded([&] {
+        if (chunks < 1) throw std::invalid_argument("comm chunks must be positive");
+        ctx->impl.comm_chunks = chunks;
     });
 }
 int slm_context_set_deterministic(slm_context* ctx, int on) {

@@ -99,6 +99,10 @@ void launch_tangents(const float* beta32, const float* p, int G, int Gp, const D
 void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
                   float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
                   cudaStream_t st);
+void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+                        float* inter, const DetOrder& det, const float* p, float lambda, float* out,
+                        const int* done, int g0, int g1, bool reduce, cudaStream_t st);
+void launch_sum_ranks(void* const* srcs, int world, void* dst, size_t n, bool f64, cudaStream_t st);
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V,
                           const float4* rec, float* diagacc, const DetOrder& det, float* out, cudaStream_t st);
 void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,

@@ -58,6 +58,7 @@ _SIGS = {
     "slm_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "slm_local_group_destroy": (None, [_vp]),
     "slm_context_init_local": (C.c_int, [_vp, _vp, C.c_int]),
+    "slm_context_set_comm_chunks": (C.c_int, [_vp, C.c_int]),
     "slm_context_rank": (C.c_int, [_vp, _i32p, _i32p]),
     "slm_rng_create": (C.c_int, [C.c_uint64, C.POINTER(_vp)]),
     "slm_rng_destroy": (None, [_vp]),
@@ -402,6 +403,10 @@ class Lib(HostSampler):
         lm_step / products with the group's rank-order sums as the collectives."""
         self._check(self.dll.slm_context_init_local(self.ctx, group.h, rank))
         self._group = group  # keep the group alive while this context uses it
+
+    def set_comm_chunks(self, chunks: int):
+        """Gaussian chunks of the pipelined chain + allreduce (world > 1)."""
+        self._check(self.dll.slm_context_set_comm_chunks(self.ctx, chunks))
 
     def init_comm(self, uid: bytes, rank: int, world: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

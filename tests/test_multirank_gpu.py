@@ -22,39 +22,42 @@ pytestmark = pytest.mark.gpu
 STEPS = 8
 
 
-def _setup(L):
+def _setup(L, n=40):
     d = golden("lm")
     tc = g_cams(d["toy_train_cams"])
     rng = L.rng(1)
-    st = L.random_init(40, [-1, -1, -1], [1, 1, 1], rng)
+    st = L.random_init(n, [-1, -1, -1], [1, 1, 1], rng)
     td = L.train_data(tc, list(d["toy_train_imgs"]))
     td.rebuild_clusters(8, 1 ^ 0x9E3779B97F4A7C15)
     return st, td, rng
 
 
-def _run(L, cfg):
-    st, td, rng = _setup(L)
+def _run(L, cfg, n=40):
+    st, td, rng = _setup(L, n)
     reps = [L.lm_step(st, td, cfg, it, rng) for it in range(STEPS)]
     return [(r.loss_before, r.loss_after, r.eta, r.pcg_iterations, tuple(r.batch)) for r in reps], st.pack(), rng()
 
 
-def _world2(cfg):
+def _world2(cfg, chunks=4, n=40):
     from paper_2504_12905_b200 import splatlm
     group = splatlm.LocalGroup(2)
     libs = [splatlm.Lib(0), splatlm.Lib(0)]
     for r, L in enumerate(libs):
         L.init_local(group, r)
+        L.set_comm_chunks(chunks)
     with ThreadPoolExecutor(2) as ex:
-        out = list(ex.map(lambda L: _run(L, cfg), libs))
+        out = list(ex.map(lambda L: _run(L, cfg, n), libs))
     return out
 
 
-@pytest.mark.parametrize("loss", [0, 1])
-def test_two_ranks_match_one(loss):
+@pytest.mark.parametrize("loss,chunks,n", [(0, 1, 40), (1, 3, 40), (0, 1, 2000), (0, 4, 2000), (1, 3, 2000)])
+def test_two_ranks_match_one(loss, chunks, n):
+    """chunks: the product's chain + allreduce pipeline depth (1 = one allreduce); with
+    2000 Gaussians the chain runs in up to 4 chunks of 512."""
     from paper_2504_12905_b200 import splatlm
     cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, loss=loss, ssim_weight=0.2)
-    one = _run(splatlm.Lib(0), cfg)
-    r0, r1 = _world2(cfg)
+    one = _run(splatlm.Lib(0), cfg, n)
+    r0, r1 = _world2(cfg, chunks, n)
     # the ranks agree bit for bit (replicated CG vectors, rank-order sums)
     assert r0[0] == r1[0] and np.array_equal(r0[1], r1[1]) and r0[2] == r1[2]
     # same batches and RNG position as one rank; losses and state to the float tolerance
