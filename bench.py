@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--views", type=int, default=200)
     ap.add_argument("--width", type=int, default=1280)
     ap.add_argument("--height", type=int, default=720)
-    ap.add_argument("--batch", type=int, default=8, help="views per rank per LM batch")
+    ap.add_argument("--batch", type=int, default=8, help="views per rank per LM batch (weak scaling)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: this many views per LM batch in total, split over the ranks")
     ap.add_argument("--spt", type=int, default=32, help="samples per tile")
     ap.add_argument("--lm-steps", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -81,6 +83,7 @@ def workload_config(args) -> dict:
                         "N=32 samples/tile, lambda=0.1",
             "gaussians": args.gaussians, "views": args.views, "width": args.width, "height": args.height,
             "batch_views_per_rank": args.batch, "samples_per_tile": args.spt,
+            **({"global_batch_views": args.global_batch} if args.global_batch else {}),
             "l2": "working set > 126 MB L2 (no flush needed)"}
 
 
@@ -117,13 +120,22 @@ def LmConfig(**kw):
     return _L(**kw)
 
 
+def rank_views(args, world) -> int:
+    """Views per rank: --batch (weak scaling) or --global-batch / world (strong)."""
+    if args.global_batch:
+        if args.global_batch % world:
+            raise SystemExit("--global-batch must be a multiple of the rank count")
+        return args.global_batch // world
+    return args.batch
+
+
 def host_inputs(H, args, world):
     """Seeded exactly like train_run (run.cpp:126-167): random_init consumes the
     run RNG first, then the view batch and the sample plan draw from it."""
     rng = H.rng(1)
     state = H.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)
     cams = cameras(args)
-    clusters = H.kmeans_cameras(cams, args.batch * world, 1 ^ KMEANS_SALT)
+    clusters = H.kmeans_cameras(cams, rank_views(args, world) * world, 1 ^ KMEANS_SALT)
     batch = H.sample_view_batch(clusters, rng)
     plan = H.build_sample_plan([cams[i] for i in batch], args.spt, 0, rng, 32)
     return state, cams, clusters, batch, plan
@@ -368,6 +380,9 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # NCCL's init lines (rank, nRanks, transport) stay on stderr for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         try:
@@ -390,7 +405,8 @@ def run_b200(args):
     t_setup = time.perf_counter()
     state, cams, clusters, batch, plan = host_inputs(L, args, world)
     log(f"host inputs: G={args.gaussians}, batch={batch}, samples={plan.total_samples()}")
-    lo, hi = rank * args.batch, (rank + 1) * args.batch
+    nv = rank_views(args, world)
+    lo, hi = rank * nv, (rank + 1) * nv
     scene = splatlm.Scene(L, state)
     # Global N_total weights, this rank's views: slice the plan but keep weights
     # relative to the whole batch (the solver's allreduce sums the slices).
@@ -431,7 +447,9 @@ def run_b200(args):
         ms = float(t.item())
         dist.barrier()
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms / 1000.0)  # 8-view products, all ranks
+    # in units of 8-view products: weak = one per rank per step, strong = global batch / 8
+    units = world * nv / 8.0
+    value = units * args.steps / (ms / 1000.0)
 
     # per-kernel breakdown of the product (CUDA events around each kernel)
     L.set_profiling(True)
@@ -467,7 +485,7 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     del host_jac
-    e2e_value = world / e2e_s
+    e2e_value = units / e2e_s
     log(f"e2e host gn_apply: {e2e_s * 1000:.1f} ms")
 
     # LM iterations/s on the device-resident scene (lm_step, lm.cpp:56-157)
@@ -481,8 +499,8 @@ def run_b200(args):
         del imgs
         td.set_clusters(clusters)
         lm_scene = splatlm.Scene(L, state)
-        cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, batch_size_initial=args.batch * world,
-                       batch_size_late=args.batch * world, samples_per_tile=args.spt)
+        cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8, batch_size_initial=nv * world,
+                       batch_size_late=nv * world, samples_per_tile=args.spt)
         rng = L.rng(1)
         L.random_init(args.gaussians, [-1, -1, -1], [1, 1, 1], rng)  # same stream position as train_run
         L.set_timing(True)
@@ -542,7 +560,7 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": "strong" if args.global_batch else "weak", "vs_baseline": None,
         "dtype": "f32 (raster, linearisation, CG vectors; f64 projection, blend decisions and parameters)",
         "data": DATA_TEXT,
         "config": workload_config(args),
@@ -554,7 +572,7 @@ def run_b200(args):
                      "avg_launch_ms": raster_ms, "peak_source": peak_src},
         "matvec_roofline": {"achieved": matvec_achieved, "peak": peak, "unit": "GB/s",
                             "frac": matvec_achieved / peak, "bytes_per_matvec": bytes_["matvec"],
-                            "roofline_matvecs_per_s": peak * 1e9 / bytes_["matvec"] * world,
+                            "roofline_matvecs_per_s": peak * 1e9 / bytes_["matvec"] * units,
                             **{k: bytes_[k] for k in ("G_v_sum", "E_v_sum", "S_v_sum")}},
         "breakdown_ms": {"tangents": prof["tangents_ms"] / n, "raster": raster_ms, "chain": prof["chain_ms"] / n},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * 14 * args.gaussians,
