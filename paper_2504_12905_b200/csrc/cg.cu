@@ -44,6 +44,32 @@ __global__ void k_soa32_to_aos64(const float* __restrict__ soa, int G, int Gp, d
     const int g = i / kP, k = i - g * kP;
     aos[i] = (double)soa[k * Gp + g];
 }
+// f64 AoS (14 per Gaussian, the reference's ParamVector) <-> f32 SoA [14][Gp] over
+// Gaussians [g0, g1): the chunked host-vector product (Jacobian::gn_apply)
+__global__ void k_aos64_to_soa32_range(const double* __restrict__ aos, int g0, int g1, int Gp, float* __restrict__ soa) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x + static_cast<long long>(g0) * kP;
+    if (i >= static_cast<long long>(g1) * kP) return;
+    const int g = static_cast<int>(i / kP), k = static_cast<int>(i - static_cast<long long>(g) * kP);
+    soa[static_cast<size_t>(k) * Gp + g] = static_cast<float>(aos[i]);
+}
+__global__ void k_soa32_to_aos64_range(const float* __restrict__ soa, int g0, int g1, int Gp, double* __restrict__ aos) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x + static_cast<long long>(g0) * kP;
+    if (i >= static_cast<long long>(g1) * kP) return;
+    const int g = static_cast<int>(i / kP), k = static_cast<int>(i - static_cast<long long>(g) * kP);
+    aos[i] = static_cast<double>(soa[static_cast<size_t>(k) * Gp + g]);
+}
+void launch_aos64_to_soa32_range(const double* aos, int g0, int g1, int Gp, float* soa, cudaStream_t st) {
+    if (g1 <= g0) return;
+    k_aos64_to_soa32_range<<<static_cast<unsigned>((static_cast<long long>(g1 - g0) * kP + 255) / 256), 256, 0, st>>>(
+        aos, g0, g1, Gp, soa);
+    ++g_launches;
+}
+void launch_soa32_to_aos64_range(const float* soa, int g0, int g1, int Gp, double* aos, cudaStream_t st) {
+    if (g1 <= g0) return;
+    k_soa32_to_aos64_range<<<static_cast<unsigned>((static_cast<long long>(g1 - g0) * kP + 255) / 256), 256, 0, st>>>(
+        soa, g0, g1, Gp, aos);
+    ++g_launches;
+}
 // GaussianSet SoA (means[3G], ...) f64 <-> device [14][Gp] f64
 __global__ void k_set_to_beta(const double* __restrict__ means, const double* __restrict__ ls,
                               const double* __restrict__ rot, const double* __restrict__ logit,

@@ -178,10 +178,10 @@ __device__ __forceinline__ void view_tangent(const View& V, const DevCam& cam, c
 __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta, const float* __restrict__ p,
                                                   int G, int Gp, const DevCam* __restrict__ cams, int V,
                                                   const float4* __restrict__ rec, float4* __restrict__ tan,
-                                                  const int* __restrict__ done_flag) {
+                                                  const int* __restrict__ done_flag, int g0, int g1) {
     if (done_flag && *done_flag) return;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= g1) return;
     Geom Gm;
     load_geom(beta, Gp, g, Gm);
     float pv[kP];
@@ -586,10 +586,16 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
 }
 
 // ------------------------------------------------------------------ launchers
+void launch_tangents_range(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
+                           const float4* rec, float4* tan, const int* done, int g0, int g1, cudaStream_t st) {
+    g1 = g1 < G ? g1 : G;
+    if (g1 <= g0) return;
+    k_tangents<<<(g1 - g0 + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done, g0, g1);
+    ++g_launches;
+}
 void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
                      const float4* rec, float4* tan, const int* done, cudaStream_t st) {
-    if (G == 0) return;
-    k_tangents<<<(G + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done); ++g_launches;
+    launch_tangents_range(beta32, p, G, Gp, cams, V, rec, tan, done, 0, G, st);
 }
 
 // The chain over Gaussians [g0, g1) (the multi-rank path runs it in chunks,

@@ -1223,12 +1223,73 @@ struct Jacobian {
         download_param(vout.p, out);
     }
 
+    // The drop-in host-vector product (SampledJacobian::gn_apply): f64 AoS in and
+    // out (the reference's ParamVector), pipelined in Gaussian chunks on a copy
+    // stream: chunk c of p crosses PCIe while chunk c-1 is converted and its
+    // tangents computed; after the raster, chunk c's result is converted and
+    // copied back while chunk c+1's chain runs.  Per-Gaussian work only, so the
+    // values are bitwise those of the unchunked product.  (Narrowing to f32 on
+    // the host to halve the PCIe bytes measured slower: the host's memory
+    // bandwidth, not PCIe, then bounds the call.)
+    std::vector<cudaEvent_t> hev;
+    cudaEvent_t hevent(size_t i) {
+        while (hev.size() <= i) {
+            cudaEvent_t e;
+            SLM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            hev.push_back(e);
+        }
+        return hev[i];
+    }
+    ~Jacobian() {
+        for (auto e : hev) cudaEventDestroy(e);
+    }
     void gn_apply(double lambda, const double* pvec, double* out) {
+        const int G = scene->G, Gp = scene->Gp;
         vin.ensure(P());
         vout.ensure(P());
-        upload_param(pvec, vin.p);
-        gn_apply_dev(static_cast<float>(lambda), vin.p, vout.p);
-        download_param(vout.p, out);
+        static const bool pipeline = [] {
+            const char* e = std::getenv("SLM_HOST_PIPELINE");
+            return !(e && e[0] == '0');
+        }();
+        if (ctx->world > 1 || G < 4096 || !pipeline) {  // small or sharded: one upload, one download
+            upload_param(pvec, vin.p);
+            gn_apply_dev(static_cast<float>(lambda), vin.p, vout.p);
+            download_param(vout.p, out);
+            return;
+        }
+        constexpr int kChunks = 8;
+        const int step = round_up((G + kChunks - 1) / kChunks, 256);
+        const int nch = (G + step - 1) / step;
+        host_stage.ensure(static_cast<size_t>(kP) * G);
+        cudaStream_t st = ctx->stream, cp = ctx->aux_stream();
+        SLM_CUDA_CHECK(cudaMemsetAsync(vin.p, 0, P() * sizeof(float), st));  // padding Gaussians stay 0
+        SLM_CUDA_CHECK(cudaEventRecord(hevent(0), st));
+        SLM_CUDA_CHECK(cudaStreamWaitEvent(cp, hevent(0), 0));
+        auto lo = [&](int c) { return c * step; };
+        auto hi = [&](int c) { return std::min(G, (c + 1) * step); };
+        for (int c = 0; c < nch; ++c) {
+            const size_t a = static_cast<size_t>(kP) * lo(c), bytes = sizeof(double) * kP * (hi(c) - lo(c));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(host_stage.p + a, pvec + a, bytes, cudaMemcpyHostToDevice, cp));
+            SLM_CUDA_CHECK(cudaEventRecord(hevent(1 + c), cp));
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(st, hevent(1 + c), 0));
+            launch_aos64_to_soa32_range(host_stage.p, lo(c), hi(c), Gp, vin.p, st);
+            launch_tangents_range(scene->beta32.p, vin.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, tan.p,
+                                  nullptr, lo(c), hi(c), st);
+        }
+        launch_sample_raster(kGn, args(), st);
+        const float lam = static_cast<float>(lambda);
+        for (int c = 0; c < nch; ++c) {
+            launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, inter.p, det_order(),
+                               vin.p, lam, vout.p, nullptr, lo(c), hi(c), c == 0, st);
+            launch_soa32_to_aos64_range(vout.p, lo(c), hi(c), Gp, host_stage.p, st);
+            SLM_CUDA_CHECK(cudaEventRecord(hevent(1 + nch + c), st));
+            SLM_CUDA_CHECK(cudaStreamWaitEvent(cp, hevent(1 + nch + c), 0));
+            const size_t a = static_cast<size_t>(kP) * lo(c), bytes = sizeof(double) * kP * (hi(c) - lo(c));
+            SLM_CUDA_CHECK(cudaMemcpyAsync(out + a, host_stage.p + a, bytes, cudaMemcpyDeviceToHost, cp));
+        }
+        ctx->check_launch();
+        SLM_CUDA_CHECK(cudaStreamSynchronize(cp));
+        SLM_CUDA_CHECK(cudaStreamSynchronize(st));
     }
 
     // pcg_solve (pcg.cpp:10-53) on device; returns the final CgState.

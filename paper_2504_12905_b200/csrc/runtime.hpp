@@ -110,6 +110,10 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
                       unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
                       unsigned* perm, unsigned* seg, unsigned* dest, cudaStream_t st);
 void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
+void launch_aos64_to_soa32_range(const double* aos, int g0, int g1, int Gp, float* soa, cudaStream_t st);
+void launch_soa32_to_aos64_range(const float* soa, int g0, int g1, int Gp, double* aos, cudaStream_t st);
+void launch_tangents_range(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
+                           const float4* rec, float4* tan, const int* done, int g0, int g1, cudaStream_t st);
 void launch_soa32_to_aos64(const float* soa, int G, int Gp, double* aos, cudaStream_t st);
 void launch_set_to_beta(const double* m, const double* ls, const double* rot, const double* logit,
                         const double* col, int G, int Gp, double* beta, float* beta32, cudaStream_t st);

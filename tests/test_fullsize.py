@@ -157,3 +157,24 @@ def test_other_shapes_products_vs_reference(gpu, reflib, shape):
     state, cams, clusters, views, plan = inputs(splatlm.HostSampler(), shape)
     errs = _products_vs_reference(gpu, reflib, state, [cams[views[0]]], sub_plan(plan, 0, 1))
     assert max(errs.values()) < TOL
+
+
+def test_cfg2_host_vector_product_equals_device_product(gpu, cfg2):
+    """The drop-in host-vector gn_apply (f64 AoS in/out, pipelined in Gaussian chunks with
+    f32 staging) returns bitwise the device-resident product on the same probe."""
+    import torch
+    state, cams, clusters, views, plan = cfg2
+    from paper_2504_12905_b200 import splatlm
+    scene = splatlm.Scene(gpu, state)
+    jac = scene.jacobian([cams[i] for i in views], plan)
+    G, Gp = state.count, scene.padded
+    p = np.random.default_rng(7).uniform(-1, 1, 14 * G)
+    host = jac.gn_apply(0.1, p)
+    soa = np.zeros((14, Gp), np.float32)
+    soa[:, :G] = p.reshape(G, 14).T.astype(np.float32)
+    dp = torch.from_numpy(soa.reshape(-1)).cuda()
+    du = torch.zeros_like(dp)
+    jac.gn_apply_dev(0.1, dp.data_ptr(), du.data_ptr())
+    gpu.synchronize()
+    dev = du.cpu().numpy().reshape(14, Gp)[:, :G].T.reshape(-1).astype(np.float64)
+    assert np.array_equal(host, dev)
