@@ -70,6 +70,13 @@ int slm_context_set_comm_chunks(slm_context* ctx, int chunks);
  * test_solver.cpp:268-286).  off: float red.global.add (order follows the
  * scheduler).  Takes effect at the next plan (Jacobian / lm_step). */
 int slm_context_set_deterministic(slm_context* ctx, int on);
+/* The sampled pixels of this context's last lm_step (this rank's views), in plan
+ * order (view, tile, draw) -- drawn on the host (uniform) or on the device from
+ * the FP64 render's CDFs (weighted) -- with their residual weights
+ * (1/q)/N_total as the products use them (f32, mse loss).  Call with capacity 0
+ * to get n. */
+int slm_context_last_samples(slm_context* ctx, int64_t capacity, int64_t* n, int32_t* px, int32_t* py,
+                             float* weight);
 /* Counters of this context's last lm_step: [views, sum_v G_v, tile-list entries,
  * samples, pixels, PCG iterations, sum_v G_v and entries after the update]. */
 int slm_context_step_stats(slm_context* ctx, int64_t out[8]);

@@ -2188,6 +2188,31 @@ int slm_context_set_stream(slm_context* ctx, void* stream) {
         c.own_stream = false;
     });
 }
+int slm_context_last_samples(slm_context* ctx, int64_t capacity, int64_t* n, int32_t* px, int32_t* py,
+                              float* weight) {
+    return guarded([&] {
+        Context& c = ctx->impl;
+        if (!c.step) throw std::invalid_argument("no lm_step has run on this context");
+        Samples& S = c.step->jac.samples;
+        const long long total = S.total;
+        *n = total;
+        if (capacity < total || total == 0) return;
+        std::vector<int> pix(total), orig(total);
+        std::vector<float> w(3 * total);
+        c.activate();
+        SLM_CUDA_CHECK(cudaMemcpyAsync(pix.data(), S.spix.p, sizeof(int) * total, cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(orig.data(), S.sorig.p, sizeof(int) * total, cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(w.data(), S.sw.p, sizeof(float) * 3 * total, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        for (long long k = 0; k < total; ++k) {  // group order -> plan order (view, tile, draw)
+            const long long o = orig[k];
+            if (o < 0 || o >= total) throw std::runtime_error("sample order out of range");
+            px[o] = pix[k] & 0xffff;
+            py[o] = pix[k] >> 16;
+            weight[o] = w[3 * k];
+        }
+    });
+}
 int slm_context_step_stats(slm_context* ctx, int64_t out[8]) {
     return guarded([&] {
         for (int i = 0; i < 8; ++i) out[i] = ctx->impl.step_stats[i];
@@ -2477,8 +2502,10 @@ int slm_estimate_loss(const slm_camera* cams, const slm_plan* plan, const double
             return;
         }
         double pixels = 0.0;
-        for (int v = 0; v < plan->n_views; ++v)
+        for (int v = 0; v < plan->n_views; ++v) {
+            if (!fields || !fields[v]) throw std::invalid_argument("one residual field per plan view required");
             pixels += static_cast<double>(cams[plan->view_camera[v]].width) * cams[plan->view_camera[v]].height;
+        }
         double acc = 0.0;
         for (int v = 0; v < plan->n_views; ++v) {
             const int w = cams[plan->view_camera[v]].width;

@@ -48,6 +48,7 @@ _SIGS = {
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
     "slm_context_set_deterministic": (C.c_int, [_vp, C.c_int]),
     "slm_context_step_stats": (C.c_int, [_vp, _i64p]),
+    "slm_context_last_samples": (C.c_int, [_vp, C.c_int64, _i64p, _i32p, _i32p, _f32p]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
     "slm_context_timing_names": (C.c_char_p, [_vp]),
     "slm_launch_count": (C.c_longlong, []),
@@ -269,6 +270,10 @@ class HostSampler:
         return plan
 
     def estimate_loss(self, cams, plan: SamplePlan, residual_fields) -> float:
+        """sampling::estimate_loss (sample_plan.cpp:199-222): residual_fields[v] is the
+        H x W x 3 residual image of plan view v."""
+        if len(residual_fields) != plan.n_views:
+            raise ValueError("one residual field per plan view required")
         arr = (_f64p * plan.n_views)()
         keep = [np.ascontiguousarray(f, np.float64) for f in residual_fields]
         for i, f in enumerate(keep):
@@ -352,6 +357,16 @@ class Lib(HostSampler):
         """Fixed-order J^T / diag accumulation (default on): bitwise reproducible
         products, PCG solutions and LM trajectories.  Off: float atomics."""
         self._check(self.dll.slm_context_set_deterministic(self.ctx, 1 if on else 0))
+
+    def last_samples(self):
+        """(px, py, weight) of the last lm_step's sampled pixels in plan order."""
+        n = C.c_int64()
+        self._check(self.dll.slm_context_last_samples(self.ctx, 0, C.byref(n), None, None, None))
+        px, py = np.zeros(n.value, np.int32), np.zeros(n.value, np.int32)
+        w = np.zeros(n.value, np.float32)
+        self._check(self.dll.slm_context_last_samples(self.ctx, n.value, C.byref(n), i32ptr(px), i32ptr(py),
+                                                      f32ptr(w)))
+        return px, py, w
 
     def step_stats(self) -> dict:
         """Counters of the last lm_step on this context (views, sum G_v, entries,

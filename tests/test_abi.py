@@ -163,3 +163,29 @@ def test_summary_json_layout_matches_reference():
         ref = _golden_bytes(f"{case}_summary.json").decode()
         assert _json_dump(json.loads(ref)) == ref
         assert _golden_bytes(f"{case}_metrics.csv").decode().splitlines()[0] == METRICS_CSV_HEADER
+
+
+def test_estimate_loss_matches_reference(host, port):
+    """sampling::estimate_loss (sample_plan.cpp:199-222): the library's host version is
+    bitwise the reference's (same summation order) on uniform and weighted plans, and on
+    the exhaustive plan it equals the MSE (test_sampling.cpp:171-174)."""
+    import oracle
+    from oracle.cpu_bind import ref
+    libs = [port] + ([ref()] if oracle.have_ref() else [])
+    rng = np.random.default_rng(12)
+    cams = [tcam(40, 3.0), tcam(32, 2.5), tcam(48, 3.0)]
+    fields = [rng.normal(0, 0.3, (c.height, c.width, 3)) for c in cams]
+    plans = [host.build_sample_plan(cams, 32, 0, host.rng(7)), host.exhaustive_plan(cams)]
+    aux = [(rng.random((c.height, c.width, 3)), rng.integers(0, 9, (c.height, c.width)).astype(np.int32),
+            rng.random((c.height, c.width, 3))) for c in cams]
+    plans.append(host.build_sample_plan(cams, 32, 1, host.rng(8), aux=aux))
+    plans.append(host.build_sample_plan(cams, 16, 2, host.rng(9), 16, aux=aux))
+    for plan in plans:
+        mine = host.estimate_loss(cams, plan, fields)
+        for lib in libs:
+            assert mine == lib.estimate_loss(cams, plan, fields), lib.kind
+    pixels = sum(c.width * c.height for c in cams)
+    mse = sum(float(np.sum(f ** 2)) for f in fields) / (3 * pixels)
+    assert host.estimate_loss(cams, plans[1], fields) == pytest.approx(mse, rel=1e-12)
+    with pytest.raises(ValueError):
+        host.estimate_loss(cams, plans[0], fields[:2])

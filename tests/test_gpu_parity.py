@@ -684,3 +684,55 @@ def test_train_run_wall_clock_column(gpu, tmp_path):
         f = row.split(",")
         assert len(f) == 8 and f[1] and len(f[1].split(".")[1]) == 3 and f[5] == f[6] == f[7] == ""
     assert rows[-1].split(",")[3]  # the last iteration is always evaluated
+
+
+# ----------------------------------------------------------------- §8f rows: exact weighted draws, weights API
+@pytest.mark.parametrize("dist", [1, 2])
+def test_weighted_sample_sets_bit_exact_vs_reference(gpu, reflib, dist):
+    """kResidual / kGaussianCount (sample_plan.cpp:127-165): the device builds each tile's
+    density and CDF from the FP64 render (k_render_exact) and picks with the host's
+    uniforms; the reference builds them from its own render_full.  Two LM steps: the
+    picked pixels of every sample equal the reference's plan, weights to f32 rounding."""
+    gt, tc, ti, _, _ = reflib.toy_scene(20, 8, 1, 64, 20214)
+    rg, rr = gpu.rng(3), reflib.rng(3)
+    st = gpu.random_init(60, [-1, -1, -1], [1, 1, 1], rg)
+    assert st == reflib.random_init(60, [-1, -1, -1], [1, 1, 1], rr)
+    td = gpu.train_data(tc, list(ti))
+    td.rebuild_clusters(8, 5)
+    clusters = td.clusters()
+    cfg = LmConfig(pcg_iters_initial=4, samples_per_tile=32, dist=dist)
+    for it in range(2):
+        batch = reflib.sample_view_batch(clusters, rr)
+        aux = []
+        for v in batch:
+            img, _, cn = reflib.render_full(st, tc[v])
+            aux.append((img, cn, np.asarray(ti[v], np.float64)))
+        plan = reflib.build_sample_plan([tc[v] for v in batch], 32, dist, rr, 32, aux=aux)
+        rep = gpu.lm_step(st, td, cfg, it, rg)
+        assert rep.batch == batch
+        px, py, w = gpu.last_samples()
+        assert np.array_equal(px, plan.px) and np.array_equal(py, plan.py)
+        want = (plan.weight / plan.total_samples()).astype(np.float32)
+        assert np.max(np.abs(w - want) / want) <= 1e-6
+        assert rg() == rr()  # same RNG position (one uniform per draw)
+        rg, rr = gpu.rng(100 + it), reflib.rng(100 + it)
+
+
+def test_set_residual_weights_vs_reference(gpu, reflib):
+    """SampledJacobian::set_residual_weights (jacobian.cpp:121-125): custom per-residual
+    weights round-trip through residual_weights() and change jtj_diag / gn_apply like
+    the reference's; a wrong length raises std::invalid_argument (ValueError)."""
+    d = golden("jacobian")
+    st = g_set(d, "jx")
+    cams = g_cams(d["jx_cams"])
+    plan = g_plan(d, "jx")
+    jg, jr = gpu.jacobian(st, cams, plan), reflib.jacobian(st, cams, plan)
+    w = np.random.default_rng(4).uniform(0.1, 3.0, jg.residual_dim()) * jg.residual_weights()
+    jg.set_residual_weights(w)
+    jr.set_residual_weights(w)
+    assert np.array_equal(jg.residual_weights(), w)
+    p = np.random.default_rng(5).uniform(-1, 1, jg.param_dim())
+    assert norm_rel(jg.gn_apply(0.1, p), jr.gn_apply(0.1, p)) < TOL
+    assert norm_rel(jg.jtj_diag(), jr.jtj_diag()) < TOL
+    with pytest.raises(ValueError):
+        jg.set_residual_weights(w[:-1])
