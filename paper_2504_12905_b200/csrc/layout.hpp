@@ -157,6 +157,7 @@ struct TileSortBuffers {
     unsigned *v32a, *v32b, *k32a, *k32b, *count;
     unsigned *t32a, *t32b, *t32va, *t32vb;
     unsigned *hist, *part;
+    unsigned long long* runs;  // long equal-depth runs queued by k_fix_runs: [count, (start, len) ...]
 };
 
 struct CgState {

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
     const int* __restrict__ tile_offsets, const int* __restrict__ entries,
     const float4* __restrict__ rec, int Gp, const float* __restrict__ gt,
     float* __restrict__ image, float* __restrict__ trans, int* __restrict__ contrib,
-    int* __restrict__ last_out, double* __restrict__ sse_tile) {
+    int* __restrict__ last_out, double* __restrict__ sse_tile, unsigned long long* __restrict__ stats) {
     __shared__ float4 s_rec[kRenderStage][3];
     __shared__ float4 s_box[kRenderStage];
     __shared__ double s_red[kRenderThreads / 32];
@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
             qyy[i] = 1e30f;
         }
     }
+    unsigned long long st_iter = 0, st_box = 0, st_live = 0, st_blend = 0, st_stage = 0;
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
+        st_stage += min(kRenderStage, n - start);
         for (int j = threadIdx.x; j < kRenderStage && start + j < n; j += kRenderThreads) {
             const float4* r = rec + 3 * (vbase + entries[b + start + j]);
             const float4 r0 = r[0], r1 = r[1], r2 = r[2];
@@ -129,7 +131,12 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
         const int m = min(kRenderStage, n - start);
         for (int k = 0; k < m && live; ++k) {
             const float4 bx = s_box[k];
+            if (stats) ++st_iter;
             if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
+            if (stats) {
+                ++st_box;
+                st_live += __popc(live);
+            }
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column
@@ -164,6 +171,7 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
                 C2[i] = __fmaf_rn(w, q2.y, C2[i]);
                 T[i] = tt;
                 ++cnt[i];
+                if (stats) ++st_blend;
             }
         }
     }
@@ -185,6 +193,14 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
                              d2 = (double)C2[i] - (double)gp[2];
                 sq += d0 * d0 + d1 * d1 + d2 * d2;
             }
+        }
+    }
+    if (stats) {  // diagnostic counters (slm_debug_render_stats): per thread, summed per warp
+        unsigned long long v[5] = {st_iter, st_box, st_live, st_blend, st_stage};
+        for (int q = 0; q < 5; ++q) {
+            unsigned long long x = v[q];
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) == 0) atomicAdd(stats + q, x);
         }
     }
     if (sse_tile) {
@@ -1187,10 +1203,11 @@ void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, 
 // ------------------------------------------------------------------ launchers
 void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,
-                   float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st) {
+                   float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st,
+                   unsigned long long* stats) {
     if (n_tiles == 0) return;
     k_render<<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
-                                      trans, contrib, last, sse_tile); ++g_launches;
+                                      trans, contrib, last, sse_tile, stats); ++g_launches;
 }
 
 void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile,

@@ -449,7 +449,7 @@ struct Batch {
     std::vector<int> valid_count;  // G_v per view (counted by k_prepare)
     long long max_list = 0;        // longest tile list of the batch
     // radix tile-list construction scratch (sort.cu)
-    DevBuf<unsigned long long> rk64a, rk64b, and_or;
+    DevBuf<unsigned long long> rk64a, rk64b, and_or, rruns;
     DevBuf<unsigned> rv32a, rv32b, rk32a, rk32b, rcount, rt32a, rt32b, rt32va, rt32vb, rhist, rpart;
 
     bool offsets_pending = false;
@@ -555,8 +555,9 @@ struct Batch {
         const long long hmax = radix_hist_size(std::max<long long>(nvg, ne));
         rhist.ensure(hmax);
         rpart.ensure(scan_scratch(std::max<long long>(hmax, nvg)));
+        rruns.ensure(1 + 2 * (nvg / 33 + 1));
         TileSortBuffers tb{rk64a.p, rk64b.p, rv32a.p, rv32b.p, rk32a.p, rk32b.p, rcount.p,
-                           rt32a.p, rt32b.p, rt32va.p, rt32vb.p, rhist.p, rpart.p};
+                           rt32a.p, rt32b.p, rt32va.p, rt32vb.p, rhist.p, rpart.p, rruns.p};
         build_tile_lists(keys.p, rect.p, cams.p, G, Gp, V, n_tiles, n_entries, hao[0], hao[1], tb, entries.p,
                          tile_offsets.p, st);
         ctx->check_launch();
@@ -2451,6 +2452,29 @@ int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* 
     });
 }
 
+int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uint64_t* out) {
+    return guarded([&] {  // k_render work counters: [entry iterations (per thread), past the box test,
+                          //  live pixel-entry gate evaluations, blends, staged entries (per thread)]
+        Context* c = s->impl.ctx;
+        c->activate();
+        Batch b(c);
+        b.prepare(s->impl, std::vector<slm_camera>(cams, cams + n_cams));
+        b.image.ensure(3 * std::max<long long>(b.n_pix, 1));
+        b.trans.ensure(std::max<long long>(b.n_pix, 1));
+        b.contrib.ensure(std::max<long long>(b.n_pix, 1));
+        b.last.ensure(std::max<long long>(b.n_pix, 1));
+        DevBuf<unsigned long long> d;
+        d.ensure(8);
+        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 8 * sizeof(unsigned long long), c->stream));
+        launch_render(b.cams.p, b.tile_view.p, b.n_tiles, b.tile_offsets.p, b.entries.p, b.rec.p, b.Gp, nullptr,
+                      b.image.p, b.trans.p, b.contrib.p, b.last.p, nullptr, c->stream, d.p);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(out, d.p, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        out[5] = static_cast<uint64_t>(b.n_entries);
+        out[6] = static_cast<uint64_t>(b.n_pix);
+        out[7] = static_cast<uint64_t>(b.n_tiles);
+    });
+}
 int slm_scene_render(slm_scene* s, const slm_camera* cam, float* image, float* transmittance, int32_t* contrib) {
     return guarded([&] {
         Context* c = s->impl.ctx;

@@ -83,7 +83,8 @@ void launch_apply_update_f64(double* beta, const double* delta_aos, int G, int G
 void launch_beta_mirror(const double* beta, float* beta32, int n, cudaStream_t st);
 void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,
-                   float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st);
+                   float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st,
+                   unsigned long long* stats = nullptr);
 void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                          const int* entries, const double* rec64, const float4* rec, int Gp, double* image,
                          double* trans, int* contrib, cudaStream_t st);

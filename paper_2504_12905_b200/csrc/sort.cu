@@ -346,8 +346,12 @@ __device__ void heap_sift(unsigned long long* k, unsigned* v, long long root, lo
 
 // Runs are maximal stretches of equal (view, upper key half); after the view
 // pass only same-view keys can share a run (ties across views never matter).
+// Runs of <= 32 are insertion-sorted by the thread at their start; longer ones
+// (near-planar scenes: many depths within 2^-20 of each other) are queued for
+// k_sort_long_runs, one CTA per run, so no run is ever sorted by one thread.
+constexpr int kShortRun = 32;
 __global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __restrict__ vals, long long n,
-                           unsigned Gp) {
+                           unsigned Gp, unsigned long long* __restrict__ runs, long long max_runs) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned hi = static_cast<unsigned>(keys[i] >> 32);
@@ -361,7 +365,15 @@ __global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __re
     if (len <= 1) return;
     unsigned long long* k = keys + i;
     unsigned* v = vals + i;
-    if (len <= 32) {
+    if (len > kShortRun && runs) {
+        const unsigned long long q = atomicAdd(runs, 1ull);
+        if (static_cast<long long>(q) < max_runs) {
+            runs[1 + 2 * q] = static_cast<unsigned long long>(i);
+            runs[2 + 2 * q] = static_cast<unsigned long long>(len);
+            return;
+        }
+    }
+    if (len <= kShortRun) {
         for (long long a = 1; a < len; ++a) {  // insertion sort by (key, index)
             const unsigned long long ka = k[a];
             const unsigned va = v[a];
@@ -385,6 +397,116 @@ __global__ void k_fix_runs(unsigned long long* __restrict__ keys, unsigned* __re
         k[end] = tk;
         v[end] = tv;
         heap_sift(k, v, 0, end);
+    }
+}
+
+// One CTA per long run (grid-stride over the queue): chunks of 2048 (key, index)
+// pairs bitonic-sorted in shared memory, then merged pairwise (merge path,
+// 256 threads) between the run's slice of the keys/vals and the scratch.
+constexpr int kLongChunk = 2048;
+constexpr int kLongThreads = 256;
+
+__device__ __forceinline__ bool kv_less2(unsigned long long ka, unsigned va, unsigned long long kb, unsigned vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+
+__global__ void __launch_bounds__(kLongThreads) k_sort_long_runs(unsigned long long* __restrict__ keys,
+                                                                 unsigned* __restrict__ vals,
+                                                                 const unsigned long long* __restrict__ runs,
+                                                                 long long max_runs,
+                                                                 unsigned long long* __restrict__ tk,
+                                                                 unsigned* __restrict__ tv) {
+    __shared__ unsigned long long sk[kLongChunk];
+    __shared__ unsigned sv[kLongChunk];
+    const long long count = min(static_cast<long long>(runs[0]), max_runs);
+    const int t = threadIdx.x;
+    for (long long r = blockIdx.x; r < count; r += gridDim.x) {
+        const long long s = static_cast<long long>(runs[1 + 2 * r]), L = static_cast<long long>(runs[2 + 2 * r]);
+        unsigned long long* K = keys + s;
+        unsigned* Vv = vals + s;
+        // 1. sorted chunks
+        for (long long c0 = 0; c0 < L; c0 += kLongChunk) {
+            const int m = static_cast<int>(min(static_cast<long long>(kLongChunk), L - c0));
+            for (int i = t; i < kLongChunk; i += kLongThreads) {
+                sk[i] = i < m ? K[c0 + i] : ~0ull;
+                sv[i] = i < m ? Vv[c0 + i] : ~0u;
+            }
+            __syncthreads();
+            for (int k = 2; k <= kLongChunk; k <<= 1)
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = t; i < kLongChunk; i += kLongThreads) {
+                        const int ixj = i ^ j;
+                        if (ixj > i) {
+                            const bool up = (i & k) == 0;
+                            const bool gt = kv_less2(sk[ixj], sv[ixj], sk[i], sv[i]);
+                            if (gt == up) {
+                                const unsigned long long a = sk[i];
+                                const unsigned b = sv[i];
+                                sk[i] = sk[ixj];
+                                sv[i] = sv[ixj];
+                                sk[ixj] = a;
+                                sv[ixj] = b;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int i = t; i < m; i += kLongThreads) {
+                K[c0 + i] = sk[i];
+                Vv[c0 + i] = sv[i];
+            }
+            __syncthreads();
+        }
+        // 2. merge passes, ping-ponging between the run and the scratch
+        unsigned long long *srck = K, *dstk = tk + s;
+        unsigned *srcv = Vv, *dstv = tv + s;
+        for (long long w = kLongChunk; w < L; w <<= 1) {
+            for (long long a = 0; a < L; a += 2 * w) {
+                const long long na = min(w, L - a), nb = max(0ll, min(w, L - a - w));
+                const long long total = na + nb;
+                const unsigned long long* Ak = srck + a;
+                const unsigned* Av = srcv + a;
+                const unsigned long long* Bk = srck + a + na;
+                const unsigned* Bv = srcv + a + na;
+                // this thread's output range [d0, d1) and its merge-path split points
+                const long long d0 = total * t / kLongThreads, d1 = total * (t + 1) / kLongThreads;
+                auto split = [&](long long d) {  // A elements among the first d outputs
+                    long long lo = max(0ll, d - nb), hi = min(d, na);
+                    while (lo < hi) {
+                        const long long mid = (lo + hi) >> 1;
+                        if (kv_less2(Ak[mid], Av[mid], Bk[d - mid - 1], Bv[d - mid - 1])) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    return lo;
+                };
+                long long ia = split(d0), ib = d0 - ia;
+                for (long long d = d0; d < d1; ++d) {
+                    const bool takeA = ib >= nb || (ia < na && kv_less2(Ak[ia], Av[ia], Bk[ib], Bv[ib]));
+                    if (takeA) {
+                        dstk[a + d] = Ak[ia];
+                        dstv[a + d] = Av[ia];
+                        ++ia;
+                    } else {
+                        dstk[a + d] = Bk[ib];
+                        dstv[a + d] = Bv[ib];
+                        ++ib;
+                    }
+                }
+            }
+            __syncthreads();
+            unsigned long long* x = srck;
+            srck = dstk;
+            dstk = x;
+            unsigned* y = srcv;
+            srcv = dstv;
+            dstv = y;
+        }
+        if (srck != K)
+            for (long long i = t; i < L; i += kLongThreads) {
+                K[i] = srck[i];
+                Vv[i] = srcv[i];
+            }
+        __syncthreads();
     }
 }
 
@@ -507,7 +629,12 @@ void build_tile_lists(const unsigned long long* keys, const short4* rect, const 
         }
     }
     if (vary & 0xFFFFFFFFull) {
-        k_fix_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ka, va, n, static_cast<unsigned>(Gp));
+        const long long max_runs = n / (kShortRun + 1) + 1;
+        cudaMemsetAsync(b.runs, 0, sizeof(unsigned long long), st);
+        k_fix_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(ka, va, n, static_cast<unsigned>(Gp), b.runs,
+                                                                           max_runs);
+        ++g_launches;
+        k_sort_long_runs<<<148, kLongThreads, 0, st>>>(ka, va, b.runs, max_runs, kb, vb);
         ++g_launches;
     }
     // 2. emit (tile, index) pairs in (view, depth, index) order

@@ -420,18 +420,22 @@ def test_cfg0_psnr_curve_matches_reference(gpu):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("spread", [0.0, 1e-12, 1e-9, 1e-7])
-def test_tile_lists_bit_exact_near_equal_depths(gpu, spread):
+@pytest.mark.parametrize("spread,n,levels", [(0.0, 300, 5), (1e-12, 300, 5), (1e-9, 300, 5), (1e-7, 300, 5),
+                                             (1e-12, 300, 0), (1e-10, 6000, 0), (1e-11, 20000, 0), (1e-8, 20000, 9)])
+def test_tile_lists_bit_exact_near_equal_depths(gpu, spread, n, levels):
     """Depth ties and near-ties (equal upper 32 key bits, distinct doubles): the
-    radix tile-list construction sorts the upper halves, then fixes up runs; the
-    order must still be the reference's (depth, index) order, bit for bit."""
+    radix tile-list construction sorts the upper halves, then fixes up runs -- short
+    ones per thread, long ones (a near-planar scene: runs of thousands) per CTA
+    (bitonic chunks + merge path); the order must still be the reference's
+    (depth, index) order, bit for bit."""
     from oracle.cpu_bind import port
 
     rng = np.random.default_rng(11)
-    n = 300
     g = GaussianSet.zeros(n)
+    # levels > 0: that many distinct depths (exact ties); 0: n distinct depths within `spread`
+    dz = spread * (rng.integers(0, levels, n) if levels else rng.uniform(0.0, 1.0, n))
     g.means = np.column_stack([rng.uniform(-0.6, 0.6, n), rng.uniform(-0.6, 0.6, n),
-                               np.full(n, 0.25) + spread * rng.integers(0, 5, n)]).reshape(-1)
+                               np.full(n, 0.25) + dz]).reshape(-1)
     g.log_scales = np.full(3 * n, math.log(0.2))
     g.rotations = np.tile([1.0, 0.0, 0.0, 0.0], n)
     g.opacity_logits = rng.uniform(-0.5, 1.0, n)
