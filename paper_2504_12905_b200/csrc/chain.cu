@@ -80,10 +80,10 @@ struct View {  // per-view projection part
     float ca, cb, cc;
 };
 
-// The conic comes from the FP64 preparation (k_prepare's record, scaled by
-// log2(e)), so only t, J, r0, r1 and Sigma r are recomputed here.
-__device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, const float4 r0rec,
-                                          const float4 r1rec, View& V) {
+// The conic comes from the FP64 preparation (k_prepare's conic view
+// {A, B, C, opacity}, scaled by log2(e)), so only t, J, r0, r1 and Sigma r are
+// recomputed here.
+__device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, const float4 cn, View& V) {
     const float W[9] = {(float)cam.R[0], (float)cam.R[1], (float)cam.R[2], (float)cam.R[3], (float)cam.R[4],
                         (float)cam.R[5], (float)cam.R[6], (float)cam.R[7], (float)cam.R[8]};
     const float fx = (float)cam.fx, fy = (float)cam.fy;
@@ -103,9 +103,9 @@ __device__ __forceinline__ void load_view(const Geom& G, const DevCam& cam, cons
         V.Sr1[i] = G.Sig[3 * i] * V.r1[0] + G.Sig[3 * i + 1] * V.r1[1] + G.Sig[3 * i + 2] * V.r1[2];
     }
     constexpr float kLn2f = 0.69314718055994530942f;
-    V.ca = -2.0f * kLn2f * r0rec.z;
-    V.cb = -kLn2f * r0rec.w;
-    V.cc = -2.0f * kLn2f * r1rec.x;
+    V.ca = -2.0f * kLn2f * cn.x;
+    V.cb = -kLn2f * cn.y;
+    V.cc = -2.0f * kLn2f * cn.z;
 }
 
 // dSigma (full 3x3) along (dlog_scale, dquat) — forward mode of covariance_3d.
@@ -177,7 +177,7 @@ __device__ __forceinline__ void view_tangent(const View& V, const DevCam& cam, c
 // ------------------------------------------------------------------ K8
 __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta, const float* __restrict__ p,
                                                   int G, int Gp, const DevCam* __restrict__ cams, int V,
-                                                  const float4* __restrict__ rec, float4* __restrict__ tan,
+                                                  const float4* __restrict__ conic, float4* __restrict__ tan,
                                                   const int* __restrict__ done_flag, int g0, int g1) {
     if (done_flag && *done_flag) return;
     const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -190,23 +190,16 @@ __global__ void __launch_bounds__(128) k_tangents(const float* __restrict__ beta
     dsigma(Gm, pv + 3, pv + 6, dS);
     const float dop = Gm.o * (1.0f - Gm.o) * pv[10];
     const float dr = Gm.dcol[0] * pv[11], dg = Gm.dcol[1] * pv[12], db = Gm.dcol[2] * pv[13];
-    float4 nr0, nr1;  // next view's record (first 32 B: mean, conic, opacity), prefetched
-    if (V > 0) {
-        nr0 = __ldg(rec + 3 * static_cast<size_t>(g));
-        nr1 = __ldg(rec + 3 * static_cast<size_t>(g) + 1);
-    }
+    float4 nc;  // next view's conic view {A, B, C, opacity}, prefetched
+    if (V > 0) nc = __ldg(conic + static_cast<size_t>(g));
     for (int v = 0; v < V; ++v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        const float4 q0 = nr0, q1 = nr1;
-        if (v + 1 < V) {
-            const size_t ng = vg + Gp;
-            nr0 = __ldg(rec + 3 * ng);
-            nr1 = __ldg(rec + 3 * ng + 1);
-        }
-        if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
+        const float4 cn = nc;
+        if (v + 1 < V) nc = __ldg(conic + vg + Gp);
+        if (cn.w == 0.0f) continue;  // invalid (view, Gaussian): zero opacity
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, q0, q1, Vw);
+        load_view(Gm, cam, cn, Vw);
         float o5[5];
         view_tangent(Vw, cam, pv, dS, o5);
         // pre-combined so the raster's d(power) is 5 FMAs in (dx, dy):
@@ -349,7 +342,7 @@ __global__ void __launch_bounds__(256) k_det_reduce(const unsigned* __restrict__
 template <int MODE>
 __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
-                                               const float4* __restrict__ rec, float* __restrict__ inter,
+                                               const float4* __restrict__ conic, float* __restrict__ inter,
                                                DetOrder D, const float* __restrict__ p, float lambda,
                                                float* __restrict__ out, const int* __restrict__ done_flag, int g0,
                                                int g1) {
@@ -363,11 +356,10 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     // Software pipeline: view v+1's record and intermediate are loaded
     // (unconditionally; invalid pairs hold zeros) while view v is processed.
     constexpr bool DET = MODE == 1;
-    float4 nr0, nr1, ni0, ni1, ni2;
+    float4 nc, ni0, ni1, ni2;
     auto fetch = [&](int v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        nr0 = __ldg(rec + 3 * vg);
-        nr1 = __ldg(rec + 3 * vg + 1);
+        nc = __ldg(conic + vg);
         if (!DET) {
             const float4* ip = reinterpret_cast<const float4*>(inter + vg * kRec);
             ni0 = ip[0];
@@ -390,9 +382,9 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
             i1 = acc[1];
             i2 = acc[2];
         }
-        const float4 q0 = nr0, q1 = nr1;
+        const float4 cn = nc;
         if (v + 1 < V) fetch(v + 1);
-        if (q1.y == 0.0f) continue;  // invalid (view, Gaussian): zero record
+        if (cn.w == 0.0f) continue;  // invalid (view, Gaussian): zero opacity
         if (MODE == 0) {
             float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
             ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -406,7 +398,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
         gc2 += i2.x;
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, q0, q1, Vw);
+        load_view(Gm, cam, cn, Vw);
         const float ca = Vw.ca, cb = Vw.cb, cc = Vw.cc;
         // conic -> cov2d (a, b, c): adjoint of d conic = -C dA C
         const float ga = -(gca * ca * ca + gcb * ca * cb + gcc * cb * cb);
@@ -490,7 +482,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
 template <int MODE>
 __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
-                                                       const float4* __restrict__ rec,
+                                                       const float4* __restrict__ conic,
                                                        float* __restrict__ diagacc, DetOrder D,
                                                        float* __restrict__ out) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -503,12 +495,10 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
     const float zero3[3] = {0, 0, 0};
     // software pipeline: next view's record and accumulators load during this view
     constexpr bool DET = MODE == 1;
-    float4 nr0, nr1, nr2, na[5];
+    float4 nc, na[5];
     auto fetch = [&](int v) {
         const size_t vg = static_cast<size_t>(v) * Gp + g;
-        nr0 = __ldg(rec + 3 * vg);
-        nr1 = __ldg(rec + 3 * vg + 1);
-        nr2 = __ldg(rec + 3 * vg + 2);
+        nc = __ldg(conic + vg);
         if (!DET) {
             const float4* a4 = reinterpret_cast<const float4*>(diagacc + vg * kDiagRec);
             for (int q4 = 0; q4 < 5; ++q4) na[q4] = a4[q4];
@@ -524,7 +514,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
             if (v + 1 < V) sn = det_seg(D, vg + Gp);
             det_sum<kDetDiagRec / 4, 5>(D, sg, na);
         }
-        const float4 q0 = nr0, q1 = nr1, q2 = nr2;
+        const float4 cn = nc;
         float acc[20];
         for (int q4 = 0; q4 < 5; ++q4) {
             acc[4 * q4] = na[q4].x;
@@ -533,7 +523,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
             acc[4 * q4 + 3] = na[q4].w;
         }
         if (v + 1 < V) fetch(v + 1);
-        if (q2.y == 0.0f) continue;
+        if (cn.w == 0.0f) continue;  // invalid (view, Gaussian)
         if (MODE == 0) {
             float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
             for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -548,7 +538,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
             }
         const DevCam& cam = cams[v];
         View Vw;
-        load_view(Gm, cam, q0, q1, Vw);
+        load_view(Gm, cam, cn, Vw);
         // the 10 geometry probes, unrolled so every array index is static (the
         // 3 log-scale + 4 quaternion dSigma are recomputed per view rather than
         // kept as a 63-float array in local memory)
@@ -587,30 +577,30 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
 
 // ------------------------------------------------------------------ launchers
 void launch_tangents_range(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
-                           const float4* rec, float4* tan, const int* done, int g0, int g1, cudaStream_t st) {
+                           const float4* conic, float4* tan, const int* done, int g0, int g1, cudaStream_t st) {
     g1 = g1 < G ? g1 : G;
     if (g1 <= g0) return;
-    k_tangents<<<(g1 - g0 + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, rec, tan, done, g0, g1);
+    k_tangents<<<(g1 - g0 + 127) / 128, 128, 0, st>>>(beta32, p, G, Gp, cams, V, conic, tan, done, g0, g1);
     ++g_launches;
 }
 void launch_tangents(const float* beta32, const float* p, int G, int Gp, const DevCam* cams, int V,
-                     const float4* rec, float4* tan, const int* done, cudaStream_t st) {
-    launch_tangents_range(beta32, p, G, Gp, cams, V, rec, tan, done, 0, G, st);
+                     const float4* conic, float4* tan, const int* done, cudaStream_t st) {
+    launch_tangents_range(beta32, p, G, Gp, cams, V, conic, tan, done, 0, G, st);
 }
 
 // The chain over Gaussians [g0, g1) (the multi-rank path runs it in chunks,
 // each chunk's allreduce overlapping the next chunk); `reduce`: run the
 // record-parallel k_det_reduce first (deterministic path 0, all keys at once).
-void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* conic,
                         float* inter, const DetOrder& det, const float* p, float lambda, float* out,
                         const int* done, int g0, int g1, bool reduce, cudaStream_t st) {
     g1 = g1 < G ? g1 : G;
     if (g1 <= g0) return;
     const unsigned nb = (g1 - g0 + 127) / 128;
     if (!det.partial) {
-        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
     } else if (det.fused) {
-        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
     } else {
         if (reduce) {
             const long long nk = static_cast<long long>(V) * Gp;
@@ -618,31 +608,31 @@ void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, 
                 det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(inter));
             ++g_launches;
         }
-        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
     }
     ++g_launches;
 }
 
-void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* conic,
                   float* inter, const DetOrder& det, const float* p, float lambda, float* out, const int* done,
                   cudaStream_t st) {
-    launch_chain_range(beta32, G, Gp, cams, V, rec, inter, det, p, lambda, out, done, 0, G, true, st);
+    launch_chain_range(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, 0, G, true, st);
 }
 
-void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* rec,
+void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* conic,
                           float* diagacc, const DetOrder& det, float* out, cudaStream_t st) {
     if (G == 0) return;
     const unsigned nb = (G + 127) / 128;
     if (!det.partial) {
-        k_diag_finalize<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+        k_diag_finalize<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     } else if (det.fused) {
-        k_diag_finalize<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+        k_diag_finalize<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     } else {
         const long long nk = static_cast<long long>(V) * Gp;
         k_det_reduce<5, kDetDiagRec / 4, kDiagRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
             det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(diagacc));
         ++g_launches;
-        k_diag_finalize<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, rec, diagacc, det, out);
+        k_diag_finalize<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     }
     ++g_launches;
 }

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
                                                  const DevCam* __restrict__ cams, int V, float4* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys, short4* __restrict__ rect,
                                                  unsigned long long* __restrict__ n_entries, int* __restrict__ err,
-                                                 double* __restrict__ rec64) {
+                                                 double* __restrict__ rec64, float4* __restrict__ conic) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long area = 0ull;  // this Gaussian's tile-list entries over the views
     if (g < G) {
@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         R64[4] = p.valid ? p.cc : 0.0;
         R64[5] = p.valid ? p.o : 0.0;
         if (!p.valid) {
+            conic[vg] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[0] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[1] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[2] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         R[0] = make_float4((float)p.mx, (float)p.my, (float)(-0.5 * p.ca * kLog2e), (float)(-p.cb * kLog2e));
         R[1] = make_float4((float)(-0.5 * p.cc * kLog2e), (float)p.o, (float)p.col[0], (float)p.col[1]);
         R[2] = make_float4((float)p.col[2], 1.0f, 0.f, 0.f);  // .y = valid marker
+        conic[vg] = make_float4(R[0].z, R[0].w, R[1].x, R[1].y);  // the linearisation kernels' 16-B view
         // tile rect (rasterizer.cpp:29-36)
         int x0 = (int)floor((p.mx - p.radius) / kTile);
         int x1 = (int)floor((p.mx + p.radius) / kTile);
@@ -251,9 +253,9 @@ __global__ void k_beta_mirror(const double* __restrict__ beta, float* __restrict
 // ------------------------------------------------------------------ host launchers
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
                     unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err,
-                    double* rec64, cudaStream_t st) {
+                    double* rec64, float4* conic, cudaStream_t st) {
     if (G == 0 || V == 0) return;
-    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, n_entries, err, rec64);
+    k_prepare<<<(G + 127) / 128, 128, 0, st>>>(beta, G, Gp, cams, V, rec, keys, rect, n_entries, err, rec64, conic);
     ++g_launches;
 }
 

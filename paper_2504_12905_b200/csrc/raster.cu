@@ -70,7 +70,11 @@ __device__ __forceinline__ float4 alpha_box(float4 r0, float4 r1) {
     return make_float4(r0.x - hx, r0.x + hx, r0.y - hy, r0.y + hy);
 }
 
-__global__ void __launch_bounds__(kRenderThreads, 16) k_render(
+#ifndef SLM_RENDER_MINB
+#define SLM_RENDER_MINB 16
+#endif
+template <bool STATS>
+__global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
     const int* __restrict__ tile_offsets, const int* __restrict__ entries,
     const float4* __restrict__ rec, int Gp, const float* __restrict__ gt,
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
     unsigned long long st_iter = 0, st_box = 0, st_live = 0, st_blend = 0, st_stage = 0;
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
-        st_stage += min(kRenderStage, n - start);
+        if (STATS) st_stage += min(kRenderStage, n - start);
         for (int j = threadIdx.x; j < kRenderStage && start + j < n; j += kRenderThreads) {
             const float4* r = rec + 3 * (vbase + entries[b + start + j]);
             const float4 r0 = r[0], r1 = r[1], r2 = r[2];
@@ -131,9 +135,9 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
         const int m = min(kRenderStage, n - start);
         for (int k = 0; k < m && live; ++k) {
             const float4 bx = s_box[k];
-            if (stats) ++st_iter;
+            if (STATS) ++st_iter;
             if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
-            if (stats) {
+            if (STATS) {
                 ++st_box;
                 st_live += __popc(live);
             }
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
                 C2[i] = __fmaf_rn(w, q2.y, C2[i]);
                 T[i] = tt;
                 ++cnt[i];
-                if (stats) ++st_blend;
+                if (STATS) ++st_blend;
             }
         }
     }
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(kRenderThreads, 16) k_render(
             }
         }
     }
-    if (stats) {  // diagnostic counters (slm_debug_render_stats): per thread, summed per warp
+    if (STATS) {  // diagnostic counters (slm_debug_render_stats): per thread, summed per warp
         unsigned long long v[5] = {st_iter, st_box, st_live, st_blend, st_stage};
         for (int q = 0; q < 5; ++q) {
             unsigned long long x = v[q];
@@ -1206,8 +1210,13 @@ void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const 
                    float* trans, int* contrib, int* last, double* sse_tile, cudaStream_t st,
                    unsigned long long* stats) {
     if (n_tiles == 0) return;
-    k_render<<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
-                                      trans, contrib, last, sse_tile, stats); ++g_launches;
+    if (stats)
+        k_render<true><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
+                                                           trans, contrib, last, sse_tile, stats);
+    else
+        k_render<false><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt,
+                                                            image, trans, contrib, last, sse_tile, nullptr);
+    ++g_launches;
 }
 
 void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile,

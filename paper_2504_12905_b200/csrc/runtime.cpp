@@ -434,6 +434,7 @@ struct Batch {
     DevBuf<long long> total;
     DevBuf<float4> rec;
     DevBuf<double> rec64;  // FP64 [mx, my, a, b, c, o] per (view, Gaussian): exact blend decisions
+    DevBuf<float4> conic;  // {A, B, C, opacity} per (view, Gaussian): the linearisation kernels' 16-B view
     DevBuf<unsigned long long> keys;
     DevBuf<short4> rect;
     DevBuf<float> image, trans, gt;
@@ -508,6 +509,7 @@ struct Batch {
         const size_t VG = static_cast<size_t>(V) * Gp;
         rec.ensure(3 * VG);
         rec64.ensure(6 * VG);
+        conic.ensure(VG);
         keys.ensure(VG);
         rect.ensure(VG);
         tile_offsets.ensure(n_tiles + 1);
@@ -518,7 +520,7 @@ struct Batch {
         // K1 + the entry total (sum of tile-rect areas); the per-tile offsets come
         // out of the sorted tile ids (build_tile_lists), so no per-tile atomics
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p,
-                       reinterpret_cast<unsigned long long*>(total.p), err.p, rec64.p, st);
+                       reinterpret_cast<unsigned long long*>(total.p), err.p, rec64.p, conic.p, st);
         // depth-sort keys in index order + the AND/OR of the valid keys (which
         // key bytes need a radix pass)
         const long long nvg = static_cast<long long>(V) * Gp;
@@ -1038,7 +1040,7 @@ struct Jacobian {
     }
     // out = sum_v chain_v^T inter_v (+ lambda p): the J^T chain of the last J^T pass
     void chain(const float* p, float lambda, float* out, const int* done = nullptr) {
-        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+        launch_chain(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->conic.p, inter.p,
                      det_order(), p, lambda, out, done, ctx->stream);
     }
 
@@ -1083,7 +1085,7 @@ struct Jacobian {
         std::array<cudaEvent_t, 4> ev{};
         const bool prof = ctx->prof;
         if (prof) ctx->prof_record(ev, 0);
-        launch_tangents(scene->beta32.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+        launch_tangents(scene->beta32.p, dp, scene->G, scene->Gp, batch->cams.p, batch->V, batch->conic.p,
                         tan.p, done, st);
         if (prof) ctx->prof_record(ev, 1);
         SampleArgs a = args();
@@ -1103,7 +1105,7 @@ struct Jacobian {
             int c = 0;
             for (int g0 = 0; g0 < G; g0 += step, ++c) {
                 const int g1 = std::min(G, g0 + step);
-                launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, inter.p,
+                launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->conic.p, inter.p,
                                    det_order(), pp, lambda, dout, done, g0, g1, c == 0, st);
                 SLM_CUDA_CHECK(cudaEventRecord(ctx->chunk_event(c), st));
                 SLM_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->chunk_event(c), 0));
@@ -1168,7 +1170,7 @@ struct Jacobian {
         d.dest = samples.dest.p;
         launch_diag_raster(d, ctx->stream);
         launch_diag_finalize(scene->beta32.p, scene->G, scene->Gp, batch->cams.p, batch->V,
-                             batch->rec.p, diagacc.p, det_order(), dout, ctx->stream);
+                             batch->conic.p, diagacc.p, det_order(), dout, ctx->stream);
         ctx->check_launch();
     }
 
@@ -1192,7 +1194,7 @@ struct Jacobian {
         vin.ensure(P());
         res_out.ensure(std::max<long long>(rdim, 1));
         upload_param(v, vin.p);
-        launch_tangents(scene->beta32.p, vin.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->rec.p,
+        launch_tangents(scene->beta32.p, vin.p, scene->G, scene->Gp, batch->cams.p, batch->V, batch->conic.p,
                         tan.p, nullptr, ctx->stream);
         SampleArgs a = args();
         a.out_res = res_out.p;
@@ -1274,13 +1276,13 @@ struct Jacobian {
             SLM_CUDA_CHECK(cudaEventRecord(hevent(1 + c), cp));
             SLM_CUDA_CHECK(cudaStreamWaitEvent(st, hevent(1 + c), 0));
             launch_aos64_to_soa32_range(host_stage.p, lo(c), hi(c), Gp, vin.p, st);
-            launch_tangents_range(scene->beta32.p, vin.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, tan.p,
+            launch_tangents_range(scene->beta32.p, vin.p, G, Gp, batch->cams.p, batch->V, batch->conic.p, tan.p,
                                   nullptr, lo(c), hi(c), st);
         }
         launch_sample_raster(kGn, args(), st);
         const float lam = static_cast<float>(lambda);
         for (int c = 0; c < nch; ++c) {
-            launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->rec.p, inter.p, det_order(),
+            launch_chain_range(scene->beta32.p, G, Gp, batch->cams.p, batch->V, batch->conic.p, inter.p, det_order(),
                                vin.p, lam, vout.p, nullptr, lo(c), hi(c), c == 0, st);
             launch_soa32_to_aos64_range(vout.p, lo(c), hi(c), Gp, host_stage.p, st);
             SLM_CUDA_CHECK(cudaEventRecord(hevent(1 + nch + c), st));

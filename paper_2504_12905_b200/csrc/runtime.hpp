@@ -68,7 +68,7 @@ struct DevBuf {
 // ---- launchers (defined in the .cu files)
 void launch_prepare(const double* beta, int G, int Gp, const DevCam* cams, int V, float4* rec,
                     unsigned long long* keys, short4* rect, unsigned long long* n_entries, int* err,
-                    double* rec64, cudaStream_t st);
+                    double* rec64, float4* conic, cudaStream_t st);
 void launch_depth_init(const unsigned long long* keys, const short4* rect, int G, int Gp, int V,
                        unsigned long long* kout, unsigned* vout, unsigned long long* and_or, cudaStream_t st);
 void build_tile_lists(const unsigned long long* keys, const short4* rect, const DevCam* cams, int G, int Gp, int V,

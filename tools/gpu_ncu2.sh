@@ -1,5 +1,8 @@
-# ncu --set full of k_chain (det) and one GN raster launch + launch list of one product
+# ncu --set full (source-level) of one launch of kernel regex $K under profile_matvec.py
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_chain -s 2 -c 1 -f -o gpurun_out/r2_chain python tools/profile_matvec.py > gpurun_out/ncu_r2_chain.log 2>&1
-tail -2 gpurun_out/ncu_r2_chain.log
-ncu -i gpurun_out/r2_chain.ncu-rep --page details --csv > gpurun_out/r2_chain_details.csv 2>&1
+K=${K:-k_sample_raster}; S=${S:-2}; O=${O:-r2_raster}
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 -f -o gpurun_out/$O python tools/profile_matvec.py $ARGS > gpurun_out/ncu_$O.log 2>&1
+tail -1 gpurun_out/ncu_$O.log
+ncu -i gpurun_out/$O.ncu-rep --page source --csv --print-source sass > gpurun_out/${O}_sass.csv 2>/dev/null
+ncu -i gpurun_out/$O.ncu-rep --page raw --csv > gpurun_out/${O}_raw.csv 2>/dev/null
+ls -la gpurun_out/${O}*
