@@ -1013,7 +1013,7 @@ struct Jacobian {
             samples.seg.ensure(nk + 1);
             const long long hs = radix_hist_size(n1);
             samples.dhist.ensure(hs);
-            samples.dpart.ensure(scan_scratch(hs));
+            samples.dpart.ensure(scan_scratch(std::max<long long>(hs, nk)));
             samples.partial.ensure(static_cast<size_t>(kDetDiagRec) * n1);  // J^T and diag records share it
             // summation path (DetOrder::fused): the chain thread sums its own keys when
             // keys carry few records each, else a record-parallel segmented reduction

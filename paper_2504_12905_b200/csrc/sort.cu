@@ -679,6 +679,12 @@ __global__ void __launch_bounds__(128) k_slot_keys(const Group* __restrict__ gro
     }
 }
 
+__global__ void k_count_keys(const unsigned* __restrict__ keys, long long n, long long n_keys,
+                             unsigned* __restrict__ count) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && keys[i] < static_cast<unsigned>(n_keys)) atomicAdd(count + keys[i], 1u);
+}
+
 // seg[k] = first sorted slot with key >= k, k in [0, n_keys]
 __global__ void k_seg_bounds(const unsigned* __restrict__ keys, long long n, long long n_keys,
                              unsigned* __restrict__ seg) {
@@ -723,8 +729,11 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
         std::swap(ka, kb);
         std::swap(va, vb);
     }
-    k_seg_bounds<<<static_cast<unsigned>((n_keys + 1 + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
+    // seg = exclusive scan of the per-key slot counts (integer atomics: exact)
+    cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
+    k_count_keys<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
     ++g_launches;
+    launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
     k_invert_perm<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(perm, n_slots, dest);
     ++g_launches;
 }
