@@ -17,7 +17,7 @@ def main():
     args = bench.parse_args_for(1_000_000)
     L = splatlm.Lib(0)
     state, cams, clusters, batch, plan = bench.host_inputs(L, args, 1)
-    gt = splatlm.Scene(L, bench.gt_scene(args.gaussians // 2))
+    gt = splatlm.Scene(L, bench.gt_scene(args.gaussians // 2, H=L))
     imgs = [gt.render(c)[0] for c in cams]
     del gt
     td = L.train_data(cams, imgs)

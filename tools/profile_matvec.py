@@ -45,13 +45,14 @@ def main():
         jv = jac.jvp(v)
         jac.vjp(jv)
     if a.lm:
-        gt = splatlm.Scene(L, bench.gt_scene(a.gaussians // 2))
+        gt = splatlm.Scene(L, bench.gt_scene(a.gaussians // 2, H=L))
         imgs = [gt.render(c)[0] for c in cams]
         td = L.train_data(cams, imgs)
         td.set_clusters(clusters)
         rng = L.rng(1)
         L.random_init(a.gaussians, [-1, -1, -1], [1, 1, 1], rng)
         scene.lm_step(td, bench.LmConfig(pcg_iters_initial=8, pcg_iters_late=8), 0, rng)
+        L.render_full(state, cams[batch[0]])  # the FP64 drop-in render (k_render_exact)
     L.synchronize()
     print("done", jac.stats())
 

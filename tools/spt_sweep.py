@@ -35,7 +35,7 @@ def main():
     args.views, args.width, args.height = 64, 800, 800
     L = splatlm.Lib(0)
     cams = bench.cameras(args)
-    gt = splatlm.Scene(L, bench.gt_scene(a.gaussians // 2))
+    gt = splatlm.Scene(L, bench.gt_scene(a.gaussians // 2, H=L))
     imgs = [gt.render(c)[0] for c in cams]
     del gt
     td = L.train_data(cams, imgs)

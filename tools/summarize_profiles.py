@@ -28,7 +28,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum",
         "launch__registers_per_thread", "launch__shared_mem_per_block_static", "launch__grid_size",
-        "launch__block_size"]
+        "launch__block_size", "lts__t_sector_hit_rate.pct", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__t_sector_hit_rate.pct"]
 
 
 def launches(path, tag):
@@ -71,6 +72,15 @@ def ncu_full(path, tag):
                     pass
         tot = sum(v for v, _ in stalls) or 1.0
         lines = [f"# {tag}: ncu --set full, `{name}`\n", "| metric | value | unit |", "|---|---|---|"]
+        try:
+            dur = float(r[h.index("gpu__time_duration.sum")].replace(",", ""))
+            dscale = {"ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(
+                u[h.index("gpu__time_duration.sum")], 1e-3)
+            bytes_ = sum(float(r[h.index(k)].replace(",", "")) * SCALE[u[h.index(k)]]
+                         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            lines.append(f"| achieved DRAM GB/s (read+write / duration) | {bytes_ / (dur * dscale) / 1e9:.1f} | GB/s |")
+        except (ValueError, KeyError):
+            pass
         for k in KEYS:
             if k in h:
                 lines.append(f"| {k} | {r[h.index(k)]} | {u[h.index(k)]} |")
