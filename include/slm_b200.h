@@ -114,6 +114,20 @@ int slm_prepare(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam,
 /* render::render_full (rasterizer.cpp:93-95); any output may be NULL. */
 int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* cam, double* image,
                     double* transmittance, int32_t* contrib);
+/* render::render_pixel (rasterizer.hpp:160-165, rasterizer.cpp:52-60): blend_pixel at pixel
+ * centre (px, py) over an explicitly ordered list of prepared splats (render::SplatD,
+ * 10 doubles each: mean2d x, y, conic a, b, c, opacity, colour r, g, b, unused).
+ * out = {r, g, b, transmittance}.  Computed on the device in FP64. */
+int slm_render_pixel(slm_context* ctx, int n, const double* splats, double px, double py, double out[4],
+                     int32_t* contrib);
+/* render::render_with_context (rasterizer.hpp:175, rasterizer.cpp:62-91): the FP64 render
+ * of a camera from caller-prepared splats (layout as slm_render_pixel) and their tile
+ * grid as CSR (offsets[tiles + 1], indices[offsets[tiles]]). */
+int slm_render_splats(slm_context* ctx, const slm_camera* cam, int n_splats, const double* splats,
+                      const int32_t* offsets, const int32_t* indices, double* image, double* transmittance,
+                      int32_t* contrib);
+/* render::residuals (rasterizer.cpp:97-104): out = rendered - truth over n doubles (host). */
+int slm_residuals(const double* rendered, const double* truth, int64_t n, double* out);
 int slm_scene_render(slm_scene* s, const slm_camera* cam, float* image, float* transmittance,
                      int32_t* contrib);
 

@@ -28,6 +28,7 @@
 #include "splatlm/core/types.hpp"
 #include "splatlm/io/dataset.hpp"
 #include "splatlm/metrics/image_metrics.hpp"
+#include "splatlm/render/rasterizer.hpp"
 #include "splatlm/sampling/sample_plan.hpp"
 #include "splatlm/solver/lm.hpp"
 #include "splatlm/solver/pcg.hpp"
@@ -233,6 +234,100 @@ private:
     slm_jacobian* h_ = nullptr;
     int64_t rdim_ = 0, pdim_ = 0;
 };
+
+// The one-shot wrappers (jacobian.hpp:80-87).
+inline std::vector<double> jvp(Device& dev, const GaussianSet& g, std::span<const Camera> cams,
+                               const sampling::SamplePlan& plan, const ParamVector& v) {
+    return SampledJacobian(dev, g, cams, plan).jvp(v);
+}
+inline ParamVector vjp(Device& dev, const GaussianSet& g, std::span<const Camera> cams,
+                       const sampling::SamplePlan& plan, std::span<const double> u) {
+    return SampledJacobian(dev, g, cams, plan).vjp(u);
+}
+inline ParamVector jtj_diag(Device& dev, const GaussianSet& g, std::span<const Camera> cams,
+                            const sampling::SamplePlan& plan) {
+    return SampledJacobian(dev, g, cams, plan).jtj_diag();
+}
+inline ParamVector gn_apply(Device& dev, const GaussianSet& g, std::span<const Camera> cams,
+                            const sampling::SamplePlan& plan, double lambda, const ParamVector& p) {
+    return SampledJacobian(dev, g, cams, plan).gn_apply(lambda, p);
+}
+
+// ---- render:: (rasterizer.hpp:152-180) on the device, FP64 blend decisions
+namespace render {
+
+inline splatlm::render::RenderOutput make_output(int w, int h) {
+    splatlm::render::RenderOutput out;
+    out.image = Image(w, h);
+    out.final_transmittance.assign(static_cast<size_t>(w) * h, 1.0);
+    out.contrib_count.assign(static_cast<size_t>(w) * h, 0);
+    return out;
+}
+
+inline std::vector<double> pack(std::span<const splatlm::render::SplatD> splats) {
+    std::vector<double> d(10 * splats.size(), 0.0);
+    for (size_t i = 0; i < splats.size(); ++i) {
+        const auto& s = splats[i];
+        const double v[10] = {s.mean2d.x, s.mean2d.y, s.conic_a, s.conic_b, s.conic_c, s.opacity,
+                              s.color[0], s.color[1], s.color[2], 0.0};
+        std::copy(v, v + 10, d.begin() + 10 * i);
+    }
+    return d;
+}
+
+// render::render_full (rasterizer.cpp:93-95)
+inline splatlm::render::RenderOutput render_full(Device& dev, const GaussianSet& gaussians, const Camera& cam) {
+    GaussianSet copy = gaussians;
+    slm_gaussians g = to_c(copy);
+    const slm_camera c = to_c(cam);
+    auto out = make_output(cam.width, cam.height);
+    check(slm_render_full(dev.get(), &g, &c, out.image.data.data(), out.final_transmittance.data(),
+                          out.contrib_count.data()));
+    return out;
+}
+
+// render::render_with_context (rasterizer.cpp:62-91): a caller-prepared context
+inline splatlm::render::RenderOutput render_with_context(Device& dev, const splatlm::render::CameraContext& ctx) {
+    const auto d = pack(ctx.splats);
+    std::vector<int32_t> off{0}, idx;
+    for (const auto& l : ctx.grid.lists) {
+        idx.insert(idx.end(), l.begin(), l.end());
+        off.push_back(static_cast<int32_t>(idx.size()));
+    }
+    const slm_camera c = to_c(ctx.cam);
+    auto out = make_output(ctx.cam.width, ctx.cam.height);
+    check(slm_render_splats(dev.get(), &c, static_cast<int>(ctx.splats.size()), d.data(), off.data(), idx.data(),
+                            out.image.data.data(), out.final_transmittance.data(), out.contrib_count.data()));
+    return out;
+}
+
+// render::render_pixel (rasterizer.cpp:52-60)
+inline splatlm::render::PixelResult render_pixel(Device& dev, std::span<const splatlm::render::SplatD> sorted_splats,
+                                                 double px, double py) {
+    const auto d = pack(sorted_splats);
+    double o[4];
+    int32_t cnt = 0;
+    check(slm_render_pixel(dev.get(), static_cast<int>(sorted_splats.size()), d.data(), px, py, o, &cnt));
+    splatlm::render::PixelResult r;
+    r.rgb[0] = o[0];
+    r.rgb[1] = o[1];
+    r.rgb[2] = o[2];
+    r.transmittance = o[3];
+    r.contrib = cnt;
+    return r;
+}
+
+// render::residuals (rasterizer.cpp:97-104)
+inline Image residuals(const Image& rendered, const Image& ground_truth) {
+    if (rendered.width != ground_truth.width || rendered.height != ground_truth.height)
+        throw std::invalid_argument("residuals: image shapes differ");
+    Image out(rendered.width, rendered.height);
+    check(slm_residuals(rendered.data.data(), ground_truth.data.data(), static_cast<int64_t>(out.data.size()),
+                        out.data.data()));
+    return out;
+}
+
+}  // namespace render
 
 // solver::pcg_solve(ApplyFn, b, minv, max_iters) (pcg.hpp:22-23): the vector
 // algebra runs on the device, `apply` on host vectors.

@@ -1204,6 +1204,87 @@ void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, 
     ++g_launches;
 }
 
+// ------------------------------------------------------------------ drop-in render_pixel / render_with_context
+// The reference's blend over caller-prepared splats (render::SplatD, 10 doubles
+// each: mean2d x, y, conic a, b, c, opacity, colour r, g, b, unused): the
+// blend_pixel arithmetic of k_render_exact with f64 colours, so the result is
+// the reference's bit for bit up to exp's last ulp.
+constexpr int kSplatD = 10;
+
+// false: the pixel terminated (this splat not blended)
+__device__ __forceinline__ bool blend_splat_f64(const double* e, double px, double py, double& T, double& C0,
+                                                double& C1, double& C2, int& cnt) {
+    const double dx = __dsub_rn(e[0], px), dy = __dsub_rn(e[1], py);
+    const double power = __dsub_rn(
+        __dmul_rn(-0.5, __dadd_rn(__dmul_rn(__dmul_rn(e[2], dx), dx), __dmul_rn(__dmul_rn(e[4], dy), dy))),
+        __dmul_rn(__dmul_rn(e[3], dx), dy));
+    if (power > 0.0) return true;
+    double alpha = __dmul_rn(e[5], exp(power));
+    if (alpha > kAlphaClampD) alpha = kAlphaClampD;
+    if (alpha < kAlphaSkipD) return true;
+    const double test_t = __dmul_rn(T, __dsub_rn(1.0, alpha));
+    if (test_t < kTFloorD) return false;
+    const double w = __dmul_rn(alpha, T);
+    C0 = __dadd_rn(C0, __dmul_rn(w, e[6]));
+    C1 = __dadd_rn(C1, __dmul_rn(w, e[7]));
+    C2 = __dadd_rn(C2, __dmul_rn(w, e[8]));
+    T = test_t;
+    ++cnt;
+    return true;
+}
+
+// render_with_context (rasterizer.cpp:62-91): one thread per pixel, two
+// 128-pixel halves per tile on blockIdx.x; lists are CSR over the tiles.
+__global__ void __launch_bounds__(128) k_render_splats(int width, int height, int tiles_x, int n_tiles,
+                                                       const int* __restrict__ offsets, const int* __restrict__ list,
+                                                       const double* __restrict__ splats, double* __restrict__ image,
+                                                       double* __restrict__ trans, int* __restrict__ contrib) {
+    const int tile = static_cast<int>(blockIdx.x >> 1);
+    if (tile >= n_tiles) return;
+    const int idx = (blockIdx.x & 1) * blockDim.x + threadIdx.x;
+    const int x = (tile % tiles_x) * kTile + idx % kTile, y = (tile / tiles_x) * kTile + idx / kTile;
+    if (x >= width || y >= height) return;
+    const double px = x + 0.5, py = y + 0.5;
+    double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+    int cnt = 0;
+    for (int k = offsets[tile]; k < offsets[tile + 1]; ++k)
+        if (!blend_splat_f64(splats + static_cast<size_t>(kSplatD) * list[k], px, py, T, C0, C1, C2, cnt)) break;
+    const size_t pix = static_cast<size_t>(y) * width + x;
+    image[3 * pix] = C0;
+    image[3 * pix + 1] = C1;
+    image[3 * pix + 2] = C2;
+    trans[pix] = T;
+    contrib[pix] = cnt;
+}
+
+// render_pixel (rasterizer.cpp:52-60): the blend of one pixel over all splats in order.
+__global__ void k_render_pixel(int n, const double* __restrict__ splats, double px, double py,
+                               double* __restrict__ out, int* __restrict__ contrib) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double T = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+    int cnt = 0;
+    for (int k = 0; k < n; ++k)
+        if (!blend_splat_f64(splats + static_cast<size_t>(kSplatD) * k, px, py, T, C0, C1, C2, cnt)) break;
+    out[0] = C0;
+    out[1] = C1;
+    out[2] = C2;
+    out[3] = T;
+    *contrib = cnt;
+}
+
+void launch_render_splats(int width, int height, int tiles_x, int n_tiles, const int* offsets, const int* list,
+                          const double* splats, double* image, double* trans, int* contrib, cudaStream_t st) {
+    if (n_tiles == 0) return;
+    k_render_splats<<<2u * static_cast<unsigned>(n_tiles), 128, 0, st>>>(width, height, tiles_x, n_tiles, offsets, list,
+                                                                          splats, image, trans, contrib);
+    ++g_launches;
+}
+void launch_render_pixel(int n, const double* splats, double px, double py, double* out, int* contrib,
+                         cudaStream_t st) {
+    k_render_pixel<<<1, 32, 0, st>>>(n, splats, px, py, out, contrib);
+    ++g_launches;
+}
+
 // ------------------------------------------------------------------ launchers
 void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                    const int* entries, const float4* rec, int Gp, const float* gt, float* image,

@@ -2454,6 +2454,65 @@ int slm_render_full(slm_context* ctx, const slm_gaussians* g, const slm_camera* 
     });
 }
 
+int slm_render_pixel(slm_context* ctx, int n, const double* splats, double px, double py, double out[4],
+                     int32_t* contrib) {
+    return guarded([&] {  // render::render_pixel (rasterizer.cpp:52-60)
+        if (n < 0) throw std::invalid_argument("render_pixel: negative splat count");
+        Context& c = ctx->impl;
+        c.activate();
+        DevBuf<double> d, o;
+        DevBuf<int> cn;
+        d.ensure(static_cast<size_t>(std::max(n, 1)) * 10);
+        o.ensure(4);
+        cn.ensure(1);
+        if (n) SLM_CUDA_CHECK(cudaMemcpyAsync(d.p, splats, sizeof(double) * 10 * n, cudaMemcpyHostToDevice, c.stream));
+        launch_render_pixel(n, d.p, px, py, o.p, cn.p, c.stream);
+        c.check_launch();
+        SLM_CUDA_CHECK(cudaMemcpyAsync(out, o.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, cn.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+int slm_render_splats(slm_context* ctx, const slm_camera* cam, int n_splats, const double* splats,
+                      const int32_t* offsets, const int32_t* indices, double* image, double* transmittance,
+                      int32_t* contrib) {
+    return guarded([&] {  // render::render_with_context (rasterizer.cpp:62-91)
+        if (cam->width <= 0 || cam->height <= 0) throw std::invalid_argument("camera size must be positive");
+        Context& c = ctx->impl;
+        c.activate();
+        const int tx = (cam->width + kTile - 1) / kTile, ty = (cam->height + kTile - 1) / kTile, nt = tx * ty;
+        const long long ne = offsets[nt];
+        for (int t = 0; t < nt; ++t)
+            if (offsets[t] > offsets[t + 1]) throw std::invalid_argument("render_with_context: bad tile offsets");
+        for (long long k = 0; k < ne; ++k)
+            if (indices[k] < 0 || indices[k] >= n_splats) throw std::invalid_argument("render_with_context: index");
+        DevBuf<double> d, img, tr;
+        DevBuf<int> off, lst, cn;
+        const size_t np = static_cast<size_t>(cam->width) * cam->height;
+        d.ensure(static_cast<size_t>(std::max(n_splats, 1)) * 10);
+        off.ensure(nt + 1);
+        lst.ensure(std::max<long long>(ne, 1));
+        img.ensure(3 * np);
+        tr.ensure(np);
+        cn.ensure(np);
+        if (n_splats)
+            SLM_CUDA_CHECK(cudaMemcpyAsync(d.p, splats, sizeof(double) * 10 * n_splats, cudaMemcpyHostToDevice, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(off.p, offsets, sizeof(int) * (nt + 1), cudaMemcpyHostToDevice, c.stream));
+        if (ne) SLM_CUDA_CHECK(cudaMemcpyAsync(lst.p, indices, sizeof(int) * ne, cudaMemcpyHostToDevice, c.stream));
+        launch_render_splats(cam->width, cam->height, tx, nt, off.p, lst.p, d.p, img.p, tr.p, cn.p, c.stream);
+        c.check_launch();
+        SLM_CUDA_CHECK(cudaMemcpyAsync(image, img.p, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(transmittance, tr.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(contrib, cn.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    });
+}
+int slm_residuals(const double* rendered, const double* truth, int64_t n, double* out) {
+    return guarded([&] {  // render::residuals (rasterizer.cpp:97-104): elementwise rendered - truth (host)
+        if (n < 0) throw std::invalid_argument("residuals: negative length");
+        for (int64_t i = 0; i < n; ++i) out[i] = rendered[i] - truth[i];
+    });
+}
 int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uint64_t* out) {
     return guarded([&] {  // k_render work counters: [entry iterations (per thread), past the box test,
                           //  live pixel-entry gate evaluations, blends, staged entries (per thread)]

@@ -88,6 +88,10 @@ void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const 
 void launch_render_exact(const DevCam* cams, const int* tile_view, int n_tiles, const int* tile_offsets,
                          const int* entries, const double* rec64, const float4* rec, int Gp, double* image,
                          double* trans, int* contrib, cudaStream_t st);
+void launch_render_splats(int width, int height, int tiles_x, int n_tiles, const int* offsets, const int* list,
+                          const double* splats, double* image, double* trans, int* contrib, cudaStream_t st);
+void launch_render_pixel(int n, const double* splats, double px, double py, double* out, int* contrib,
+                         cudaStream_t st);
 void launch_sse_views(const DevCam* cams, int V, int n_tiles, const double* sse_tile, double* sse_view,
                       cudaStream_t st);
 void launch_sample_raster(int mode, const SampleArgs& a, cudaStream_t st);

@@ -47,6 +47,9 @@ _SIGS = {
     "slm_context_set_stream": (C.c_int, [_vp, _vp]),
     "slm_context_set_timing": (C.c_int, [_vp, C.c_int]),
     "slm_context_set_deterministic": (C.c_int, [_vp, C.c_int]),
+    "slm_render_pixel": (C.c_int, [_vp, C.c_int, _f64p, C.c_double, C.c_double, _f64p, _i32p]),
+    "slm_render_splats": (C.c_int, [_vp, C.c_void_p, C.c_int, _f64p, _i32p, _i32p, _f64p, _f64p, _i32p]),
+    "slm_residuals": (C.c_int, [_f64p, _f64p, C.c_int64, _f64p]),
     "slm_context_step_stats": (C.c_int, [_vp, _i64p]),
     "slm_context_last_samples": (C.c_int, [_vp, C.c_int64, _i64p, _i32p, _i32p, _f32p]),
     "slm_context_timings": (C.c_int, [_vp, _f64p, C.c_int, _i32p]),
@@ -452,6 +455,54 @@ class Lib(HostSampler):
                                          *(f64ptr(out[k]) for k in ("mean2d", "conic", "opacity",
                                                                     "color", "depth", "radius")),
                                          i32ptr(out["valid"])))
+        return out
+
+    @staticmethod
+    def pack_splats(prep: dict) -> np.ndarray:
+        """render::SplatD fields of a prepare() dict as the [n, 10] f64 layout of
+        render_pixel / render_with_context (mean2d, conic, opacity, colour, unused)."""
+        n = prep["opacity"].size
+        d = np.zeros((n, 10))
+        d[:, 0:2] = prep["mean2d"].reshape(n, 2)
+        d[:, 2:5] = prep["conic"].reshape(n, 3)
+        d[:, 5] = prep["opacity"]
+        d[:, 6:9] = prep["color"].reshape(n, 3)
+        return d
+
+    def render_pixel(self, splats, px: float, py: float):
+        """render::render_pixel (rasterizer.cpp:52-60) over an ordered [n, 10] splat array
+        -> (rgb[3], transmittance, contrib)."""
+        d = np.ascontiguousarray(splats, np.float64).reshape(-1, 10)
+        out = np.zeros(4)
+        cnt = C.c_int32()
+        self._check(self.dll.slm_render_pixel(self.ctx, d.shape[0], f64ptr(d), px, py, f64ptr(out), C.byref(cnt)))
+        return out[:3], float(out[3]), cnt.value
+
+    def render_with_context(self, cam: Camera, splats, offsets, indices):
+        """render::render_with_context (rasterizer.cpp:62-91) of prepared splats ([n, 10])
+        and their CSR tile grid -> (image, transmittance, contrib)."""
+        d = np.ascontiguousarray(splats, np.float64).reshape(-1, 10)
+        off = np.ascontiguousarray(offsets, np.int32)
+        idx = np.ascontiguousarray(indices, np.int32)
+        if off.size != cam.tiles_x * cam.tiles_y + 1:
+            raise ValueError("render_with_context: offsets must have tiles + 1 entries")
+        img = np.zeros((cam.height, cam.width, 3))
+        tr = np.zeros((cam.height, cam.width))
+        cn = np.zeros((cam.height, cam.width), np.int32)
+        cc = cam.to_c()
+        self._check(self.dll.slm_render_splats(self.ctx, C.byref(cc), d.shape[0], f64ptr(d), i32ptr(off),
+                                               i32ptr(idx if idx.size else np.zeros(1, np.int32)), f64ptr(img),
+                                               f64ptr(tr), i32ptr(cn)))
+        return img, tr, cn
+
+    def residuals(self, rendered, truth) -> np.ndarray:
+        """render::residuals (rasterizer.cpp:97-104)."""
+        a = np.ascontiguousarray(rendered, np.float64)
+        b = np.ascontiguousarray(truth, np.float64)
+        if a.shape != b.shape:
+            raise ValueError("residuals: image shapes differ")
+        out = np.empty_like(a)
+        self._check(self.dll.slm_residuals(f64ptr(a), f64ptr(b), a.size, f64ptr(out)))
         return out
 
     def render_full(self, g: GaussianSet, cam: Camera):

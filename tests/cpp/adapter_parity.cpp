@@ -4,6 +4,7 @@
 // Built by oracle/Makefile (`make adapter`) against the reference sources;
 // run by tests/test_gpu_parity.py::test_cpp_adapter_drop_in.  Prints one JSON
 // line.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -96,11 +97,52 @@ int main() {
         splatlm_b200::first_order_step(dev, sb, stb, fa, fcfg);
     }
     const bool fo_equal = sta.pack() == stb.pack() && sa.m1 == sb.m1 && sa.m2 == sb.m2 && sa.step == sb.step;
+    // render:: surface: render_full, render_with_context on the reference's own prepared
+    // context, render_pixel over a depth-ordered tile list, residuals
+    const Camera& rc = scene.test.cameras[0];
+    const auto rctx = render::prepare_camera(ref, rc);
+    const auto ra = render::render_with_context(rctx);
+    const auto rb = splatlm_b200::render::render_with_context(dev, rctx);
+    const auto rf = splatlm_b200::render::render_full(dev, ref, rc);
+    bool contrib_equal = ra.contrib_count == rb.contrib_count && ra.contrib_count == rf.contrib_count;
+    double img_diff = 0.0, t_diff = 0.0;
+    for (size_t i = 0; i < ra.image.data.size(); ++i)
+        img_diff = std::max(img_diff, std::abs(ra.image.data[i] - rb.image.data[i]));
+    for (size_t i = 0; i < ra.final_transmittance.size(); ++i)
+        t_diff = std::max(t_diff, std::abs(ra.final_transmittance[i] - rb.final_transmittance[i]));
+    const int tile = static_cast<int>(rctx.grid.lists.size() / 2);
+    std::vector<render::SplatD> ordered;
+    for (int idx : rctx.grid.lists[tile]) ordered.push_back(rctx.splats[idx]);
+    const double ppx = (tile % rctx.grid.tiles_x) * 16 + 7.5, ppy = (tile / rctx.grid.tiles_x) * 16 + 7.5;
+    const auto pa = render::render_pixel(ordered, ppx, ppy);
+    const auto pb = splatlm_b200::render::render_pixel(dev, ordered, ppx, ppy);
+    const double pix_diff = std::max({std::abs(pa.rgb[0] - pb.rgb[0]), std::abs(pa.rgb[1] - pb.rgb[1]),
+                                      std::abs(pa.rgb[2] - pb.rgb[2]), std::abs(pa.transmittance - pb.transmittance)});
+    contrib_equal = contrib_equal && pa.contrib == pb.contrib;
+    const Image truth = io::widen(scene.test.images[0]);
+    const bool resid_equal = render::residuals(ra.image, truth).data == splatlm_b200::render::residuals(ra.image, truth).data;
+    bool resid_throws = false;
+    try {
+        splatlm_b200::render::residuals(ra.image, Image(3, 3));
+    } catch (const std::invalid_argument&) {
+        resid_throws = true;
+    }
+    // one-shot autodiff wrappers (jacobian.hpp:80-87)
+    const auto oa = autodiff::gn_apply(ref, cams, plan, 0.1, p), ob = splatlm_b200::gn_apply(dev, ref, cams, plan, 0.1, p);
+    double onum = 0, oden = 0;
+    for (size_t i = 0; i < oa.size(); ++i) {
+        onum += (oa[i] - ob[i]) * (oa[i] - ob[i]);
+        oden += oa[i] * oa[i];
+    }
     std::printf("{\"batches_equal\": %s, \"rng_equal\": %s, \"worst_loss_rel\": %.3e, \"gn_apply_rel\": %.3e, "
                 "\"split_psnr_diff\": %.3e, \"split_ssim_diff\": %.3e, \"eval_ssim_diff\": %.3e, "
-                "\"eval_mse_rel\": %.3e, \"full_gradient_rel\": %.3e, \"first_order_equal\": %s}\n",
+                "\"eval_mse_rel\": %.3e, \"full_gradient_rel\": %.3e, \"first_order_equal\": %s, "
+                "\"render_contrib_equal\": %s, \"render_image_diff\": %.3e, \"render_t_diff\": %.3e, "
+                "\"render_pixel_diff\": %.3e, \"residuals_equal\": %s, \"one_shot_gn_rel\": %.3e}\n",
                 batches_equal ? "true" : "false", rng_equal ? "true" : "false", worst, std::sqrt(num / den),
                 std::abs(er.psnr - eb.psnr), std::abs(er.ssim - eb.ssim), std::abs(ma.ssim - mb.ssim),
-                std::abs(ma.mse - mb.mse) / ma.mse, std::sqrt(gnum / gden), fo_equal ? "true" : "false");
+                std::abs(ma.mse - mb.mse) / ma.mse, std::sqrt(gnum / gden), fo_equal ? "true" : "false",
+                contrib_equal ? "true" : "false", img_diff, t_diff, pix_diff,
+                (resid_equal && resid_throws) ? "true" : "false", std::sqrt(onum / oden));
     return 0;
 }

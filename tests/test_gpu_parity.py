@@ -386,6 +386,11 @@ def test_cpp_adapter_drop_in(gpu):
     assert r["split_psnr_diff"] < 1e-3 and r["split_ssim_diff"] < 1e-5
     assert r["eval_ssim_diff"] <= 1e-12 and r["eval_mse_rel"] <= 1e-12
     assert r["full_gradient_rel"] < TOL and r["first_order_equal"]
+    # render:: surface (render_full / render_with_context / render_pixel / residuals) and
+    # the one-shot autodiff wrappers through the adapter
+    assert r["render_contrib_equal"] and r["residuals_equal"]
+    assert r["render_image_diff"] < 1e-12 and r["render_t_diff"] < 1e-12 and r["render_pixel_diff"] < 1e-12
+    assert r["one_shot_gn_rel"] < TOL
 
 
 @pytest.mark.gpu
@@ -740,3 +745,31 @@ def test_set_residual_weights_vs_reference(gpu, reflib):
     assert norm_rel(jg.jtj_diag(), jr.jtj_diag()) < TOL
     with pytest.raises(ValueError):
         jg.set_residual_weights(w[:-1])
+
+
+# ----------------------------------------------------------------- render:: surface
+@pytest.mark.parametrize("t", range(4))
+def test_render_with_context_and_pixel_vs_reference(gpu, reflib, t):
+    """render::render_with_context on the reference's own prepared splats and tile grid
+    (prepare_camera, rasterizer.cpp:10-50) equals its render_full: contributor counts
+    exactly, colour and transmittance to 1e-12; render_pixel over one tile's ordered
+    list equals the reference pixel; residuals is rendered - truth."""
+    d = golden("render")
+    g = g_set(d, f"r{t}")
+    cam = g_cams(d[f"r{t}_cam"])[0]
+    prep = reflib.prepare(g, cam)
+    splats = gpu.pack_splats(prep)
+    off, idx = reflib.bin_and_sort(g, cam)
+    img, tr, cn = gpu.render_with_context(cam, splats, off, idx)
+    ri, rt, rc = reflib.render_full(g, cam)
+    assert np.array_equal(cn, rc)
+    assert np.max(np.abs(img - ri)) < 1e-12 and np.max(np.abs(tr - rt)) < 1e-12
+    tile = len(off) // 2
+    order = idx[off[tile]:off[tile + 1]]
+    x0, y0 = (tile % cam.tiles_x) * 16, (tile // cam.tiles_x) * 16
+    x, y = x0 + min(7, cam.width - 1 - x0), y0 + min(7, cam.height - 1 - y0)
+    rgb, T, c = gpu.render_pixel(splats[order], x + 0.5, y + 0.5)
+    assert c == rc[y, x] and abs(T - rt[y, x]) < 1e-12 and np.max(np.abs(rgb - ri[y, x])) < 1e-12
+    assert np.array_equal(gpu.residuals(img, ri), img - ri)
+    with pytest.raises(ValueError):
+        gpu.residuals(img, ri[:1])
