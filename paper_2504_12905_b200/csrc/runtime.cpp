@@ -652,49 +652,68 @@ struct Samples {
     bool device_drawn = false;  // spix / sw written on the device (weighted distributions)
 
     // Host half (no CUDA calls; runs on the sampler thread in lm_step):
-    // group the plan's samples per view by tile in chunks of <= 32.
+    // group the plan's samples per view by tile in chunks of <= 32, and the
+    // per-sample f32 weights (1/q)/N_total (jacobian.cpp:112-116) for the raster.
+    // w1 (optional) receives the f64 weight per sample.  One pass for the
+    // reference's tile-major plans; other orders are stably sorted by tile.
     void group_host(const slm_plan& plan, int view_lo, int view_hi, const std::vector<slm_camera>& cams,
-                    const std::vector<double>& weights3) {
+                    double inv_total, std::vector<double>* w1) {
         device_drawn = false;
         hgroups.clear();
         order.clear();
+        const long long a0 = plan.view_offset[view_lo], n_all = plan.view_offset[view_hi] - a0;
+        hpix.resize(n_all);
+        horig.resize(n_all);
+        hw.resize(3 * n_all);
+        if (w1) w1->resize(n_all);
+        long long k = 0;  // group-order position
+        std::vector<int> idx;
         for (int v = view_lo; v < view_hi; ++v) {
             const slm_camera& c = cams[v - view_lo];
             const int tiles = ((c.width + kTile - 1) / kTile) * ((c.height + kTile - 1) / kTile);
             const long long a = plan.view_offset[v], b = plan.view_offset[v + 1];
-            std::vector<int> idx(b - a);
-            std::iota(idx.begin(), idx.end(), static_cast<int>(a));
             bool sorted = true;
-            for (long long i = 0; i < b - a; ++i) {
-                const int s = idx[i];
+            for (long long s = a; s < b; ++s) {
                 if (plan.px[s] < 0 || plan.px[s] >= c.width || plan.py[s] < 0 || plan.py[s] >= c.height)
                     throw std::invalid_argument("sample pixel outside the camera");
                 if (plan.tile[s] < 0 || plan.tile[s] >= tiles)
                     throw std::invalid_argument("sample tile outside the camera");
-                if (i > 0 && plan.tile[s] < plan.tile[idx[i - 1]]) sorted = false;
+                if (s > a && plan.tile[s] < plan.tile[s - 1]) sorted = false;
             }
-            if (!sorted)  // reference plans are emitted tile-major already
+            const int* ord = nullptr;  // plan index of the view's i-th sample in tile order
+            if (!sorted) {
+                idx.resize(b - a);
+                std::iota(idx.begin(), idx.end(), static_cast<int>(a));
                 std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return plan.tile[x] < plan.tile[y]; });
-            size_t i = 0;
-            while (i < idx.size()) {
-                const int t = plan.tile[idx[i]];
-                size_t j = i;
-                while (j < idx.size() && plan.tile[idx[j]] == t && j - i < 32) ++j;
-                hgroups.push_back(Group{v - view_lo, t, static_cast<int>(order.size()), static_cast<int>(j - i)});
-                for (size_t k = i; k < j; ++k) order.push_back(idx[k]);
+                ord = idx.data();
+            }
+            long long i = 0;
+            const long long n = b - a;
+            while (i < n) {
+                const long long s0 = ord ? ord[i] : a + i;
+                const int t = plan.tile[s0];
+                long long j = i;
+                while (j < n && plan.tile[ord ? ord[j] : a + j] == t && j - i < 32) ++j;
+                hgroups.push_back(Group{v - view_lo, t, static_cast<int>(k), static_cast<int>(j - i)});
+                for (long long q = i; q < j; ++q, ++k) {
+                    const long long s = ord ? ord[q] : a + q;
+                    if (ord) order.push_back(static_cast<int>(s));
+                    hpix[k] = plan.px[s] | (plan.py[s] << 16);
+                    horig[k] = static_cast<int>(s - a0);
+                    const double w = plan.weight[s] * inv_total;
+                    if (w1) (*w1)[s - a0] = w;
+                    const float wf = static_cast<float>(w);
+                    hw[3 * k] = wf;
+                    hw[3 * k + 1] = wf;
+                    hw[3 * k + 2] = wf;
+                }
                 i = j;
             }
         }
-        total = static_cast<long long>(order.size());
-        hpix.resize(order.size());
-        horig.resize(order.size());
-        hw.resize(3 * order.size());
-        const int base = static_cast<int>(plan.view_offset[view_lo]);
-        for (size_t k = 0; k < order.size(); ++k) {
-            const int s = order[k];
-            hpix[k] = plan.px[s] | (plan.py[s] << 16);
-            horig[k] = s - base;
-            for (int c = 0; c < 3; ++c) hw[3 * k + c] = static_cast<float>(weights3[3 * static_cast<size_t>(s - base) + c]);
+        total = k;
+        if (order.empty()) {  // identity (tile-major plans): spelled out for take_host / upload users
+            order.resize(total);
+            std::iota(order.begin(), order.end(), static_cast<int>(a0));
         }
     }
 
@@ -800,10 +819,17 @@ struct Jacobian {
         rdim = 0;
         plan_base = plan.view_offset[lo];
         for (int v = lo; v < hi; ++v) rdim += 3 * (plan.view_offset[v + 1] - plan.view_offset[v]);
-        weights.resize(rdim);
-        for (long long s = plan.view_offset[lo], k = 0; s < plan.view_offset[hi]; ++s, ++k)
-            for (int c = 0; c < 3; ++c) weights[3 * k + c] = plan.weight[s] * inv_total;
-        samples.group_host(plan, lo, hi, cams, weights);
+        weights.clear();  // materialised on demand (residual_weights): lm_step never reads them
+        samples.group_host(plan, lo, hi, cams, inv_total, &w1);
+    }
+    std::vector<double> w1;  // (1/q)/N_total per sample (plan order), all three channels
+    const std::vector<double>& residual_weights() {
+        if (weights.empty() && !w1.empty() && static_cast<long long>(w1.size()) * 3 == rdim) {
+            weights.resize(rdim);
+            for (size_t k = 0; k < w1.size(); ++k)
+                for (int c = 0; c < 3; ++c) weights[3 * k + c] = w1[k];
+        }
+        return weights;
     }
 
     // Weighted residual distributions (sample_plan.cpp:127-165): the host draws
@@ -860,6 +886,7 @@ struct Jacobian {
         rdim = 3 * samples.total;
         plan_base = off_lo;
         weights.clear();  // drawn on the device (lm_step's Jacobian never reads them on the host)
+        w1.clear();
     }
 
     // Host half of full_gradient's exhaustive plan (sample_plan.cpp:173-197)
@@ -877,6 +904,7 @@ struct Jacobian {
         rdim = 3 * samples.total;
         plan_base = 0;
         weights.clear();
+        w1.clear();
     }
 
     // Adopt the host half computed by another (host-only) Jacobian.
@@ -893,6 +921,7 @@ struct Jacobian {
         std::swap(rdim, o.rdim);
         std::swap(plan_base, o.plan_base);
         weights.swap(o.weights);
+        w1.swap(o.w1);
         samples.hgroups.swap(o.samples.hgroups);
         samples.order.swap(o.samples.order);
         samples.hpix.swap(o.samples.hpix);
@@ -1331,6 +1360,37 @@ struct PlanH {
                         view_camera.data(), view_offset.data(), px.data(), py.data(), tile.data(),
                         weight.data()};
     }
+    void clear() {
+        view_camera.clear();
+        view_offset.assign(1, 0);
+        px.clear();
+        py.clear();
+        tile.clear();
+        weight.clear();
+    }
+};
+
+// Plans are recycled (their vectors keep their capacity): a fresh multi-MB
+// allocation per LM step costs page faults on first touch that rival the
+// sampler's own work at configs[0] (524k samples per step).
+std::mutex g_plan_mu;
+std::vector<std::unique_ptr<PlanH>> g_plan_pool;
+static std::unique_ptr<PlanH> acquire_plan() {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_plan_pool.empty()) return std::make_unique<PlanH>();
+    auto p = std::move(g_plan_pool.back());
+    g_plan_pool.pop_back();
+    p->clear();
+    return p;
+}
+static void release_plan(std::unique_ptr<PlanH> p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_plan_pool.size() < 4) g_plan_pool.push_back(std::move(p));
+}
+struct PlanReturn {  // hands a step's plan back to the pool when the step ends
+    std::unique_ptr<PlanH>& p;
+    ~PlanReturn() { release_plan(std::move(p)); }
 };
 
 static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int spt, int dist, int lane,
@@ -1345,7 +1405,7 @@ static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int
         if (dist == SLM_DIST_RESIDUAL && !aux_gt)
             throw std::invalid_argument("residual distribution needs ground-truth images");
     }
-    auto plan = std::make_unique<PlanH>();
+    auto plan = acquire_plan();
     plan->samples_per_tile = spt;
     plan->dist = dist;
     size_t total = 0;
@@ -1388,7 +1448,28 @@ static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int
                         std::uniform_int_distribution<int> d(i, m - 1);
                         std::swap(pool[i], pool[d(rng)]);
                     }
-                    for (int i = 0; i < n; ++i) emit(pool[i], 1.0 / m);
+                    // emit(pool[i], 1.0 / m) with the per-tile constants hoisted: the
+                    // weight is the same double expression for every sample of the tile
+                    const double q = (n / n_total) * (1.0 / m);
+                    const double w = 1.0 / std::max(q, 1e-12);
+                    const size_t at = plan->px.size();
+                    plan->px.resize(at + n);
+                    plan->py.resize(at + n);
+                    plan->tile.resize(at + n);
+                    plan->weight.resize(at + n);
+                    if (rw == kTile) {
+                        for (int i = 0; i < n; ++i) {
+                            plan->px[at + i] = x0 + (pool[i] & (kTile - 1));
+                            plan->py[at + i] = y0 + (pool[i] >> 4);
+                        }
+                    } else {
+                        for (int i = 0; i < n; ++i) {
+                            plan->px[at + i] = x0 + pool[i] % rw;
+                            plan->py[at + i] = y0 + pool[i] / rw;
+                        }
+                    }
+                    std::fill(plan->tile.begin() + at, plan->tile.end(), tile);
+                    std::fill(plan->weight.begin() + at, plan->weight.end(), w);
                     continue;
                 }
                 density.assign(m, 0.0);
@@ -1639,6 +1720,7 @@ struct Speculation {
     Jacobian* hj = nullptr;  // host half only (StepBuffers::spare)
     ~Speculation() {
         if (th.joinable()) th.join();
+        release_plan(std::move(plan));
     }
 };
 
@@ -1927,6 +2009,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     // uniform distribution the plan does not depend on the render, so it runs
     // on a host thread while the GPU prepares and renders the views.
     std::unique_ptr<PlanH> plan;
+    PlanReturn plan_return{plan};
     std::exception_ptr plan_err;
     auto make_plan = [&] {
         try {
@@ -2666,8 +2749,10 @@ int slm_jacobian_gn_apply(slm_jacobian* j, double lambda, const double* p, doubl
     return guarded([&] { j->jac->ctx->activate(); j->jac->gn_apply(lambda, p, out); });
 }
 int slm_jacobian_weights(slm_jacobian* j, double* out) {
-    std::copy(j->jac->weights.begin(), j->jac->weights.end(), out);
-    return SLM_OK;
+    return guarded([&] {
+        const auto& w = j->jac->residual_weights();
+        std::copy(w.begin(), w.end(), out);
+    });
 }
 int slm_jacobian_set_weights(slm_jacobian* j, const double* w) {
     return guarded([&] {
