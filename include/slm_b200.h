@@ -260,7 +260,7 @@ int slm_scene_beta_ptrs(slm_scene* s, double** beta, float** beta32);
 int slm_jacobian_device_ptrs(slm_jacobian* j, void* stream_out[1]);
 /* [views, sum_v G_v (valid view-Gaussian pairs), tile-list entries, samples, warp groups, tiles] */
 int slm_jacobian_stats(slm_jacobian* j, int64_t* out);
-/* Diagnostic: blend-mask density / lane-balance counters (13 values, see
+/* Diagnostic: blend-mask density / lane-balance counters (18 values, see
  * raster.cu k_mask_stats); used by tools/mask_stats.py. */
 int slm_jacobian_mask_stats(slm_jacobian* j, uint64_t* out);
 /* Diagnostic: k_render work counters over the given views (8 values: entry

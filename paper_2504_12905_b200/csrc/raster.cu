@@ -510,6 +510,43 @@ __global__ void __launch_bounds__(32) k_mask_stats(SampleArgs A, unsigned long l
     if (lane == 0)
         for (int i = 0; i < 7; ++i)
             if (s[i]) atomicAdd(st + i, s[i]);
+    // Balance simulations (pair steps per warp): [13] 64-entry windows (max
+    // lane popcount per 64 entries), [14]/[15]/[16] lanes may run ahead of the
+    // oldest unfinished window by 1 / 3 / unlimited windows, [17] two-pair
+    // iterations of the current walk (sum_w ceil(max popc / 2)).
+    unsigned long long x[5] = {0ull, 0ull, 0ull, 0ull, 0ull};
+    for (int w = 0; w < ncw; w += 2) {
+        int p = c.active ? __popc(masks[32 * w + lane]) : 0;
+        if (w + 1 < ncw && c.active) p += __popc(masks[32 * (w + 1) + lane]);
+        x[0] += __reduce_max_sync(0xffffffffu, p);
+    }
+    for (int w = 0; w < ncw; ++w) {
+        const int p = c.active ? __popc(masks[32 * w + lane]) : 0;
+        x[4] += (__reduce_max_sync(0xffffffffu, p) + 1) >> 1;
+    }
+    const int look[3] = {1, 3, 1 << 30};
+    for (int q = 0; q < 3; ++q) {
+        // lane position: the first window it has not finished (ncw = done)
+        int wl = 0, rem = (c.active && ncw > 0) ? __popc(masks[lane]) : 0;
+        unsigned long long steps = 0;
+        while (true) {
+            const int wmin = __reduce_min_sync(0xffffffffu, rem > 0 ? wl : wl + 1);
+            if (wmin >= ncw) break;
+            // advance past exhausted windows (free) within the look-ahead of the oldest
+            while (rem == 0 && wl + 1 < ncw && wl + 1 <= wmin + look[q]) {
+                ++wl;
+                rem = c.active ? __popc(masks[32 * wl + lane]) : 0;
+            }
+            const bool work = rem > 0;
+            if (!__any_sync(0xffffffffu, work)) continue;
+            if (work) --rem;
+            ++steps;
+        }
+        x[1 + q] = steps;
+    }
+    if (lane == 0)
+        for (int i = 0; i < 5; ++i)
+            if (x[i]) atomicAdd(st + 13 + i, x[i]);
 }
 
 void launch_mask_stats(const SampleArgs& a, unsigned long long* st, cudaStream_t stream) {

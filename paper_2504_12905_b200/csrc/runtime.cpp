@@ -2784,10 +2784,10 @@ int slm_jacobian_mask_stats(slm_jacobian* j, uint64_t* out) {
         Jacobian& J = *j->jac;
         J.ctx->activate();
         DevBuf<unsigned long long> d;
-        d.ensure(16);
-        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 16 * sizeof(unsigned long long), J.ctx->stream));
+        d.ensure(18);
+        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 18 * sizeof(unsigned long long), J.ctx->stream));
         launch_mask_stats(J.args(), d.p, J.ctx->stream);
-        SLM_CUDA_CHECK(cudaMemcpyAsync(out, d.p, 13 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, J.ctx->stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(out, d.p, 18 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, J.ctx->stream));
         J.ctx->sync();
     });
 }

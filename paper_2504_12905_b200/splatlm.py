@@ -852,10 +852,11 @@ class Jacobian:
 
     def mask_stats(self) -> dict:
         """Diagnostic counters of the blend masks (raster.cu k_mask_stats)."""
-        out = np.zeros(13, np.int64)
+        out = np.zeros(18, np.int64)
         self.L._check(self.L.dll.slm_jacobian_mask_stats(self.h, i64ptr(out)))
         keys = ["groups", "windows", "pairs", "it_walk", "entries", "it_walk64", "it_col",
-                "rows_le8", "rows_le16", "rows_le20", "rows_le24", "rows_le28", "rows_le32"]
+                "rows_le8", "rows_le16", "rows_le20", "rows_le24", "rows_le28", "rows_le32",
+                "it_win64", "it_ahead1", "it_ahead3", "it_ahead_inf", "it_pair_iters"]
         return dict(zip(keys, (int(x) for x in out)))
 
 
