@@ -263,9 +263,11 @@ int slm_jacobian_stats(slm_jacobian* j, int64_t* out);
 /* Diagnostic: blend-mask density / lane-balance counters (18 values, see
  * raster.cu k_mask_stats); used by tools/mask_stats.py. */
 int slm_jacobian_mask_stats(slm_jacobian* j, uint64_t* out);
-/* Diagnostic: k_render work counters over the given views (8 values: entry
+/* Diagnostic: k_render work counters over the given views (10 values: entry
  * iterations, entries past the warp box test, live pixel-entry gates, blends,
- * staged entries -- per thread -- and the batch's entries, pixels, tiles). */
+ * staged entries -- per thread --, the batch's entries, pixels, tiles, and per
+ * warp the entries past an exact ellipse/half-tile test and the entries some
+ * pixel of the warp blended). */
 int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uint64_t* out);
 
 #ifdef __cplusplus

@@ -70,10 +70,45 @@ __device__ __forceinline__ float4 alpha_box(float4 r0, float4 r1) {
     return make_float4(r0.x - hx, r0.x + hx, r0.y - hy, r0.y + hy);
 }
 
+// Maximum of the (concave) gate polynomial q'(x, y) over the rectangle
+// [x0, x1] x [y0, y1] (tile-centred coordinates): the stationary point when it
+// lies inside, else the best of the four edges (each a 1-D concave quadratic).
+__device__ __forceinline__ float gate_rect_max(const Gate& g, float x0, float x1, float y0, float y1) {
+    const float det = 4.0f * g.g3 * g.g5 - g.g4 * g.g4;
+    if (det > 0.0f) {
+        const float xs = (g.g4 * g.g2 - 2.0f * g.g5 * g.g1) / det, ys = (g.g4 * g.g1 - 2.0f * g.g3 * g.g2) / det;
+        if (xs >= x0 && xs <= x1 && ys >= y0 && ys <= y1)
+            return g.g0 + g.g1 * xs + g.g2 * ys + g.g3 * xs * xs + g.g4 * xs * ys + g.g5 * ys * ys;
+    }
+    float best = -1e30f;
+    auto along_y = [&](float x) {  // x fixed, maximise over y
+        const float a = g.g0 + g.g1 * x + g.g3 * x * x, b = g.g2 + g.g4 * x;
+        const float y = g.g5 < 0.0f ? fminf(fmaxf(-b / (2.0f * g.g5), y0), y1) : (b > 0.0f ? y1 : y0);
+        best = fmaxf(best, a + b * y + g.g5 * y * y);
+    };
+    auto along_x = [&](float y) {
+        const float a = g.g0 + g.g2 * y + g.g5 * y * y, b = g.g1 + g.g4 * y;
+        const float x = g.g3 < 0.0f ? fminf(fmaxf(-b / (2.0f * g.g3), x0), x1) : (b > 0.0f ? x1 : x0);
+        best = fmaxf(best, a + b * x + g.g3 * x * x);
+    };
+    along_y(x0);
+    along_y(x1);
+    along_x(y0);
+    along_x(y1);
+    return best;
+}
+
 #ifndef SLM_RENDER_MINB
 #define SLM_RENDER_MINB 16
 #endif
-template <bool STATS>
+// The 4 pixels of a thread are two packed pairs (rows 0,1 and 2,3 of its
+// column); each entry is blended branch-free: a pixel whose gate fails gets
+// alpha = 0, which leaves T (T (1 - 0) = T) and the colour (fma(0, c, C) = C)
+// bit-identical, so only the rare termination takes a branch, and every
+// packed op (fma/mul/sub .rn.f32x2) rounds each pixel like the scalar
+// blend_pixel arithmetic.  FULL: also write T, contrib and `last` (the
+// drop-in render); the LM step's loss renders need only colour + SSE.
+template <bool STATS, bool FULL>
 __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     const DevCam* __restrict__ cams, const int* __restrict__ tile_view,
     const int* __restrict__ tile_offsets, const int* __restrict__ entries,
@@ -100,25 +135,32 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
 
     const float tcx = (float)(tx * kTile + kTile / 2), tcy = (float)(ty * kTile + kTile / 2);
     const float qx = pxc - tcx, qxx = __fmul_rn(qx, qx);
-    float T[kRenderPix], C0[kRenderPix], C1[kRenderPix], C2[kRenderPix], qy[kRenderPix], qyy[kRenderPix];
-    int cnt[kRenderPix], last[kRenderPix];
+    // pair p holds pixels 2p, 2p+1 (rows y0 + 4p, y0 + 4p + 2)
+    float2 T[2], C0[2], C1[2], C2[2], qy[2], qyy[2];
+    int cnt[4], last[4];
     unsigned live = 0u;  // bit i: pixel i still blending
 #pragma unroll
-    for (int i = 0; i < kRenderPix; ++i) {
-        const int y = y0 + 2 * i;
-        T[i] = 1.0f;
-        C0[i] = C1[i] = C2[i] = 0.0f;
-        cnt[i] = 0;
-        last[i] = n;
-        qy[i] = (float)y + 0.5f - tcy;
-        qyy[i] = __fmul_rn(qy[i], qy[i]);
-        if (x < cam.width && y < cam.height) live |= 1u << i;
-        else {  // a dead pixel's gate is -huge: every pair skips it
-            qy[i] = 0.0f;
-            qyy[i] = 1e30f;
+    for (int p = 0; p < 2; ++p) {
+        T[p] = make_float2(1.0f, 1.0f);
+        C0[p] = C1[p] = C2[p] = make_float2(0.0f, 0.0f);
+        float yv[2], yy[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = 2 * p + h, y = y0 + 2 * i;
+            cnt[i] = 0;
+            last[i] = n;
+            yv[h] = (float)y + 0.5f - tcy;
+            yy[h] = __fmul_rn(yv[h], yv[h]);
+            if (x < cam.width && y < cam.height) live |= 1u << i;
+            else {  // a dead pixel's gate is -huge: every pair skips it
+                yv[h] = 0.0f;
+                yy[h] = 1e30f;
+            }
         }
+        qy[p] = make_float2(yv[0], yv[1]);
+        qyy[p] = make_float2(yy[0], yy[1]);
     }
-    unsigned long long st_iter = 0, st_box = 0, st_live = 0, st_blend = 0, st_stage = 0;
+    unsigned long long st_iter = 0, st_box = 0, st_live = 0, st_blend = 0, st_stage = 0, st_exact = 0, st_useful = 0;
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
         if (STATS) st_stage += min(kRenderStage, n - start);
@@ -137,45 +179,73 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             const float4 bx = s_box[k];
             if (STATS) ++st_iter;
             if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
-            if (STATS) {
-                ++st_box;
-                st_live += __popc(live);
-            }
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column
-            // the gates of the 4 pixels as two packed FMA chains (fma.rn.f32x2 rounds
-            // each lane like __fmaf_rn: the same q' as gate_qy); terminated pixels
-            // carry qyy = 1e30, so they fail the gate without a live test
-            float qv[kRenderPix];
+            // q' of the 4 pixels as two packed FMA chains (fma.rn.f32x2 rounds each
+            // lane like __fmaf_rn: gate_qy's q'); dead pixels carry qyy = 1e30
+            float2 a[2];
+            bool ps[4];
 #pragma unroll
-            for (int i = 0; i < kRenderPix; i += 2) {
-                const float2 qq = ffma2(make_float2(g.g5, g.g5), make_float2(qyy[i], qyy[i + 1]),
-                                        ffma2(make_float2(gx1, gx1), make_float2(qy[i], qy[i + 1]),
-                                              make_float2(gx0, gx0)));
-                qv[i] = qq.x;
-                qv[i + 1] = qq.y;
+            for (int p = 0; p < 2; ++p) {
+                const float2 q = ffma2(make_float2(g.g5, g.g5), qyy[p],
+                                       ffma2(make_float2(gx1, gx1), qy[p], make_float2(gx0, gx0)));
+                const float qv[2] = {q.x, q.y};
+                float av[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    ps[2 * p + h] = !(qv[h] > g.lo || qv[h] < kLog2Skip);  // gate_alpha's tests
+                    float e;
+                    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(qv[h]));
+                    av[h] = ps[2 * p + h] ? fminf(e, 0.99f) : 0.0f;  // clamp (rasterizer.hpp:15)
+                }
+                a[p] = make_float2(av[0], av[1]);
+            }
+            float2 tt[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) tt[p] = fmul2(T[p], fsub2(make_float2(1.0f, 1.0f), a[p]));
+            const bool tm0 = ps[0] && tt[0].x < 1e-4f, tm1 = ps[1] && tt[0].y < 1e-4f;
+            const bool tm2 = ps[2] && tt[1].x < 1e-4f, tm3 = ps[3] && tt[1].y < 1e-4f;
+            if (tm0 || tm1 || tm2 || tm3) {  // termination (rasterizer.hpp:121-122): not blended, the pixel stops
+                const bool tm[4] = {tm0, tm1, tm2, tm3};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (tm[i]) {
+                        ps[i] = false;
+                        live &= ~(1u << i);
+                        if (FULL) last[i] = start + k;
+                    }
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const bool l = tm[2 * p], h = tm[2 * p + 1];
+                    a[p] = make_float2(l ? 0.0f : a[p].x, h ? 0.0f : a[p].y);
+                    tt[p] = make_float2(l ? T[p].x : tt[p].x, h ? T[p].y : tt[p].y);
+                    qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
+                    qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
+                }
             }
 #pragma unroll
-            for (int i = 0; i < kRenderPix; ++i) {
-                float alpha;
-                bool cl;
-                if (!gate_alpha(qv[i], g.lo, alpha, cl)) continue;
-                float tt;
-                if (terminates(T[i], alpha, tt)) {
-                    live &= ~(1u << i);
-                    last[i] = start + k;
-                    qy[i] = 0.0f;
-                    qyy[i] = 1e30f;
-                    continue;
-                }
-                const float w = __fmul_rn(alpha, T[i]);
-                C0[i] = __fmaf_rn(w, q1.w, C0[i]);
-                C1[i] = __fmaf_rn(w, q2.x, C1[i]);
-                C2[i] = __fmaf_rn(w, q2.y, C2[i]);
-                T[i] = tt;
-                ++cnt[i];
-                if (STATS) ++st_blend;
+            for (int p = 0; p < 2; ++p) {
+                const float2 w = fmul2(a[p], T[p]);
+                C0[p] = ffma2(w, make_float2(q1.w, q1.w), C0[p]);
+                C1[p] = ffma2(w, make_float2(q2.x, q2.x), C1[p]);
+                C2[p] = ffma2(w, make_float2(q2.y, q2.y), C2[p]);
+                T[p] = tt[p];
+            }
+            if (FULL) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cnt[i] += ps[i] ? 1 : 0;
+            }
+            if (STATS) {
+                const int nb = (ps[0] ? 1 : 0) + (ps[1] ? 1 : 0) + (ps[2] ? 1 : 0) + (ps[3] ? 1 : 0);
+                ++st_box;
+                st_live += __popc(live | (tm0 ? 1u : 0u) | (tm1 ? 2u : 0u) | (tm2 ? 4u : 0u) | (tm3 ? 8u : 0u));
+                st_blend += nb;
+                const unsigned act = __activemask();
+                const bool leader = (threadIdx.x & 31) == __ffs(act) - 1;  // one count per warp
+                if (leader && gate_rect_max(g, wx0 - tcx, wx1 - tcx, wy0 - tcy, wy1 - tcy) >= kLog2Skip - 0.01f)
+                    ++st_exact;
+                if (__any_sync(act, nb > 0) && leader) ++st_useful;
             }
         }
     }
@@ -183,28 +253,33 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
 #pragma unroll
     for (int i = 0; i < kRenderPix; ++i) {
         const int y = y0 + 2 * i;
+        const float c0 = (i & 1) ? C0[i >> 1].y : C0[i >> 1].x;
+        const float c1 = (i & 1) ? C1[i >> 1].y : C1[i >> 1].x;
+        const float c2 = (i & 1) ? C2[i >> 1].y : C2[i >> 1].x;
         if (x < cam.width && y < cam.height) {
             const size_t pix = cam.pix_base + static_cast<size_t>(y) * cam.width + x;
-            image[3 * pix] = C0[i];
-            image[3 * pix + 1] = C1[i];
-            image[3 * pix + 2] = C2[i];
-            trans[pix] = T[i];
-            contrib[pix] = cnt[i];
-            last_out[pix] = last[i];
+            image[3 * pix] = c0;
+            image[3 * pix + 1] = c1;
+            image[3 * pix + 2] = c2;
+            if (FULL) {
+                trans[pix] = (i & 1) ? T[i >> 1].y : T[i >> 1].x;
+                contrib[pix] = cnt[i];
+                last_out[pix] = last[i];
+            }
             if (gt) {
                 const float* gp = gt + 3 * pix;
-                const double d0 = (double)C0[i] - (double)gp[0], d1 = (double)C1[i] - (double)gp[1],
-                             d2 = (double)C2[i] - (double)gp[2];
+                const double d0 = (double)c0 - (double)gp[0], d1 = (double)c1 - (double)gp[1],
+                             d2 = (double)c2 - (double)gp[2];
                 sq += d0 * d0 + d1 * d1 + d2 * d2;
             }
         }
     }
     if (STATS) {  // diagnostic counters (slm_debug_render_stats): per thread, summed per warp
-        unsigned long long v[5] = {st_iter, st_box, st_live, st_blend, st_stage};
-        for (int q = 0; q < 5; ++q) {
+        unsigned long long v[7] = {st_iter, st_box, st_live, st_blend, st_stage, st_exact, st_useful};
+        for (int q = 0; q < 7; ++q) {
             unsigned long long x = v[q];
             for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            if ((threadIdx.x & 31) == 0) atomicAdd(stats + q, x);
+            if ((threadIdx.x & 31) == 0) atomicAdd(stats + (q < 5 ? q : q + 3), x);
         }
     }
     if (sse_tile) {
@@ -1329,11 +1404,15 @@ void launch_render(const DevCam* cams, const int* tile_view, int n_tiles, const 
                    unsigned long long* stats) {
     if (n_tiles == 0) return;
     if (stats)
-        k_render<true><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt, image,
-                                                           trans, contrib, last, sse_tile, stats);
-    else
-        k_render<false><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt,
-                                                            image, trans, contrib, last, sse_tile, nullptr);
+        k_render<true, true><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt,
+                                                                 image, trans, contrib, last, sse_tile, stats);
+    else if (contrib)
+        k_render<false, true><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp, gt,
+                                                                  image, trans, contrib, last, sse_tile, nullptr);
+    else  // colour + SSE only (the LM step's loss renders)
+        k_render<false, false><<<n_tiles, kRenderThreads, 0, st>>>(cams, tile_view, tile_offsets, entries, rec, Gp,
+                                                                   gt, image, nullptr, nullptr, nullptr, sse_tile,
+                                                                   nullptr);
     ++g_launches;
 }
 

@@ -597,17 +597,21 @@ struct Batch {
 
     // Forward render of every pixel of every view (K6); gt (concatenated f32
     // H*W*3 per view, device) enables the per-view SSE.
-    void render(bool with_gt) {
+    // full: also T, contrib and `last` per pixel (the drop-in render); the
+    // LM step's loss renders and the metrics need only colour (+ SSE).
+    void render(bool with_gt, bool full = true) {
         cudaStream_t st = ctx->stream;
         image.ensure(3 * std::max<long long>(n_pix, 1));
-        trans.ensure(std::max<long long>(n_pix, 1));
-        contrib.ensure(std::max<long long>(n_pix, 1));
-        last.ensure(std::max<long long>(n_pix, 1));
+        if (full) {
+            trans.ensure(std::max<long long>(n_pix, 1));
+            contrib.ensure(std::max<long long>(n_pix, 1));
+            last.ensure(std::max<long long>(n_pix, 1));
+        }
         sse_tile.ensure(std::max(n_tiles, 1));
         sse_view.ensure(std::max(V, 1));
         launch_render(cams.p, tile_view.p, n_tiles, tile_offsets.p, entries.p, rec.p, Gp,
-                      with_gt ? gt.p : nullptr, image.p, trans.p, contrib.p, last.p,
-                      with_gt ? sse_tile.p : nullptr, st);
+                      with_gt ? gt.p : nullptr, image.p, full ? trans.p : nullptr, full ? contrib.p : nullptr,
+                      full ? last.p : nullptr, with_gt ? sse_tile.p : nullptr, st);
         if (with_gt) launch_sse_views(cams.p, V, n_tiles, sse_tile.p, sse_view.p, st);
         ctx->check_launch();
         ctx->mark("render");
@@ -1850,7 +1854,7 @@ static double batch_loss_dev(Scene& s, Train& t, const std::vector<int>& ids, in
         }
         b.prepare(s, cv);
         copy_gt(t, b, chunk);
-        b.render(true);
+        b.render(true, false);
         auto sse = b.view_sse();
         std::vector<double2> ss;
         if (loss == SLM_LOSS_MSE_SSIM) {  // both terms of the FP64 render, like the reference's
@@ -1891,7 +1895,7 @@ static void full_gradient_dev(Scene& s, Train& t, int loss, double ssim_weight, 
         }
         B.prepare(s, cv);
         copy_gt(t, B, ids);
-        B.render(false);
+        B.render(false, false);
         if (loss == SLM_LOSS_MSE_SSIM) batch_ssim(B, true);
         J.init_host_exhaustive(cv, loss == SLM_LOSS_MSE_SSIM ? B.ssim_res.p : nullptr, B.ssim_dc.p,
                                static_cast<float>(ssim_weight), scale);
@@ -2046,7 +2050,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     try {
         B.prepare(s, my_cams);
         copy_gt(t, B, my_ids);
-        B.render(true);
+        B.render(true, false);
     } catch (...) {
         if (sampler.joinable()) sampler.join();
         throw;
@@ -2148,7 +2152,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     ctx->mark("update");
     // loss_after = batch_loss of the updated state (lm.cpp:149-153)
     B.prepare(s, my_cams);
-    B.render(true);
+    B.render(true, false);
     ctx->step_stats[6] = std::accumulate(B.valid_count.begin(), B.valid_count.end(), 0ll);
     ctx->step_stats[7] = B.n_entries;
     double after = 0.0;
@@ -2608,11 +2612,13 @@ int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uin
         b.contrib.ensure(std::max<long long>(b.n_pix, 1));
         b.last.ensure(std::max<long long>(b.n_pix, 1));
         DevBuf<unsigned long long> d;
-        d.ensure(8);
-        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 8 * sizeof(unsigned long long), c->stream));
+        d.ensure(10);
+        SLM_CUDA_CHECK(cudaMemsetAsync(d.p, 0, 10 * sizeof(unsigned long long), c->stream));
         launch_render(b.cams.p, b.tile_view.p, b.n_tiles, b.tile_offsets.p, b.entries.p, b.rec.p, b.Gp, nullptr,
                       b.image.p, b.trans.p, b.contrib.p, b.last.p, nullptr, c->stream, d.p);
         SLM_CUDA_CHECK(cudaMemcpyAsync(out, d.p, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+        // [8] warps past the exact ellipse/half-tile test, [9] warp-entries where some pixel blended
+        SLM_CUDA_CHECK(cudaMemcpyAsync(out + 8, d.p + 8, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
         c->sync();
         out[5] = static_cast<uint64_t>(b.n_entries);
         out[6] = static_cast<uint64_t>(b.n_pix);
@@ -3118,7 +3124,7 @@ int slm_evaluate_split(slm_scene* s, slm_train* split, slm_metric_report* out) {
             Batch b(c);
             b.prepare(s->impl, cv);
             copy_gt(t, b, ids);
-            b.render(false);
+            b.render(false, false);
             std::vector<ImageRef> imgs;
             for (int v = 0; v < b.V; ++v) imgs.push_back({3 * b.hcams[v].pix_base, cv[v].width, cv[v].height});
             const auto sums = image_metrics<float>(c, b.image.p, b.gt.p, imgs);

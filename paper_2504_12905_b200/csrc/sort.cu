@@ -13,10 +13,10 @@
 //   3. a stable sort of the pairs by tile id leaves every tile's entries in
 //      (depth, index) order at the tile's CSR offset.
 // One radix pass = digit histogram per 4096-element block (per-warp smem
-// counters), an exclusive scan of the digit-major histogram, and a
-// stable scatter that ranks each 256-element chunk with nine ballots (equal
-// digits within a warp) and per-warp digit counts, stages the block's elements in shared memory in digit
-// order and writes each digit's run out coalesced.
+// counters), an exclusive scan of the digit-major histogram, and a stable
+// scatter that ranks each warp's 512 elements with __match_any_sync (equal
+// digits) against per-warp running digit counts, stages the block's elements
+// in shared memory in digit order and writes each digit's run out coalesced.
 #include <cstdint>
 
 #include <atomic>
@@ -59,11 +59,15 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
     hist[static_cast<size_t>(t) * nblocks + blockIdx.x] = sum;
 }
 
-// Stable scatter, block-staged: the block's 4096 elements are first placed in
-// shared memory in (digit, input) order, then written out so consecutive
-// threads write consecutive positions of each digit's run (coalesced), instead
-// of 256 scattered 4-byte writes per round.
-// `pin`/`pout` (optional) carry a 64-bit payload per element along.
+// Stable scatter, block-staged, one ranking sweep per block: warp w owns the
+// block's elements [512 w, 512 w + 512) (item i, lane l = element 512 w + 32 i
+// + l), ranks them with __match_any_sync (the lanes holding the same digit)
+// against a per-warp running digit count in shared memory, so the local order
+// within a digit is (warp, item, lane) = input order (stable).  The per-warp
+// counts are then turned into the block's digit-major local offsets, the
+// elements are placed in shared memory in (digit, input) order and written
+// out so consecutive threads write consecutive positions of each digit's run
+// (coalesced).  `pin`/`pout` (optional) carry a 64-bit payload per element.
 template <typename K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __restrict__ kin,
                                                                   const unsigned* __restrict__ vin,
@@ -73,21 +77,42 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
                                                                   const unsigned long long* __restrict__ pin,
                                                                   unsigned long long* __restrict__ pout) {
     constexpr int NW = kRadixThreads / 32;
+    constexpr int WE = kRadixTile / NW;  // elements per warp
     extern __shared__ __align__(16) unsigned char s_raw[];
     unsigned long long* s_pay = reinterpret_cast<unsigned long long*>(s_raw);  // used only with a payload
     K* s_key = reinterpret_cast<K*>(s_raw + (pin ? sizeof(unsigned long long) * kRadixTile : 0));
     unsigned* s_val = reinterpret_cast<unsigned*>(s_key + kRadixTile);
-    __shared__ unsigned s_gbase[256], s_lbase[256], s_run[256], s_warp[NW];
-    __shared__ unsigned s_wc[NW][256];
+    __shared__ unsigned s_gbase[256], s_lbase[256], s_warp[NW];
+    __shared__ unsigned s_wc[NW][257];  // per-warp running digit counts (+ a slot for invalid)
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
     const int cnt = static_cast<int>(n - base < kRadixTile ? n - base : kRadixTile);
-    const size_t idx0 = static_cast<size_t>(t) * nblocks + blockIdx.x;
-    const unsigned g0 = offs[idx0];
-    const unsigned g1 = idx0 + 1 < 256ull * nblocks ? offs[idx0 + 1] : static_cast<unsigned>(n);
-    s_gbase[t] = g0;
-    {   // block-local digit starts: exclusive scan of this block's digit counts
-        unsigned x = g1 - g0, incl = x;
+    for (int d = lane; d < 257; d += 32) s_wc[warp][d] = 0u;
+    __syncwarp();
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned short rank[kRadixItems];
+#pragma unroll
+    for (int i = 0; i < kRadixItems; ++i) {
+        const int li = warp * WE + i * 32 + lane;
+        const bool valid = li < cnt;
+        const unsigned d = valid ? digit_of(kin[base + li], shift) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned before = s_wc[warp][d];
+        __syncwarp();
+        if ((peers & lt) == 0u) s_wc[warp][d] = before + __popc(peers);  // the group's first lane
+        __syncwarp();
+        rank[i] = static_cast<unsigned short>(before + __popc(peers & lt));
+    }
+    __syncthreads();
+    {   // thread t = digit t: exclusive over warps, then the block's digit starts
+        unsigned run = 0u;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const unsigned c = s_wc[w][t];
+            s_wc[w][t] = run;
+            run += c;
+        }
+        unsigned incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -97,50 +122,21 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
         __syncthreads();
         unsigned wo = 0u;
         for (int w = 0; w < warp; ++w) wo += s_warp[w];
-        s_lbase[t] = wo + incl - x;
-        s_run[t] = 0u;
+        s_lbase[t] = wo + incl - run;
+        s_gbase[t] = offs[static_cast<size_t>(t) * nblocks + blockIdx.x];
     }
-    const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < kRadixItems; ++r) {
+    __syncthreads();
 #pragma unroll
-        for (int w = 0; w < NW; ++w) s_wc[w][t] = 0u;
-        __syncthreads();
-        const int li = r * kRadixThreads + t;
-        const bool valid = li < cnt;
-        K key = 0;
-        unsigned val = 0u;
-        unsigned long long pay = 0ull;
-        if (valid) {
-            key = kin[base + li];
-            val = vin[base + li];
-            if (pin) pay = pin[base + li];
-        }
-        const unsigned d = valid ? digit_of(key, shift) : 256u;
-        unsigned peers = 0xffffffffu;  // lanes with the same digit, from nine ballots
-#pragma unroll
-        for (int b = 0; b < 9; ++b) {
-            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ((d >> b) & 1u) ? bal : ~bal;
-        }
-        const unsigned wrank = __popc(peers & lt);
-        if (d < 256u && wrank == 0u) s_wc[warp][d] = __popc(peers);
-        __syncthreads();
-        unsigned run = 0u;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const unsigned c = s_wc[w][t];
-            s_wc[w][t] = run;
-            run += c;
-        }
-        __syncthreads();
-        if (d < 256u) {
-            const unsigned lpos = s_lbase[d] + s_run[d] + s_wc[warp][d] + wrank;
+    for (int i = 0; i < kRadixItems; ++i) {
+        const int li = warp * WE + i * 32 + lane;
+        if (li < cnt) {
+            const K key = kin[base + li];  // L1/L2-resident: read a second time instead of held in registers
+            const unsigned d = digit_of(key, shift);
+            const unsigned lpos = s_lbase[d] + s_wc[warp][d] + rank[i];
             s_key[lpos] = key;
-            s_val[lpos] = val;
-            if (pin) s_pay[lpos] = pay;
+            s_val[lpos] = vin[base + li];
+            if (pin) s_pay[lpos] = pin[base + li];
         }
-        __syncthreads();
-        s_run[t] += run;
     }
     __syncthreads();
     for (int i = t; i < cnt; i += kRadixThreads) {

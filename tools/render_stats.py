@@ -20,14 +20,15 @@ def main():
     bc = [cams[i] for i in batch]
     for name, g in (("random_init", state), ("gt_scene", bench.gt_scene(args.gaussians // 2, H=L))):
         sc = splatlm.Scene(L, g)
-        out = np.zeros(8, np.uint64)
+        out = np.zeros(10, np.uint64)
         rc = L.dll.slm_debug_render_stats(sc.h, cameras_to_c(bc), len(bc), out.ctypes.data_as(C.POINTER(C.c_uint64)))
         assert rc == 0, L.dll.slm_last_error()
-        it, box, live, blend, staged, E, npix, nt = [int(x) for x in out]
+        it, box, live, blend, staged, E, npix, nt, exact, useful = [int(x) for x in out]
         # per thread counters: 64 threads per tile
         print(f"{name}: entries {E} ({E / nt:.0f}/tile), staged/tile {staged / 64 / nt:.0f}, "
               f"iterated/warp {it / 64 / (2 * nt):.0f}... thread-iter {it / (64 * nt):.0f}, box-pass {box / (64 * nt):.0f}, "
-              f"live gates/px {live / npix:.0f}, blends/px {blend / npix:.0f}")
+              f"live gates/px {live / npix:.0f}, blends/px {blend / npix:.0f}, "
+              f"warp-entries: box {box / 32:.0f}, exact {exact:.0f}, useful {useful:.0f}")
 
 
 if __name__ == "__main__":
