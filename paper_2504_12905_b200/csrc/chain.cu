@@ -264,6 +264,67 @@ __device__ __forceinline__ void det_sum(const DetOrder& D, DetSeg sg, float4 acc
     }
 }
 
+// Warp-staged ordered sums (the fused deterministic path): the records of
+// the 32 consecutive keys (v, g0 .. g0+31) of a warp are ONE contiguous range
+// [seg[v Gp + g0], seg[v Gp + g0 + 32]), so lane 0 brings the next view's
+// range into shared memory with one cp.async.bulk while the warp works on the
+// current view (double-buffered, one mbarrier per buffer); each lane then
+// sums its own records from shared memory in the same order as det_sum
+// (bitwise the same result).  A range longer than CAP records is summed from
+// global memory instead.
+template <int STRIDE4, int CAP>
+struct DetStage {
+    float4* buf;    // [2][CAP * STRIDE4]
+    uint64_t* bar;  // [2]
+    unsigned A0, B0, A1, B1;  // the staged range per buffer (no dynamic indexing: registers)
+    uint32_t par;
+    __device__ __forceinline__ void init(int lane) {
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+        }
+        par = 0u;
+        __syncwarp();
+    }
+    // the warp's range of this key segment set (lane 31 holds the last key)
+    __device__ __forceinline__ void issue(const DetOrder& D, DetSeg sg, int slot, int lane) {
+        const unsigned a = __shfl_sync(0xffffffffu, sg.a, 0), b = __shfl_sync(0xffffffffu, sg.b, 31);
+        if (slot) {
+            A1 = a;
+            B1 = b;
+        } else {
+            A0 = a;
+            B0 = b;
+        }
+        if (lane == 0 && b > a && b - a <= CAP)
+            bulk_load(buf + slot * CAP * STRIDE4, reinterpret_cast<const float4*>(D.partial) + static_cast<size_t>(a) * STRIDE4,
+                      (b - a) * STRIDE4 * 16u, bar + slot);
+    }
+    template <int NF4>
+    __device__ __forceinline__ void sum(const DetOrder& D, DetSeg sg, int slot, float4 acc[NF4]) {
+        const unsigned a = slot ? A1 : A0, b = slot ? B1 : B0;
+        if (!(b > a && b - a <= CAP)) {
+            det_sum<STRIDE4, NF4>(D, sg, acc);
+            return;
+        }
+        mbar_wait(bar + slot, (par >> slot) & 1u);
+        par ^= 1u << slot;
+#pragma unroll
+        for (int q = 0; q < NF4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* r = buf + slot * CAP * STRIDE4 + static_cast<size_t>(sg.a - a) * STRIDE4;
+        for (unsigned j = sg.a; j < sg.b; ++j, r += STRIDE4) {
+#pragma unroll
+            for (int q = 0; q < NF4; ++q) {
+                const float4 v = r[q];
+                acc[q].x += v.x;
+                acc[q].y += v.y;
+                acc[q].z += v.z;
+                acc[q].w += v.w;
+            }
+        }
+    }
+};
+
 // Deterministic segmented reduction, parallel over records: one warp per 32
 // consecutive keys (view, Gaussian) -- their records are the contiguous range
 // [seg[k0], seg[k0 + 32]) -- walked in chunks of 32 records (one per lane,
@@ -339,8 +400,10 @@ __global__ void __launch_bounds__(256) k_det_reduce(const unsigned* __restrict__
 // red.global.add sums and is zeroed after reading.  MODE 1 (deterministic,
 // fused): inter_v[g] is the ordered sum of the (view, Gaussian)'s records
 // (det_sum).  MODE 2 (deterministic, k_det_reduce first): inter is read as is.
+constexpr int kChainThreads = 64;
+constexpr int kChainCap = 128;  // staged records per warp and view (6 KB)
 template <int MODE>
-__global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(kChainThreads) k_chain(const float* __restrict__ beta, int G, int Gp,
                                                const DevCam* __restrict__ cams, int V,
                                                const float4* __restrict__ conic, float* __restrict__ inter,
                                                DetOrder D, const float* __restrict__ p, float lambda,
@@ -348,17 +411,25 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
                                                int g1) {
     if (done_flag && *done_flag) return;
     const int g = g0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= g1) return;
+    constexpr bool DET = MODE == 1;
+    // the fused deterministic path stages each view's records per warp
+    // (DetStage): every lane of a warp with any live Gaussian takes part
+    __shared__ __align__(16) float4 s_det[DET ? kChainThreads / 32 : 1][DET ? 2 * kChainCap * (kDetRec / 4) : 1];
+    __shared__ uint64_t s_dbar[kChainThreads / 32][2];
+    if (g0 + blockIdx.x * blockDim.x + (threadIdx.x & ~31) >= g1) return;  // whole warp past the range
+    const bool live = g < g1;
+    const int gl = live ? g : g1 - 1;  // dead lanes shadow a live Gaussian (never written)
+    DetStage<kDetRec / 4, kChainCap> ds{s_det[threadIdx.x >> 5], s_dbar[threadIdx.x >> 5], 0u, 0u, 0u, 0u, 0u};
+    if (DET) ds.init(threadIdx.x & 31);
     Geom Gm;
-    load_geom(beta, Gp, g, Gm);
+    load_geom(beta, Gp, gl, Gm);
     float gs00 = 0, gs01 = 0, gs02 = 0, gs11 = 0, gs12 = 0, gs22 = 0;  // gS + gS^T
     float gmu0 = 0, gmu1 = 0, gmu2 = 0, go = 0, gc0 = 0, gc1 = 0, gc2 = 0;
     // Software pipeline: view v+1's record and intermediate are loaded
     // (unconditionally; invalid pairs hold zeros) while view v is processed.
-    constexpr bool DET = MODE == 1;
     float4 nc, ni0, ni1, ni2;
     auto fetch = [&](int v) {
-        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        const size_t vg = static_cast<size_t>(v) * Gp + gl;
         nc = __ldg(conic + vg);
         if (!DET) {
             const float4* ip = reinterpret_cast<const float4*>(inter + vg * kRec);
@@ -368,23 +439,35 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
         }
     };
     if (V > 0) fetch(0);
-    DetSeg sn{0u, 0u};
-    if (DET && V > 0) sn = det_seg(D, g);
+    // segments of views v (cur) and v + 1 (nxt); view v + 1's range is in flight
+    // while view v is summed
+    DetSeg sc{0u, 0u}, sn{0u, 0u};
+    const unsigned lane = threadIdx.x & 31;
+    if (DET && V > 0) {
+        sc = det_seg(D, g);
+        if (!live) sc.b = sc.a;
+        ds.issue(D, det_seg(D, g), 0, lane);  // (dead lanes: g < Gp, keys without records)
+        if (V > 1) sn = det_seg(D, static_cast<size_t>(Gp) + g);
+    }
     for (int v = 0; v < V; ++v) {
-        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        const size_t vg = static_cast<size_t>(v) * Gp + gl;
         float4 i0 = ni0, i1 = ni1, i2 = ni2;
         if (DET) {
-            const DetSeg sg = sn;
-            if (v + 1 < V) sn = det_seg(D, vg + Gp);
+            __syncwarp();  // every lane is done with the buffer view v + 1 reuses
+            if (v + 1 < V) ds.issue(D, sn, (v + 1) & 1, lane);
+            const DetSeg sg = sc;
+            sc = sn;
+            if (!live) sc.b = sc.a;
+            if (v + 2 < V) sn = det_seg(D, static_cast<size_t>(v + 2) * Gp + g);
             float4 acc[3];
-            det_sum<kDetRec / 4, 3>(D, sg, acc);
+            ds.template sum<3>(D, sg, v & 1, acc);
             i0 = acc[0];
             i1 = acc[1];
             i2 = acc[2];
         }
         const float4 cn = nc;
         if (v + 1 < V) fetch(v + 1);
-        if (cn.w == 0.0f) continue;  // invalid (view, Gaussian): zero opacity
+        if (!live || cn.w == 0.0f) continue;  // invalid (view, Gaussian): zero opacity
         if (MODE == 0) {
             float4* ip = reinterpret_cast<float4*>(inter + vg * kRec);
             ip[0] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -469,6 +552,7 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
     res[11] = gc0 * Gm.dcol[0];
     res[12] = gc1 * Gm.dcol[1];
     res[13] = gc2 * Gm.dcol[2];
+    if (!live) return;
     for (int k = 0; k < kP; ++k) {
         float val = res[k];
         if (p) val += lambda * p[k * Gp + g];
@@ -479,25 +563,33 @@ __global__ void __launch_bounds__(128) k_chain(const float* __restrict__ beta, i
 // ------------------------------------------------------------------ K13 finalize
 // diag[j] = sum_v P_j^T M_v P_j (j < 10) + opacity / colour rows; the 5x10
 // ProjChain columns P_j are the view_tangent of the unit probes e_j.
+constexpr int kDiagThreads = 64;
+constexpr int kDiagCap = 90;  // staged diag records per warp and view (8.4 KB): 6 CTAs per SM
 template <int MODE>
-__global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
+__global__ void __launch_bounds__(kDiagThreads, 6) k_diag_finalize(const float* __restrict__ beta, int G, int Gp,
                                                        const DevCam* __restrict__ cams, int V,
                                                        const float4* __restrict__ conic,
                                                        float* __restrict__ diagacc, DetOrder D,
                                                        float* __restrict__ out) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= G) return;
+    constexpr bool DET = MODE == 1;
+    __shared__ __align__(16) float4 s_det[DET ? kDiagThreads / 32 : 1][DET ? 2 * kDiagCap * (kDetDiagRec / 4) : 1];
+    __shared__ uint64_t s_dbar[kDiagThreads / 32][2];
+    if (blockIdx.x * blockDim.x + (threadIdx.x & ~31) >= G) return;  // whole warp past the end
+    const bool live = g < G;
+    const int gl = live ? g : G - 1;  // dead lanes shadow a live Gaussian (never written)
+    DetStage<kDetDiagRec / 4, kDiagCap> ds{s_det[threadIdx.x >> 5], s_dbar[threadIdx.x >> 5], 0u, 0u, 0u, 0u, 0u};
+    if (DET) ds.init(threadIdx.x & 31);
     Geom Gm;
-    load_geom(beta, Gp, g, Gm);
+    load_geom(beta, Gp, gl, Gm);
     float d[kP];
     for (int k = 0; k < kP; ++k) d[k] = 0.0f;
     const float zero9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const float zero3[3] = {0, 0, 0};
     // software pipeline: next view's record and accumulators load during this view
-    constexpr bool DET = MODE == 1;
     float4 nc, na[5];
     auto fetch = [&](int v) {
-        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        const size_t vg = static_cast<size_t>(v) * Gp + gl;
         nc = __ldg(conic + vg);
         if (!DET) {
             const float4* a4 = reinterpret_cast<const float4*>(diagacc + vg * kDiagRec);
@@ -505,14 +597,26 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
         }
     };
     if (V > 0) fetch(0);
-    DetSeg sn{0u, 0u};
-    if (DET && V > 0) sn = det_seg(D, g);
+    // segments of views v (cur) and v + 1 (nxt); view v + 1's records are in
+    // flight (DetStage) while view v is summed
+    DetSeg sc{0u, 0u}, sn{0u, 0u};
+    const unsigned lane = threadIdx.x & 31;
+    if (DET && V > 0) {
+        sc = det_seg(D, g);
+        if (!live) sc.b = sc.a;
+        ds.issue(D, det_seg(D, g), 0, lane);
+        if (V > 1) sn = det_seg(D, static_cast<size_t>(Gp) + g);
+    }
     for (int v = 0; v < V; ++v) {
-        const size_t vg = static_cast<size_t>(v) * Gp + g;
+        const size_t vg = static_cast<size_t>(v) * Gp + gl;
         if (DET) {
-            const DetSeg sg = sn;
-            if (v + 1 < V) sn = det_seg(D, vg + Gp);
-            det_sum<kDetDiagRec / 4, 5>(D, sg, na);
+            __syncwarp();  // every lane is done with the buffer view v + 1 reuses
+            if (v + 1 < V) ds.issue(D, sn, (v + 1) & 1, lane);
+            const DetSeg sg = sc;
+            sc = sn;
+            if (!live) sc.b = sc.a;
+            if (v + 2 < V) sn = det_seg(D, static_cast<size_t>(v + 2) * Gp + g);
+            ds.template sum<5>(D, sg, v & 1, na);
         }
         const float4 cn = nc;
         float acc[20];
@@ -523,7 +627,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
             acc[4 * q4 + 3] = na[q4].w;
         }
         if (v + 1 < V) fetch(v + 1);
-        if (cn.w == 0.0f) continue;  // invalid (view, Gaussian)
+        if (!live || cn.w == 0.0f) continue;  // invalid (view, Gaussian)
         if (MODE == 0) {
             float4* acc4 = reinterpret_cast<float4*>(diagacc + vg * kDiagRec);
             for (int q4 = 0; q4 < 5; ++q4) acc4[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -572,6 +676,7 @@ __global__ void __launch_bounds__(128, 3) k_diag_finalize(const float* __restric
     }
     // each row is a sum of squares (jtj_diag, jacobian.cpp:272-337); the quadratic
     // form P^T M P of rounded moment sums can dip a few ulp below zero -- clamp
+    if (!live) return;
     for (int k = 0; k < kP; ++k) out[k * Gp + g] = fmaxf(d[k], 0.0f);
 }
 
@@ -596,11 +701,13 @@ void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, 
                         const int* done, int g0, int g1, bool reduce, cudaStream_t st) {
     g1 = g1 < G ? g1 : G;
     if (g1 <= g0) return;
-    const unsigned nb = (g1 - g0 + 127) / 128;
+    const unsigned nb = (g1 - g0 + kChainThreads - 1) / kChainThreads;
     if (!det.partial) {
-        k_chain<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<0><<<nb, kChainThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0,
+                                                 g1);
     } else if (det.fused) {
-        k_chain<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<1><<<nb, kChainThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0,
+                                                 g1);
     } else {
         if (reduce) {
             const long long nk = static_cast<long long>(V) * Gp;
@@ -608,7 +715,8 @@ void launch_chain_range(const float* beta32, int G, int Gp, const DevCam* cams, 
                 det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(inter));
             ++g_launches;
         }
-        k_chain<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0, g1);
+        k_chain<2><<<nb, kChainThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, inter, det, p, lambda, out, done, g0,
+                                                 g1);
     }
     ++g_launches;
 }
@@ -622,17 +730,17 @@ void launch_chain(const float* beta32, int G, int Gp, const DevCam* cams, int V,
 void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams, int V, const float4* conic,
                           float* diagacc, const DetOrder& det, float* out, cudaStream_t st) {
     if (G == 0) return;
-    const unsigned nb = (G + 127) / 128;
+    const unsigned nb = (G + kDiagThreads - 1) / kDiagThreads;
     if (!det.partial) {
-        k_diag_finalize<0><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
+        k_diag_finalize<0><<<nb, kDiagThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     } else if (det.fused) {
-        k_diag_finalize<1><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
+        k_diag_finalize<1><<<nb, kDiagThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     } else {
         const long long nk = static_cast<long long>(V) * Gp;
         k_det_reduce<5, kDetDiagRec / 4, kDiagRec / 4><<<static_cast<unsigned>((nk + 255) / 256), 256, 0, st>>>(
             det.seg, reinterpret_cast<const float4*>(det.partial), nk, reinterpret_cast<float4*>(diagacc));
         ++g_launches;
-        k_diag_finalize<2><<<nb, 128, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
+        k_diag_finalize<2><<<nb, kDiagThreads, 0, st>>>(beta32, G, Gp, cams, V, conic, diagacc, det, out);
     }
     ++g_launches;
 }

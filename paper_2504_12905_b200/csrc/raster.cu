@@ -737,38 +737,6 @@ __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, 
     dst[8][lane] = c.x;
 }
 
-// ---- TMA bulk copies of alpha-stream rows into shared memory
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// One lane: arm the barrier with the byte count and start the copy.
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// Copy only (the barrier is armed separately).
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // Double-buffered window inputs of one warp: window w's alpha rows and record
 // block land in buffer w & 1 (one mbarrier per buffer, one transaction count),
 // the copies for window w+1 are in flight while window w runs.
@@ -840,7 +808,7 @@ __device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0
 constexpr int kRasterWarps = 2;
 
 template <int MODE>
-__global__ void __launch_bounds__(32 * kRasterWarps) k_sample_raster(SampleArgs A) {
+__global__ void __maxnreg__(144) k_sample_raster(SampleArgs A) {  // 144 regs x 64 threads: 7 CTAs per SM
     constexpr int NW = kRasterWarps;
     __shared__ __align__(128) float s_alpha[NW][2][kAlphaRows * 32];
     __shared__ __align__(128) float s_blk[NW][2][kRecBlock];  // record blocks [9][32] (TMA)
