@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     float* __restrict__ image, float* __restrict__ trans, int* __restrict__ contrib,
     int* __restrict__ last_out, double* __restrict__ sse_tile, unsigned long long* __restrict__ stats) {
     __shared__ float4 s_rec[kRenderStage][3];
-    __shared__ float4 s_box[kRenderStage];
+    __shared__ float4 s_box[STATS ? kRenderStage : 1];
+    __shared__ unsigned s_wm[kRenderStage];  // bit w: the entry's alpha box meets warp w's half-tile
     __shared__ double s_red[kRenderThreads / 32];
     const int tile = blockIdx.x;
     const int v = tile_view[tile];
@@ -171,14 +172,20 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             s_rec[j][0] = make_float4(g.g0, g.g1, g.g2, g.g3);
             s_rec[j][1] = make_float4(g.g4, g.g5, g.lo, r1.z);
             s_rec[j][2] = make_float4(r1.w, r2.x, 0.f, 0.f);
-            s_box[j] = alpha_box(r0, r1);
+            const float4 bx = alpha_box(r0, r1);
+            if (STATS) s_box[j] = bx;
+            // the half-tiles span x in [tx 16 + .5, + 15], y in [ty 16 + 8 w + .5, + 7]
+            const float x0 = (float)(tx * kTile) + 0.5f, y0h = (float)(ty * kTile) + 0.5f;
+            const bool inx = !(bx.y < x0 || bx.x > x0 + 15.0f);
+            const unsigned m0 = (inx && !(bx.w < y0h || bx.z > y0h + 7.0f)) ? 1u : 0u;
+            const unsigned m1 = (inx && !(bx.w < y0h + 8.0f || bx.z > y0h + 15.0f)) ? 2u : 0u;
+            s_wm[j] = m0 | m1;
         }
         __syncthreads();
         const int m = min(kRenderStage, n - start);
         for (int k = 0; k < m && live; ++k) {
-            const float4 bx = s_box[k];
             if (STATS) ++st_iter;
-            if (bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1) continue;  // warp-uniform
+            if (!((s_wm[k] >> warp) & 1u)) continue;  // warp-uniform: the box misses this half-tile
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column
@@ -204,9 +211,11 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             float2 tt[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) tt[p] = fmul2(T[p], fsub2(make_float2(1.0f, 1.0f), a[p]));
-            const bool tm0 = ps[0] && tt[0].x < 1e-4f, tm1 = ps[1] && tt[0].y < 1e-4f;
-            const bool tm2 = ps[2] && tt[1].x < 1e-4f, tm3 = ps[3] && tt[1].y < 1e-4f;
-            if (tm0 || tm1 || tm2 || tm3) {  // termination (rasterizer.hpp:121-122): not blended, the pixel stops
+            // a pixel that fails the gate keeps tt = T >= 1e-4 (alpha = 0), so
+            // tt < 1e-4 alone marks a termination
+            if (fminf(fminf(tt[0].x, tt[0].y), fminf(tt[1].x, tt[1].y)) < 1e-4f) {
+                // termination (rasterizer.hpp:121-122): not blended, the pixel stops (rare)
+                const bool tm0 = tt[0].x < 1e-4f, tm1 = tt[0].y < 1e-4f, tm2 = tt[1].x < 1e-4f, tm3 = tt[1].y < 1e-4f;
                 const bool tm[4] = {tm0, tm1, tm2, tm3};
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             if (STATS) {
                 const int nb = (ps[0] ? 1 : 0) + (ps[1] ? 1 : 0) + (ps[2] ? 1 : 0) + (ps[3] ? 1 : 0);
                 ++st_box;
-                st_live += __popc(live | (tm0 ? 1u : 0u) | (tm1 ? 2u : 0u) | (tm2 ? 4u : 0u) | (tm3 ? 8u : 0u));
+                st_live += __popc(live);
                 st_blend += nb;
                 const unsigned act = __activemask();
                 const bool leader = (threadIdx.x & 31) == __ffs(act) - 1;  // one count per warp
@@ -743,7 +752,10 @@ __device__ __forceinline__ void stage_rec(float (*dst)[32], int lane, float4 a, 
 // Rows staged per window by TMA; the rest (windows whose busiest lane blends
 // more than 18 entries) are prefetched into L2 with the window and read from
 // global.  18 (not the ~98th-percentile 22) so the product CTA fits 7 per SM.
-constexpr int kAlphaRows = 18;
+#ifndef SLM_ALPHA_ROWS
+#define SLM_ALPHA_ROWS 18
+#endif
+constexpr int kAlphaRows = SLM_ALPHA_ROWS;
 
 struct AlphaPipe {
     float* buf0;
@@ -805,7 +817,10 @@ __device__ __forceinline__ int max_popc(unsigned m) { return __reduce_max_sync(0
 //      FFMA2; the entry's conic turns the moments into the 9-float
 //      intermediate gradient once (dL/do = sum dL/dpower / o), one vector
 //      red.global.add per 4 floats.
-constexpr int kRasterWarps = 2;
+#ifndef SLM_RASTER_WARPS
+#define SLM_RASTER_WARPS 2
+#endif
+constexpr int kRasterWarps = SLM_RASTER_WARPS;
 
 template <int MODE>
 __global__ void __maxnreg__(144) k_sample_raster(SampleArgs A) {  // 144 regs x 64 threads: 7 CTAs per SM
