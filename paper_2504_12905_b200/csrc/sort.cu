@@ -27,6 +27,9 @@ namespace slm { extern std::atomic<long long> g_launches; }
 
 namespace slm {
 
+#ifndef SLM_RADIX_MATCH
+#define SLM_RADIX_MATCH 0
+#endif
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;
@@ -45,13 +48,15 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
     const int t = threadIdx.x;
     __syncthreads();
     const long long base = static_cast<long long>(blockIdx.x) * kRadixTile;
-#pragma unroll 4
+    unsigned dig[kRadixItems];
+#pragma unroll
     for (int i = 0; i < kRadixItems; ++i) {
         const long long idx = base + i * kRadixThreads + t;
-        const bool valid = idx < n;
-        const unsigned d = valid ? digit_of(keys[idx], shift) : 256u;
-        if (valid) atomicAdd(&hw[t >> 5][d], 1u);
+        dig[i] = idx < n ? digit_of(keys[idx], shift) : 256u;
     }
+#pragma unroll
+    for (int i = 0; i < kRadixItems; ++i)
+        if (dig[i] < 256u) atomicAdd(&hw[t >> 5][dig[i]], 1u);
     __syncthreads();
     unsigned sum = 0u;
 #pragma unroll
@@ -90,13 +95,28 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __rest
     for (int d = lane; d < 257; d += 32) s_wc[warp][d] = 0u;
     __syncwarp();
     const unsigned lt = (1u << lane) - 1u;
-    unsigned short rank[kRadixItems];
+    // all of the warp's keys in flight at once (the ranking below is separated
+    // by __syncwarp, which the compiler does not move loads across)
+    unsigned dig[kRadixItems];
 #pragma unroll
     for (int i = 0; i < kRadixItems; ++i) {
         const int li = warp * WE + i * 32 + lane;
-        const bool valid = li < cnt;
-        const unsigned d = valid ? digit_of(kin[base + li], shift) : 256u;
+        dig[i] = li < cnt ? digit_of(kin[base + li], shift) : 256u;
+    }
+    unsigned short rank[kRadixItems];
+#pragma unroll
+    for (int i = 0; i < kRadixItems; ++i) {
+        const unsigned d = dig[i];
+#if SLM_RADIX_MATCH
         const unsigned peers = __match_any_sync(0xffffffffu, d);
+#else
+        unsigned peers = 0xffffffffu;  // lanes with the same 9-bit digit (256 = invalid): nine ballots
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+            const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bal : ~bal;
+        }
+#endif
         const unsigned before = s_wc[warp][d];
         __syncwarp();
         if ((peers & lt) == 0u) s_wc[warp][d] = before + __popc(peers);  // the group's first lane
