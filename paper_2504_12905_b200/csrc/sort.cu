@@ -31,7 +31,10 @@ namespace slm {
 #define SLM_RADIX_MATCH 0
 #endif
 constexpr int kRadixThreads = 256;
-constexpr int kRadixItems = 16;
+#ifndef SLM_RADIX_ITEMS
+#define SLM_RADIX_ITEMS 8
+#endif
+constexpr int kRadixItems = SLM_RADIX_ITEMS;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;
 
 template <typename K>
