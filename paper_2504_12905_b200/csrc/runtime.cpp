@@ -1397,6 +1397,95 @@ struct PlanReturn {  // hands a step's plan back to the pool when the step ends
     ~PlanReturn() { release_plan(std::move(p)); }
 };
 
+// Uniform plans with many samples (configs[0]: full pixels, 524k draws): the
+// draws are libstdc++'s uniform_int_distribution<int>(i, m-1) on mt19937_64,
+// i.e. Lemire's nearly-divisionless map (uniform_int_dist.h _S_nd): one 64-bit
+// output x per draw gives i + (x * (m - i)) >> 64 unless the low half falls
+// below (2^64 - r) % r (probability ~r / 2^64).  So the outputs are drawn
+// sequentially (the RNG stream is the reference's) and the per-tile shuffles
+// run on several threads; if any draw would have been rejected the whole plan
+// is redone by the sequential reference loop from the saved RNG state.
+// false: not handled (the caller runs the sequential loop).
+static bool uniform_plan_parallel(PlanH* plan, const slm_camera* cams, int n_cams, int spt, size_t total,
+                                  std::mt19937_64& rng) {
+    struct TileJob {
+        int x0, y0, rw, m, n, tile;
+        size_t off;
+    };
+    std::vector<TileJob> jobs;
+    std::vector<size_t> view_end;
+    size_t off = 0;
+    for (int ci = 0; ci < n_cams; ++ci) {
+        const int txn = (cams[ci].width + kTile - 1) / kTile, tyn = (cams[ci].height + kTile - 1) / kTile;
+        for (int ty = 0; ty < tyn; ++ty)
+            for (int tx = 0; tx < txn; ++tx) {
+                const int x0 = tx * kTile, y0 = ty * kTile;
+                const int rw = std::min(cams[ci].width - x0, kTile), rh = std::min(cams[ci].height - y0, kTile);
+                const int m = rw * rh, n = std::min(spt, m);
+                jobs.push_back(TileJob{x0, y0, rw, m, n, ty * txn + tx, off});
+                off += n;
+            }
+        view_end.push_back(off);
+    }
+    const std::mt19937_64 saved = rng;
+    thread_local std::vector<uint64_t> raw;  // keeps its capacity (no first-touch faults per step)
+    raw.resize(total);
+    for (size_t k = 0; k < total; ++k) raw[k] = rng();
+    plan->px.resize(total);
+    plan->py.resize(total);
+    plan->tile.resize(total);
+    plan->weight.resize(total);
+    const double n_total = static_cast<double>(total);
+    const uint64_t* rawp = raw.data();  // (raw is this thread's thread_local: the workers get the pointer)
+    std::atomic<bool> rejected{false};
+    auto work = [&](size_t j0, size_t j1) {
+        int pool[kTile * kTile];
+        for (size_t j = j0; j < j1; ++j) {
+            const TileJob& J = jobs[j];
+            for (int l = 0; l < J.m; ++l) pool[l] = l;
+            const uint64_t* x = rawp + J.off;
+            for (int i = 0; i < J.n; ++i) {
+                const uint64_t r = static_cast<uint64_t>(J.m - i);
+                const unsigned __int128 prod = static_cast<unsigned __int128>(x[i]) * r;
+                const uint64_t low = static_cast<uint64_t>(prod);
+                if (low < r && low < (-r) % r) {  // _S_nd would draw again
+                    rejected.store(true, std::memory_order_relaxed);
+                    return;
+                }
+                std::swap(pool[i], pool[i + static_cast<int>(prod >> 64)]);
+            }
+            const double q = (J.n / n_total) * (1.0 / J.m);
+            const double w = 1.0 / std::max(q, 1e-12);
+            for (int i = 0; i < J.n; ++i) {
+                plan->px[J.off + i] = J.x0 + pool[i] % J.rw;
+                plan->py[J.off + i] = J.y0 + pool[i] / J.rw;
+                plan->tile[J.off + i] = J.tile;
+                plan->weight[J.off + i] = w;
+            }
+        }
+    };
+    const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+    std::vector<std::thread> th;
+    const size_t per = (jobs.size() + nt - 1) / nt;
+    for (unsigned t = 1; t < nt; ++t)
+        if (t * per < jobs.size()) th.emplace_back(work, t * per, std::min(jobs.size(), (t + 1) * per));
+    work(0, std::min(jobs.size(), per));
+    for (auto& t : th) t.join();
+    if (rejected.load()) {  // vanishingly rare: redo sequentially from the same RNG state
+        rng = saved;
+        plan->px.clear();
+        plan->py.clear();
+        plan->tile.clear();
+        plan->weight.clear();
+        return false;
+    }
+    for (int ci = 0; ci < n_cams; ++ci) {
+        plan->view_camera.push_back(ci);
+        plan->view_offset.push_back(static_cast<int64_t>(view_end[ci]));
+    }
+    return true;
+}
+
 static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int spt, int dist, int lane,
                                          std::mt19937_64& rng, const double* const* aux_image,
                                          const int32_t* const* aux_contrib, const double* const* aux_gt) {
@@ -1423,6 +1512,8 @@ static std::unique_ptr<PlanH> build_plan(const slm_camera* cams, int n_cams, int
             }
     }
     const double n_total = static_cast<double>(total);
+    if (dist == SLM_DIST_UNIFORM && total >= (1u << 16) && uniform_plan_parallel(plan.get(), cams, n_cams, spt, total, rng))
+        return plan;
     plan->px.reserve(total);
     plan->py.reserve(total);
     plan->tile.reserve(total);
@@ -2059,22 +2150,9 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     if (sampler.joinable()) sampler.join();
     ctx->mark("plan:host");
     if (plan_err) std::rethrow_exception(plan_err);
-    J.upload_early();  // overlaps the render still running on the main stream
-    // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
-    double before = 0.0;
-    if (ssim) {  // mse + ssim_weight * mean s^2 per view (lm.cpp:143-147) of the FP64 render; planes for the rhs fold
-        const auto ss = batch_ssim(B, true, true);
-        for (int v = 0; v < B.V; ++v)
-            before += (ss[v].x + cfg.ssim_weight * ss[v].y) / (3.0 * my_cams[v].width * my_cams[v].height);
-        ctx->mark("ssim");
-    } else {
-        const auto sse = B.view_sse();
-        for (int v = 0; v < B.V; ++v)
-            before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
-    }
-    J.init_device();
-    ctx->mark("plan");
-    {  // speculate the next step's batch + plan (uniform) or uniforms (weighted) while this one solves
+    {  // speculate the next step's batch + plan (uniform) or uniforms (weighted) while this one
+       // solves: started as soon as this step's draws are final, so the host draw of a
+       // full-pixel plan (configs[0]: 524k samples) hides behind the whole step
         auto sp = std::make_unique<Speculation>();
         sp->rng_before = rng;
         sp->assign = t.assign;
@@ -2111,6 +2189,21 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
         });
         sb.spec = std::move(sp);
     }
+    J.upload_early();  // overlaps the render still running on the main stream
+    // loss_before: mean of the per-view MSE of the pre-update renders (lm.cpp:143-147)
+    double before = 0.0;
+    if (ssim) {  // mse + ssim_weight * mean s^2 per view (lm.cpp:143-147) of the FP64 render; planes for the rhs fold
+        const auto ss = batch_ssim(B, true, true);
+        for (int v = 0; v < B.V; ++v)
+            before += (ss[v].x + cfg.ssim_weight * ss[v].y) / (3.0 * my_cams[v].width * my_cams[v].height);
+        ctx->mark("ssim");
+    } else {
+        const auto sse = B.view_sse();
+        for (int v = 0; v < B.V; ++v)
+            before += sse[v] / (3.0 * my_cams[v].width * my_cams[v].height);
+    }
+    J.init_device();
+    ctx->mark("plan");
     const size_t P = s.P();
     sb.b.ensure(2 * P);  // [b | diag] contiguous for one fused allreduce
     sb.x.ensure(P);

@@ -189,3 +189,21 @@ def test_estimate_loss_matches_reference(host, port):
     assert host.estimate_loss(cams, plans[1], fields) == pytest.approx(mse, rel=1e-12)
     with pytest.raises(ValueError):
         host.estimate_loss(cams, plans[0], fields[:2])
+
+
+def test_large_uniform_plans_parallel_path_bit_exact(host, port):
+    """Uniform plans of >= 65536 samples take the parallel path (raw mt19937_64
+    outputs drawn in order, per-tile shuffles on several threads): the sampled
+    pixels, weights and the RNG position after the plan are the C restatement's
+    (pinned bitwise to the reference) -- full-pixel 256x256 views (configs[0])
+    and a 1280x720 view at 64 samples per tile, two plans in a row each."""
+    from support import test_camera as tc
+    for cams, spt in (([tc(256, 3.0 + 0.1 * i) for i in range(8)], 256), ([tc(1280, 3.0)], 64)):
+        ra, rb = host.rng(31), port.rng(31)
+        for _ in range(2):
+            a = host.build_sample_plan(cams, spt, 0, ra)
+            b = port.build_sample_plan(cams, spt, 0, rb)
+            assert len(a.px) >= 65536
+            for k in ("view_camera", "view_offset", "px", "py", "tile", "weight"):
+                assert np.array_equal(getattr(a, k), getattr(b, k)), k
+        assert ra() == rb(), "RNG position after the plans"
