@@ -312,13 +312,12 @@ PSNR_TARGET = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", 
 def cfg0_scene(L, c):
     """configs[0] as io::train_run builds the toy scene (run.cpp:26-36, scene_gen.cpp:38-86):
     ground truth from the reference's generator (bit-exact), ring cameras, images rendered here."""
-    from paper_2504_12905_b200 import splatlm
-
-    gt = splatlm.Scene(L, L.toy_gaussians(c["toy_gaussians"], c["scene_seed"]))
+    gt = L.toy_gaussians(c["toy_gaussians"], c["scene_seed"])
     train = [L.ring_camera(2.0 * math.pi * i / c["train"], 3.2, 1.1, c["size"]) for i in range(c["train"])]
     test = [L.ring_camera(0.37 + 2.0 * math.pi * i / c["test"], 3.2, 1.6, c["size"]) for i in range(c["test"])]
-    timgs = [gt.render(cam)[0] for cam in train]
-    simgs = [gt.render(cam)[0] for cam in test]
+    # make_split (scene_gen.cpp:73-86): narrow(render_full(gt)), the FP64 render narrowed to f32
+    timgs = [L.render_full(gt, cam)[0].astype(np.float32) for cam in train]
+    simgs = [L.render_full(gt, cam)[0].astype(np.float32) for cam in test]
     return train, timgs, test, simgs
 
 

@@ -20,6 +20,8 @@ out of scope (no libpng on the path); ``scene`` must be ``"toy"``.
 from __future__ import annotations
 
 import json
+
+import numpy as np
 import math
 import os
 import time
@@ -83,12 +85,14 @@ def toy_scene(L, cfg: RunConfig):
     from .splatlm import Scene
 
     t = cfg.toy
-    gt = Scene(L, L.toy_gaussians(t.gaussians, cfg.scene_seed))
+    gt = L.toy_gaussians(t.gaussians, cfg.scene_seed)
     train = [L.ring_camera(0.0 + 2.0 * math.pi * i / t.train_cameras, 3.2, 1.1, t.image_size)
              for i in range(t.train_cameras)]
     test = [L.ring_camera(0.37 + 2.0 * math.pi * i / t.test_cameras, 3.2, 1.6, t.image_size)
             for i in range(t.test_cameras)]
-    return train, [gt.render(c)[0] for c in train], test, [gt.render(c)[0] for c in test]
+    # make_split (scene_gen.cpp:73-86): narrow(render_full(gt)) -- the FP64 drop-in render narrowed to f32
+    return (train, [L.render_full(gt, c)[0].astype(np.float32) for c in train], test,
+            [L.render_full(gt, c)[0].astype(np.float32) for c in test])
 
 
 def _config_json(cfg: RunConfig) -> dict:  # run.cpp:106-118
