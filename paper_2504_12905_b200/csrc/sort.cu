@@ -27,6 +27,9 @@ namespace slm { extern std::atomic<long long> g_launches; }
 
 namespace slm {
 
+#ifndef SLM_SCATTER_MINB
+#define SLM_SCATTER_MINB 1
+#endif
 #ifndef SLM_RADIX_MATCH
 #define SLM_RADIX_MATCH 0
 #endif
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
 // out so consecutive threads write consecutive positions of each digit's run
 // (coalesced).  `pin`/`pout` (optional) carry a 64-bit payload per element.
 template <typename K>
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const K* __restrict__ kin,
+__global__ void __launch_bounds__(kRadixThreads, SLM_SCATTER_MINB) k_radix_scatter(const K* __restrict__ kin,
                                                                   const unsigned* __restrict__ vin,
                                                                   K* __restrict__ kout, unsigned* __restrict__ vout,
                                                                   long long n, int shift,
