@@ -168,15 +168,17 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         }
         keys[vg] = depth_key(p.depth);
         float4* R = rec + 3 * vg;
-        double* R64 = rec64 + 6 * vg;  // FP64 geometry for the exact blend decisions (k_masks)
-        R64[0] = p.valid ? p.mx : 0.0;
-        R64[1] = p.valid ? p.my : 0.0;
-        R64[2] = p.valid ? p.ca : 0.0;
-        R64[3] = p.valid ? p.cb : 0.0;
-        R64[4] = p.valid ? p.cc : 0.0;
-        R64[5] = p.valid ? p.o : 0.0;
+        if (rec64) {  // FP64 geometry for the exact blend decisions (k_masks); null: render-only batch
+            double* R64 = rec64 + 6 * vg;
+            R64[0] = p.valid ? p.mx : 0.0;
+            R64[1] = p.valid ? p.my : 0.0;
+            R64[2] = p.valid ? p.ca : 0.0;
+            R64[3] = p.valid ? p.cb : 0.0;
+            R64[4] = p.valid ? p.cc : 0.0;
+            R64[5] = p.valid ? p.o : 0.0;
+        }
         if (!p.valid) {
-            conic[vg] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (conic) conic[vg] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[0] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[1] = make_float4(0.f, 0.f, 0.f, 0.f);
             R[2] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(128) k_prepare(const double* __restrict__ beta
         R[0] = make_float4((float)p.mx, (float)p.my, (float)(-0.5 * p.ca * kLog2e), (float)(-p.cb * kLog2e));
         R[1] = make_float4((float)(-0.5 * p.cc * kLog2e), (float)p.o, (float)p.col[0], (float)p.col[1]);
         R[2] = make_float4((float)p.col[2], 1.0f, 0.f, 0.f);  // .y = valid marker
-        conic[vg] = make_float4(R[0].z, R[0].w, R[1].x, R[1].y);  // the linearisation kernels' 16-B view
+        if (conic) conic[vg] = make_float4(R[0].z, R[0].w, R[1].x, R[1].y);  // the linearisation kernels' 16-B view
         // tile rect (rasterizer.cpp:29-36)
         int x0 = (int)floor((p.mx - p.radius) / kTile);
         int x1 = (int)floor((p.mx + p.radius) / kTile);

@@ -470,7 +470,9 @@ struct Batch {
             max_list = std::max<long long>(max_list, htile_offsets[t + 1] - htile_offsets[t]);
     }
 
-    void prepare(const Scene& s, const std::vector<slm_camera>& cv) {
+    // geometry = false: a render-only batch (the LM step's loss_after) -- no FP64
+    // geometry and no conic views (only the products and k_masks read them)
+    void prepare(const Scene& s, const std::vector<slm_camera>& cv, bool geometry = true) {
         ctx->activate();
         cudaStream_t st = ctx->stream;
         V = static_cast<int>(cv.size());
@@ -520,7 +522,8 @@ struct Batch {
         // K1 + the entry total (sum of tile-rect areas); the per-tile offsets come
         // out of the sorted tile ids (build_tile_lists), so no per-tile atomics
         launch_prepare(s.beta.p, G, Gp, cams.p, V, rec.p, keys.p, rect.p,
-                       reinterpret_cast<unsigned long long*>(total.p), err.p, rec64.p, conic.p, st);
+                       reinterpret_cast<unsigned long long*>(total.p), err.p, geometry ? rec64.p : nullptr,
+                       geometry ? conic.p : nullptr, st);
         // depth-sort keys in index order + the AND/OR of the valid keys (which
         // key bytes need a radix pass)
         const long long nvg = static_cast<long long>(V) * Gp;
@@ -2244,7 +2247,7 @@ static void lm_step(Scene& s, Train& t, const slm_lm_config& cfg, int iteration,
     ctx->check_launch();
     ctx->mark("update");
     // loss_after = batch_loss of the updated state (lm.cpp:149-153)
-    B.prepare(s, my_cams);
+    B.prepare(s, my_cams, ssim);  // mse+ssim: both terms come from the FP64 render
     B.render(true, false);
     ctx->step_stats[6] = std::accumulate(B.valid_count.begin(), B.valid_count.end(), 0ll);
     ctx->step_stats[7] = B.n_entries;
