@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     __shared__ float4 s_rec[kRenderStage][3];
     __shared__ float4 s_box[STATS ? kRenderStage : 1];
     __shared__ unsigned s_wm[kRenderStage];  // bit w: the entry's alpha box meets warp w's half-tile
+    __shared__ unsigned char s_list[kRenderThreads / 32][kRenderStage];  // per warp: its staged entries
     __shared__ double s_red[kRenderThreads / 32];
     const int tile = blockIdx.x;
     const int v = tile_view[tile];
@@ -183,9 +184,21 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
         }
         __syncthreads();
         const int m = min(kRenderStage, n - start);
-        for (int k = 0; k < m && live; ++k) {
-            if (STATS) ++st_iter;
-            if (!((s_wm[k] >> warp) & 1u)) continue;  // warp-uniform: the box misses this half-tile
+        // this warp's list of the staged entries whose alpha box meets its
+        // half-tile (ballot compaction, in list order): the walk below never
+        // visits an entry it would skip
+        int nk = 0;
+        for (int j0 = 0; j0 < m; j0 += 32) {
+            const int j = j0 + lane;
+            const bool hit = j < m && ((s_wm[j] >> warp) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (hit) s_list[warp][nk + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned char>(j);
+            nk += __popc(bal);
+        }
+        __syncwarp();
+        if (STATS && live) st_iter += m;
+        for (int ii = 0; ii < nk && live; ++ii) {
+            const int k = s_list[warp][ii];
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
             const Gate g{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
             const float gx0 = gate_x0(g, qx, qxx), gx1 = gate_x1(g, qx);  // shared by the column

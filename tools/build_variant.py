@@ -2,7 +2,7 @@
 recompiled with extra flags (e.g. -DSLM_E1), linked with the normal objects,
 written to exp/NAME.so.
 
-    [SRC=sort.cu] python tools/build_variant.py NAME [-DFLAG ...]
+    [SRC=sort.cu] [SRCPATH=/tmp/old_raster.cu] python tools/build_variant.py NAME [-DFLAG ...]
 """
 import os
 import subprocess
@@ -20,7 +20,8 @@ def main():
     src = os.environ.get("SRC", "raster.cu")
     obj = os.path.join(ROOT, "exp", f"{name}_{src}.o")
     B._run([B.NVCC, "-std=c++17", "-O3", "-lineinfo", *B.ARCH, "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-            f"-I{B.INCLUDE}", f"-I{B.CSRC}", *B.CU_SOURCES[src], *flags, "-c", os.path.join(B.CSRC, src),
+            f"-I{B.INCLUDE}", f"-I{B.CSRC}", *B.CU_SOURCES[src], *flags, "-c",
+            os.environ.get("SRCPATH") or os.path.join(B.CSRC, src),
             "-o", obj])
     objs = [obj if s == src else os.path.join(B.BUILD, s + ".o") for s in B.CU_SOURCES]
     objs += [os.path.join(B.BUILD, s + ".o") for s in B.CPP_SOURCES]
