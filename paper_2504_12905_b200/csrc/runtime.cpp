@@ -647,7 +647,7 @@ struct Samples {
     DevBuf<long long> srow_off, wbase;
     DevBuf<float> astream, rstream;
     // deterministic accumulation (DetOrder): slot sort scratch, order, partials
-    DevBuf<unsigned> dka, dkb, dva, dvb, dhist, dpart, perm, seg, dest;
+    DevBuf<unsigned> dka, dkb, dva, dvb, dhist, dpart, perm, seg, dest, fill;
     DevBuf<float> partial;
     long long n_slots = 0;
     std::vector<int> hrows, hcount;
@@ -1047,6 +1047,9 @@ struct Jacobian {
             samples.perm.ensure(n1);
             samples.dest.ensure(n1);
             samples.seg.ensure(nk + 1);
+            const char* so = std::getenv("SLM_SLOT_ORDER");  // "radix": the round-2 stable radix passes
+            const bool counting = !(so && std::strcmp(so, "radix") == 0);
+            if (counting) samples.fill.ensure(nk);
             const long long hs = radix_hist_size(n1);
             samples.dhist.ensure(hs);
             samples.dpart.ensure(scan_scratch(std::max<long long>(hs, nk)));
@@ -1063,7 +1066,8 @@ struct Jacobian {
             build_slot_order(samples.groups.p, static_cast<int>(ng), samples.gcount.p, samples.glist.p,
                              samples.mask_off.p, samples.wbase.p, scene->Gp, batch->V, ns, samples.dka.p,
                              samples.dkb.p, samples.dva.p, samples.dvb.p, samples.dhist.p, samples.dpart.p,
-                             samples.perm.p, samples.seg.p, samples.dest.p, ctx->stream);
+                             samples.perm.p, samples.seg.p, samples.dest.p, counting ? samples.fill.p : nullptr,
+                             ctx->stream);
             ctx->check_launch();
         }
         ctx->sync();  // hrow_off is read by the async copy

@@ -113,7 +113,7 @@ void launch_diag_finalize(const float* beta32, int G, int Gp, const DevCam* cams
 void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
                       const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
                       unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
-                      unsigned* perm, unsigned* seg, unsigned* dest, cudaStream_t st);
+                      unsigned* perm, unsigned* seg, unsigned* dest, unsigned* fill, cudaStream_t st);
 void launch_aos64_to_soa32(const double* aos, int G, int Gp, float* soa, cudaStream_t st);
 void launch_aos64_to_soa32_range(const double* aos, int g0, int g1, int Gp, float* soa, cudaStream_t st);
 void launch_soa32_to_aos64_range(const float* soa, int g0, int g1, int Gp, double* aos, cudaStream_t st);

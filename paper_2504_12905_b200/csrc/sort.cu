@@ -726,13 +726,47 @@ __global__ void k_invert_perm(const unsigned* __restrict__ perm, long long n, un
     if (i < n) dest[perm[i]] = static_cast<unsigned>(i);
 }
 
-// dest (n_slots) and seg (V * Gp + 1) of a plan: stable LSD radix passes over
-// the key bits of (view * Gp + Gaussian), so equal keys keep slot order; dest
-// inverts the sorted slot list.
+// Counting placement: slot i goes to seg[key] + (an atomic ticket of its key),
+// so each key's segment holds its slots in arbitrary order ...
+__global__ void k_place_slots(const unsigned* __restrict__ keys, long long n, long long n_keys,
+                              const unsigned* __restrict__ seg, unsigned* __restrict__ fill,
+                              unsigned* __restrict__ perm) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned k = keys[i];
+    if (k < static_cast<unsigned>(n_keys)) perm[seg[k] + atomicAdd(fill + k, 1u)] = static_cast<unsigned>(i);
+}
+
+// ... which one thread per key then puts in ascending slot order (insertion
+// sort: segments hold a few slots -- the number of the plan's groups in which
+// some sample blends the (view, Gaussian)) and inverts into dest.  The result
+// is exactly the stable sort's: within a key, ascending slot index.
+__global__ void k_sort_segments(const unsigned* __restrict__ seg, long long n_keys, unsigned* __restrict__ perm,
+                                unsigned* __restrict__ dest) {
+    const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n_keys) return;
+    const unsigned a = seg[k], b = seg[k + 1];
+    for (unsigned j = a + 1; j < b; ++j) {
+        const unsigned x = perm[j];
+        unsigned q = j;
+        while (q > a && perm[q - 1] > x) {
+            perm[q] = perm[q - 1];
+            --q;
+        }
+        perm[q] = x;
+    }
+    for (unsigned j = a; j < b; ++j) dest[perm[j]] = j;
+}
+
+// dest (n_slots) and seg (V * Gp + 1) of a plan: within each key (view * Gp +
+// Gaussian) the slots in ascending order, seg the keys' first positions, dest
+// the inverse.  `fill` (n_keys) is scratch.  (Round 2 ran three stable radix
+// passes over the keys; the counting placement + segment sort gives the same
+// order in three light passes.)
 void build_slot_order(const Group* groups, int n_groups, const int* gcount, const int* glist,
                       const long long* mask_off, const long long* wbase, int Gp, int V, long long n_slots,
                       unsigned* ka, unsigned* kb, unsigned* va, unsigned* vb, unsigned* hist, unsigned* part,
-                      unsigned* perm, unsigned* seg, unsigned* dest, cudaStream_t st) {
+                      unsigned* perm, unsigned* seg, unsigned* dest, unsigned* fill, cudaStream_t st) {
     const long long n_keys = static_cast<long long>(V) * Gp;
     if (n_slots == 0) {
         cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
@@ -742,6 +776,19 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
     k_slot_keys<<<(n_groups + 3) / 4, 128, 0, st>>>(groups, n_groups, gcount, glist, mask_off, wbase, Gp, sentinel,
                                                     ka, va);
     ++g_launches;
+    if (fill) {
+        cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
+        cudaMemsetAsync(fill, 0, sizeof(unsigned) * n_keys, st);
+        k_count_keys<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
+        ++g_launches;
+        launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
+        k_place_slots<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg, fill,
+                                                                                     perm);
+        ++g_launches;
+        k_sort_segments<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, st>>>(seg, n_keys, perm, dest);
+        ++g_launches;
+        return;
+    }
     int bits = 0;
     while ((1ull << bits) <= sentinel) ++bits;
     const int passes = (bits + 7) / 8;

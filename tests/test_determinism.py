@@ -53,6 +53,18 @@ def test_products_bitwise_reproducible(gpu, port):
         assert np.array_equal(a, c)
 
 
+def test_slot_order_counting_equals_radix(gpu, port, monkeypatch):
+    """The per-plan summation order built by counting placement + per-key segment
+    sort (default) is the stable radix order: products bitwise equal."""
+    st, cams, plan = _toy_inputs(port, n=600, seed=5)
+    monkeypatch.setenv("SLM_SLOT_ORDER", "radix")
+    radix = _products(gpu.jacobian(st, cams, plan))
+    monkeypatch.delenv("SLM_SLOT_ORDER")
+    counting = _products(gpu.jacobian(st, cams, plan))
+    for a, b in zip(radix, counting):
+        assert np.array_equal(a, b)
+
+
 def test_pcg_bitwise_reproducible(gpu, port):
     st, cams, plan = _toy_inputs(port, n=300, seed=9)
     jac = gpu.jacobian(st, cams, plan)
