@@ -730,11 +730,15 @@ __global__ void k_invert_perm(const unsigned* __restrict__ perm, long long n, un
 // so each key's segment holds its slots in arbitrary order ...
 __global__ void k_place_slots(const unsigned* __restrict__ keys, long long n, long long n_keys,
                               const unsigned* __restrict__ seg, unsigned* __restrict__ fill,
-                              unsigned* __restrict__ perm) {
+                              unsigned* __restrict__ perm, unsigned* __restrict__ dest) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const unsigned k = keys[i];
-    if (k < static_cast<unsigned>(n_keys)) perm[seg[k] + atomicAdd(fill + k, 1u)] = static_cast<unsigned>(i);
+    if (k < static_cast<unsigned>(n_keys)) {
+        const unsigned pos = seg[k] + atomicAdd(fill + k, 1u);
+        perm[pos] = static_cast<unsigned>(i);
+        dest[i] = pos;  // coalesced; rewritten below only where the segment needed sorting
+    }
 }
 
 // ... which one thread per key then puts in ascending slot order (insertion
@@ -746,6 +750,9 @@ __global__ void k_sort_segments(const unsigned* __restrict__ seg, long long n_ke
     const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= n_keys) return;
     const unsigned a = seg[k], b = seg[k + 1];
+    bool sorted = true;
+    for (unsigned j = a + 1; j < b && sorted; ++j) sorted = perm[j - 1] < perm[j];
+    if (sorted) return;  // the placement order already ascends; dest is right
     for (unsigned j = a + 1; j < b; ++j) {
         const unsigned x = perm[j];
         unsigned q = j;
@@ -783,7 +790,7 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
         ++g_launches;
         launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
         k_place_slots<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg, fill,
-                                                                                     perm);
+                                                                                     perm, dest);
         ++g_launches;
         k_sort_segments<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, st>>>(seg, n_keys, perm, dest);
         ++g_launches;
