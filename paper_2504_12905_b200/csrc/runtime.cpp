@@ -1047,8 +1047,11 @@ struct Jacobian {
             samples.perm.ensure(n1);
             samples.dest.ensure(n1);
             samples.seg.ensure(nk + 1);
-            const char* so = std::getenv("SLM_SLOT_ORDER");  // "radix": the round-2 stable radix passes
-            const bool counting = !(so && std::strcmp(so, "radix") == 0);
+            // slot order: counting placement + per-key segment sort when keys carry a
+            // few slots each (the segment sort is serial per key), else the stable
+            // radix passes (SLM_SLOT_ORDER=radix|counting overrides)
+            const char* so = std::getenv("SLM_SLOT_ORDER");
+            const bool counting = so ? std::strcmp(so, "radix") != 0 : ns <= 4 * static_cast<long long>(batch->V) * scene->G;
             if (counting) samples.fill.ensure(nk);
             const long long hs = radix_hist_size(n1);
             samples.dhist.ensure(hs);
