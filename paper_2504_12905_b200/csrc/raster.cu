@@ -214,10 +214,18 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
                 float av[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    ps[2 * p + h] = !(qv[h] > g.lo || qv[h] < kLog2Skip);  // gate_alpha's tests
                     float e;
                     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(qv[h]));
-                    av[h] = ps[2 * p + h] ? fminf(e, 0.99f) : 0.0f;  // clamp (rasterizer.hpp:15)
+                    e = fminf(e, 0.99f);  // clamp (rasterizer.hpp:15)
+                    if (FULL || STATS) {
+                        ps[2 * p + h] = !(qv[h] > g.lo || qv[h] < kLog2Skip);  // gate_alpha's tests
+                        av[h] = ps[2 * p + h] ? e : 0.0f;
+                    } else {  // the same two tests as one predicate chain and one select
+                        asm("{\n\t.reg .pred p1, p2;\n\tsetp.le.f32 p1, %1, %2;\n\t"
+                            "setp.ge.and.f32 p2, %1, %3, p1;\n\tselp.f32 %0, %4, 0f00000000, p2;\n\t}"
+                            : "=f"(av[h])
+                            : "f"(qv[h]), "f"(g.lo), "f"(kLog2Skip), "f"(e));
+                    }
                 }
                 a[p] = make_float2(av[0], av[1]);
             }
