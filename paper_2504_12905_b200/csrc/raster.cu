@@ -229,38 +229,70 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
                 }
                 a[p] = make_float2(av[0], av[1]);
             }
-            float2 tt[2];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) tt[p] = fmul2(T[p], fsub2(make_float2(1.0f, 1.0f), a[p]));
-            // a pixel that fails the gate keeps tt = T >= 1e-4 (alpha = 0), so
-            // tt < 1e-4 alone marks a termination
-            if (fminf(fminf(tt[0].x, tt[0].y), fminf(tt[1].x, tt[1].y)) < 1e-4f) {
-                // termination (rasterizer.hpp:121-122): not blended, the pixel stops (rare)
-                const bool tm0 = tt[0].x < 1e-4f, tm1 = tt[0].y < 1e-4f, tm2 = tt[1].x < 1e-4f, tm3 = tt[1].y < 1e-4f;
-                const bool tm[4] = {tm0, tm1, tm2, tm3};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (tm[i]) {
-                        ps[i] = false;
-                        live &= ~(1u << i);
-                        if (FULL) last[i] = start + k;
-                    }
+            if constexpr (!FULL && !STATS) {
+                // loss render (colour only): w = alpha T, T' = T - w (one rounding
+                // each; the loss is compared to the f64 reference within tolerance),
+                // updated in place; a terminated pixel gets w = 0 and T = 1 (its T is
+                // not an output, and T = 1 never triggers the test again)
+                float2 w[2];
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const bool l = tm[2 * p], h = tm[2 * p + 1];
-                    a[p] = make_float2(l ? 0.0f : a[p].x, h ? 0.0f : a[p].y);
-                    tt[p] = make_float2(l ? T[p].x : tt[p].x, h ? T[p].y : tt[p].y);
-                    qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
-                    qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
+                    w[p] = fmul2(a[p], T[p]);
+                    T[p] = fsub2(T[p], w[p]);
                 }
-            }
+                if (fminf(fminf(T[0].x, T[0].y), fminf(T[1].x, T[1].y)) < 1e-4f) {
+                    // termination (rasterizer.hpp:121-122): not blended, the pixel stops (rare)
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const float2 w = fmul2(a[p], T[p]);
-                C0[p] = ffma2(w, make_float2(q1.w, q1.w), C0[p]);
-                C1[p] = ffma2(w, make_float2(q2.x, q2.x), C1[p]);
-                C2[p] = ffma2(w, make_float2(q2.y, q2.y), C2[p]);
-                T[p] = tt[p];
+                    for (int p = 0; p < 2; ++p) {
+                        const bool l = T[p].x < 1e-4f, h = T[p].y < 1e-4f;
+                        if (l) live &= ~(1u << (2 * p));
+                        if (h) live &= ~(1u << (2 * p + 1));
+                        w[p] = make_float2(l ? 0.0f : w[p].x, h ? 0.0f : w[p].y);
+                        T[p] = make_float2(l ? 1.0f : T[p].x, h ? 1.0f : T[p].y);
+                        qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
+                        qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    C0[p] = ffma2(w[p], make_float2(q1.w, q1.w), C0[p]);
+                    C1[p] = ffma2(w[p], make_float2(q2.x, q2.x), C1[p]);
+                    C2[p] = ffma2(w[p], make_float2(q2.y, q2.y), C2[p]);
+                }
+            } else {
+                float2 tt[2];
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) tt[p] = fmul2(T[p], fsub2(make_float2(1.0f, 1.0f), a[p]));
+                // a pixel that fails the gate keeps tt = T >= 1e-4 (alpha = 0), so
+                // tt < 1e-4 alone marks a termination
+                if (fminf(fminf(tt[0].x, tt[0].y), fminf(tt[1].x, tt[1].y)) < 1e-4f) {
+                    // termination (rasterizer.hpp:121-122): not blended, the pixel stops (rare)
+                    const bool tm0 = tt[0].x < 1e-4f, tm1 = tt[0].y < 1e-4f, tm2 = tt[1].x < 1e-4f, tm3 = tt[1].y < 1e-4f;
+                    const bool tm[4] = {tm0, tm1, tm2, tm3};
+    #pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (tm[i]) {
+                            ps[i] = false;
+                            live &= ~(1u << i);
+                            if (FULL) last[i] = start + k;
+                        }
+    #pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        const bool l = tm[2 * p], h = tm[2 * p + 1];
+                        a[p] = make_float2(l ? 0.0f : a[p].x, h ? 0.0f : a[p].y);
+                        tt[p] = make_float2(l ? T[p].x : tt[p].x, h ? T[p].y : tt[p].y);
+                        qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
+                        qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
+                    }
+                }
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const float2 w = fmul2(a[p], T[p]);
+                    C0[p] = ffma2(w, make_float2(q1.w, q1.w), C0[p]);
+                    C1[p] = ffma2(w, make_float2(q2.x, q2.x), C1[p]);
+                    C2[p] = ffma2(w, make_float2(q2.y, q2.y), C2[p]);
+                    T[p] = tt[p];
+                }
             }
             if (FULL) {
 #pragma unroll
