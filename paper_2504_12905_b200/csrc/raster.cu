@@ -217,14 +217,17 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
                     float e;
                     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(qv[h]));
                     e = fminf(e, 0.99f);  // clamp (rasterizer.hpp:15)
-                    if (FULL || STATS) {
-                        ps[2 * p + h] = !(qv[h] > g.lo || qv[h] < kLog2Skip);  // gate_alpha's tests
+                    // the alpha < 1/255 skip only: power > 0 (q' > log2 o) cannot happen
+                    // for a valid splat (positive definite conic) except by the FP32
+                    // rounding of q' within ~1e-3 px of a centre, so that test of
+                    // blend_pixel is left to the exact FP64 passes (k_masks,
+                    // k_render_exact); STATS keeps it for the work counters
+                    if (STATS) {
+                        ps[2 * p + h] = !(qv[h] > g.lo || qv[h] < kLog2Skip);
                         av[h] = ps[2 * p + h] ? e : 0.0f;
-                    } else {  // the same two tests as one predicate chain and one select
-                        asm("{\n\t.reg .pred p1, p2;\n\tsetp.le.f32 p1, %1, %2;\n\t"
-                            "setp.ge.and.f32 p2, %1, %3, p1;\n\tselp.f32 %0, %4, 0f00000000, p2;\n\t}"
-                            : "=f"(av[h])
-                            : "f"(qv[h]), "f"(g.lo), "f"(kLog2Skip), "f"(e));
+                    } else {
+                        ps[2 * p + h] = qv[h] >= kLog2Skip;
+                        av[h] = ps[2 * p + h] ? e : 0.0f;
                     }
                 }
                 a[p] = make_float2(av[0], av[1]);
