@@ -726,6 +726,17 @@ __global__ void k_invert_perm(const unsigned* __restrict__ perm, long long n, un
     if (i < n) dest[perm[i]] = static_cast<unsigned>(i);
 }
 
+// Longest per-key slot count (the counting path's guard).
+constexpr unsigned kMaxSortedSegment = 64;
+__global__ void k_max_count(const unsigned* __restrict__ count, long long n, unsigned* __restrict__ out) {
+    unsigned m = 0u;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        m = max(m, count[i]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 // Counting placement: slot i goes to seg[key] + (an atomic ticket of its key),
 // so each key's segment holds its slots in arbitrary order ...
 __global__ void k_place_slots(const unsigned* __restrict__ keys, long long n, long long n_keys,
@@ -785,16 +796,27 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
     ++g_launches;
     if (fill) {
         cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
-        cudaMemsetAsync(fill, 0, sizeof(unsigned) * n_keys, st);
+        cudaMemsetAsync(fill, 0, sizeof(unsigned), st);
         k_count_keys<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg);
         ++g_launches;
-        launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
+        // the per-key segment sort is serial: a key with many slots (one splat
+        // blended in many of the plan's groups) takes the radix passes instead
+        k_max_count<<<static_cast<unsigned>(std::min<long long>((n_keys + 255) / 256, 1184)), 256, 0, st>>>(seg, n_keys,
+                                                                                                            fill);
+        ++g_launches;
+        unsigned longest = 0;
+        cudaMemcpyAsync(&longest, fill, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (longest <= kMaxSortedSegment) {
+            cudaMemsetAsync(fill, 0, sizeof(unsigned) * n_keys, st);
+            launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
         k_place_slots<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg, fill,
                                                                                      perm, dest);
         ++g_launches;
-        k_sort_segments<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, st>>>(seg, n_keys, perm, dest);
-        ++g_launches;
-        return;
+            k_sort_segments<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, st>>>(seg, n_keys, perm, dest);
+            ++g_launches;
+            return;
+        }
     }
     int bits = 0;
     while ((1ull << bits) <= sentinel) ++bits;

@@ -65,6 +65,22 @@ def test_slot_order_counting_equals_radix(gpu, port, monkeypatch):
         assert np.array_equal(a, b)
 
 
+def test_slot_order_with_a_splat_in_every_group(gpu, port, monkeypatch):
+    """One wide, faint splat at the origin is blended in nearly every group of the
+    plan (one key with over 64 slots: the counting path's guard hands the plan to
+    the radix passes); products still equal the radix order bitwise."""
+    st, cams, plan = _toy_inputs(port, n=600, size=192, seed=7)
+    st.means[0:3] = 0.0
+    st.log_scales[0:3] = np.log(0.8)
+    st.opacity_logits[0] = -2.0
+    monkeypatch.setenv("SLM_SLOT_ORDER", "radix")
+    radix = _products(gpu.jacobian(st, cams, plan))
+    monkeypatch.setenv("SLM_SLOT_ORDER", "counting")
+    counting = _products(gpu.jacobian(st, cams, plan))
+    for a, b in zip(radix, counting):
+        assert np.array_equal(a, b)
+
+
 def test_pcg_bitwise_reproducible(gpu, port):
     st, cams, plan = _toy_inputs(port, n=300, seed=9)
     jac = gpu.jacobian(st, cams, plan)
