@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     const float4* __restrict__ rec, int Gp, const float* __restrict__ gt,
     float* __restrict__ image, float* __restrict__ trans, int* __restrict__ contrib,
     int* __restrict__ last_out, double* __restrict__ sse_tile, unsigned long long* __restrict__ stats) {
-    __shared__ float4 s_rec[kRenderStage][3];
+    __shared__ float4 s_rec[kRenderStage + 1][3];  // + a zero-alpha record (the loss loop's odd-count pad)
     __shared__ float4 s_box[STATS ? kRenderStage : 1];
     __shared__ unsigned s_wm[kRenderStage];  // bit w: the entry's alpha box meets warp w's half-tile
     __shared__ unsigned char s_list[kRenderThreads / 32][kRenderStage];  // per warp: its staged entries
@@ -163,6 +163,9 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
         qyy[p] = make_float2(yy[0], yy[1]);
     }
     unsigned long long st_iter = 0, st_box = 0, st_live = 0, st_blend = 0, st_stage = 0, st_exact = 0, st_useful = 0;
+    constexpr bool kLoss = !FULL && !STATS;
+    if (kLoss && threadIdx.x < 3)  // q' = -1e30 at every pixel: alpha 0, colour 0
+        s_rec[kRenderStage][threadIdx.x] = make_float4(threadIdx.x == 0 ? -1e30f : 0.f, 0.f, 0.f, 0.f);
     for (int start = 0; start < n; start += kRenderStage) {
         if (__syncthreads_count(live != 0u) == 0) break;
         if (STATS) st_stage += min(kRenderStage, n - start);
@@ -195,8 +198,71 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             if (hit) s_list[warp][nk + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned char>(j);
             nk += __popc(bal);
         }
+        if (kLoss && (nk & 1) && lane == 0) s_list[warp][nk] = static_cast<unsigned char>(kRenderStage);
         __syncwarp();
         if (STATS && live) st_iter += m;
+        if constexpr (kLoss) {
+            // loss render: two entries per iteration, one loop test and one
+            // termination test per pair (an odd list ends on the zero record)
+            for (int ii = 0; ii < nk && live; ii += 2) {
+                const int ka = s_list[warp][ii], kb = s_list[warp][ii + 1];
+                float2 a[2][2];  // [entry][pixel pair]
+                float4 cc[2];    // the entries' colours
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int k = e ? kb : ka;
+                    const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
+                    cc[e] = make_float4(q1.w, q2.x, q2.y, 0.f);
+                    const float gx0 = __fmaf_rn(q0.w, qxx, __fmaf_rn(q0.y, qx, q0.x)), gx1 = __fmaf_rn(q1.x, qx, q0.z);
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        const float2 q = ffma2(make_float2(q1.y, q1.y), qyy[p],
+                                               ffma2(make_float2(gx1, gx1), qy[p], make_float2(gx0, gx0)));
+                        float e0, e1;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(q.x));
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(q.y));
+                        // the alpha < 1/255 skip; the clamp at 0.99 (power > 0: see below)
+                        a[e][p] = make_float2(q.x >= kLog2Skip ? fminf(e0, 0.99f) : 0.0f,
+                                              q.y >= kLog2Skip ? fminf(e1, 0.99f) : 0.0f);
+                    }
+                }
+                float2 w[2][2], T1[2];
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    w[0][p] = fmul2(a[0][p], T[p]);
+                    T1[p] = fsub2(T[p], w[0][p]);
+                    w[1][p] = fmul2(a[1][p], T1[p]);
+                    T[p] = fsub2(T1[p], w[1][p]);
+                }
+                // termination (rasterizer.hpp:121-122): the entry that would push T
+                // under 1e-4 is not blended and the pixel stops -- at the first entry
+                // of the pair (neither blends) or the second (rare)
+                if (fminf(fminf(fminf(T1[0].x, T1[0].y), fminf(T1[1].x, T1[1].y)),
+                          fminf(fminf(T[0].x, T[0].y), fminf(T[1].x, T[1].y))) < 1e-4f) {
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        const bool l1 = T1[p].x < 1e-4f, h1 = T1[p].y < 1e-4f;
+                        const bool l = l1 || T[p].x < 1e-4f, h = h1 || T[p].y < 1e-4f;
+                        if (l) live &= ~(1u << (2 * p));
+                        if (h) live &= ~(1u << (2 * p + 1));
+                        w[0][p] = make_float2(l1 ? 0.0f : w[0][p].x, h1 ? 0.0f : w[0][p].y);
+                        w[1][p] = make_float2(l ? 0.0f : w[1][p].x, h ? 0.0f : w[1][p].y);
+                        T[p] = make_float2(l ? 1.0f : T[p].x, h ? 1.0f : T[p].y);
+                        qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
+                        qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        C0[p] = ffma2(w[e][p], make_float2(cc[e].x, cc[e].x), C0[p]);
+                        C1[p] = ffma2(w[e][p], make_float2(cc[e].y, cc[e].y), C1[p]);
+                        C2[p] = ffma2(w[e][p], make_float2(cc[e].z, cc[e].z), C2[p]);
+                    }
+            }
+            continue;
+        }
         for (int ii = 0; ii < nk && live; ++ii) {
             const int k = s_list[warp][ii];
             const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
