@@ -56,6 +56,10 @@ namespace slm {
 constexpr int kRenderThreads = 64;
 constexpr int kRenderPix = 4;      // pixels per thread
 constexpr int kRenderStage = 128;  // records staged per round
+#ifndef SLM_LOSS_ENTRIES
+#define SLM_LOSS_ENTRIES 2
+#endif
+constexpr int kLossE = SLM_LOSS_ENTRIES;  // list entries per iteration of the loss render
 
 // Bounding box of {alpha >= 1/255} for a record (A, B, C: log2-domain conic,
 // o: opacity): q = A dx^2 + B dx dy + C dy^2 >= L = log2(1/(255 o)).
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
     __shared__ float4 s_rec[kRenderStage + 1][3];  // + a zero-alpha record (the loss loop's odd-count pad)
     __shared__ float4 s_box[STATS ? kRenderStage : 1];
     __shared__ unsigned s_wm[kRenderStage];  // bit w: the entry's alpha box meets warp w's half-tile
-    __shared__ unsigned char s_list[kRenderThreads / 32][kRenderStage];  // per warp: its staged entries
+    __shared__ unsigned char s_list[kRenderThreads / 32][kRenderStage + 4];  // per warp: its staged entries (+ pads)
     __shared__ double s_red[kRenderThreads / 32];
     const int tile = blockIdx.x;
     const int v = tile_view[tile];
@@ -198,19 +202,20 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
             if (hit) s_list[warp][nk + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned char>(j);
             nk += __popc(bal);
         }
-        if (kLoss && (nk & 1) && lane == 0) s_list[warp][nk] = static_cast<unsigned char>(kRenderStage);
+        if (kLoss && lane == 0)
+            for (int j = nk; j < ((nk + kLossE - 1) / kLossE) * kLossE; ++j)
+                s_list[warp][j] = static_cast<unsigned char>(kRenderStage);
         __syncwarp();
         if (STATS && live) st_iter += m;
         if constexpr (kLoss) {
-            // loss render: two entries per iteration, one loop test and one
-            // termination test per pair (an odd list ends on the zero record)
-            for (int ii = 0; ii < nk && live; ii += 2) {
-                const int ka = s_list[warp][ii], kb = s_list[warp][ii + 1];
-                float2 a[2][2];  // [entry][pixel pair]
-                float4 cc[2];    // the entries' colours
+            // loss render: kLossE entries per iteration, one loop test and one
+            // termination test per group (a list ends on zero-alpha records)
+            for (int ii = 0; ii < nk && live; ii += kLossE) {
+                float2 a[kLossE][2];  // [entry][pixel pair]
+                float4 cc[kLossE];    // the entries' colours
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int k = e ? kb : ka;
+                for (int e = 0; e < kLossE; ++e) {
+                    const int k = s_list[warp][ii + e];
                     const float4 q0 = s_rec[k][0], q1 = s_rec[k][1], q2 = s_rec[k][2];
                     cc[e] = make_float4(q1.w, q2.x, q2.y, 0.f);
                     const float gx0 = __fmaf_rn(q0.w, qxx, __fmaf_rn(q0.y, qx, q0.x)), gx1 = __fmaf_rn(q1.x, qx, q0.z);
@@ -226,34 +231,38 @@ __global__ void __launch_bounds__(kRenderThreads, SLM_RENDER_MINB) k_render(
                                               q.y >= kLog2Skip ? fminf(e1, 0.99f) : 0.0f);
                     }
                 }
-                float2 w[2][2], T1[2];
+                float2 w[kLossE][2], Te[kLossE][2];
+                float tmin = 1.0f;
 #pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    w[0][p] = fmul2(a[0][p], T[p]);
-                    T1[p] = fsub2(T[p], w[0][p]);
-                    w[1][p] = fmul2(a[1][p], T1[p]);
-                    T[p] = fsub2(T1[p], w[1][p]);
-                }
-                // termination (rasterizer.hpp:121-122): the entry that would push T
-                // under 1e-4 is not blended and the pixel stops -- at the first entry
-                // of the pair (neither blends) or the second (rare)
-                if (fminf(fminf(fminf(T1[0].x, T1[0].y), fminf(T1[1].x, T1[1].y)),
-                          fminf(fminf(T[0].x, T[0].y), fminf(T[1].x, T[1].y))) < 1e-4f) {
+                for (int e = 0; e < kLossE; ++e)
 #pragma unroll
                     for (int p = 0; p < 2; ++p) {
-                        const bool l1 = T1[p].x < 1e-4f, h1 = T1[p].y < 1e-4f;
-                        const bool l = l1 || T[p].x < 1e-4f, h = h1 || T[p].y < 1e-4f;
+                        w[e][p] = fmul2(a[e][p], T[p]);
+                        T[p] = fsub2(T[p], w[e][p]);
+                        Te[e][p] = T[p];
+                        tmin = fminf(tmin, fminf(T[p].x, T[p].y));
+                    }
+                // termination (rasterizer.hpp:121-122): the entry that would push T
+                // under 1e-4 is not blended and the pixel stops there (rare)
+                if (tmin < 1e-4f) {
+#pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        bool l = false, h = false;
+#pragma unroll
+                        for (int e = 0; e < kLossE; ++e) {
+                            l = l || Te[e][p].x < 1e-4f;
+                            h = h || Te[e][p].y < 1e-4f;
+                            w[e][p] = make_float2(l ? 0.0f : w[e][p].x, h ? 0.0f : w[e][p].y);
+                        }
                         if (l) live &= ~(1u << (2 * p));
                         if (h) live &= ~(1u << (2 * p + 1));
-                        w[0][p] = make_float2(l1 ? 0.0f : w[0][p].x, h1 ? 0.0f : w[0][p].y);
-                        w[1][p] = make_float2(l ? 0.0f : w[1][p].x, h ? 0.0f : w[1][p].y);
                         T[p] = make_float2(l ? 1.0f : T[p].x, h ? 1.0f : T[p].y);
                         qy[p] = make_float2(l ? 0.0f : qy[p].x, h ? 0.0f : qy[p].y);
                         qyy[p] = make_float2(l ? 1e30f : qyy[p].x, h ? 1e30f : qyy[p].y);
                     }
                 }
 #pragma unroll
-                for (int e = 0; e < 2; ++e)
+                for (int e = 0; e < kLossE; ++e)
 #pragma unroll
                     for (int p = 0; p < 2; ++p) {
                         C0[p] = ffma2(w[e][p], make_float2(cc[e].x, cc[e].x), C0[p]);
