@@ -1029,12 +1029,14 @@ struct Jacobian {
             SLM_CUDA_CHECK(cudaMemcpyAsync(samples.wbase.p, samples.hwbase.data(), sizeof(long long) * ng,
                                            cudaMemcpyHostToDevice, ctx->stream));
         }
+        ctx->mark("plan:rows");
         SampleArgs b = args();
         b.astream_out = samples.astream.p;
         b.rstream_out = samples.rstream.p;
         b.cols_out = samples.cols.p;
         launch_alpha(b, ctx->stream);
         ctx->check_launch();
+        ctx->mark("plan:alpha");
         if (det) {  // the fixed summation order of this plan's J^T / diag slots
             const long long ns = 32 * wins;
             samples.n_slots = ns;

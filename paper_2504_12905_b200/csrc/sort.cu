@@ -20,6 +20,8 @@
 #include <cstdint>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -791,9 +793,33 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
         return;
     }
     const unsigned sentinel = static_cast<unsigned>(n_keys);
+    static const bool prof = std::getenv("SLM_SORT_PROF") && std::getenv("SLM_SORT_PROF")[0] == '1';
+    cudaEvent_t pev[12];
+    const char* pname[12];
+    int np = 0;
+    auto pmark = [&](const char* name) {
+        if (!prof) return;
+        cudaEventCreate(&pev[np]);
+        cudaEventRecord(pev[np], st);
+        pname[np++] = name;
+    };
+    auto pdump = [&]() {
+        if (!prof) return;
+        cudaEventSynchronize(pev[np - 1]);
+        std::fprintf(stderr, "[slots] n=%lld keys=%lld:", n_slots, n_keys);
+        for (int q = 1; q < np; ++q) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pev[q - 1], pev[q]);
+            std::fprintf(stderr, " %s %.3f", pname[q], ms);
+        }
+        std::fprintf(stderr, "\n");
+        for (int q = 0; q < np; ++q) cudaEventDestroy(pev[q]);
+    };
+    pmark("start");
     k_slot_keys<<<(n_groups + 3) / 4, 128, 0, st>>>(groups, n_groups, gcount, glist, mask_off, wbase, Gp, sentinel,
                                                     ka, va);
     ++g_launches;
+    pmark("keys");
     if (fill) {
         cudaMemsetAsync(seg, 0, sizeof(unsigned) * (n_keys + 1), st);
         cudaMemsetAsync(fill, 0, sizeof(unsigned), st);
@@ -806,15 +832,21 @@ void build_slot_order(const Group* groups, int n_groups, const int* gcount, cons
         ++g_launches;
         unsigned longest = 0;
         cudaMemcpyAsync(&longest, fill, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+        pmark("count+max");
         cudaStreamSynchronize(st);
         if (longest <= kMaxSortedSegment) {
             cudaMemsetAsync(fill, 0, sizeof(unsigned) * n_keys, st);
+            pmark("sync+memset");
             launch_exclusive_scan(seg, seg, n_keys, part, seg + n_keys, st);
+            pmark("scan");
         k_place_slots<<<static_cast<unsigned>((n_slots + 255) / 256), 256, 0, st>>>(ka, n_slots, n_keys, seg, fill,
                                                                                      perm, dest);
         ++g_launches;
+            pmark("place");
             k_sort_segments<<<static_cast<unsigned>((n_keys + 255) / 256), 256, 0, st>>>(seg, n_keys, perm, dest);
             ++g_launches;
+            pmark("sort");
+            pdump();
             return;
         }
     }
