@@ -502,10 +502,12 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, int lane) {
 // list order and the pixel bits are re-packed (column compaction through two
 // bit transposes) into 32-entry windows, so the per-product passes walk dense
 // windows and never stage an entry no lane uses.
-__global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
+__global__ void __launch_bounds__(128, 8) k_masks(SampleArgs A) {  // 64 registers: 8 CTAs per SM
     __shared__ double s_r[4][32][6];  // staged entries: FP64 mx, my, a, b, c, o
     __shared__ double s_thr[4][32];   // power below which alpha < 1/255 for sure
-    __shared__ float4 s_g[4][32][2];  // FP32 gate polynomials (pre-filter)
+    // FP32 gate polynomials (pre-filter), entry pairs interleaved so one packed
+    // FFMA2 chain evaluates two entries: [pair][q] = (g_2q(a), g_2q(b), g_2q+1(a), g_2q+1(b))
+    __shared__ float4 s_g[4][16][3];
     __shared__ float s_c[4][32][3];   // their colours
     __shared__ unsigned s_col[4][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -538,21 +540,35 @@ __global__ void __launch_bounds__(128) k_masks(SampleArgs A) {
             s_c[warp][lane][1] = r1.w;
             s_c[warp][lane][2] = rf[2].x;
             const Gate gt = make_gate(r0, r1, c.ox, c.oy);
-            s_g[warp][lane][0] = make_float4(gt.g0, gt.g1, gt.g2, gt.g3);
-            s_g[warp][lane][1] = make_float4(gt.g4, gt.g5, gt.lo, 0.f);
+            float* pg = reinterpret_cast<float*>(&s_g[warp][lane >> 1][0]) + (lane & 1);
+            pg[0] = gt.g0;
+            pg[2] = gt.g1;
+            pg[4] = gt.g2;
+            pg[6] = gt.g3;
+            pg[8] = gt.g4;
+            pg[10] = gt.g5;
         }
         __syncwarp();
         const int mn = min(32, n - base);
         // FP32 pre-filter (the shared gate): a pair whose q' is below log2(1/255) by
         // far more than FP32 rounding cannot blend; the others are decided in FP64,
         // and only entries some lane may blend get their FP64 record staged
+        // two entries per packed chain (fma.rn.f32x2 rounds each lane like the
+        // scalar gate_q); an odd last entry evaluates stale coefficients, masked off
         unsigned cand = 0u;
-        if (live)
-            for (int k = 0; k < mn; ++k) {
-                const float4 q0 = s_g[warp][k][0], q1 = s_g[warp][k][1];
-                const Gate gt{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
-                if (gate_q(gt, pq) >= kLog2Skip - 0.5f) cand |= 1u << k;  // FP32 q' error < 1e-3 measured
+        if (live) {
+            const float2 X = make_float2(pq.x, pq.x), XX = make_float2(pq.xx, pq.xx);
+            const float2 Y = make_float2(pq.y, pq.y), YY = make_float2(pq.yy, pq.yy);
+            for (int k = 0; k < mn; k += 2) {
+                const float4 a = s_g[warp][k >> 1][0], b = s_g[warp][k >> 1][1], d = s_g[warp][k >> 1][2];
+                const float2 gx0 = ffma2(make_float2(b.z, b.w), XX, ffma2(make_float2(a.z, a.w), X, make_float2(a.x, a.y)));
+                const float2 gx1 = ffma2(make_float2(d.x, d.y), X, make_float2(b.x, b.y));
+                const float2 q = ffma2(make_float2(d.z, d.w), YY, ffma2(gx1, Y, gx0));
+                const unsigned two = (q.x >= kLog2Skip - 0.5f ? 1u : 0u) | (q.y >= kLog2Skip - 0.5f ? 2u : 0u);
+                cand |= two << k;  // FP32 q' error < 1e-3 measured
             }
+            if (mn < 32) cand &= (1u << mn) - 1u;
+        }
         const unsigned any_cand = __reduce_or_sync(0xffffffffu, cand);
         if (j < n && ((any_cand >> lane) & 1u)) {
             const double* r = A.rec64 + 6 * (c.vbase + g);
