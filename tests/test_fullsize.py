@@ -32,7 +32,9 @@ SHAPES = {  # BASELINE.json configs: Gaussians, views, width, height, samples pe
     "cfg1": (100_000, 64, 800, 800, 64),
     "cfg2": (1_000_000, 200, 1280, 720, 32),
     "cfg4": (3_000_000, 300, 1600, 1066, 32),
+    "cfg3": (500_000, 64, 800, 800, 13),  # the sweep's 5% point: N = 13 needs lane width 1 (sample_plan.cpp:68-69)
 }
+LANE = {"cfg3": 1}
 
 
 @pytest.fixture(scope="module")
@@ -63,7 +65,7 @@ def inputs(H, shape: str, batch: int = 8):
     cams = [ring_camera(2.0 * math.pi * i / nv, 3.2, 1.1, w, h) for i in range(nv)]
     clusters = H.kmeans_cameras(cams, batch, 1 ^ KMEANS_SALT)
     views = H.sample_view_batch(clusters, rng)
-    plan = H.build_sample_plan([cams[i] for i in views], spt, 0, rng, 32)
+    plan = H.build_sample_plan([cams[i] for i in views], spt, 0, rng, LANE.get(shape, 32))
     return state, cams, clusters, views, plan
 
 
@@ -149,10 +151,12 @@ def test_cfg2_batch_properties_and_reproducibility(gpu, cfg2):
     assert np.array_equal(d1, d2) and np.all(d1 >= 0)
 
 
-@pytest.mark.parametrize("shape", ["cfg1", "cfg4"])
+@pytest.mark.parametrize("shape", ["cfg1", "cfg4", "cfg3"])
 def test_other_shapes_products_vs_reference(gpu, reflib, shape):
-    """configs[1] (100k, 800x800, N = 64) and configs[4] (3M, 1600x1066 -- a partial
-    bottom tile row, N = 32): one batch view, all four products vs the reference."""
+    """configs[1] (100k, 800x800, N = 64), configs[4] (3M, 1600x1066 -- a partial
+    bottom tile row, N = 32) and configs[3]'s sparsest sweep point (500k, 800x800,
+    N = 13 with lane width 1: groups of 13 samples, partial warps): one batch view,
+    all four products vs the reference."""
     from paper_2504_12905_b200 import splatlm
     state, cams, clusters, views, plan = inputs(splatlm.HostSampler(), shape)
     errs = _products_vs_reference(gpu, reflib, state, [cams[views[0]]], sub_plan(plan, 0, 1))
