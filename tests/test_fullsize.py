@@ -115,6 +115,21 @@ def test_cfg2_tile_lists_bit_exact(gpu, reflib, cfg2):
     assert np.array_equal(i_gpu, i_ref)
 
 
+@pytest.mark.parametrize("shape", ["cfg1", "cfg4"])
+def test_other_shapes_tile_lists_bit_exact(gpu, reflib, shape):
+    """render::bin_and_sort at configs[1] (100k, 800x800) and configs[4] (3M,
+    1600x1066, a partial bottom tile row): CSR offsets and every tile's order equal
+    the reference's."""
+    from paper_2504_12905_b200 import splatlm
+    state, cams, clusters, views, plan = inputs(splatlm.HostSampler(), shape)
+    cam = cams[views[0]]
+    o_ref, i_ref = reflib.bin_and_sort(state, cam)
+    o_gpu, i_gpu = gpu.bin_and_sort(state, cam)
+    print(shape, "entries", len(i_ref), "longest list", int(np.max(np.diff(o_ref))))
+    assert np.array_equal(o_gpu, o_ref)
+    assert np.array_equal(i_gpu, i_ref)
+
+
 def test_cfg2_step_inputs_bit_exact(gpu, reflib, cfg2):
     """The library's host sampler vs the reference at the configs[2] shape: random_init
     state, view clusters, the view batch and the 921,600 sampled pixels, tiles and
