@@ -1231,6 +1231,7 @@ __global__ void __maxnreg__(144) k_sample_raster(SampleArgs A) {  // 144 regs x 
 __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
     __shared__ float s_f[4][9][32];
     __shared__ float s_gate[4][7][32];  // the entries' gate polynomials (make_gate)
+    __shared__ float s_io[4][32];        // the entries' 1/o
     __shared__ int s_g[4][32];
     __shared__ float s_t[4][3][32][17];
     __shared__ float4 s_pix[4][32];  // (px+.5, py+.5, W0, W1)
@@ -1274,6 +1275,7 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
             s_gate[warp][4][lane] = gt.g4;
             s_gate[warp][5][lane] = gt.g5;
             s_gate[warp][6][lane] = gt.lo;
+            s_io[warp][lane] = rcp_approx(P.r1.y);
         }
         __syncwarp();
         prefetch<false>(c, W, A.rec, nullptr, w + 1, lane, P);
@@ -1289,13 +1291,13 @@ __global__ void __launch_bounds__(128) k_diag_raster(DiagArgs A) {
                 float alpha = 0.0f;
                 bool clamped = false;
                 blended_alpha(gate_q(gt, pq), alpha, clamped);  // blended: the mask already decided
-                const float e = __fdividef(alpha, sf[5][k]);  // the falloff before opacity (unclamped)
+                const float e = alpha * s_io[warp][k];  // the falloff before opacity (unclamped)
                 const float4 r1 = make_float4(sf[4][k], sf[5][k], sf[6][k], sf[7][k]);
                 const float c2 = sf[8][k];
                 const float wgt = __fmul_rn(alpha, T);
                 const float n0 = __fmaf_rn(wgt, r1.z, S0), n1 = __fmaf_rn(wgt, r1.w, S1),
                             n2 = __fmaf_rn(wgt, c2, S2);
-                const float inv1m = __fdividef(1.0f, 1.0f - alpha);
+                const float inv1m = rcp_approx(1.0f - alpha);  // 1 - alpha in [0.01, 1): no denormal range
                 const float da0 = T * r1.z - (Cf0 - n0) * inv1m;
                 const float da1 = T * r1.w - (Cf1 - n1) * inv1m;
                 const float da2 = T * c2 - (Cf2 - n2) * inv1m;
