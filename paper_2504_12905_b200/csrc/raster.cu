@@ -68,9 +68,14 @@ __device__ __forceinline__ float4 alpha_box(float4 r0, float4 r1) {
     const float det = A * C - 0.25f * B * B;  // > 0 for a valid (negative-definite) conic
     const float L = -__log2f(255.0f * o);     // <= 0 when o >= 1/255
     if (!(det > 0.0f) || !(L < 0.0f)) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never blends
-    // half-widths sqrt(L * C / det), sqrt(L * A / det) (all three signs negative), widened
-    const float hx = sqrtf(fmaxf(L * C / det, 0.0f)) * 1.001f + 0.05f;
-    const float hy = sqrtf(fmaxf(L * A / det, 0.0f)) * 1.001f + 0.05f;
+    // half-widths sqrt(L * C / det), sqrt(L * A / det) (all three signs negative),
+    // widened by 0.1% + 0.05 px, which also covers sqrt.approx's few-ulp error
+    const float ld = L / det;
+    float hx, hy;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(hx) : "f"(fmaxf(ld * C, 0.0f)));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(hy) : "f"(fmaxf(ld * A, 0.0f)));
+    hx = hx * 1.001f + 0.05f;
+    hy = hy * 1.001f + 0.05f;
     return make_float4(r0.x - hx, r0.x + hx, r0.y - hy, r0.y + hy);
 }
 
