@@ -269,6 +269,12 @@ int slm_jacobian_mask_stats(slm_jacobian* j, uint64_t* out);
  * warp the entries past an exact ellipse/half-tile test and the entries some
  * pixel of the warp blended). */
 int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uint64_t* out);
+/* Diagnostic: the NCCL seam in one process (a one-rank communicator on the
+ * context's device): dlopen + unique id + init, then the product's two
+ * collectives (allreduce of f32 and f64 vectors, the grouped row allreduce) on
+ * known data.  out[0] = largest |result - input| (0 for one rank), out[1] =
+ * elements checked.  Fails with the NCCL error when the library is missing. */
+int slm_debug_nccl_selftest(slm_context* ctx, double* out);
 
 #ifdef __cplusplus
 }

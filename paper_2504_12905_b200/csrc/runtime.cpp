@@ -2705,6 +2705,44 @@ int slm_residuals(const double* rendered, const double* truth, int64_t n, double
         for (int64_t i = 0; i < n; ++i) out[i] = rendered[i] - truth[i];
     });
 }
+int slm_debug_nccl_selftest(slm_context* ctx, double* out) {
+    return guarded([&] {
+        Context& c = ctx->impl;
+        c.activate();
+        ncclUniqueId uid;
+        SLM_NCCL_CHECK(nccl().GetUniqueId(&uid));
+        NcclComm nc;
+        SLM_NCCL_CHECK(nccl().CommInitRank(&nc.c, 1, uid, 0));
+        const size_t n = 4 * 1000 + 7, pitch = 1024, rows = 4, len = 1000;
+        std::vector<float> hf(n);
+        std::vector<double> hd(n);
+        for (size_t i = 0; i < n; ++i) {
+            hf[i] = static_cast<float>(i) * 0.25f - 3.0f;
+            hd[i] = static_cast<double>(i) * 0.125 + 1.0;
+        }
+        DevBuf<float> df;
+        DevBuf<double> dd;
+        df.ensure(n);
+        dd.ensure(n);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(df.p, hf.data(), n * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(dd.p, hd.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+        nc.allreduce(df.p, n, false, c.stream);
+        nc.allreduce(dd.p, n, true, c.stream);
+        nc.allreduce_rows(df.p, pitch, static_cast<int>(rows), len, c.stream);
+        std::vector<float> rf(n);
+        std::vector<double> rd(n);
+        SLM_CUDA_CHECK(cudaMemcpyAsync(rf.data(), df.p, n * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+        SLM_CUDA_CHECK(cudaMemcpyAsync(rd.data(), dd.p, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        double err = 0.0;
+        for (size_t i = 0; i < n; ++i) {
+            err = std::max(err, std::fabs(static_cast<double>(rf[i]) - hf[i]));
+            err = std::max(err, std::fabs(rd[i] - hd[i]));
+        }
+        out[0] = err;
+        out[1] = static_cast<double>(2 * n);
+    });
+}
 int slm_debug_render_stats(slm_scene* s, const slm_camera* cams, int n_cams, uint64_t* out) {
     return guarded([&] {  // k_render work counters: [entry iterations (per thread), past the box test,
                           //  live pixel-entry gate evaluations, blends, staged entries (per thread)]

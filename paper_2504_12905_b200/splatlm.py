@@ -58,6 +58,7 @@ _SIGS = {
     "slm_context_set_profiling": (C.c_int, [_vp, C.c_int]),
     "slm_context_profile_collect": (C.c_int, [_vp, _f64p, _i32p]),
     "slm_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "slm_debug_nccl_selftest": (C.c_int, [_vp, _f64p]),
     "slm_context_init_comm": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int, C.c_int]),
     "slm_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "slm_local_group_destroy": (None, [_vp]),
@@ -425,6 +426,12 @@ class Lib(HostSampler):
     def set_comm_chunks(self, chunks: int):
         """Gaussian chunks of the pipelined chain + allreduce (world > 1)."""
         self._check(self.dll.slm_context_set_comm_chunks(self.ctx, chunks))
+
+    def nccl_selftest(self):
+        """One-rank NCCL communicator on this device: (max |error|, elements checked)."""
+        out = np.zeros(2)
+        self._check(self.dll.slm_debug_nccl_selftest(self.ctx, f64ptr(out)))
+        return float(out[0]), int(out[1])
 
     def init_comm(self, uid: bytes, rank: int, world: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)

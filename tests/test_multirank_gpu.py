@@ -75,3 +75,21 @@ def test_two_ranks_bitwise_reproducible():
     cfg = LmConfig(pcg_iters_initial=8, pcg_iters_late=8)
     a, b = _world2(cfg), _world2(cfg)
     assert a[0][0] == b[0][0] and np.array_equal(a[0][1], b[0][1])
+
+
+def test_nccl_seam_one_rank():
+    """The NCCL implementation of the collective seam (the deployment's, one
+    process per GPU) in one process: dlopen of the NCCL library (PyTorch's
+    bundled one, as bench.py picks it), unique id, a one-rank communicator, and
+    the product path's f32 / f64 allreduce and grouped row allreduce on known
+    data -- the calls and enums the multi-GPU runs make, exercised on one B200."""
+    import os
+    try:
+        import nvidia.nccl
+        os.environ.setdefault("SLM_NCCL_LIB", os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib",
+                                                           "libnccl.so.2"))
+    except Exception:
+        pass
+    from paper_2504_12905_b200 import splatlm
+    err, n = splatlm.lib().nccl_selftest()
+    assert n > 0 and err == 0.0
